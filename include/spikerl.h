@@ -1,0 +1,276 @@
+/*
+ * spikerl.h — C ABI of libspikerl.so: the B200-native (sm_100a) data-parallel hot path of
+ * SpikeRL (arxiv 2502.17496): the batched forward and surrogate-gradient backward of the
+ * population-coded spiking actor inside a TD3 update, the twin-critic MLP, Adam/Polyak and
+ * the per-step gradient allreduce.
+ *
+ * Sources of each operation (PAPER.md line numbers; DESIGN.md "Readings" R1..R30 cover every
+ * point the paper leaves open):
+ *   encoder   PAPER.md:129-131 (§III-A, "populations use Gaussian distributions to transform
+ *             continuous input values into spike trains"), north_star ("deterministic
+ *             soft-reset encoder spikes").
+ *   LIF       PAPER.md:131 ("integrates presynaptic spikes into a current, which then charges
+ *             the membrane voltage ... the neuron fires"); north_star equations
+ *             c = d_c*c + W*o, v = d_v*v*(1-o_prev) + c, o = [v > V_th].
+ *   decoder   PAPER.md:131 ("aggregates these spikes over time to compute firing rates ...
+ *             through a weighted sum").
+ *   backward  north_star ("BPTT with a rectangular pseudo-gradient").
+ *   critic    PAPER.md:131 ("evaluated by the deep critic network ... TD3"); configs[1].
+ *   TD3       PAPER.md:131; SPEC.md:235-259 (target, train_step, soft_update).
+ *   comm      PAPER.md:135 (broadcast_weights / average_gradients), PAPER.md:144 (DDP
+ *             allreduce over NCCL).
+ *
+ * Conventions
+ *   - Every pointer is a DEVICE pointer unless marked (host).
+ *   - Every call only enqueues work on `stream` (a cudaStream_t) and returns; no call
+ *     synchronises the device, so the calls are CUDA-graph capturable (except comm init).
+ *   - The caller owns every buffer (params, grads, tape, workspace, replay). The library frees
+ *     nothing it did not allocate; it owns only spikerl_comm objects and internal caches.
+ *   - Synchronous errors (SPIKERL_E_ARG, _DOMAIN, _STATE, _NOTREADY) are detected on the host
+ *     before anything is enqueued, so outputs are untouched. Asynchronous device faults show
+ *     up as SPIKERL_E_CUDA at the next call. spikerl_last_error() gives the message.
+ *   - Data-dependent preconditions (sigma > 0, finite observations) are documented, not
+ *     checked on the device.
+ */
+#ifndef SPIKERL_H
+#define SPIKERL_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef void* spikerl_stream_t; /* a cudaStream_t (NULL = legacy default stream) */
+
+enum spikerl_status {
+  SPIKERL_OK = 0,
+  SPIKERL_E_ARG = 1,         /* null pointer, batch < 1, size/shape mismatch                  */
+  SPIKERL_E_DOMAIN = 2,      /* T<1 or T>255, d_c/d_v outside [0,1], v_th<=0, window<=0, pop<1 */
+  SPIKERL_E_STATE = 3,       /* tape header does not match (cfg hash, batch) */
+  SPIKERL_E_NOTREADY = 4,    /* replay size < batch: nothing enqueued */
+  SPIKERL_E_CUDA = 5,
+  SPIKERL_E_NCCL = 6,
+  SPIKERL_E_UNSUPPORTED = 7  /* configuration outside what a kernel supports                 */
+};
+
+enum spikerl_precision {
+  SPIKERL_FP32 = 0,          /* true fp32 (no TF32) SIMT path; configs[0]                      */
+  SPIKERL_BF16 = 1           /* bf16 operands, fp32 accumulate, fp32 master */
+};
+
+enum spikerl_engine {
+  SPIKERL_ENGINE_AUTO = 0,   /* bf16 -> tcgen05 tensor-core GEMMs; fp32 -> SIMT              */
+  SPIKERL_ENGINE_SIMT = 1,   /* plain SIMT kernels (fp32 FFMA), any precision                 */
+  SPIKERL_ENGINE_TCGEN05 = 2 /* force tcgen05 (bf16 only)                                     */
+};
+
+/* Actor problem statement (PAPER.md:131 + north_star): obs dim S, action dim A, encoder
+ * population E, decoder population D, hidden widths N1, N2, T timesteps, LIF constants. */
+typedef struct {
+  int obs_dim, act_dim, pop_enc, pop_dec; /* S, A, E, D; K0 = S*E inputs, N3 = A*D outputs    */
+  int hidden1, hidden2;                   /* N1, N2                                           */
+  int T;                                  /* timesteps, 1..255                                */
+  float d_c, d_v, v_th;                   /* LIF constants (0.5, 0.75, 0.5)                   */
+  float surr_window, surr_height;         /* h(v) = height*[|v-v_th| < window] (0.5, 1.0)     */
+  float sigma_floor;                      /* sigma clamp after the actor Adam step (1e-3)     */
+  int precision;                          /* enum spikerl_precision                           */
+  int engine;                             /* enum spikerl_engine                              */
+} spikerl_actor_cfg;
+
+/* Twin critic Q_i(s,a) = W3 relu(W2 relu(W1 [s;a] + b1) + b2) + b3 (configs[1]). */
+typedef struct {
+  int in_dim;                             /* S + A                                            */
+  int hidden1, hidden2;                   /* 256, 256                                         */
+  int precision;                          /* enum spikerl_precision                           */
+} spikerl_critic_cfg;
+
+typedef struct {
+  float gamma, tau, policy_noise, noise_clip; /* 0.99, 0.005, 0.2, 0.5                        */
+  int policy_delay;                           /* 2                                            */
+  float lr_actor, lr_critic, beta1, beta2, eps; /* 1e-4, 1e-3, 0.9, 0.999, 1e-8             */
+  int batch;                                  /* per-rank batch B                             */
+} spikerl_td3_cfg;
+
+/* ------------------------------------------------------------------------------------------
+ * Sizes and layouts (host-only calls, no device work).
+ * Actor flat fp32 parameter layout (also used for grads and Adam m, v), element offsets:
+ *   mu[S][E] | sigma[S][E] | W1[N1][K0] | W2[N2][N1] | W3[N3][N2] | Wd[A][D] | bd[A]
+ * Critic flat fp32 layout (one critic; twins are [2][P]):
+ *   W1[H1][in] | b1[H1] | W2[H2][H1] | b2[H2] | W3[H2] | b3[1]
+ * ---------------------------------------------------------------------------------------- */
+enum { SPIKERL_ACTOR_MU = 0, SPIKERL_ACTOR_SIGMA, SPIKERL_ACTOR_W1, SPIKERL_ACTOR_W2,
+       SPIKERL_ACTOR_W3, SPIKERL_ACTOR_WD, SPIKERL_ACTOR_BD, SPIKERL_ACTOR_NPARAM };
+enum { SPIKERL_CRITIC_W1 = 0, SPIKERL_CRITIC_B1, SPIKERL_CRITIC_W2, SPIKERL_CRITIC_B2,
+       SPIKERL_CRITIC_W3, SPIKERL_CRITIC_B3, SPIKERL_CRITIC_NPARAM };
+
+/* Validate a cfg (returns a status, no side effects besides spikerl_last_error). */
+int spikerl_actor_cfg_check(const spikerl_actor_cfg* cfg);
+/* offsets (host, [SPIKERL_ACTOR_NPARAM+1] elements; last = total count). */
+int spikerl_actor_param_offsets(const spikerl_actor_cfg* cfg, size_t* offsets /* host */);
+size_t spikerl_actor_param_count(const spikerl_actor_cfg* cfg);
+int spikerl_critic_param_offsets(const spikerl_critic_cfg* cfg, size_t* offsets /* host */);
+size_t spikerl_critic_param_count(const spikerl_critic_cfg* cfg);
+/* bf16 working copies (opaque, zero-padded tensor-core layout); produced by *_refresh_bf16. */
+size_t spikerl_actor_bf16_bytes(const spikerl_actor_cfg* cfg);
+size_t spikerl_critic_bf16_bytes(const spikerl_critic_cfg* cfg);
+/* Device buffers the caller allocates for one forward(+backward) at `batch`. */
+size_t spikerl_actor_tape_bytes(const spikerl_actor_cfg* cfg, int batch);
+size_t spikerl_actor_workspace_bytes(const spikerl_actor_cfg* cfg, int batch);
+size_t spikerl_critic_workspace_bytes(const spikerl_critic_cfg* cfg, int batch);
+size_t spikerl_td3_workspace_bytes(const spikerl_actor_cfg* acfg, const spikerl_critic_cfg* ccfg,
+                                   int batch);
+
+/* Tape layout (byte offsets into the tape device buffer; all 256-byte aligned).
+ * Spike / surrogate-mask bit planes are u32 words [T][B][P_l/32]: bit j of word w is neuron
+ * 32w+j of layer l at (t, b); P_l = padded width (multiple of 128; pad bits are 0).
+ *   A      fp32 [B][K0]        Gaussian stimulation (kept for the encoder gradient)
+ *   bits0  u32  [T][B][P0/32]  encoder spikes
+ *   bits_l u32  [T][B][Pl/32]  LIF spikes of layer l = 1, 2, 3
+ *   mask_l u32  [T][B][Pl/32]  surrogate window bits [|v - v_th| < window], layer l = 1..3
+ *   counts u8   [B][N3]        output spike counts
+ *   act    fp32 [B][A]         decoded actions (for the decoder backward)              */
+typedef struct {
+  size_t A, bits[4], mask[4], counts, act, total;
+  int padded[4];           /* P0..P3                                                        */
+} spikerl_tape_layout;
+int spikerl_actor_tape_layout(const spikerl_actor_cfg* cfg, int batch, spikerl_tape_layout* out);
+
+/* Tape = HOST descriptor + caller-owned DEVICE buffer. forward() stamps magic/cfg_hash/batch
+ * on the host so backward() validates without a device->host copy. */
+typedef struct {
+  unsigned long long magic, cfg_hash;
+  int batch;
+  void* dev;               /* device buffer of spikerl_actor_tape_bytes(cfg, batch)          */
+  size_t bytes;
+} spikerl_tape;
+
+/* ------------------------------------------------------------------------------------------
+ * Compute entry points
+ * ---------------------------------------------------------------------------------------- */
+
+/* Refresh the bf16 working copy from the fp32 master (RNE; PAPER.md:153-174 master weights). */
+int spikerl_actor_refresh_bf16(const spikerl_actor_cfg* cfg, const float* params,
+                               void* params_bf16, spikerl_stream_t stream);
+int spikerl_critic_refresh_bf16(const spikerl_critic_cfg* cfg, int n_critics, const float* params,
+                                void* params_bf16, spikerl_stream_t stream);
+
+/* Actor forward: obs [B][S] fp32 -> actions [B][A] fp32 (tanh, bound 1).
+ * params: flat fp32 (layout above); params_bf16: working copy (required iff precision=BF16).
+ * tape: host descriptor whose .dev/.bytes the caller set (NULL = inference only: the spike
+ * planes go to `workspace`). workspace: spikerl_actor_workspace_bytes(cfg, batch). */
+int spikerl_actor_forward(const spikerl_actor_cfg* cfg, int batch, const float* params,
+                          const void* params_bf16, const float* obs, float* actions,
+                          spikerl_tape* tape, void* workspace, spikerl_stream_t stream);
+
+/* Actor backward (surrogate-gradient BPTT, reset gate detached).
+ * grad_actions [B][A] = dL/da. grad_params: flat fp32, overwritten (accumulate=0) or added to
+ * (accumulate=1). The tape must come from spikerl_actor_forward with the same cfg and batch
+ * (else SPIKERL_E_STATE). */
+int spikerl_actor_backward(const spikerl_actor_cfg* cfg, int batch, const float* params,
+                           const void* params_bf16, const float* obs, const spikerl_tape* tape,
+                           const float* grad_actions, float* grad_params, int accumulate,
+                           void* workspace, spikerl_stream_t stream);
+
+/* Twin critic forward (+ backward). x = [obs ; act] with obs_dim + act_dim == in_dim.
+ * params2 [2][P] fp32 (+ bf16 copy iff precision=BF16). q [2][B] receives Q1, Q2.
+ * If target_y [B] != NULL: loss (device scalar, may be NULL) = mean(Q1-y)^2 + mean(Q2-y)^2 and,
+ * if grad_params2 != NULL, its gradient w.r.t. both critics (overwritten).
+ * If grad_act [B][A] != NULL: grad_act = act_grad_scale * dQ1/da (per sample). */
+int spikerl_critic_fwd_bwd(const spikerl_critic_cfg* cfg, int batch, const float* params2,
+                           const void* params2_bf16, const float* obs, int obs_dim,
+                           const float* act, int act_dim, const float* target_y, float* q,
+                           float* loss, float* grad_params2, float* grad_act,
+                           float act_grad_scale, void* workspace, spikerl_stream_t stream);
+
+/* Adam (PyTorch form) over a flat fp32 buffer. step_counter: device int64[2] = {t, scratch};
+ * t is read as the previous step count and incremented by the call; scratch must be zero
+ * before the first call (the kernel restores it to zero). clamp_lo..clamp_hi (element range, may be empty) is clamped to
+ * >= clamp_min after the update (actor sigma floor). */
+int spikerl_adam(float* params, const float* grads, float* m, float* v, size_t n,
+                 long long* step_counter, float lr, float beta1, float beta2, float eps,
+                 size_t clamp_lo, size_t clamp_hi, float clamp_min, spikerl_stream_t stream);
+/* Polyak: target <- tau*source + (1-tau)*target over n fp32 elements. */
+int spikerl_polyak(float* target, const float* source, size_t n, float tau,
+                   spikerl_stream_t stream);
+
+/* ------------------------------------------------------------------------------------------
+ * TD3 update (one step k). All buffers caller-owned.
+ * ---------------------------------------------------------------------------------------- */
+typedef struct {
+  float *actor, *actor_t;          /* [Pa] fp32 master: online, target                        */
+  void *actor_bf16, *actor_t_bf16; /* working copies (BF16 precision)                         */
+  float *critic, *critic_t;        /* [2][Pc] fp32: online twins, target twins                */
+  void *critic_bf16, *critic_t_bf16;
+  float *m_actor, *v_actor;        /* Adam state [Pa]                                         */
+  float *m_critic, *v_critic;      /* Adam state [2][Pc]                                      */
+  float *grad_actor, *grad_critic; /* [Pa], [2][Pc]                                           */
+  long long* adam_steps;           /* device [4]: {critic t, 0, actor t, 0} (zero-initialised)  */
+  unsigned long long* rng_counter; /* device [1]: Philox counter, advanced every update       */
+  const float *rs, *ra, *rr, *rs2, *rd; /* replay shard SoA: s[N][S] a[N][A] r[N] s2[N][S] d[N] */
+  long long replay_size;           /* (host) N valid transitions                               */
+} spikerl_td3_bufs;
+
+struct spikerl_comm;
+typedef struct spikerl_comm spikerl_comm;
+
+/* One TD3 update. step = 1-based k; the actor and all targets are updated when
+ * k % policy_delay == 0. indices [B] (device int64) / noise [B][A] (device fp32 raw eps, before
+ * the clip to +-noise_clip) may be NULL: then they are drawn on the device with Philox
+ * (seed, rank, *rng_counter). comm == NULL means one GPU (no allreduce). losses: device [2]
+ * (critic loss; actor loss or unchanged on critic-only steps). */
+int spikerl_td3_update(const spikerl_actor_cfg* acfg, const spikerl_critic_cfg* ccfg,
+                       const spikerl_td3_cfg* hp, const spikerl_td3_bufs* bufs, long long step,
+                       unsigned long long seed, const long long* indices, const float* noise,
+                       spikerl_comm* comm, float* losses, void* workspace,
+                       spikerl_stream_t stream);
+
+/* Fill a replay shard on the device: s,s2 ~ N(0,1) clip +-5, a ~ U[-1,1], r ~ N(0,1),
+ * done ~ Bernoulli(p_done) (configs[1]); Philox keyed by (seed, rank). */
+int spikerl_replay_fill(float* s, float* a, float* r, float* s2, float* d, long long n, int obs_dim,
+                        int act_dim, float p_done, unsigned long long seed, int rank,
+                        spikerl_stream_t stream);
+
+/* ------------------------------------------------------------------------------------------
+ * Data-parallel communication (NCCL 2.28, loaded at spikerl_comm_init). PyTorch supplies only
+ * the rendezvous (broadcast of the 128-byte id).
+ * ---------------------------------------------------------------------------------------- */
+int spikerl_comm_get_unique_id(void* out128 /* host, 128 bytes */);
+int spikerl_comm_init(int rank, int world, const void* id128 /* host */, spikerl_comm** out);
+int spikerl_comm_destroy(spikerl_comm* comm);
+int spikerl_comm_world(const spikerl_comm* comm);
+int spikerl_comm_rank(const spikerl_comm* comm);
+/* in place: grads <- mean over ranks (ncclAvg, fp32)  — PAPER.md:135 average_gradients */
+int spikerl_allreduce_grads(spikerl_comm* comm, float* grads, size_t count,
+                            spikerl_stream_t stream);
+/* params <- params of `root`  — PAPER.md:135 broadcast_weights */
+int spikerl_broadcast_params(spikerl_comm* comm, float* params, size_t count, int root,
+                             spikerl_stream_t stream);
+
+/* ------------------------------------------------------------------------------------------
+ * Diagnostics
+ * ---------------------------------------------------------------------------------------- */
+const char* spikerl_last_error(void);   /* thread-local message for the last non-OK status  */
+const char* spikerl_version(void);
+/* Number of kernel launches the library enqueued since the last reset (host counter). */
+long long spikerl_launch_count(int reset);
+
+/* Opt-in per-launch timing: while enabled (and the stream is not capturing) every kernel launch
+ * is bracketed by CUDA events on its own stream, tagged with the algorithmic work the launcher
+ * attributes to it. enable(0/1) clears previous records. summary() synchronises on the recorded
+ * events and aggregates per kernel name; returns the number of distinct kernels (or -1). */
+typedef struct {
+  char name[48];
+  int bound;            /* 0 = HBM bytes, 1 = tensor-core flops, 2 = SIMT ALU flops, 3 = latency */
+  long long launches;
+  double total_ms;
+  double flops, bytes;  /* algorithmic work summed over the launches                            */
+} spikerl_prof_entry;
+void spikerl_prof_enable(int on);
+int spikerl_prof_summary(spikerl_prof_entry* out, int max_entries);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* SPIKERL_H */

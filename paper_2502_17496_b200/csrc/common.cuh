@@ -1,0 +1,130 @@
+// common.cuh — shared internals of libspikerl.so (product path only; no oracle code here).
+#pragma once
+#include <cuda_runtime.h>
+#include <cuda_bf16.h>
+#include <cstdint>
+#include <cstddef>
+#include "spikerl.h"
+
+namespace spk {
+
+// ----------------------------------------------------------------------------- errors
+void set_error(const char* fmt, ...);
+void note_launch(int n = 1);
+
+#define SPK_CHECK_CUDA(expr)                                                         \
+  do {                                                                               \
+    cudaError_t e_ = (expr);                                                         \
+    if (e_ != cudaSuccess) {                                                         \
+      ::spk::set_error("%s failed: %s (%s:%d)", #expr, cudaGetErrorString(e_),       \
+                       __FILE__, __LINE__);                                          \
+      return SPIKERL_E_CUDA;                                                         \
+    }                                                                                \
+  } while (0)
+
+#define SPK_LAUNCHED()                                                               \
+  do {                                                                               \
+    ::spk::note_launch();                                                            \
+    cudaError_t e_ = cudaGetLastError();                                             \
+    if (e_ != cudaSuccess) {                                                         \
+      ::spk::set_error("kernel launch failed: %s (%s:%d)", cudaGetErrorString(e_),   \
+                       __FILE__, __LINE__);                                          \
+      return SPIKERL_E_CUDA;                                                         \
+    }                                                                                \
+  } while (0)
+
+#define SPK_TRY(expr)                                                                \
+  do {                                                                               \
+    int s_ = (expr);                                                                 \
+    if (s_ != SPIKERL_OK) return s_;                                                 \
+  } while (0)
+
+inline size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
+inline int round_up(int x, int a) { return (x + a - 1) / a * a; }
+inline int cdiv(long long x, long long a) { return (int)((x + a - 1) / a); }
+
+// ----------------------------------------------------------------------------- dims
+constexpr int kPad = 128;  // neuron padding (MMA M tile; multiple of the 64-wide K tile)
+
+struct ActorDims {
+  int S, A, E, D, K0, N1, N2, N3, T;
+  int N[4];       // true widths N0=K0, N1, N2, N3
+  int P[4];       // padded widths (multiples of kPad)
+  int Wd[4];      // u32 words per (t,b) row = P/32
+  size_t off[SPIKERL_ACTOR_NPARAM + 1];
+  size_t boff[4]; // bf16 copy element offsets of W1, W2, W3 ([P_l][P_{l-1}] each); boff[3] = total
+  float dc, dv, vth, win, zh, sigma_floor;
+  int bf16;       // precision == BF16
+  int engine;     // resolved: SPIKERL_ENGINE_SIMT or SPIKERL_ENGINE_TCGEN05
+};
+int actor_dims(const spikerl_actor_cfg* cfg, ActorDims* d);
+unsigned long long actor_cfg_hash(const spikerl_actor_cfg* cfg);
+
+struct TapeLayout {
+  size_t A, bits[4], mask[4], counts, act, total;
+};
+TapeLayout tape_layout(const ActorDims& d, int B);
+
+struct CriticDims {
+  int in, H1, H2, bf16;
+  size_t off[SPIKERL_CRITIC_NPARAM + 1];
+};
+int critic_dims(const spikerl_critic_cfg* cfg, CriticDims* d);
+
+// ----------------------------------------------------------------------------- device helpers
+__device__ __forceinline__ float bf16_round(float x) {
+  return __bfloat162float(__float2bfloat16_rn(x));
+}
+
+template <typename T> struct GT;
+template <> struct GT<float> {
+  __device__ __forceinline__ static float load(const float* p) { return *p; }
+  __device__ __forceinline__ static void store(float* p, float v) { *p = v; }
+  __device__ __forceinline__ static float round(float v) { return v; }
+};
+template <> struct GT<__nv_bfloat16> {
+  __device__ __forceinline__ static float load(const __nv_bfloat16* p) { return __bfloat162float(*p); }
+  __device__ __forceinline__ static void store(__nv_bfloat16* p, float v) { *p = __float2bfloat16_rn(v); }
+  __device__ __forceinline__ static float round(float v) { return bf16_round(v); }
+};
+
+// LIF scan step shared by every forward kernel (north_star equations).
+// Uses explicit round-to-nearest ops (no FMA contraction) so all engines agree bit-for-bit on
+// identical currents.
+struct LifConst { float dc, dv, vth, win; };
+__device__ __forceinline__ void lif_step(const LifConst& k, float I, float& c, float& v, bool& o,
+                                         bool& h) {
+  c = __fadd_rn(__fmul_rn(k.dc, c), I);
+  float vv = o ? 0.0f : __fmul_rn(k.dv, v);   // d_v * v * (1 - o_prev), exact gate
+  v = __fadd_rn(vv, c);
+  o = v > k.vth;
+  h = fabsf(__fsub_rn(v, k.vth)) < k.win;
+}
+
+// Reverse-scan step (rho = 0; reset gate detached): given g_o(t), o_t, h_t (bits) and the
+// carried (dv_next, dc_next), returns G_t = delta_c_t.  SPEC.md:168-176; R11.
+__device__ __forceinline__ float lif_back_step(float zh, float dvc, float dcc, float g, bool o,
+                                               bool h, float& dvn, float& dcn) {
+  float dvt = __fadd_rn(h ? __fmul_rn(zh, g) : 0.0f, o ? 0.0f : __fmul_rn(dvc, dvn));
+  float dct = __fadd_rn(dvt, __fmul_rn(dcc, dcn));
+  dvn = dvt;
+  dcn = dct;
+  return dct;
+}
+
+}  // namespace spk
+
+// ----------------------------------------------------------------------------- profiling
+// Optional per-launch CUDA-event timing (spikerl_prof_*): bench.py uses it to time the
+// dominant kernel on the stream it is launched on and to read the algorithmic work the
+// launcher attributes to that launch (flops or bytes), for the roofline fraction.
+namespace spk {
+enum ProfBound { PB_HBM = 0, PB_TENSOR = 1, PB_ALU = 2, PB_LATENCY = 3 };
+bool prof_on();
+struct ProfScope {
+  int slot = -1;
+  cudaStream_t st;
+  ProfScope(const char* name, int bound, double flops, double bytes, cudaStream_t s);
+  ~ProfScope();
+};
+}  // namespace spk

@@ -1,0 +1,72 @@
+// internal.h — launchers shared between the ABI layer and the kernel files.
+#pragma once
+#include "common.cuh"
+
+namespace spk {
+
+// ---- encoder (k_encoder.cu)
+int launch_enc_fwd(const ActorDims& d, int B, const float* obs, const float* mu, const float* sigma,
+                   float* A, uint32_t* bits0, cudaStream_t st);
+
+// ---- SIMT actor kernels (k_actor_simt.cu)
+// forward layer l (1..3): bits_in [T][B][W_{l-1}] -> bits_out, mask_out [T][B][W_l] (+counts)
+int launch_lif_fwd_simt(const ActorDims& d, int l, int B, const uint32_t* bits_in,
+                        const float* Wf32, const __nv_bfloat16* Wb16, uint32_t* bits_out,
+                        uint32_t* mask_out, uint8_t* counts, cudaStream_t st);
+int launch_dec_fwd(const ActorDims& d, int B, const uint8_t* counts, const float* Wd,
+                   const float* bd, float* act_out, float* act_tape, cudaStream_t st);
+// decoder backward + output-layer reverse scan -> G3 [T][B][P3] (fp32 or bf16 per precision)
+int launch_dec_bwd_outscan(const ActorDims& d, int B, const float* grad_a, const float* act,
+                           const uint8_t* counts, const float* Wd, const uint32_t* bits3,
+                           const uint32_t* mask3, void* G3, float* g_pre, cudaStream_t st);
+int launch_dec_param_grads(const ActorDims& d, int B, const float* g_pre, const uint8_t* counts,
+                           float* dWd, float* dbd, int accumulate, cudaStream_t st);
+// dX of layer l (3 or 2) fused with the reverse scan of layer l-1 -> G_{l-1} (+Gsum if l==2)
+int launch_lif_dx_simt(const ActorDims& d, int l, int B, const void* Gl, const float* Wf32,
+                       const __nv_bfloat16* Wb16, const uint32_t* bits_prev,
+                       const uint32_t* mask_prev, void* Gprev, void* Gsum, cudaStream_t st);
+// dW_l = sum_{t,b} G_l^T o_{l-1}  (fp32 [N_l][N_{l-1}] in the master layout)
+int launch_lif_dw_simt(const ActorDims& d, int l, int B, const void* Gl, const uint32_t* bits_prev,
+                       float* dW, int accumulate, cudaStream_t st);
+// encoder gradient from Gsum1 [B][P1]: dmu, dsigma (two-pass deterministic)
+int launch_enc_grad_simt(const ActorDims& d, int B, const void* Gsum, const float* W1f32,
+                         const __nv_bfloat16* W1b16, const float* A, const float* obs,
+                         const float* mu, const float* sigma, float* partial, float* dmu,
+                         float* dsigma, int accumulate, cudaStream_t st);
+size_t enc_grad_partial_bytes(const ActorDims& d, int B);
+
+// ---- tcgen05 engine (k_tc_gemm.cu)
+bool tc_supported(const ActorDims& d);
+int launch_lif_fwd_tc(const ActorDims& d, int l, int B, const uint32_t* bits_in,
+                      const __nv_bfloat16* Wb16, uint32_t* bits_out, uint32_t* mask_out,
+                      uint8_t* counts, cudaStream_t st);
+
+// ---- optimiser / copies (k_optim.cu)
+int launch_actor_refresh_bf16(const ActorDims& d, const float* params, __nv_bfloat16* out,
+                              cudaStream_t st);
+int launch_f32_to_bf16(const float* in, __nv_bfloat16* out, size_t n, cudaStream_t st);
+int launch_adam(float* p, const float* g, float* m, float* v, size_t n, long long* counter,
+                float lr, float b1, float b2, float eps, size_t clo, size_t chi, float cmin,
+                unsigned int* done_ticket, cudaStream_t st);
+int launch_polyak(float* t, const float* s, size_t n, float tau, cudaStream_t st);
+
+// ---- critic (k_critic.cu)
+size_t critic_ws_bytes(const CriticDims& c, int B);
+int critic_fwd_bwd(const CriticDims& c, int B, const float* params2, const __nv_bfloat16* pb16,
+                   const float* obs, int S, const float* act, int A, const float* y, float* q,
+                   float* loss, float* grad2, float* grad_act, float act_scale, int n_critics,
+                   void* ws, cudaStream_t st);
+
+// ---- replay / TD3 glue (k_replay.cu)
+int launch_replay_gather(int B, int S, int A, const float* rs, const float* ra, const float* rr,
+                         const float* rs2, const float* rd, long long N, const long long* idx,
+                         unsigned long long seed, int rank, const unsigned long long* counter,
+                         float* s, float* a, float* r, float* s2, float* d, cudaStream_t st);
+int launch_target_action(int B, int A, const float* a2, const float* noise, float sigma,
+                         float clip, unsigned long long seed, int rank,
+                         unsigned long long* counter, float* at, cudaStream_t st);
+int launch_td_target(int B, const float* r, const float* d, const float* q2, float gamma,
+                     float* y, cudaStream_t st);
+int launch_scale(float* x, size_t n, float s, cudaStream_t st);
+
+}  // namespace spk

@@ -1,0 +1,53 @@
+// k_encoder.cu — K1: Gaussian receptive-field stimulation + deterministic soft-reset encoder
+// spikes, written straight into the bit-packed spike plane of layer 0.
+//   PAPER.md:131 (§III-A "populations use Gaussian distributions to transform continuous input
+//   values into spike trains"); north_star ("deterministic soft-reset encoder spikes");
+//   SPEC.md:123-140; R4 (fp64 exponent, RNE to fp32, no FTZ) and R5 (acc >= 1).
+// HBM-bound elementwise kernel: one thread per (b, k); a warp owns 32 consecutive encoder
+// neurons so one __ballot_sync per timestep yields exactly one u32 word of bits0[t][b][:].
+#include "internal.h"
+
+namespace spk {
+
+__global__ void __launch_bounds__(128) enc_fwd_kernel(int B, int S, int E, int K0, int W0, int T,
+                                                      const float* __restrict__ obs,
+                                                      const float* __restrict__ mu,
+                                                      const float* __restrict__ sigma,
+                                                      float* __restrict__ A_out,
+                                                      uint32_t* __restrict__ bits0) {
+  const int b = blockIdx.x;
+  const int k = blockIdx.y * blockDim.x + threadIdx.x;
+  const int lane = threadIdx.x & 31;
+  float A = 0.0f;
+  if (k < K0) {
+    const int i = k / E;
+    const double s = (double)__ldg(obs + (size_t)b * S + i);
+    const double m = (double)__ldg(mu + k);
+    const double sg = (double)__ldg(sigma + k);
+    const double dd = __dsub_rn(s, m);
+    const double q = __dmul_rn(dd, dd);
+    const double den = __dmul_rn(2.0, __dmul_rn(sg, sg));
+    A = (float)exp(-__ddiv_rn(q, den));  // RNE double -> float
+    A_out[(size_t)b * K0 + k] = A;
+  }
+  float acc = 0.0f;
+  const size_t word = (size_t)b * W0 + (k >> 5);
+  for (int t = 0; t < T; ++t) {
+    acc = __fadd_rn(acc, A);
+    const bool fire = acc >= 1.0f;
+    if (fire) acc = __fsub_rn(acc, 1.0f);
+    const uint32_t w = __ballot_sync(0xffffffffu, fire);
+    if (lane == 0) bits0[(size_t)t * B * W0 + word] = w;
+  }
+}
+
+int launch_enc_fwd(const ActorDims& d, int B, const float* obs, const float* mu, const float* sigma,
+                   float* A, uint32_t* bits0, cudaStream_t st) {
+  ProfScope ps_("enc_fwd", PB_HBM, 0.0, 4.0 * B * (d.S + d.K0 + (double)d.T * d.Wd[0]), st);
+  dim3 grid(B, d.P[0] / 128);
+  enc_fwd_kernel<<<grid, 128, 0, st>>>(B, d.S, d.E, d.K0, d.Wd[0], d.T, obs, mu, sigma, A, bits0);
+  SPK_LAUNCHED();
+  return SPIKERL_OK;
+}
+
+}  // namespace spk

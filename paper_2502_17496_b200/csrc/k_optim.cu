@@ -1,0 +1,145 @@
+// k_optim.cu — K10 Adam (PyTorch form, R19) with the actor sigma floor
+// (R12), K11 Polyak soft update, and the bf16 working-copy
+// refresh (master fp32 -> RNE bf16; "master copy of weights in full precision").
+// HBM-bound, vectorised elementwise kernels, grid sized in multiples of the 148 SMs.
+#include "internal.h"
+
+namespace spk {
+
+constexpr int kSMs = 148;
+
+static int ew_grid(size_t n, int per_thread) {
+  const size_t threads = (n + per_thread - 1) / per_thread;
+  const size_t blocks = (threads + 255) / 256;
+  const size_t cap = (size_t)kSMs * 8;
+  return (int)(blocks < cap ? (blocks > 0 ? blocks : 1) : cap);
+}
+
+// ------------------------------------------------------------------ bf16 working copies
+// Actor: W_l (fp32 [N_l][N_{l-1}]) -> bf16 [P_l][P_{l-1}], zero padded. One thread per padded
+// element so the padding is (re)written with zeros every refresh.
+__global__ void actor_refresh_kernel(const float* __restrict__ W, int N, int K, int P, int Pk,
+                                     __nv_bfloat16* __restrict__ out) {
+  const size_t total = (size_t)P * Pk;
+  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < total;
+       i += (size_t)gridDim.x * blockDim.x) {
+    const int n = (int)(i / Pk), k = (int)(i % Pk);
+    const float v = (n < N && k < K) ? W[(size_t)n * K + k] : 0.0f;
+    out[i] = __float2bfloat16_rn(v);
+  }
+}
+
+int launch_actor_refresh_bf16(const ActorDims& d, const float* params, __nv_bfloat16* out,
+                              cudaStream_t st) {
+  ProfScope ps_("refresh_bf16", PB_HBM, 0.0, 6.0 * d.boff[3], st);
+  for (int l = 1; l <= 3; ++l) {
+    const size_t total = (size_t)d.P[l] * d.P[l - 1];
+    actor_refresh_kernel<<<ew_grid(total, 4), 256, 0, st>>>(
+        params + d.off[SPIKERL_ACTOR_W1 + l - 1], d.N[l], d.N[l - 1], d.P[l], d.P[l - 1],
+        out + d.boff[l - 1]);
+    SPK_LAUNCHED();
+  }
+  return SPIKERL_OK;
+}
+
+__global__ void f32_to_bf16_kernel(const float* __restrict__ in, __nv_bfloat16* __restrict__ out,
+                                   size_t n) {
+  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n;
+       i += (size_t)gridDim.x * blockDim.x)
+    out[i] = __float2bfloat16_rn(in[i]);
+}
+
+int launch_f32_to_bf16(const float* in, __nv_bfloat16* out, size_t n, cudaStream_t st) {
+  ProfScope ps_("f32_to_bf16", PB_HBM, 0.0, 6.0 * n, st);
+  f32_to_bf16_kernel<<<ew_grid(n, 4), 256, 0, st>>>(in, out, n);
+  SPK_LAUNCHED();
+  return SPIKERL_OK;
+}
+
+// ------------------------------------------------------------------ Adam
+// t = *counter + 1 is read by every block; the last block to finish (atomic ticket) stores it
+// back, so the call is graph-replayable with an on-device step count.
+__global__ void __launch_bounds__(256) adam_kernel(float* __restrict__ p, const float* __restrict__ g,
+                                                   float* __restrict__ m, float* __restrict__ v,
+                                                   size_t n, long long* counter, float lr, float b1,
+                                                   float b2, float eps, size_t clo, size_t chi,
+                                                   float cmin, unsigned int* ticket) {
+  const long long t = *(volatile long long*)counter + 1;
+  const double bc1 = 1.0 - pow((double)b1, (double)t);
+  const double bc2 = 1.0 - pow((double)b2, (double)t);
+  const float step_size = (float)((double)lr / bc1);
+  const float bc2_sqrt = (float)sqrt(bc2);
+  const float omb1 = 1.0f - b1, omb2 = 1.0f - b2;
+  const size_t n4 = n / 4;
+  const size_t stride = (size_t)gridDim.x * blockDim.x;
+  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n4; i += stride) {
+    float4 pp = reinterpret_cast<float4*>(p)[i];
+    const float4 gg = reinterpret_cast<const float4*>(g)[i];
+    float4 mm = reinterpret_cast<float4*>(m)[i];
+    float4 vv = reinterpret_cast<float4*>(v)[i];
+    float* pa = &pp.x; const float* ga = &gg.x; float* ma = &mm.x; float* va = &vv.x;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      ma[j] = __fadd_rn(__fmul_rn(b1, ma[j]), __fmul_rn(omb1, ga[j]));
+      va[j] = __fadd_rn(__fmul_rn(b2, va[j]), __fmul_rn(__fmul_rn(omb2, ga[j]), ga[j]));
+      const float denom = __fadd_rn(__fdiv_rn(sqrtf(va[j]), bc2_sqrt), eps);
+      pa[j] = __fsub_rn(pa[j], __fmul_rn(step_size, __fdiv_rn(ma[j], denom)));
+      const size_t e = 4 * i + j;
+      if (e >= clo && e < chi) pa[j] = fmaxf(pa[j], cmin);
+    }
+    reinterpret_cast<float4*>(p)[i] = pp;
+    reinterpret_cast<float4*>(m)[i] = mm;
+    reinterpret_cast<float4*>(v)[i] = vv;
+  }
+  for (size_t e = 4 * n4 + blockIdx.x * (size_t)blockDim.x + threadIdx.x; e < n; e += stride) {
+    float mm = __fadd_rn(__fmul_rn(b1, m[e]), __fmul_rn(omb1, g[e]));
+    float vv = __fadd_rn(__fmul_rn(b2, v[e]), __fmul_rn(__fmul_rn(omb2, g[e]), g[e]));
+    const float denom = __fadd_rn(__fdiv_rn(sqrtf(vv), bc2_sqrt), eps);
+    float pp = __fsub_rn(p[e], __fmul_rn(step_size, __fdiv_rn(mm, denom)));
+    if (e >= clo && e < chi) pp = fmaxf(pp, cmin);
+    p[e] = pp; m[e] = mm; v[e] = vv;
+  }
+  // publish the new step count once every block has read the old one
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    const unsigned int done = atomicAdd(ticket, 1u);
+    if (done == gridDim.x - 1) {
+      *counter = t;
+      *ticket = 0u;
+      __threadfence();
+    }
+  }
+}
+
+int launch_adam(float* p, const float* g, float* m, float* v, size_t n, long long* counter,
+                float lr, float b1, float b2, float eps, size_t clo, size_t chi, float cmin,
+                unsigned int* ticket, cudaStream_t st) {
+  ProfScope ps_("adam", PB_HBM, 0.0, 28.0 * n, st);
+  if (((uintptr_t)p | (uintptr_t)g | (uintptr_t)m | (uintptr_t)v) & 15) {
+    set_error("adam: buffers must be 16-byte aligned");
+    return SPIKERL_E_ARG;
+  }
+  adam_kernel<<<ew_grid(n, 4), 256, 0, st>>>(p, g, m, v, n, counter, lr, b1, b2, eps, clo, chi,
+                                             cmin, ticket);
+  SPK_LAUNCHED();
+  return SPIKERL_OK;
+}
+
+// ------------------------------------------------------------------ Polyak
+__global__ void polyak_kernel(float* __restrict__ t, const float* __restrict__ s, size_t n,
+                              float tau) {
+  const float omt = 1.0f - tau;
+  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n;
+       i += (size_t)gridDim.x * blockDim.x)
+    t[i] = __fadd_rn(__fmul_rn(tau, s[i]), __fmul_rn(omt, t[i]));
+}
+
+int launch_polyak(float* t, const float* s, size_t n, float tau, cudaStream_t st) {
+  ProfScope ps_("polyak", PB_HBM, 0.0, 12.0 * n, st);
+  polyak_kernel<<<ew_grid(n, 1), 256, 0, st>>>(t, s, n, tau);
+  SPK_LAUNCHED();
+  return SPIKERL_OK;
+}
+
+}  // namespace spk

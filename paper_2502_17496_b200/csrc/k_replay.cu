@@ -1,0 +1,186 @@
+// k_replay.cu — K9: device-resident replay sampling and the TD3 target arithmetic.
+//   Replay: uniform sampling with replacement; synthetic shard recipe of
+//   configs[1] (s, s' ~ N(0,1) clipped +-5; a ~ U[-1,1]; r ~ N(0,1); done ~ Bernoulli(0.01)).
+//   Target smoothing and target: SPEC.md:235-243 (a~ = clip(pi'(s') + clip(eps,-c,c), -1, 1);
+//   y = r + gamma (1 - done) min(Q1', Q2')).
+// Random numbers: counter-based Philox4x32-10 keyed by (seed, rank); the counter lives on the
+// device so a captured CUDA graph draws fresh numbers on every replay.
+#include "internal.h"
+
+namespace spk {
+
+struct Philox {
+  __device__ static uint4 round(uint4 c, uint2 k) {
+    const uint32_t M0 = 0xD2511F53u, M1 = 0xCD9E8D57u;
+    const uint32_t hi0 = __umulhi(M0, c.x), lo0 = M0 * c.x;
+    const uint32_t hi1 = __umulhi(M1, c.z), lo1 = M1 * c.z;
+    return make_uint4(hi1 ^ c.y ^ k.x, lo1, hi0 ^ c.w ^ k.y, lo0);
+  }
+  __device__ static uint4 gen(uint4 c, uint2 k) {
+#pragma unroll
+    for (int i = 0; i < 10; ++i) {
+      c = round(c, k);
+      k.x += 0x9E3779B9u;
+      k.y += 0xBB67AE85u;
+    }
+    return c;
+  }
+};
+
+__device__ __forceinline__ uint2 philox_key(unsigned long long seed, int rank) {
+  return make_uint2((uint32_t)seed, (uint32_t)(seed >> 32) ^ (0x85EBCA6Bu * (uint32_t)(rank + 1)));
+}
+__device__ __forceinline__ float u01(uint32_t x) {  // (0, 1]
+  return ((float)(x >> 8) + 1.0f) * (1.0f / 16777216.0f);
+}
+__device__ __forceinline__ float2 box_muller(uint32_t a, uint32_t b) {
+  const float r = sqrtf(-2.0f * logf(u01(a)));
+  float s, c;
+  sincospif(2.0f * u01(b), &s, &c);
+  return make_float2(r * c, r * s);
+}
+
+enum Purpose : uint32_t { P_INDEX = 1, P_NOISE = 2, P_FILL = 3 };
+
+// one warp per sampled row: lane 0 draws the index, the warp copies the row's columns
+__global__ void replay_gather_kernel(int B, int S, int A, const float* __restrict__ rs,
+                                     const float* __restrict__ ra, const float* __restrict__ rr,
+                                     const float* __restrict__ rs2, const float* __restrict__ rd,
+                                     long long N, const long long* __restrict__ idx,
+                                     unsigned long long seed, int rank,
+                                     const unsigned long long* __restrict__ counter,
+                                     float* __restrict__ s, float* __restrict__ a,
+                                     float* __restrict__ r, float* __restrict__ s2,
+                                     float* __restrict__ d) {
+  const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
+  if (warp >= B) return;
+  long long i = 0;
+  if (lane == 0) {
+    if (idx) {
+      i = idx[warp];
+    } else {
+      const unsigned long long ctr = *counter;
+      const uint4 x = Philox::gen(make_uint4((uint32_t)warp, P_INDEX, (uint32_t)ctr, (uint32_t)(ctr >> 32)),
+                                  philox_key(seed, rank));
+      const unsigned long long u = ((unsigned long long)x.x << 32) | x.y;
+      i = (long long)(u % (unsigned long long)N);
+    }
+  }
+  i = __shfl_sync(0xffffffffu, i, 0);
+  for (int c = lane; c < S; c += 32) {
+    s[(size_t)warp * S + c] = rs[(size_t)i * S + c];
+    s2[(size_t)warp * S + c] = rs2[(size_t)i * S + c];
+  }
+  for (int c = lane; c < A; c += 32) a[(size_t)warp * A + c] = ra[(size_t)i * A + c];
+  if (lane == 0) {
+    r[warp] = rr[i];
+    d[warp] = rd[i];
+  }
+}
+
+int launch_replay_gather(int B, int S, int A, const float* rs, const float* ra, const float* rr,
+                         const float* rs2, const float* rd, long long N, const long long* idx,
+                         unsigned long long seed, int rank, const unsigned long long* counter,
+                         float* s, float* a, float* r, float* s2, float* d, cudaStream_t st) {
+  ProfScope ps_("replay_gather", PB_LATENCY, 0.0, 8.0 * B * (2.0 * S + A + 2), st);
+  replay_gather_kernel<<<cdiv((long long)B * 32, 256), 256, 0, st>>>(B, S, A, rs, ra, rr, rs2, rd, N, idx,
+                                                                     seed, rank, counter, s, a, r, s2, d);
+  SPK_LAUNCHED();
+  return SPIKERL_OK;
+}
+
+// a~ = clip(a2 + clip(eps, -c, c), -1, 1); single block; advances the Philox counter at the end.
+__global__ void __launch_bounds__(1024) target_action_kernel(int B, int A, const float* __restrict__ a2,
+                                                             const float* __restrict__ noise,
+                                                             float sigma, float clip,
+                                                             unsigned long long seed, int rank,
+                                                             unsigned long long* counter,
+                                                             float* __restrict__ at) {
+  const unsigned long long ctr = *counter;
+  const int n = B * A;
+  for (int i = threadIdx.x; i < n; i += blockDim.x) {
+    float eps;
+    if (noise) {
+      eps = noise[i];
+    } else {
+      const uint4 x = Philox::gen(make_uint4((uint32_t)(i >> 1), P_NOISE, (uint32_t)ctr, (uint32_t)(ctr >> 32)),
+                                  philox_key(seed, rank));
+      const float2 z = box_muller(x.x, x.y);
+      eps = sigma * ((i & 1) ? z.y : z.x);
+    }
+    eps = fminf(fmaxf(eps, -clip), clip);
+    at[i] = fminf(fmaxf(__fadd_rn(a2[i], eps), -1.0f), 1.0f);
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) *counter = ctr + 1;
+}
+
+int launch_target_action(int B, int A, const float* a2, const float* noise, float sigma, float clip,
+                         unsigned long long seed, int rank, unsigned long long* counter, float* at,
+                         cudaStream_t st) {
+  ProfScope ps_("target_action", PB_LATENCY, 0.0, 12.0 * B * A, st);
+  target_action_kernel<<<1, 1024, 0, st>>>(B, A, a2, noise, sigma, clip, seed, rank, counter, at);
+  SPK_LAUNCHED();
+  return SPIKERL_OK;
+}
+
+__global__ void td_target_kernel(int B, const float* __restrict__ r, const float* __restrict__ d,
+                                 const float* __restrict__ q2, float gamma, float* __restrict__ y) {
+  const int b = blockIdx.x * blockDim.x + threadIdx.x;
+  if (b >= B) return;
+  const float qmin = fminf(q2[b], q2[B + b]);
+  y[b] = __fadd_rn(r[b], __fmul_rn(__fmul_rn(gamma, __fsub_rn(1.0f, d[b])), qmin));
+}
+
+int launch_td_target(int B, const float* r, const float* d, const float* q2, float gamma, float* y,
+                     cudaStream_t st) {
+  ProfScope ps_("td_target", PB_LATENCY, 0.0, 20.0 * B, st);
+  td_target_kernel<<<cdiv(B, 256), 256, 0, st>>>(B, r, d, q2, gamma, y);
+  SPK_LAUNCHED();
+  return SPIKERL_OK;
+}
+
+__global__ void scale_kernel(float* x, size_t n, float s) {
+  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x)
+    x[i] = __fmul_rn(x[i], s);
+}
+
+int launch_scale(float* x, size_t n, float s, cudaStream_t st) {
+  scale_kernel<<<cdiv((long long)n, 256) < 1184 ? cdiv((long long)n, 256) : 1184, 256, 0, st>>>(x, n, s);
+  SPK_LAUNCHED();
+  return SPIKERL_OK;
+}
+
+// synthetic shard fill (configs[1] distributions)
+__global__ void replay_fill_kernel(float* s, float* a, float* r, float* s2, float* d, long long n,
+                                   int S, int A, float p_done, unsigned long long seed, int rank) {
+  const long long stride = (long long)gridDim.x * blockDim.x;
+  const uint2 key = philox_key(seed, rank);
+  const long long per = 2LL * S + A + 2;
+  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < n * per; e += stride) {
+    const uint4 x = Philox::gen(make_uint4((uint32_t)e, P_FILL, (uint32_t)(e >> 32), 0u), key);
+    const long long row = e / per;
+    const int c = (int)(e % per);
+    const float z = box_muller(x.x, x.y).x;
+    if (c < S) s[row * S + c] = fminf(fmaxf(z, -5.f), 5.f);
+    else if (c < 2 * S) s2[row * S + (c - S)] = fminf(fmaxf(z, -5.f), 5.f);
+    else if (c < 2 * S + A) a[row * A + (c - 2 * S)] = 2.0f * u01(x.z) - 1.0f;
+    else if (c == 2 * S + A) r[row] = z;
+    else d[row] = u01(x.w) <= p_done ? 1.0f : 0.0f;
+  }
+}
+
+}  // namespace spk
+
+extern "C" int spikerl_replay_fill(float* s, float* a, float* r, float* s2, float* d, long long n,
+                                   int obs_dim, int act_dim, float p_done, unsigned long long seed,
+                                   int rank, spikerl_stream_t stream) {
+  if (!s || !a || !r || !s2 || !d || n < 1 || obs_dim < 1 || act_dim < 1) {
+    spk::set_error("spikerl_replay_fill: bad arguments");
+    return SPIKERL_E_ARG;
+  }
+  spk::replay_fill_kernel<<<148 * 8, 256, 0, (cudaStream_t)stream>>>(s, a, r, s2, d, n, obs_dim, act_dim,
+                                                                      p_done, seed, rank);
+  SPK_LAUNCHED();
+  return SPIKERL_OK;
+}

@@ -1,0 +1,80 @@
+// prof.cu — opt-in launch timing with CUDA events (never active inside a graph capture).
+#include <cstring>
+#include <map>
+#include <mutex>
+#include <string>
+#include <vector>
+#include "internal.h"
+
+namespace spk {
+namespace {
+struct Rec {
+  const char* name;
+  int bound;
+  double flops, bytes;
+  cudaEvent_t e0, e1;
+};
+std::mutex g_mu;
+std::vector<Rec> g_recs;
+bool g_on = false;
+}  // namespace
+
+bool prof_on() { return g_on; }
+
+ProfScope::ProfScope(const char* name, int bound, double flops, double bytes, cudaStream_t s) : st(s) {
+  if (!g_on) return;
+  cudaStreamCaptureStatus cs;
+  if (cudaStreamIsCapturing(s, &cs) != cudaSuccess || cs != cudaStreamCaptureStatusNone) return;
+  Rec r{name, bound, flops, bytes, nullptr, nullptr};
+  cudaEventCreate(&r.e0);
+  cudaEventCreate(&r.e1);
+  cudaEventRecord(r.e0, s);
+  std::lock_guard<std::mutex> lk(g_mu);
+  slot = (int)g_recs.size();
+  g_recs.push_back(r);
+}
+
+ProfScope::~ProfScope() {
+  if (slot < 0) return;
+  std::lock_guard<std::mutex> lk(g_mu);
+  cudaEventRecord(g_recs[slot].e1, st);
+}
+
+}  // namespace spk
+
+extern "C" {
+
+void spikerl_prof_enable(int on) {
+  std::lock_guard<std::mutex> lk(spk::g_mu);
+  for (auto& r : spk::g_recs) { cudaEventDestroy(r.e0); cudaEventDestroy(r.e1); }
+  spk::g_recs.clear();
+  spk::g_on = on != 0;
+}
+
+int spikerl_prof_summary(spikerl_prof_entry* out, int max_entries) {
+  std::lock_guard<std::mutex> lk(spk::g_mu);
+  std::map<std::string, spikerl_prof_entry> agg;
+  for (auto& r : spk::g_recs) {
+    if (cudaEventSynchronize(r.e1) != cudaSuccess) { spk::set_error("prof: event sync failed"); return -1; }
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, r.e0, r.e1);
+    auto& e = agg[r.name];
+    if (e.launches == 0) {
+      memset(&e, 0, sizeof(e));
+      strncpy(e.name, r.name, sizeof(e.name) - 1);
+      e.bound = r.bound;
+    }
+    e.launches += 1;
+    e.total_ms += ms;
+    e.flops += r.flops;
+    e.bytes += r.bytes;
+  }
+  int n = 0;
+  for (auto& kv : agg) {
+    if (n < max_entries && out) out[n] = kv.second;
+    ++n;
+  }
+  return n;
+}
+
+}  // extern "C"

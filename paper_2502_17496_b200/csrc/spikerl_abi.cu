@@ -1,0 +1,527 @@
+// spikerl_abi.cu — the extern "C" boundary (include/spikerl.h): argument validation (host-side,
+// before anything is enqueued), layouts, and the orchestration of the hot path
+//   actor forward  = K1 enc_fwd -> K2 lif_fwd x3 -> K3 dec_fwd
+//   actor backward = K4 dec_bwd_outscan -> K7 dW3 -> K5 dX3 -> K7 dW2 -> K5 dX2 -> K7 dW1 -> K6
+//   TD3 update     = K9 sample -> target actor -> target critics -> y -> critic fwd/bwd ->
+//                    C1 allreduce -> K10 Adam -> [actor fwd, dQ1/da, actor bwd, C1, K10, K11]
+//
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <atomic>
+#include "internal.h"
+
+namespace spk {
+
+static thread_local char g_err[1024] = "";
+static std::atomic<long long> g_launches{0};
+
+void set_error(const char* fmt, ...) {
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(g_err, sizeof(g_err), fmt, ap);
+  va_end(ap);
+}
+void note_launch(int n) { g_launches += n; }
+
+static int resolve_engine(const spikerl_actor_cfg* c, ActorDims* d) {
+  const bool bf = c->precision == SPIKERL_BF16;
+  switch (c->engine) {
+    case SPIKERL_ENGINE_SIMT: d->engine = SPIKERL_ENGINE_SIMT; return SPIKERL_OK;
+    case SPIKERL_ENGINE_TCGEN05:
+      if (!bf) { set_error("tcgen05 engine needs BF16 precision"); return SPIKERL_E_UNSUPPORTED; }
+      d->engine = SPIKERL_ENGINE_TCGEN05;
+      if (!tc_supported(*d)) { set_error("tcgen05 engine does not support this shape"); return SPIKERL_E_UNSUPPORTED; }
+      return SPIKERL_OK;
+    case SPIKERL_ENGINE_AUTO:
+      d->engine = SPIKERL_ENGINE_SIMT;
+      if (bf) {
+        d->engine = SPIKERL_ENGINE_TCGEN05;
+        if (!tc_supported(*d)) d->engine = SPIKERL_ENGINE_SIMT;
+      }
+      return SPIKERL_OK;
+    default: set_error("unknown engine %d", c->engine); return SPIKERL_E_ARG;
+  }
+}
+
+int actor_dims(const spikerl_actor_cfg* c, ActorDims* d) {
+  if (!c) { set_error("null actor cfg"); return SPIKERL_E_ARG; }
+  if (c->obs_dim < 1 || c->act_dim < 1 || c->pop_enc < 1 || c->pop_dec < 1 || c->hidden1 < 1 ||
+      c->hidden2 < 1) {
+    set_error("actor dims must be >= 1 (obs %d act %d pop %d/%d hidden %d/%d)", c->obs_dim, c->act_dim,
+              c->pop_enc, c->pop_dec, c->hidden1, c->hidden2);
+    return SPIKERL_E_DOMAIN;
+  }
+  if (c->T < 1 || c->T > 255) { set_error("T=%d outside [1,255]", c->T); return SPIKERL_E_DOMAIN; }
+  if (!(c->d_c >= 0.f && c->d_c <= 1.f) || !(c->d_v >= 0.f && c->d_v <= 1.f) || !(c->v_th > 0.f) ||
+      !(c->surr_window > 0.f) || !(c->sigma_floor >= 0.f)) {
+    set_error("LIF constants out of domain (d_c %g d_v %g v_th %g window %g)", c->d_c, c->d_v, c->v_th,
+              c->surr_window);
+    return SPIKERL_E_DOMAIN;
+  }
+  if (c->precision != SPIKERL_FP32 && c->precision != SPIKERL_BF16) {
+    set_error("unknown precision %d", c->precision);
+    return SPIKERL_E_ARG;
+  }
+  const long long k0 = (long long)c->obs_dim * c->pop_enc, n3 = (long long)c->act_dim * c->pop_dec;
+  if (k0 > (1 << 20) || n3 > (1 << 20) || c->hidden1 > (1 << 20) || c->hidden2 > (1 << 20)) {
+    set_error("actor too large");
+    return SPIKERL_E_UNSUPPORTED;
+  }
+  d->S = c->obs_dim; d->A = c->act_dim; d->E = c->pop_enc; d->D = c->pop_dec;
+  d->K0 = (int)k0; d->N1 = c->hidden1; d->N2 = c->hidden2; d->N3 = (int)n3; d->T = c->T;
+  d->N[0] = d->K0; d->N[1] = d->N1; d->N[2] = d->N2; d->N[3] = d->N3;
+  for (int l = 0; l < 4; ++l) { d->P[l] = round_up(d->N[l], kPad); d->Wd[l] = d->P[l] / 32; }
+  size_t o = 0;
+  const size_t sizes[SPIKERL_ACTOR_NPARAM] = {(size_t)d->K0, (size_t)d->K0, (size_t)d->N1 * d->K0,
+                                               (size_t)d->N2 * d->N1, (size_t)d->N3 * d->N2,
+                                               (size_t)d->A * d->D, (size_t)d->A};
+  for (int i = 0; i < SPIKERL_ACTOR_NPARAM; ++i) { d->off[i] = o; o += sizes[i]; }
+  d->off[SPIKERL_ACTOR_NPARAM] = o;
+  size_t bo = 0;
+  for (int l = 1; l <= 3; ++l) { d->boff[l - 1] = bo; bo += (size_t)d->P[l] * d->P[l - 1]; }
+  d->boff[3] = bo;
+  d->dc = c->d_c; d->dv = c->d_v; d->vth = c->v_th; d->win = c->surr_window; d->zh = c->surr_height;
+  d->sigma_floor = c->sigma_floor;
+  d->bf16 = c->precision == SPIKERL_BF16;
+  return resolve_engine(c, d);
+}
+
+unsigned long long actor_cfg_hash(const spikerl_actor_cfg* c) {
+  unsigned long long h = 1469598103934665603ULL;
+  const unsigned char* p = (const unsigned char*)c;
+  for (size_t i = 0; i < sizeof(*c); ++i) { h ^= p[i]; h *= 1099511628211ULL; }
+  return h;
+}
+
+TapeLayout tape_layout(const ActorDims& d, int B) {
+  TapeLayout L{};
+  size_t o = 0;
+  auto take = [&](size_t bytes) { size_t r = o; o += align_up(bytes, 256); return r; };
+  L.A = take(sizeof(float) * (size_t)B * d.K0);
+  for (int l = 0; l < 4; ++l) L.bits[l] = take(sizeof(uint32_t) * (size_t)d.T * B * d.Wd[l]);
+  L.mask[0] = 0;
+  for (int l = 1; l < 4; ++l) L.mask[l] = take(sizeof(uint32_t) * (size_t)d.T * B * d.Wd[l]);
+  L.counts = take((size_t)B * d.N3);
+  L.act = take(sizeof(float) * (size_t)B * d.A);
+  L.total = o;
+  return L;
+}
+
+int critic_dims(const spikerl_critic_cfg* c, CriticDims* d) {
+  if (!c) { set_error("null critic cfg"); return SPIKERL_E_ARG; }
+  if (c->in_dim < 1 || c->hidden1 < 1 || c->hidden2 < 1) {
+    set_error("critic dims must be >= 1");
+    return SPIKERL_E_DOMAIN;
+  }
+  if (c->precision != SPIKERL_FP32 && c->precision != SPIKERL_BF16) {
+    set_error("unknown precision %d", c->precision);
+    return SPIKERL_E_ARG;
+  }
+  d->in = c->in_dim; d->H1 = c->hidden1; d->H2 = c->hidden2; d->bf16 = c->precision == SPIKERL_BF16;
+  const size_t sizes[SPIKERL_CRITIC_NPARAM] = {(size_t)d->H1 * d->in, (size_t)d->H1,
+                                                (size_t)d->H2 * d->H1, (size_t)d->H2, (size_t)d->H2, 1};
+  size_t o = 0;
+  for (int i = 0; i < SPIKERL_CRITIC_NPARAM; ++i) { d->off[i] = o; o += sizes[i]; }
+  d->off[SPIKERL_CRITIC_NPARAM] = o;
+  return SPIKERL_OK;
+}
+
+// ------------------------------------------------------------------ actor workspace layout
+struct ActorWs {
+  size_t tape;      // inference-only spike planes (TapeLayout at offset 0)
+  size_t G[4];      // G1..G3 [T][B][P_l] (fp32 or bf16); G[0] unused
+  size_t Gsum;      // [B][P1]
+  size_t g_pre;     // [B][A] fp32
+  size_t enc_part;  // encoder partials
+  size_t total;
+};
+
+static ActorWs actor_ws_layout(const ActorDims& d, int B) {
+  ActorWs w{};
+  size_t o = 0;
+  auto take = [&](size_t bytes) { size_t r = o; o += align_up(bytes, 256); return r; };
+  const size_t gsz = d.bf16 ? 2 : 4;
+  w.tape = take(tape_layout(d, B).total);
+  w.G[0] = 0;
+  for (int l = 1; l <= 3; ++l) w.G[l] = take(gsz * (size_t)d.T * B * d.P[l]);
+  w.Gsum = take(gsz * (size_t)B * d.P[1]);
+  w.g_pre = take(sizeof(float) * (size_t)B * d.A);
+  w.enc_part = take(enc_grad_partial_bytes(d, B));
+  w.total = o;
+  return w;
+}
+
+static int actor_forward_impl(const ActorDims& d, int B, const float* params,
+                              const __nv_bfloat16* pb16, const float* obs, float* actions,
+                              char* tape, cudaStream_t st) {
+  const TapeLayout L = tape_layout(d, B);
+  float* A = (float*)(tape + L.A);
+  uint32_t* bits[4];
+  uint32_t* mask[4];
+  for (int l = 0; l < 4; ++l) { bits[l] = (uint32_t*)(tape + L.bits[l]); mask[l] = (uint32_t*)(tape + L.mask[l]); }
+  uint8_t* counts = (uint8_t*)(tape + L.counts);
+  SPK_TRY(launch_enc_fwd(d, B, obs, params + d.off[SPIKERL_ACTOR_MU], params + d.off[SPIKERL_ACTOR_SIGMA],
+                         A, bits[0], st));
+  for (int l = 1; l <= 3; ++l) {
+    const float* Wf = params + d.off[SPIKERL_ACTOR_W1 + l - 1];
+    const __nv_bfloat16* Wb = d.bf16 ? pb16 + d.boff[l - 1] : nullptr;
+    uint8_t* cnt = (l == 3) ? counts : nullptr;
+    if (d.engine == SPIKERL_ENGINE_TCGEN05)
+      SPK_TRY(launch_lif_fwd_tc(d, l, B, bits[l - 1], Wb, bits[l], mask[l], cnt, st));
+    else
+      SPK_TRY(launch_lif_fwd_simt(d, l, B, bits[l - 1], Wf, Wb, bits[l], mask[l], cnt, st));
+  }
+  SPK_TRY(launch_dec_fwd(d, B, counts, params + d.off[SPIKERL_ACTOR_WD], params + d.off[SPIKERL_ACTOR_BD],
+                         actions, (float*)(tape + L.act), st));
+  return SPIKERL_OK;
+}
+
+static int actor_backward_impl(const ActorDims& d, int B, const float* params,
+                               const __nv_bfloat16* pb16, const float* obs, const char* tape,
+                               const float* grad_a, float* grads, int accum, char* ws,
+                               cudaStream_t st) {
+  const TapeLayout L = tape_layout(d, B);
+  const ActorWs W = actor_ws_layout(d, B);
+  const uint32_t* bits[4];
+  const uint32_t* mask[4];
+  for (int l = 0; l < 4; ++l) {
+    bits[l] = (const uint32_t*)(tape + L.bits[l]);
+    mask[l] = (const uint32_t*)(tape + L.mask[l]);
+  }
+  const uint8_t* counts = (const uint8_t*)(tape + L.counts);
+  const float* act = (const float*)(tape + L.act);
+  void* G[4] = {nullptr, ws + W.G[1], ws + W.G[2], ws + W.G[3]};
+  void* Gsum = ws + W.Gsum;
+  float* g_pre = (float*)(ws + W.g_pre);
+  SPK_TRY(launch_dec_bwd_outscan(d, B, grad_a, act, counts, params + d.off[SPIKERL_ACTOR_WD], bits[3], mask[3],
+                                 G[3], g_pre, st));
+  SPK_TRY(launch_dec_param_grads(d, B, g_pre, counts, grads + d.off[SPIKERL_ACTOR_WD],
+                                 grads + d.off[SPIKERL_ACTOR_BD], accum, st));
+  for (int l = 3; l >= 1; --l) {
+    const float* Wf = params + d.off[SPIKERL_ACTOR_W1 + l - 1];
+    const __nv_bfloat16* Wb = d.bf16 ? pb16 + d.boff[l - 1] : nullptr;
+    SPK_TRY(launch_lif_dw_simt(d, l, B, G[l], bits[l - 1], grads + d.off[SPIKERL_ACTOR_W1 + l - 1], accum, st));
+    if (l >= 2)
+      SPK_TRY(launch_lif_dx_simt(d, l, B, G[l], Wf, Wb, bits[l - 1], mask[l - 1], G[l - 1],
+                                 l == 2 ? Gsum : nullptr, st));
+  }
+  SPK_TRY(launch_enc_grad_simt(d, B, Gsum, params + d.off[SPIKERL_ACTOR_W1], d.bf16 ? pb16 + d.boff[0] : nullptr,
+                               (const float*)(tape + L.A), obs, params + d.off[SPIKERL_ACTOR_MU],
+                               params + d.off[SPIKERL_ACTOR_SIGMA], (float*)(ws + W.enc_part),
+                               grads + d.off[SPIKERL_ACTOR_MU], grads + d.off[SPIKERL_ACTOR_SIGMA], accum, st));
+  return SPIKERL_OK;
+}
+
+// ------------------------------------------------------------------ TD3 workspace layout
+struct Td3Ws {
+  size_t s, a, r, s2, d, a2, at, api, qt, q, y, ga, lossa, tape, actor_ws, critic_ws, total;
+};
+
+static Td3Ws td3_ws_layout(const ActorDims& ad, const CriticDims& cd, int B) {
+  Td3Ws w{};
+  size_t o = 0;
+  auto take = [&](size_t bytes) { size_t r = o; o += align_up(bytes, 256); return r; };
+  const size_t f = sizeof(float);
+  w.s = take(f * B * ad.S); w.a = take(f * B * ad.A); w.r = take(f * B); w.s2 = take(f * B * ad.S);
+  w.d = take(f * B); w.a2 = take(f * B * ad.A); w.at = take(f * B * ad.A); w.api = take(f * B * ad.A);
+  w.qt = take(f * 2 * B); w.q = take(f * 2 * B); w.y = take(f * B); w.ga = take(f * B * ad.A);
+  w.lossa = take(f * 4);
+  w.tape = take(tape_layout(ad, B).total);
+  w.actor_ws = take(actor_ws_layout(ad, B).total);
+  w.critic_ws = take(critic_ws_bytes(cd, B));
+  w.total = o;
+  return w;
+}
+
+__global__ void neg_mean_kernel(int B, const float* __restrict__ q, float* __restrict__ out) {
+  __shared__ float red[256];
+  float s = 0.f;
+  for (int b = threadIdx.x; b < B; b += 256) s = __fadd_rn(s, q[b]);
+  red[threadIdx.x] = s;
+  __syncthreads();
+  for (int w = 128; w > 0; w >>= 1) {
+    if (threadIdx.x < w) red[threadIdx.x] = __fadd_rn(red[threadIdx.x], red[threadIdx.x + w]);
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) *out = -__fdiv_rn(red[0], (float)B);
+}
+
+}  // namespace spk
+
+using namespace spk;
+
+extern "C" {
+
+const char* spikerl_last_error(void) { return g_err; }
+const char* spikerl_version(void) { return "spikerl-b200 0.1 (sm_100a)"; }
+long long spikerl_launch_count(int reset) {
+  return reset ? g_launches.exchange(0) : g_launches.load();
+}
+
+int spikerl_actor_cfg_check(const spikerl_actor_cfg* cfg) {
+  ActorDims d;
+  return actor_dims(cfg, &d);
+}
+
+int spikerl_actor_param_offsets(const spikerl_actor_cfg* cfg, size_t* offsets) {
+  ActorDims d;
+  SPK_TRY(actor_dims(cfg, &d));
+  if (!offsets) { set_error("null offsets"); return SPIKERL_E_ARG; }
+  memcpy(offsets, d.off, sizeof(d.off));
+  return SPIKERL_OK;
+}
+
+size_t spikerl_actor_param_count(const spikerl_actor_cfg* cfg) {
+  ActorDims d;
+  return actor_dims(cfg, &d) == SPIKERL_OK ? d.off[SPIKERL_ACTOR_NPARAM] : 0;
+}
+
+int spikerl_critic_param_offsets(const spikerl_critic_cfg* cfg, size_t* offsets) {
+  CriticDims d;
+  SPK_TRY(critic_dims(cfg, &d));
+  if (!offsets) { set_error("null offsets"); return SPIKERL_E_ARG; }
+  memcpy(offsets, d.off, sizeof(d.off));
+  return SPIKERL_OK;
+}
+
+size_t spikerl_critic_param_count(const spikerl_critic_cfg* cfg) {
+  CriticDims d;
+  return critic_dims(cfg, &d) == SPIKERL_OK ? d.off[SPIKERL_CRITIC_NPARAM] : 0;
+}
+
+size_t spikerl_actor_bf16_bytes(const spikerl_actor_cfg* cfg) {
+  ActorDims d;
+  return actor_dims(cfg, &d) == SPIKERL_OK ? d.boff[3] * sizeof(__nv_bfloat16) : 0;
+}
+
+size_t spikerl_critic_bf16_bytes(const spikerl_critic_cfg* cfg) {
+  CriticDims d;
+  return critic_dims(cfg, &d) == SPIKERL_OK ? align_up(d.off[SPIKERL_CRITIC_NPARAM] * 2, 16) : 0;
+}
+
+size_t spikerl_actor_tape_bytes(const spikerl_actor_cfg* cfg, int batch) {
+  ActorDims d;
+  if (actor_dims(cfg, &d) != SPIKERL_OK || batch < 1) return 0;
+  return tape_layout(d, batch).total;
+}
+
+size_t spikerl_actor_workspace_bytes(const spikerl_actor_cfg* cfg, int batch) {
+  ActorDims d;
+  if (actor_dims(cfg, &d) != SPIKERL_OK || batch < 1) return 0;
+  return actor_ws_layout(d, batch).total;
+}
+
+size_t spikerl_critic_workspace_bytes(const spikerl_critic_cfg* cfg, int batch) {
+  CriticDims d;
+  if (critic_dims(cfg, &d) != SPIKERL_OK || batch < 1) return 0;
+  return critic_ws_bytes(d, batch);
+}
+
+size_t spikerl_td3_workspace_bytes(const spikerl_actor_cfg* acfg, const spikerl_critic_cfg* ccfg, int batch) {
+  ActorDims ad;
+  CriticDims cd;
+  if (actor_dims(acfg, &ad) != SPIKERL_OK || critic_dims(ccfg, &cd) != SPIKERL_OK || batch < 1) return 0;
+  return td3_ws_layout(ad, cd, batch).total;
+}
+
+int spikerl_actor_tape_layout(const spikerl_actor_cfg* cfg, int batch, spikerl_tape_layout* out) {
+  ActorDims d;
+  SPK_TRY(actor_dims(cfg, &d));
+  if (!out || batch < 1) { set_error("bad tape layout arguments"); return SPIKERL_E_ARG; }
+  const TapeLayout L = tape_layout(d, batch);
+  out->A = L.A;
+  for (int l = 0; l < 4; ++l) { out->bits[l] = L.bits[l]; out->mask[l] = L.mask[l]; out->padded[l] = d.P[l]; }
+  out->counts = L.counts; out->act = L.act; out->total = L.total;
+  return SPIKERL_OK;
+}
+
+int spikerl_actor_refresh_bf16(const spikerl_actor_cfg* cfg, const float* params, void* params_bf16,
+                               spikerl_stream_t stream) {
+  ActorDims d;
+  SPK_TRY(actor_dims(cfg, &d));
+  if (!params || !params_bf16) { set_error("null params"); return SPIKERL_E_ARG; }
+  return launch_actor_refresh_bf16(d, params, (__nv_bfloat16*)params_bf16, (cudaStream_t)stream);
+}
+
+int spikerl_critic_refresh_bf16(const spikerl_critic_cfg* cfg, int n_critics, const float* params,
+                                void* params_bf16, spikerl_stream_t stream) {
+  CriticDims d;
+  SPK_TRY(critic_dims(cfg, &d));
+  if (!params || !params_bf16 || n_critics < 1) { set_error("bad refresh arguments"); return SPIKERL_E_ARG; }
+  return launch_f32_to_bf16(params, (__nv_bfloat16*)params_bf16, d.off[SPIKERL_CRITIC_NPARAM] * n_critics,
+                            (cudaStream_t)stream);
+}
+
+static const unsigned long long kTapeMagic = 0x5350494b45524c31ULL;  // "SPIKERL1"
+
+int spikerl_actor_forward(const spikerl_actor_cfg* cfg, int batch, const float* params,
+                          const void* params_bf16, const float* obs, float* actions, spikerl_tape* tape,
+                          void* workspace, spikerl_stream_t stream) {
+  ActorDims d;
+  SPK_TRY(actor_dims(cfg, &d));
+  if (batch < 1 || !params || !obs || !actions || (d.bf16 && !params_bf16)) {
+    set_error("spikerl_actor_forward: bad arguments (batch %d)", batch);
+    return SPIKERL_E_ARG;
+  }
+  const TapeLayout L = tape_layout(d, batch);
+  char* tp;
+  if (tape) {
+    if (!tape->dev || tape->bytes < L.total) {
+      set_error("tape buffer too small (%zu < %zu)", tape->bytes, L.total);
+      return SPIKERL_E_ARG;
+    }
+    tp = (char*)tape->dev;
+  } else {
+    if (!workspace) { set_error("inference-only forward needs a workspace"); return SPIKERL_E_ARG; }
+    tp = (char*)workspace + actor_ws_layout(d, batch).tape;
+  }
+  SPK_TRY(actor_forward_impl(d, batch, params, (const __nv_bfloat16*)params_bf16, obs, actions, tp,
+                             (cudaStream_t)stream));
+  if (tape) {
+    tape->magic = kTapeMagic;
+    tape->cfg_hash = actor_cfg_hash(cfg);
+    tape->batch = batch;
+  }
+  return SPIKERL_OK;
+}
+
+int spikerl_actor_backward(const spikerl_actor_cfg* cfg, int batch, const float* params,
+                           const void* params_bf16, const float* obs, const spikerl_tape* tape,
+                           const float* grad_actions, float* grad_params, int accumulate, void* workspace,
+                           spikerl_stream_t stream) {
+  ActorDims d;
+  SPK_TRY(actor_dims(cfg, &d));
+  if (batch < 1 || !params || !obs || !tape || !grad_actions || !grad_params || !workspace ||
+      (d.bf16 && !params_bf16)) {
+    set_error("spikerl_actor_backward: bad arguments");
+    return SPIKERL_E_ARG;
+  }
+  if (tape->magic != kTapeMagic || tape->cfg_hash != actor_cfg_hash(cfg) || tape->batch != batch || !tape->dev) {
+    set_error("tape does not belong to this (cfg, batch)");
+    return SPIKERL_E_STATE;
+  }
+  return actor_backward_impl(d, batch, params, (const __nv_bfloat16*)params_bf16, obs, (const char*)tape->dev,
+                             grad_actions, grad_params, accumulate ? 1 : 0, (char*)workspace,
+                             (cudaStream_t)stream);
+}
+
+int spikerl_critic_fwd_bwd(const spikerl_critic_cfg* cfg, int batch, const float* params2,
+                           const void* params2_bf16, const float* obs, int obs_dim, const float* act, int act_dim,
+                           const float* target_y, float* q, float* loss, float* grad_params2, float* grad_act,
+                           float act_grad_scale, void* workspace, spikerl_stream_t stream) {
+  CriticDims c;
+  SPK_TRY(critic_dims(cfg, &c));
+  if (batch < 1 || !params2 || !obs || !act || !q || !workspace || obs_dim < 0 || act_dim < 1 ||
+      obs_dim + act_dim != c.in || (c.bf16 && !params2_bf16)) {
+    set_error("spikerl_critic_fwd_bwd: bad arguments");
+    return SPIKERL_E_ARG;
+  }
+  return critic_fwd_bwd(c, batch, params2, (const __nv_bfloat16*)params2_bf16, obs, obs_dim, act, act_dim, target_y,
+                        q, loss, grad_params2, grad_act, act_grad_scale, 2, workspace, (cudaStream_t)stream);
+}
+
+int spikerl_adam(float* params, const float* grads, float* m, float* v, size_t n, long long* step_counter,
+                 float lr, float beta1, float beta2, float eps, size_t clamp_lo, size_t clamp_hi, float clamp_min,
+                 spikerl_stream_t stream) {
+  if (!params || !grads || !m || !v || !step_counter || n == 0) {
+    set_error("spikerl_adam: bad arguments");
+    return SPIKERL_E_ARG;
+  }
+  return launch_adam(params, grads, m, v, n, step_counter, lr, beta1, beta2, eps, clamp_lo, clamp_hi, clamp_min,
+                     (unsigned int*)(step_counter + 1), (cudaStream_t)stream);
+}
+
+int spikerl_polyak(float* target, const float* source, size_t n, float tau, spikerl_stream_t stream) {
+  if (!target || !source || n == 0) { set_error("spikerl_polyak: bad arguments"); return SPIKERL_E_ARG; }
+  return launch_polyak(target, source, n, tau, (cudaStream_t)stream);
+}
+
+int spikerl_td3_update(const spikerl_actor_cfg* acfg, const spikerl_critic_cfg* ccfg, const spikerl_td3_cfg* hp,
+                       const spikerl_td3_bufs* b, long long step, unsigned long long seed, const long long* indices,
+                       const float* noise, spikerl_comm* comm, float* losses, void* workspace,
+                       spikerl_stream_t stream) {
+  ActorDims ad;
+  CriticDims cd;
+  SPK_TRY(actor_dims(acfg, &ad));
+  SPK_TRY(critic_dims(ccfg, &cd));
+  if (!hp || !b || !workspace || !losses || step < 1) {
+    set_error("spikerl_td3_update: bad arguments");
+    return SPIKERL_E_ARG;
+  }
+  const int B = hp->batch;
+  if (B < 1 || cd.in != ad.S + ad.A || hp->policy_delay < 1 || cd.bf16 != ad.bf16) {
+    set_error("spikerl_td3_update: inconsistent configs (batch %d, critic in %d vs S+A %d)", B, cd.in, ad.S + ad.A);
+    return SPIKERL_E_ARG;
+  }
+  if (!b->actor || !b->actor_t || !b->critic || !b->critic_t || !b->m_actor || !b->v_actor || !b->m_critic ||
+      !b->v_critic || !b->grad_actor || !b->grad_critic || !b->adam_steps || !b->rng_counter || !b->rs ||
+      !b->ra || !b->rr || !b->rs2 || !b->rd ||
+      (ad.bf16 && (!b->actor_bf16 || !b->actor_t_bf16 || !b->critic_bf16 || !b->critic_t_bf16))) {
+    set_error("spikerl_td3_update: null buffer");
+    return SPIKERL_E_ARG;
+  }
+  if (b->replay_size < B) {
+    set_error("replay holds %lld < batch %d transitions", b->replay_size, B);
+    return SPIKERL_E_NOTREADY;
+  }
+  cudaStream_t st = (cudaStream_t)stream;
+  const Td3Ws W = td3_ws_layout(ad, cd, B);
+  char* ws = (char*)workspace;
+  float* s = (float*)(ws + W.s); float* a = (float*)(ws + W.a); float* r = (float*)(ws + W.r);
+  float* s2 = (float*)(ws + W.s2); float* dn = (float*)(ws + W.d); float* a2 = (float*)(ws + W.a2);
+  float* at = (float*)(ws + W.at); float* api = (float*)(ws + W.api); float* qt = (float*)(ws + W.qt);
+  float* q = (float*)(ws + W.q); float* y = (float*)(ws + W.y); float* ga = (float*)(ws + W.ga);
+  char* tape = ws + W.tape;
+  char* aws = ws + W.actor_ws;
+  void* cws = ws + W.critic_ws;
+  const int rank = spikerl_comm_rank(comm);
+  const size_t Pa = ad.off[SPIKERL_ACTOR_NPARAM];
+  const size_t Pc = cd.off[SPIKERL_CRITIC_NPARAM];
+  const __nv_bfloat16* abf = (const __nv_bfloat16*)b->actor_bf16;
+  const __nv_bfloat16* atbf = (const __nv_bfloat16*)b->actor_t_bf16;
+  const __nv_bfloat16* cbf = (const __nv_bfloat16*)b->critic_bf16;
+  const __nv_bfloat16* ctbf = (const __nv_bfloat16*)b->critic_t_bf16;
+
+  // K9: sample (s, a, r, s', d)
+  SPK_TRY(launch_replay_gather(B, ad.S, ad.A, b->rs, b->ra, b->rr, b->rs2, b->rd, b->replay_size, indices, seed,
+                               rank, b->rng_counter, s, a, r, s2, dn, st));
+  // 1. target policy smoothing: a~ = clip(pi'(s') + clip(eps), -1, 1)
+  SPK_TRY(actor_forward_impl(ad, B, b->actor_t, atbf, s2, a2, aws + actor_ws_layout(ad, B).tape, st));
+  SPK_TRY(launch_target_action(B, ad.A, a2, noise, hp->policy_noise, hp->noise_clip, seed, rank, b->rng_counter, at,
+                               st));
+  // 2. y = r + gamma (1 - d) min(Q1', Q2')(s', a~)
+  SPK_TRY(critic_fwd_bwd(cd, B, b->critic_t, ctbf, s2, ad.S, at, ad.A, nullptr, qt, nullptr, nullptr, nullptr, 0.f,
+                         2, cws, st));
+  SPK_TRY(launch_td_target(B, r, dn, qt, hp->gamma, y, st));
+  // 3. critic loss, grads, allreduce, Adam
+  SPK_TRY(critic_fwd_bwd(cd, B, b->critic, cbf, s, ad.S, a, ad.A, y, q, losses, b->grad_critic, nullptr, 0.f, 2,
+                         cws, st));
+  SPK_TRY(spikerl_allreduce_grads(comm, b->grad_critic, 2 * Pc, stream));
+  SPK_TRY(launch_adam(b->critic, b->grad_critic, b->m_critic, b->v_critic, 2 * Pc, b->adam_steps, hp->lr_critic,
+                      hp->beta1, hp->beta2, hp->eps, 0, 0, 0.f, (unsigned int*)(b->adam_steps + 1), st));
+  if (ad.bf16) SPK_TRY(launch_f32_to_bf16(b->critic, (__nv_bfloat16*)b->critic_bf16, 2 * Pc, st));
+  // 4. delayed actor update + targets
+  if (step % hp->policy_delay == 0) {
+    SPK_TRY(actor_forward_impl(ad, B, b->actor, abf, s, api, tape, st));
+    SPK_TRY(critic_fwd_bwd(cd, B, b->critic, cbf, s, ad.S, api, ad.A, nullptr, q, nullptr, nullptr, ga,
+                           -1.0f / (float)B, 1, cws, st));
+    neg_mean_kernel<<<1, 256, 0, st>>>(B, q, losses + 1);
+    SPK_LAUNCHED();
+    SPK_TRY(actor_backward_impl(ad, B, b->actor, abf, s, tape, ga, b->grad_actor, 0, aws, st));
+    SPK_TRY(spikerl_allreduce_grads(comm, b->grad_actor, Pa, stream));
+    SPK_TRY(launch_adam(b->actor, b->grad_actor, b->m_actor, b->v_actor, Pa, b->adam_steps + 2, hp->lr_actor,
+                        hp->beta1, hp->beta2, hp->eps, ad.off[SPIKERL_ACTOR_SIGMA], ad.off[SPIKERL_ACTOR_W1],
+                        ad.sigma_floor, (unsigned int*)(b->adam_steps + 3), st));
+    SPK_TRY(launch_polyak(b->actor_t, b->actor, Pa, hp->tau, st));
+    SPK_TRY(launch_polyak(b->critic_t, b->critic, 2 * Pc, hp->tau, st));
+    if (ad.bf16) {
+      SPK_TRY(launch_actor_refresh_bf16(ad, b->actor, (__nv_bfloat16*)b->actor_bf16, st));
+      SPK_TRY(launch_actor_refresh_bf16(ad, b->actor_t, (__nv_bfloat16*)b->actor_t_bf16, st));
+      SPK_TRY(launch_f32_to_bf16(b->critic_t, (__nv_bfloat16*)b->critic_t_bf16, 2 * Pc, st));
+    }
+  }
+  return SPIKERL_OK;
+}
+
+}  // extern "C"

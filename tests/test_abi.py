@@ -1,0 +1,108 @@
+"""C-ABI boundary checks that need no GPU: the library loads, exports every symbol
+include/spikerl.h declares, and the host-side validation / size / layout calls behave."""
+import ctypes as C
+import os
+import re
+
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+@pytest.fixture(scope="module")
+def L():
+    from paper_2502_17496_b200 import _lib
+    if not os.path.exists(_lib.LIB_PATH):
+        import __graft_entry__
+        __graft_entry__.build()
+    return _lib
+
+
+def header_functions():
+    src = open(os.path.join(ROOT, "include", "spikerl.h")).read()
+    src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
+    return sorted(set(re.findall(r"\b(spikerl_[a-z0-9_]+)\s*\(", src)))
+
+
+def test_exports_every_header_symbol(L):
+    lib = L.lib()
+    names = header_functions()
+    assert len(names) >= 25
+    for n in names:
+        assert hasattr(lib, n), n
+    assert set(names) == set(L.EXPORTS)
+
+
+def test_version_and_launch_counter(L):
+    assert b"sm_100a" in L.lib().spikerl_version()
+    L.lib().spikerl_launch_count(1)
+    assert L.lib().spikerl_launch_count(0) == 0
+
+
+def cfg(**kw):
+    from paper_2502_17496_b200 import actor_cfg
+    base = dict(obs_dim=17, act_dim=6, precision="fp32")
+    base.update(kw)
+    return actor_cfg(**base)
+
+
+def test_param_offsets_layout(L):
+    from paper_2502_17496_b200 import actor_offsets, critic_offsets, critic_cfg
+    off = actor_offsets(cfg())
+    S, E, N1, N2, A, D = 17, 10, 256, 256, 6, 10
+    sizes = [S * E, S * E, N1 * S * E, N2 * N1, A * D * N2, A * D, A]
+    assert off == [0] + list(__import__("itertools").accumulate(sizes))
+    assert L.lib().spikerl_actor_param_count(C.byref(cfg())) == off[-1] == 124_822
+    coff = critic_offsets(critic_cfg(23))
+    assert coff[-1] == 23 * 256 + 256 + 256 * 256 + 256 + 256 + 1
+
+
+@pytest.mark.parametrize("field,value,status", [
+    ("T", 0, 2), ("T", 256, 2), ("d_c", 1.5, 2), ("d_v", -0.1, 2), ("v_th", 0.0, 2),
+    ("surr_window", 0.0, 2), ("obs_dim", 0, 2), ("pop_enc", 0, 2), ("precision", 7, 1), ("engine", 9, 1)])
+def test_cfg_validation(L, field, value, status):
+    c = cfg()
+    setattr(c, field, value)
+    assert L.lib().spikerl_actor_cfg_check(C.byref(c)) == status
+    assert len(L.last_error()) > 0
+    assert L.lib().spikerl_actor_param_count(C.byref(c)) == 0
+
+
+def test_tcgen05_needs_bf16(L):
+    c = cfg(engine="tcgen05")
+    assert L.lib().spikerl_actor_cfg_check(C.byref(c)) == L.E_UNSUPPORTED
+
+
+def test_tape_layout_sizes(L):
+    c = cfg(precision="bf16")
+    lay = L.TapeLayout()
+    B = 256
+    assert L.lib().spikerl_actor_tape_layout(C.byref(c), B, C.byref(lay)) == 0
+    assert list(lay.padded) == [256, 256, 256, 128]
+    assert lay.total == L.lib().spikerl_actor_tape_bytes(C.byref(c), B)
+    offs = [lay.A, *lay.bits, *lay.mask[1:], lay.counts, lay.act]
+    assert all(o % 256 == 0 for o in offs) and sorted(offs) == offs
+    assert lay.bits[1] - lay.bits[0] >= 5 * B * 8 * 4
+    assert L.lib().spikerl_actor_tape_bytes(C.byref(c), 0) == 0
+
+
+def test_sync_errors_enqueue_nothing(L):
+    """Argument errors are reported on the host before any device work (no GPU needed)."""
+    lib = L.lib()
+    c = cfg()
+    assert lib.spikerl_actor_forward(C.byref(c), 0, None, None, None, None, None, None, None) == L.E_ARG
+    t = L.Tape(0, 0, 0, None, 0)
+    assert lib.spikerl_actor_backward(C.byref(c), 4, C.c_void_p(16), None, C.c_void_p(16), C.byref(t),
+                                      C.c_void_p(16), C.c_void_p(16), 0, C.c_void_p(16), None) == L.E_STATE
+    assert lib.spikerl_adam(None, None, None, None, 0, None, 1e-3, 0.9, 0.999, 1e-8, 0, 0, 0.0, None) == L.E_ARG
+    assert lib.spikerl_allreduce_grads(None, None, 10, None) == 0      # no comm: identity
+    from paper_2502_17496_b200 import critic_cfg, td3_cfg
+    cc = critic_cfg(23, precision="fp32")
+    bufs = L.TD3Bufs()
+    for f, _ in L.TD3Bufs._fields_[:-1]:
+        setattr(bufs, f, 256)
+    bufs.replay_size = 10
+    hp = td3_cfg(256)
+    st = lib.spikerl_td3_update(C.byref(c), C.byref(cc), C.byref(hp), C.byref(bufs), 1, 0, None, None, None,
+                                C.c_void_p(256), C.c_void_p(256), None)
+    assert st == L.E_NOTREADY, L.last_error()

@@ -1,0 +1,319 @@
+"""GPU parity: the CUDA path (through the C ABI) against the oracle on identical seeded inputs.
+Tolerances (north_star): encoder spikes bit-exact; fp32 actions
+1e-4 relative, spike disagreement <= 1e-5 of spikes and only within 1e-5 of V_th; bf16 actions
+2e-2 absolute, gradients 1e-2 relative L2 (fp32 mode: 1e-4)."""
+import numpy as np
+import pytest
+
+import oracle
+import synthgen as sg
+from tests._parity import run_gpu_actor, check_actor, rel_l2
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _cuda():
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    torch.cuda.set_device(0)
+
+
+def _inputs(shape, B, seed=0):
+    rng = np.random.default_rng(seed)
+    p = sg.actor_params(shape, rng)
+    s = sg.observations(rng, B, shape.obs_dim)
+    g = sg.action_grads(rng, B, shape.act_dim)
+    return p, s, g
+
+
+# ------------------------------------------------------------------ encoder (bit-exact, every config shape)
+@pytest.mark.parametrize("name,B", [("cfg0", 100), ("cfg1", 256), ("cfg2", 512), ("cfg3s", 100), ("cfg3L", 1024),
+                                    ("cfg4", 256)])
+def test_encoder_bit_exact(name, B):
+    shape, _, _ = sg.preset(name)
+    p, s, _ = _inputs(shape, B, seed=1)
+    gpu = run_gpu_actor(shape, B, p, s, None, engine="simt")
+    from tests._parity import check_encoder
+    assert check_encoder(gpu, shape, p, s) == 0
+
+
+def test_encoder_edge_values():
+    """s exactly on mu (A = 1 -> fires every step), far tails (A underflows / subnormal)."""
+    shape = sg.ActorShape(1, 1, pop_enc=10, pop_dec=2, n1=32, n2=32, T=5, precision="fp32")
+    rng = np.random.default_rng(0)
+    p = sg.actor_params(shape, rng)
+    s = np.array([[-3.0], [-1.0], [1.0], [0.3333333432674408], [5.0], [-5.0], [0.1], [0.2], [-0.5], [2.9],
+                  [1e-30], [4.99]], np.float32)
+    gpu = run_gpu_actor(shape, len(s), p, s, None, engine="simt")
+    from tests._parity import check_encoder
+    assert check_encoder(gpu, shape, p, s) == 0
+
+
+# ------------------------------------------------------------------ fp32 actor (configs[0])
+def test_actor_fp32_cfg0():
+    shape, _, B = sg.preset("cfg0")
+    p, s, g = _inputs(shape, B)
+    gpu = run_gpu_actor(shape, B, p, s, g)
+    st = check_actor(gpu, shape, p, s, g)
+    assert st["free_flips"] == [0, 0, 0], st
+
+
+@pytest.mark.parametrize("B", [1, 7, 33, 129])
+def test_actor_fp32_ragged_batches(B):
+    shape, _, _ = sg.preset("cfg0")
+    p, s, g = _inputs(shape, B, seed=B)
+    check_actor(run_gpu_actor(shape, B, p, s, g), shape, p, s, g)
+
+
+@pytest.mark.parametrize("T", [1, 2, 16, 31])
+def test_actor_fp32_timesteps(T):
+    shape = sg.with_(sg.preset("cfg0")[0], T=T)
+    p, s, g = _inputs(shape, 64, seed=T)
+    check_actor(run_gpu_actor(shape, 64, p, s, g), shape, p, s, g)
+
+
+def test_actor_fp32_odd_widths():
+    # widths that are not multiples of 32/128: padding must not change results (R28)
+    shape = sg.ActorShape(5, 3, pop_enc=7, pop_dec=9, n1=45, n2=161, T=5, precision="fp32")
+    p, s, g = _inputs(shape, 50, seed=3)
+    check_actor(run_gpu_actor(shape, 50, p, s, g), shape, p, s, g)
+
+
+def test_zero_decoder_and_zero_network():
+    shape, _, _ = sg.preset("cfg0")
+    p, s, g = _inputs(shape, 32)
+    p["Wd"] = np.zeros_like(p["Wd"]); p["bd"] = np.linspace(-0.5, 0.5, shape.act_dim).astype(np.float32)
+    gpu = run_gpu_actor(shape, 32, p, s, g)
+    assert np.allclose(gpu["a"], np.tanh(p["bd"].astype(np.float64))[None], atol=1e-6)
+    for k in ("mu", "sigma", "W1", "W2", "W3"):
+        assert np.all(gpu["grads"][k] == 0), k
+    check_actor(gpu, shape, p, s, g)
+    for k in ("W1", "W2", "W3", "Wd", "bd"):
+        p[k] = np.zeros_like(p[k])
+    gpu = run_gpu_actor(shape, 32, p, s, np.zeros_like(g))
+    assert np.all(gpu["a"] == 0) and all(np.all(v == 0) for v in gpu["grads"].values())
+
+
+# ------------------------------------------------------------------ bf16 actor (configs[1..4] shapes)
+@pytest.mark.parametrize("name,B,engine", [("cfg1", 256, "auto"), ("cfg2", 512, "auto"), ("cfg3s", 100, "auto"),
+                                           ("cfg3L", 1024, "auto"), ("cfg1", 256, "simt"), ("cfg3L", 300, "simt")])
+def test_actor_bf16(name, B, engine):
+    shape, _, _ = sg.preset(name)
+    p, s, g = _inputs(shape, B, seed=2)
+    st = check_actor(run_gpu_actor(shape, B, p, s, g, engine=engine), shape, p, s, g)
+    print(name, B, engine, st)
+
+
+def test_actor_bf16_cfg4_shape_subsample():
+    """configs[4] widths (1024-1024, T=16) on a 64-row sample (teacher forced)."""
+    shape, _, _ = sg.preset("cfg4")
+    p, s, g = _inputs(shape, 64, seed=4)
+    st = check_actor(run_gpu_actor(shape, 64, p, s, g), shape, p, s, g)
+    print(st)
+
+
+def test_backward_rejects_foreign_tape():
+    import torch
+    import paper_2502_17496_b200 as pk
+    shape, _, _ = sg.preset("cfg0")
+    p, s, g = _inputs(shape, 8)
+    a1 = pk.SpikingActor(pk.actor_cfg_from(shape), 8)
+    a1.load(p)
+    obs = torch.from_numpy(s).cuda()
+    with pytest.raises(pk.SpikeRLError) as e:
+        a1.backward(obs, torch.from_numpy(g).cuda())       # no forward yet -> tape not stamped
+    assert e.value.status == 3
+    a1.forward(obs)
+    a2 = pk.SpikingActor(pk.actor_cfg_from(sg.with_(shape, T=4)), 8)
+    a2.load(p)
+    a2.tape = a1.tape
+    with pytest.raises(pk.SpikeRLError):
+        a2.backward(obs, torch.from_numpy(g).cuda())
+
+
+def test_forward_deterministic_and_accumulate():
+    import torch
+    import paper_2502_17496_b200 as pk
+    shape, _, _ = sg.preset("cfg1")
+    p, s, g = _inputs(shape, 64)
+    act = pk.SpikingActor(pk.actor_cfg_from(shape), 64)
+    act.load(p)
+    obs = torch.from_numpy(s).cuda(); ga = torch.from_numpy(g).cuda()
+    a1 = act.forward(obs).clone(); g1 = act.backward(obs, ga).clone()
+    a2 = act.forward(obs).clone(); g2 = act.backward(obs, ga).clone()
+    assert torch.equal(a1, a2) and torch.equal(g1, g2)           # bitwise run-to-run
+    g3 = act.backward(obs, ga, accumulate=True).clone()
+    assert torch.allclose(g3, 2 * g1, rtol=1e-6, atol=0)
+
+
+# ------------------------------------------------------------------ critic
+@pytest.mark.parametrize("prec,B", [("fp32", 100), ("bf16", 256), ("bf16", 4096)])
+def test_critic_parity(prec, B):
+    import torch
+    import paper_2502_17496_b200 as pk
+    rng = np.random.default_rng(5)
+    cs = sg.CriticShape(23, precision=prec)
+    c1, c2 = sg.critic_params(cs, rng), sg.critic_params(cs, rng)
+    for c in (c1, c2):
+        for k in ("b1", "b2", "b3"):
+            c[k] = rng.uniform(-0.2, 0.2, c[k].shape).astype(np.float32)
+    batch = sg.replay_batch(rng, B, 17, 6)
+    y = rng.standard_normal(B).astype(np.float32)
+    tc = pk.TwinCritic(pk.critic_cfg(23, precision=prec), B)
+    tc.load(c1, c2)
+    obs = torch.from_numpy(batch["s"]).cuda(); act = torch.from_numpy(batch["a"]).cuda()
+    yt = torch.from_numpy(y).cuda()
+    ga = torch.zeros(B, 6, device="cuda")
+    q = tc(obs, act, yt).cpu().numpy()
+    grads = tc.grads.cpu().numpy()
+    loss = float(tc.loss.cpu())
+    tc(obs, act, None, grad_act=ga, act_grad_scale=-1.0 / B)
+    ga = ga.cpu().numpy()
+    x = np.concatenate([batch["s"], batch["a"]], 1).astype(np.float64)
+    tol_q = 1e-4 if prec == "fp32" else 2e-2
+    gt = 1e-4 if prec == "fp32" else 1e-2
+    lref = 0.0
+    P = tc.P
+    for i, cp in enumerate((c1, c2)):
+        qr, cache = oracle.critic_forward(cp, x, prec)
+        assert np.allclose(q[i], qr, rtol=tol_q, atol=tol_q), (i, np.abs(q[i] - qr).max())
+        lref += np.mean((qr - y) ** 2)
+        gr, _ = oracle.critic_backward(cp, cache, 2 * (qr - y) / B, prec)
+        mine = pk.unpack_critic(tc.cfg, grads[i * P:(i + 1) * P])
+        for k in gr:
+            assert rel_l2(mine[k].reshape(gr[k].shape), gr[k]) <= gt, (i, k)
+        if i == 0:
+            _, dx = oracle.critic_backward(cp, cache, np.full(B, -1.0 / B), prec, need_param_grads=False)
+            assert rel_l2(ga, dx[:, 17:]) <= gt
+    assert abs(loss - lref) <= gt * abs(lref)
+
+
+# ------------------------------------------------------------------ Adam / Polyak
+def test_adam_and_polyak():
+    import torch
+    import paper_2502_17496_b200 as pk
+    rng = np.random.default_rng(6)
+    n = 10007
+    p = rng.standard_normal(n).astype(np.float32)
+    p[:10] = 0.0005
+    pt = torch.from_numpy(p).cuda()
+    m = torch.zeros(n, device="cuda"); v = torch.zeros(n, device="cuda")
+    cnt = torch.zeros(2, dtype=torch.int64, device="cuda")
+    pr, mr, vr = p.astype(np.float64), np.zeros(n), np.zeros(n)
+    for t in range(1, 4):
+        g = rng.standard_normal(n).astype(np.float32)
+        pk.adam(pt, torch.from_numpy(g).cuda(), m, v, cnt, 1e-3, clamp=(0, 10, 1e-3))
+        pr, mr, vr = oracle.adam_update(pr, g, mr, vr, t, 1e-3)
+        pr[:10] = np.maximum(pr[:10], 1e-3)
+    assert int(cnt[0]) == 3 and int(cnt[1]) == 0
+    assert np.allclose(pt.cpu().numpy(), pr, rtol=0, atol=1e-6)
+    assert np.allclose(m.cpu().numpy(), mr, rtol=1e-5, atol=1e-7)
+    assert np.all(pt.cpu().numpy()[:10] >= 1e-3)
+    src = torch.from_numpy(rng.standard_normal(n).astype(np.float32)).cuda()
+    tgt = torch.from_numpy(rng.standard_normal(n).astype(np.float32)).cuda()
+    ref = oracle.polyak(tgt.cpu().numpy(), src.cpu().numpy(), 0.005)
+    pk.polyak(tgt, src, 0.005)
+    assert np.allclose(tgt.cpu().numpy(), ref, rtol=0, atol=1e-6)
+    pk.polyak(tgt, src, 1.0)
+    assert torch.equal(tgt, src)
+
+
+# ------------------------------------------------------------------ TD3 update (2 steps, injected randomness)
+@pytest.mark.parametrize("prec", ["fp32", "bf16"])
+def test_td3_two_steps(prec):
+    import torch
+    import paper_2502_17496_b200 as pk
+    rng = np.random.default_rng(7)
+    shape = sg.with_(sg.preset("cfg1")[0], precision=prec)
+    cs = sg.CriticShape(23, precision=prec)
+    hp = sg.TD3Hyper()
+    B = 256
+    actor = sg.actor_params(shape, rng)
+    c1, c2 = sg.critic_params(cs, rng), sg.critic_params(cs, rng)
+    N = 4096
+    rb = sg.replay_batch(rng, N, 17, 6)
+    replay = pk.replay_from_host(rb)
+    td3 = pk.TD3(pk.actor_cfg_from(shape), pk.critic_cfg(23, precision=prec), pk.td3_cfg(B), replay, seed=1)
+    td3.load(actor, c1, c2)
+    st = oracle.init_state(actor, c1, c2)
+    tol = 1e-4 if prec == "fp32" else 1e-2
+    for k in (1, 2):
+        idx = rng.integers(0, N, B)
+        eps = sg.target_noise(rng, B, 6)
+        td3.update(k, torch.from_numpy(idx).cuda(), torch.from_numpy(eps).cuda())
+        torch.cuda.synchronize()
+        batch = {key: rb[key][idx] for key in rb}
+        st, info = oracle.td3_update(st, shape, cs, hp, batch, eps, k)
+        losses = td3.losses.cpu().numpy()
+        assert abs(losses[0] - info["critic_loss"]) <= tol * abs(info["critic_loss"]), (k, losses, info["critic_loss"])
+        P = td3.Pc
+        crit = td3.critic.cpu().numpy()
+        for i in range(2):
+            mine = pk.unpack_critic(td3.ccfg, crit[i * P:(i + 1) * P])
+            for key in mine:
+                d_ref = st["c"][i][key] - (c1 if i == 0 else c2)[key].astype(np.float64).reshape(st["c"][i][key].shape)
+                d_me = mine[key].reshape(d_ref.shape) - (c1 if i == 0 else c2)[key].astype(np.float64).reshape(d_ref.shape)
+                # Adam moves every element by ~lr; compare the updates (sign flips of tiny grads allowed)
+                assert rel_l2(d_me, d_ref) <= 0.1, (k, i, key, rel_l2(d_me, d_ref))
+        if k == 2:
+            assert abs(losses[1] - info["actor_loss"]) <= max(tol * abs(info["actor_loss"]), 1e-5)
+            ga = pk.unpack_actor(td3.acfg, td3.grad_actor.cpu().numpy())
+            for key in ga:
+                if np.linalg.norm(info["grads_a"][key]) > 0:
+                    assert rel_l2(ga[key], info["grads_a"][key]) <= (1e-4 if prec == "fp32" else 2e-2), key
+            at = pk.unpack_actor(td3.acfg, td3.actor_t.cpu().numpy())
+            for key in at:
+                assert np.allclose(at[key], st["actor_t"][key], rtol=1e-5, atol=3e-6), key
+        else:
+            a_now = pk.unpack_actor(td3.acfg, td3.actor.cpu().numpy())
+            assert all(np.array_equal(a_now[key], actor[key]) for key in actor)
+    assert td3.adam_steps.cpu().tolist() == [2, 0, 1, 0]
+
+
+def test_td3_graph_replay_matches_eager():
+    import torch
+    import paper_2502_17496_b200 as pk
+    shape, cs_, B = sg.preset("cfg1")
+    replay = pk.replay_fill(20000, 17, 6, seed=3)
+    outs = []
+    for mode in ("eager", "graph"):
+        rng = np.random.default_rng(8)
+        actor = sg.actor_params(shape, rng)
+        cs = sg.CriticShape(23, precision="bf16")
+        c1, c2 = sg.critic_params(cs, rng), sg.critic_params(cs, rng)
+        td3 = pk.TD3(pk.actor_cfg_from(shape), pk.critic_cfg(23), pk.td3_cfg(B), replay, seed=11)
+        td3.load(actor, c1, c2)
+        if mode == "graph":
+            snap = [t.clone() for t in (td3.actor, td3.critic, td3.actor_t, td3.critic_t)]
+            td3.capture()          # capture enqueues nothing; restore state to be safe
+            for t, sn in zip((td3.actor, td3.critic, td3.actor_t, td3.critic_t), snap):
+                t.copy_(sn)
+            td3.refresh()
+            for t in (td3.m_actor, td3.v_actor, td3.m_critic, td3.v_critic, td3.adam_steps, td3.rng_counter):
+                t.zero_()
+            for k in range(1, 7):
+                td3.replay_graph(k)
+        else:
+            for k in range(1, 7):
+                td3.update(k)
+        torch.cuda.synchronize()
+        outs.append([t.cpu().clone() for t in (td3.actor, td3.critic, td3.actor_t, td3.losses, td3.rng_counter)])
+    for a, b in zip(*outs):
+        assert torch.equal(a, b)
+
+
+def test_device_replay_and_rng():
+    import torch
+    import paper_2502_17496_b200 as pk
+    n = 200_000
+    r = pk.replay_fill(n, 17, 6, seed=5)
+    s = r.s.cpu().numpy()
+    assert abs(s.mean()) < 0.01 and abs(s.std() - 1) < 0.01 and s.max() <= 5 and s.min() >= -5
+    a = r.a.cpu().numpy()
+    assert a.min() >= -1 and a.max() <= 1 and abs(a.mean()) < 0.01
+    d = r.d.cpu().numpy()
+    assert set(np.unique(d)) <= {0.0, 1.0} and abs(d.mean() - 0.01) < 0.002
+    r2 = pk.replay_fill(n, 17, 6, seed=5, rank=1)
+    assert not torch.equal(r.s, r2.s)
