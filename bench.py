@@ -1,0 +1,487 @@
+#!/usr/bin/env python
+"""Benchmark of the SpikeRL hot path on B200 (contract: see DESIGN.md "Measurement").
+
+  python bench.py [--gpus N --steps K --warmup W] [--workload cfg1|cfg2|cfg3s|cfg3L|cfg4]
+  python -m torch.distributed.run --nproc-per-node N ... bench.py --gpus N   (data parallel)
+  python bench.py --impl reference      (the CPU oracle, timed on the host cores)
+
+One JSON line on rank 0. A "step" is one TD3 update (configs[1..3]: replay sample -> target
+actor -> target critics -> critic fwd/bwd -> allreduce -> Adam -> [delayed actor fwd/BPTT,
+allreduce, Adam, Polyak]) or, for cfg4, one actor forward + BPTT + gradient allreduce over the
+rank's shard. Inputs are device-resident when the timed region starts (replay shard filled on
+the device); `e2e` re-times the same step through the public API with the minibatch copied
+from pinned host memory and the losses read back every step.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "TD3 spiking-actor updates/sec at 1/2/4/8 B200; actor fwd+bwd samples/sec"
+SIMT_FP32_PEAK_TFLOPS = 148 * 128 * 2 * 1.965e9 / 1e12  # guide: 148 SMs x 128 FP32 lanes x FMA x max clock
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=200)
+    ap.add_argument("--warmup", type=int, default=20)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--workload", default="cfg1", choices=["cfg1", "cfg2", "cfg3s", "cfg3L", "cfg4"])
+    ap.add_argument("--engine", default="auto", choices=["auto", "simt", "tcgen05"])
+    ap.add_argument("--no-flush", action="store_true", help="do not flush L2 between timed steps")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--replay-size", type=int, default=1_000_000)
+    return ap.parse_args()
+
+
+def peaks():
+    p = {"hbm_gbs": 6546.6, "bf16_tflops": 1631.2, "bf16_tflops_sustained": 1376.6, "src": "fallback"}
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            m = json.load(f)
+        p.update({k: m[k] for k in ("hbm_gbs", "bf16_tflops", "bf16_tflops_sustained") if k in m})
+        p["src"] = "measured"
+    except Exception:
+        pass
+    return p
+
+
+# ---------------------------------------------------------------------------------- clocks
+class ClockSampler:
+    Q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index, self.proc, self.lines = index, None, []
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self):
+        if not self.proc:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        sm, mx, reasons = [], None, set()
+        names = ("hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap")
+        for ln in self.lines:
+            f = [x.strip() for x in ln.split(",")]
+            if len(f) < 8:
+                continue
+            try:
+                sm.append(float(f[0])); mx = float(f[1])
+            except ValueError:
+                continue
+            for n, v in zip(names, f[4:8]):
+                if v.lower().startswith("active"):
+                    reasons.add(n)
+        sm.sort()
+        return {"sm_mhz": sm[len(sm) // 2] if sm else None, "sm_max_mhz": mx, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+# ---------------------------------------------------------------------------------- dist
+def dist_init(args):
+    import torch
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1:
+        import torch.distributed as dist
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    else:
+        torch.cuda.set_device(0)
+    return rank, world, local
+
+
+def barrier(world):
+    import torch
+    if world > 1:
+        import torch.distributed as dist
+        dist.barrier()
+    torch.cuda.synchronize()
+
+
+def max_over_ranks(x, world):
+    import torch
+    if world == 1:
+        return x
+    import torch.distributed as dist
+    t = torch.tensor([x], dtype=torch.float64, device="cuda")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+# ---------------------------------------------------------------------------------- workloads
+def build_td3(name, world, rank, engine, replay_size, seed=0):
+    import numpy as np
+    import synthgen as sg
+    import paper_2502_17496_b200 as pk
+    shape, cshape, B = sg.preset(name)
+    acfg = pk.actor_cfg_from(shape, engine=engine)
+    ccfg = pk.critic_cfg(cshape.in_dim, precision=shape.precision)
+    replay = pk.replay_fill(replay_size, shape.obs_dim, shape.act_dim, seed=seed, rank=rank)
+    comm = pk.Comm(rank, world) if world > 1 else None
+    td3 = pk.TD3(acfg, ccfg, pk.td3_cfg(B), replay, seed=seed, comm=comm)
+    rng = np.random.default_rng(seed)
+    td3.load(sg.actor_params(shape, rng), sg.critic_params(cshape, rng), sg.critic_params(cshape, rng))
+    return td3, shape, B
+
+
+def time_steps(run_step, K, flush_buf, world):
+    """Per-step CUDA events on the launching stream; L2 flushed between steps (outside events)."""
+    import torch
+    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(K)]
+    barrier(world)
+    for k in range(K):
+        if flush_buf is not None:
+            flush_buf.zero_()
+        evs[k][0].record()
+        run_step(k)
+        evs[k][1].record()
+    torch.cuda.synchronize()
+    barrier(world)
+    total_ms = sum(a.elapsed_time(b) for a, b in evs)
+    return max_over_ranks(total_ms, world)
+
+
+def dominant_kernel(summary, pk_peaks, long_step):
+    from paper_2502_17496_b200 import _lib
+    best = max(summary, key=lambda e: e["total_ms"])
+    avg_s = best["total_ms"] / best["launches"] / 1e3
+    if best["bound"] == "tensor":
+        per = best["flops"] / best["launches"]
+        peak = pk_peaks["bf16_tflops_sustained" if long_step else "bf16_tflops"]
+        ach, unit, bound = per / avg_s / 1e12, "TFLOP/s", "tensor"
+    elif best["bound"] == "alu":
+        per = best["flops"] / best["launches"]
+        peak = SIMT_FP32_PEAK_TFLOPS
+        ach, unit, bound = per / avg_s / 1e12, "TFLOP/s", "alu"
+    else:
+        per = best["bytes"] / best["launches"]
+        peak = pk_peaks["hbm_gbs"]
+        ach, unit, bound = per / avg_s / 1e9, "GB/s", "hbm"
+    traffic = None
+    try:
+        with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as f:
+            traffic = json.load(f).get(best["name"])
+    except Exception:
+        pass
+    total = sum(e["total_ms"] for e in summary)
+    return {"kernel": best["name"], "bound": bound, "achieved": round(ach, 3), "peak": peak, "unit": unit,
+            "frac": round(ach / peak, 5), "traffic": traffic, "work_per_launch": per,
+            "avg_launch_us": round(avg_s * 1e6, 3), "share_of_step": round(best["total_ms"] / total, 4),
+            "peak_src": pk_peaks["src"] if bound != "alu" else "derived (guide: 148 SM x 128 lanes x 2 x 1.965 GHz)"}
+
+
+def cpu_baseline_td3(name, seconds=12.0, min_steps=4):
+    import numpy as np
+    import oracle
+    import synthgen as sg
+    shape, cs, B = sg.preset(name)
+    rng = np.random.default_rng(0)
+    st = oracle.init_state(sg.actor_params(shape, rng), sg.critic_params(cs, rng), sg.critic_params(cs, rng))
+    hp = sg.TD3Hyper()
+    t0 = time.time()
+    k = 0
+    while k < min_steps or (time.time() - t0 < seconds and k % 2 == 0) or k % 2 == 1:
+        k += 1
+        st, _ = oracle.td3_update(st, shape, cs, hp, sg.replay_batch(rng, B, shape.obs_dim, shape.act_dim),
+                                  sg.target_noise(rng, B, shape.act_dim), k)
+        if time.time() - t0 > 4 * seconds:
+            break
+    dt = time.time() - t0
+    return {"value": round(k * B / dt, 3), "unit": "samples/s", "updates_per_s": round(k / dt, 4),
+            "cores": len(os.sched_getaffinity(0)), "kind": "oracle",
+            "sample": f"{k} full TD3 updates of {name} (B={B}, half with the delayed actor step), numpy fp64 oracle"}
+
+
+def cpu_baseline_actor(name, B_sample=16, seconds=12.0):
+    import numpy as np
+    import oracle
+    import synthgen as sg
+    shape, _, B = sg.preset(name)
+    rng = np.random.default_rng(0)
+    p = sg.actor_params(shape, rng)
+    t0 = time.time()
+    n = 0
+    while n == 0 or time.time() - t0 < seconds:
+        s = sg.observations(rng, B_sample, shape.obs_dim)
+        a, tape = oracle.actor_forward(p, shape, s)
+        oracle.actor_backward(p, shape, tape, sg.action_grads(rng, B_sample, shape.act_dim))
+        n += B_sample
+    dt = time.time() - t0
+    return {"value": round(n / dt, 3), "unit": "samples/s", "cores": len(os.sched_getaffinity(0)), "kind": "oracle",
+            "sample": f"{n} samples of {name} actor fwd+BPTT in batches of {B_sample} (extrapolates linearly in B)"}
+
+
+# ---------------------------------------------------------------------------------- ours
+def run_td3(args, rank, world):
+    import torch
+    import paper_2502_17496_b200 as pk
+    from paper_2502_17496_b200 import _lib
+    td3, shape, B = build_td3(args.workload, world, rank, args.engine, args.replay_size)
+    td3.capture()
+    launches = {}
+    lib = pk.lib()
+    for k in (1, 2):            # launches per phase, counted from an eager enqueue
+        lib.spikerl_launch_count(1)
+        td3.update(k)
+        launches[k % 2] = lib.spikerl_launch_count(1)
+    torch.cuda.synchronize()
+    flush = None if args.no_flush else torch.empty(64 * 1024 * 1024, dtype=torch.float32, device="cuda")  # 256 MB > L2
+    step0 = [2]
+
+    def graph_step(k):
+        td3.replay_graph(step0[0] + k)
+
+    for k in range(args.warmup):
+        graph_step(k)
+    step0[0] += args.warmup
+    torch.cuda.synchronize()
+    clk = ClockSampler(int(os.environ.get("LOCAL_RANK", "0")))
+    clk.start()
+    total_ms = time_steps(graph_step, args.steps, flush, world)
+    clocks = clk.stop()
+    gpu_launches = sum(launches[(step0[0] + k) % 2] for k in range(args.steps))
+    step0[0] += args.steps
+    secs = total_ms / 1e3
+    value = args.steps * B * world / secs
+    out = {"metric": METRIC, "value": round(value, 2), "unit": "samples/s", "n_gpus": world, "steps": args.steps,
+           "warmup": args.warmup, "ms_per_step": round(total_ms / args.steps, 5), "higher_is_better": True,
+           "scaling": "weak", "vs_baseline": None, "dtype": "bf16" if shape.precision == "bf16" else "f32",
+           "data": "synthetic (device-resident replay shard filled with Philox; configs[1] distributions)",
+           "updates_per_s": round(args.steps / secs, 3),
+           "config": {"workload": f"{args.workload}: TD3 update, spiking actor obs {shape.obs_dim} act "
+                                  f"{shape.act_dim} pop 10/10 hidden {shape.n1}-{shape.n2} T={shape.T}, twin critics "
+                                  f"{shape.obs_dim + shape.act_dim}->256->256->1",
+                      "global_batch": B * world, "per_rank_batch": B, "replay_per_rank": args.replay_size,
+                      "parallelism": f"dp{world}", "engine": args.engine,
+                      "l2": "flushed between timed steps (256 MB write, outside the events)" if flush is not None
+                      else "not flushed", "cuda_graph": True},
+           "clocks": clocks, "gpu_launches": int(gpu_launches)}
+    # e2e: minibatch from pinned host memory every step + loss read-back, through the public API
+    if not args.no_e2e:
+        out["e2e"] = e2e_td3(args, rank, world, td3, shape, B)
+    # roofline: eager profiling pass (CUDA events around every launch on its own stream)
+    _lib.prof_enable(True)
+    for k in range(8):
+        td3.update(step0[0] + k)
+    torch.cuda.synchronize()
+    summ = _lib.prof_summary()
+    _lib.prof_enable(False)
+    out["roofline"] = dominant_kernel(summ, peaks(), long_step=False)
+    out["kernel_breakdown"] = sorted([{k: (round(v, 4) if isinstance(v, float) else v) for k, v in e.items()}
+                                      for e in summ], key=lambda e: -e["total_ms"])[:12]
+    return out
+
+
+def e2e_td3(args, rank, world, td3_dev, shape, B):
+    import numpy as np
+    import torch
+    import paper_2502_17496_b200 as pk
+    S, A = shape.obs_dim, shape.act_dim
+    per = 2 * S + A + 2
+    nbuf = 8
+    rng = np.random.default_rng(100 + rank)
+    host = [pk.replay_from_host(__import__("synthgen").replay_batch(rng, B, S, A), device="cpu") for _ in range(nbuf)]
+    host = [pk.ReplayShard(*(t.pin_memory() for t in (h.s, h.a, h.r, h.s2, h.d))) for h in host]
+    f32 = dict(dtype=torch.float32, device="cuda")
+    rs = pk.ReplayShard(torch.empty(B, S, **f32), torch.empty(B, A, **f32), torch.empty(B, **f32),
+                        torch.empty(B, S, **f32), torch.empty(B, **f32))   # device staging = a replay of size B
+    td3 = pk.TD3(td3_dev.acfg, td3_dev.ccfg, td3_dev.hp, rs, seed=1, comm=td3_dev.comm)
+    for t_src, t_dst in ((td3_dev.actor, td3.actor), (td3_dev.actor_t, td3.actor_t), (td3_dev.critic, td3.critic),
+                         (td3_dev.critic_t, td3.critic_t)):
+        t_dst.copy_(t_src)
+    td3.refresh()
+    idx = torch.arange(B, dtype=torch.int64, device="cuda")
+    loss_host = torch.empty(2, dtype=torch.float32).pin_memory()
+
+    def step(k):
+        h = host[k % nbuf]
+        for src, dst in ((h.s, rs.s), (h.a, rs.a), (h.r, rs.r), (h.s2, rs.s2), (h.d, rs.d)):
+            dst.copy_(src, non_blocking=True)          # one cudaMemcpyAsync H2D each
+        td3.update(k + 1, indices=idx)
+        loss_host.copy_(td3.losses, non_blocking=True)
+
+    for k in range(args.warmup):
+        step(k)
+    total_ms = time_steps(step, args.steps, None, world)
+    torch.cuda.synchronize()
+    return {"value": round(args.steps * B * world / (total_ms / 1e3), 2), "unit": "samples/s",
+            "h2d_bytes_per_step": B * per * 4, "d2h_bytes_per_step": 8,
+            "path": "TD3.update (eager C-ABI call) fed from pinned host minibatches; losses read back"}
+
+
+def run_actor(args, rank, world):
+    """cfg4: actor forward + BPTT + gradient allreduce over the rank's shard (strong scaling)."""
+    import numpy as np
+    import torch
+    import synthgen as sg
+    import paper_2502_17496_b200 as pk
+    from paper_2502_17496_b200 import _lib
+    shape, _, Bg = sg.preset("cfg4")
+    B = Bg // world
+    actor = pk.SpikingActor(pk.actor_cfg_from(shape, engine=args.engine), B)
+    rng = np.random.default_rng(0)
+    actor.load(sg.actor_params(shape, rng))
+    comm = pk.Comm(rank, world) if world > 1 else None
+    if comm:
+        comm.broadcast(actor.params)
+        actor.refresh()
+    g = torch.Generator(device="cuda").manual_seed(rank)
+    obs = torch.clamp(torch.randn(B, shape.obs_dim, device="cuda", generator=g), -5, 5)
+    ga = torch.randn(B, shape.act_dim, device="cuda", generator=g)
+
+    def step(k):
+        actor.forward(obs)
+        actor.backward(obs, ga)
+        if comm:
+            comm.allreduce_mean(actor.grads)
+
+    for k in range(args.warmup):
+        step(k)
+    lib = pk.lib()
+    lib.spikerl_launch_count(1)
+    clk = ClockSampler(int(os.environ.get("LOCAL_RANK", "0")))
+    clk.start()
+    total_ms = time_steps(step, args.steps, None, world)
+    clocks = clk.stop()
+    n_launch = lib.spikerl_launch_count(1)
+    secs = total_ms / 1e3
+    out = {"metric": METRIC, "value": round(args.steps * Bg / secs, 2), "unit": "samples/s", "n_gpus": world,
+           "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(total_ms / args.steps, 4),
+           "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "bf16",
+           "data": "synthetic observations ~N(0,1) clipped +-5, upstream grads ~N(0,1)",
+           "config": {"workload": "cfg4: spiking actor fwd+BPTT (+allreduce), obs 376 act 17 pop 10/10 hidden "
+                                  "1024-1024 T=16", "global_batch": Bg, "per_rank_batch": B,
+                      "parallelism": f"dp{world}", "engine": args.engine,
+                      "l2": "inputs and tape (GBs) exceed L2"},
+           "clocks": clocks, "gpu_launches": int(n_launch)}
+    _lib.prof_enable(True)
+    step(0)
+    torch.cuda.synchronize()
+    summ = _lib.prof_summary()
+    _lib.prof_enable(False)
+    out["roofline"] = dominant_kernel(summ, peaks(), long_step=True)
+    out["kernel_breakdown"] = sorted([{k: (round(v, 4) if isinstance(v, float) else v) for k, v in e.items()}
+                                      for e in summ], key=lambda e: -e["total_ms"])[:12]
+    if not args.no_e2e:
+        host_obs = obs.cpu().pin_memory(); host_ga = ga.cpu().pin_memory()
+        grads_host = torch.empty(actor.n_params, dtype=torch.float32).pin_memory()
+
+        def e2e_step(k):
+            obs.copy_(host_obs, non_blocking=True); ga.copy_(host_ga, non_blocking=True)
+            step(k)
+            grads_host.copy_(actor.grads, non_blocking=True)
+        total = time_steps(e2e_step, max(3, args.steps // 4), None, world)
+        n = max(3, args.steps // 4)
+        out["e2e"] = {"value": round(n * Bg / (total / 1e3), 2), "unit": "samples/s",
+                      "h2d_bytes_per_step": B * (shape.obs_dim + shape.act_dim) * 4,
+                      "d2h_bytes_per_step": actor.n_params * 4}
+    return out
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        return reference(args)
+    import torch
+    rank, world, local = dist_init(args)
+    if args.workload == "cfg4":
+        out = run_actor(args, rank, world)
+        if rank == 0 and world == 1 and not args.no_cpu_baseline:
+            out["cpu_baseline"] = cpu_baseline_actor("cfg4")
+    else:
+        out = run_td3(args, rank, world)
+        if rank == 0 and world == 1 and not args.no_cpu_baseline:
+            out["cpu_baseline"] = cpu_baseline_td3(args.workload)
+    if rank == 0:
+        print(json.dumps(out), flush=True)
+    if world > 1:
+        import torch.distributed as dist
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+def reference(args):
+    """The oracle, as it stands, on the host cores: same metric/unit/config as our arm."""
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    import numpy as np
+    import oracle
+    import synthgen as sg
+    name = args.workload
+    shape, cs, B = sg.preset(name)
+    rng = np.random.default_rng(0)
+    if name == "cfg4":
+        p = sg.actor_params(shape, rng)
+        Bs = 8
+
+        def step(k):
+            s = sg.observations(rng, Bs, shape.obs_dim)
+            a, tape = oracle.actor_forward(p, shape, s)
+            oracle.actor_backward(p, shape, tape, sg.action_grads(rng, Bs, shape.act_dim))
+        per_step, sample = Bs, f"each step = {Bs} rows of cfg4 actor fwd+BPTT (value extrapolates linearly in B)"
+    else:
+        st = [oracle.init_state(sg.actor_params(shape, rng), sg.critic_params(cs, rng), sg.critic_params(cs, rng))]
+        hp = sg.TD3Hyper()
+
+        def step(k):
+            st[0], _ = oracle.td3_update(st[0], shape, cs, hp, sg.replay_batch(rng, B, shape.obs_dim, shape.act_dim),
+                                         sg.target_noise(rng, B, shape.act_dim), k + 1)
+        per_step, sample = B, f"each step = one full TD3 update of {name} at B={B}"
+    budget = 150.0
+    t_start = time.time()
+    for k in range(min(args.warmup, 3)):
+        step(k)
+    t0 = time.time()
+    done = 0
+    for k in range(args.steps):
+        step(args.warmup + k)
+        done += 1
+        if time.time() - t_start > budget:
+            break
+    dt = time.time() - t0
+    v = done * per_step / dt
+    cores = len(os.sched_getaffinity(0))
+    out = {"impl": "reference", "metric": METRIC, "value": round(v, 3), "unit": "samples/s", "n_gpus": args.gpus,
+           "steps": done, "warmup": min(args.warmup, 3), "ms_per_step": round(dt / done * 1e3, 3),
+           "higher_is_better": True, "scaling": "weak" if name != "cfg4" else "strong", "vs_baseline": None,
+           "dtype": "f64", "data": "synthetic", "config": {"workload": name, "per_rank_batch": B},
+           "cpu_baseline": {"value": round(v, 3), "unit": "samples/s", "cores": cores, "kind": "oracle",
+                            "sample": sample + (f"; stopped after {done} of {args.steps} steps (time budget)"
+                                                if done < args.steps else "")},
+           "e2e": {"value": round(v, 3), "unit": "samples/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(out), flush=True)
+
+
+if __name__ == "__main__":
+    main()

@@ -40,6 +40,18 @@ bool tc_supported(const ActorDims& d);
 int launch_lif_fwd_tc(const ActorDims& d, int l, int B, const uint32_t* bits_in,
                       const __nv_bfloat16* Wb16, uint32_t* bits_out, uint32_t* mask_out,
                       uint8_t* counts, cudaStream_t st);
+int launch_lif_dx_tc(const ActorDims& d, int l, int B, const void* Gl, const __nv_bfloat16* Wb16,
+                     const uint32_t* bits_prev, const uint32_t* mask_prev, void* Gprev, void* Gsum,
+                     cudaStream_t st);
+int launch_enc_grad_tc(const ActorDims& d, int B, const void* Gsum, const __nv_bfloat16* W1b16,
+                       const float* A, const float* obs, const float* mu, const float* sigma,
+                       float* partial, float* dmu, float* dsigma, int accumulate, cudaStream_t st);
+int launch_lif_dw_tc(const ActorDims& d, int l, int B, const void* Gl, const uint32_t* bits_prev,
+                     float* dW, float* part, int accumulate, cudaStream_t st);
+size_t tc_enc_partial_bytes(const ActorDims& d, int B);
+size_t tc_dw_partial_bytes(const ActorDims& d, int B);
+int launch_enc_grad_reduce(const ActorDims& d, int nchunk, const float* partial, float* dmu,
+                           float* dsigma, int accumulate, cudaStream_t st);
 
 // ---- optimiser / copies (k_optim.cu)
 int launch_actor_refresh_bf16(const ActorDims& d, const float* params, __nv_bfloat16* out,

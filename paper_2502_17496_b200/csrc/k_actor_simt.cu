@@ -351,6 +351,13 @@ __global__ void enc_grad_reduce_kernel(int nchunk, int K0, const float* __restri
   dsg[k] = accum ? __fadd_rn(dsg[k], s) : s;
 }
 
+int launch_enc_grad_reduce(const ActorDims& d, int nchunk, const float* partial, float* dmu,
+                           float* dsigma, int accumulate, cudaStream_t st) {
+  enc_grad_reduce_kernel<<<cdiv(d.K0, 256), 256, 0, st>>>(nchunk, d.K0, partial, dmu, dsigma, accumulate);
+  SPK_LAUNCHED();
+  return SPIKERL_OK;
+}
+
 int launch_enc_grad_simt(const ActorDims& d, int B, const void* Gsum, const float* W1f32,
                          const __nv_bfloat16* W1b16, const float* A, const float* obs,
                          const float* mu, const float* sigma, float* partial, float* dmu,

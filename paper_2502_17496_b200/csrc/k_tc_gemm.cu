@@ -1,20 +1,723 @@
-// k_tc_gemm.cu — tcgen05/TMEM/TMA tensor-core engine (bring-up pending).
+// k_tc_gemm.cu — tcgen05 / TMEM / TMA tensor-core engine for the four contractions of the
+// spiking actor, each with its epilogue fused:
+//   FWD  I_l = W_l o_{l-1} over all (t,b)  -> LIF forward scan in registers -> spike / mask
+//        bit planes (+ output counts)                      north_star
+//   DX   g_{l-1} = W_l^T G_l over all (t,b) -> reverse LIF scan of layer l-1 -> G_{l-1} bf16
+//        (+ sum_t G_1 for the encoder)                     SPEC.md:168-176; R11
+//   ENC  dL/dA = (sum_t G_1) W_1            -> dmu, dsigma partial sums over the tile's rows
+//                                                          DESIGN.md R6 (straight-through encoder)
+//   DW   dW_l = sum_{t,b} G_l^T o_{l-1}     -> deterministic split-K fp32 partials
+// One persistent, warp-specialised kernel (1 CTA/SM, 320 threads):
+//   warp 0      TMA producer (A tiles; B tiles when they are bf16 tensors)
+//   warp 1      TMEM allocator + single-thread tcgen05.mma issuer (M=128, N<=256, K=16 steps)
+//   warps 2-5   spike-bit expanders: u32 spike words -> bf16 {0,1} tiles in the 128B-swizzled
+//               UMMA layout (K-major for FWD, MN-major for DW)
+//   warps 6-9   epilogue: tcgen05.ld (32x32b) of the TMEM accumulator, one thread per neuron
+// Pipelines: 4-stage smem ring (full/empty mbarriers), 2-stage TMEM accumulator (2 x 256 cols).
+// Neurons sit on TMEM lanes (MMA M) and (t,b) on columns (MMA N) with t-major order, so a
+// thread owns every timestep of its neuron: the LIF scans never leave registers, and one
+// __ballot_sync per (t,b) yields exactly one u32 word of the next layer's bit plane.
+#include <cuda.h>
+#include <mutex>
 #include "internal.h"
 
 namespace spk {
+namespace tc {
+
+enum Mode { FWD = 0, DX = 1, ENC = 2, DW = 3 };
+
+constexpr int BM = 128, BK = 64, STAGES = 4;
+constexpr int A_STAGE = BM * BK * 2;             // 16 KB
+constexpr int B_STAGE = 256 * BK * 2;            // 32 KB
+constexpr int STAGE_BYTES = A_STAGE + B_STAGE;   // 48 KB
+constexpr int NUM_EXP_WARPS = 4, NUM_EPI_WARPS = 4;
+constexpr int EXP_WARP0 = 2, EPI_WARP0 = 2 + NUM_EXP_WARPS;
+constexpr int NUM_THREADS = (EPI_WARP0 + NUM_EPI_WARPS) * 32;  // 320
+constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + 1024 + 256;
+constexpr int TMEM_COLS = 512;
+constexpr int DW_BN = 256;
+
+struct Params {
+  int T, B, Bt, BN;
+  int m_tiles, n_tiles, k_blocks, kps, n_units;
+  // FWD
+  const uint32_t* bits_in; int w_in;
+  uint32_t* bits_out; uint32_t* mask_out; int w_out; uint8_t* counts; int n_valid; int n3;
+  LifConst kc; float zh;
+  // DX
+  const uint32_t* bits_prev; const uint32_t* mask_prev; int w_prev;
+  __nv_bfloat16* g_prev; int p_prev; __nv_bfloat16* g_sum;
+  // ENC
+  const float* A; const float* obs; const float* mu; const float* sigma; float* partial; int K0, S, E;
+  // DW
+  const uint32_t* bits_dw; int w_dw; float* dw_part; long long split_stride; int ldp; int R;
+};
+
+// ------------------------------------------------------------------------- PTX helpers
+__device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n"
+      "WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+      "@!p bra WAIT_%=;\n}" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void fence_barrier_init() { asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory"); }
+__device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
+__device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
+
+__device__ __forceinline__ void tma_2d(const CUtensorMap* map, void* dst, uint64_t* bar, int c0, int c1) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4}], [%2];" ::"r"(
+          smem_u32(dst)),
+      "l"(map), "r"(smem_u32(bar)), "r"(c0), "r"(c1)
+      : "memory");
+}
+__device__ __forceinline__ void tma_3d(const CUtensorMap* map, void* dst, uint64_t* bar, int c0, int c1, int c2) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4, %5}], [%2];" ::"r"(
+          smem_u32(dst)),
+      "l"(map), "r"(smem_u32(bar)), "r"(c0), "r"(c1), "r"(c2)
+      : "memory");
+}
+
+__device__ __forceinline__ void tmem_alloc(uint32_t* dst, uint32_t ncols) {
+  asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(dst)), "r"(ncols)
+               : "memory");
+  asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+}
+__device__ __forceinline__ void tmem_dealloc(uint32_t taddr, uint32_t ncols) {
+  asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(taddr), "r"(ncols) : "memory");
+}
+
+// UMMA shared-memory descriptor, 128B swizzle (sm_100 "version 1" descriptor).
+__device__ __forceinline__ uint64_t make_desc(uint32_t saddr, uint32_t lbo_bytes, uint32_t sbo_bytes) {
+  uint64_t d = 0;
+  d |= (uint64_t)((saddr & 0x3FFFF) >> 4);
+  d |= (uint64_t)((lbo_bytes >> 4) & 0x3FFF) << 16;
+  d |= (uint64_t)((sbo_bytes >> 4) & 0x3FFF) << 32;
+  d |= (uint64_t)1 << 46;  // version
+  d |= (uint64_t)2 << 61;  // SWIZZLE_128B
+  return d;
+}
+// instruction descriptor: bf16 x bf16 -> f32, M = 128
+__host__ __device__ constexpr uint32_t make_idesc(int N, int a_mn, int b_mn) {
+  return (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)a_mn << 15) | ((uint32_t)b_mn << 16) |
+         ((uint32_t)(N >> 3) << 17) | ((uint32_t)(BM >> 4) << 24);
+}
+__device__ __forceinline__ void mma_bf16(uint32_t d_tmem, uint64_t adesc, uint64_t bdesc, uint32_t idesc, uint32_t acc) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n}" ::"r"(d_tmem),
+      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(acc)
+      : "memory");
+}
+__device__ __forceinline__ void mma_commit(uint64_t* bar) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(bar))
+               : "memory");
+}
+__device__ __forceinline__ void tmem_ld8(uint32_t taddr, uint32_t (&r)[8]) {
+  asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0, %1, %2, %3, %4, %5, %6, %7}, [%8];"
+               : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7])
+               : "r"(taddr));
+}
+__device__ __forceinline__ void tmem_ld_wait() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
+
+// 8 spike bits -> 8 bf16 values {0, 1.0} (16 bytes)
+__device__ __forceinline__ uint4 expand_byte(uint32_t byte) {
+  uint4 r;
+  r.x = ((byte & 1u) ? 0x3F80u : 0u) | ((byte & 2u) ? 0x3F800000u : 0u);
+  r.y = ((byte & 4u) ? 0x3F80u : 0u) | ((byte & 8u) ? 0x3F800000u : 0u);
+  r.z = ((byte & 16u) ? 0x3F80u : 0u) | ((byte & 32u) ? 0x3F800000u : 0u);
+  r.w = ((byte & 64u) ? 0x3F80u : 0u) | ((byte & 128u) ? 0x3F800000u : 0u);
+  return r;
+}
+__device__ __forceinline__ void st_shared_v4(uint32_t addr, uint4 v) {
+  asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(addr), "r"(v.x), "r"(v.y), "r"(v.z), "r"(v.w)
+               : "memory");
+}
+
+struct Tile { int m, n, kb0, kb1, split; };
+
+template <int MODE>
+__device__ __forceinline__ Tile decode(const Params& p, int u) {
+  Tile t;
+  t.m = u % p.m_tiles;
+  int rest = u / p.m_tiles;
+  if (MODE == DW) {
+    t.n = rest % p.n_tiles;
+    t.split = rest / p.n_tiles;
+    t.kb0 = t.split * p.kps;
+    t.kb1 = min(p.k_blocks, t.kb0 + p.kps);
+  } else {
+    t.n = rest;
+    t.split = 0;
+    t.kb0 = 0;
+    t.kb1 = p.k_blocks;
+  }
+  return t;
+}
+
+// ------------------------------------------------------------------------- the kernel
+template <int MODE, int BT>
+__global__ void __launch_bounds__(NUM_THREADS, 1)
+    tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, const Params p) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
+  uint64_t* full = (uint64_t*)(smem + STAGES * STAGE_BYTES);
+  uint64_t* empty = full + STAGES;
+  uint64_t* tfull = empty + STAGES;
+  uint64_t* tempty = tfull + 2;
+  uint32_t* tmem_slot = (uint32_t*)(tempty + 2);
+  constexpr bool B_EXPAND = (MODE == FWD || MODE == DW);
+  constexpr bool A_MN = (MODE != FWD);
+  constexpr bool B_MN = (MODE == DW);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < STAGES; ++s) {
+      mbar_init(&full[s], 1 + (B_EXPAND ? NUM_EXP_WARPS : 0));
+      mbar_init(&empty[s], 1);
+    }
+    for (int a = 0; a < 2; ++a) {
+      mbar_init(&tfull[a], 1);
+      mbar_init(&tempty[a], NUM_EPI_WARPS);
+    }
+    fence_barrier_init();
+  }
+  if (warp == 1) tmem_alloc(tmem_slot, TMEM_COLS);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp == 0) {
+    // ===================== TMA producer =====================
+    if (lane == 0) {
+      uint32_t it = 0;
+      const uint32_t bytes_b = (MODE == DX) ? 128u * p.T * p.Bt : (MODE == ENC ? 128u * p.BN : 0u);
+      for (int u = blockIdx.x; u < p.n_units; u += gridDim.x) {
+        const Tile t = decode<MODE>(p, u);
+        for (int kb = t.kb0; kb < t.kb1; ++kb, ++it) {
+          const int stage = it % STAGES;
+          const uint32_t ph = (it / STAGES) & 1;
+          mbar_wait(&empty[stage], ph ^ 1);
+          uint8_t* sA = smem + stage * STAGE_BYTES;
+          uint8_t* sB = sA + A_STAGE;
+          mbar_expect_tx(&full[stage], (uint32_t)A_STAGE + bytes_b);
+          if (!A_MN) {
+            tma_2d(&tmA, sA, &full[stage], kb * BK, t.m * BM);
+          } else {
+            tma_2d(&tmA, sA, &full[stage], t.m * BM, kb * BK);
+            tma_2d(&tmA, sA + 8192, &full[stage], t.m * BM + 64, kb * BK);
+          }
+          if (MODE == DX) tma_3d(&tmB, sB, &full[stage], kb * BK, t.n * p.Bt, 0);
+          if (MODE == ENC) tma_2d(&tmB, sB, &full[stage], kb * BK, t.n * p.BN);
+        }
+      }
+    }
+  } else if (warp == 1) {
+    // ===================== MMA issuer =====================
+    if (lane == 0) {
+      uint32_t it = 0, titer = 0;
+      const uint32_t idesc = make_idesc(p.BN, A_MN ? 1 : 0, B_MN ? 1 : 0);
+      for (int u = blockIdx.x; u < p.n_units; u += gridDim.x, ++titer) {
+        const Tile t = decode<MODE>(p, u);
+        const uint32_t a = titer & 1, aph = (titer >> 1) & 1;
+        mbar_wait(&tempty[a], aph ^ 1);
+        tc_fence_after();
+        const uint32_t d_tmem = tmem + a * 256;
+        for (int kb = t.kb0; kb < t.kb1; ++kb, ++it) {
+          const int stage = it % STAGES;
+          const uint32_t ph = (it / STAGES) & 1;
+          mbar_wait(&full[stage], ph);
+          tc_fence_after();
+          const uint32_t sA = smem_u32(smem + stage * STAGE_BYTES);
+          const uint32_t sB = sA + A_STAGE;
+#pragma unroll
+          for (int kk = 0; kk < BK / 16; ++kk) {
+            const uint64_t ad = A_MN ? make_desc(sA + kk * 2048, 8192, 1024) : make_desc(sA + kk * 32, 16, 1024);
+            const uint64_t bd = B_MN ? make_desc(sB + kk * 2048, 8192, 1024) : make_desc(sB + kk * 32, 16, 1024);
+            mma_bf16(d_tmem, ad, bd, idesc, (kb > t.kb0 || kk > 0) ? 1u : 0u);
+          }
+          mma_commit(&empty[stage]);
+        }
+        mma_commit(&tfull[a]);
+      }
+    }
+  } else if (warp < EPI_WARP0) {
+    // ===================== spike-bit expanders =====================
+    if (B_EXPAND) {
+      const int et = threadIdx.x - EXP_WARP0 * 32;
+      uint32_t it = 0;
+      for (int u = blockIdx.x; u < p.n_units; u += gridDim.x) {
+        const Tile t = decode<MODE>(p, u);
+        for (int kb = t.kb0; kb < t.kb1; ++kb, ++it) {
+          const int stage = it % STAGES;
+          const uint32_t ph = (it / STAGES) & 1;
+          mbar_wait(&empty[stage], ph ^ 1);
+          const uint32_t sB = smem_u32(smem + stage * STAGE_BYTES + A_STAGE);
+          if (MODE == FWD) {
+            // K-major: row = t*Bt + j (one (t,b) spike row), 64 k = 2 words = 8 chunks of 16 B
+            const int rows = p.T * p.Bt;
+            for (int idx = et; idx < rows * 2; idx += NUM_EXP_WARPS * 32) {
+              const int row = idx >> 1, half = idx & 1;
+              const int tt = row / p.Bt, j = row - tt * p.Bt;
+              const int b = t.n * p.Bt + j;
+              const uint32_t w = (b < p.B) ? __ldg(p.bits_in + ((size_t)tt * p.B + b) * p.w_in + kb * 2 + half) : 0u;
+#pragma unroll
+              for (int c = 0; c < 4; ++c) {
+                const int chunk = half * 4 + c;
+                st_shared_v4(sB + row * 128 + ((chunk ^ (row & 7)) << 4), expand_byte((w >> (8 * c)) & 0xFFu));
+              }
+            }
+          } else {
+            // MN-major: K row r (one (t,b)), 256 output columns k = 4 atoms x 64 = 8 words
+            const int r0 = kb * BK;
+            const int wbase = t.n * (DW_BN / 32);
+            for (int idx = et; idx < BK * 8; idx += NUM_EXP_WARPS * 32) {
+              const int r = idx >> 3, wi = idx & 7;
+              const int rg = r0 + r;
+              const int wcol = wbase + wi;
+              const uint32_t w = (rg < p.R && wcol < p.w_dw) ? __ldg(p.bits_dw + (size_t)rg * p.w_dw + wcol) : 0u;
+              const int atom = wi >> 1, half = wi & 1;
+#pragma unroll
+              for (int c = 0; c < 4; ++c) {
+                const int chunk = half * 4 + c;
+                st_shared_v4(sB + atom * 8192 + r * 128 + ((chunk ^ (r & 7)) << 4),
+                             expand_byte((w >> (8 * c)) & 0xFFu));
+              }
+            }
+          }
+          fence_proxy_async();
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&full[stage]);
+        }
+      }
+    }
+  } else {
+    // ===================== epilogue =====================
+    const int q = warp & 3;
+    uint32_t titer = 0;
+    for (int u = blockIdx.x; u < p.n_units; u += gridDim.x, ++titer) {
+      const Tile t = decode<MODE>(p, u);
+      const uint32_t a = titer & 1, aph = (titer >> 1) & 1;
+      mbar_wait(&tfull[a], aph);
+      tc_fence_after();
+      const uint32_t taddr = tmem + ((uint32_t)(32 * q) << 16) + a * 256;
+      const int row = t.m * BM + 32 * q + lane;  // neuron index (M)
+      if (MODE == FWD) {
+        const bool valid = row < p.n_valid;
+        const int b0 = t.n * BT;
+        float c[BT], v[BT];
+        int cnt[BT];
+        uint64_t oprev = 0;
+#pragma unroll
+        for (int j = 0; j < BT; ++j) { c[j] = 0.f; v[j] = 0.f; cnt[j] = 0; }
+        const size_t wcol = (size_t)(t.m * BM + 32 * q) >> 5;
+        for (int tt = 0; tt < p.T; ++tt) {
+#pragma unroll
+          for (int j0 = 0; j0 < BT; j0 += 8) {
+            uint32_t r[8];
+            tmem_ld8(taddr + tt * BT + j0, r);
+            tmem_ld_wait();
+            uint32_t wo = 0, wh = 0;
+#pragma unroll
+            for (int jj = 0; jj < 8; ++jj) {
+              const int j = j0 + jj;
+              bool o = (oprev >> j) & 1ull, h;
+              lif_step(p.kc, __uint_as_float(r[jj]), c[j], v[j], o, h);
+              if (!valid) { o = false; h = false; }
+              oprev = o ? (oprev | (1ull << j)) : (oprev & ~(1ull << j));
+              cnt[j] += o ? 1 : 0;
+              const uint32_t ob = __ballot_sync(0xffffffffu, o), hb = __ballot_sync(0xffffffffu, h);
+              if (lane == jj) { wo = ob; wh = hb; }
+            }
+            const int b = b0 + j0 + lane;
+            if (lane < 8 && b < p.B) {
+              const size_t wi = ((size_t)tt * p.B + b) * p.w_out + wcol;
+              p.bits_out[wi] = wo;
+              p.mask_out[wi] = wh;
+            }
+          }
+        }
+        if (p.counts && row < p.n3) {
+#pragma unroll
+          for (int j = 0; j < BT; ++j) {
+            const int b = b0 + j;
+            if (b < p.B) p.counts[(size_t)b * p.n3 + row] = (uint8_t)cnt[j];
+          }
+        }
+      } else if (MODE == DX) {
+        const bool valid = row < p.n_valid;
+        const int b0 = t.n * BT;
+        float dvn[BT], dcn[BT], gs[BT];
+#pragma unroll
+        for (int j = 0; j < BT; ++j) { dvn[j] = 0.f; dcn[j] = 0.f; gs[j] = 0.f; }
+        const size_t wcol = (size_t)(t.m * BM + 32 * q) >> 5;
+        for (int tt = p.T - 1; tt >= 0; --tt) {
+          uint32_t ow0 = 0, hw0 = 0, ow1 = 0, hw1 = 0;
+          if (lane < BT && b0 + lane < p.B) {
+            const size_t wi = ((size_t)tt * p.B + b0 + lane) * p.w_prev + wcol;
+            ow0 = __ldg(p.bits_prev + wi);
+            hw0 = __ldg(p.mask_prev + wi);
+          }
+          if (BT > 32 && lane + 32 < BT && b0 + lane + 32 < p.B) {
+            const size_t wi = ((size_t)tt * p.B + b0 + lane + 32) * p.w_prev + wcol;
+            ow1 = __ldg(p.bits_prev + wi);
+            hw1 = __ldg(p.mask_prev + wi);
+          }
+#pragma unroll
+          for (int j0 = 0; j0 < BT; j0 += 8) {
+            uint32_t r[8];
+            tmem_ld8(taddr + tt * BT + j0, r);
+            tmem_ld_wait();
+#pragma unroll
+            for (int jj = 0; jj < 8; ++jj) {
+              const int j = j0 + jj;
+              const uint32_t ow = __shfl_sync(0xffffffffu, j < 32 ? ow0 : ow1, j & 31);
+              const uint32_t hw = __shfl_sync(0xffffffffu, j < 32 ? hw0 : hw1, j & 31);
+              const bool o = (ow >> lane) & 1u, h = (hw >> lane) & 1u;
+              float G = lif_back_step(p.zh, p.kc.dv, p.kc.dc, __uint_as_float(r[jj]), o, h, dvn[j], dcn[j]);
+              if (!valid) G = 0.f;
+              gs[j] = __fadd_rn(gs[j], G);
+              const int b = b0 + j;
+              if (b < p.B) p.g_prev[((size_t)tt * p.B + b) * p.p_prev + row] = __float2bfloat16_rn(G);
+            }
+          }
+        }
+        if (p.g_sum) {
+#pragma unroll
+          for (int j = 0; j < BT; ++j) {
+            const int b = b0 + j;
+            if (b < p.B) p.g_sum[(size_t)b * p.p_prev + row] = __float2bfloat16_rn(gs[j]);
+          }
+        }
+      } else if (MODE == ENC) {
+        const bool valid = row < p.K0;
+        const float m = valid ? p.mu[row] : 0.f, sg = valid ? p.sigma[row] : 1.f;
+        const float sg2 = __fmul_rn(sg, sg), sg3 = __fmul_rn(sg2, sg);
+        const int i = valid ? row / p.E : 0;
+        float pm = 0.f, ps = 0.f;
+        for (int j0 = 0; j0 < p.BN; j0 += 8) {
+          uint32_t r[8];
+          tmem_ld8(taddr + j0, r);
+          tmem_ld_wait();
+#pragma unroll
+          for (int jj = 0; jj < 8; ++jj) {
+            const int b = t.n * p.BN + j0 + jj;
+            if (valid && b < p.B) {
+              const float gA = __uint_as_float(r[jj]);
+              const float av = __ldg(p.A + (size_t)b * p.K0 + row);
+              const float dd = __fsub_rn(__ldg(p.obs + (size_t)b * p.S + i), m);
+              const float ga = __fmul_rn(gA, av);
+              pm = __fadd_rn(pm, __fdiv_rn(__fmul_rn(ga, dd), sg2));
+              ps = __fadd_rn(ps, __fdiv_rn(__fmul_rn(ga, __fmul_rn(dd, dd)), sg3));
+            }
+          }
+        }
+        if (valid) {
+          p.partial[((size_t)t.n * p.K0 + row) * 2 + 0] = pm;
+          p.partial[((size_t)t.n * p.K0 + row) * 2 + 1] = ps;
+        }
+      } else {  // DW
+        float* dst = p.dw_part + (size_t)t.split * p.split_stride + (size_t)row * p.ldp + t.n * DW_BN;
+        for (int j0 = 0; j0 < DW_BN; j0 += 8) {
+          uint32_t r[8];
+          tmem_ld8(taddr + j0, r);
+          tmem_ld_wait();
+          if (t.n * DW_BN + j0 < p.ldp) {
+            float4* d4 = reinterpret_cast<float4*>(dst + j0);
+            d4[0] = make_float4(__uint_as_float(r[0]), __uint_as_float(r[1]), __uint_as_float(r[2]), __uint_as_float(r[3]));
+            d4[1] = make_float4(__uint_as_float(r[4]), __uint_as_float(r[5]), __uint_as_float(r[6]), __uint_as_float(r[7]));
+          }
+        }
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&tempty[a]);
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    tmem_dealloc(tmem, TMEM_COLS);
+  }
+}
+
+// dW[n][k] (master layout) = sum over splits (fixed order) of the partial tiles
+__global__ void dw_reduce_kernel(const float* __restrict__ part, int splits, long long split_stride, int ldp,
+                                 int N, int K, float* __restrict__ dW, int accum) {
+  const long long total = (long long)N * K;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < total; i += (long long)gridDim.x * blockDim.x) {
+    const int n = (int)(i / K), k = (int)(i % K);
+    const float* src = part + (size_t)n * ldp + k;
+    float s = 0.f;
+    for (int sp = 0; sp < splits; ++sp) s = __fadd_rn(s, src[(size_t)sp * split_stride]);
+    dW[i] = accum ? __fadd_rn(dW[i], s) : s;
+  }
+}
+
+// ------------------------------------------------------------------------- host side
+typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                  const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                  CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+static EncodeTiledFn encode_fn() {
+  static EncodeTiledFn fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    cudaDriverEntryPointQueryResult q;
+    void* f = nullptr;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &f, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = (EncodeTiledFn)f;
+  });
+  return fn;
+}
+
+// bf16 tensor map, 128B swizzle, dims/strides listed innermost first (strides in bytes, rank-1 of them)
+static int make_map(CUtensorMap* m, const void* base, int rank, const uint64_t* dims, const uint64_t* strides,
+                    const uint32_t* box) {
+  EncodeTiledFn fn = encode_fn();
+  if (!fn) { set_error("cuTensorMapEncodeTiled unavailable"); return SPIKERL_E_CUDA; }
+  cuuint64_t gd[3], gs[2];
+  cuuint32_t bx[3], es[3] = {1, 1, 1};
+  for (int i = 0; i < rank; ++i) { gd[i] = dims[i]; bx[i] = box[i]; }
+  for (int i = 0; i < rank - 1; ++i) gs[i] = strides[i];
+  CUresult r = fn(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, rank, const_cast<void*>(base), gd, gs, bx, es,
+                  CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                  CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) { set_error("cuTensorMapEncodeTiled failed (%d)", (int)r); return SPIKERL_E_CUDA; }
+  return SPIKERL_OK;
+}
+
+static int num_sms() {
+  static int n = 0;
+  if (!n) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+    if (n <= 0) n = 148;
+  }
+  return n;
+}
+
+template <int MODE, int BT>
+static int launch(const CUtensorMap& ma, const CUtensorMap& mb, const Params& p, cudaStream_t st) {
+  static bool attr = false;
+  if (!attr) {
+    cudaError_t e = cudaFuncSetAttribute(tc_kernel<MODE, BT>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES);
+    if (e != cudaSuccess) { set_error("cudaFuncSetAttribute: %s", cudaGetErrorString(e)); return SPIKERL_E_CUDA; }
+    attr = true;
+  }
+  const int grid = p.n_units < num_sms() ? p.n_units : num_sms();
+  tc_kernel<MODE, BT><<<grid, NUM_THREADS, SMEM_BYTES, st>>>(ma, mb, p);
+  SPK_LAUNCHED();
+  return SPIKERL_OK;
+}
+
+template <int MODE>
+static int launch_bt(int bt, const CUtensorMap& ma, const CUtensorMap& mb, const Params& p, cudaStream_t st) {
+  if (MODE == ENC || MODE == DW) return launch<MODE, 8>(ma, mb, p, st);
+  switch (bt) {
+    case 8: return launch<MODE, 8>(ma, mb, p, st);
+    case 16: return launch<MODE, 16>(ma, mb, p, st);
+    case 24: return launch<MODE, 24>(ma, mb, p, st);
+    case 32: if (MODE == FWD) return launch<MODE, 32>(ma, mb, p, st); break;
+  }
+  set_error("unsupported batch tile %d", bt);
+  return SPIKERL_E_UNSUPPORTED;
+}
+
+// batch rows per N tile: Bt % 8 == 0, T*Bt % 16 == 0, T*Bt <= 256, Bt <= max_bt (register budget:
+// FWD keeps c, v per row, DX keeps dv, dc, sum per row); prefer the largest Bt that still gives >= one
+// wave of tiles, else the smallest valid one.
+static int choose_bt(int T, int B, int m_tiles, int max_bt) {
+  int best = 0, smallest = 0;
+  for (int bt = 8; bt <= max_bt; bt += 8) {
+    if ((T * bt) % 16 != 0 || T * bt > 256) continue;
+    if (!smallest) smallest = bt;
+    const long long tiles = (long long)m_tiles * ((B + bt - 1) / bt);
+    if (tiles >= num_sms()) best = bt;
+  }
+  return best ? best : smallest;
+}
+
+constexpr int FWD_MAX_BT = 32, DX_MAX_BT = 24;
+
+}  // namespace tc
+
+using namespace tc;
 
 bool tc_supported(const ActorDims& d) {
-  (void)d;
+  if (!d.bf16) return false;
+  for (int bt = 8; bt <= DX_MAX_BT; bt += 8)
+    if ((d.T * bt) % 16 == 0 && d.T * bt <= 256) return true;
   return false;
 }
 
-int launch_lif_fwd_tc(const ActorDims& d, int l, int B, const uint32_t* bits_in,
-                      const __nv_bfloat16* Wb16, uint32_t* bits_out, uint32_t* mask_out,
-                      uint8_t* counts, cudaStream_t st) {
-  (void)d; (void)l; (void)B; (void)bits_in; (void)Wb16; (void)bits_out; (void)mask_out;
-  (void)counts; (void)st;
-  set_error("tcgen05 engine not available");
-  return SPIKERL_E_UNSUPPORTED;
+int launch_lif_fwd_tc(const ActorDims& d, int l, int B, const uint32_t* bits_in, const __nv_bfloat16* Wb16,
+                      uint32_t* bits_out, uint32_t* mask_out, uint8_t* counts, cudaStream_t st) {
+  ProfScope ps_(l == 1 ? "lif_fwd_tc_L1" : (l == 2 ? "lif_fwd_tc_L2" : "lif_fwd_tc_L3"), PB_TENSOR,
+                2.0 * d.T * B * (double)d.N[l] * d.N[l - 1], 0.0, st);
+  Params p{};
+  p.T = d.T; p.B = B;
+  p.m_tiles = d.P[l] / BM;
+  p.Bt = choose_bt(d.T, B, p.m_tiles, FWD_MAX_BT);
+  p.BN = d.T * p.Bt;
+  p.n_tiles = (B + p.Bt - 1) / p.Bt;
+  p.k_blocks = d.P[l - 1] / BK;
+  p.n_units = p.m_tiles * p.n_tiles;
+  p.bits_in = bits_in; p.w_in = d.Wd[l - 1];
+  p.bits_out = bits_out; p.mask_out = mask_out; p.w_out = d.Wd[l];
+  p.counts = counts; p.n_valid = d.N[l]; p.n3 = d.N[3];
+  p.kc = LifConst{d.dc, d.dv, d.vth, d.win}; p.zh = d.zh;
+  CUtensorMap ma, mb;
+  const uint64_t dims[2] = {(uint64_t)d.P[l - 1], (uint64_t)d.P[l]};
+  const uint64_t strides[1] = {(uint64_t)d.P[l - 1] * 2};
+  const uint32_t box[2] = {64, 128};
+  SPK_TRY(make_map(&ma, Wb16, 2, dims, strides, box));
+  mb = ma;
+  return launch_bt<FWD>(p.Bt, ma, mb, p, st);
+}
+
+// dX of layer l fused with the reverse scan of layer l-1 (G_l bf16 [T][B][P_l])
+int launch_lif_dx_tc(const ActorDims& d, int l, int B, const void* Gl, const __nv_bfloat16* Wb16,
+                     const uint32_t* bits_prev, const uint32_t* mask_prev, void* Gprev, void* Gsum,
+                     cudaStream_t st) {
+  ProfScope ps_(l == 3 ? "lif_dx_tc_L3" : "lif_dx_tc_L2", PB_TENSOR, 2.0 * d.T * B * (double)d.N[l] * d.N[l - 1],
+                0.0, st);
+  Params p{};
+  p.T = d.T; p.B = B;
+  p.m_tiles = d.P[l - 1] / BM;
+  p.Bt = choose_bt(d.T, B, p.m_tiles, DX_MAX_BT);
+  p.BN = d.T * p.Bt;
+  p.n_tiles = (B + p.Bt - 1) / p.Bt;
+  p.k_blocks = d.P[l] / BK;
+  p.n_units = p.m_tiles * p.n_tiles;
+  p.bits_prev = bits_prev; p.mask_prev = mask_prev; p.w_prev = d.Wd[l - 1];
+  p.g_prev = (__nv_bfloat16*)Gprev; p.p_prev = d.P[l - 1]; p.g_sum = (__nv_bfloat16*)Gsum;
+  p.n_valid = d.N[l - 1];
+  p.kc = LifConst{d.dc, d.dv, d.vth, d.win}; p.zh = d.zh;
+  CUtensorMap ma, mb;
+  {  // A = W_l^T: W_l [P_l][P_{l-1}], M = P_{l-1} (contiguous) -> MN-major boxes of 64 x 64
+    const uint64_t dims[2] = {(uint64_t)d.P[l - 1], (uint64_t)d.P[l]};
+    const uint64_t strides[1] = {(uint64_t)d.P[l - 1] * 2};
+    const uint32_t box[2] = {64, 64};
+    SPK_TRY(make_map(&ma, Wb16, 2, dims, strides, box));
+  }
+  {  // B = G_l [T][B][P_l]: rows (t, b) t-major per tile, K = P_l
+    const uint64_t dims[3] = {(uint64_t)d.P[l], (uint64_t)B, (uint64_t)d.T};
+    const uint64_t strides[2] = {(uint64_t)d.P[l] * 2, (uint64_t)d.P[l] * 2 * B};
+    const uint32_t box[3] = {64, (uint32_t)p.Bt, (uint32_t)d.T};
+    SPK_TRY(make_map(&mb, Gl, 3, dims, strides, box));
+  }
+  return launch_bt<DX>(p.Bt, ma, mb, p, st);
+}
+
+size_t tc_enc_partial_bytes(const ActorDims& d, int B) {
+  const int BN = B >= 256 ? 256 : round_up(B, 16);
+  return sizeof(float) * 2 * (size_t)cdiv(B, BN) * d.K0;
+}
+
+int launch_enc_grad_tc(const ActorDims& d, int B, const void* Gsum, const __nv_bfloat16* W1b16, const float* A,
+                       const float* obs, const float* mu, const float* sigma, float* partial, float* dmu,
+                       float* dsigma, int accumulate, cudaStream_t st) {
+  ProfScope ps_("enc_grad_tc", PB_TENSOR, 2.0 * B * (double)d.N1 * d.K0, 0.0, st);
+  Params p{};
+  p.T = 1; p.B = B;
+  p.BN = B >= 256 ? 256 : round_up(B, 16);
+  p.m_tiles = d.P[0] / BM;
+  p.n_tiles = cdiv(B, p.BN);
+  p.k_blocks = d.P[1] / BK;
+  p.n_units = p.m_tiles * p.n_tiles;
+  p.A = A; p.obs = obs; p.mu = mu; p.sigma = sigma; p.partial = partial; p.K0 = d.K0; p.S = d.S; p.E = d.E;
+  CUtensorMap ma, mb;
+  {
+    const uint64_t dims[2] = {(uint64_t)d.P[0], (uint64_t)d.P[1]};
+    const uint64_t strides[1] = {(uint64_t)d.P[0] * 2};
+    const uint32_t box[2] = {64, 64};
+    SPK_TRY(make_map(&ma, W1b16, 2, dims, strides, box));
+  }
+  {
+    const uint64_t dims[2] = {(uint64_t)d.P[1], (uint64_t)B};
+    const uint64_t strides[1] = {(uint64_t)d.P[1] * 2};
+    const uint32_t box[2] = {64, (uint32_t)p.BN};
+    SPK_TRY(make_map(&mb, Gsum, 2, dims, strides, box));
+  }
+  SPK_TRY(launch_bt<ENC>(8, ma, mb, p, st));
+  return launch_enc_grad_reduce(d, p.n_tiles, partial, dmu, dsigma, accumulate, st);
+}
+
+// split-K plan for dW_l
+void tc_dw_plan(const ActorDims& d, int l, int B, int* splits, int* kps) {
+  const int m_tiles = d.P[l] / BM, n_tiles = cdiv(d.P[l - 1], DW_BN);
+  const int k_blocks = cdiv((long long)d.T * B, BK);
+  int s = cdiv(2LL * num_sms(), (long long)m_tiles * n_tiles);
+  if (s < 1) s = 1;
+  if (s > k_blocks) s = k_blocks;
+  const int per = cdiv(k_blocks, s);
+  *kps = per;
+  *splits = cdiv(k_blocks, per);
+}
+
+size_t tc_dw_partial_bytes(const ActorDims& d, int B) {
+  size_t mx = 0;
+  for (int l = 1; l <= 3; ++l) {
+    int s, k;
+    tc_dw_plan(d, l, B, &s, &k);
+    const size_t b = sizeof(float) * (size_t)s * d.P[l] * d.P[l - 1];
+    if (b > mx) mx = b;
+  }
+  return mx;
+}
+
+int launch_lif_dw_tc(const ActorDims& d, int l, int B, const void* Gl, const uint32_t* bits_prev, float* dW,
+                     float* part, int accumulate, cudaStream_t st) {
+  ProfScope ps_(l == 1 ? "lif_dw_tc_L1" : (l == 2 ? "lif_dw_tc_L2" : "lif_dw_tc_L3"), PB_TENSOR,
+                2.0 * d.T * B * (double)d.N[l] * d.N[l - 1], 0.0, st);
+  Params p{};
+  p.T = d.T; p.B = B; p.BN = DW_BN;
+  p.R = d.T * B;
+  p.m_tiles = d.P[l] / BM;
+  p.n_tiles = cdiv(d.P[l - 1], DW_BN);
+  p.k_blocks = cdiv(p.R, BK);
+  int splits, kps;
+  tc_dw_plan(d, l, B, &splits, &kps);
+  p.kps = kps;
+  p.n_units = p.m_tiles * p.n_tiles * splits;
+  p.bits_dw = bits_prev; p.w_dw = d.Wd[l - 1];
+  p.dw_part = part; p.ldp = d.P[l - 1]; p.split_stride = (long long)d.P[l] * d.P[l - 1];
+  CUtensorMap ma, mb;
+  {  // A = G_l viewed [T*B][P_l]: M = P_l contiguous (MN-major), K = rows
+    const uint64_t dims[2] = {(uint64_t)d.P[l], (uint64_t)p.R};
+    const uint64_t strides[1] = {(uint64_t)d.P[l] * 2};
+    const uint32_t box[2] = {64, 64};
+    SPK_TRY(make_map(&ma, Gl, 2, dims, strides, box));
+  }
+  mb = ma;
+  SPK_TRY(launch_bt<DW>(8, ma, mb, p, st));
+  const long long total = (long long)d.N[l] * d.N[l - 1];
+  const int grid = (int)((total + 255) / 256 < 148 * 8 ? (total + 255) / 256 : 148 * 8);
+  dw_reduce_kernel<<<grid, 256, 0, st>>>(part, splits, p.split_stride, p.ldp, d.N[l], d.N[l - 1], dW, accumulate);
+  SPK_LAUNCHED();
+  return SPIKERL_OK;
 }
 
 }  // namespace spk

@@ -134,6 +134,7 @@ struct ActorWs {
   size_t Gsum;      // [B][P1]
   size_t g_pre;     // [B][A] fp32
   size_t enc_part;  // encoder partials
+  size_t dw_part;   // tcgen05 split-K dW partials
   size_t total;
 };
 
@@ -147,7 +148,10 @@ static ActorWs actor_ws_layout(const ActorDims& d, int B) {
   for (int l = 1; l <= 3; ++l) w.G[l] = take(gsz * (size_t)d.T * B * d.P[l]);
   w.Gsum = take(gsz * (size_t)B * d.P[1]);
   w.g_pre = take(sizeof(float) * (size_t)B * d.A);
-  w.enc_part = take(enc_grad_partial_bytes(d, B));
+  const bool tc = d.engine == SPIKERL_ENGINE_TCGEN05;
+  const size_t ep = enc_grad_partial_bytes(d, B), ept = tc ? tc_enc_partial_bytes(d, B) : 0;
+  w.enc_part = take(ep > ept ? ep : ept);
+  w.dw_part = take(tc ? tc_dw_partial_bytes(d, B) : 0);
   w.total = o;
   return w;
 }
@@ -198,18 +202,33 @@ static int actor_backward_impl(const ActorDims& d, int B, const float* params,
                                  G[3], g_pre, st));
   SPK_TRY(launch_dec_param_grads(d, B, g_pre, counts, grads + d.off[SPIKERL_ACTOR_WD],
                                  grads + d.off[SPIKERL_ACTOR_BD], accum, st));
+  const bool tc = d.engine == SPIKERL_ENGINE_TCGEN05;
   for (int l = 3; l >= 1; --l) {
     const float* Wf = params + d.off[SPIKERL_ACTOR_W1 + l - 1];
     const __nv_bfloat16* Wb = d.bf16 ? pb16 + d.boff[l - 1] : nullptr;
-    SPK_TRY(launch_lif_dw_simt(d, l, B, G[l], bits[l - 1], grads + d.off[SPIKERL_ACTOR_W1 + l - 1], accum, st));
-    if (l >= 2)
-      SPK_TRY(launch_lif_dx_simt(d, l, B, G[l], Wf, Wb, bits[l - 1], mask[l - 1], G[l - 1],
-                                 l == 2 ? Gsum : nullptr, st));
+    float* dW = grads + d.off[SPIKERL_ACTOR_W1 + l - 1];
+    if (l >= 2) {
+      if (tc)
+        SPK_TRY(launch_lif_dx_tc(d, l, B, G[l], Wb, bits[l - 1], mask[l - 1], G[l - 1], l == 2 ? Gsum : nullptr, st));
+      else
+        SPK_TRY(launch_lif_dx_simt(d, l, B, G[l], Wf, Wb, bits[l - 1], mask[l - 1], G[l - 1],
+                                   l == 2 ? Gsum : nullptr, st));
+    }
+    if (tc)
+      SPK_TRY(launch_lif_dw_tc(d, l, B, G[l], bits[l - 1], dW, (float*)(ws + W.dw_part), accum, st));
+    else
+      SPK_TRY(launch_lif_dw_simt(d, l, B, G[l], bits[l - 1], dW, accum, st));
   }
-  SPK_TRY(launch_enc_grad_simt(d, B, Gsum, params + d.off[SPIKERL_ACTOR_W1], d.bf16 ? pb16 + d.boff[0] : nullptr,
-                               (const float*)(tape + L.A), obs, params + d.off[SPIKERL_ACTOR_MU],
+  const float* A = (const float*)(tape + L.A);
+  if (tc)
+    SPK_TRY(launch_enc_grad_tc(d, B, Gsum, pb16 + d.boff[0], A, obs, params + d.off[SPIKERL_ACTOR_MU],
                                params + d.off[SPIKERL_ACTOR_SIGMA], (float*)(ws + W.enc_part),
                                grads + d.off[SPIKERL_ACTOR_MU], grads + d.off[SPIKERL_ACTOR_SIGMA], accum, st));
+  else
+    SPK_TRY(launch_enc_grad_simt(d, B, Gsum, params + d.off[SPIKERL_ACTOR_W1], d.bf16 ? pb16 + d.boff[0] : nullptr,
+                                 A, obs, params + d.off[SPIKERL_ACTOR_MU], params + d.off[SPIKERL_ACTOR_SIGMA],
+                                 (float*)(ws + W.enc_part), grads + d.off[SPIKERL_ACTOR_MU],
+                                 grads + d.off[SPIKERL_ACTOR_SIGMA], accum, st));
   return SPIKERL_OK;
 }
 
