@@ -27,9 +27,11 @@ template <typename TA, typename TB> struct Ld;
 __device__ __forceinline__ float tof(float x) { return x; }
 __device__ __forceinline__ float tof(__nv_bfloat16 x) { return __bfloat162float(x); }
 
-constexpr int TM = 64, TN = 64, TK = 16;
+// 32x32 output tiles (latency-bound sizes: maximise the number of blocks), 256 threads with 2x2
+// outputs each, K chunks of 32 staged in shared memory with loads coalesced along whichever of
+// (m, k) / (k, n) is contiguous in memory; fp32 accumulation in a fixed k order.
+constexpr int TM = 32, TN = 32, TK = 32;
 
-// 256 threads, 4x4 outputs per thread, fp32 accumulate in a fixed k order.
 template <typename TA, typename TB, int EPI>
 __global__ void __launch_bounds__(256) gemm_simt_kernel(GemmArgs g) {
   __shared__ float sA[TK][TM + 1];
@@ -39,41 +41,60 @@ __global__ void __launch_bounds__(256) gemm_simt_kernel(GemmArgs g) {
   const TB* Bm = (const TB*)g.Bm + z * g.b_bs;
   const int m0 = blockIdx.y * TM, n0 = blockIdx.x * TN;
   const int tx = threadIdx.x % 16, ty = threadIdx.x / 16;
-  float acc[4][4] = {};
-  for (int k0 = 0; k0 < g.K; k0 += TK) {
-    for (int i = threadIdx.x; i < TK * TM; i += 256) {
-      const int kk = i / TM, mm = i % TM;
-      const int m = m0 + mm, k = k0 + kk;
-      sA[kk][mm] = (m < g.M && k < g.K) ? tof(A[(long long)m * g.sam + (long long)k * g.sak]) : 0.f;
+  const bool a_kfast = g.sak == 1, b_kfast = g.sbk == 1;
+  float acc[2][2] = {};
+  // register double buffering: the next K chunk's global loads are in flight while the current
+  // chunk is multiplied out of shared memory (loads go through the read-only path, so they are
+  // not serialised behind the shared-memory stores)
+  constexpr int PER = TK * TM / 256;  // 4 elements of A and of B per thread per chunk
+  float ra[PER], rb[PER];
+  auto load = [&](int k0) {
+#pragma unroll
+    for (int r = 0; r < PER; ++r) {
+      const int i = threadIdx.x + r * 256;
+      {
+        const int kk = a_kfast ? i % TK : i / TM, mm = a_kfast ? i / TK : i % TM;
+        const int m = m0 + mm, k = k0 + kk;
+        ra[r] = (m < g.M && k < g.K) ? tof(__ldg(A + (long long)m * g.sam + (long long)k * g.sak)) : 0.f;
+      }
+      {
+        const int kk = b_kfast ? i % TK : i / TN, nn = b_kfast ? i / TK : i % TN;
+        const int n = n0 + nn, k = k0 + kk;
+        rb[r] = (n < g.N && k < g.K) ? tof(__ldg(Bm + (long long)k * g.sbk + (long long)n * g.sbn)) : 0.f;
+      }
     }
-    for (int i = threadIdx.x; i < TK * TN; i += 256) {
-      const int kk = i / TN, nn = i % TN;
-      const int n = n0 + nn, k = k0 + kk;
-      sB[kk][nn] = (n < g.N && k < g.K) ? tof(Bm[(long long)k * g.sbk + (long long)n * g.sbn]) : 0.f;
+  };
+  load(0);
+  for (int k0 = 0; k0 < g.K; k0 += TK) {
+#pragma unroll
+    for (int r = 0; r < PER; ++r) {
+      const int i = threadIdx.x + r * 256;
+      const int ka = a_kfast ? i % TK : i / TM, ma = a_kfast ? i / TK : i % TM;
+      const int kb = b_kfast ? i % TK : i / TN, nb = b_kfast ? i / TK : i % TN;
+      sA[ka][ma] = ra[r];
+      sB[kb][nb] = rb[r];
     }
     __syncthreads();
+    if (k0 + TK < g.K) load(k0 + TK);
 #pragma unroll
     for (int kk = 0; kk < TK; ++kk) {
-      float a[4], b[4];
-#pragma unroll
-      for (int i = 0; i < 4; ++i) a[i] = sA[kk][ty * 4 + i];
-#pragma unroll
-      for (int j = 0; j < 4; ++j) b[j] = sB[kk][tx * 4 + j];
-#pragma unroll
-      for (int i = 0; i < 4; ++i)
-#pragma unroll
-        for (int j = 0; j < 4; ++j) acc[i][j] = __fmaf_rn(a[i], b[j], acc[i][j]);
+      const float a0 = sA[kk][ty * 2], a1 = sA[kk][ty * 2 + 1];
+      const float b0 = sB[kk][tx * 2], b1 = sB[kk][tx * 2 + 1];
+      acc[0][0] = __fmaf_rn(a0, b0, acc[0][0]);
+      acc[0][1] = __fmaf_rn(a0, b1, acc[0][1]);
+      acc[1][0] = __fmaf_rn(a1, b0, acc[1][0]);
+      acc[1][1] = __fmaf_rn(a1, b1, acc[1][1]);
     }
     __syncthreads();
   }
   float* C = g.C + z * g.c_bs;
 #pragma unroll
-  for (int i = 0; i < 4; ++i) {
-    const int m = m0 + ty * 4 + i;
+  for (int i = 0; i < 2; ++i) {
+    const int m = m0 + ty * 2 + i;
     if (m >= g.M) continue;
 #pragma unroll
-    for (int j = 0; j < 4; ++j) {
-      const int n = n0 + tx * 4 + j;
+    for (int j = 0; j < 2; ++j) {
+      const int n = n0 + tx * 2 + j;
       if (n >= g.N) continue;
       float val = acc[i][j];
       const long long ci = (long long)m * g.ldc + n;
@@ -177,19 +198,30 @@ __global__ void critic_dz2_kernel(int B, int H2, const float* __restrict__ dq,
   }
 }
 
-// column sums: out[z*obs_ + j] = sum_b M[z][b][j] (b ascending);  also used for dW3 = dQ^T H2
-__global__ void colsum_kernel(int B, int N, const float* __restrict__ M, long long m_bs,
-                              const float* __restrict__ wgt, long long w_bs, float* __restrict__ out,
-                              long long o_bs) {
+// column sums: out[z*o_bs + j] = sum_b w_b M[z][b][j]; also dW3 = dQ^T H2. Block = 32 columns x
+// 8 row-groups; each row-group sums a strided subset of b, then a fixed-order combine.
+__global__ void __launch_bounds__(256) colsum_kernel(int B, int N, const float* __restrict__ M, long long m_bs,
+                                                     const float* __restrict__ wgt, long long w_bs,
+                                                     float* __restrict__ out, long long o_bs) {
+  __shared__ float red[8][33];
   const int z = blockIdx.y;
-  const int j = blockIdx.x * blockDim.x + threadIdx.x;
-  if (j >= N) return;
+  const int jl = threadIdx.x & 31, rg = threadIdx.x >> 5;
+  const int j = blockIdx.x * 32 + jl;
   float s = 0.f;
-  for (int b = 0; b < B; ++b) {
-    const float m = M[z * m_bs + (size_t)b * N + j];
-    s = wgt ? __fmaf_rn(wgt[z * w_bs + b], m, s) : __fadd_rn(s, m);
+  if (j < N) {
+    for (int b = rg; b < B; b += 8) {
+      const float m = __ldg(M + z * m_bs + (size_t)b * N + j);
+      s = wgt ? __fmaf_rn(__ldg(wgt + z * w_bs + b), m, s) : __fadd_rn(s, m);
+    }
   }
-  out[z * o_bs + j] = s;
+  red[rg][jl] = s;
+  __syncthreads();
+  if (rg == 0 && j < N) {
+    float t = red[0][jl];
+#pragma unroll
+    for (int r = 1; r < 8; ++r) t = __fadd_rn(t, red[r][jl]);
+    out[z * o_bs + j] = t;
+  }
 }
 
 // db3[z] = sum_b dQ[z][b]
@@ -323,7 +355,7 @@ int critic_fwd_bwd(const CriticDims& c, int B, const float* params2, const __nv_
   }
   if (want_params) {
     // dW3 = dQ^T H2, db3 = sum dQ
-    colsum_kernel<<<dim3(cdiv(H2, 128), nz), 128, 0, st>>>(B, H2, w.H2, (long long)B * H2, w.dq, B,
+    colsum_kernel<<<dim3(cdiv(H2, 32), nz), 256, 0, st>>>(B, H2, w.H2, (long long)B * H2, w.dq, B,
                                                            grad2 + c.off[SPIKERL_CRITIC_W3], P);
     SPK_LAUNCHED();
     sum_dq_kernel<<<nz, 32, 0, st>>>(B, w.dq, grad2 + c.off[SPIKERL_CRITIC_B3], P);
@@ -337,7 +369,7 @@ int critic_fwd_bwd(const CriticDims& c, int B, const float* params2, const __nv_
       g.C = grad2 + c.off[SPIKERL_CRITIC_W2]; g.ldc = H1; g.c_bs = P;
       SPK_TRY(run_gemm<EPI_STORE>(g, nz, false, false, st));
     }
-    colsum_kernel<<<dim3(cdiv(H2, 128), nz), 128, 0, st>>>(B, H2, w.dZ2, (long long)B * H2, nullptr, 0,
+    colsum_kernel<<<dim3(cdiv(H2, 32), nz), 256, 0, st>>>(B, H2, w.dZ2, (long long)B * H2, nullptr, 0,
                                                            grad2 + c.off[SPIKERL_CRITIC_B2], P);
     SPK_LAUNCHED();
     // dW1 = dZ1^T X ; db1 = colsum dZ1
@@ -349,7 +381,7 @@ int critic_fwd_bwd(const CriticDims& c, int B, const float* params2, const __nv_
       g.C = grad2 + c.off[SPIKERL_CRITIC_W1]; g.ldc = in; g.c_bs = P;
       SPK_TRY(run_gemm<EPI_STORE>(g, nz, false, false, st));
     }
-    colsum_kernel<<<dim3(cdiv(H1, 128), nz), 128, 0, st>>>(B, H1, w.dZ1, (long long)B * H1, nullptr, 0,
+    colsum_kernel<<<dim3(cdiv(H1, 32), nz), 256, 0, st>>>(B, H1, w.dZ1, (long long)B * H1, nullptr, 0,
                                                            grad2 + c.off[SPIKERL_CRITIC_B1], P);
     SPK_LAUNCHED();
   }

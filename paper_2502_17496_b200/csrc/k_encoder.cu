@@ -32,12 +32,18 @@ __global__ void __launch_bounds__(128) enc_fwd_kernel(int B, int S, int E, int K
   }
   float acc = 0.0f;
   const size_t word = (size_t)b * W0 + (k >> 5);
+  // lane (t mod 32) keeps the ballot word of timestep t; one store instruction per 32 steps
+  uint32_t mine = 0;
   for (int t = 0; t < T; ++t) {
     acc = __fadd_rn(acc, A);
     const bool fire = acc >= 1.0f;
     if (fire) acc = __fsub_rn(acc, 1.0f);
     const uint32_t w = __ballot_sync(0xffffffffu, fire);
-    if (lane == 0) bits0[(size_t)t * B * W0 + word] = w;
+    if (lane == (t & 31)) mine = w;
+    if ((t & 31) == 31 || t == T - 1) {
+      const int tb = t & ~31;
+      if (lane <= (t & 31)) bits0[(size_t)(tb + lane) * B * W0 + word] = mine;
+    }
   }
 }
 

@@ -7,12 +7,13 @@
 //   ENC  dL/dA = (sum_t G_1) W_1            -> dmu, dsigma partial sums over the tile's rows
 //                                                          DESIGN.md R6 (straight-through encoder)
 //   DW   dW_l = sum_{t,b} G_l^T o_{l-1}     -> deterministic split-K fp32 partials
-// One persistent, warp-specialised kernel (1 CTA/SM, 320 threads):
+// One persistent, warp-specialised kernel (1 CTA/SM, 448 threads):
 //   warp 0      TMA producer (A tiles; B tiles when they are bf16 tensors)
 //   warp 1      TMEM allocator + single-thread tcgen05.mma issuer (M=128, N<=256, K=16 steps)
 //   warps 2-5   spike-bit expanders: u32 spike words -> bf16 {0,1} tiles in the 128B-swizzled
 //               UMMA layout (K-major for FWD, MN-major for DW)
-//   warps 6-9   epilogue: tcgen05.ld (32x32b) of the TMEM accumulator, one thread per neuron
+//   warps 6-13  epilogue, 2 groups x 4 warps: tcgen05.ld (32x32b) of the TMEM accumulator, one
+//               thread per neuron, each group owning half of the tile's columns
 // Pipelines: 4-stage smem ring (full/empty mbarriers), 2-stage TMEM accumulator (2 x 256 cols).
 // Neurons sit on TMEM lanes (MMA M) and (t,b) on columns (MMA N) with t-major order, so a
 // thread owns every timestep of its neuron: the LIF scans never leave registers, and one
@@ -30,9 +31,9 @@ constexpr int BM = 128, BK = 64, STAGES = 4;
 constexpr int A_STAGE = BM * BK * 2;             // 16 KB
 constexpr int B_STAGE = 256 * BK * 2;            // 32 KB
 constexpr int STAGE_BYTES = A_STAGE + B_STAGE;   // 48 KB
-constexpr int NUM_EXP_WARPS = 4, NUM_EPI_WARPS = 4;
+constexpr int NUM_EXP_WARPS = 4, NUM_EPI_WARPS = 8;
 constexpr int EXP_WARP0 = 2, EPI_WARP0 = 2 + NUM_EXP_WARPS;
-constexpr int NUM_THREADS = (EPI_WARP0 + NUM_EPI_WARPS) * 32;  // 320
+constexpr int NUM_THREADS = (EPI_WARP0 + NUM_EPI_WARPS) * 32;  // 448
 constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + 1024 + 256;
 constexpr int TMEM_COLS = 512;
 constexpr int DW_BN = 256;
@@ -173,6 +174,9 @@ __device__ __forceinline__ Tile decode(const Params& p, int u) {
 }
 
 // ------------------------------------------------------------------------- the kernel
+// Expander prefetch depth (k-blocks of spike words kept in registers ahead of the smem ring).
+constexpr int PF = 4;
+
 template <int MODE, int BT>
 __global__ void __launch_bounds__(NUM_THREADS, 1)
     tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, const Params p) {
@@ -261,57 +265,116 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     }
   } else if (warp < EPI_WARP0) {
     // ===================== spike-bit expanders =====================
+    // Each thread owns fixed rows of the B tile for the whole unit and keeps the spike words of
+    // the next PF k-blocks in registers, so global-load latency overlaps the smem ring.
     if (B_EXPAND) {
       const int et = threadIdx.x - EXP_WARP0 * 32;
       uint32_t it = 0;
       for (int u = blockIdx.x; u < p.n_units; u += gridDim.x) {
         const Tile t = decode<MODE>(p, u);
-        for (int kb = t.kb0; kb < t.kb1; ++kb, ++it) {
-          const int stage = it % STAGES;
-          const uint32_t ph = (it / STAGES) & 1;
-          mbar_wait(&empty[stage], ph ^ 1);
-          const uint32_t sB = smem_u32(smem + stage * STAGE_BYTES + A_STAGE);
-          if (MODE == FWD) {
-            // K-major: row = t*Bt + j (one (t,b) spike row), 64 k = 2 words = 8 chunks of 16 B
-            const int rows = p.T * p.Bt;
-            for (int idx = et; idx < rows * 2; idx += NUM_EXP_WARPS * 32) {
-              const int row = idx >> 1, half = idx & 1;
-              const int tt = row / p.Bt, j = row - tt * p.Bt;
-              const int b = t.n * p.Bt + j;
-              const uint32_t w = (b < p.B) ? __ldg(p.bits_in + ((size_t)tt * p.B + b) * p.w_in + kb * 2 + half) : 0u;
+        if (MODE == FWD) {
+          // K-major: row = t*Bt + j (spike row (t, b)), one k-block = 2 words = 8 chunks of 16 B
+          const int rows = p.T * p.Bt;
+          const uint32_t* rp[2];
+          bool rv[2];
 #pragma unroll
-              for (int c = 0; c < 4; ++c) {
-                const int chunk = half * 4 + c;
-                st_shared_v4(sB + row * 128 + ((chunk ^ (row & 7)) << 4), expand_byte((w >> (8 * c)) & 0xFFu));
-              }
-            }
-          } else {
-            // MN-major: K row r (one (t,b)), 256 output columns k = 4 atoms x 64 = 8 words
-            const int r0 = kb * BK;
-            const int wbase = t.n * (DW_BN / 32);
-            for (int idx = et; idx < BK * 8; idx += NUM_EXP_WARPS * 32) {
-              const int r = idx >> 3, wi = idx & 7;
-              const int rg = r0 + r;
-              const int wcol = wbase + wi;
-              const uint32_t w = (rg < p.R && wcol < p.w_dw) ? __ldg(p.bits_dw + (size_t)rg * p.w_dw + wcol) : 0u;
-              const int atom = wi >> 1, half = wi & 1;
-#pragma unroll
-              for (int c = 0; c < 4; ++c) {
-                const int chunk = half * 4 + c;
-                st_shared_v4(sB + atom * 8192 + r * 128 + ((chunk ^ (r & 7)) << 4),
-                             expand_byte((w >> (8 * c)) & 0xFFu));
-              }
-            }
+          for (int i = 0; i < 2; ++i) {
+            const int row = et + 128 * i;
+            const int tt = row / p.Bt, j = row - tt * p.Bt;
+            const int b = t.n * p.Bt + j;
+            rv[i] = row < rows && b < p.B;
+            rp[i] = rv[i] ? p.bits_in + ((size_t)tt * p.B + b) * p.w_in : p.bits_in;
           }
-          fence_proxy_async();
-          __syncwarp();
-          if (lane == 0) mbar_arrive(&full[stage]);
+          uint2 q[PF][2];
+#pragma unroll
+          for (int f = 0; f < PF; ++f)
+#pragma unroll
+            for (int i = 0; i < 2; ++i) {
+              const int kb = t.kb0 + f;
+              q[f][i] = (rv[i] && kb < t.kb1) ? __ldg(reinterpret_cast<const uint2*>(rp[i] + 2 * kb)) : make_uint2(0u, 0u);
+            }
+          for (int kb = t.kb0; kb < t.kb1; ++kb, ++it) {
+            const int stage = it % STAGES;
+            const uint32_t ph = (it / STAGES) & 1;
+            mbar_wait(&empty[stage], ph ^ 1);
+            const uint32_t sB = smem_u32(smem + stage * STAGE_BYTES + A_STAGE);
+#pragma unroll
+            for (int i = 0; i < 2; ++i) {
+              const int row = et + 128 * i;
+              if (row < rows) {
+                const uint32_t base = sB + row * 128;
+                const uint32_t sw = row & 7;
+#pragma unroll
+                for (int c = 0; c < 8; ++c) {
+                  const uint32_t w = c < 4 ? q[0][i].x : q[0][i].y;
+                  st_shared_v4(base + ((c ^ sw) << 4), expand_byte((w >> (8 * (c & 3))) & 0xFFu));
+                }
+              }
+            }
+#pragma unroll
+            for (int f = 0; f < PF - 1; ++f) { q[f][0] = q[f + 1][0]; q[f][1] = q[f + 1][1]; }
+#pragma unroll
+            for (int i = 0; i < 2; ++i) {
+              const int kn = kb + PF;
+              q[PF - 1][i] = (rv[i] && kn < t.kb1) ? __ldg(reinterpret_cast<const uint2*>(rp[i] + 2 * kn))
+                                                  : make_uint2(0u, 0u);
+            }
+            fence_proxy_async();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&full[stage]);
+          }
+        } else {
+          // MN-major: K row r = one (t,b) row, 256 output columns = 8 words; thread = (row, half)
+          const int r = et >> 1, half = et & 1;
+          const int wcol = t.n * (DW_BN / 32) + 4 * half;
+          const bool cv = wcol < p.w_dw;
+          uint4 q[PF];
+#pragma unroll
+          for (int f = 0; f < PF; ++f) {
+            const int kb = t.kb0 + f;
+            const int rg = kb * BK + r;
+            q[f] = (cv && kb < t.kb1 && rg < p.R)
+                       ? __ldg(reinterpret_cast<const uint4*>(p.bits_dw + (size_t)rg * p.w_dw + wcol))
+                       : make_uint4(0u, 0u, 0u, 0u);
+          }
+          for (int kb = t.kb0; kb < t.kb1; ++kb, ++it) {
+            const int stage = it % STAGES;
+            const uint32_t ph = (it / STAGES) & 1;
+            mbar_wait(&empty[stage], ph ^ 1);
+            const uint32_t sB = smem_u32(smem + stage * STAGE_BYTES + A_STAGE);
+            const uint32_t sw = r & 7;
+            const uint32_t w4[4] = {q[0].x, q[0].y, q[0].z, q[0].w};
+#pragma unroll
+            for (int wi = 0; wi < 4; ++wi) {
+              const int atom = 2 * half + (wi >> 1), hw = wi & 1;
+              const uint32_t base = sB + atom * 8192 + r * 128;
+#pragma unroll
+              for (int c = 0; c < 4; ++c) {
+                const int chunk = hw * 4 + c;
+                st_shared_v4(base + ((chunk ^ sw) << 4), expand_byte((w4[wi] >> (8 * c)) & 0xFFu));
+              }
+            }
+#pragma unroll
+            for (int f = 0; f < PF - 1; ++f) q[f] = q[f + 1];
+            {
+              const int kn = kb + PF;
+              const int rg = kn * BK + r;
+              q[PF - 1] = (cv && kn < t.kb1 && rg < p.R)
+                              ? __ldg(reinterpret_cast<const uint4*>(p.bits_dw + (size_t)rg * p.w_dw + wcol))
+                              : make_uint4(0u, 0u, 0u, 0u);
+            }
+            fence_proxy_async();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&full[stage]);
+          }
         }
       }
     }
   } else {
-    // ===================== epilogue =====================
+    // ===================== epilogue (2 groups x 4 warps) =====================
+    // group g handles half of the tile's columns; warp%4 selects the TMEM lane quarter.
     const int q = warp & 3;
+    const int g = (warp - EPI_WARP0) >> 2;
     uint32_t titer = 0;
     for (int u = blockIdx.x; u < p.n_units; u += gridDim.x, ++titer) {
       const Tile t = decode<MODE>(p, u);
@@ -321,126 +384,155 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       const uint32_t taddr = tmem + ((uint32_t)(32 * q) << 16) + a * 256;
       const int row = t.m * BM + 32 * q + lane;  // neuron index (M)
       if (MODE == FWD) {
-        const bool valid = row < p.n_valid;
-        const int b0 = t.n * BT;
-        float c[BT], v[BT];
-        int cnt[BT];
-        uint64_t oprev = 0;
+        constexpr int HB = BT >= 16 ? BT / 2 : BT;  // batch rows per group
+        if (BT >= 16 || g == 0) {
+          const int jb = BT >= 16 ? g * HB : 0;
+          const bool valid = row < p.n_valid;
+          const int b0 = t.n * BT + jb;
+          float c[HB], v[HB];
+          int cnt[HB];
+          uint32_t oprev = 0;
 #pragma unroll
-        for (int j = 0; j < BT; ++j) { c[j] = 0.f; v[j] = 0.f; cnt[j] = 0; }
-        const size_t wcol = (size_t)(t.m * BM + 32 * q) >> 5;
-        for (int tt = 0; tt < p.T; ++tt) {
+          for (int j = 0; j < HB; ++j) { c[j] = 0.f; v[j] = 0.f; cnt[j] = 0; }
+          const size_t wcol = (size_t)(t.m * BM + 32 * q) >> 5;
+          for (int tt = 0; tt < p.T; ++tt) {
 #pragma unroll
-          for (int j0 = 0; j0 < BT; j0 += 8) {
-            uint32_t r[8];
-            tmem_ld8(taddr + tt * BT + j0, r);
-            tmem_ld_wait();
-            uint32_t wo = 0, wh = 0;
+            for (int j0 = 0; j0 < HB; j0 += 8) {
+              uint32_t r[8];
+              tmem_ld8(taddr + tt * BT + jb + j0, r);
+              tmem_ld_wait();
+              uint32_t wo = 0, wh = 0;
 #pragma unroll
-            for (int jj = 0; jj < 8; ++jj) {
-              const int j = j0 + jj;
-              bool o = (oprev >> j) & 1ull, h;
-              lif_step(p.kc, __uint_as_float(r[jj]), c[j], v[j], o, h);
-              if (!valid) { o = false; h = false; }
-              oprev = o ? (oprev | (1ull << j)) : (oprev & ~(1ull << j));
-              cnt[j] += o ? 1 : 0;
-              const uint32_t ob = __ballot_sync(0xffffffffu, o), hb = __ballot_sync(0xffffffffu, h);
-              if (lane == jj) { wo = ob; wh = hb; }
-            }
-            const int b = b0 + j0 + lane;
-            if (lane < 8 && b < p.B) {
-              const size_t wi = ((size_t)tt * p.B + b) * p.w_out + wcol;
-              p.bits_out[wi] = wo;
-              p.mask_out[wi] = wh;
+              for (int jj = 0; jj < 8; ++jj) {
+                const int j = j0 + jj;
+                bool o = (oprev >> j) & 1u, h;
+                lif_step(p.kc, __uint_as_float(r[jj]), c[j], v[j], o, h);
+                if (!valid) { o = false; h = false; }
+                oprev = o ? (oprev | (1u << j)) : (oprev & ~(1u << j));
+                cnt[j] += o ? 1 : 0;
+                const uint32_t ob = __ballot_sync(0xffffffffu, o), hb = __ballot_sync(0xffffffffu, h);
+                if (lane == jj) { wo = ob; wh = hb; }
+              }
+              const int b = b0 + j0 + lane;
+              if (lane < 8 && b < p.B) {
+                const size_t wi = ((size_t)tt * p.B + b) * p.w_out + wcol;
+                p.bits_out[wi] = wo;
+                p.mask_out[wi] = wh;
+              }
             }
           }
-        }
-        if (p.counts && row < p.n3) {
+          if (p.counts && row < p.n3) {
 #pragma unroll
-          for (int j = 0; j < BT; ++j) {
-            const int b = b0 + j;
-            if (b < p.B) p.counts[(size_t)b * p.n3 + row] = (uint8_t)cnt[j];
+            for (int j = 0; j < HB; ++j) {
+              const int b = b0 + j;
+              if (b < p.B) p.counts[(size_t)b * p.n3 + row] = (uint8_t)cnt[j];
+            }
           }
         }
       } else if (MODE == DX) {
-        const bool valid = row < p.n_valid;
-        const int b0 = t.n * BT;
-        float dvn[BT], dcn[BT], gs[BT];
+        constexpr int HB = BT >= 16 ? BT / 2 : BT;
+        if (BT >= 16 || g == 0) {
+          const int jb = BT >= 16 ? g * HB : 0;
+          const bool valid = row < p.n_valid;
+          const int b0 = t.n * BT + jb;
+          float dvn[HB], dcn[HB], gs[HB];
 #pragma unroll
-        for (int j = 0; j < BT; ++j) { dvn[j] = 0.f; dcn[j] = 0.f; gs[j] = 0.f; }
-        const size_t wcol = (size_t)(t.m * BM + 32 * q) >> 5;
-        for (int tt = p.T - 1; tt >= 0; --tt) {
-          uint32_t ow0 = 0, hw0 = 0, ow1 = 0, hw1 = 0;
-          if (lane < BT && b0 + lane < p.B) {
-            const size_t wi = ((size_t)tt * p.B + b0 + lane) * p.w_prev + wcol;
-            ow0 = __ldg(p.bits_prev + wi);
-            hw0 = __ldg(p.mask_prev + wi);
+          for (int j = 0; j < HB; ++j) { dvn[j] = 0.f; dcn[j] = 0.f; gs[j] = 0.f; }
+          const size_t wcol = (size_t)(t.m * BM + 32 * q) >> 5;
+          // lane j < HB fetches the spike / mask words of row (t, b0 + j); a ring of PFD timesteps
+          // is kept in flight so the global-load latency hides behind the scan of earlier steps
+          constexpr int PFD = 4;
+          uint32_t ro[PFD], rh[PFD];
+          const bool lane_row = lane < HB && b0 + lane < p.B;
+          auto fetch = [&](int tt, uint32_t& o_, uint32_t& h_) {
+            if (tt >= 0 && lane_row) {
+              const size_t wi = ((size_t)tt * p.B + b0 + lane) * p.w_prev + wcol;
+              o_ = __ldg(p.bits_prev + wi);
+              h_ = __ldg(p.mask_prev + wi);
+            } else {
+              o_ = 0u; h_ = 0u;
+            }
+          };
+#pragma unroll
+          for (int f = 0; f < PFD; ++f) fetch(p.T - 1 - f, ro[f], rh[f]);
+          for (int tt = p.T - 1; tt >= 0; --tt) {
+            const uint32_t ow0 = ro[0], hw0 = rh[0];
+#pragma unroll
+            for (int f = 0; f < PFD - 1; ++f) { ro[f] = ro[f + 1]; rh[f] = rh[f + 1]; }
+            fetch(tt - PFD, ro[PFD - 1], rh[PFD - 1]);
+#pragma unroll
+            for (int j0 = 0; j0 < HB; j0 += 8) {
+              uint32_t r[8];
+              tmem_ld8(taddr + tt * BT + jb + j0, r);
+              tmem_ld_wait();
+#pragma unroll
+              for (int jj = 0; jj < 8; ++jj) {
+                const int j = j0 + jj;
+                const uint32_t ow = __shfl_sync(0xffffffffu, ow0, j);
+                const uint32_t hw = __shfl_sync(0xffffffffu, hw0, j);
+                const bool o = (ow >> lane) & 1u, h = (hw >> lane) & 1u;
+                float G = lif_back_step(p.zh, p.kc.dv, p.kc.dc, __uint_as_float(r[jj]), o, h, dvn[j], dcn[j]);
+                if (!valid) G = 0.f;
+                gs[j] = __fadd_rn(gs[j], G);
+                const int b = b0 + j;
+                if (b < p.B) p.g_prev[((size_t)tt * p.B + b) * p.p_prev + row] = __float2bfloat16_rn(G);
+              }
+            }
           }
-          if (BT > 32 && lane + 32 < BT && b0 + lane + 32 < p.B) {
-            const size_t wi = ((size_t)tt * p.B + b0 + lane + 32) * p.w_prev + wcol;
-            ow1 = __ldg(p.bits_prev + wi);
-            hw1 = __ldg(p.mask_prev + wi);
-          }
+          if (p.g_sum) {
 #pragma unroll
-          for (int j0 = 0; j0 < BT; j0 += 8) {
-            uint32_t r[8];
-            tmem_ld8(taddr + tt * BT + j0, r);
-            tmem_ld_wait();
-#pragma unroll
-            for (int jj = 0; jj < 8; ++jj) {
-              const int j = j0 + jj;
-              const uint32_t ow = __shfl_sync(0xffffffffu, j < 32 ? ow0 : ow1, j & 31);
-              const uint32_t hw = __shfl_sync(0xffffffffu, j < 32 ? hw0 : hw1, j & 31);
-              const bool o = (ow >> lane) & 1u, h = (hw >> lane) & 1u;
-              float G = lif_back_step(p.zh, p.kc.dv, p.kc.dc, __uint_as_float(r[jj]), o, h, dvn[j], dcn[j]);
-              if (!valid) G = 0.f;
-              gs[j] = __fadd_rn(gs[j], G);
+            for (int j = 0; j < HB; ++j) {
               const int b = b0 + j;
-              if (b < p.B) p.g_prev[((size_t)tt * p.B + b) * p.p_prev + row] = __float2bfloat16_rn(G);
+              if (b < p.B) p.g_sum[(size_t)b * p.p_prev + row] = __float2bfloat16_rn(gs[j]);
             }
           }
         }
-        if (p.g_sum) {
-#pragma unroll
-          for (int j = 0; j < BT; ++j) {
-            const int b = b0 + j;
-            if (b < p.B) p.g_sum[(size_t)b * p.p_prev + row] = __float2bfloat16_rn(gs[j]);
-          }
-        }
       } else if (MODE == ENC) {
+        // dmu_k = (1/sigma^2) sum_b gA A (s - mu); dsigma_k = (1/sigma^3) sum_b gA A (s - mu)^2
         const bool valid = row < p.K0;
-        const float m = valid ? p.mu[row] : 0.f, sg = valid ? p.sigma[row] : 1.f;
-        const float sg2 = __fmul_rn(sg, sg), sg3 = __fmul_rn(sg2, sg);
-        const int i = valid ? row / p.E : 0;
+        const int rr = valid ? row : 0;
+        const float m = p.mu[rr];
+        const int i = rr / p.E;
+        const int half = p.BN >> 1;
+        const int c0 = g * half;
         float pm = 0.f, ps = 0.f;
-        for (int j0 = 0; j0 < p.BN; j0 += 8) {
+        for (int j0 = 0; j0 < half; j0 += 8) {
           uint32_t r[8];
-          tmem_ld8(taddr + j0, r);
+          tmem_ld8(taddr + c0 + j0, r);
+          float av[8], sv[8];
+#pragma unroll
+          for (int jj = 0; jj < 8; ++jj) {
+            const int b = t.n * p.BN + c0 + j0 + jj;
+            const int bb = b < p.B ? b : 0;
+            av[jj] = __ldg(p.A + (size_t)bb * p.K0 + rr);
+            sv[jj] = __ldg(p.obs + (size_t)bb * p.S + i);
+          }
           tmem_ld_wait();
 #pragma unroll
           for (int jj = 0; jj < 8; ++jj) {
-            const int b = t.n * p.BN + j0 + jj;
-            if (valid && b < p.B) {
-              const float gA = __uint_as_float(r[jj]);
-              const float av = __ldg(p.A + (size_t)b * p.K0 + row);
-              const float dd = __fsub_rn(__ldg(p.obs + (size_t)b * p.S + i), m);
-              const float ga = __fmul_rn(gA, av);
-              pm = __fadd_rn(pm, __fdiv_rn(__fmul_rn(ga, dd), sg2));
-              ps = __fadd_rn(ps, __fdiv_rn(__fmul_rn(ga, __fmul_rn(dd, dd)), sg3));
+            const int b = t.n * p.BN + c0 + j0 + jj;
+            if (b < p.B) {
+              const float dd = __fsub_rn(sv[jj], m);
+              const float gad = __fmul_rn(__fmul_rn(__uint_as_float(r[jj]), av[jj]), dd);
+              pm = __fadd_rn(pm, gad);
+              ps = __fadd_rn(ps, __fmul_rn(gad, dd));
             }
           }
         }
         if (valid) {
-          p.partial[((size_t)t.n * p.K0 + row) * 2 + 0] = pm;
-          p.partial[((size_t)t.n * p.K0 + row) * 2 + 1] = ps;
+          const float sg = p.sigma[row];
+          const float sg2 = __fmul_rn(sg, sg), sg3 = __fmul_rn(sg2, sg);
+          p.partial[(((size_t)t.n * 2 + g) * p.K0 + row) * 2 + 0] = __fdiv_rn(pm, sg2);
+          p.partial[(((size_t)t.n * 2 + g) * p.K0 + row) * 2 + 1] = __fdiv_rn(ps, sg3);
         }
-      } else {  // DW
-        float* dst = p.dw_part + (size_t)t.split * p.split_stride + (size_t)row * p.ldp + t.n * DW_BN;
-        for (int j0 = 0; j0 < DW_BN; j0 += 8) {
-          uint32_t r[8];
-          tmem_ld8(taddr + j0, r);
-          tmem_ld_wait();
-          if (t.n * DW_BN + j0 < p.ldp) {
+      } else {  // DW: group g writes columns [128 g, 128 g + 128)
+        const int c0 = g * (DW_BN / 2);
+        float* dst = p.dw_part + (size_t)t.split * p.split_stride + (size_t)row * p.ldp + t.n * DW_BN + c0;
+        if (t.n * DW_BN + c0 < p.ldp) {
+          for (int j0 = 0; j0 < DW_BN / 2; j0 += 8) {
+            uint32_t r[8];
+            tmem_ld8(taddr + c0 + j0, r);
+            tmem_ld_wait();
             float4* d4 = reinterpret_cast<float4*>(dst + j0);
             d4[0] = make_float4(__uint_as_float(r[0]), __uint_as_float(r[1]), __uint_as_float(r[2]), __uint_as_float(r[3]));
             d4[1] = make_float4(__uint_as_float(r[4]), __uint_as_float(r[5]), __uint_as_float(r[6]), __uint_as_float(r[7]));
@@ -538,19 +630,18 @@ static int launch_bt(int bt, const CUtensorMap& ma, const CUtensorMap& mb, const
   switch (bt) {
     case 8: return launch<MODE, 8>(ma, mb, p, st);
     case 16: return launch<MODE, 16>(ma, mb, p, st);
-    case 24: return launch<MODE, 24>(ma, mb, p, st);
     case 32: if (MODE == FWD) return launch<MODE, 32>(ma, mb, p, st); break;
   }
   set_error("unsupported batch tile %d", bt);
   return SPIKERL_E_UNSUPPORTED;
 }
 
-// batch rows per N tile: Bt % 8 == 0, T*Bt % 16 == 0, T*Bt <= 256, Bt <= max_bt (register budget:
-// FWD keeps c, v per row, DX keeps dv, dc, sum per row); prefer the largest Bt that still gives >= one
-// wave of tiles, else the smallest valid one.
+// batch rows per N tile: Bt in {8, 16, 32}, T*Bt % 16 == 0, T*Bt <= 256, Bt <= max_bt (register
+// budget: each epilogue group keeps Bt/2 rows of LIF state); prefer the largest Bt that still gives
+// >= one wave of tiles, else the smallest valid one.
 static int choose_bt(int T, int B, int m_tiles, int max_bt) {
   int best = 0, smallest = 0;
-  for (int bt = 8; bt <= max_bt; bt += 8) {
+  for (int bt = 8; bt <= max_bt; bt *= 2) {
     if ((T * bt) % 16 != 0 || T * bt > 256) continue;
     if (!smallest) smallest = bt;
     const long long tiles = (long long)m_tiles * ((B + bt - 1) / bt);
@@ -559,7 +650,7 @@ static int choose_bt(int T, int B, int m_tiles, int max_bt) {
   return best ? best : smallest;
 }
 
-constexpr int FWD_MAX_BT = 32, DX_MAX_BT = 24;
+constexpr int FWD_MAX_BT = 32, DX_MAX_BT = 16;
 
 }  // namespace tc
 
@@ -567,7 +658,7 @@ using namespace tc;
 
 bool tc_supported(const ActorDims& d) {
   if (!d.bf16) return false;
-  for (int bt = 8; bt <= DX_MAX_BT; bt += 8)
+  for (int bt = 8; bt <= DX_MAX_BT; bt *= 2)
     if ((d.T * bt) % 16 == 0 && d.T * bt <= 256) return true;
   return false;
 }
@@ -633,7 +724,7 @@ int launch_lif_dx_tc(const ActorDims& d, int l, int B, const void* Gl, const __n
 
 size_t tc_enc_partial_bytes(const ActorDims& d, int B) {
   const int BN = B >= 256 ? 256 : round_up(B, 16);
-  return sizeof(float) * 2 * (size_t)cdiv(B, BN) * d.K0;
+  return sizeof(float) * 2 * 2 * (size_t)cdiv(B, BN) * d.K0;   // 2 epilogue groups per N tile
 }
 
 int launch_enc_grad_tc(const ActorDims& d, int B, const void* Gsum, const __nv_bfloat16* W1b16, const float* A,
@@ -662,17 +753,28 @@ int launch_enc_grad_tc(const ActorDims& d, int B, const void* Gsum, const __nv_b
     SPK_TRY(make_map(&mb, Gsum, 2, dims, strides, box));
   }
   SPK_TRY(launch_bt<ENC>(8, ma, mb, p, st));
-  return launch_enc_grad_reduce(d, p.n_tiles, partial, dmu, dsigma, accumulate, st);
+  return launch_enc_grad_reduce(d, 2 * p.n_tiles, partial, dmu, dsigma, accumulate, st);
 }
 
-// split-K plan for dW_l
+// split-K plan for dW_l: at least two waves of units, splits chosen to minimise the idle tail of
+// the last wave (persistent grid = #SMs); never an empty split.
 void tc_dw_plan(const ActorDims& d, int l, int B, int* splits, int* kps) {
   const int m_tiles = d.P[l] / BM, n_tiles = cdiv(d.P[l - 1], DW_BN);
   const int k_blocks = cdiv((long long)d.T * B, BK);
-  int s = cdiv(2LL * num_sms(), (long long)m_tiles * n_tiles);
-  if (s < 1) s = 1;
-  if (s > k_blocks) s = k_blocks;
-  const int per = cdiv(k_blocks, s);
+  const long long mn = (long long)m_tiles * n_tiles;
+  const int sms = num_sms();
+  int s_lo = (int)cdiv(2LL * sms, mn);
+  if (s_lo < 1) s_lo = 1;
+  int best_s = s_lo;
+  double best_eff = -1.0;
+  for (int s = s_lo; s <= 4 * s_lo && s <= k_blocks; ++s) {
+    const int per = cdiv(k_blocks, s), ss = cdiv(k_blocks, per);
+    const long long units = mn * ss;
+    const double eff = (double)units / ((double)cdiv(units, sms) * sms);
+    if (eff > best_eff + 1e-3) { best_eff = eff; best_s = s; }
+  }
+  if (best_s > k_blocks) best_s = k_blocks;
+  const int per = cdiv(k_blocks, best_s);
   *kps = per;
   *splits = cdiv(k_blocks, per);
 }
