@@ -130,10 +130,15 @@ size_t spikerl_td3_workspace_bytes(const spikerl_actor_cfg* acfg, const spikerl_
  *   bits_l u32  [T][B][Pl/32]  LIF spikes of layer l = 1, 2, 3
  *   mask_l u32  [T][B][Pl/32]  surrogate window bits [|v - v_th| < window], layer l = 1..3
  *   counts u8   [B][N3]        output spike counts
- *   act    fp32 [B][A]         decoded actions (for the decoder backward)              */
+ *   act    fp32 [B][A]         decoded actions (for the decoder backward)
+ *   bitsT_l, maskT_l u8 [ceil32(B)/8][P_l][tpad]  (tcgen05 engine, l = 1, 2; else offset 0)
+ *                              octet-major copies of the hidden planes: bit j of byte
+ *                              (o, n, t) is batch row 8o + j (read by the fused dX epilogue) */
 typedef struct {
   size_t A, bits[4], mask[4], counts, act, total;
   int padded[4];           /* P0..P3                                                        */
+  size_t bitsT[4], maskT[4];
+  int tpad;                /* T rounded up to 16                                            */
 } spikerl_tape_layout;
 int spikerl_actor_tape_layout(const spikerl_actor_cfg* cfg, int batch, spikerl_tape_layout* out);
 

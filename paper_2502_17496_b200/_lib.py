@@ -47,7 +47,8 @@ class TD3Cfg(C.Structure):
 class TapeLayout(C.Structure):
     _fields_ = [("A", C.c_size_t), ("bits", C.c_size_t * 4), ("mask", C.c_size_t * 4),
                 ("counts", C.c_size_t), ("act", C.c_size_t), ("total", C.c_size_t),
-                ("padded", C.c_int * 4)]
+                ("padded", C.c_int * 4), ("bitsT", C.c_size_t * 4), ("maskT", C.c_size_t * 4),
+                ("tpad", C.c_int)]
 
 
 class Tape(C.Structure):

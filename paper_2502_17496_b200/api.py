@@ -176,6 +176,11 @@ class SpikingActor:
             out[f"bits{l}"] = seg(lay.bits[l], 4 * T * B * W, torch.int32, (T, B, W))
             if l:
                 out[f"mask{l}"] = seg(lay.mask[l], 4 * T * B * W, torch.int32, (T, B, W))
+            if l and lay.bitsT[l]:
+                P = lay.padded[l]
+                O = (B + 31) // 32 * 4
+                out[f"bitsT{l}"] = seg(lay.bitsT[l], O * P * lay.tpad, torch.uint8, (O, P, lay.tpad))
+                out[f"maskT{l}"] = seg(lay.maskT[l], O * P * lay.tpad, torch.uint8, (O, P, lay.tpad))
         out["counts"] = seg(lay.counts, B * N3, torch.uint8, (B, N3))
         out["act"] = seg(lay.act, 4 * B * cfg.act_dim, torch.float32, (B, cfg.act_dim))
         return out

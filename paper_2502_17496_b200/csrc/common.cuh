@@ -62,6 +62,11 @@ unsigned long long actor_cfg_hash(const spikerl_actor_cfg* cfg);
 
 struct TapeLayout {
   size_t A, bits[4], mask[4], counts, act, total;
+  // neuron-major copies of the hidden layers' spike / mask planes (tcgen05 engine only):
+  // u8 [ceil32(B)/8][P_l][tpad]: byte (o, n, t) holds batch rows 8o..8o+7 of neuron n at step t;
+  // written by the forward epilogue, read by the DX epilogue
+  size_t bitsT[4], maskT[4];
+  int tpad;   // T rounded up to 16
 };
 TapeLayout tape_layout(const ActorDims& d, int B);
 

@@ -39,10 +39,11 @@ size_t enc_grad_partial_bytes(const ActorDims& d, int B);
 bool tc_supported(const ActorDims& d);
 int launch_lif_fwd_tc(const ActorDims& d, int l, int B, const uint32_t* bits_in,
                       const __nv_bfloat16* Wb16, uint32_t* bits_out, uint32_t* mask_out,
-                      uint8_t* counts, cudaStream_t st);
+                      uint8_t* counts, uint8_t* bitsT_out, uint8_t* maskT_out, int row_bytes,
+                      cudaStream_t st);
 int launch_lif_dx_tc(const ActorDims& d, int l, int B, const void* Gl, const __nv_bfloat16* Wb16,
-                     const uint32_t* bits_prev, const uint32_t* mask_prev, void* Gprev, void* Gsum,
-                     cudaStream_t st);
+                     const uint8_t* bitsT_prev, const uint8_t* maskT_prev, int row_bytes, void* Gprev,
+                     void* Gsum, cudaStream_t st);
 int launch_enc_grad_tc(const ActorDims& d, int B, const void* Gsum, const __nv_bfloat16* W1b16,
                        const float* A, const float* obs, const float* mu, const float* sigma,
                        float* partial, float* dmu, float* dsigma, int accumulate, cudaStream_t st);

@@ -44,9 +44,11 @@ struct Params {
   // FWD
   const uint32_t* bits_in; int w_in;
   uint32_t* bits_out; uint32_t* mask_out; int w_out; uint8_t* counts; int n_valid; int n3;
+  uint8_t* bitsT_out; uint8_t* maskT_out; int p_out;   // octet-major copies (may be null)
   LifConst kc; float zh;
+  int tpad;                                              // bytes per (octet, neuron) row = T rounded to 16
   // DX
-  const uint32_t* bits_prev; const uint32_t* mask_prev; int w_prev;
+  const uint8_t* bitsT_prev; const uint8_t* maskT_prev;
   __nv_bfloat16* g_prev; int p_prev; __nv_bfloat16* g_sum;
   // ENC
   const float* A; const float* obs; const float* mu; const float* sigma; float* partial; int K0, S, E;
@@ -150,6 +152,18 @@ __device__ __forceinline__ uint4 expand_byte(uint32_t byte) {
 __device__ __forceinline__ void st_shared_v4(uint32_t addr, uint4 v) {
   asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(addr), "r"(v.x), "r"(v.y), "r"(v.z), "r"(v.w)
                : "memory");
+}
+
+// 16-byte shift register: the newest byte enters at the top (byte 15)
+__device__ __forceinline__ void shift_in(uint32_t (&q)[4], uint32_t byte) {
+  q[0] = __funnelshift_r(q[0], q[1], 8);
+  q[1] = __funnelshift_r(q[1], q[2], 8);
+  q[2] = __funnelshift_r(q[2], q[3], 8);
+  q[3] = (q[3] >> 8) | (byte << 24);
+}
+__device__ __forceinline__ uint32_t byte_of(const uint4& q, int i) {
+  const uint32_t w = i < 8 ? (i < 4 ? q.x : q.y) : (i < 12 ? q.z : q.w);
+  return (w >> ((i & 3) * 8)) & 0xFFu;
 }
 
 struct Tile { int m, n, kb0, kb1, split; };
@@ -395,7 +409,17 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
 #pragma unroll
           for (int j = 0; j < HB; ++j) { c[j] = 0.f; v[j] = 0.f; cnt[j] = 0; }
           const size_t wcol = (size_t)(t.m * BM + 32 * q) >> 5;
+          // octet-major copy (DX epilogue input): per batch octet, the byte of step t is shifted
+          // into a 16-byte register window and written once per 16 steps (coalesced uint4)
+          constexpr int NOC = HB / 8;
+          const bool wT = p.bitsT_out != nullptr;
+          uint32_t qo[NOC][4], qh[NOC][4];
+#pragma unroll
+          for (int oc = 0; oc < NOC; ++oc)
+#pragma unroll
+            for (int i = 0; i < 4; ++i) { qo[oc][i] = 0u; qh[oc][i] = 0u; }
           for (int tt = 0; tt < p.T; ++tt) {
+            uint32_t hcur = 0;
 #pragma unroll
             for (int j0 = 0; j0 < HB; j0 += 8) {
               uint32_t r[8];
@@ -409,6 +433,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
                 lif_step(p.kc, __uint_as_float(r[jj]), c[j], v[j], o, h);
                 if (!valid) { o = false; h = false; }
                 oprev = o ? (oprev | (1u << j)) : (oprev & ~(1u << j));
+                hcur |= h ? (1u << j) : 0u;
                 cnt[j] += o ? 1 : 0;
                 const uint32_t ob = __ballot_sync(0xffffffffu, o), hb = __ballot_sync(0xffffffffu, h);
                 if (lane == jj) { wo = ob; wh = hb; }
@@ -420,6 +445,25 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
                 p.mask_out[wi] = wh;
               }
             }
+            if (wT) {
+#pragma unroll
+              for (int oc = 0; oc < NOC; ++oc) {
+                shift_in(qo[oc], (oprev >> (8 * oc)) & 0xFFu);
+                shift_in(qh[oc], (hcur >> (8 * oc)) & 0xFFu);
+              }
+              if ((tt & 15) == 15 || tt == p.T - 1) {
+                for (int k = (tt & 15) + 1; k < 16; ++k) {
+#pragma unroll
+                  for (int oc = 0; oc < NOC; ++oc) { shift_in(qo[oc], 0u); shift_in(qh[oc], 0u); }
+                }
+#pragma unroll
+                for (int oc = 0; oc < NOC; ++oc) {
+                  const size_t off = ((size_t)((b0 >> 3) + oc) * p.p_out + row) * p.tpad + (tt & ~15);
+                  *reinterpret_cast<uint4*>(p.bitsT_out + off) = make_uint4(qo[oc][0], qo[oc][1], qo[oc][2], qo[oc][3]);
+                  *reinterpret_cast<uint4*>(p.maskT_out + off) = make_uint4(qh[oc][0], qh[oc][1], qh[oc][2], qh[oc][3]);
+                }
+              }
+            }
           }
           if (p.counts && row < p.n3) {
 #pragma unroll
@@ -429,7 +473,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
             }
           }
         }
-      } else if (MODE == DX) {
+      } else if constexpr (MODE == DX) {
         constexpr int HB = BT >= 16 ? BT / 2 : BT;
         if (BT >= 16 || g == 0) {
           const int jb = BT >= 16 ? g * HB : 0;
@@ -438,28 +482,23 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
           float dvn[HB], dcn[HB], gs[HB];
 #pragma unroll
           for (int j = 0; j < HB; ++j) { dvn[j] = 0.f; dcn[j] = 0.f; gs[j] = 0.f; }
-          const size_t wcol = (size_t)(t.m * BM + 32 * q) >> 5;
-          // lane j < HB fetches the spike / mask words of row (t, b0 + j); a ring of PFD timesteps
-          // is kept in flight so the global-load latency hides behind the scan of earlier steps
-          constexpr int PFD = 4;
-          uint32_t ro[PFD], rh[PFD];
-          const bool lane_row = lane < HB && b0 + lane < p.B;
-          auto fetch = [&](int tt, uint32_t& o_, uint32_t& h_) {
-            if (tt >= 0 && lane_row) {
-              const size_t wi = ((size_t)tt * p.B + b0 + lane) * p.w_prev + wcol;
-              o_ = __ldg(p.bits_prev + wi);
-              h_ = __ldg(p.mask_prev + wi);
-            } else {
-              o_ = 0u; h_ = 0u;
-            }
-          };
-#pragma unroll
-          for (int f = 0; f < PFD; ++f) fetch(p.T - 1 - f, ro[f], rh[f]);
+          // this thread's own spike / mask bits for (t, b0..b0+7) come from the octet-major planes
+          // [B/8][P][Tpad] written by the forward epilogue: one coalesced uint4 per 16 steps
+          // (the next lower 16-step chunk is prefetched)
+          static_assert(HB == 8, "DX epilogue reads one batch octet per (t, neuron)");
+          const uint4* bT = reinterpret_cast<const uint4*>(p.bitsT_prev + ((size_t)(b0 >> 3) * p.p_prev + row) * p.tpad);
+          const uint4* mT = reinterpret_cast<const uint4*>(p.maskT_prev + ((size_t)(b0 >> 3) * p.p_prev + row) * p.tpad);
+          int ch = (p.T - 1) >> 4;
+          uint4 qo = __ldg(bT + ch), qh = __ldg(mT + ch);
+          uint4 nqo = ch > 0 ? __ldg(bT + ch - 1) : make_uint4(0u, 0u, 0u, 0u);
+          uint4 nqh = ch > 0 ? __ldg(mT + ch - 1) : make_uint4(0u, 0u, 0u, 0u);
           for (int tt = p.T - 1; tt >= 0; --tt) {
-            const uint32_t ow0 = ro[0], hw0 = rh[0];
-#pragma unroll
-            for (int f = 0; f < PFD - 1; ++f) { ro[f] = ro[f + 1]; rh[f] = rh[f + 1]; }
-            fetch(tt - PFD, ro[PFD - 1], rh[PFD - 1]);
+            if ((tt >> 4) != ch) {
+              ch = tt >> 4;
+              qo = nqo; qh = nqh;
+              if (ch > 0) { nqo = __ldg(bT + ch - 1); nqh = __ldg(mT + ch - 1); }
+            }
+            const uint32_t ow0 = byte_of(qo, tt & 15), hw0 = byte_of(qh, tt & 15);
 #pragma unroll
             for (int j0 = 0; j0 < HB; j0 += 8) {
               uint32_t r[8];
@@ -468,9 +507,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
 #pragma unroll
               for (int jj = 0; jj < 8; ++jj) {
                 const int j = j0 + jj;
-                const uint32_t ow = __shfl_sync(0xffffffffu, ow0, j);
-                const uint32_t hw = __shfl_sync(0xffffffffu, hw0, j);
-                const bool o = (ow >> lane) & 1u, h = (hw >> lane) & 1u;
+                const bool o = (ow0 >> j) & 1u, h = (hw0 >> j) & 1u;
                 float G = lif_back_step(p.zh, p.kc.dv, p.kc.dc, __uint_as_float(r[jj]), o, h, dvn[j], dcn[j]);
                 if (!valid) G = 0.f;
                 gs[j] = __fadd_rn(gs[j], G);
@@ -552,6 +589,44 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
   }
 }
 
+// Bit-plane transpose [T][B][P/32] (word = 32 neurons of one (t,b)) -> [T][ceil(B/32)][P]
+// (word = 32 batch rows of one (t, neuron)): one warp per 32x32 bit block, 32 ballots; loads hit
+// one word per batch row, stores are 128 B coalesced. Feeds the DX epilogue's per-neuron bits.
+// One block per (t, 32-row batch chunk): the 32 x W word tile is read coalesced into shared
+// memory, then each warp transposes 32x32 bit blocks with ballots and writes 128 B rows.
+constexpr int TR_MAXW = 64;  // P <= 2048 (hidden layers)
+__global__ void __launch_bounds__(256) bits_transpose_kernel(int T, int B, int P, const uint32_t* __restrict__ in,
+                                                              uint32_t* __restrict__ out) {
+  __shared__ uint32_t s[32][TR_MAXW + 1];
+  const int W = P >> 5, BW = (B + 31) >> 5;
+  const int bw = blockIdx.x % BW, t = blockIdx.x / BW;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  for (int i = threadIdx.x; i < 32 * W; i += 256) {
+    const int r = i / W, c = i - r * W;
+    const int b = bw * 32 + r;
+    s[r][c] = b < B ? __ldg(in + ((size_t)t * B + b) * W + c) : 0u;
+  }
+  __syncthreads();
+  for (int w = warp; w < W; w += 8) {
+    const uint32_t x = s[lane][w];
+    uint32_t mine = 0;
+#pragma unroll
+    for (int n = 0; n < 32; ++n) {
+      const uint32_t r = __ballot_sync(0xffffffffu, (x >> n) & 1u);
+      if (lane == n) mine = r;
+    }
+    out[((size_t)t * BW + bw) * P + w * 32 + lane] = mine;
+  }
+}
+
+int launch_bits_transpose(int T, int B, int P, const uint32_t* in, uint32_t* out, cudaStream_t st) {
+  ProfScope ps_("bits_transpose", PB_HBM, 0.0, 8.0 * T * (double)B * (P / 32), st);
+  if (P / 32 > TR_MAXW) { set_error("bits_transpose: width %d too large", P); return SPIKERL_E_UNSUPPORTED; }
+  bits_transpose_kernel<<<(unsigned)(T * ((B + 31) / 32)), 256, 0, st>>>(T, B, P, in, out);
+  SPK_LAUNCHED();
+  return SPIKERL_OK;
+}
+
 // dW[n][k] (master layout) = sum over splits (fixed order) of the partial tiles
 __global__ void dw_reduce_kernel(const float* __restrict__ part, int splits, long long split_stride, int ldp,
                                  int N, int K, float* __restrict__ dW, int accum) {
@@ -630,7 +705,9 @@ static int launch_bt(int bt, const CUtensorMap& ma, const CUtensorMap& mb, const
   switch (bt) {
     case 8: return launch<MODE, 8>(ma, mb, p, st);
     case 16: return launch<MODE, 16>(ma, mb, p, st);
-    case 32: if (MODE == FWD) return launch<MODE, 32>(ma, mb, p, st); break;
+    case 32:
+      if constexpr (MODE == FWD) return launch<MODE, 32>(ma, mb, p, st);
+      break;
   }
   set_error("unsupported batch tile %d", bt);
   return SPIKERL_E_UNSUPPORTED;
@@ -658,13 +735,15 @@ using namespace tc;
 
 bool tc_supported(const ActorDims& d) {
   if (!d.bf16) return false;
+  if (d.P[1] > 32 * TR_MAXW || d.P[2] > 32 * TR_MAXW) return false;
   for (int bt = 8; bt <= DX_MAX_BT; bt *= 2)
     if ((d.T * bt) % 16 == 0 && d.T * bt <= 256) return true;
   return false;
 }
 
 int launch_lif_fwd_tc(const ActorDims& d, int l, int B, const uint32_t* bits_in, const __nv_bfloat16* Wb16,
-                      uint32_t* bits_out, uint32_t* mask_out, uint8_t* counts, cudaStream_t st) {
+                      uint32_t* bits_out, uint32_t* mask_out, uint8_t* counts, uint8_t* bitsT_out,
+                      uint8_t* maskT_out, int row_bytes, cudaStream_t st) {
   ProfScope ps_(l == 1 ? "lif_fwd_tc_L1" : (l == 2 ? "lif_fwd_tc_L2" : "lif_fwd_tc_L3"), PB_TENSOR,
                 2.0 * d.T * B * (double)d.N[l] * d.N[l - 1], 0.0, st);
   Params p{};
@@ -678,6 +757,7 @@ int launch_lif_fwd_tc(const ActorDims& d, int l, int B, const uint32_t* bits_in,
   p.bits_in = bits_in; p.w_in = d.Wd[l - 1];
   p.bits_out = bits_out; p.mask_out = mask_out; p.w_out = d.Wd[l];
   p.counts = counts; p.n_valid = d.N[l]; p.n3 = d.N[3];
+  p.bitsT_out = bitsT_out; p.maskT_out = maskT_out; p.p_out = d.P[l]; p.tpad = row_bytes;
   p.kc = LifConst{d.dc, d.dv, d.vth, d.win}; p.zh = d.zh;
   CUtensorMap ma, mb;
   const uint64_t dims[2] = {(uint64_t)d.P[l - 1], (uint64_t)d.P[l]};
@@ -690,8 +770,8 @@ int launch_lif_fwd_tc(const ActorDims& d, int l, int B, const uint32_t* bits_in,
 
 // dX of layer l fused with the reverse scan of layer l-1 (G_l bf16 [T][B][P_l])
 int launch_lif_dx_tc(const ActorDims& d, int l, int B, const void* Gl, const __nv_bfloat16* Wb16,
-                     const uint32_t* bits_prev, const uint32_t* mask_prev, void* Gprev, void* Gsum,
-                     cudaStream_t st) {
+                     const uint8_t* bitsT_prev, const uint8_t* maskT_prev, int row_bytes, void* Gprev,
+                     void* Gsum, cudaStream_t st) {
   ProfScope ps_(l == 3 ? "lif_dx_tc_L3" : "lif_dx_tc_L2", PB_TENSOR, 2.0 * d.T * B * (double)d.N[l] * d.N[l - 1],
                 0.0, st);
   Params p{};
@@ -702,7 +782,7 @@ int launch_lif_dx_tc(const ActorDims& d, int l, int B, const void* Gl, const __n
   p.n_tiles = (B + p.Bt - 1) / p.Bt;
   p.k_blocks = d.P[l] / BK;
   p.n_units = p.m_tiles * p.n_tiles;
-  p.bits_prev = bits_prev; p.mask_prev = mask_prev; p.w_prev = d.Wd[l - 1];
+  p.bitsT_prev = bitsT_prev; p.maskT_prev = maskT_prev; p.tpad = row_bytes;
   p.g_prev = (__nv_bfloat16*)Gprev; p.p_prev = d.P[l - 1]; p.g_sum = (__nv_bfloat16*)Gsum;
   p.n_valid = d.N[l - 1];
   p.kc = LifConst{d.dc, d.dv, d.vth, d.win}; p.zh = d.zh;

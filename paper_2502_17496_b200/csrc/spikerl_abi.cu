@@ -104,6 +104,15 @@ TapeLayout tape_layout(const ActorDims& d, int B) {
   for (int l = 1; l < 4; ++l) L.mask[l] = take(sizeof(uint32_t) * (size_t)d.T * B * d.Wd[l]);
   L.counts = take((size_t)B * d.N3);
   L.act = take(sizeof(float) * (size_t)B * d.A);
+  L.tpad = round_up(d.T, 16);
+  for (int l = 0; l < 4; ++l) { L.bitsT[l] = 0; L.maskT[l] = 0; }
+  if (d.engine == SPIKERL_ENGINE_TCGEN05) {
+    const size_t octets = (size_t)round_up(B, 32) / 8;
+    for (int l = 1; l <= 2; ++l) {
+      L.bitsT[l] = take(octets * d.P[l] * L.tpad);
+      L.maskT[l] = take(octets * d.P[l] * L.tpad);
+    }
+  }
   L.total = o;
   return L;
 }
@@ -172,7 +181,9 @@ static int actor_forward_impl(const ActorDims& d, int B, const float* params,
     const __nv_bfloat16* Wb = d.bf16 ? pb16 + d.boff[l - 1] : nullptr;
     uint8_t* cnt = (l == 3) ? counts : nullptr;
     if (d.engine == SPIKERL_ENGINE_TCGEN05)
-      SPK_TRY(launch_lif_fwd_tc(d, l, B, bits[l - 1], Wb, bits[l], mask[l], cnt, st));
+      SPK_TRY(launch_lif_fwd_tc(d, l, B, bits[l - 1], Wb, bits[l], mask[l], cnt,
+                                L.bitsT[l] ? (uint8_t*)(tape + L.bitsT[l]) : nullptr,
+                                L.maskT[l] ? (uint8_t*)(tape + L.maskT[l]) : nullptr, L.tpad, st));
     else
       SPK_TRY(launch_lif_fwd_simt(d, l, B, bits[l - 1], Wf, Wb, bits[l], mask[l], cnt, st));
   }
@@ -209,7 +220,9 @@ static int actor_backward_impl(const ActorDims& d, int B, const float* params,
     float* dW = grads + d.off[SPIKERL_ACTOR_W1 + l - 1];
     if (l >= 2) {
       if (tc)
-        SPK_TRY(launch_lif_dx_tc(d, l, B, G[l], Wb, bits[l - 1], mask[l - 1], G[l - 1], l == 2 ? Gsum : nullptr, st));
+        SPK_TRY(launch_lif_dx_tc(d, l, B, G[l], Wb, (const uint8_t*)(tape + L.bitsT[l - 1]),
+                                 (const uint8_t*)(tape + L.maskT[l - 1]), L.tpad, G[l - 1],
+                                 l == 2 ? Gsum : nullptr, st));
       else
         SPK_TRY(launch_lif_dx_simt(d, l, B, G[l], Wf, Wb, bits[l - 1], mask[l - 1], G[l - 1],
                                    l == 2 ? Gsum : nullptr, st));
@@ -350,7 +363,11 @@ int spikerl_actor_tape_layout(const spikerl_actor_cfg* cfg, int batch, spikerl_t
   if (!out || batch < 1) { set_error("bad tape layout arguments"); return SPIKERL_E_ARG; }
   const TapeLayout L = tape_layout(d, batch);
   out->A = L.A;
-  for (int l = 0; l < 4; ++l) { out->bits[l] = L.bits[l]; out->mask[l] = L.mask[l]; out->padded[l] = d.P[l]; }
+  for (int l = 0; l < 4; ++l) {
+    out->bits[l] = L.bits[l]; out->mask[l] = L.mask[l]; out->padded[l] = d.P[l];
+    out->bitsT[l] = L.bitsT[l]; out->maskT[l] = L.maskT[l];
+  }
+  out->tpad = L.tpad;
   out->counts = L.counts; out->act = L.act; out->total = L.total;
   return SPIKERL_OK;
 }

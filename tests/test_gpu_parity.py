@@ -114,6 +114,30 @@ def test_actor_bf16_cfg4_shape_subsample():
     print(st)
 
 
+@pytest.mark.parametrize("B", [100, 257])
+def test_neuron_major_planes_are_transposes(B):
+    """tcgen05 engine: the octet-major spike/mask copies read by the fused dX epilogue hold
+    exactly the transposed bits of the batch-major planes (bit-exact, ragged batch)."""
+    import torch
+    import paper_2502_17496_b200 as pk
+    shape, _, _ = sg.preset("cfg1")
+    p, s, _ = _inputs(shape, B)
+    actor = pk.SpikingActor(pk.actor_cfg_from(shape, engine="tcgen05"), B)
+    actor.load(p)
+    actor.forward(torch.from_numpy(s).cuda())
+    torch.cuda.synchronize()
+    v = actor.tape_view()
+    for l in (1, 2):
+        for a, bname in ((f"bits{l}", f"bitsT{l}"), (f"mask{l}", f"maskT{l}")):
+            bm = pk.unpack_bits(v[a], v[a].shape[-1] * 32)              # [T][B][P]
+            raw = v[bname].cpu().numpy()                                # [O][P][tpad] bytes
+            bits = np.unpackbits(raw[..., None], axis=-1, bitorder="little")   # [O][P][tpad][8]
+            nm = bits.transpose(2, 1, 0, 3).reshape(raw.shape[2], raw.shape[1], -1)  # [tpad][P][O*8]
+            T = shape.T
+            assert np.array_equal(nm[:T, :, :B], bm.transpose(0, 2, 1)), (l, a)
+            assert not nm[:T, :, B:].any() and not nm[T:].any()
+
+
 def test_backward_rejects_foreign_tape():
     import torch
     import paper_2502_17496_b200 as pk
