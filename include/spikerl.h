@@ -114,7 +114,7 @@ int spikerl_critic_param_offsets(const spikerl_critic_cfg* cfg, size_t* offsets 
 size_t spikerl_critic_param_count(const spikerl_critic_cfg* cfg);
 /* bf16 working copies (opaque, zero-padded tensor-core layout); produced by *_refresh_bf16. */
 size_t spikerl_actor_bf16_bytes(const spikerl_actor_cfg* cfg);
-size_t spikerl_critic_bf16_bytes(const spikerl_critic_cfg* cfg);
+size_t spikerl_critic_bf16_bytes(const spikerl_critic_cfg* cfg); /* twin pair: [2][P] + W1^T, W2^T each */
 /* Device buffers the caller allocates for one forward(+backward) at `batch`. */
 size_t spikerl_actor_tape_bytes(const spikerl_actor_cfg* cfg, int batch);
 size_t spikerl_actor_workspace_bytes(const spikerl_actor_cfg* cfg, int batch);

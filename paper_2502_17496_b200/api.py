@@ -203,7 +203,7 @@ class TwinCritic:
         self.P = self.offsets[-1]
         self.params = torch.zeros(2 * self.P, dtype=torch.float32, device=device)
         self.bf16 = cfg.precision == L.BF16
-        self.params_bf16 = _alloc(2 * lib().spikerl_critic_bf16_bytes(C.byref(cfg)), device) if self.bf16 else None
+        self.params_bf16 = _alloc(lib().spikerl_critic_bf16_bytes(C.byref(cfg)), device) if self.bf16 else None
         self.ws = _alloc(lib().spikerl_critic_workspace_bytes(C.byref(cfg), batch), device)
         self.q = torch.zeros(2, batch, dtype=torch.float32, device=device)
         self.loss = torch.zeros(1, dtype=torch.float32, device=device)
@@ -301,8 +301,8 @@ class TD3:
         cb = lb.spikerl_critic_bf16_bytes(C.byref(ccfg))
         self.actor_bf16 = _alloc(ab, device) if self.bf16 else None
         self.actor_t_bf16 = _alloc(ab, device) if self.bf16 else None
-        self.critic_bf16 = _alloc(2 * cb, device) if self.bf16 else None
-        self.critic_t_bf16 = _alloc(2 * cb, device) if self.bf16 else None
+        self.critic_bf16 = _alloc(cb, device) if self.bf16 else None
+        self.critic_t_bf16 = _alloc(cb, device) if self.bf16 else None
         self.adam_steps = torch.zeros(4, dtype=torch.int64, device=device)
         self.rng_counter = torch.zeros(1, dtype=torch.int64, device=device)
         self.losses = torch.zeros(2, **f32)

@@ -65,6 +65,13 @@ int launch_polyak(float* t, const float* s, size_t n, float tau, cudaStream_t st
 
 // ---- critic (k_critic.cu)
 size_t critic_ws_bytes(const CriticDims& c, int B);
+size_t critic_bf16_elems(const CriticDims& c);   // twin pair incl. the mma path's padded/transposed copies
+int launch_critic_refresh(const CriticDims& c, const float* params2, __nv_bfloat16* out, cudaStream_t st);
+bool critic_mma_ok(const CriticDims& c);
+size_t critic_mma_ws_bytes(const CriticDims& c, int B);
+int critic_mma_fwd_bwd(const CriticDims& c, int B, const float* params2, const __nv_bfloat16* pb, const float* obs,
+                       int S, const float* act, int A, const float* y, float* q, float* loss, float* grad2,
+                       float* grad_act, float act_scale, int nz, void* ws, cudaStream_t st);
 int critic_fwd_bwd(const CriticDims& c, int B, const float* params2, const __nv_bfloat16* pb16,
                    const float* obs, int S, const float* act, int A, const float* y, float* q,
                    float* loss, float* grad2, float* grad_act, float act_scale, int n_critics,

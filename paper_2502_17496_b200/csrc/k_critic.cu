@@ -267,13 +267,17 @@ size_t critic_ws_bytes(const CriticDims& c, int B) {
   add((size_t)B * c.in);
   add(2ull * B * c.H1); add(2ull * B * c.H1); add(2ull * B * c.H2); add(2ull * B * c.H2);
   add(2ull * B); add(2ull * B); add(2ull * B * c.H2); add(2ull * B * c.H1); add((size_t)B * c.in);
-  return n;
+  const size_t m = critic_mma_ok(c) ? critic_mma_ws_bytes(c, B) : 0;
+  return n > m ? n : m;
 }
 
+// SIMT GEMM path: fp32 precision (configs[0]-style critics) and shapes outside the mma path.
 int critic_fwd_bwd(const CriticDims& c, int B, const float* params2, const __nv_bfloat16* pb16,
                    const float* obs, int S, const float* act, int A, const float* y, float* q,
                    float* loss, float* grad2, float* grad_act, float act_scale, int nz, void* ws,
                    cudaStream_t st) {
+  if (critic_mma_ok(c))
+    return critic_mma_fwd_bwd(c, B, params2, pb16, obs, S, act, A, y, q, loss, grad2, grad_act, act_scale, nz, ws, st);
   CriticWs w = carve(c, B, ws);
   const bool bf = c.bf16 != 0;
   const long long P = (long long)c.off[SPIKERL_CRITIC_NPARAM];

@@ -1,0 +1,480 @@
+// k_critic_mma.cu — K8, bf16 twin critic on warp-level tensor cores (mma.sync m16n8k16 bf16 ->
+// fp32). The critic ("deep critic network"; configs[1] 23->256->256->1) is
+// latency-bound at the TD3 batch sizes: the whole forward of both critics is one
+// launch (a CTA = 16 batch rows of one critic, hidden activations stay in shared memory), the
+// data backward is one launch, the weight gradients are one GEMM launch plus one reduction launch.
+// Rounding points follow DESIGN.md R20 exactly as the oracle does: x, h1, h2, dz2, dz1 and the
+// weights are bf16 where they enter a contraction; pre-activations, Q, losses and gradients fp32.
+// Operand layouts (all k-contiguous so every fragment load is one 32-bit word):
+//   forward L1  A = X [16][in_p] (smem)      B = W1p [H1][in_p]   (bf16 copy, rows zero-padded)
+//   forward L2  A = h1 [16][H1] (smem)       B = W2  [H2][H1]
+//   dH1         A = dz2 [16][H2] (smem)      B = W2T [H1][H2]
+//   dQ1/da      A = dz1 [16][H1] (smem)      B = W1T [in_p+32][H1]
+//   dW2         A = dZ2T [H2][Bp]            B = H1T [H1][Bp]
+//   dW1         A = dZ1T [H1][Bp]            B = XT  [in_q][Bp]
+#include "internal.h"
+
+namespace spk {
+
+namespace {
+
+constexpr int RB = 16;       // batch rows per CTA (the MMA M)
+constexpr int HW = 256;      // hidden width handled by the MMA path (4 warps x 8 n-tiles x 8)
+constexpr int SPAD = 8;      // smem row padding (bf16) -> conflict-free fragment loads
+
+__device__ __forceinline__ uint32_t ld32(const __nv_bfloat16* p) { return *reinterpret_cast<const uint32_t*>(p); }
+
+__device__ __forceinline__ void mma16816(float (&c)[4], const uint32_t (&a)[4], uint32_t b0, uint32_t b1) {
+  asm volatile(
+      "mma.sync.aligned.m16n8k16.row.col.f32.bf16.bf16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, {%0,%1,%2,%3};"
+      : "+f"(c[0]), "+f"(c[1]), "+f"(c[2]), "+f"(c[3])
+      : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));
+}
+
+// acc[nt] += A[16 x K] * B^T, A rows k-contiguous (lda), B = NT*8 rows (n) k-contiguous (ldb).
+// Fragments of the next D k-steps are kept in flight in registers (static rotation), so the
+// L2 latency of the weight / activation loads overlaps the MMAs of earlier k-steps.
+template <int NT, int D = 4>
+__device__ __forceinline__ void warp_mma(float (&acc)[NT][4], const __nv_bfloat16* A, int lda,
+                                         const __nv_bfloat16* Bm, long long ldb, int K) {
+  const int lane = threadIdx.x & 31, g = lane >> 2, t = lane & 3;
+  const __nv_bfloat16* a0 = A + g * lda + 2 * t;
+  const __nv_bfloat16* a1 = A + (g + 8) * lda + 2 * t;
+  const __nv_bfloat16* bp = Bm + g * ldb + 2 * t;
+  uint32_t a[D][4], b[D][NT][2];
+  auto load = [&](uint32_t (&as)[4], uint32_t (&bs)[NT][2], int k0) {
+    if (k0 < K) {
+      as[0] = ld32(a0 + k0); as[1] = ld32(a1 + k0); as[2] = ld32(a0 + k0 + 8); as[3] = ld32(a1 + k0 + 8);
+#pragma unroll
+      for (int nt = 0; nt < NT; ++nt) {
+        bs[nt][0] = __ldg(reinterpret_cast<const unsigned int*>(bp + nt * 8 * ldb + k0));
+        bs[nt][1] = __ldg(reinterpret_cast<const unsigned int*>(bp + nt * 8 * ldb + k0 + 8));
+      }
+    }
+  };
+#pragma unroll
+  for (int s = 0; s < D; ++s) load(a[s], b[s], s * 16);
+  for (int k0 = 0; k0 < K; k0 += 16 * D) {
+#pragma unroll
+    for (int s = 0; s < D; ++s) {
+      if (k0 + s * 16 < K) {
+#pragma unroll
+        for (int nt = 0; nt < NT; ++nt) mma16816(acc[nt], a[s], b[s][nt][0], b[s][nt][1]);
+        load(a[s], b[s], k0 + (s + D) * 16);
+      }
+    }
+  }
+}
+
+// bf16 twin buffer: [2][P] (fp32 layout; P may be odd), then one block per critic holding every
+// operand the MMA path reads with 32-bit fragment loads (even offsets): W1p | W1T | W2T | W2
+struct MmaLayout {
+  long long P, W1p, W1T, W2T, W2c, tb;
+  int inp, inq;          // in rounded to 16 (K of L1) and to 64 (+32 rows of W1T / XT)
+};
+
+MmaLayout mma_layout(const CriticDims& c) {
+  MmaLayout L;
+  L.P = (long long)c.off[SPIKERL_CRITIC_NPARAM];
+  L.inp = round_up(c.in, 16);
+  L.inq = round_up(c.in, 64) + 32;
+  L.W1p = 0;
+  L.W1T = (long long)c.H1 * L.inp;
+  L.W2T = L.W1T + (long long)L.inq * c.H1;
+  L.W2c = L.W2T + (long long)c.H1 * c.H2;
+  L.tb = L.W2c + (long long)c.H2 * c.H1;
+  return L;
+}
+
+struct MmaWs {
+  __nv_bfloat16 *XT, *H1T, *dZ2T, *dZ1T;   // [inq][Bp], [2][H][Bp] x3
+  float *Z1, *Z2, *Hh2, *q, *dq;           // [2][B][H] x3, [2][B] x2
+};
+
+MmaWs mma_carve(const CriticDims& c, int B, void* base, size_t* total) {
+  const MmaLayout L = mma_layout(c);
+  const size_t Bp = round_up(B, RB);
+  MmaWs w{};
+  char* p = (char*)base;
+  size_t off = 0;
+  auto take = [&](size_t bytes) { char* r = p ? p + off : nullptr; off += align_up(bytes, 256); return r; };
+  w.XT = (__nv_bfloat16*)take(2 * (size_t)L.inq * Bp);
+  w.H1T = (__nv_bfloat16*)take(2 * 2 * (size_t)c.H1 * Bp);
+  w.dZ2T = (__nv_bfloat16*)take(2 * 2 * (size_t)c.H2 * Bp);
+  w.dZ1T = (__nv_bfloat16*)take(2 * 2 * (size_t)c.H1 * Bp);
+  w.Z1 = (float*)take(4 * 2 * (size_t)B * c.H1);
+  w.Z2 = (float*)take(4 * 2 * (size_t)B * c.H2);
+  w.Hh2 = (float*)take(4 * 2 * (size_t)B * c.H2);
+  w.q = (float*)take(4 * 2 * (size_t)B);
+  w.dq = (float*)take(4 * 2 * (size_t)B);
+  if (total) *total = off;
+  return w;
+}
+
+// ------------------------------------------------------------------ forward (both critics)
+constexpr int NWARP = 8, NTW = HW / (NWARP * 8);   // 8 warps x 4 n-tiles x 8 columns
+
+__global__ void __launch_bounds__(256) critic_fwd_mma_kernel(
+    int B, int Bp, int S, int A, int inp, int inq, const float* __restrict__ obs, const float* __restrict__ act,
+    const __nv_bfloat16* __restrict__ pb, long long P, long long tb, long long oW1p, long long oW2,
+    long long oW3, const float* __restrict__ params, long long oB1, long long oB2, long long oB3,
+    __nv_bfloat16* __restrict__ XT, __nv_bfloat16* __restrict__ H1T, float* __restrict__ Z1,
+    float* __restrict__ Z2, float* __restrict__ Hh2, float* __restrict__ q, int store) {
+  __shared__ __align__(16) __nv_bfloat16 xs[RB * (512 + SPAD)];
+  __shared__ __align__(16) __nv_bfloat16 h1s[RB * (HW + SPAD)];
+  __shared__ float red[NWARP][RB];
+  const int z = blockIdx.y, r0 = blockIdx.x * RB, tid = threadIdx.x, warp = tid >> 5;
+  const int lane = tid & 31, g = lane >> 2, t = lane & 3;
+  const int in = S + A, ldx = inp + SPAD, ldh = HW + SPAD;
+  // X tile (bf16-rounded [s; a]); the z == 0 CTAs also write X^T (zeros beyond in / B) for dW1
+  for (int idx = tid; idx < RB * inp; idx += 256) {
+    const int r = idx / inp, i = idx - r * inp, b = r0 + r;
+    float v = 0.f;
+    if (b < B && i < in) v = i < S ? obs[(size_t)b * S + i] : act[(size_t)b * A + (i - S)];
+    xs[r * ldx + i] = __float2bfloat16_rn(v);
+  }
+  __syncthreads();
+  if (store && z == 0) {
+    for (int idx = tid; idx < RB * inq; idx += 256) {
+      const int i = idx / RB, r = idx - i * RB;
+      XT[(size_t)i * Bp + r0 + r] = i < inp ? xs[r * ldx + i] : __float2bfloat16_rn(0.f);
+    }
+  }
+  const __nv_bfloat16* W1p = pb + 2 * P + z * tb + oW1p;
+  const __nv_bfloat16* W2 = pb + 2 * P + z * tb + oW2;
+  const float* b1 = params + z * P + oB1;
+  const float* b2 = params + z * P + oB2;
+  const int n0 = warp * NTW * 8;
+  {
+    float acc[NTW][4] = {};
+    warp_mma<NTW>(acc, xs, ldx, W1p + (size_t)n0 * inp, inp, inp);
+#pragma unroll
+    for (int nt = 0; nt < NTW; ++nt) {
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        const int r = g + (e >> 1) * 8, col = n0 + nt * 8 + 2 * t + (e & 1), b = r0 + r;
+        const float zz = __fadd_rn(acc[nt][e], b1[col]);
+        h1s[r * ldh + col] = b < B ? __float2bfloat16_rn(fmaxf(zz, 0.f)) : __float2bfloat16_rn(0.f);
+        if (store && b < B) Z1[((size_t)z * B + b) * HW + col] = zz;
+      }
+    }
+  }
+  __syncthreads();
+  if (store) {   // h1^T for dW2 (zero rows beyond B), coalesced along the batch
+    for (int idx = tid; idx < RB * HW; idx += 256) {
+      const int col = idx / RB, r = idx - col * RB;
+      H1T[((size_t)z * HW + col) * Bp + r0 + r] = h1s[r * ldh + col];
+    }
+  }
+  const __nv_bfloat16* W3 = pb + z * P + oW3;
+  float qp[2] = {0.f, 0.f};
+  {
+    float acc[NTW][4] = {};
+    warp_mma<NTW>(acc, h1s, ldh, W2 + (size_t)n0 * HW, HW, HW);
+#pragma unroll
+    for (int nt = 0; nt < NTW; ++nt) {
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        const int r = g + (e >> 1) * 8, col = n0 + nt * 8 + 2 * t + (e & 1), b = r0 + r;
+        const float zz = __fadd_rn(acc[nt][e], b2[col]);
+        const float h = bf16_round(fmaxf(zz, 0.f));
+        qp[e >> 1] = __fmaf_rn(h, __bfloat162float(W3[col]), qp[e >> 1]);
+        if (store && b < B) {
+          Z2[((size_t)z * B + b) * HW + col] = zz;
+          Hh2[((size_t)z * B + b) * HW + col] = h;
+        }
+      }
+    }
+  }
+  // Q[r] = sum_j h2[r][j] w3[j] + b3: reduce over the quad (t), then warps in a fixed order
+#pragma unroll
+  for (int hh = 0; hh < 2; ++hh) {
+    float s = qp[hh];
+    s = __fadd_rn(s, __shfl_xor_sync(0xffffffffu, s, 1));
+    s = __fadd_rn(s, __shfl_xor_sync(0xffffffffu, s, 2));
+    if (t == 0) red[warp][g + hh * 8] = s;
+  }
+  __syncthreads();
+  if (tid < RB && r0 + tid < B) {
+    float s = red[0][tid];
+    for (int w = 1; w < NWARP; ++w) s = __fadd_rn(s, red[w][tid]);
+    q[(size_t)z * B + r0 + tid] = __fadd_rn(s, params[z * P + oB3]);
+  }
+}
+
+// ------------------------------------------------------------------ data backward
+// dZ2 = round(dQ w3 [Z2 > 0]); dZ1 = round((dZ2 W2) [Z1 > 0]); grad_act = (dZ1 W1)[:, S:S+A]
+__global__ void __launch_bounds__(256) critic_bwd_data_mma_kernel(
+    int B, int Bp, int S, int A, int inp, const float* __restrict__ dq, const __nv_bfloat16* __restrict__ pb,
+    long long P, long long tb, long long oW3, long long oW1T, long long oW2T, const float* __restrict__ Z1,
+    const float* __restrict__ Z2, __nv_bfloat16* __restrict__ dZ2T, __nv_bfloat16* __restrict__ dZ1T,
+    float* __restrict__ grad_act, int store_t) {
+  __shared__ __align__(16) __nv_bfloat16 d2s[RB * (HW + SPAD)];
+  __shared__ __align__(16) __nv_bfloat16 d1s[RB * (HW + SPAD)];
+  const int z = blockIdx.y, r0 = blockIdx.x * RB, tid = threadIdx.x, warp = tid >> 5;
+  const int lane = tid & 31, g = lane >> 2, t = lane & 3;
+  const int ldh = HW + SPAD;
+  const __nv_bfloat16* W3 = pb + z * P + oW3;
+  for (int idx = tid; idx < RB * HW; idx += 256) {   // coalesced along j
+    const int r = idx / HW, j = idx - r * HW, b = r0 + r;
+    float d = 0.f;
+    if (b < B && Z2[((size_t)z * B + b) * HW + j] > 0.f) d = __fmul_rn(dq[(size_t)z * B + b], __bfloat162float(W3[j]));
+    d2s[r * ldh + j] = __float2bfloat16_rn(d);
+  }
+  __syncthreads();
+  if (store_t) {
+    for (int idx = tid; idx < RB * HW; idx += 256) {
+      const int j = idx / RB, r = idx - j * RB;
+      dZ2T[((size_t)z * HW + j) * Bp + r0 + r] = d2s[r * ldh + j];
+    }
+  }
+  const __nv_bfloat16* W2T = pb + 2 * P + z * tb + oW2T;
+  const int n0 = warp * NTW * 8;
+  {
+    float acc[NTW][4] = {};
+    warp_mma<NTW>(acc, d2s, ldh, W2T + (size_t)n0 * HW, HW, HW);
+#pragma unroll
+    for (int nt = 0; nt < NTW; ++nt) {
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        const int r = g + (e >> 1) * 8, col = n0 + nt * 8 + 2 * t + (e & 1), b = r0 + r;
+        float d = 0.f;
+        if (b < B && Z1[((size_t)z * B + b) * HW + col] > 0.f) d = acc[nt][e];
+        d1s[r * ldh + col] = __float2bfloat16_rn(d);
+      }
+    }
+  }
+  __syncthreads();
+  if (store_t) {
+    for (int idx = tid; idx < RB * HW; idx += 256) {
+      const int j = idx / RB, r = idx - j * RB;
+      dZ1T[((size_t)z * HW + j) * Bp + r0 + r] = d1s[r * ldh + j];
+    }
+  }
+  if (grad_act == nullptr || z != 0) return;
+  if (warp == 0) {   // columns [S, S+A) of dZ1 W1 = dZ1 (W1T)^T, in n-tiles of 8 from S rounded down
+    const __nv_bfloat16* W1T = pb + 2 * P + oW1T;
+    const int c0 = S & ~7;
+    for (int cb = c0; cb < S + A; cb += 32) {
+      float acc[4][4] = {};
+      warp_mma<4>(acc, d1s, ldh, W1T + (size_t)cb * HW, HW, HW);
+#pragma unroll
+      for (int nt = 0; nt < 4; ++nt) {
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          const int r = g + (e >> 1) * 8, col = cb + nt * 8 + 2 * t + (e & 1), b = r0 + r;
+          if (b < B && col >= S && col < S + A) grad_act[(size_t)b * A + (col - S)] = acc[nt][e];
+        }
+      }
+    }
+  }
+}
+
+// ------------------------------------------------------------------ weight gradients
+// blockIdx.z = critic; blockIdx.y < HW/16: dW2 row tile; else dW1 row tile. Each CTA: 16 rows x
+// 256 columns (4 warps x 64), K = Bp batch rows. Writes the fp32 master layout.
+__global__ void __launch_bounds__(256) critic_wgrad_mma_kernel(
+    int Bp, int in, int inq, long long P, long long oW1, long long oW2, const __nv_bfloat16* __restrict__ XT,
+    const __nv_bfloat16* __restrict__ H1T, const __nv_bfloat16* __restrict__ dZ2T,
+    const __nv_bfloat16* __restrict__ dZ1T, float* __restrict__ grad2) {
+  const int z = blockIdx.z, tid = threadIdx.x, warp = tid >> 5;
+  const int lane = tid & 31, g = lane >> 2, t = lane & 3;
+  const int ntile = HW / RB;
+  const bool w2 = blockIdx.y < ntile;
+  const int m0 = (w2 ? blockIdx.y : blockIdx.y - ntile) * RB;
+  const int ncols = w2 ? HW : in;
+  const int n0 = blockIdx.x * 256 + warp * NTW * 8;
+  if (n0 >= ncols) return;
+  const __nv_bfloat16* Am = (w2 ? dZ2T : dZ1T) + ((size_t)z * HW + m0) * Bp;
+  const __nv_bfloat16* Bm = w2 ? H1T + (size_t)z * HW * Bp : XT;
+  if (!w2 && n0 + NTW * 8 > inq) return;
+  float acc[NTW][4] = {};
+  // A is read straight from global (16 rows x Bp); fragments are 32-bit words
+  warp_mma<NTW>(acc, Am, Bp, Bm + (size_t)n0 * Bp, Bp, Bp);
+  float* out = grad2 + z * P + (w2 ? oW2 : oW1);
+#pragma unroll
+  for (int nt = 0; nt < NTW; ++nt) {
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      const int r = m0 + g + (e >> 1) * 8, col = n0 + nt * 8 + 2 * t + (e & 1);
+      if (col < ncols) out[(size_t)r * ncols + col] = acc[nt][e];
+    }
+  }
+}
+
+// db1 = rowsum dZ1T, db2 = rowsum dZ2T, dW3 = dQ^T H2, db3 = sum dQ: one warp per output
+__global__ void __launch_bounds__(256) critic_bias_grads_kernel(int B, int Bp, long long P, long long oB1,
+                                                                long long oB2, long long oW3, long long oB3,
+                                                                const __nv_bfloat16* __restrict__ dZ1T,
+                                                                const __nv_bfloat16* __restrict__ dZ2T,
+                                                                const float* __restrict__ dq,
+                                                                const float* __restrict__ Hh2,
+                                                                float* __restrict__ grad2) {
+  const int z = blockIdx.y;
+  const int o = blockIdx.x * 8 + (threadIdx.x >> 5), lane = threadIdx.x & 31;
+  const int nout = 3 * HW + 1;
+  if (o >= nout) return;
+  float s = 0.f;
+  if (o < 2 * HW) {
+    const __nv_bfloat16* row = (o < HW ? dZ1T + ((size_t)z * HW + o) * Bp : dZ2T + ((size_t)z * HW + o - HW) * Bp);
+    for (int b = lane; b < B; b += 32) s = __fadd_rn(s, __bfloat162float(row[b]));
+  } else if (o < 3 * HW) {
+    const int j = o - 2 * HW;
+    for (int b = lane; b < B; b += 32)
+      s = __fmaf_rn(dq[(size_t)z * B + b], Hh2[((size_t)z * B + b) * HW + j], s);
+  } else {
+    for (int b = lane; b < B; b += 32) s = __fadd_rn(s, dq[(size_t)z * B + b]);
+  }
+  for (int off = 16; off > 0; off >>= 1) s = __fadd_rn(s, __shfl_xor_sync(0xffffffffu, s, off));
+  if (lane == 0) {
+    float* base = grad2 + z * P;
+    if (o < HW) base[oB1 + o] = s;
+    else if (o < 2 * HW) base[oB2 + (o - HW)] = s;
+    else if (o < 3 * HW) base[oW3 + (o - 2 * HW)] = s;
+    else base[oB3] = s;
+  }
+}
+
+// bf16 refresh of the twin pair: [2][P] plain copy, then per critic W1p, W1T, W2T (zero padded)
+__global__ void critic_refresh_kernel(const float* __restrict__ params, long long P, int in, int H1, int H2,
+                                      int inp, int inq, long long oW1, long long oW2, long long tb,
+                                      __nv_bfloat16* __restrict__ out) {
+  const long long total = 2 * P + 2 * tb;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < total; i += (long long)gridDim.x * blockDim.x) {
+    float v;
+    if (i < 2 * P) {
+      v = params[i];
+    } else {
+      const long long f = i - 2 * P;
+      const int z = (int)(f / tb);
+      long long e = f - z * tb;
+      const float* W1 = params + z * P + oW1;
+      const float* W2 = params + z * P + oW2;
+      const long long n1p = (long long)H1 * inp, n1t = (long long)inq * H1;
+      if (e < n1p) {                         // W1p[k][i]
+        const int k = (int)(e / inp), ii = (int)(e - (long long)k * inp);
+        v = ii < in ? W1[(size_t)k * in + ii] : 0.f;
+      } else if ((e -= n1p) < n1t) {         // W1T[i][k]
+        const int ii = (int)(e / H1), k = (int)(e - (long long)ii * H1);
+        v = ii < in ? W1[(size_t)k * in + ii] : 0.f;
+      } else if ((e -= n1t) < (long long)H1 * H2) {   // W2T[k][j] = W2[j][k]
+        const int k = (int)(e / H2), j = (int)(e - (long long)k * H2);
+        v = W2[(size_t)j * H1 + k];
+      } else {                               // W2 (aligned copy)
+        v = W2[e - (long long)H1 * H2];
+      }
+    }
+    out[i] = __float2bfloat16_rn(v);
+  }
+}
+
+__global__ void fill_dq_kernel(float* x, int n, float v) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) x[i] = v;
+}
+
+// loss = sum_z mean_b (Q_z - y)^2 ; dQ[z][b] = 2 (Q_z - y)/B. Single block, fixed order.
+__global__ void __launch_bounds__(256) critic_loss_mma_kernel(int B, int nz, const float* __restrict__ q,
+                                                              const float* __restrict__ y, float* __restrict__ dq,
+                                                              float* __restrict__ loss) {
+  __shared__ float red[256];
+  float tot = 0.f;
+  for (int z = 0; z < nz; ++z) {
+    float s = 0.f;
+    for (int b = threadIdx.x; b < B; b += 256) {
+      const float e = __fsub_rn(q[(size_t)z * B + b], y[b]);
+      s = __fmaf_rn(e, e, s);
+      dq[(size_t)z * B + b] = __fdiv_rn(__fmul_rn(2.0f, e), (float)B);
+    }
+    red[threadIdx.x] = s;
+    __syncthreads();
+    for (int w = 128; w > 0; w >>= 1) {
+      if (threadIdx.x < w) red[threadIdx.x] = __fadd_rn(red[threadIdx.x], red[threadIdx.x + w]);
+      __syncthreads();
+    }
+    tot = __fadd_rn(tot, __fdiv_rn(red[0], (float)B));
+    __syncthreads();
+  }
+  if (threadIdx.x == 0 && loss) *loss = tot;
+}
+
+}  // namespace
+
+bool critic_mma_ok(const CriticDims& c) { return c.bf16 && c.H1 == HW && c.H2 == HW && c.in <= 512; }
+
+size_t critic_bf16_elems(const CriticDims& c) {
+  if (!critic_mma_ok(c)) return 2 * c.off[SPIKERL_CRITIC_NPARAM];
+  const MmaLayout L = mma_layout(c);
+  return 2 * L.P + 2 * L.tb;
+}
+
+size_t critic_mma_ws_bytes(const CriticDims& c, int B) {
+  size_t total = 0;
+  mma_carve(c, B, nullptr, &total);
+  return total;
+}
+
+int launch_critic_refresh(const CriticDims& c, const float* params2, __nv_bfloat16* out, cudaStream_t st) {
+  ProfScope ps_("critic_refresh_bf16", PB_HBM, 0.0, 6.0 * critic_bf16_elems(c), st);
+  if (!critic_mma_ok(c)) return launch_f32_to_bf16(params2, out, 2 * c.off[SPIKERL_CRITIC_NPARAM], st);
+  const MmaLayout L = mma_layout(c);
+  const long long total = 2 * L.P + 2 * L.tb;
+  critic_refresh_kernel<<<(int)(cdiv(total, 256) < 1184 ? cdiv(total, 256) : 1184), 256, 0, st>>>(
+      params2, L.P, c.in, c.H1, c.H2, L.inp, L.inq, (long long)c.off[SPIKERL_CRITIC_W1],
+      (long long)c.off[SPIKERL_CRITIC_W2], L.tb, out);
+  SPK_LAUNCHED();
+  return SPIKERL_OK;
+}
+
+int critic_mma_fwd_bwd(const CriticDims& c, int B, const float* params2, const __nv_bfloat16* pb, const float* obs,
+                       int S, const float* act, int A, const float* y, float* q, float* loss, float* grad2,
+                       float* grad_act, float act_scale, int nz, void* ws, cudaStream_t st) {
+  const MmaLayout L = mma_layout(c);
+  MmaWs w = mma_carve(c, B, ws, nullptr);
+  const int Bp = round_up(B, RB);
+  const bool want_params = (y != nullptr && grad2 != nullptr);
+  const bool need_bwd = want_params || grad_act != nullptr;
+  const long long oW3 = (long long)c.off[SPIKERL_CRITIC_W3];
+  {
+    ProfScope ps_("critic_fwd_mma", PB_LATENCY, 2.0 * B * nz * ((double)c.in * HW + (double)HW * HW + HW), 0.0, st);
+    dim3 grid(Bp / RB, nz);
+    critic_fwd_mma_kernel<<<grid, 256, 0, st>>>(
+        B, Bp, S, A, L.inp, L.inq, obs, act, pb, L.P, L.tb, L.W1p, L.W2c, oW3, params2,
+        (long long)c.off[SPIKERL_CRITIC_B1], (long long)c.off[SPIKERL_CRITIC_B2], (long long)c.off[SPIKERL_CRITIC_B3],
+        w.XT, w.H1T, w.Z1, w.Z2, w.Hh2, q, need_bwd ? 1 : 0);
+    SPK_LAUNCHED();
+  }
+  if (y) {
+    critic_loss_mma_kernel<<<1, 256, 0, st>>>(B, nz, q, y, w.dq, loss);
+    SPK_LAUNCHED();
+  }
+  if (!need_bwd) return SPIKERL_OK;
+  int nb = nz;
+  if (!want_params) {
+    fill_dq_kernel<<<cdiv(B, 256), 256, 0, st>>>(w.dq, B, act_scale);
+    SPK_LAUNCHED();
+    nb = 1;
+  }
+  {
+    ProfScope ps_("critic_bwd_data_mma", PB_LATENCY, 2.0 * B * nb * ((double)HW * HW), 0.0, st);
+    dim3 grid(Bp / RB, nb);
+    critic_bwd_data_mma_kernel<<<grid, 256, 0, st>>>(B, Bp, S, A, L.inp, w.dq, pb, L.P, L.tb, oW3, L.W1T, L.W2T, w.Z1,
+                                                     w.Z2, w.dZ2T, w.dZ1T, grad_act, want_params ? 1 : 0);
+    SPK_LAUNCHED();
+  }
+  if (want_params) {
+    ProfScope ps_("critic_wgrad_mma", PB_LATENCY, 2.0 * B * nz * ((double)HW * HW + (double)HW * c.in), 0.0, st);
+    dim3 grid(cdiv(L.inq > HW ? L.inq : HW, 256), 2 * (HW / RB), nz);
+    critic_wgrad_mma_kernel<<<grid, 256, 0, st>>>(Bp, c.in, L.inq, L.P, (long long)c.off[SPIKERL_CRITIC_W1],
+                                                  (long long)c.off[SPIKERL_CRITIC_W2], w.XT, w.H1T, w.dZ2T, w.dZ1T,
+                                                  grad2);
+    SPK_LAUNCHED();
+    critic_bias_grads_kernel<<<dim3(cdiv(3 * HW + 1, 8), nz), 256, 0, st>>>(
+        B, Bp, L.P, (long long)c.off[SPIKERL_CRITIC_B1], (long long)c.off[SPIKERL_CRITIC_B2], oW3,
+        (long long)c.off[SPIKERL_CRITIC_B3], w.dZ1T, w.dZ2T, w.dq, w.Hh2, grad2);
+    SPK_LAUNCHED();
+  }
+  return SPIKERL_OK;
+}
+
+}  // namespace spk

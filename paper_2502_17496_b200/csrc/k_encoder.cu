@@ -3,8 +3,10 @@
 //   PAPER.md:131 (§III-A "populations use Gaussian distributions to transform continuous input
 //   values into spike trains"); north_star ("deterministic soft-reset encoder spikes");
 //   SPEC.md:123-140; R4 (fp64 exponent, RNE to fp32, no FTZ) and R5 (acc >= 1).
-// HBM-bound elementwise kernel: one thread per (b, k); a warp owns 32 consecutive encoder
-// neurons so one __ballot_sync per timestep yields exactly one u32 word of bits0[t][b][:].
+// A warp owns 32 consecutive encoder neurons k, so one __ballot_sync per timestep yields exactly
+// one u32 word of bits0[t][b][:]. Each thread keeps its neuron's constants (obs index, mu, the
+// fp64 2 sigma^2) in registers and walks a strided set of batch rows, prefetching the next
+// observation, so the grid is a few blocks per SM instead of one block per (b, 128 neurons).
 #include "internal.h"
 
 namespace spk {
@@ -15,34 +17,42 @@ __global__ void __launch_bounds__(128) enc_fwd_kernel(int B, int S, int E, int K
                                                       const float* __restrict__ sigma,
                                                       float* __restrict__ A_out,
                                                       uint32_t* __restrict__ bits0) {
-  const int b = blockIdx.x;
   const int k = blockIdx.y * blockDim.x + threadIdx.x;
   const int lane = threadIdx.x & 31;
-  float A = 0.0f;
-  if (k < K0) {
-    const int i = k / E;
-    const double s = (double)__ldg(obs + (size_t)b * S + i);
-    const double m = (double)__ldg(mu + k);
-    const double sg = (double)__ldg(sigma + k);
-    const double dd = __dsub_rn(s, m);
-    const double q = __dmul_rn(dd, dd);
-    const double den = __dmul_rn(2.0, __dmul_rn(sg, sg));
-    A = (float)exp(-__ddiv_rn(q, den));  // RNE double -> float
-    A_out[(size_t)b * K0 + k] = A;
-  }
-  float acc = 0.0f;
-  const size_t word = (size_t)b * W0 + (k >> 5);
-  // lane (t mod 32) keeps the ballot word of timestep t; one store instruction per 32 steps
-  uint32_t mine = 0;
-  for (int t = 0; t < T; ++t) {
-    acc = __fadd_rn(acc, A);
-    const bool fire = acc >= 1.0f;
-    if (fire) acc = __fsub_rn(acc, 1.0f);
-    const uint32_t w = __ballot_sync(0xffffffffu, fire);
-    if (lane == (t & 31)) mine = w;
-    if ((t & 31) == 31 || t == T - 1) {
-      const int tb = t & ~31;
-      if (lane <= (t & 31)) bits0[(size_t)(tb + lane) * B * W0 + word] = mine;
+  const bool kv = k < K0;
+  const int i = kv ? k / E : 0;
+  const double m = kv ? (double)__ldg(mu + k) : 0.0;
+  const double sg = kv ? (double)__ldg(sigma + k) : 1.0;
+  const double den = __dmul_rn(2.0, __dmul_rn(sg, sg));
+  const size_t wk = (size_t)(k >> 5);
+  const size_t tstride = (size_t)B * W0;
+  int b = blockIdx.x;
+  float s_next = (kv && b < B) ? __ldg(obs + (size_t)b * S + i) : 0.f;
+  for (; b < B; b += gridDim.x) {
+    const float s = s_next;
+    const int bn = b + gridDim.x;
+    if (kv && bn < B) s_next = __ldg(obs + (size_t)bn * S + i);
+    float A = 0.0f;
+    if (kv) {
+      const double dd = __dsub_rn((double)s, m);
+      const double q = __dmul_rn(dd, dd);
+      A = (float)exp(-__ddiv_rn(q, den));  // RNE double -> float
+      A_out[(size_t)b * K0 + k] = A;
+    }
+    float acc = 0.0f;
+    const size_t word = (size_t)b * W0 + wk;
+    // lane (t mod 32) keeps the ballot word of timestep t; one store instruction per 32 steps
+    uint32_t mine = 0;
+    for (int t = 0; t < T; ++t) {
+      acc = __fadd_rn(acc, A);
+      const bool fire = acc >= 1.0f;
+      if (fire) acc = __fsub_rn(acc, 1.0f);
+      const uint32_t w = __ballot_sync(0xffffffffu, fire);
+      if (lane == (t & 31)) mine = w;
+      if ((t & 31) == 31 || t == T - 1) {
+        const int tb = t & ~31;
+        if (lane <= (t & 31)) bits0[(size_t)(tb + lane) * tstride + word] = mine;
+      }
     }
   }
 }
@@ -50,7 +60,11 @@ __global__ void __launch_bounds__(128) enc_fwd_kernel(int B, int S, int E, int K
 int launch_enc_fwd(const ActorDims& d, int B, const float* obs, const float* mu, const float* sigma,
                    float* A, uint32_t* bits0, cudaStream_t st) {
   ProfScope ps_("enc_fwd", PB_HBM, 0.0, 4.0 * B * (d.S + d.K0 + (double)d.T * d.Wd[0]), st);
-  dim3 grid(B, d.P[0] / 128);
+  const int ky = d.P[0] / 128;
+  int bx = (148 * 16 + ky - 1) / ky;  // ~16 resident 128-thread blocks per SM in total
+  if (bx > B) bx = B;
+  if (bx < 1) bx = 1;
+  dim3 grid(bx, ky);
   enc_fwd_kernel<<<grid, 128, 0, st>>>(B, d.S, d.E, d.K0, d.Wd[0], d.T, obs, mu, sigma, A, bits0);
   SPK_LAUNCHED();
   return SPIKERL_OK;

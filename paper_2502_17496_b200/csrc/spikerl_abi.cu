@@ -329,7 +329,7 @@ size_t spikerl_actor_bf16_bytes(const spikerl_actor_cfg* cfg) {
 
 size_t spikerl_critic_bf16_bytes(const spikerl_critic_cfg* cfg) {
   CriticDims d;
-  return critic_dims(cfg, &d) == SPIKERL_OK ? align_up(d.off[SPIKERL_CRITIC_NPARAM] * 2, 16) : 0;
+  return critic_dims(cfg, &d) == SPIKERL_OK ? align_up(critic_bf16_elems(d) * 2, 16) : 0;
 }
 
 size_t spikerl_actor_tape_bytes(const spikerl_actor_cfg* cfg, int batch) {
@@ -384,9 +384,11 @@ int spikerl_critic_refresh_bf16(const spikerl_critic_cfg* cfg, int n_critics, co
                                 void* params_bf16, spikerl_stream_t stream) {
   CriticDims d;
   SPK_TRY(critic_dims(cfg, &d));
-  if (!params || !params_bf16 || n_critics < 1) { set_error("bad refresh arguments"); return SPIKERL_E_ARG; }
-  return launch_f32_to_bf16(params, (__nv_bfloat16*)params_bf16, d.off[SPIKERL_CRITIC_NPARAM] * n_critics,
-                            (cudaStream_t)stream);
+  if (!params || !params_bf16 || n_critics != 2) {
+    set_error("bad refresh arguments (the bf16 working copy holds a twin pair: n_critics must be 2)");
+    return SPIKERL_E_ARG;
+  }
+  return launch_critic_refresh(d, params, (__nv_bfloat16*)params_bf16, (cudaStream_t)stream);
 }
 
 static const unsigned long long kTapeMagic = 0x5350494b45524c31ULL;  // "SPIKERL1"
@@ -536,7 +538,7 @@ int spikerl_td3_update(const spikerl_actor_cfg* acfg, const spikerl_critic_cfg* 
   SPK_TRY(spikerl_allreduce_grads(comm, b->grad_critic, 2 * Pc, stream));
   SPK_TRY(launch_adam(b->critic, b->grad_critic, b->m_critic, b->v_critic, 2 * Pc, b->adam_steps, hp->lr_critic,
                       hp->beta1, hp->beta2, hp->eps, 0, 0, 0.f, (unsigned int*)(b->adam_steps + 1), st));
-  if (ad.bf16) SPK_TRY(launch_f32_to_bf16(b->critic, (__nv_bfloat16*)b->critic_bf16, 2 * Pc, st));
+  if (ad.bf16) SPK_TRY(launch_critic_refresh(cd, b->critic, (__nv_bfloat16*)b->critic_bf16, st));
   // 4. delayed actor update + targets
   if (step % hp->policy_delay == 0) {
     SPK_TRY(actor_forward_impl(ad, B, b->actor, abf, s, api, tape, st));
@@ -554,7 +556,7 @@ int spikerl_td3_update(const spikerl_actor_cfg* acfg, const spikerl_critic_cfg* 
     if (ad.bf16) {
       SPK_TRY(launch_actor_refresh_bf16(ad, b->actor, (__nv_bfloat16*)b->actor_bf16, st));
       SPK_TRY(launch_actor_refresh_bf16(ad, b->actor_t, (__nv_bfloat16*)b->actor_t_bf16, st));
-      SPK_TRY(launch_f32_to_bf16(b->critic_t, (__nv_bfloat16*)b->critic_t_bf16, 2 * Pc, st));
+      SPK_TRY(launch_critic_refresh(cd, b->critic_t, (__nv_bfloat16*)b->critic_t_bf16, st));
     }
   }
   return SPIKERL_OK;

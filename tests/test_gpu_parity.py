@@ -173,23 +173,24 @@ def test_forward_deterministic_and_accumulate():
 
 
 # ------------------------------------------------------------------ critic
-@pytest.mark.parametrize("prec,B", [("fp32", 100), ("bf16", 256), ("bf16", 4096)])
-def test_critic_parity(prec, B):
+@pytest.mark.parametrize("prec,B,S,A", [("fp32", 100, 17, 6), ("bf16", 256, 17, 6), ("bf16", 4096, 17, 6),
+                                        ("bf16", 100, 376, 17), ("bf16", 512, 111, 8), ("bf16", 37, 17, 6)])
+def test_critic_parity(prec, B, S, A):
     import torch
     import paper_2502_17496_b200 as pk
     rng = np.random.default_rng(5)
-    cs = sg.CriticShape(23, precision=prec)
+    cs = sg.CriticShape(S + A, precision=prec)
     c1, c2 = sg.critic_params(cs, rng), sg.critic_params(cs, rng)
     for c in (c1, c2):
         for k in ("b1", "b2", "b3"):
             c[k] = rng.uniform(-0.2, 0.2, c[k].shape).astype(np.float32)
-    batch = sg.replay_batch(rng, B, 17, 6)
+    batch = sg.replay_batch(rng, B, S, A)
     y = rng.standard_normal(B).astype(np.float32)
-    tc = pk.TwinCritic(pk.critic_cfg(23, precision=prec), B)
+    tc = pk.TwinCritic(pk.critic_cfg(S + A, precision=prec), B)
     tc.load(c1, c2)
     obs = torch.from_numpy(batch["s"]).cuda(); act = torch.from_numpy(batch["a"]).cuda()
     yt = torch.from_numpy(y).cuda()
-    ga = torch.zeros(B, 6, device="cuda")
+    ga = torch.zeros(B, A, device="cuda")
     q = tc(obs, act, yt).cpu().numpy()
     grads = tc.grads.cpu().numpy()
     loss = float(tc.loss.cpu())
@@ -210,7 +211,7 @@ def test_critic_parity(prec, B):
             assert rel_l2(mine[k].reshape(gr[k].shape), gr[k]) <= gt, (i, k)
         if i == 0:
             _, dx = oracle.critic_backward(cp, cache, np.full(B, -1.0 / B), prec, need_param_grads=False)
-            assert rel_l2(ga, dx[:, 17:]) <= gt
+            assert rel_l2(ga, dx[:, S:]) <= gt
     assert abs(loss - lref) <= gt * abs(lref)
 
 
