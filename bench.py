@@ -58,17 +58,60 @@ def peaks():
 
 # ---------------------------------------------------------------------------------- clocks
 class ClockSampler:
+    """SM clock + throttle reasons during the timed region: NVML polled every ~2 ms from a thread
+    (a latency-bound timed region lasts only tens of ms), nvidia-smi as the fallback."""
     Q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
          "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
          "clocks_event_reasons.sw_power_cap")
 
     def __init__(self, index):
         self.index, self.proc, self.lines = index, None, []
+        self.nvml = None
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self.nvml = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(index)
+        except Exception:
+            self.nvml = None
 
     def start(self):
+        if self.nvml is not None:
+            self.samples, self.reasons, self.stop_flag = [], 0, False
+            nv = self.nvml
+
+            def poll():
+                while not self.stop_flag:
+                    try:
+                        self.samples.append(nv.nvmlDeviceGetClockInfo(self.h, nv.NVML_CLOCK_SM))
+                        self.reasons |= nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+                    except Exception:
+                        pass
+                    time.sleep(0.002)
+            self.t = threading.Thread(target=poll, daemon=True)
+            self.t.start()
+            return
+        self._start_smi()
+
+    def _stop_nvml(self):
+        self.stop_flag = True
+        self.t.join(timeout=2)
+        nv = self.nvml
+        mx = None
+        try:
+            mx = nv.nvmlDeviceGetMaxClockInfo(self.h, nv.NVML_CLOCK_SM)
+        except Exception:
+            pass
+        names = {0x8: "hw_slowdown", 0x40: "hw_thermal_slowdown", 0x20: "sw_thermal_slowdown", 0x4: "sw_power_cap"}
+        reasons = sorted(n for bit, n in names.items() if self.reasons & bit)
+        sm = sorted(self.samples)
+        return {"sm_mhz": sm[len(sm) // 2] if sm else None, "sm_max_mhz": mx, "reasons": reasons,
+                "samples": len(sm), "source": "nvml"}
+
+    def _start_smi(self):
         try:
             self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
-                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                          "--format=csv,noheader,nounits", "-lms", "20"],
                                          stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             self.t = threading.Thread(target=self._read, daemon=True)
             self.t.start()
@@ -80,6 +123,8 @@ class ClockSampler:
             self.lines.append(line.strip())
 
     def stop(self):
+        if self.nvml is not None:
+            return self._stop_nvml()
         if not self.proc:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
         self.proc.terminate()

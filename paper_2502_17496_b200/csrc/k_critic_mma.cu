@@ -436,7 +436,7 @@ int critic_mma_fwd_bwd(const CriticDims& c, int B, const float* params2, const _
   const bool need_bwd = want_params || grad_act != nullptr;
   const long long oW3 = (long long)c.off[SPIKERL_CRITIC_W3];
   {
-    ProfScope ps_("critic_fwd_mma", PB_LATENCY, 2.0 * B * nz * ((double)c.in * HW + (double)HW * HW + HW), 0.0, st);
+    ProfScope ps_("critic_fwd_mma", PB_TENSOR, 2.0 * B * nz * ((double)c.in * HW + (double)HW * HW + HW), 0.0, st);
     dim3 grid(Bp / RB, nz);
     critic_fwd_mma_kernel<<<grid, 256, 0, st>>>(
         B, Bp, S, A, L.inp, L.inq, obs, act, pb, L.P, L.tb, L.W1p, L.W2c, oW3, params2,
@@ -456,14 +456,14 @@ int critic_mma_fwd_bwd(const CriticDims& c, int B, const float* params2, const _
     nb = 1;
   }
   {
-    ProfScope ps_("critic_bwd_data_mma", PB_LATENCY, 2.0 * B * nb * ((double)HW * HW), 0.0, st);
+    ProfScope ps_("critic_bwd_data_mma", PB_TENSOR, 2.0 * B * nb * ((double)HW * HW), 0.0, st);
     dim3 grid(Bp / RB, nb);
     critic_bwd_data_mma_kernel<<<grid, 256, 0, st>>>(B, Bp, S, A, L.inp, w.dq, pb, L.P, L.tb, oW3, L.W1T, L.W2T, w.Z1,
                                                      w.Z2, w.dZ2T, w.dZ1T, grad_act, want_params ? 1 : 0);
     SPK_LAUNCHED();
   }
   if (want_params) {
-    ProfScope ps_("critic_wgrad_mma", PB_LATENCY, 2.0 * B * nz * ((double)HW * HW + (double)HW * c.in), 0.0, st);
+    ProfScope ps_("critic_wgrad_mma", PB_TENSOR, 2.0 * B * nz * ((double)HW * HW + (double)HW * c.in), 0.0, st);
     dim3 grid(cdiv(L.inq > HW ? L.inq : HW, 256), 2 * (HW / RB), nz);
     critic_wgrad_mma_kernel<<<grid, 256, 0, st>>>(Bp, c.in, L.inq, L.P, (long long)c.off[SPIKERL_CRITIC_W1],
                                                   (long long)c.off[SPIKERL_CRITIC_W2], w.XT, w.H1T, w.dZ2T, w.dZ1T,
