@@ -106,6 +106,28 @@ def test_actor_bf16(name, B, engine):
     print(name, B, engine, st)
 
 
+@pytest.mark.parametrize("T,B", [(1, 17), (2, 1), (3, 50), (5, 1), (8, 33), (16, 19), (24, 40)])
+def test_actor_bf16_tcgen05_edges(T, B):
+    """tcgen05 engine on odd widths (padding rows/cols), ragged and tiny batches and every
+    batch-tile shape the tile chooser can pick (T*Bt in {16..256})."""
+    shape = sg.ActorShape(5, 3, pop_enc=7, pop_dec=9, n1=45, n2=161, T=T, precision="bf16")
+    p, s, g = _inputs(shape, B, seed=10 + T)
+    check_actor(run_gpu_actor(shape, B, p, s, g, engine="tcgen05"), shape, p, s, g)
+
+
+def test_engines_agree_on_spikes():
+    """tcgen05 and SIMT engines compute the same currents up to summation order: their spike
+    planes agree except for decisions within 1e-5 of the threshold (none expected here)."""
+    shape, _, _ = sg.preset("cfg2")
+    p, s, g = _inputs(shape, 96, seed=21)
+    a = run_gpu_actor(shape, 96, p, s, g, engine="tcgen05")
+    b = run_gpu_actor(shape, 96, p, s, g, engine="simt")
+    for l in range(4):
+        assert np.array_equal(a["sp"][f"o{l}"], b["sp"][f"o{l}"]), l
+    for k in a["grads"]:
+        assert rel_l2(a["grads"][k], b["grads"][k]) <= 5e-3, k
+
+
 def test_actor_bf16_cfg4_shape_subsample():
     """configs[4] widths (1024-1024, T=16) on a 64-row sample (teacher forced)."""
     shape, _, _ = sg.preset("cfg4")
