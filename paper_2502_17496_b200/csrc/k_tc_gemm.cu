@@ -40,7 +40,8 @@ constexpr int DW_BN = 256;
 
 struct Params {
   int T, B, Bt, BN;
-  int m_tiles, n_tiles, k_blocks, kps, n_units;
+  int m_tiles, n_tiles, k_blocks, kps, n_units;   // m_tiles: 128-row tiles per CTA group
+  int cg;                                          // 1 = one CTA, 2 = CTA pair (cta_group::2)
   // FWD
   const uint32_t* bits_in; int w_in;
   uint32_t* bits_out; uint32_t* mask_out; int w_out; uint8_t* counts; int n_valid; int n3;
@@ -116,10 +117,10 @@ __device__ __forceinline__ uint64_t make_desc(uint32_t saddr, uint32_t lbo_bytes
   d |= (uint64_t)2 << 61;  // SWIZZLE_128B
   return d;
 }
-// instruction descriptor: bf16 x bf16 -> f32, M = 128
-__host__ __device__ constexpr uint32_t make_idesc(int N, int a_mn, int b_mn) {
+// instruction descriptor: bf16 x bf16 -> f32, M = 128 (one CTA) or 256 (CTA pair)
+__host__ __device__ constexpr uint32_t make_idesc(int N, int a_mn, int b_mn, int M = BM) {
   return (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)a_mn << 15) | ((uint32_t)b_mn << 16) |
-         ((uint32_t)(N >> 3) << 17) | ((uint32_t)(BM >> 4) << 24);
+         ((uint32_t)(N >> 3) << 17) | ((uint32_t)(M >> 4) << 24);
 }
 __device__ __forceinline__ void mma_bf16(uint32_t d_tmem, uint64_t adesc, uint64_t bdesc, uint32_t idesc, uint32_t acc) {
   asm volatile(
@@ -166,12 +167,73 @@ __device__ __forceinline__ uint32_t byte_of(const uint4& q, int i) {
   return (w >> ((i & 3) * 8)) & 0xFFu;
 }
 
+// ---- CTA-pair (cta_group::2) helpers: M = 256 per pair, A split by rows, B split by columns
+__device__ __forceinline__ uint32_t cluster_ctarank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ void cluster_sync_all() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+// arrive on the barrier at the same shared-memory offset in CTA rank 0 of the pair. Default
+// (.release.cta) semantics: the data this arrival publishes is either shared memory already made
+// visible to the async proxy by fence.proxy.async (expanders) or TMEM reads ordered by
+// tcgen05.fence::before_thread_sync (epilogue), both consumed by tcgen05 ops the leader issues.
+// A .release.cluster arrive costs a MEMBAR.ALL.GPU per arrival (ncu: 1.6x slower FWD).
+__device__ __forceinline__ void mbar_arrive_leader(uint64_t* bar) {
+  uint32_t r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, 0;" : "=r"(r) : "r"(smem_u32(bar)));
+  asm volatile("mbarrier.arrive.shared::cluster.b64 _, [%0];" ::"r"(r) : "memory");
+}
+constexpr uint32_t kPeerBitMask = 0xFEFFFFFFu;   // shared::cluster address of the pair leader
+__device__ __forceinline__ void tma_2d_cg2(const CUtensorMap* map, void* dst, uint64_t* bar, int c0, int c1) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4}], [%2];" ::"r"(
+          smem_u32(dst)),
+      "l"(map), "r"(smem_u32(bar) & kPeerBitMask), "r"(c0), "r"(c1)
+      : "memory");
+}
+__device__ __forceinline__ void tma_3d_cg2(const CUtensorMap* map, void* dst, uint64_t* bar, int c0, int c1, int c2) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4, %5}], [%2];" ::"r"(
+          smem_u32(dst)),
+      "l"(map), "r"(smem_u32(bar) & kPeerBitMask), "r"(c0), "r"(c1), "r"(c2)
+      : "memory");
+}
+__device__ __forceinline__ void tmem_alloc_cg2(uint32_t* dst, uint32_t ncols) {
+  asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(dst)), "r"(ncols)
+               : "memory");
+  asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;" ::: "memory");
+}
+__device__ __forceinline__ void tmem_dealloc_cg2(uint32_t taddr, uint32_t ncols) {
+  asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(taddr), "r"(ncols) : "memory");
+}
+__device__ __forceinline__ void mma_bf16_cg2(uint32_t d_tmem, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
+                                             uint32_t acc) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n}" ::"r"(d_tmem),
+      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(acc)
+      : "memory");
+}
+// commit to the barrier at the same offset in both CTAs of the pair
+__device__ __forceinline__ void mma_commit_pair(uint64_t* bar) {
+  asm volatile(
+      "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(
+          smem_u32(bar)),
+      "h"((uint16_t)3)
+      : "memory");
+}
+
 struct Tile { int m, n, kb0, kb1, split; };
 
+// unit u -> this CTA's tile; p.m_tiles counts 128-row tiles per CTA group (pairs when CG = 2)
 template <int MODE>
-__device__ __forceinline__ Tile decode(const Params& p, int u) {
+__device__ __forceinline__ Tile decode(const Params& p, int u, int rank, int CG) {
   Tile t;
-  t.m = u % p.m_tiles;
+  t.m = (u % p.m_tiles) * CG + rank;
   int rest = u / p.m_tiles;
   if (MODE == DW) {
     t.n = rest % p.n_tiles;
@@ -191,7 +253,11 @@ __device__ __forceinline__ Tile decode(const Params& p, int u) {
 // Expander prefetch depth (k-blocks of spike words kept in registers ahead of the smem ring).
 constexpr int PF = 4;
 
-template <int MODE, int BT>
+// CG = 1: one CTA computes a 128-row tile. CG = 2: a CTA pair (cluster of 2) computes a 256-row
+// tile with tcgen05.mma.cta_group::2 issued by rank 0: each CTA holds its 128 rows of A and half
+// of the B columns, every TMA / expander / epilogue completion signals rank 0's barriers, and the
+// MMA commits multicast back to both CTAs.
+template <int MODE, int BT, int CG>
 __global__ void __launch_bounds__(NUM_THREADS, 1)
     tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, const Params p) {
   extern __shared__ uint8_t smem_raw[];
@@ -205,56 +271,74 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
   constexpr bool A_MN = (MODE != FWD);
   constexpr bool B_MN = (MODE == DW);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int rank = CG == 2 ? (int)cluster_ctarank() : 0;
+  const int cid = blockIdx.x / CG, ncl = gridDim.x / CG;   // pair (or CTA) index and count
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < STAGES; ++s) {
-      mbar_init(&full[s], 1 + (B_EXPAND ? NUM_EXP_WARPS : 0));
+      mbar_init(&full[s], 1 + (B_EXPAND ? CG * NUM_EXP_WARPS : 0));
       mbar_init(&empty[s], 1);
     }
     for (int a = 0; a < 2; ++a) {
       mbar_init(&tfull[a], 1);
-      mbar_init(&tempty[a], NUM_EPI_WARPS);
+      mbar_init(&tempty[a], CG * NUM_EPI_WARPS);
     }
     fence_barrier_init();
   }
-  if (warp == 1) tmem_alloc(tmem_slot, TMEM_COLS);
+  if (warp == 1) {
+    if (CG == 2) tmem_alloc_cg2(tmem_slot, TMEM_COLS);
+    else tmem_alloc(tmem_slot, TMEM_COLS);
+  }
   tc_fence_before();
   __syncthreads();
+  if (CG == 2) cluster_sync_all();   // the peer's barriers exist before any remote arrive
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
 
   if (warp == 0) {
-    // ===================== TMA producer =====================
+    // ===================== TMA producer (both CTAs load their own halves) =====================
     if (lane == 0) {
       uint32_t it = 0;
-      const uint32_t bytes_b = (MODE == DX) ? 128u * p.T * p.Bt : (MODE == ENC ? 128u * p.BN : 0u);
-      for (int u = blockIdx.x; u < p.n_units; u += gridDim.x) {
-        const Tile t = decode<MODE>(p, u);
+      const uint32_t bytes_b = (MODE == DX) ? 128u * p.T * p.Bt / CG : (MODE == ENC ? 128u * p.BN / CG : 0u);
+      for (int u = cid; u < p.n_units; u += ncl) {
+        const Tile t = decode<MODE>(p, u, rank, CG);
         for (int kb = t.kb0; kb < t.kb1; ++kb, ++it) {
           const int stage = it % STAGES;
           const uint32_t ph = (it / STAGES) & 1;
           mbar_wait(&empty[stage], ph ^ 1);
           uint8_t* sA = smem + stage * STAGE_BYTES;
           uint8_t* sB = sA + A_STAGE;
-          mbar_expect_tx(&full[stage], (uint32_t)A_STAGE + bytes_b);
-          if (!A_MN) {
-            tma_2d(&tmA, sA, &full[stage], kb * BK, t.m * BM);
+          if (CG == 1) {
+            mbar_expect_tx(&full[stage], (uint32_t)A_STAGE + bytes_b);
+            if (!A_MN) {
+              tma_2d(&tmA, sA, &full[stage], kb * BK, t.m * BM);
+            } else {
+              tma_2d(&tmA, sA, &full[stage], t.m * BM, kb * BK);
+              tma_2d(&tmA, sA + 8192, &full[stage], t.m * BM + 64, kb * BK);
+            }
+            if (MODE == DX) tma_3d(&tmB, sB, &full[stage], kb * BK, t.n * p.Bt, 0);
+            if (MODE == ENC) tma_2d(&tmB, sB, &full[stage], kb * BK, t.n * p.BN);
           } else {
-            tma_2d(&tmA, sA, &full[stage], t.m * BM, kb * BK);
-            tma_2d(&tmA, sA + 8192, &full[stage], t.m * BM + 64, kb * BK);
+            if (rank == 0) mbar_expect_tx(&full[stage], 2u * ((uint32_t)A_STAGE + bytes_b));
+            if (!A_MN) {
+              tma_2d_cg2(&tmA, sA, &full[stage], kb * BK, t.m * BM);
+            } else {
+              tma_2d_cg2(&tmA, sA, &full[stage], t.m * BM, kb * BK);
+              tma_2d_cg2(&tmA, sA + 8192, &full[stage], t.m * BM + 64, kb * BK);
+            }
+            if (MODE == DX) tma_3d_cg2(&tmB, sB, &full[stage], kb * BK, t.n * p.Bt, rank * (p.T / 2));
+            if (MODE == ENC) tma_2d_cg2(&tmB, sB, &full[stage], kb * BK, t.n * p.BN + rank * (p.BN / 2));
           }
-          if (MODE == DX) tma_3d(&tmB, sB, &full[stage], kb * BK, t.n * p.Bt, 0);
-          if (MODE == ENC) tma_2d(&tmB, sB, &full[stage], kb * BK, t.n * p.BN);
         }
       }
     }
   } else if (warp == 1) {
-    // ===================== MMA issuer =====================
-    if (lane == 0) {
+    // ===================== MMA issuer (rank 0 of a pair) =====================
+    if (lane == 0 && rank == 0) {
       uint32_t it = 0, titer = 0;
-      const uint32_t idesc = make_idesc(p.BN, A_MN ? 1 : 0, B_MN ? 1 : 0);
-      for (int u = blockIdx.x; u < p.n_units; u += gridDim.x, ++titer) {
-        const Tile t = decode<MODE>(p, u);
+      const uint32_t idesc = make_idesc(p.BN, A_MN ? 1 : 0, B_MN ? 1 : 0, BM * CG);
+      for (int u = cid; u < p.n_units; u += ncl, ++titer) {
+        const Tile t = decode<MODE>(p, u, rank, CG);
         const uint32_t a = titer & 1, aph = (titer >> 1) & 1;
         mbar_wait(&tempty[a], aph ^ 1);
         tc_fence_after();
@@ -270,11 +354,14 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
           for (int kk = 0; kk < BK / 16; ++kk) {
             const uint64_t ad = A_MN ? make_desc(sA + kk * 2048, 8192, 1024) : make_desc(sA + kk * 32, 16, 1024);
             const uint64_t bd = B_MN ? make_desc(sB + kk * 2048, 8192, 1024) : make_desc(sB + kk * 32, 16, 1024);
-            mma_bf16(d_tmem, ad, bd, idesc, (kb > t.kb0 || kk > 0) ? 1u : 0u);
+            if (CG == 2) mma_bf16_cg2(d_tmem, ad, bd, idesc, (kb > t.kb0 || kk > 0) ? 1u : 0u);
+            else mma_bf16(d_tmem, ad, bd, idesc, (kb > t.kb0 || kk > 0) ? 1u : 0u);
           }
-          mma_commit(&empty[stage]);
+          if (CG == 2) mma_commit_pair(&empty[stage]);
+          else mma_commit(&empty[stage]);
         }
-        mma_commit(&tfull[a]);
+        if (CG == 2) mma_commit_pair(&tfull[a]);
+        else mma_commit(&tfull[a]);
       }
     }
   } else if (warp < EPI_WARP0) {
@@ -284,17 +371,19 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     if (B_EXPAND) {
       const int et = threadIdx.x - EXP_WARP0 * 32;
       uint32_t it = 0;
-      for (int u = blockIdx.x; u < p.n_units; u += gridDim.x) {
-        const Tile t = decode<MODE>(p, u);
+      for (int u = cid; u < p.n_units; u += ncl) {
+        const Tile t = decode<MODE>(p, u, rank, CG);
         if (MODE == FWD) {
-          // K-major: row = t*Bt + j (spike row (t, b)), one k-block = 2 words = 8 chunks of 16 B
-          const int rows = p.T * p.Bt;
+          // K-major: row = t*Bt + j (spike row (t, b)), one k-block = 2 words = 8 chunks of 16 B;
+          // a CTA of a pair expands its half of the rows (the MMA's B columns) into local rows
+          const int rows = p.T * p.Bt / CG;
           const uint32_t* rp[2];
           bool rv[2];
 #pragma unroll
           for (int i = 0; i < 2; ++i) {
             const int row = et + 128 * i;
-            const int tt = row / p.Bt, j = row - tt * p.Bt;
+            const int rg = rank * rows + row;
+            const int tt = rg / p.Bt, j = rg - tt * p.Bt;
             const int b = t.n * p.Bt + j;
             rv[i] = row < rows && b < p.B;
             rp[i] = rv[i] ? p.bits_in + ((size_t)tt * p.B + b) * p.w_in : p.bits_in;
@@ -335,51 +424,60 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
             }
             fence_proxy_async();
             __syncwarp();
-            if (lane == 0) mbar_arrive(&full[stage]);
+            if (lane == 0) {
+              if (CG == 2) mbar_arrive_leader(&full[stage]);
+              else mbar_arrive(&full[stage]);
+            }
           }
         } else {
-          // MN-major: K row r = one (t,b) row, 256 output columns = 8 words; thread = (row, half)
-          const int r = et >> 1, half = et & 1;
-          const int wcol = t.n * (DW_BN / 32) + 4 * half;
+          // MN-major: K row r = one (t,b) row, 256 output columns = 8 words (4 atoms of 64); a CTA
+          // of a pair expands its 128 columns (2 atoms, 4 words). thread = (row, part)
+          constexpr int WPT = 4 / CG;                  // words per thread per k-block
+          const int r = et >> 1, part = et & 1;
+          const int wcol = t.n * (DW_BN / 32) + rank * 4 + WPT * part;
           const bool cv = wcol < p.w_dw;
-          uint4 q[PF];
-#pragma unroll
-          for (int f = 0; f < PF; ++f) {
-            const int kb = t.kb0 + f;
+          uint32_t q[PF][WPT];
+          auto ldw = [&](uint32_t (&dst)[WPT], int kb) {
             const int rg = kb * BK + r;
-            q[f] = (cv && kb < t.kb1 && rg < p.R)
-                       ? __ldg(reinterpret_cast<const uint4*>(p.bits_dw + (size_t)rg * p.w_dw + wcol))
-                       : make_uint4(0u, 0u, 0u, 0u);
-          }
+            const bool ok = cv && kb < t.kb1 && rg < p.R;
+            const uint32_t* src = p.bits_dw + (size_t)rg * p.w_dw + wcol;
+            if (WPT == 4) {
+              const uint4 v = ok ? __ldg(reinterpret_cast<const uint4*>(src)) : make_uint4(0u, 0u, 0u, 0u);
+              dst[0] = v.x; dst[1 % WPT] = v.y; dst[2 % WPT] = v.z; dst[3 % WPT] = v.w;
+            } else {
+              const uint2 v = ok ? __ldg(reinterpret_cast<const uint2*>(src)) : make_uint2(0u, 0u);
+              dst[0] = v.x; dst[1 % WPT] = v.y;
+            }
+          };
+#pragma unroll
+          for (int f = 0; f < PF; ++f) ldw(q[f], t.kb0 + f);
           for (int kb = t.kb0; kb < t.kb1; ++kb, ++it) {
             const int stage = it % STAGES;
             const uint32_t ph = (it / STAGES) & 1;
             mbar_wait(&empty[stage], ph ^ 1);
             const uint32_t sB = smem_u32(smem + stage * STAGE_BYTES + A_STAGE);
             const uint32_t sw = r & 7;
-            const uint32_t w4[4] = {q[0].x, q[0].y, q[0].z, q[0].w};
 #pragma unroll
-            for (int wi = 0; wi < 4; ++wi) {
-              const int atom = 2 * half + (wi >> 1), hw = wi & 1;
+            for (int wi = 0; wi < WPT; ++wi) {
+              const int atom = (WPT * part + wi) >> 1, hw = wi & 1;
               const uint32_t base = sB + atom * 8192 + r * 128;
 #pragma unroll
               for (int c = 0; c < 4; ++c) {
                 const int chunk = hw * 4 + c;
-                st_shared_v4(base + ((chunk ^ sw) << 4), expand_byte((w4[wi] >> (8 * c)) & 0xFFu));
+                st_shared_v4(base + ((chunk ^ sw) << 4), expand_byte((q[0][wi] >> (8 * c)) & 0xFFu));
               }
             }
 #pragma unroll
-            for (int f = 0; f < PF - 1; ++f) q[f] = q[f + 1];
-            {
-              const int kn = kb + PF;
-              const int rg = kn * BK + r;
-              q[PF - 1] = (cv && kn < t.kb1 && rg < p.R)
-                              ? __ldg(reinterpret_cast<const uint4*>(p.bits_dw + (size_t)rg * p.w_dw + wcol))
-                              : make_uint4(0u, 0u, 0u, 0u);
-            }
+            for (int f = 0; f < PF - 1; ++f)
+#pragma unroll
+              for (int wi = 0; wi < WPT; ++wi) q[f][wi] = q[f + 1][wi];
+            ldw(q[PF - 1], kb + PF);
             fence_proxy_async();
             __syncwarp();
-            if (lane == 0) mbar_arrive(&full[stage]);
+            if (lane == 0) {
+              if (CG == 2) mbar_arrive_leader(&full[stage]);
+              else mbar_arrive(&full[stage]);
+            }
           }
         }
       }
@@ -390,8 +488,8 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     const int q = warp & 3;
     const int g = (warp - EPI_WARP0) >> 2;
     uint32_t titer = 0;
-    for (int u = blockIdx.x; u < p.n_units; u += gridDim.x, ++titer) {
-      const Tile t = decode<MODE>(p, u);
+    for (int u = cid; u < p.n_units; u += ncl, ++titer) {
+      const Tile t = decode<MODE>(p, u, rank, CG);
       const uint32_t a = titer & 1, aph = (titer >> 1) & 1;
       mbar_wait(&tfull[a], aph);
       tc_fence_after();
@@ -578,53 +676,20 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       }
       tc_fence_before();
       __syncwarp();
-      if (lane == 0) mbar_arrive(&tempty[a]);
+      if (lane == 0) {
+        if (CG == 2) mbar_arrive_leader(&tempty[a]);
+        else mbar_arrive(&tempty[a]);
+      }
     }
   }
   tc_fence_before();
   __syncthreads();
+  if (CG == 2) cluster_sync_all();   // no CTA of the pair releases smem / TMEM the other still uses
   if (warp == 1) {
     tc_fence_after();
-    tmem_dealloc(tmem, TMEM_COLS);
+    if (CG == 2) tmem_dealloc_cg2(tmem, TMEM_COLS);
+    else tmem_dealloc(tmem, TMEM_COLS);
   }
-}
-
-// Bit-plane transpose [T][B][P/32] (word = 32 neurons of one (t,b)) -> [T][ceil(B/32)][P]
-// (word = 32 batch rows of one (t, neuron)): one warp per 32x32 bit block, 32 ballots; loads hit
-// one word per batch row, stores are 128 B coalesced. Feeds the DX epilogue's per-neuron bits.
-// One block per (t, 32-row batch chunk): the 32 x W word tile is read coalesced into shared
-// memory, then each warp transposes 32x32 bit blocks with ballots and writes 128 B rows.
-constexpr int TR_MAXW = 64;  // P <= 2048 (hidden layers)
-__global__ void __launch_bounds__(256) bits_transpose_kernel(int T, int B, int P, const uint32_t* __restrict__ in,
-                                                              uint32_t* __restrict__ out) {
-  __shared__ uint32_t s[32][TR_MAXW + 1];
-  const int W = P >> 5, BW = (B + 31) >> 5;
-  const int bw = blockIdx.x % BW, t = blockIdx.x / BW;
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  for (int i = threadIdx.x; i < 32 * W; i += 256) {
-    const int r = i / W, c = i - r * W;
-    const int b = bw * 32 + r;
-    s[r][c] = b < B ? __ldg(in + ((size_t)t * B + b) * W + c) : 0u;
-  }
-  __syncthreads();
-  for (int w = warp; w < W; w += 8) {
-    const uint32_t x = s[lane][w];
-    uint32_t mine = 0;
-#pragma unroll
-    for (int n = 0; n < 32; ++n) {
-      const uint32_t r = __ballot_sync(0xffffffffu, (x >> n) & 1u);
-      if (lane == n) mine = r;
-    }
-    out[((size_t)t * BW + bw) * P + w * 32 + lane] = mine;
-  }
-}
-
-int launch_bits_transpose(int T, int B, int P, const uint32_t* in, uint32_t* out, cudaStream_t st) {
-  ProfScope ps_("bits_transpose", PB_HBM, 0.0, 8.0 * T * (double)B * (P / 32), st);
-  if (P / 32 > TR_MAXW) { set_error("bits_transpose: width %d too large", P); return SPIKERL_E_UNSUPPORTED; }
-  bits_transpose_kernel<<<(unsigned)(T * ((B + 31) / 32)), 256, 0, st>>>(T, B, P, in, out);
-  SPK_LAUNCHED();
-  return SPIKERL_OK;
 }
 
 // dW[n][k] (master layout) = sum over splits (fixed order) of the partial tiles
@@ -685,18 +750,83 @@ static int num_sms() {
   return n;
 }
 
-template <int MODE, int BT>
-static int launch(const CUtensorMap& ma, const CUtensorMap& mb, const Params& p, cudaStream_t st) {
+// Co-resident CTA pairs: every tc_kernel instance uses one CTA per SM (SMEM_BYTES), so one query
+// answers for all; cached so the split-K plan and the launch always agree.
+static int pair_slots() {
+  static int slots = 0;
+  if (!slots) {
+    cudaFuncSetAttribute(tc_kernel<FWD, 8, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES);
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(num_sms() / 2 * 2, 1, 1);
+    cfg.blockDim = dim3(NUM_THREADS, 1, 1);
+    cfg.dynamicSmemBytes = SMEM_BYTES;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = 2;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    int nc = 0;
+    if (cudaOccupancyMaxActiveClusters(&nc, tc_kernel<FWD, 8, 2>, &cfg) != cudaSuccess || nc <= 0) {
+      cudaGetLastError();
+      nc = num_sms() / 2;
+    }
+    slots = nc;
+  }
+  return slots;
+}
+
+// CTA pairs (cta_group::2) are used when the tile count allows; SPIKERL_TC_PAIR=0 forces single CTAs.
+static bool pairs_enabled() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("SPIKERL_TC_PAIR");
+    v = (e && e[0] == '0') ? 0 : 1;
+  }
+  return v == 1;
+}
+
+template <int MODE, int BT, int CG>
+static int launch_cg(const CUtensorMap& ma, const CUtensorMap& mb, const Params& p, cudaStream_t st) {
   static bool attr = false;
   if (!attr) {
-    cudaError_t e = cudaFuncSetAttribute(tc_kernel<MODE, BT>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES);
+    cudaError_t e =
+        cudaFuncSetAttribute(tc_kernel<MODE, BT, CG>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES);
     if (e != cudaSuccess) { set_error("cudaFuncSetAttribute: %s", cudaGetErrorString(e)); return SPIKERL_E_CUDA; }
     attr = true;
   }
-  const int grid = p.n_units < num_sms() ? p.n_units : num_sms();
-  tc_kernel<MODE, BT><<<grid, NUM_THREADS, SMEM_BYTES, st>>>(ma, mb, p);
+  if (CG == 1) {
+    const int ncta = num_sms();
+    const int grid = p.n_units < ncta ? (int)p.n_units : ncta;
+    tc_kernel<MODE, BT, CG><<<grid, NUM_THREADS, SMEM_BYTES, st>>>(ma, mb, p);
+  } else {
+    cudaLaunchConfig_t cfg = {};
+    cfg.blockDim = dim3(NUM_THREADS, 1, 1);
+    cfg.dynamicSmemBytes = SMEM_BYTES;
+    cfg.stream = st;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = CG;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    // A persistent grid larger than the number of co-resident pairs would run a second wave of
+    // whole pairs; size it to what the GPCs can actually hold (not simply 148 / 2).
+    const int slots = pair_slots();
+    const long long grid = p.n_units < slots ? p.n_units : slots;
+    cfg.gridDim = dim3((unsigned)(grid * CG), 1, 1);
+    cudaError_t e = cudaLaunchKernelEx(&cfg, tc_kernel<MODE, BT, CG>, ma, mb, p);
+    if (e != cudaSuccess) { set_error("cudaLaunchKernelEx (pair): %s", cudaGetErrorString(e)); return SPIKERL_E_CUDA; }
+  }
   SPK_LAUNCHED();
   return SPIKERL_OK;
+}
+
+template <int MODE, int BT>
+static int launch(const CUtensorMap& ma, const CUtensorMap& mb, const Params& p, cudaStream_t st) {
+  return p.cg == 2 ? launch_cg<MODE, BT, 2>(ma, mb, p, st) : launch_cg<MODE, BT, 1>(ma, mb, p, st);
 }
 
 template <int MODE>
@@ -735,7 +865,6 @@ using namespace tc;
 
 bool tc_supported(const ActorDims& d) {
   if (!d.bf16) return false;
-  if (d.P[1] > 32 * TR_MAXW || d.P[2] > 32 * TR_MAXW) return false;
   for (int bt = 8; bt <= DX_MAX_BT; bt *= 2)
     if ((d.T * bt) % 16 == 0 && d.T * bt <= 256) return true;
   return false;
@@ -748,9 +877,11 @@ int launch_lif_fwd_tc(const ActorDims& d, int l, int B, const uint32_t* bits_in,
                 2.0 * d.T * B * (double)d.N[l] * d.N[l - 1], 0.0, st);
   Params p{};
   p.T = d.T; p.B = B;
-  p.m_tiles = d.P[l] / BM;
-  p.Bt = choose_bt(d.T, B, p.m_tiles, FWD_MAX_BT);
+  const int mt = d.P[l] / BM;
+  p.Bt = choose_bt(d.T, B, mt, FWD_MAX_BT);
   p.BN = d.T * p.Bt;
+  p.cg = (pairs_enabled() && mt % 2 == 0) ? 2 : 1;
+  p.m_tiles = mt / p.cg;
   p.n_tiles = (B + p.Bt - 1) / p.Bt;
   p.k_blocks = d.P[l - 1] / BK;
   p.n_units = p.m_tiles * p.n_tiles;
@@ -776,9 +907,11 @@ int launch_lif_dx_tc(const ActorDims& d, int l, int B, const void* Gl, const __n
                 0.0, st);
   Params p{};
   p.T = d.T; p.B = B;
-  p.m_tiles = d.P[l - 1] / BM;
-  p.Bt = choose_bt(d.T, B, p.m_tiles, DX_MAX_BT);
+  const int mt = d.P[l - 1] / BM;
+  p.Bt = choose_bt(d.T, B, mt, DX_MAX_BT);
   p.BN = d.T * p.Bt;
+  p.cg = (pairs_enabled() && mt % 2 == 0 && d.T % 2 == 0) ? 2 : 1;   // B halves split along t
+  p.m_tiles = mt / p.cg;
   p.n_tiles = (B + p.Bt - 1) / p.Bt;
   p.k_blocks = d.P[l] / BK;
   p.n_units = p.m_tiles * p.n_tiles;
@@ -796,7 +929,7 @@ int launch_lif_dx_tc(const ActorDims& d, int l, int B, const void* Gl, const __n
   {  // B = G_l [T][B][P_l]: rows (t, b) t-major per tile, K = P_l
     const uint64_t dims[3] = {(uint64_t)d.P[l], (uint64_t)B, (uint64_t)d.T};
     const uint64_t strides[2] = {(uint64_t)d.P[l] * 2, (uint64_t)d.P[l] * 2 * B};
-    const uint32_t box[3] = {64, (uint32_t)p.Bt, (uint32_t)d.T};
+    const uint32_t box[3] = {64, (uint32_t)p.Bt, (uint32_t)(d.T / p.cg)};
     SPK_TRY(make_map(&mb, Gl, 3, dims, strides, box));
   }
   return launch_bt<DX>(p.Bt, ma, mb, p, st);
@@ -814,7 +947,8 @@ int launch_enc_grad_tc(const ActorDims& d, int B, const void* Gsum, const __nv_b
   Params p{};
   p.T = 1; p.B = B;
   p.BN = B >= 256 ? 256 : round_up(B, 16);
-  p.m_tiles = d.P[0] / BM;
+  p.cg = (pairs_enabled() && (d.P[0] / BM) % 2 == 0) ? 2 : 1;
+  p.m_tiles = d.P[0] / BM / p.cg;
   p.n_tiles = cdiv(B, p.BN);
   p.k_blocks = d.P[1] / BK;
   p.n_units = p.m_tiles * p.n_tiles;
@@ -829,7 +963,7 @@ int launch_enc_grad_tc(const ActorDims& d, int B, const void* Gsum, const __nv_b
   {
     const uint64_t dims[2] = {(uint64_t)d.P[1], (uint64_t)B};
     const uint64_t strides[1] = {(uint64_t)d.P[1] * 2};
-    const uint32_t box[2] = {64, (uint32_t)p.BN};
+    const uint32_t box[2] = {64, (uint32_t)(p.BN / p.cg)};
     SPK_TRY(make_map(&mb, Gsum, 2, dims, strides, box));
   }
   SPK_TRY(launch_bt<ENC>(8, ma, mb, p, st));
@@ -838,11 +972,14 @@ int launch_enc_grad_tc(const ActorDims& d, int B, const void* Gsum, const __nv_b
 
 // split-K plan for dW_l: at least two waves of units, splits chosen to minimise the idle tail of
 // the last wave (persistent grid = #SMs); never an empty split.
+static int dw_cg(const ActorDims& d, int l) { return (pairs_enabled() && (d.P[l] / BM) % 2 == 0) ? 2 : 1; }
+
 void tc_dw_plan(const ActorDims& d, int l, int B, int* splits, int* kps) {
-  const int m_tiles = d.P[l] / BM, n_tiles = cdiv(d.P[l - 1], DW_BN);
+  const int cg = dw_cg(d, l);
+  const int m_tiles = d.P[l] / BM / cg, n_tiles = cdiv(d.P[l - 1], DW_BN);
   const int k_blocks = cdiv((long long)d.T * B, BK);
   const long long mn = (long long)m_tiles * n_tiles;
-  const int sms = num_sms();
+  const int sms = cg == 2 ? pair_slots() : num_sms();   // concurrent units (CTA pairs when cg = 2)
   int s_lo = (int)cdiv(2LL * sms, mn);
   if (s_lo < 1) s_lo = 1;
   int best_s = s_lo;
@@ -877,7 +1014,8 @@ int launch_lif_dw_tc(const ActorDims& d, int l, int B, const void* Gl, const uin
   Params p{};
   p.T = d.T; p.B = B; p.BN = DW_BN;
   p.R = d.T * B;
-  p.m_tiles = d.P[l] / BM;
+  p.cg = dw_cg(d, l);
+  p.m_tiles = d.P[l] / BM / p.cg;
   p.n_tiles = cdiv(d.P[l - 1], DW_BN);
   p.k_blocks = cdiv(p.R, BK);
   int splits, kps;
