@@ -8,6 +8,18 @@
 
 namespace spk {
 
+// SM count of the current device (cached; grids of persistent / grid-strided kernels are sized by it)
+inline int num_sms() {
+  static int n = 0;
+  if (!n) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+    if (n <= 0) n = 148;
+  }
+  return n;
+}
+
 // ----------------------------------------------------------------------------- errors
 void set_error(const char* fmt, ...);
 void note_launch(int n = 1);

@@ -120,9 +120,9 @@ __global__ void __launch_bounds__(128) dec_bwd_outscan_kernel(
     const float* __restrict__ grad_a, const float* __restrict__ act, const float* __restrict__ Wd,
     const uint32_t* __restrict__ bits3, const uint32_t* __restrict__ mask3, GTy* __restrict__ G3,
     float* __restrict__ g_pre_out) {
-  const int b = blockIdx.x;
   const int n = blockIdx.y * 128 + threadIdx.x;
   const int N3 = A * D;
+  for (int b = blockIdx.x; b < B; b += gridDim.x) {
   float g = 0.f;
   if (n < N3) {
     const int j = n / D, e = n % D;
@@ -132,6 +132,27 @@ __global__ void __launch_bounds__(128) dec_bwd_outscan_kernel(
     g = __fdiv_rn(__fmul_rn(gp, Wd[j * D + e]), (float)T);  // g_o3 = g_fr / T, constant in t
   }
   float dvn = 0.f, dcn = 0.f;
+  if (T <= 32) {
+    // all T spike/mask words are loaded first (independent loads) and kept as per-neuron bit masks
+    // over t, so the reverse scan below does not wait on a load per step
+    uint32_t om = 0, hm = 0;
+    if (n < N3) {
+      const uint32_t* po = bits3 + (size_t)b * W3 + (n >> 5);
+      const uint32_t* ph = mask3 + (size_t)b * W3 + (n >> 5);
+      const size_t ts = (size_t)B * W3;
+      for (int t = 0; t < T; ++t) {
+        om |= ((__ldg(po + t * ts) >> (n & 31)) & 1u) << t;
+        hm |= ((__ldg(ph + t * ts) >> (n & 31)) & 1u) << t;
+      }
+    }
+    for (int t = T - 1; t >= 0; --t) {
+      const size_t row = (size_t)t * B + b;
+      float Gt = 0.f;
+      if (n < N3) Gt = lif_back_step(zh, dvc, dcc, g, (om >> t) & 1u, (hm >> t) & 1u, dvn, dcn);
+      GT<GTy>::store(G3 + row * P3 + n, Gt);
+    }
+    continue;
+  }
   for (int t = T - 1; t >= 0; --t) {
     const size_t row = (size_t)t * B + b;
     float Gt = 0.f;
@@ -142,6 +163,7 @@ __global__ void __launch_bounds__(128) dec_bwd_outscan_kernel(
     }
     GT<GTy>::store(G3 + row * P3 + n, Gt);
   }
+  }  // b
 }
 
 int launch_dec_bwd_outscan(const ActorDims& d, int B, const float* grad_a, const float* act,
@@ -149,7 +171,11 @@ int launch_dec_bwd_outscan(const ActorDims& d, int B, const float* grad_a, const
                            const uint32_t* mask3, void* G3, float* g_pre, cudaStream_t st) {
   ProfScope ps_("dec_bwd_outscan", PB_HBM, 0.0, (double)d.T * B * (d.P[3] * (d.bf16 ? 2.0 : 4.0) + 2.0 * d.Wd[3] * 4), st);
   (void)counts;
-  dim3 grid(B, d.P[3] / 128);
+  // grid-strided over b: one 128-thread block per (b, 128 neurons) was block-scheduling bound
+  const int gy = d.P[3] / 128;
+  int gx = (num_sms() * 16 + gy - 1) / gy;
+  if (gx > B) gx = B;
+  dim3 grid(gx, gy);
   if (d.bf16)
     dec_bwd_outscan_kernel<__nv_bfloat16><<<grid, 128, 0, st>>>(
         B, d.T, d.A, d.D, d.P[3], d.Wd[3], d.dc, d.dv, d.zh, grad_a, act, Wd, bits3, mask3,

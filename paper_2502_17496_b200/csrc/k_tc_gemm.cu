@@ -739,17 +739,6 @@ static int make_map(CUtensorMap* m, const void* base, int rank, const uint64_t* 
   return SPIKERL_OK;
 }
 
-static int num_sms() {
-  static int n = 0;
-  if (!n) {
-    int dev = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
-    if (n <= 0) n = 148;
-  }
-  return n;
-}
-
 // Co-resident CTA pairs: every tc_kernel instance uses one CTA per SM (SMEM_BYTES), so one query
 // answers for all; cached so the split-K plan and the launch always agree.
 static int pair_slots() {

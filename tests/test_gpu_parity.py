@@ -51,6 +51,16 @@ def test_encoder_edge_values():
     assert check_encoder(gpu, shape, p, s) == 0
 
 
+@pytest.mark.parametrize("T", [7, 32, 33, 70])
+def test_encoder_timesteps(T):
+    """Unrolled (T in the compiled set) and runtime-T (chunks of 32 steps) encoder variants."""
+    shape = sg.with_(sg.preset("cfg2")[0], T=T)
+    p, s, _ = _inputs(shape, 45, seed=T)
+    gpu = run_gpu_actor(shape, 45, p, s, None, engine="simt")
+    from tests._parity import check_encoder
+    assert check_encoder(gpu, shape, p, s) == 0
+
+
 # ------------------------------------------------------------------ fp32 actor (configs[0])
 def test_actor_fp32_cfg0():
     shape, _, B = sg.preset("cfg0")
