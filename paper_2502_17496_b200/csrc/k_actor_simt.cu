@@ -114,6 +114,22 @@ int launch_dec_fwd(const ActorDims& d, int B, const uint8_t* counts, const float
 }
 
 // ------------------------------------------------------- decoder backward + output reverse scan
+// 32x32 bit-matrix transpose across a warp: lane i holds row i on entry, column i on exit
+// (five butterfly stages, each swapping the off-diagonal s x s blocks).
+__device__ __forceinline__ uint32_t warp_transpose32(uint32_t x, int lane) {
+  const uint32_t lo[5] = {0x0000FFFFu, 0x00FF00FFu, 0x0F0F0F0Fu, 0x33333333u, 0x55555555u};
+#pragma unroll
+  for (int k = 0, s = 16; k < 5; ++k, s >>= 1) {
+    const uint32_t y = __shfl_xor_sync(0xffffffffu, x, s);
+    x = (lane & s) ? ((x & ~lo[k]) | ((y & ~lo[k]) >> s)) : ((x & lo[k]) | ((y & lo[k]) << s));
+  }
+  return x;
+}
+
+// One warp per (b, 32 output neurons), grid-strided over b. For T <= 32 lane t loads the spike
+// and mask words of step t and a warp bit transpose hands each neuron its bits over t, so the
+// reverse scan waits on no load (ncu r01: per-neuron redundant word loads and 64-bit index math
+// made this kernel ~50 instructions per element).
 template <typename GTy>
 __global__ void __launch_bounds__(128) dec_bwd_outscan_kernel(
     int B, int T, int A, int D, int P3, int W3, float dcc, float dvc, float zh,
@@ -121,49 +137,45 @@ __global__ void __launch_bounds__(128) dec_bwd_outscan_kernel(
     const uint32_t* __restrict__ bits3, const uint32_t* __restrict__ mask3, GTy* __restrict__ G3,
     float* __restrict__ g_pre_out) {
   const int n = blockIdx.y * 128 + threadIdx.x;
+  const int lane = threadIdx.x & 31;
   const int N3 = A * D;
+  const bool nv = n < N3;
+  const int j = nv ? n / D : 0, e = nv ? n % D : 0;
+  const float wd = nv ? Wd[j * D + e] : 0.f;
+  const size_t ts = (size_t)B * W3;   // bit-plane stride between timesteps
+  const size_t gts = (size_t)B * P3;  // G3 stride between timesteps
   for (int b = blockIdx.x; b < B; b += gridDim.x) {
-  float g = 0.f;
-  if (n < N3) {
-    const int j = n / D, e = n % D;
-    const float a = act[(size_t)b * A + j];
-    const float gp = __fmul_rn(grad_a[(size_t)b * A + j], __fsub_rn(1.0f, __fmul_rn(a, a)));
-    if (e == 0) g_pre_out[(size_t)b * A + j] = gp;
-    g = __fdiv_rn(__fmul_rn(gp, Wd[j * D + e]), (float)T);  // g_o3 = g_fr / T, constant in t
-  }
-  float dvn = 0.f, dcn = 0.f;
-  if (T <= 32) {
-    // all T spike/mask words are loaded first (independent loads) and kept as per-neuron bit masks
-    // over t, so the reverse scan below does not wait on a load per step
-    uint32_t om = 0, hm = 0;
-    if (n < N3) {
-      const uint32_t* po = bits3 + (size_t)b * W3 + (n >> 5);
-      const uint32_t* ph = mask3 + (size_t)b * W3 + (n >> 5);
-      const size_t ts = (size_t)B * W3;
-      for (int t = 0; t < T; ++t) {
-        om |= ((__ldg(po + t * ts) >> (n & 31)) & 1u) << t;
-        hm |= ((__ldg(ph + t * ts) >> (n & 31)) & 1u) << t;
+    float g = 0.f;
+    if (nv) {
+      const float a = act[(size_t)b * A + j];
+      const float gp = __fmul_rn(grad_a[(size_t)b * A + j], __fsub_rn(1.0f, __fmul_rn(a, a)));
+      if (e == 0) g_pre_out[(size_t)b * A + j] = gp;
+      g = __fdiv_rn(__fmul_rn(gp, wd), (float)T);  // g_o3 = g_fr / T, constant in t
+    }
+    float dvn = 0.f, dcn = 0.f;
+    GTy* gt = G3 + (size_t)b * P3 + n;
+    const uint32_t* po = bits3 + (size_t)b * W3 + (n >> 5);
+    const uint32_t* ph = mask3 + (size_t)b * W3 + (n >> 5);
+    if (T <= 32) {
+      uint32_t wo = 0u, wh = 0u;
+      if (lane < T) { wo = __ldg(po + lane * ts); wh = __ldg(ph + lane * ts); }
+      const uint32_t om = warp_transpose32(wo, lane), hm = warp_transpose32(wh, lane);
+      gt += (size_t)(T - 1) * gts;
+      for (int t = T - 1; t >= 0; --t, gt -= gts) {
+        const float Gt = lif_back_step(zh, dvc, dcc, g, (om >> t) & 1u, (hm >> t) & 1u, dvn, dcn);
+        GT<GTy>::store(gt, nv ? Gt : 0.f);
       }
+      continue;
     }
     for (int t = T - 1; t >= 0; --t) {
-      const size_t row = (size_t)t * B + b;
       float Gt = 0.f;
-      if (n < N3) Gt = lif_back_step(zh, dvc, dcc, g, (om >> t) & 1u, (hm >> t) & 1u, dvn, dcn);
-      GT<GTy>::store(G3 + row * P3 + n, Gt);
+      if (nv) {
+        const uint32_t ow = __ldg(po + t * ts), hw = __ldg(ph + t * ts);
+        Gt = lif_back_step(zh, dvc, dcc, g, (ow >> lane) & 1u, (hw >> lane) & 1u, dvn, dcn);
+      }
+      GT<GTy>::store(gt + (size_t)t * gts, Gt);
     }
-    continue;
   }
-  for (int t = T - 1; t >= 0; --t) {
-    const size_t row = (size_t)t * B + b;
-    float Gt = 0.f;
-    if (n < N3) {
-      const uint32_t ow = bits3[row * W3 + (n >> 5)], hw = mask3[row * W3 + (n >> 5)];
-      const bool o = (ow >> (n & 31)) & 1u, h = (hw >> (n & 31)) & 1u;
-      Gt = lif_back_step(zh, dvc, dcc, g, o, h, dvn, dcn);
-    }
-    GT<GTy>::store(G3 + row * P3 + n, Gt);
-  }
-  }  // b
 }
 
 int launch_dec_bwd_outscan(const ActorDims& d, int B, const float* grad_a, const float* act,

@@ -590,6 +590,11 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
           uint4 qo = __ldg(bT + ch), qh = __ldg(mT + ch);
           uint4 nqo = ch > 0 ? __ldg(bT + ch - 1) : make_uint4(0u, 0u, 0u, 0u);
           uint4 nqh = ch > 0 ? __ldg(mT + ch - 1) : make_uint4(0u, 0u, 0u, 0u);
+          // G_{l-1}[t][b][row]: one base pointer per thread, strides added per (t, j) (ncu r01: the
+          // per-element 64-bit index math and b < B branch were half of the epilogue's instructions)
+          const bool full = b0 + HB <= p.B;
+          const size_t bstr = (size_t)p.p_prev, tstr = (size_t)p.B * p.p_prev;
+          __nv_bfloat16* const gbase = p.g_prev + (size_t)b0 * bstr + row;
           for (int tt = p.T - 1; tt >= 0; --tt) {
             if ((tt >> 4) != ch) {
               ch = tt >> 4;
@@ -597,6 +602,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
               if (ch > 0) { nqo = __ldg(bT + ch - 1); nqh = __ldg(mT + ch - 1); }
             }
             const uint32_t ow0 = byte_of(qo, tt & 15), hw0 = byte_of(qh, tt & 15);
+            __nv_bfloat16* gt = gbase + (size_t)tt * tstr;
 #pragma unroll
             for (int j0 = 0; j0 < HB; j0 += 8) {
               uint32_t r[8];
@@ -609,8 +615,8 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
                 float G = lif_back_step(p.zh, p.kc.dv, p.kc.dc, __uint_as_float(r[jj]), o, h, dvn[j], dcn[j]);
                 if (!valid) G = 0.f;
                 gs[j] = __fadd_rn(gs[j], G);
-                const int b = b0 + j;
-                if (b < p.B) p.g_prev[((size_t)tt * p.B + b) * p.p_prev + row] = __float2bfloat16_rn(G);
+                if (full || b0 + j < p.B) *gt = __float2bfloat16_rn(G);
+                gt += bstr;
               }
             }
           }
