@@ -224,7 +224,11 @@ typedef struct spikerl_comm spikerl_comm;
  * k % policy_delay == 0. indices [B] (device int64) / noise [B][A] (device fp32 raw eps, before
  * the clip to +-noise_clip) may be NULL: then they are drawn on the device with Philox
  * (seed, rank, *rng_counter). comm == NULL means one GPU (no allreduce). losses: device [2]
- * (critic loss; actor loss or unchanged on critic-only steps). */
+ * (critic loss; actor loss or unchanged on critic-only steps).
+ * BF16: the four working copies must have been produced once by *_refresh_bf16 (which writes
+ * their zero padding); the update then keeps them current itself — Adam and Polyak store the RNE
+ * bf16 value of every element they change into each of its places in the copy — so no refresh
+ * is needed between updates. */
 int spikerl_td3_update(const spikerl_actor_cfg* acfg, const spikerl_critic_cfg* ccfg,
                        const spikerl_td3_cfg* hp, const spikerl_td3_bufs* bufs, long long step,
                        unsigned long long seed, const long long* indices, const float* noise,

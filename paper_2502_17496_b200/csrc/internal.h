@@ -58,10 +58,23 @@ int launch_enc_grad_reduce(const ActorDims& d, int nchunk, const float* partial,
 int launch_actor_refresh_bf16(const ActorDims& d, const float* params, __nv_bfloat16* out,
                               cudaStream_t st);
 int launch_f32_to_bf16(const float* in, __nv_bfloat16* out, size_t n, cudaStream_t st);
+// bf16 working-copy views of an fp32 master vector: Adam / Polyak write the RNE bf16 value of every
+// element they update into each place the refresh kernels would put it (the zero padding, written
+// once by a full refresh, is never touched), so the TD3 step needs no separate refresh launches.
+struct Bf16Views {
+  int kind;                  // 0 none, 1 actor W1..W3, 2 critic twin (mma layout), 3 plain copy
+  __nv_bfloat16* out;
+  long long src[3], dst[3];  // actor: fp32 offset of W_l, bf16 offset of its padded copy
+  int rows[3], cols[3], ldd[3];
+  long long P, tb, oW1, oW2, W1p, W1T, W2T, W2c;   // critic (per-critic block after the [2][P] copy)
+  int in, H1, H2, inp;
+};
+Bf16Views actor_bf16_views(const ActorDims& d, __nv_bfloat16* out);
+Bf16Views critic_bf16_views(const CriticDims& c, __nv_bfloat16* out);
 int launch_adam(float* p, const float* g, float* m, float* v, size_t n, long long* counter,
                 float lr, float b1, float b2, float eps, size_t clo, size_t chi, float cmin,
-                unsigned int* done_ticket, cudaStream_t st);
-int launch_polyak(float* t, const float* s, size_t n, float tau, cudaStream_t st);
+                unsigned int* done_ticket, const Bf16Views* views, cudaStream_t st);
+int launch_polyak(float* t, const float* s, size_t n, float tau, const Bf16Views* views, cudaStream_t st);
 
 // ---- critic (k_critic.cu)
 size_t critic_ws_bytes(const CriticDims& c, int B);

@@ -414,6 +414,22 @@ size_t critic_mma_ws_bytes(const CriticDims& c, int B) {
   return total;
 }
 
+Bf16Views critic_bf16_views(const CriticDims& c, __nv_bfloat16* out) {
+  Bf16Views v{};
+  if (!out || !c.bf16) return v;
+  v.out = out;
+  v.P = (long long)c.off[SPIKERL_CRITIC_NPARAM];
+  if (!critic_mma_ok(c)) { v.kind = 3; return v; }
+  const MmaLayout L = mma_layout(c);
+  v.kind = 2;
+  v.tb = L.tb;
+  v.oW1 = (long long)c.off[SPIKERL_CRITIC_W1];
+  v.oW2 = (long long)c.off[SPIKERL_CRITIC_W2];
+  v.W1p = L.W1p; v.W1T = L.W1T; v.W2T = L.W2T; v.W2c = L.W2c;
+  v.in = c.in; v.H1 = c.H1; v.H2 = c.H2; v.inp = L.inp;
+  return v;
+}
+
 int launch_critic_refresh(const CriticDims& c, const float* params2, __nv_bfloat16* out, cudaStream_t st) {
   ProfScope ps_("critic_refresh_bf16", PB_HBM, 0.0, 6.0 * critic_bf16_elems(c), st);
   if (!critic_mma_ok(c)) return launch_f32_to_bf16(params2, out, 2 * c.off[SPIKERL_CRITIC_NPARAM], st);

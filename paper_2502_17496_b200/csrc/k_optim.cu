@@ -56,6 +56,54 @@ int launch_f32_to_bf16(const float* in, __nv_bfloat16* out, size_t n, cudaStream
   return SPIKERL_OK;
 }
 
+Bf16Views actor_bf16_views(const ActorDims& d, __nv_bfloat16* out) {
+  Bf16Views v{};
+  v.kind = out ? 1 : 0;
+  v.out = out;
+  for (int l = 1; l <= 3; ++l) {
+    v.src[l - 1] = (long long)d.off[SPIKERL_ACTOR_W1 + l - 1];
+    v.dst[l - 1] = (long long)d.boff[l - 1];
+    v.rows[l - 1] = d.N[l];
+    v.cols[l - 1] = d.N[l - 1];
+    v.ldd[l - 1] = d.P[l - 1];
+  }
+  return v;
+}
+
+__device__ __forceinline__ void store_views(const Bf16Views& v, size_t e, float x) {
+  if (v.kind == 0) return;
+  const __nv_bfloat16 h = __float2bfloat16_rn(x);
+  const long long le = (long long)e;
+  if (v.kind == 1) {
+#pragma unroll
+    for (int l = 0; l < 3; ++l) {
+      const long long r = le - v.src[l];
+      if (r >= 0 && r < (long long)v.rows[l] * v.cols[l]) {
+        const long long n = r / v.cols[l], k = r - n * v.cols[l];
+        v.out[v.dst[l] + n * v.ldd[l] + k] = h;
+      }
+    }
+    return;
+  }
+  v.out[le] = h;   // [2][P] plain copy (kinds 2 and 3)
+  if (v.kind != 2) return;
+  const long long z = le / v.P, l = le - z * v.P;
+  __nv_bfloat16* blk = v.out + 2 * v.P + z * v.tb;
+  long long r = l - v.oW1;
+  if (r >= 0 && r < (long long)v.H1 * v.in) {          // W1[j][i] -> W1p[j][i], W1T[i][j]
+    const long long j = r / v.in, i = r - j * v.in;
+    blk[v.W1p + j * v.inp + i] = h;
+    blk[v.W1T + i * v.H1 + j] = h;
+    return;
+  }
+  r = l - v.oW2;
+  if (r >= 0 && r < (long long)v.H2 * v.H1) {          // W2[j2][j1] -> W2T[j1][j2], W2c[j2][j1]
+    const long long j2 = r / v.H1, j1 = r - j2 * v.H1;
+    blk[v.W2T + j1 * v.H2 + j2] = h;
+    blk[v.W2c + r] = h;
+  }
+}
+
 // ------------------------------------------------------------------ Adam
 // t = *counter + 1 is read by every block; the last block to finish (atomic ticket) stores it
 // back, so the call is graph-replayable with an on-device step count.
@@ -63,7 +111,8 @@ __global__ void __launch_bounds__(256) adam_kernel(float* __restrict__ p, const 
                                                    float* __restrict__ m, float* __restrict__ v,
                                                    size_t n, long long* counter, float lr, float b1,
                                                    float b2, float eps, size_t clo, size_t chi,
-                                                   float cmin, unsigned int* ticket) {
+                                                   float cmin, unsigned int* ticket,
+                                                   const __grid_constant__ Bf16Views views) {
   const long long t = *(volatile long long*)counter + 1;
   const double bc1 = 1.0 - pow((double)b1, (double)t);
   const double bc2 = 1.0 - pow((double)b2, (double)t);
@@ -86,6 +135,7 @@ __global__ void __launch_bounds__(256) adam_kernel(float* __restrict__ p, const 
       pa[j] = __fsub_rn(pa[j], __fmul_rn(step_size, __fdiv_rn(ma[j], denom)));
       const size_t e = 4 * i + j;
       if (e >= clo && e < chi) pa[j] = fmaxf(pa[j], cmin);
+      store_views(views, e, pa[j]);
     }
     reinterpret_cast<float4*>(p)[i] = pp;
     reinterpret_cast<float4*>(m)[i] = mm;
@@ -98,6 +148,7 @@ __global__ void __launch_bounds__(256) adam_kernel(float* __restrict__ p, const 
     float pp = __fsub_rn(p[e], __fmul_rn(step_size, __fdiv_rn(mm, denom)));
     if (e >= clo && e < chi) pp = fmaxf(pp, cmin);
     p[e] = pp; m[e] = mm; v[e] = vv;
+    store_views(views, e, pp);
   }
   // publish the new step count once every block has read the old one
   __syncthreads();
@@ -114,30 +165,35 @@ __global__ void __launch_bounds__(256) adam_kernel(float* __restrict__ p, const 
 
 int launch_adam(float* p, const float* g, float* m, float* v, size_t n, long long* counter,
                 float lr, float b1, float b2, float eps, size_t clo, size_t chi, float cmin,
-                unsigned int* ticket, cudaStream_t st) {
+                unsigned int* ticket, const Bf16Views* views, cudaStream_t st) {
   ProfScope ps_("adam", PB_HBM, 0.0, 28.0 * n, st);
+  const Bf16Views none{};
   if (((uintptr_t)p | (uintptr_t)g | (uintptr_t)m | (uintptr_t)v) & 15) {
     set_error("adam: buffers must be 16-byte aligned");
     return SPIKERL_E_ARG;
   }
   adam_kernel<<<ew_grid(n, 4), 256, 0, st>>>(p, g, m, v, n, counter, lr, b1, b2, eps, clo, chi,
-                                             cmin, ticket);
+                                             cmin, ticket, views ? *views : none);
   SPK_LAUNCHED();
   return SPIKERL_OK;
 }
 
 // ------------------------------------------------------------------ Polyak
 __global__ void polyak_kernel(float* __restrict__ t, const float* __restrict__ s, size_t n,
-                              float tau) {
+                              float tau, const __grid_constant__ Bf16Views views) {
   const float omt = 1.0f - tau;
   for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n;
-       i += (size_t)gridDim.x * blockDim.x)
-    t[i] = __fadd_rn(__fmul_rn(tau, s[i]), __fmul_rn(omt, t[i]));
+       i += (size_t)gridDim.x * blockDim.x) {
+    const float x = __fadd_rn(__fmul_rn(tau, s[i]), __fmul_rn(omt, t[i]));
+    t[i] = x;
+    store_views(views, i, x);
+  }
 }
 
-int launch_polyak(float* t, const float* s, size_t n, float tau, cudaStream_t st) {
+int launch_polyak(float* t, const float* s, size_t n, float tau, const Bf16Views* views, cudaStream_t st) {
+  const Bf16Views none{};
   ProfScope ps_("polyak", PB_HBM, 0.0, 12.0 * n, st);
-  polyak_kernel<<<ew_grid(n, 1), 256, 0, st>>>(t, s, n, tau);
+  polyak_kernel<<<ew_grid(n, 1), 256, 0, st>>>(t, s, n, tau, views ? *views : none);
   SPK_LAUNCHED();
   return SPIKERL_OK;
 }

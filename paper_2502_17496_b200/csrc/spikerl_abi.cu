@@ -467,12 +467,12 @@ int spikerl_adam(float* params, const float* grads, float* m, float* v, size_t n
     return SPIKERL_E_ARG;
   }
   return launch_adam(params, grads, m, v, n, step_counter, lr, beta1, beta2, eps, clamp_lo, clamp_hi, clamp_min,
-                     (unsigned int*)(step_counter + 1), (cudaStream_t)stream);
+                     (unsigned int*)(step_counter + 1), nullptr, (cudaStream_t)stream);
 }
 
 int spikerl_polyak(float* target, const float* source, size_t n, float tau, spikerl_stream_t stream) {
   if (!target || !source || n == 0) { set_error("spikerl_polyak: bad arguments"); return SPIKERL_E_ARG; }
-  return launch_polyak(target, source, n, tau, (cudaStream_t)stream);
+  return launch_polyak(target, source, n, tau, nullptr, (cudaStream_t)stream);
 }
 
 int spikerl_td3_update(const spikerl_actor_cfg* acfg, const spikerl_critic_cfg* ccfg, const spikerl_td3_cfg* hp,
@@ -536,9 +536,13 @@ int spikerl_td3_update(const spikerl_actor_cfg* acfg, const spikerl_critic_cfg* 
   SPK_TRY(critic_fwd_bwd(cd, B, b->critic, cbf, s, ad.S, a, ad.A, y, q, losses, b->grad_critic, nullptr, 0.f, 2,
                          cws, st));
   SPK_TRY(spikerl_allreduce_grads(comm, b->grad_critic, 2 * Pc, stream));
+  // the bf16 working copies are kept current by the optimiser kernels themselves (Bf16Views)
+  const Bf16Views cv = critic_bf16_views(cd, ad.bf16 ? (__nv_bfloat16*)b->critic_bf16 : nullptr);
+  const Bf16Views ctv = critic_bf16_views(cd, ad.bf16 ? (__nv_bfloat16*)b->critic_t_bf16 : nullptr);
+  const Bf16Views av = actor_bf16_views(ad, ad.bf16 ? (__nv_bfloat16*)b->actor_bf16 : nullptr);
+  const Bf16Views atv = actor_bf16_views(ad, ad.bf16 ? (__nv_bfloat16*)b->actor_t_bf16 : nullptr);
   SPK_TRY(launch_adam(b->critic, b->grad_critic, b->m_critic, b->v_critic, 2 * Pc, b->adam_steps, hp->lr_critic,
-                      hp->beta1, hp->beta2, hp->eps, 0, 0, 0.f, (unsigned int*)(b->adam_steps + 1), st));
-  if (ad.bf16) SPK_TRY(launch_critic_refresh(cd, b->critic, (__nv_bfloat16*)b->critic_bf16, st));
+                      hp->beta1, hp->beta2, hp->eps, 0, 0, 0.f, (unsigned int*)(b->adam_steps + 1), &cv, st));
   // 4. delayed actor update + targets
   if (step % hp->policy_delay == 0) {
     SPK_TRY(actor_forward_impl(ad, B, b->actor, abf, s, api, tape, st));
@@ -550,14 +554,9 @@ int spikerl_td3_update(const spikerl_actor_cfg* acfg, const spikerl_critic_cfg* 
     SPK_TRY(spikerl_allreduce_grads(comm, b->grad_actor, Pa, stream));
     SPK_TRY(launch_adam(b->actor, b->grad_actor, b->m_actor, b->v_actor, Pa, b->adam_steps + 2, hp->lr_actor,
                         hp->beta1, hp->beta2, hp->eps, ad.off[SPIKERL_ACTOR_SIGMA], ad.off[SPIKERL_ACTOR_W1],
-                        ad.sigma_floor, (unsigned int*)(b->adam_steps + 3), st));
-    SPK_TRY(launch_polyak(b->actor_t, b->actor, Pa, hp->tau, st));
-    SPK_TRY(launch_polyak(b->critic_t, b->critic, 2 * Pc, hp->tau, st));
-    if (ad.bf16) {
-      SPK_TRY(launch_actor_refresh_bf16(ad, b->actor, (__nv_bfloat16*)b->actor_bf16, st));
-      SPK_TRY(launch_actor_refresh_bf16(ad, b->actor_t, (__nv_bfloat16*)b->actor_t_bf16, st));
-      SPK_TRY(launch_critic_refresh(cd, b->critic_t, (__nv_bfloat16*)b->critic_t_bf16, st));
-    }
+                        ad.sigma_floor, (unsigned int*)(b->adam_steps + 3), &av, st));
+    SPK_TRY(launch_polyak(b->actor_t, b->actor, Pa, hp->tau, &atv, st));
+    SPK_TRY(launch_polyak(b->critic_t, b->critic, 2 * Pc, hp->tau, &ctv, st));
   }
   return SPIKERL_OK;
 }

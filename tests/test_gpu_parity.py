@@ -329,6 +329,29 @@ def test_td3_two_steps(prec):
     assert td3.adam_steps.cpu().tolist() == [2, 0, 1, 0]
 
 
+@pytest.mark.parametrize("obs,act", [(17, 6), (111, 8)])
+def test_td3_bf16_copies_track_masters(obs, act):
+    """Adam / Polyak write the bf16 working copies in place (Bf16Views): after several updates they
+    must equal, bit for bit, a full refresh of the fp32 masters (padding included)."""
+    import torch
+    import paper_2502_17496_b200 as pk
+    shape = sg.with_(sg.preset("cfg1")[0], obs_dim=obs, act_dim=act)
+    replay = pk.replay_fill(5000, obs, act, seed=5)
+    rng = np.random.default_rng(9)
+    cs = sg.CriticShape(obs + act, precision="bf16")
+    td3 = pk.TD3(pk.actor_cfg_from(shape), pk.critic_cfg(obs + act), pk.td3_cfg(64), replay, seed=2)
+    td3.load(sg.actor_params(shape, rng), sg.critic_params(cs, rng), sg.critic_params(cs, rng))
+    for k in range(1, 5):
+        td3.update(k)
+    torch.cuda.synchronize()
+    kept = [t.clone() for t in (td3.actor_bf16, td3.actor_t_bf16, td3.critic_bf16, td3.critic_t_bf16)]
+    td3.refresh()
+    torch.cuda.synchronize()
+    for name, a, b in zip(("actor", "actor_t", "critic", "critic_t"), kept,
+                          (td3.actor_bf16, td3.actor_t_bf16, td3.critic_bf16, td3.critic_t_bf16)):
+        assert torch.equal(a, b), name
+
+
 def test_td3_graph_replay_matches_eager():
     import torch
     import paper_2502_17496_b200 as pk
