@@ -50,7 +50,7 @@ int launch_enc_grad_tc(const ActorDims& d, int B, const void* Gsum, const __nv_b
 int launch_lif_dw_tc(const ActorDims& d, int l, int B, const void* Gl, const uint32_t* bits_prev,
                      float* dW, float* part, int accumulate, cudaStream_t st);
 size_t tc_enc_partial_bytes(const ActorDims& d, int B);
-size_t tc_dw_partial_bytes(const ActorDims& d, int B);
+size_t tc_dw_partial_bytes(const ActorDims& d, int B, int l);   // split-K partials of dW_l
 int launch_enc_grad_reduce(const ActorDims& d, int nchunk, const float* partial, float* dmu,
                            float* dsigma, int accumulate, cudaStream_t st);
 
@@ -84,11 +84,14 @@ bool critic_mma_ok(const CriticDims& c);
 size_t critic_mma_ws_bytes(const CriticDims& c, int B);
 int critic_mma_fwd_bwd(const CriticDims& c, int B, const float* params2, const __nv_bfloat16* pb, const float* obs,
                        int S, const float* act, int A, const float* y, float* q, float* loss, float* grad2,
-                       float* grad_act, float act_scale, int nz, void* ws, cudaStream_t st);
+                       float* grad_act, float act_scale, int nz, void* ws, cudaStream_t st,
+                       cudaEvent_t wait_before_loss = nullptr);
+// wait_before_loss (optional): the stream waits on this event after the forward and before the
+// loss (the TD target y is produced concurrently on another stream).
 int critic_fwd_bwd(const CriticDims& c, int B, const float* params2, const __nv_bfloat16* pb16,
                    const float* obs, int S, const float* act, int A, const float* y, float* q,
                    float* loss, float* grad2, float* grad_act, float act_scale, int n_critics,
-                   void* ws, cudaStream_t st);
+                   void* ws, cudaStream_t st, cudaEvent_t wait_before_loss = nullptr);
 
 // ---- replay / TD3 glue (k_replay.cu)
 int launch_replay_gather(int B, int S, int A, const float* rs, const float* ra, const float* rr,

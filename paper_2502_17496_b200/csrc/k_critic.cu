@@ -275,9 +275,10 @@ size_t critic_ws_bytes(const CriticDims& c, int B) {
 int critic_fwd_bwd(const CriticDims& c, int B, const float* params2, const __nv_bfloat16* pb16,
                    const float* obs, int S, const float* act, int A, const float* y, float* q,
                    float* loss, float* grad2, float* grad_act, float act_scale, int nz, void* ws,
-                   cudaStream_t st) {
+                   cudaStream_t st, cudaEvent_t wait_before_loss) {
   if (critic_mma_ok(c))
-    return critic_mma_fwd_bwd(c, B, params2, pb16, obs, S, act, A, y, q, loss, grad2, grad_act, act_scale, nz, ws, st);
+    return critic_mma_fwd_bwd(c, B, params2, pb16, obs, S, act, A, y, q, loss, grad2, grad_act, act_scale, nz, ws, st,
+                              wait_before_loss);
   CriticWs w = carve(c, B, ws);
   const bool bf = c.bf16 != 0;
   const long long P = (long long)c.off[SPIKERL_CRITIC_NPARAM];
@@ -324,6 +325,7 @@ int critic_fwd_bwd(const CriticDims& c, int B, const float* params2, const __nv_
     SPK_LAUNCHED();
   }
   const bool want_params = (y != nullptr && grad2 != nullptr);
+  if (wait_before_loss) SPK_CHECK_CUDA(cudaStreamWaitEvent(st, wait_before_loss, 0));
   if (y) {
     critic_loss_kernel<<<1, 256, 0, st>>>(B, nz, q, y, w.dq, loss);
     SPK_LAUNCHED();

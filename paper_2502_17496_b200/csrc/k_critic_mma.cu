@@ -444,7 +444,8 @@ int launch_critic_refresh(const CriticDims& c, const float* params2, __nv_bfloat
 
 int critic_mma_fwd_bwd(const CriticDims& c, int B, const float* params2, const __nv_bfloat16* pb, const float* obs,
                        int S, const float* act, int A, const float* y, float* q, float* loss, float* grad2,
-                       float* grad_act, float act_scale, int nz, void* ws, cudaStream_t st) {
+                       float* grad_act, float act_scale, int nz, void* ws, cudaStream_t st,
+                       cudaEvent_t wait_before_loss) {
   const MmaLayout L = mma_layout(c);
   MmaWs w = mma_carve(c, B, ws, nullptr);
   const int Bp = round_up(B, RB);
@@ -460,6 +461,7 @@ int critic_mma_fwd_bwd(const CriticDims& c, int B, const float* params2, const _
         w.XT, w.H1T, w.Z1, w.Z2, w.Hh2, q, need_bwd ? 1 : 0);
     SPK_LAUNCHED();
   }
+  if (wait_before_loss) SPK_CHECK_CUDA(cudaStreamWaitEvent(st, wait_before_loss, 0));
   if (y) {
     critic_loss_mma_kernel<<<1, 256, 0, st>>>(B, nz, q, y, w.dq, loss);
     SPK_LAUNCHED();

@@ -991,15 +991,10 @@ void tc_dw_plan(const ActorDims& d, int l, int B, int* splits, int* kps) {
   *splits = cdiv(k_blocks, per);
 }
 
-size_t tc_dw_partial_bytes(const ActorDims& d, int B) {
-  size_t mx = 0;
-  for (int l = 1; l <= 3; ++l) {
-    int s, k;
-    tc_dw_plan(d, l, B, &s, &k);
-    const size_t b = sizeof(float) * (size_t)s * d.P[l] * d.P[l - 1];
-    if (b > mx) mx = b;
-  }
-  return mx;
+size_t tc_dw_partial_bytes(const ActorDims& d, int B, int l) {
+  int s, k;
+  tc_dw_plan(d, l, B, &s, &k);
+  return sizeof(float) * (size_t)s * d.P[l] * d.P[l - 1];
 }
 
 int launch_lif_dw_tc(const ActorDims& d, int l, int B, const void* Gl, const uint32_t* bits_prev, float* dW,

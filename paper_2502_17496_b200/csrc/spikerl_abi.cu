@@ -8,6 +8,7 @@
 #include <cstdarg>
 #include <cstdio>
 #include <cstring>
+#include <cstdlib>
 #include <atomic>
 #include "internal.h"
 
@@ -143,7 +144,7 @@ struct ActorWs {
   size_t Gsum;      // [B][P1]
   size_t g_pre;     // [B][A] fp32
   size_t enc_part;  // encoder partials
-  size_t dw_part;   // tcgen05 split-K dW partials
+  size_t dw_part[4];   // tcgen05 split-K dW_l partials (one region per layer: the dW run concurrently)
   size_t total;
 };
 
@@ -160,9 +161,41 @@ static ActorWs actor_ws_layout(const ActorDims& d, int B) {
   const bool tc = d.engine == SPIKERL_ENGINE_TCGEN05;
   const size_t ep = enc_grad_partial_bytes(d, B), ept = tc ? tc_enc_partial_bytes(d, B) : 0;
   w.enc_part = take(ep > ept ? ep : ept);
-  w.dw_part = take(tc ? tc_dw_partial_bytes(d, B) : 0);
+  w.dw_part[0] = 0;
+  for (int l = 1; l <= 3; ++l) w.dw_part[l] = take(tc ? tc_dw_partial_bytes(d, B, l) : 0);
   w.total = o;
   return w;
+}
+
+// Auxiliary streams / events (per device, created once outside any capture: the workspace-size
+// queries create them). The TD3 step (side 0-2, ev 0-7) and the actor backward (side 3-5,
+// ev 8-15) fork independent branches onto them and join them back before they return, so a
+// CUDA-graph capture records a DAG with parallel branches.
+struct Td3Aux {
+  cudaStream_t side[6];
+  cudaEvent_t ev[16];
+};
+
+static int td3_aux(Td3Aux** out) {
+  static Td3Aux pool[16];
+  static bool made[16] = {};
+  int dev = 0;
+  SPK_CHECK_CUDA(cudaGetDevice(&dev));
+  if (dev < 0 || dev >= 16) { set_error("device index %d out of range", dev); return SPIKERL_E_ARG; }
+  if (!made[dev]) {
+    for (auto& x : pool[dev].side) SPK_CHECK_CUDA(cudaStreamCreateWithFlags(&x, cudaStreamNonBlocking));
+    for (auto& e : pool[dev].ev) SPK_CHECK_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    made[dev] = true;
+  }
+  *out = &pool[dev];
+  return SPIKERL_OK;
+}
+
+// dst waits for everything enqueued on src so far
+static int stream_after(cudaStream_t dst, cudaStream_t src, cudaEvent_t ev) {
+  SPK_CHECK_CUDA(cudaEventRecord(ev, src));
+  SPK_CHECK_CUDA(cudaStreamWaitEvent(dst, ev, 0));
+  return SPIKERL_OK;
 }
 
 static int actor_forward_impl(const ActorDims& d, int B, const float* params,
@@ -211,13 +244,32 @@ static int actor_backward_impl(const ActorDims& d, int B, const float* params,
   float* g_pre = (float*)(ws + W.g_pre);
   SPK_TRY(launch_dec_bwd_outscan(d, B, grad_a, act, counts, params + d.off[SPIKERL_ACTOR_WD], bits[3], mask[3],
                                  G[3], g_pre, st));
-  SPK_TRY(launch_dec_param_grads(d, B, g_pre, counts, grads + d.off[SPIKERL_ACTOR_WD],
-                                 grads + d.off[SPIKERL_ACTOR_BD], accum, st));
+  // Small problems (kernels far from filling the GPU): dW_l and the decoder parameter grads run
+  // on side streams next to the dX chain, each as soon as its G_l exists; the critical path is
+  // then outscan -> dX3 -> dX2 -> max(encoder grad, dW1). Large problems stay on one stream
+  // (persistent kernels that each own every SM).
   const bool tc = d.engine == SPIKERL_ENGINE_TCGEN05;
+  Td3Aux* aux = nullptr;
+  SPK_TRY(td3_aux(&aux));
+  const bool fork = (long long)d.T * B <= 32768;
+  cudaStream_t sw[4] = {st, st, st, st};   // sw[l]: stream of dW_l; sw[0]: decoder params
+  if (fork) { sw[0] = aux->side[3]; sw[3] = aux->side[3]; sw[2] = aux->side[4]; sw[1] = aux->side[5]; }
+  auto branch = [&](cudaStream_t s, int e) -> int {   // s continues after everything enqueued on st
+    if (s == st) return SPIKERL_OK;
+    return stream_after(s, st, aux->ev[8 + e]);
+  };
+  SPK_TRY(branch(sw[0], 0));
+  SPK_TRY(launch_dec_param_grads(d, B, g_pre, counts, grads + d.off[SPIKERL_ACTOR_WD],
+                                 grads + d.off[SPIKERL_ACTOR_BD], accum, sw[0]));
   for (int l = 3; l >= 1; --l) {
     const float* Wf = params + d.off[SPIKERL_ACTOR_W1 + l - 1];
     const __nv_bfloat16* Wb = d.bf16 ? pb16 + d.boff[l - 1] : nullptr;
     float* dW = grads + d.off[SPIKERL_ACTOR_W1 + l - 1];
+    if (l != 3) SPK_TRY(branch(sw[l], l));   // G_l was produced on st
+    if (tc)
+      SPK_TRY(launch_lif_dw_tc(d, l, B, G[l], bits[l - 1], dW, (float*)(ws + W.dw_part[l]), accum, sw[l]));
+    else
+      SPK_TRY(launch_lif_dw_simt(d, l, B, G[l], bits[l - 1], dW, accum, sw[l]));
     if (l >= 2) {
       if (tc)
         SPK_TRY(launch_lif_dx_tc(d, l, B, G[l], Wb, (const uint8_t*)(tape + L.bitsT[l - 1]),
@@ -227,10 +279,6 @@ static int actor_backward_impl(const ActorDims& d, int B, const float* params,
         SPK_TRY(launch_lif_dx_simt(d, l, B, G[l], Wf, Wb, bits[l - 1], mask[l - 1], G[l - 1],
                                    l == 2 ? Gsum : nullptr, st));
     }
-    if (tc)
-      SPK_TRY(launch_lif_dw_tc(d, l, B, G[l], bits[l - 1], dW, (float*)(ws + W.dw_part), accum, st));
-    else
-      SPK_TRY(launch_lif_dw_simt(d, l, B, G[l], bits[l - 1], dW, accum, st));
   }
   const float* A = (const float*)(tape + L.A);
   if (tc)
@@ -242,12 +290,18 @@ static int actor_backward_impl(const ActorDims& d, int B, const float* params,
                                  A, obs, params + d.off[SPIKERL_ACTOR_MU], params + d.off[SPIKERL_ACTOR_SIGMA],
                                  (float*)(ws + W.enc_part), grads + d.off[SPIKERL_ACTOR_MU],
                                  grads + d.off[SPIKERL_ACTOR_SIGMA], accum, st));
+  if (fork) {   // join every side stream back into st
+    for (int i = 3; i <= 5; ++i) {
+      SPK_CHECK_CUDA(cudaEventRecord(aux->ev[8 + i], aux->side[i]));
+      SPK_CHECK_CUDA(cudaStreamWaitEvent(st, aux->ev[8 + i], 0));
+    }
+  }
   return SPIKERL_OK;
 }
 
 // ------------------------------------------------------------------ TD3 workspace layout
 struct Td3Ws {
-  size_t s, a, r, s2, d, a2, at, api, qt, q, y, ga, lossa, tape, actor_ws, critic_ws, total;
+  size_t s, a, r, s2, d, a2, at, api, qt, q, y, ga, lossa, tape, actor_ws, critic_ws, critic_ws_t, total;
 };
 
 static Td3Ws td3_ws_layout(const ActorDims& ad, const CriticDims& cd, int B) {
@@ -262,6 +316,7 @@ static Td3Ws td3_ws_layout(const ActorDims& ad, const CriticDims& cd, int B) {
   w.tape = take(tape_layout(ad, B).total);
   w.actor_ws = take(actor_ws_layout(ad, B).total);
   w.critic_ws = take(critic_ws_bytes(cd, B));
+  w.critic_ws_t = take(critic_ws_bytes(cd, B));   // target-critic forward runs concurrently
   w.total = o;
   return w;
 }
@@ -341,6 +396,8 @@ size_t spikerl_actor_tape_bytes(const spikerl_actor_cfg* cfg, int batch) {
 size_t spikerl_actor_workspace_bytes(const spikerl_actor_cfg* cfg, int batch) {
   ActorDims d;
   if (actor_dims(cfg, &d) != SPIKERL_OK || batch < 1) return 0;
+  Td3Aux* aux = nullptr;   // create the fork/join streams now, outside any graph capture
+  if (td3_aux(&aux) != SPIKERL_OK) cudaGetLastError();   // no device (host-only query): later
   return actor_ws_layout(d, batch).total;
 }
 
@@ -354,6 +411,8 @@ size_t spikerl_td3_workspace_bytes(const spikerl_actor_cfg* acfg, const spikerl_
   ActorDims ad;
   CriticDims cd;
   if (actor_dims(acfg, &ad) != SPIKERL_OK || critic_dims(ccfg, &cd) != SPIKERL_OK || batch < 1) return 0;
+  Td3Aux* aux = nullptr;   // create the fork/join streams now, outside any graph capture
+  if (td3_aux(&aux) != SPIKERL_OK) cudaGetLastError();   // no device (host-only query): later
   return td3_ws_layout(ad, cd, batch).total;
 }
 
@@ -521,31 +580,50 @@ int spikerl_td3_update(const spikerl_actor_cfg* acfg, const spikerl_critic_cfg* 
   const __nv_bfloat16* cbf = (const __nv_bfloat16*)b->critic_bf16;
   const __nv_bfloat16* ctbf = (const __nv_bfloat16*)b->critic_t_bf16;
 
+  Td3Aux* aux = nullptr;
+  SPK_TRY(td3_aux(&aux));
+  cudaStream_t sA = aux->side[0], sB = aux->side[1], sC = aux->side[2];
+  static const bool serial = [] { const char* e = getenv("SPIKERL_TD3_SERIAL"); return e && e[0] == '1'; }();
+  if (serial) sA = sB = sC = st;   // A/B switch: the same work on one stream
+  const bool actor_step = (step % hp->policy_delay == 0);
+  void* cws_t = ws + W.critic_ws_t;
+
   // K9: sample (s, a, r, s', d)
   SPK_TRY(launch_replay_gather(B, ad.S, ad.A, b->rs, b->ra, b->rr, b->rs2, b->rd, b->replay_size, indices, seed,
                                rank, b->rng_counter, s, a, r, s2, dn, st));
-  // 1. target policy smoothing: a~ = clip(pi'(s') + clip(eps), -1, 1)
-  SPK_TRY(actor_forward_impl(ad, B, b->actor_t, atbf, s2, a2, aws + actor_ws_layout(ad, B).tape, st));
+  // branch A: target path. 1. a~ = clip(pi'(s') + clip(eps), -1, 1); 2. y = r + gamma (1 - d) min(Q1', Q2')(s', a~)
+  SPK_TRY(stream_after(sA, st, aux->ev[0]));
+  SPK_TRY(actor_forward_impl(ad, B, b->actor_t, atbf, s2, a2, aws + actor_ws_layout(ad, B).tape, sA));
   SPK_TRY(launch_target_action(B, ad.A, a2, noise, hp->policy_noise, hp->noise_clip, seed, rank, b->rng_counter, at,
-                               st));
-  // 2. y = r + gamma (1 - d) min(Q1', Q2')(s', a~)
+                               sA));
   SPK_TRY(critic_fwd_bwd(cd, B, b->critic_t, ctbf, s2, ad.S, at, ad.A, nullptr, qt, nullptr, nullptr, nullptr, 0.f,
-                         2, cws, st));
-  SPK_TRY(launch_td_target(B, r, dn, qt, hp->gamma, y, st));
-  // 3. critic loss, grads, allreduce, Adam
-  SPK_TRY(critic_fwd_bwd(cd, B, b->critic, cbf, s, ad.S, a, ad.A, y, q, losses, b->grad_critic, nullptr, 0.f, 2,
-                         cws, st));
-  SPK_TRY(spikerl_allreduce_grads(comm, b->grad_critic, 2 * Pc, stream));
-  // the bf16 working copies are kept current by the optimiser kernels themselves (Bf16Views)
+                         2, cws_t, sA));
+  SPK_TRY(launch_td_target(B, r, dn, qt, hp->gamma, y, sA));
+  SPK_CHECK_CUDA(cudaEventRecord(aux->ev[1], sA));
+  // branch B (actor steps): the policy's own forward pi(s) depends only on s and the actor
+  if (actor_step) {
+    SPK_TRY(stream_after(sB, st, aux->ev[2]));
+    SPK_TRY(actor_forward_impl(ad, B, b->actor, abf, s, api, tape, sB));
+    SPK_CHECK_CUDA(cudaEventRecord(aux->ev[3], sB));
+  }
+  // 3. critic forward Q(s, a) overlaps branch A; the loss waits for y; grads, allreduce, Adam
+  // (the bf16 working copies are kept current by the optimiser kernels themselves: Bf16Views)
   const Bf16Views cv = critic_bf16_views(cd, ad.bf16 ? (__nv_bfloat16*)b->critic_bf16 : nullptr);
   const Bf16Views ctv = critic_bf16_views(cd, ad.bf16 ? (__nv_bfloat16*)b->critic_t_bf16 : nullptr);
   const Bf16Views av = actor_bf16_views(ad, ad.bf16 ? (__nv_bfloat16*)b->actor_bf16 : nullptr);
   const Bf16Views atv = actor_bf16_views(ad, ad.bf16 ? (__nv_bfloat16*)b->actor_t_bf16 : nullptr);
+  SPK_TRY(critic_fwd_bwd(cd, B, b->critic, cbf, s, ad.S, a, ad.A, y, q, losses, b->grad_critic, nullptr, 0.f, 2,
+                         cws, st, aux->ev[1]));
+  SPK_TRY(spikerl_allreduce_grads(comm, b->grad_critic, 2 * Pc, stream));
   SPK_TRY(launch_adam(b->critic, b->grad_critic, b->m_critic, b->v_critic, 2 * Pc, b->adam_steps, hp->lr_critic,
                       hp->beta1, hp->beta2, hp->eps, 0, 0, 0.f, (unsigned int*)(b->adam_steps + 1), &cv, st));
   // 4. delayed actor update + targets
-  if (step % hp->policy_delay == 0) {
-    SPK_TRY(actor_forward_impl(ad, B, b->actor, abf, s, api, tape, st));
+  if (actor_step) {
+    // branch C: the critic targets only need the updated critic
+    SPK_TRY(stream_after(sC, st, aux->ev[4]));
+    SPK_TRY(launch_polyak(b->critic_t, b->critic, 2 * Pc, hp->tau, &ctv, sC));
+    SPK_CHECK_CUDA(cudaEventRecord(aux->ev[5], sC));
+    SPK_CHECK_CUDA(cudaStreamWaitEvent(st, aux->ev[3], 0));   // pi(s) from branch B
     SPK_TRY(critic_fwd_bwd(cd, B, b->critic, cbf, s, ad.S, api, ad.A, nullptr, q, nullptr, nullptr, ga,
                            -1.0f / (float)B, 1, cws, st));
     neg_mean_kernel<<<1, 256, 0, st>>>(B, q, losses + 1);
@@ -556,7 +634,7 @@ int spikerl_td3_update(const spikerl_actor_cfg* acfg, const spikerl_critic_cfg* 
                         hp->beta1, hp->beta2, hp->eps, ad.off[SPIKERL_ACTOR_SIGMA], ad.off[SPIKERL_ACTOR_W1],
                         ad.sigma_floor, (unsigned int*)(b->adam_steps + 3), &av, st));
     SPK_TRY(launch_polyak(b->actor_t, b->actor, Pa, hp->tau, &atv, st));
-    SPK_TRY(launch_polyak(b->critic_t, b->critic, 2 * Pc, hp->tau, &ctv, st));
+    SPK_CHECK_CUDA(cudaStreamWaitEvent(st, aux->ev[5], 0));   // join branch C
   }
   return SPIKERL_OK;
 }

@@ -106,3 +106,18 @@ def test_sync_errors_enqueue_nothing(L):
     st = lib.spikerl_td3_update(C.byref(c), C.byref(cc), C.byref(hp), C.byref(bufs), 1, 0, None, None, None,
                                 C.c_void_p(256), C.c_void_p(256), None)
     assert st == L.E_NOTREADY, L.last_error()
+
+
+def test_workspace_sizes_host_only(L):
+    """Workspace-size queries are host logic: they answer without a device (they also create the
+    fork/join streams when one is present) and grow with the batch."""
+    lib = L.lib()
+    from paper_2502_17496_b200 import critic_cfg, td3_cfg
+    c = cfg(precision="bf16")
+    cc = critic_cfg(23)
+    a1, a2 = lib.spikerl_actor_workspace_bytes(C.byref(c), 64), lib.spikerl_actor_workspace_bytes(C.byref(c), 256)
+    assert 0 < a1 < a2
+    w = lib.spikerl_td3_workspace_bytes(C.byref(c), C.byref(cc), 256)
+    # the TD3 workspace holds the actor workspace, a tape and two critic workspaces (online + target)
+    assert w > a2 + lib.spikerl_actor_tape_bytes(C.byref(c), 256) + 2 * lib.spikerl_critic_workspace_bytes(C.byref(cc), 256) - 1
+    assert lib.spikerl_actor_workspace_bytes(C.byref(c), 0) == 0
