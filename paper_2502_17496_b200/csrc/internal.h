@@ -54,6 +54,17 @@ size_t tc_dw_partial_bytes(const ActorDims& d, int B, int l);   // split-K parti
 int launch_enc_grad_reduce(const ActorDims& d, int nchunk, const float* partial, float* dmu,
                            float* dsigma, int accumulate, cudaStream_t st);
 
+// ---- auxiliary streams (prof.cu): per device, created once outside any graph capture (the
+// workspace-size queries create them). Kernels forked onto them are joined back before the
+// forking call returns, so a graph capture of the call records a DAG with parallel branches.
+// Slots: TD3 step side 0-2 / ev 0-7; actor backward side 3-5 / ev 8-15; critic side 6 / ev 16-19.
+struct AuxPool {
+  cudaStream_t side[8];
+  cudaEvent_t ev[24];
+};
+int aux_pool(AuxPool** out);
+int stream_after(cudaStream_t dst, cudaStream_t src, cudaEvent_t ev);   // dst waits for src's work so far
+
 // ---- optimiser / copies (k_optim.cu)
 int launch_actor_refresh_bf16(const ActorDims& d, const float* params, __nv_bfloat16* out,
                               cudaStream_t st);

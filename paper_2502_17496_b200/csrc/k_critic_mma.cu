@@ -89,6 +89,8 @@ MmaLayout mma_layout(const CriticDims& c) {
 struct MmaWs {
   __nv_bfloat16 *XT, *H1T, *dZ2T, *dZ1T;   // [inq][Bp], [2][H][Bp] x3
   float *Z1, *Z2, *Hh2, *q, *dq;           // [2][B][H] x3, [2][B] x2
+  float* part;                             // [2][Bp/RB] loss partials
+  unsigned int* ticket;
 };
 
 MmaWs mma_carve(const CriticDims& c, int B, void* base, size_t* total) {
@@ -107,6 +109,8 @@ MmaWs mma_carve(const CriticDims& c, int B, void* base, size_t* total) {
   w.Hh2 = (float*)take(4 * 2 * (size_t)B * c.H2);
   w.q = (float*)take(4 * 2 * (size_t)B);
   w.dq = (float*)take(4 * 2 * (size_t)B);
+  w.part = (float*)take(4 * 2 * (Bp / RB));
+  w.ticket = (unsigned int*)take(4);
   if (total) *total = off;
   return w;
 }
@@ -119,13 +123,14 @@ __global__ void __launch_bounds__(256) critic_fwd_mma_kernel(
     const __nv_bfloat16* __restrict__ pb, long long P, long long tb, long long oW1p, long long oW2,
     long long oW3, const float* __restrict__ params, long long oB1, long long oB2, long long oB3,
     __nv_bfloat16* __restrict__ XT, __nv_bfloat16* __restrict__ H1T, float* __restrict__ Z1,
-    float* __restrict__ Z2, float* __restrict__ Hh2, float* __restrict__ q, int store) {
+    float* __restrict__ Z2, float* __restrict__ Hh2, float* __restrict__ q, int store, unsigned int* ticket) {
   __shared__ __align__(16) __nv_bfloat16 xs[RB * (512 + SPAD)];
   __shared__ __align__(16) __nv_bfloat16 h1s[RB * (HW + SPAD)];
   __shared__ float red[NWARP][RB];
   const int z = blockIdx.y, r0 = blockIdx.x * RB, tid = threadIdx.x, warp = tid >> 5;
   const int lane = tid & 31, g = lane >> 2, t = lane & 3;
   const int in = S + A, ldx = inp + SPAD, ldh = HW + SPAD;
+  if (ticket && blockIdx.x == 0 && z == 0 && tid == 0) *ticket = 0u;   // for the backward launch
   // X tile (bf16-rounded [s; a]); the z == 0 CTAs also write X^T (zeros beyond in / B) for dW1
   for (int idx = tid; idx < RB * inp; idx += 256) {
     const int r = idx / inp, i = idx - r * inp, b = r0 + r;
@@ -204,22 +209,75 @@ __global__ void __launch_bounds__(256) critic_fwd_mma_kernel(
 
 // ------------------------------------------------------------------ data backward
 // dZ2 = round(dQ w3 [Z2 > 0]); dZ1 = round((dZ2 W2) [Z1 > 0]); grad_act = (dZ1 W1)[:, S:S+A]
+// dQ is formed here (no separate loss launch): mode 0 (critic update) dQ_z[b] = 2 (Q_z - y)/B and
+// the loss sum_z mean_b (Q_z - y)^2; mode 1 (actor step, critic 0 only) dQ = act_scale and the
+// actor loss -mean_b Q. Each CTA writes dQ for its rows and one partial sum (fixed row order);
+// the last CTA to finish (atomic ticket, zeroed by the forward launch) adds the partials in
+// a fixed order, so the scalar is deterministic.
 __global__ void __launch_bounds__(256) critic_bwd_data_mma_kernel(
-    int B, int Bp, int S, int A, int inp, const float* __restrict__ dq, const __nv_bfloat16* __restrict__ pb,
+    int B, int Bp, int S, int A, int inp, const float* __restrict__ q, const float* __restrict__ y, int mode,
+    float act_scale, float* __restrict__ dq, float* __restrict__ part, unsigned int* __restrict__ ticket,
+    float* __restrict__ loss, const __nv_bfloat16* __restrict__ pb,
     long long P, long long tb, long long oW3, long long oW1T, long long oW2T, const float* __restrict__ Z1,
     const float* __restrict__ Z2, __nv_bfloat16* __restrict__ dZ2T, __nv_bfloat16* __restrict__ dZ1T,
     float* __restrict__ grad_act, int store_t) {
   __shared__ __align__(16) __nv_bfloat16 d2s[RB * (HW + SPAD)];
   __shared__ __align__(16) __nv_bfloat16 d1s[RB * (HW + SPAD)];
+  __shared__ float dqs[RB];
+  __shared__ bool last;
   const int z = blockIdx.y, r0 = blockIdx.x * RB, tid = threadIdx.x, warp = tid >> 5;
   const int lane = tid & 31, g = lane >> 2, t = lane & 3;
   const int ldh = HW + SPAD;
   const __nv_bfloat16* W3 = pb + z * P + oW3;
+  if (warp == 0) {
+    float d = 0.f, c = 0.f;
+    const int b = r0 + lane;
+    if (lane < RB && b < B) {
+      const float qv = q[(size_t)z * B + b];
+      if (mode == 0) {
+        const float e = __fsub_rn(qv, y[b]);
+        d = __fdiv_rn(__fmul_rn(2.0f, e), (float)B);
+        c = __fmul_rn(e, e);
+      } else {
+        d = act_scale;
+        c = qv;
+      }
+      dq[(size_t)z * B + b] = d;
+    }
+    if (lane < RB) dqs[lane] = d;
+    // partial over this CTA's rows in row order (lane 0 sums the 16 values serially)
+    float cs[RB];
+#pragma unroll
+    for (int r = 0; r < RB; ++r) cs[r] = __shfl_sync(0xffffffffu, c, r);
+    if (lane == 0) {
+      float sum = 0.f;
+#pragma unroll
+      for (int r = 0; r < RB; ++r) sum = __fadd_rn(sum, cs[r]);
+      part[z * gridDim.x + blockIdx.x] = sum;
+    }
+  }
+  __syncthreads();
   for (int idx = tid; idx < RB * HW; idx += 256) {   // coalesced along j
     const int r = idx / HW, j = idx - r * HW, b = r0 + r;
     float d = 0.f;
-    if (b < B && Z2[((size_t)z * B + b) * HW + j] > 0.f) d = __fmul_rn(dq[(size_t)z * B + b], __bfloat162float(W3[j]));
+    if (b < B && Z2[((size_t)z * B + b) * HW + j] > 0.f) d = __fmul_rn(dqs[r], __bfloat162float(W3[j]));
     d2s[r * ldh + j] = __float2bfloat16_rn(d);
+  }
+  if (tid == 0) {   // publish the partial; the last CTA reduces all of them in (z, block) order
+    __threadfence();
+    const unsigned int n = gridDim.x * gridDim.y;
+    last = atomicAdd(ticket, 1u) == n - 1;
+    if (last && loss) {
+      __threadfence();
+      float tot = 0.f;
+      for (int zz = 0; zz < (int)gridDim.y; ++zz) {
+        float sz = 0.f;
+        for (int bx = 0; bx < (int)gridDim.x; ++bx) sz = __fadd_rn(sz, *(volatile float*)&part[zz * gridDim.x + bx]);
+        tot = mode == 0 ? __fadd_rn(tot, __fdiv_rn(sz, (float)B)) : __fsub_rn(tot, __fdiv_rn(sz, (float)B));
+      }
+      *loss = tot;
+    }
+    if (last) *ticket = 0u;
   }
   __syncthreads();
   if (store_t) {
@@ -368,11 +426,6 @@ __global__ void critic_refresh_kernel(const float* __restrict__ params, long lon
   }
 }
 
-__global__ void fill_dq_kernel(float* x, int n, float v) {
-  const int i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i < n) x[i] = v;
-}
-
 // loss = sum_z mean_b (Q_z - y)^2 ; dQ[z][b] = 2 (Q_z - y)/B. Single block, fixed order.
 __global__ void __launch_bounds__(256) critic_loss_mma_kernel(int B, int nz, const float* __restrict__ q,
                                                               const float* __restrict__ y, float* __restrict__ dq,
@@ -458,39 +511,47 @@ int critic_mma_fwd_bwd(const CriticDims& c, int B, const float* params2, const _
     critic_fwd_mma_kernel<<<grid, 256, 0, st>>>(
         B, Bp, S, A, L.inp, L.inq, obs, act, pb, L.P, L.tb, L.W1p, L.W2c, oW3, params2,
         (long long)c.off[SPIKERL_CRITIC_B1], (long long)c.off[SPIKERL_CRITIC_B2], (long long)c.off[SPIKERL_CRITIC_B3],
-        w.XT, w.H1T, w.Z1, w.Z2, w.Hh2, q, need_bwd ? 1 : 0);
+        w.XT, w.H1T, w.Z1, w.Z2, w.Hh2, q, need_bwd ? 1 : 0, need_bwd ? w.ticket : nullptr);
     SPK_LAUNCHED();
   }
   if (wait_before_loss) SPK_CHECK_CUDA(cudaStreamWaitEvent(st, wait_before_loss, 0));
-  if (y) {
+  // mode 0: critic update (dQ and the MSE from y); mode 1: actor step (dQ = act_scale, critic 0,
+  // scalar -mean Q). Both are formed inside the data-backward launch.
+  const int mode = want_params ? 0 : 1;
+  const bool fused_scalar = need_bwd && (want_params || !y);
+  if (y && !fused_scalar) {
     critic_loss_mma_kernel<<<1, 256, 0, st>>>(B, nz, q, y, w.dq, loss);
     SPK_LAUNCHED();
   }
   if (!need_bwd) return SPIKERL_OK;
-  int nb = nz;
-  if (!want_params) {
-    fill_dq_kernel<<<cdiv(B, 256), 256, 0, st>>>(w.dq, B, act_scale);
-    SPK_LAUNCHED();
-    nb = 1;
-  }
+  const int nb = want_params ? nz : 1;
   {
     ProfScope ps_("critic_bwd_data_mma", PB_TENSOR, 2.0 * B * nb * ((double)HW * HW), 0.0, st);
     dim3 grid(Bp / RB, nb);
-    critic_bwd_data_mma_kernel<<<grid, 256, 0, st>>>(B, Bp, S, A, L.inp, w.dq, pb, L.P, L.tb, oW3, L.W1T, L.W2T, w.Z1,
-                                                     w.Z2, w.dZ2T, w.dZ1T, grad_act, want_params ? 1 : 0);
+    critic_bwd_data_mma_kernel<<<grid, 256, 0, st>>>(
+        B, Bp, S, A, L.inp, q, y, mode, act_scale, w.dq, w.part, w.ticket, fused_scalar ? loss : nullptr, pb, L.P, L.tb,
+        oW3, L.W1T, L.W2T, w.Z1, w.Z2, w.dZ2T, w.dZ1T, grad_act, want_params ? 1 : 0);
     SPK_LAUNCHED();
   }
   if (want_params) {
-    ProfScope ps_("critic_wgrad_mma", PB_TENSOR, 2.0 * B * nz * ((double)HW * HW + (double)HW * c.in), 0.0, st);
-    dim3 grid(cdiv(L.inq > HW ? L.inq : HW, 256), 2 * (HW / RB), nz);
-    critic_wgrad_mma_kernel<<<grid, 256, 0, st>>>(Bp, c.in, L.inq, L.P, (long long)c.off[SPIKERL_CRITIC_W1],
-                                                  (long long)c.off[SPIKERL_CRITIC_W2], w.XT, w.H1T, w.dZ2T, w.dZ1T,
-                                                  grad2);
-    SPK_LAUNCHED();
-    critic_bias_grads_kernel<<<dim3(cdiv(3 * HW + 1, 8), nz), 256, 0, st>>>(
+    // the bias / w3 gradients run next to the weight-gradient GEMM
+    AuxPool* aux = nullptr;
+    SPK_TRY(aux_pool(&aux));
+    cudaStream_t sb = aux->side[6];
+    SPK_TRY(stream_after(sb, st, aux->ev[16]));
+    critic_bias_grads_kernel<<<dim3(cdiv(3 * HW + 1, 8), nz), 256, 0, sb>>>(
         B, Bp, L.P, (long long)c.off[SPIKERL_CRITIC_B1], (long long)c.off[SPIKERL_CRITIC_B2], oW3,
         (long long)c.off[SPIKERL_CRITIC_B3], w.dZ1T, w.dZ2T, w.dq, w.Hh2, grad2);
     SPK_LAUNCHED();
+    {
+      ProfScope ps_("critic_wgrad_mma", PB_TENSOR, 2.0 * B * nz * ((double)HW * HW + (double)HW * c.in), 0.0, st);
+      dim3 grid(cdiv(L.inq > HW ? L.inq : HW, 256), 2 * (HW / RB), nz);
+      critic_wgrad_mma_kernel<<<grid, 256, 0, st>>>(Bp, c.in, L.inq, L.P, (long long)c.off[SPIKERL_CRITIC_W1],
+                                                    (long long)c.off[SPIKERL_CRITIC_W2], w.XT, w.H1T, w.dZ2T, w.dZ1T,
+                                                    grad2);
+      SPK_LAUNCHED();
+    }
+    SPK_TRY(stream_after(st, sb, aux->ev[17]));
   }
   return SPIKERL_OK;
 }

@@ -78,3 +78,28 @@ int spikerl_prof_summary(spikerl_prof_entry* out, int max_entries) {
 }
 
 }  // extern "C"
+
+namespace spk {
+
+int aux_pool(AuxPool** out) {
+  static AuxPool pool[16];
+  static bool made[16] = {};
+  int dev = 0;
+  SPK_CHECK_CUDA(cudaGetDevice(&dev));
+  if (dev < 0 || dev >= 16) { set_error("device index %d out of range", dev); return SPIKERL_E_ARG; }
+  if (!made[dev]) {
+    for (auto& x : pool[dev].side) SPK_CHECK_CUDA(cudaStreamCreateWithFlags(&x, cudaStreamNonBlocking));
+    for (auto& e : pool[dev].ev) SPK_CHECK_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    made[dev] = true;
+  }
+  *out = &pool[dev];
+  return SPIKERL_OK;
+}
+
+int stream_after(cudaStream_t dst, cudaStream_t src, cudaEvent_t ev) {
+  SPK_CHECK_CUDA(cudaEventRecord(ev, src));
+  SPK_CHECK_CUDA(cudaStreamWaitEvent(dst, ev, 0));
+  return SPIKERL_OK;
+}
+
+}  // namespace spk

@@ -167,37 +167,6 @@ static ActorWs actor_ws_layout(const ActorDims& d, int B) {
   return w;
 }
 
-// Auxiliary streams / events (per device, created once outside any capture: the workspace-size
-// queries create them). The TD3 step (side 0-2, ev 0-7) and the actor backward (side 3-5,
-// ev 8-15) fork independent branches onto them and join them back before they return, so a
-// CUDA-graph capture records a DAG with parallel branches.
-struct Td3Aux {
-  cudaStream_t side[6];
-  cudaEvent_t ev[16];
-};
-
-static int td3_aux(Td3Aux** out) {
-  static Td3Aux pool[16];
-  static bool made[16] = {};
-  int dev = 0;
-  SPK_CHECK_CUDA(cudaGetDevice(&dev));
-  if (dev < 0 || dev >= 16) { set_error("device index %d out of range", dev); return SPIKERL_E_ARG; }
-  if (!made[dev]) {
-    for (auto& x : pool[dev].side) SPK_CHECK_CUDA(cudaStreamCreateWithFlags(&x, cudaStreamNonBlocking));
-    for (auto& e : pool[dev].ev) SPK_CHECK_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
-    made[dev] = true;
-  }
-  *out = &pool[dev];
-  return SPIKERL_OK;
-}
-
-// dst waits for everything enqueued on src so far
-static int stream_after(cudaStream_t dst, cudaStream_t src, cudaEvent_t ev) {
-  SPK_CHECK_CUDA(cudaEventRecord(ev, src));
-  SPK_CHECK_CUDA(cudaStreamWaitEvent(dst, ev, 0));
-  return SPIKERL_OK;
-}
-
 static int actor_forward_impl(const ActorDims& d, int B, const float* params,
                               const __nv_bfloat16* pb16, const float* obs, float* actions,
                               char* tape, cudaStream_t st) {
@@ -249,8 +218,8 @@ static int actor_backward_impl(const ActorDims& d, int B, const float* params,
   // then outscan -> dX3 -> dX2 -> max(encoder grad, dW1). Large problems stay on one stream
   // (persistent kernels that each own every SM).
   const bool tc = d.engine == SPIKERL_ENGINE_TCGEN05;
-  Td3Aux* aux = nullptr;
-  SPK_TRY(td3_aux(&aux));
+  AuxPool* aux = nullptr;
+  SPK_TRY(aux_pool(&aux));
   const bool fork = (long long)d.T * B <= 32768;
   cudaStream_t sw[4] = {st, st, st, st};   // sw[l]: stream of dW_l; sw[0]: decoder params
   if (fork) { sw[0] = aux->side[3]; sw[3] = aux->side[3]; sw[2] = aux->side[4]; sw[1] = aux->side[5]; }
@@ -396,14 +365,16 @@ size_t spikerl_actor_tape_bytes(const spikerl_actor_cfg* cfg, int batch) {
 size_t spikerl_actor_workspace_bytes(const spikerl_actor_cfg* cfg, int batch) {
   ActorDims d;
   if (actor_dims(cfg, &d) != SPIKERL_OK || batch < 1) return 0;
-  Td3Aux* aux = nullptr;   // create the fork/join streams now, outside any graph capture
-  if (td3_aux(&aux) != SPIKERL_OK) cudaGetLastError();   // no device (host-only query): later
+  AuxPool* aux = nullptr;   // create the fork/join streams now, outside any graph capture
+  if (aux_pool(&aux) != SPIKERL_OK) cudaGetLastError();   // no device (host-only query): later
   return actor_ws_layout(d, batch).total;
 }
 
 size_t spikerl_critic_workspace_bytes(const spikerl_critic_cfg* cfg, int batch) {
   CriticDims d;
   if (critic_dims(cfg, &d) != SPIKERL_OK || batch < 1) return 0;
+  AuxPool* aux = nullptr;   // create the fork/join streams now, outside any graph capture
+  if (aux_pool(&aux) != SPIKERL_OK) cudaGetLastError();   // no device (host-only query): later
   return critic_ws_bytes(d, batch);
 }
 
@@ -411,8 +382,8 @@ size_t spikerl_td3_workspace_bytes(const spikerl_actor_cfg* acfg, const spikerl_
   ActorDims ad;
   CriticDims cd;
   if (actor_dims(acfg, &ad) != SPIKERL_OK || critic_dims(ccfg, &cd) != SPIKERL_OK || batch < 1) return 0;
-  Td3Aux* aux = nullptr;   // create the fork/join streams now, outside any graph capture
-  if (td3_aux(&aux) != SPIKERL_OK) cudaGetLastError();   // no device (host-only query): later
+  AuxPool* aux = nullptr;   // create the fork/join streams now, outside any graph capture
+  if (aux_pool(&aux) != SPIKERL_OK) cudaGetLastError();   // no device (host-only query): later
   return td3_ws_layout(ad, cd, batch).total;
 }
 
@@ -515,7 +486,8 @@ int spikerl_critic_fwd_bwd(const spikerl_critic_cfg* cfg, int batch, const float
     return SPIKERL_E_ARG;
   }
   return critic_fwd_bwd(c, batch, params2, (const __nv_bfloat16*)params2_bf16, obs, obs_dim, act, act_dim, target_y,
-                        q, loss, grad_params2, grad_act, act_grad_scale, 2, workspace, (cudaStream_t)stream);
+                        q, target_y ? loss : nullptr, grad_params2, grad_act, act_grad_scale, 2, workspace,
+                        (cudaStream_t)stream);
 }
 
 int spikerl_adam(float* params, const float* grads, float* m, float* v, size_t n, long long* step_counter,
@@ -580,8 +552,8 @@ int spikerl_td3_update(const spikerl_actor_cfg* acfg, const spikerl_critic_cfg* 
   const __nv_bfloat16* cbf = (const __nv_bfloat16*)b->critic_bf16;
   const __nv_bfloat16* ctbf = (const __nv_bfloat16*)b->critic_t_bf16;
 
-  Td3Aux* aux = nullptr;
-  SPK_TRY(td3_aux(&aux));
+  AuxPool* aux = nullptr;
+  SPK_TRY(aux_pool(&aux));
   cudaStream_t sA = aux->side[0], sB = aux->side[1], sC = aux->side[2];
   static const bool serial = [] { const char* e = getenv("SPIKERL_TD3_SERIAL"); return e && e[0] == '1'; }();
   if (serial) sA = sB = sC = st;   // A/B switch: the same work on one stream
@@ -624,10 +596,14 @@ int spikerl_td3_update(const spikerl_actor_cfg* acfg, const spikerl_critic_cfg* 
     SPK_TRY(launch_polyak(b->critic_t, b->critic, 2 * Pc, hp->tau, &ctv, sC));
     SPK_CHECK_CUDA(cudaEventRecord(aux->ev[5], sC));
     SPK_CHECK_CUDA(cudaStreamWaitEvent(st, aux->ev[3], 0));   // pi(s) from branch B
-    SPK_TRY(critic_fwd_bwd(cd, B, b->critic, cbf, s, ad.S, api, ad.A, nullptr, q, nullptr, nullptr, ga,
-                           -1.0f / (float)B, 1, cws, st));
-    neg_mean_kernel<<<1, 256, 0, st>>>(B, q, losses + 1);
-    SPK_LAUNCHED();
+    // actor loss -mean Q1(s, pi(s)): formed by the mma critic's data-backward launch itself
+    const bool mma = critic_mma_ok(cd);
+    SPK_TRY(critic_fwd_bwd(cd, B, b->critic, cbf, s, ad.S, api, ad.A, nullptr, q, mma ? losses + 1 : nullptr, nullptr,
+                           ga, -1.0f / (float)B, 1, cws, st));
+    if (!mma) {
+      neg_mean_kernel<<<1, 256, 0, st>>>(B, q, losses + 1);
+      SPK_LAUNCHED();
+    }
     SPK_TRY(actor_backward_impl(ad, B, b->actor, abf, s, tape, ga, b->grad_actor, 0, aws, st));
     SPK_TRY(spikerl_allreduce_grads(comm, b->grad_actor, Pa, stream));
     SPK_TRY(launch_adam(b->actor, b->grad_actor, b->m_actor, b->v_actor, Pa, b->adam_steps + 2, hp->lr_actor,
