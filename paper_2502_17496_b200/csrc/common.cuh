@@ -23,6 +23,7 @@ inline int num_sms() {
 // ----------------------------------------------------------------------------- errors
 void set_error(const char* fmt, ...);
 void note_launch(int n = 1);
+cudaError_t take_launch_error();
 
 #define SPK_CHECK_CUDA(expr)                                                         \
   do {                                                                               \
@@ -37,7 +38,8 @@ void note_launch(int n = 1);
 #define SPK_LAUNCHED()                                                               \
   do {                                                                               \
     ::spk::note_launch();                                                            \
-    cudaError_t e_ = cudaGetLastError();                                             \
+    cudaError_t e_ = ::spk::take_launch_error();                                     \
+    if (e_ == cudaSuccess) e_ = cudaGetLastError();                                  \
     if (e_ != cudaSuccess) {                                                         \
       ::spk::set_error("kernel launch failed: %s (%s:%d)", cudaGetErrorString(e_),   \
                        __FILE__, __LINE__);                                          \
@@ -50,6 +52,45 @@ void note_launch(int n = 1);
     int s_ = (expr);                                                                 \
     if (s_ != SPIKERL_OK) return s_;                                                 \
   } while (0)
+
+// ----------------------------------------------------------------------------- PDL
+// Programmatic dependent launch: every library kernel is launched with programmatic stream
+// serialization and begins with pdl_wait() (returns once the preceding kernel in the stream has
+// completed and its writes are visible; a no-op without PDL) and pdl_trigger() (the next kernel
+// may be scheduled now and run its prologue: launch latency, barrier / TMEM setup, tensor-map
+// prefetch overlap this kernel). Because every kernel waits before touching global memory,
+// completion stays transitive along the stream. SPIKERL_PDL=0 turns the attribute off.
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+bool pdl_enabled();
+void note_launch_error(cudaError_t e);
+
+template <typename... KArgs>
+struct PdlLaunch {
+  void (*k)(KArgs...);
+  dim3 g, b;
+  size_t smem;
+  cudaStream_t st;
+  template <typename... Args>
+  void operator()(Args&&... args) const {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = g;
+    cfg.blockDim = b;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = pdl_enabled() ? 1 : 0;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    const cudaError_t e = cudaLaunchKernelEx(&cfg, k, static_cast<KArgs>(args)...);
+    if (e != cudaSuccess) note_launch_error(e);
+  }
+};
+template <typename... KArgs>
+inline PdlLaunch<KArgs...> pdl(void (*k)(KArgs...), dim3 g, dim3 b, size_t smem, cudaStream_t st) {
+  return PdlLaunch<KArgs...>{k, g, b, smem, st};
+}
 
 inline size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
 inline int round_up(int x, int a) { return (x + a - 1) / a * a; }

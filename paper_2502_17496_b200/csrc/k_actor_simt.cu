@@ -23,6 +23,8 @@ __global__ void __launch_bounds__(128) lif_fwd_simt_kernel(
     int B, int T, int N, int Win, int Wout, const uint32_t* __restrict__ bits_in,
     const WT* __restrict__ W, int ldw_, LifConst kc, uint32_t* __restrict__ bits_out,
     uint32_t* __restrict__ mask_out, uint8_t* __restrict__ counts) {
+  pdl_wait();
+  pdl_trigger();
   extern __shared__ uint32_t s_words[];
   const int b = blockIdx.x;
   const int n = blockIdx.y * 128 + threadIdx.x;
@@ -73,10 +75,10 @@ int launch_lif_fwd_simt(const ActorDims& d, int l, int B, const uint32_t* bits_i
   const int Win = d.Wd[l - 1], Wout = d.Wd[l];
   const size_t smem = sizeof(uint32_t) * Win;
   if (d.bf16) {
-    lif_fwd_simt_kernel<__nv_bfloat16><<<grid, 128, smem, st>>>(
+    pdl((lif_fwd_simt_kernel<__nv_bfloat16>), grid, 128, smem, st)(
         B, d.T, d.N[l], Win, Wout, bits_in, Wb16, d.P[l - 1], kc, bits_out, mask_out, counts);
   } else {
-    lif_fwd_simt_kernel<float><<<grid, 128, smem, st>>>(B, d.T, d.N[l], Win, Wout, bits_in, Wf32,
+    pdl((lif_fwd_simt_kernel<float>), grid, 128, smem, st)(B, d.T, d.N[l], Win, Wout, bits_in, Wf32,
                                                        d.N[l - 1], kc, bits_out, mask_out, counts);
   }
   SPK_LAUNCHED();
@@ -87,6 +89,8 @@ int launch_lif_fwd_simt(const ActorDims& d, int l, int B, const uint32_t* bits_i
 __global__ void dec_fwd_kernel(int B, int A, int D, int T, const uint8_t* __restrict__ counts,
                                const float* __restrict__ Wd, const float* __restrict__ bd,
                                float* __restrict__ act_out, float* __restrict__ act_tape) {
+  pdl_wait();
+  pdl_trigger();
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= B * A) return;
   const int b = i / A, j = i % A;
@@ -108,7 +112,7 @@ int launch_dec_fwd(const ActorDims& d, int B, const uint8_t* counts, const float
                    const float* bd, float* act_out, float* act_tape, cudaStream_t st) {
   ProfScope ps_("dec_fwd", PB_LATENCY, 0.0, (double)B * (d.N3 + 8.0 * d.A), st);
   const int n = B * d.A;
-  dec_fwd_kernel<<<cdiv(n, 256), 256, 0, st>>>(B, d.A, d.D, d.T, counts, Wd, bd, act_out, act_tape);
+  pdl(dec_fwd_kernel, cdiv(n, 256), 256, 0, st)(B, d.A, d.D, d.T, counts, Wd, bd, act_out, act_tape);
   SPK_LAUNCHED();
   return SPIKERL_OK;
 }
@@ -136,6 +140,8 @@ __global__ void __launch_bounds__(128) dec_bwd_outscan_kernel(
     const float* __restrict__ grad_a, const float* __restrict__ act, const float* __restrict__ Wd,
     const uint32_t* __restrict__ bits3, const uint32_t* __restrict__ mask3, GTy* __restrict__ G3,
     float* __restrict__ g_pre_out) {
+  pdl_wait();
+  pdl_trigger();
   const int n = blockIdx.y * 128 + threadIdx.x;
   const int lane = threadIdx.x & 31;
   const int N3 = A * D;
@@ -189,11 +195,11 @@ int launch_dec_bwd_outscan(const ActorDims& d, int B, const float* grad_a, const
   if (gx > B) gx = B;
   dim3 grid(gx, gy);
   if (d.bf16)
-    dec_bwd_outscan_kernel<__nv_bfloat16><<<grid, 128, 0, st>>>(
+    pdl((dec_bwd_outscan_kernel<__nv_bfloat16>), grid, 128, 0, st)(
         B, d.T, d.A, d.D, d.P[3], d.Wd[3], d.dc, d.dv, d.zh, grad_a, act, Wd, bits3, mask3,
         (__nv_bfloat16*)G3, g_pre);
   else
-    dec_bwd_outscan_kernel<float><<<grid, 128, 0, st>>>(B, d.T, d.A, d.D, d.P[3], d.Wd[3], d.dc,
+    pdl((dec_bwd_outscan_kernel<float>), grid, 128, 0, st)(B, d.T, d.A, d.D, d.P[3], d.Wd[3], d.dc,
                                                         d.dv, d.zh, grad_a, act, Wd, bits3, mask3,
                                                         (float*)G3, g_pre);
   SPK_LAUNCHED();
@@ -207,6 +213,8 @@ __global__ void __launch_bounds__(256) dec_param_grads_kernel(int B, int A, int 
                                                               const uint8_t* __restrict__ counts,
                                                               float* __restrict__ dWd,
                                                               float* __restrict__ dbd, int accum) {
+  pdl_wait();
+  pdl_trigger();
   const int j = blockIdx.x, e = blockIdx.y;  // e == D -> bias
   const int N3 = A * D;
   float s = 0.f;
@@ -232,7 +240,7 @@ int launch_dec_param_grads(const ActorDims& d, int B, const float* g_pre, const 
                            float* dWd, float* dbd, int accumulate, cudaStream_t st) {
   ProfScope ps_("dec_param_grads", PB_LATENCY, 0.0, (double)B * (4.0 * d.A + d.N3), st);
   dim3 grid(d.A, d.D + 1);
-  dec_param_grads_kernel<<<grid, 256, 0, st>>>(B, d.A, d.D, d.T, g_pre, counts, dWd, dbd, accumulate);
+  pdl(dec_param_grads_kernel, grid, 256, 0, st)(B, d.A, d.D, d.T, g_pre, counts, dWd, dbd, accumulate);
   SPK_LAUNCHED();
   return SPIKERL_OK;
 }
@@ -245,6 +253,8 @@ __global__ void __launch_bounds__(128) lif_dx_simt_kernel(
     int B, int T, int Nl, int Pl, int Nprev, int Pprev, int Wprev, float dcc, float dvc, float zh,
     const GTy* __restrict__ Gl, const WT* __restrict__ W, int ldw_, const uint32_t* __restrict__ bits,
     const uint32_t* __restrict__ mask, GTy* __restrict__ Gprev, GTy* __restrict__ Gsum) {
+  pdl_wait();
+  pdl_trigger();
   extern __shared__ float s_g[];
   const int b = blockIdx.x;
   const int k = blockIdx.y * 128 + threadIdx.x;
@@ -274,12 +284,12 @@ int launch_lif_dx_simt(const ActorDims& d, int l, int B, const void* Gl, const f
   dim3 grid(B, d.P[l - 1] / 128);
   const size_t smem = sizeof(float) * d.N[l];
   if (d.bf16)
-    lif_dx_simt_kernel<__nv_bfloat16, __nv_bfloat16><<<grid, 128, smem, st>>>(
+    pdl((lif_dx_simt_kernel<__nv_bfloat16, __nv_bfloat16>), grid, 128, smem, st)(
         B, d.T, d.N[l], d.P[l], d.N[l - 1], d.P[l - 1], d.Wd[l - 1], d.dc, d.dv, d.zh,
         (const __nv_bfloat16*)Gl, Wb16, d.P[l - 1], bits_prev, mask_prev, (__nv_bfloat16*)Gprev,
         (__nv_bfloat16*)Gsum);
   else
-    lif_dx_simt_kernel<float, float><<<grid, 128, smem, st>>>(
+    pdl((lif_dx_simt_kernel<float, float>), grid, 128, smem, st)(
         B, d.T, d.N[l], d.P[l], d.N[l - 1], d.P[l - 1], d.Wd[l - 1], d.dc, d.dv, d.zh,
         (const float*)Gl, Wf32, d.N[l - 1], bits_prev, mask_prev, (float*)Gprev, (float*)Gsum);
   SPK_LAUNCHED();
@@ -294,6 +304,8 @@ __global__ void __launch_bounds__(128) lif_dw_simt_kernel(int R, int Nl, int Pl,
                                                           const GTy* __restrict__ Gl,
                                                           const uint32_t* __restrict__ bits,
                                                           float* __restrict__ dW, int accum) {
+  pdl_wait();
+  pdl_trigger();
   __shared__ float s_g[256];
   const int n = blockIdx.y;
   const int k = blockIdx.x * 128 + threadIdx.x;
@@ -325,10 +337,10 @@ int launch_lif_dw_simt(const ActorDims& d, int l, int B, const void* Gl, const u
   dim3 grid(cdiv(K, 128), d.N[l]);
   const int R = d.T * B;
   if (d.bf16)
-    lif_dw_simt_kernel<__nv_bfloat16><<<grid, 128, 0, st>>>(
+    pdl((lif_dw_simt_kernel<__nv_bfloat16>), grid, 128, 0, st)(
         R, d.N[l], d.P[l], K, d.Wd[l - 1], (const __nv_bfloat16*)Gl, bits_prev, dW, accumulate);
   else
-    lif_dw_simt_kernel<float><<<grid, 128, 0, st>>>(R, d.N[l], d.P[l], K, d.Wd[l - 1],
+    pdl((lif_dw_simt_kernel<float>), grid, 128, 0, st)(R, d.N[l], d.P[l], K, d.Wd[l - 1],
                                                     (const float*)Gl, bits_prev, dW, accumulate);
   SPK_LAUNCHED();
   return SPIKERL_OK;
@@ -349,6 +361,8 @@ __global__ void __launch_bounds__(128) enc_grad_partial_kernel(
     const WT* __restrict__ W1, int ldw_, const float* __restrict__ A,
     const float* __restrict__ obs, const float* __restrict__ mu, const float* __restrict__ sigma,
     float* __restrict__ partial) {
+  pdl_wait();
+  pdl_trigger();
   extern __shared__ float s_g[];
   const int k = blockIdx.x * 128 + threadIdx.x;
   const int chunk = blockIdx.y;
@@ -378,6 +392,8 @@ __global__ void __launch_bounds__(128) enc_grad_partial_kernel(
 
 __global__ void enc_grad_reduce_kernel(int nchunk, int K0, const float* __restrict__ partial,
                                        float* __restrict__ dmu, float* __restrict__ dsg, int accum) {
+  pdl_wait();
+  pdl_trigger();
   const int k = blockIdx.x * blockDim.x + threadIdx.x;
   if (k >= K0) return;
   float a = 0.f, s = 0.f;
@@ -391,7 +407,7 @@ __global__ void enc_grad_reduce_kernel(int nchunk, int K0, const float* __restri
 
 int launch_enc_grad_reduce(const ActorDims& d, int nchunk, const float* partial, float* dmu,
                            float* dsigma, int accumulate, cudaStream_t st) {
-  enc_grad_reduce_kernel<<<cdiv(d.K0, 256), 256, 0, st>>>(nchunk, d.K0, partial, dmu, dsigma, accumulate);
+  pdl(enc_grad_reduce_kernel, cdiv(d.K0, 256), 256, 0, st)(nchunk, d.K0, partial, dmu, dsigma, accumulate);
   SPK_LAUNCHED();
   return SPIKERL_OK;
 }
@@ -405,15 +421,15 @@ int launch_enc_grad_simt(const ActorDims& d, int B, const void* Gsum, const floa
   dim3 grid(cdiv(d.K0, 128), nchunk);
   const size_t smem = sizeof(float) * d.N1;
   if (d.bf16)
-    enc_grad_partial_kernel<__nv_bfloat16, __nv_bfloat16><<<grid, 128, smem, st>>>(
+    pdl((enc_grad_partial_kernel<__nv_bfloat16, __nv_bfloat16>), grid, 128, smem, st)(
         B, d.S, d.E, d.K0, d.N1, d.P[1], (const __nv_bfloat16*)Gsum, W1b16, d.P[0], A, obs, mu,
         sigma, partial);
   else
-    enc_grad_partial_kernel<float, float><<<grid, 128, smem, st>>>(
+    pdl((enc_grad_partial_kernel<float, float>), grid, 128, smem, st)(
         B, d.S, d.E, d.K0, d.N1, d.P[1], (const float*)Gsum, W1f32, d.K0, A, obs, mu, sigma,
         partial);
   SPK_LAUNCHED();
-  enc_grad_reduce_kernel<<<cdiv(d.K0, 256), 256, 0, st>>>(nchunk, d.K0, partial, dmu, dsigma,
+  pdl(enc_grad_reduce_kernel, cdiv(d.K0, 256), 256, 0, st)(nchunk, d.K0, partial, dmu, dsigma,
                                                           accumulate);
   SPK_LAUNCHED();
   return SPIKERL_OK;

@@ -34,6 +34,8 @@ constexpr int TM = 32, TN = 32, TK = 32;
 
 template <typename TA, typename TB, int EPI>
 __global__ void __launch_bounds__(256) gemm_simt_kernel(GemmArgs g) {
+  pdl_wait();
+  pdl_trigger();
   __shared__ float sA[TK][TM + 1];
   __shared__ float sB[TK][TN + 1];
   const int z = blockIdx.z;
@@ -118,16 +120,18 @@ template <int EPI>
 int run_gemm(const GemmArgs& g, int nz, bool a_bf16, bool b_bf16, cudaStream_t st) {
   ProfScope ps_("critic_gemm_simt", PB_ALU, 2.0 * g.M * (double)g.N * g.K * nz, 0.0, st);
   dim3 grid(cdiv(g.N, TN), cdiv(g.M, TM), nz);
-  if (a_bf16 && b_bf16) gemm_simt_kernel<__nv_bfloat16, __nv_bfloat16, EPI><<<grid, 256, 0, st>>>(g);
-  else if (a_bf16) gemm_simt_kernel<__nv_bfloat16, float, EPI><<<grid, 256, 0, st>>>(g);
-  else if (b_bf16) gemm_simt_kernel<float, __nv_bfloat16, EPI><<<grid, 256, 0, st>>>(g);
-  else gemm_simt_kernel<float, float, EPI><<<grid, 256, 0, st>>>(g);
+  if (a_bf16 && b_bf16) pdl((gemm_simt_kernel<__nv_bfloat16, __nv_bfloat16, EPI>), grid, 256, 0, st)(g);
+  else if (a_bf16) pdl((gemm_simt_kernel<__nv_bfloat16, float, EPI>), grid, 256, 0, st)(g);
+  else if (b_bf16) pdl((gemm_simt_kernel<float, __nv_bfloat16, EPI>), grid, 256, 0, st)(g);
+  else pdl((gemm_simt_kernel<float, float, EPI>), grid, 256, 0, st)(g);
   SPK_LAUNCHED();
   return SPIKERL_OK;
 }
 
 __global__ void build_x_kernel(int B, int S, int A, const float* __restrict__ obs,
                                const float* __restrict__ act, int round, float* __restrict__ X) {
+  pdl_wait();
+  pdl_trigger();
   const int in = S + A;
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < B * in; i += gridDim.x * blockDim.x) {
     const int b = i / in, c = i % in;
@@ -142,6 +146,8 @@ template <typename TW>
 __global__ void critic_out_kernel(int B, int H2, const float* __restrict__ H, long long h_bs,
                                   const TW* __restrict__ W3, long long w_bs,
                                   const float* __restrict__ b3, long long b_bs, float* __restrict__ q) {
+  pdl_wait();
+  pdl_trigger();
   const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
   const int z = blockIdx.y;
   if (warp >= B) return;
@@ -158,6 +164,8 @@ __global__ void __launch_bounds__(256) critic_loss_kernel(int B, int nz, const f
                                                           const float* __restrict__ y,
                                                           float* __restrict__ dq,
                                                           float* __restrict__ loss) {
+  pdl_wait();
+  pdl_trigger();
   __shared__ float red[256];
   float tot = 0.f;
   for (int z = 0; z < nz; ++z) {
@@ -180,6 +188,8 @@ __global__ void __launch_bounds__(256) critic_loss_kernel(int B, int nz, const f
 }
 
 __global__ void fill_kernel(float* x, int n, float v) {
+  pdl_wait();
+  pdl_trigger();
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i < n) x[i] = v;
 }
@@ -190,6 +200,8 @@ __global__ void critic_dz2_kernel(int B, int H2, const float* __restrict__ dq,
                                   const TW* __restrict__ W3, long long w_bs,
                                   const float* __restrict__ Z2, long long zb, int round,
                                   float* __restrict__ dZ2) {
+  pdl_wait();
+  pdl_trigger();
   const int z = blockIdx.y;
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < B * H2; i += gridDim.x * blockDim.x) {
     const int b = i / H2, j = i % H2;
@@ -203,6 +215,8 @@ __global__ void critic_dz2_kernel(int B, int H2, const float* __restrict__ dq,
 __global__ void __launch_bounds__(256) colsum_kernel(int B, int N, const float* __restrict__ M, long long m_bs,
                                                      const float* __restrict__ wgt, long long w_bs,
                                                      float* __restrict__ out, long long o_bs) {
+  pdl_wait();
+  pdl_trigger();
   __shared__ float red[8][33];
   const int z = blockIdx.y;
   const int jl = threadIdx.x & 31, rg = threadIdx.x >> 5;
@@ -227,6 +241,8 @@ __global__ void __launch_bounds__(256) colsum_kernel(int B, int N, const float* 
 // db3[z] = sum_b dQ[z][b]
 __global__ void sum_dq_kernel(int B, const float* __restrict__ dq, float* __restrict__ out,
                               long long o_bs) {
+  pdl_wait();
+  pdl_trigger();
   const int z = blockIdx.x;
   if (threadIdx.x != 0) return;
   float s = 0.f;
@@ -236,6 +252,8 @@ __global__ void sum_dq_kernel(int B, const float* __restrict__ dq, float* __rest
 
 __global__ void slice_cols_kernel(int B, int in, int S, int A, const float* __restrict__ dX,
                                   float* __restrict__ out) {
+  pdl_wait();
+  pdl_trigger();
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= B * A) return;
   const int b = i / A, a = i % A;
@@ -288,7 +306,7 @@ int critic_fwd_bwd(const CriticDims& c, int B, const float* params2, const __nv_
   };
   (void)Wbase;
   const int in = c.in, H1 = c.H1, H2 = c.H2;
-  build_x_kernel<<<cdiv((long long)B * in, 256) < 1184 ? cdiv((long long)B * in, 256) : 1184, 256, 0, st>>>(
+  pdl(build_x_kernel, cdiv((long long)B * in, 256) < 1184 ? cdiv((long long)B * in, 256) : 1184, 256, 0, st)(
       B, S, A, obs, act, bf, w.X);
   SPK_LAUNCHED();
   // layer 1: Z1 = X W1^T + b1 ; H1 = round(relu(Z1))
@@ -315,11 +333,11 @@ int critic_fwd_bwd(const CriticDims& c, int B, const float* params2, const __nv_
   {
     dim3 grid(cdiv((long long)B * 32, 256), nz);
     if (bf)
-      critic_out_kernel<__nv_bfloat16><<<grid, 256, 0, st>>>(
+      pdl((critic_out_kernel<__nv_bfloat16>), grid, 256, 0, st)(
           B, H2, w.H2, (long long)B * H2, pb16 + c.off[SPIKERL_CRITIC_W3], P,
           params2 + c.off[SPIKERL_CRITIC_B3], P, q);
     else
-      critic_out_kernel<float><<<grid, 256, 0, st>>>(B, H2, w.H2, (long long)B * H2,
+      pdl((critic_out_kernel<float>), grid, 256, 0, st)(B, H2, w.H2, (long long)B * H2,
                                                      params2 + c.off[SPIKERL_CRITIC_W3], P,
                                                      params2 + c.off[SPIKERL_CRITIC_B3], P, q);
     SPK_LAUNCHED();
@@ -327,14 +345,14 @@ int critic_fwd_bwd(const CriticDims& c, int B, const float* params2, const __nv_
   const bool want_params = (y != nullptr && grad2 != nullptr);
   if (wait_before_loss) SPK_CHECK_CUDA(cudaStreamWaitEvent(st, wait_before_loss, 0));
   if (y) {
-    critic_loss_kernel<<<1, 256, 0, st>>>(B, nz, q, y, w.dq, loss);
+    pdl(critic_loss_kernel, 1, 256, 0, st)(B, nz, q, y, w.dq, loss);
     SPK_LAUNCHED();
   }
   if (!want_params && !grad_act) return SPIKERL_OK;
   int nb = nz;
   if (!want_params) {
     // actor step: dQ1 = act_scale for every sample, critic 0 only
-    fill_kernel<<<cdiv(B, 256), 256, 0, st>>>(w.dq, B, act_scale);
+    pdl(fill_kernel, cdiv(B, 256), 256, 0, st)(w.dq, B, act_scale);
     SPK_LAUNCHED();
     nb = 1;
   }
@@ -342,10 +360,10 @@ int critic_fwd_bwd(const CriticDims& c, int B, const float* params2, const __nv_
   {
     dim3 grid(cdiv((long long)B * H2, 256) < 1184 ? cdiv((long long)B * H2, 256) : 1184, nb);
     if (bf)
-      critic_dz2_kernel<__nv_bfloat16><<<grid, 256, 0, st>>>(B, H2, w.dq, pb16 + c.off[SPIKERL_CRITIC_W3], P,
+      pdl((critic_dz2_kernel<__nv_bfloat16>), grid, 256, 0, st)(B, H2, w.dq, pb16 + c.off[SPIKERL_CRITIC_W3], P,
                                                              w.Z2, (long long)B * H2, bf, w.dZ2);
     else
-      critic_dz2_kernel<float><<<grid, 256, 0, st>>>(B, H2, w.dq, params2 + c.off[SPIKERL_CRITIC_W3], P,
+      pdl((critic_dz2_kernel<float>), grid, 256, 0, st)(B, H2, w.dq, params2 + c.off[SPIKERL_CRITIC_W3], P,
                                                      w.Z2, (long long)B * H2, bf, w.dZ2);
     SPK_LAUNCHED();
   }
@@ -361,10 +379,10 @@ int critic_fwd_bwd(const CriticDims& c, int B, const float* params2, const __nv_
   }
   if (want_params) {
     // dW3 = dQ^T H2, db3 = sum dQ
-    colsum_kernel<<<dim3(cdiv(H2, 32), nz), 256, 0, st>>>(B, H2, w.H2, (long long)B * H2, w.dq, B,
+    pdl(colsum_kernel, dim3(cdiv(H2, 32), nz), 256, 0, st)(B, H2, w.H2, (long long)B * H2, w.dq, B,
                                                            grad2 + c.off[SPIKERL_CRITIC_W3], P);
     SPK_LAUNCHED();
-    sum_dq_kernel<<<nz, 32, 0, st>>>(B, w.dq, grad2 + c.off[SPIKERL_CRITIC_B3], P);
+    pdl(sum_dq_kernel, nz, 32, 0, st)(B, w.dq, grad2 + c.off[SPIKERL_CRITIC_B3], P);
     SPK_LAUNCHED();
     // dW2 = dZ2^T H1 ; db2 = colsum dZ2
     {
@@ -375,7 +393,7 @@ int critic_fwd_bwd(const CriticDims& c, int B, const float* params2, const __nv_
       g.C = grad2 + c.off[SPIKERL_CRITIC_W2]; g.ldc = H1; g.c_bs = P;
       SPK_TRY(run_gemm<EPI_STORE>(g, nz, false, false, st));
     }
-    colsum_kernel<<<dim3(cdiv(H2, 32), nz), 256, 0, st>>>(B, H2, w.dZ2, (long long)B * H2, nullptr, 0,
+    pdl(colsum_kernel, dim3(cdiv(H2, 32), nz), 256, 0, st)(B, H2, w.dZ2, (long long)B * H2, nullptr, 0,
                                                            grad2 + c.off[SPIKERL_CRITIC_B2], P);
     SPK_LAUNCHED();
     // dW1 = dZ1^T X ; db1 = colsum dZ1
@@ -387,7 +405,7 @@ int critic_fwd_bwd(const CriticDims& c, int B, const float* params2, const __nv_
       g.C = grad2 + c.off[SPIKERL_CRITIC_W1]; g.ldc = in; g.c_bs = P;
       SPK_TRY(run_gemm<EPI_STORE>(g, nz, false, false, st));
     }
-    colsum_kernel<<<dim3(cdiv(H1, 32), nz), 256, 0, st>>>(B, H1, w.dZ1, (long long)B * H1, nullptr, 0,
+    pdl(colsum_kernel, dim3(cdiv(H1, 32), nz), 256, 0, st)(B, H1, w.dZ1, (long long)B * H1, nullptr, 0,
                                                            grad2 + c.off[SPIKERL_CRITIC_B1], P);
     SPK_LAUNCHED();
   }
@@ -399,7 +417,7 @@ int critic_fwd_bwd(const CriticDims& c, int B, const float* params2, const __nv_
     g.Bm = Wp(SPIKERL_CRITIC_W1); g.sbk = in; g.sbn = 1; g.b_bs = 0;
     g.C = w.dX; g.ldc = in; g.c_bs = 0;
     SPK_TRY(run_gemm<EPI_STORE>(g, 1, false, bf, st));
-    slice_cols_kernel<<<cdiv((long long)B * A, 256), 256, 0, st>>>(B, in, S, A, w.dX, grad_act);
+    pdl(slice_cols_kernel, cdiv((long long)B * A, 256), 256, 0, st)(B, in, S, A, w.dX, grad_act);
     SPK_LAUNCHED();
   }
   return SPIKERL_OK;

@@ -124,6 +124,8 @@ __global__ void __launch_bounds__(256) critic_fwd_mma_kernel(
     long long oW3, const float* __restrict__ params, long long oB1, long long oB2, long long oB3,
     __nv_bfloat16* __restrict__ XT, __nv_bfloat16* __restrict__ H1T, float* __restrict__ Z1,
     float* __restrict__ Z2, float* __restrict__ Hh2, float* __restrict__ q, int store, unsigned int* ticket) {
+  pdl_wait();
+  pdl_trigger();
   __shared__ __align__(16) __nv_bfloat16 xs[RB * (512 + SPAD)];
   __shared__ __align__(16) __nv_bfloat16 h1s[RB * (HW + SPAD)];
   __shared__ float red[NWARP][RB];
@@ -221,6 +223,8 @@ __global__ void __launch_bounds__(256) critic_bwd_data_mma_kernel(
     long long P, long long tb, long long oW3, long long oW1T, long long oW2T, const float* __restrict__ Z1,
     const float* __restrict__ Z2, __nv_bfloat16* __restrict__ dZ2T, __nv_bfloat16* __restrict__ dZ1T,
     float* __restrict__ grad_act, int store_t) {
+  pdl_wait();
+  pdl_trigger();
   __shared__ __align__(16) __nv_bfloat16 d2s[RB * (HW + SPAD)];
   __shared__ __align__(16) __nv_bfloat16 d1s[RB * (HW + SPAD)];
   __shared__ float dqs[RB];
@@ -335,6 +339,8 @@ __global__ void __launch_bounds__(256) critic_wgrad_mma_kernel(
     int Bp, int in, int inq, long long P, long long oW1, long long oW2, const __nv_bfloat16* __restrict__ XT,
     const __nv_bfloat16* __restrict__ H1T, const __nv_bfloat16* __restrict__ dZ2T,
     const __nv_bfloat16* __restrict__ dZ1T, float* __restrict__ grad2) {
+  pdl_wait();
+  pdl_trigger();
   const int z = blockIdx.z, tid = threadIdx.x, warp = tid >> 5;
   const int lane = tid & 31, g = lane >> 2, t = lane & 3;
   const int ntile = HW / RB;
@@ -368,6 +374,8 @@ __global__ void __launch_bounds__(256) critic_bias_grads_kernel(int B, int Bp, l
                                                                 const float* __restrict__ dq,
                                                                 const float* __restrict__ Hh2,
                                                                 float* __restrict__ grad2) {
+  pdl_wait();
+  pdl_trigger();
   const int z = blockIdx.y;
   const int o = blockIdx.x * 8 + (threadIdx.x >> 5), lane = threadIdx.x & 31;
   const int nout = 3 * HW + 1;
@@ -397,6 +405,8 @@ __global__ void __launch_bounds__(256) critic_bias_grads_kernel(int B, int Bp, l
 __global__ void critic_refresh_kernel(const float* __restrict__ params, long long P, int in, int H1, int H2,
                                       int inp, int inq, long long oW1, long long oW2, long long tb,
                                       __nv_bfloat16* __restrict__ out) {
+  pdl_wait();
+  pdl_trigger();
   const long long total = 2 * P + 2 * tb;
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < total; i += (long long)gridDim.x * blockDim.x) {
     float v;
@@ -430,6 +440,8 @@ __global__ void critic_refresh_kernel(const float* __restrict__ params, long lon
 __global__ void __launch_bounds__(256) critic_loss_mma_kernel(int B, int nz, const float* __restrict__ q,
                                                               const float* __restrict__ y, float* __restrict__ dq,
                                                               float* __restrict__ loss) {
+  pdl_wait();
+  pdl_trigger();
   __shared__ float red[256];
   float tot = 0.f;
   for (int z = 0; z < nz; ++z) {
@@ -488,7 +500,7 @@ int launch_critic_refresh(const CriticDims& c, const float* params2, __nv_bfloat
   if (!critic_mma_ok(c)) return launch_f32_to_bf16(params2, out, 2 * c.off[SPIKERL_CRITIC_NPARAM], st);
   const MmaLayout L = mma_layout(c);
   const long long total = 2 * L.P + 2 * L.tb;
-  critic_refresh_kernel<<<(int)(cdiv(total, 256) < 1184 ? cdiv(total, 256) : 1184), 256, 0, st>>>(
+  pdl(critic_refresh_kernel, (int)(cdiv(total, 256) < 1184 ? cdiv(total, 256) : 1184), 256, 0, st)(
       params2, L.P, c.in, c.H1, c.H2, L.inp, L.inq, (long long)c.off[SPIKERL_CRITIC_W1],
       (long long)c.off[SPIKERL_CRITIC_W2], L.tb, out);
   SPK_LAUNCHED();
@@ -508,7 +520,7 @@ int critic_mma_fwd_bwd(const CriticDims& c, int B, const float* params2, const _
   {
     ProfScope ps_("critic_fwd_mma", PB_TENSOR, 2.0 * B * nz * ((double)c.in * HW + (double)HW * HW + HW), 0.0, st);
     dim3 grid(Bp / RB, nz);
-    critic_fwd_mma_kernel<<<grid, 256, 0, st>>>(
+    pdl(critic_fwd_mma_kernel, grid, 256, 0, st)(
         B, Bp, S, A, L.inp, L.inq, obs, act, pb, L.P, L.tb, L.W1p, L.W2c, oW3, params2,
         (long long)c.off[SPIKERL_CRITIC_B1], (long long)c.off[SPIKERL_CRITIC_B2], (long long)c.off[SPIKERL_CRITIC_B3],
         w.XT, w.H1T, w.Z1, w.Z2, w.Hh2, q, need_bwd ? 1 : 0, need_bwd ? w.ticket : nullptr);
@@ -520,7 +532,7 @@ int critic_mma_fwd_bwd(const CriticDims& c, int B, const float* params2, const _
   const int mode = want_params ? 0 : 1;
   const bool fused_scalar = need_bwd && (want_params || !y);
   if (y && !fused_scalar) {
-    critic_loss_mma_kernel<<<1, 256, 0, st>>>(B, nz, q, y, w.dq, loss);
+    pdl(critic_loss_mma_kernel, 1, 256, 0, st)(B, nz, q, y, w.dq, loss);
     SPK_LAUNCHED();
   }
   if (!need_bwd) return SPIKERL_OK;
@@ -528,7 +540,7 @@ int critic_mma_fwd_bwd(const CriticDims& c, int B, const float* params2, const _
   {
     ProfScope ps_("critic_bwd_data_mma", PB_TENSOR, 2.0 * B * nb * ((double)HW * HW), 0.0, st);
     dim3 grid(Bp / RB, nb);
-    critic_bwd_data_mma_kernel<<<grid, 256, 0, st>>>(
+    pdl(critic_bwd_data_mma_kernel, grid, 256, 0, st)(
         B, Bp, S, A, L.inp, q, y, mode, act_scale, w.dq, w.part, w.ticket, fused_scalar ? loss : nullptr, pb, L.P, L.tb,
         oW3, L.W1T, L.W2T, w.Z1, w.Z2, w.dZ2T, w.dZ1T, grad_act, want_params ? 1 : 0);
     SPK_LAUNCHED();
@@ -539,14 +551,14 @@ int critic_mma_fwd_bwd(const CriticDims& c, int B, const float* params2, const _
     SPK_TRY(aux_pool(&aux));
     cudaStream_t sb = aux->side[6];
     SPK_TRY(stream_after(sb, st, aux->ev[16]));
-    critic_bias_grads_kernel<<<dim3(cdiv(3 * HW + 1, 8), nz), 256, 0, sb>>>(
+    pdl(critic_bias_grads_kernel, dim3(cdiv(3 * HW + 1, 8), nz), 256, 0, sb)(
         B, Bp, L.P, (long long)c.off[SPIKERL_CRITIC_B1], (long long)c.off[SPIKERL_CRITIC_B2], oW3,
         (long long)c.off[SPIKERL_CRITIC_B3], w.dZ1T, w.dZ2T, w.dq, w.Hh2, grad2);
     SPK_LAUNCHED();
     {
       ProfScope ps_("critic_wgrad_mma", PB_TENSOR, 2.0 * B * nz * ((double)HW * HW + (double)HW * c.in), 0.0, st);
       dim3 grid(cdiv(L.inq > HW ? L.inq : HW, 256), 2 * (HW / RB), nz);
-      critic_wgrad_mma_kernel<<<grid, 256, 0, st>>>(Bp, c.in, L.inq, L.P, (long long)c.off[SPIKERL_CRITIC_W1],
+      pdl(critic_wgrad_mma_kernel, grid, 256, 0, st)(Bp, c.in, L.inq, L.P, (long long)c.off[SPIKERL_CRITIC_W1],
                                                     (long long)c.off[SPIKERL_CRITIC_W2], w.XT, w.H1T, w.dZ2T, w.dZ1T,
                                                     grad2);
       SPK_LAUNCHED();

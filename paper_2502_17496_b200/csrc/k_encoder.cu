@@ -21,6 +21,8 @@ __global__ void __launch_bounds__(256) enc_fwd_kernel(int B, int S, int E, int K
                                                       const float* __restrict__ sigma,
                                                       float* __restrict__ A_out,
                                                       uint32_t* __restrict__ bits0) {
+  pdl_wait();
+  pdl_trigger();
   const int k = blockIdx.y * blockDim.x + threadIdx.x;
   const int lane = threadIdx.x & 31;
   if ((k >> 5) >= W0) return;   // whole warp past the padded width
@@ -78,7 +80,7 @@ __global__ void __launch_bounds__(256) enc_fwd_kernel(int B, int S, int E, int K
 template <int TT>
 static void enc_launch(dim3 grid, cudaStream_t st, const ActorDims& d, int B, const float* obs, const float* mu,
                        const float* sigma, float* A, uint32_t* bits0) {
-  enc_fwd_kernel<TT><<<grid, 256, 0, st>>>(B, d.S, d.E, d.K0, d.Wd[0], d.T, obs, mu, sigma, A, bits0);
+  pdl((enc_fwd_kernel<TT>), grid, 256, 0, st)(B, d.S, d.E, d.K0, d.Wd[0], d.T, obs, mu, sigma, A, bits0);
 }
 
 int launch_enc_fwd(const ActorDims& d, int B, const float* obs, const float* mu, const float* sigma,

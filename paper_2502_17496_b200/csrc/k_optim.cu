@@ -20,6 +20,8 @@ static int ew_grid(size_t n, int per_thread) {
 // element so the padding is (re)written with zeros every refresh.
 __global__ void actor_refresh_kernel(const float* __restrict__ W, int N, int K, int P, int Pk,
                                      __nv_bfloat16* __restrict__ out) {
+  pdl_wait();
+  pdl_trigger();
   const size_t total = (size_t)P * Pk;
   for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < total;
        i += (size_t)gridDim.x * blockDim.x) {
@@ -34,7 +36,7 @@ int launch_actor_refresh_bf16(const ActorDims& d, const float* params, __nv_bflo
   ProfScope ps_("refresh_bf16", PB_HBM, 0.0, 6.0 * d.boff[3], st);
   for (int l = 1; l <= 3; ++l) {
     const size_t total = (size_t)d.P[l] * d.P[l - 1];
-    actor_refresh_kernel<<<ew_grid(total, 4), 256, 0, st>>>(
+    pdl(actor_refresh_kernel, ew_grid(total, 4), 256, 0, st)(
         params + d.off[SPIKERL_ACTOR_W1 + l - 1], d.N[l], d.N[l - 1], d.P[l], d.P[l - 1],
         out + d.boff[l - 1]);
     SPK_LAUNCHED();
@@ -44,6 +46,8 @@ int launch_actor_refresh_bf16(const ActorDims& d, const float* params, __nv_bflo
 
 __global__ void f32_to_bf16_kernel(const float* __restrict__ in, __nv_bfloat16* __restrict__ out,
                                    size_t n) {
+  pdl_wait();
+  pdl_trigger();
   for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n;
        i += (size_t)gridDim.x * blockDim.x)
     out[i] = __float2bfloat16_rn(in[i]);
@@ -51,7 +55,7 @@ __global__ void f32_to_bf16_kernel(const float* __restrict__ in, __nv_bfloat16* 
 
 int launch_f32_to_bf16(const float* in, __nv_bfloat16* out, size_t n, cudaStream_t st) {
   ProfScope ps_("f32_to_bf16", PB_HBM, 0.0, 6.0 * n, st);
-  f32_to_bf16_kernel<<<ew_grid(n, 4), 256, 0, st>>>(in, out, n);
+  pdl(f32_to_bf16_kernel, ew_grid(n, 4), 256, 0, st)(in, out, n);
   SPK_LAUNCHED();
   return SPIKERL_OK;
 }
@@ -113,6 +117,8 @@ __global__ void __launch_bounds__(256) adam_kernel(float* __restrict__ p, const 
                                                    float b2, float eps, size_t clo, size_t chi,
                                                    float cmin, unsigned int* ticket,
                                                    const __grid_constant__ Bf16Views views) {
+  pdl_wait();
+  pdl_trigger();
   const long long t = *(volatile long long*)counter + 1;
   const double bc1 = 1.0 - pow((double)b1, (double)t);
   const double bc2 = 1.0 - pow((double)b2, (double)t);
@@ -172,7 +178,7 @@ int launch_adam(float* p, const float* g, float* m, float* v, size_t n, long lon
     set_error("adam: buffers must be 16-byte aligned");
     return SPIKERL_E_ARG;
   }
-  adam_kernel<<<ew_grid(n, 4), 256, 0, st>>>(p, g, m, v, n, counter, lr, b1, b2, eps, clo, chi,
+  pdl(adam_kernel, ew_grid(n, 4), 256, 0, st)(p, g, m, v, n, counter, lr, b1, b2, eps, clo, chi,
                                              cmin, ticket, views ? *views : none);
   SPK_LAUNCHED();
   return SPIKERL_OK;
@@ -181,6 +187,8 @@ int launch_adam(float* p, const float* g, float* m, float* v, size_t n, long lon
 // ------------------------------------------------------------------ Polyak
 __global__ void polyak_kernel(float* __restrict__ t, const float* __restrict__ s, size_t n,
                               float tau, const __grid_constant__ Bf16Views views) {
+  pdl_wait();
+  pdl_trigger();
   const float omt = 1.0f - tau;
   for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n;
        i += (size_t)gridDim.x * blockDim.x) {
@@ -193,7 +201,7 @@ __global__ void polyak_kernel(float* __restrict__ t, const float* __restrict__ s
 int launch_polyak(float* t, const float* s, size_t n, float tau, const Bf16Views* views, cudaStream_t st) {
   const Bf16Views none{};
   ProfScope ps_("polyak", PB_HBM, 0.0, 12.0 * n, st);
-  polyak_kernel<<<ew_grid(n, 1), 256, 0, st>>>(t, s, n, tau, views ? *views : none);
+  pdl(polyak_kernel, ew_grid(n, 1), 256, 0, st)(t, s, n, tau, views ? *views : none);
   SPK_LAUNCHED();
   return SPIKERL_OK;
 }

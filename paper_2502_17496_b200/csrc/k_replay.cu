@@ -52,6 +52,8 @@ __global__ void replay_gather_kernel(int B, int S, int A, const float* __restric
                                      float* __restrict__ s, float* __restrict__ a,
                                      float* __restrict__ r, float* __restrict__ s2,
                                      float* __restrict__ d) {
+  pdl_wait();
+  pdl_trigger();
   const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
   if (warp >= B) return;
   long long i = 0;
@@ -83,7 +85,7 @@ int launch_replay_gather(int B, int S, int A, const float* rs, const float* ra, 
                          unsigned long long seed, int rank, const unsigned long long* counter,
                          float* s, float* a, float* r, float* s2, float* d, cudaStream_t st) {
   ProfScope ps_("replay_gather", PB_LATENCY, 0.0, 8.0 * B * (2.0 * S + A + 2), st);
-  replay_gather_kernel<<<cdiv((long long)B * 32, 256), 256, 0, st>>>(B, S, A, rs, ra, rr, rs2, rd, N, idx,
+  pdl(replay_gather_kernel, cdiv((long long)B * 32, 256), 256, 0, st)(B, S, A, rs, ra, rr, rs2, rd, N, idx,
                                                                      seed, rank, counter, s, a, r, s2, d);
   SPK_LAUNCHED();
   return SPIKERL_OK;
@@ -96,6 +98,8 @@ __global__ void __launch_bounds__(1024) target_action_kernel(int B, int A, const
                                                              unsigned long long seed, int rank,
                                                              unsigned long long* counter,
                                                              float* __restrict__ at) {
+  pdl_wait();
+  pdl_trigger();
   const unsigned long long ctr = *counter;
   const int n = B * A;
   for (int i = threadIdx.x; i < n; i += blockDim.x) {
@@ -119,13 +123,15 @@ int launch_target_action(int B, int A, const float* a2, const float* noise, floa
                          unsigned long long seed, int rank, unsigned long long* counter, float* at,
                          cudaStream_t st) {
   ProfScope ps_("target_action", PB_LATENCY, 0.0, 12.0 * B * A, st);
-  target_action_kernel<<<1, 1024, 0, st>>>(B, A, a2, noise, sigma, clip, seed, rank, counter, at);
+  pdl(target_action_kernel, 1, 1024, 0, st)(B, A, a2, noise, sigma, clip, seed, rank, counter, at);
   SPK_LAUNCHED();
   return SPIKERL_OK;
 }
 
 __global__ void td_target_kernel(int B, const float* __restrict__ r, const float* __restrict__ d,
                                  const float* __restrict__ q2, float gamma, float* __restrict__ y) {
+  pdl_wait();
+  pdl_trigger();
   const int b = blockIdx.x * blockDim.x + threadIdx.x;
   if (b >= B) return;
   const float qmin = fminf(q2[b], q2[B + b]);
@@ -135,18 +141,20 @@ __global__ void td_target_kernel(int B, const float* __restrict__ r, const float
 int launch_td_target(int B, const float* r, const float* d, const float* q2, float gamma, float* y,
                      cudaStream_t st) {
   ProfScope ps_("td_target", PB_LATENCY, 0.0, 20.0 * B, st);
-  td_target_kernel<<<cdiv(B, 256), 256, 0, st>>>(B, r, d, q2, gamma, y);
+  pdl(td_target_kernel, cdiv(B, 256), 256, 0, st)(B, r, d, q2, gamma, y);
   SPK_LAUNCHED();
   return SPIKERL_OK;
 }
 
 __global__ void scale_kernel(float* x, size_t n, float s) {
+  pdl_wait();
+  pdl_trigger();
   for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x)
     x[i] = __fmul_rn(x[i], s);
 }
 
 int launch_scale(float* x, size_t n, float s, cudaStream_t st) {
-  scale_kernel<<<cdiv((long long)n, 256) < 1184 ? cdiv((long long)n, 256) : 1184, 256, 0, st>>>(x, n, s);
+  pdl(scale_kernel, cdiv((long long)n, 256) < 1184 ? cdiv((long long)n, 256) : 1184, 256, 0, st)(x, n, s);
   SPK_LAUNCHED();
   return SPIKERL_OK;
 }
@@ -154,6 +162,8 @@ int launch_scale(float* x, size_t n, float s, cudaStream_t st) {
 // synthetic shard fill (configs[1] distributions)
 __global__ void replay_fill_kernel(float* s, float* a, float* r, float* s2, float* d, long long n,
                                    int S, int A, float p_done, unsigned long long seed, int rank) {
+  pdl_wait();
+  pdl_trigger();
   const long long stride = (long long)gridDim.x * blockDim.x;
   const uint2 key = philox_key(seed, rank);
   const long long per = 2LL * S + A + 2;
@@ -179,7 +189,7 @@ extern "C" int spikerl_replay_fill(float* s, float* a, float* r, float* s2, floa
     spk::set_error("spikerl_replay_fill: bad arguments");
     return SPIKERL_E_ARG;
   }
-  spk::replay_fill_kernel<<<148 * 8, 256, 0, (cudaStream_t)stream>>>(s, a, r, s2, d, n, obs_dim, act_dim,
+  spk::pdl(spk::replay_fill_kernel, 148 * 8, 256, 0, (cudaStream_t)stream)(s, a, r, s2, d, n, obs_dim, act_dim,
                                                                       p_done, seed, rank);
   SPK_LAUNCHED();
   return SPIKERL_OK;

@@ -55,7 +55,19 @@ struct Params {
   const float* A; const float* obs; const float* mu; const float* sigma; float* partial; int K0, S, E;
   // DW
   const uint32_t* bits_dw; int w_dw; float* dw_part; long long split_stride; int ldp; int R;
+  int trace;   // diagnostics: CTA 0 stamps %globaltimer at phase boundaries into g_trace
 };
+
+// Phase timeline of one launch (SPIKERL_TC_TRACE=<n>: the n-th tc launch of the process), read by
+// tools/tc_trace.py through spikerl_debug_tc_trace (not part of the public header).
+__device__ unsigned long long g_trace[16];
+__device__ __forceinline__ void trace_stamp(const Params& p, int i) {
+  if (p.trace && blockIdx.x == 0) {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    g_trace[i] = t;
+  }
+}
 
 // ------------------------------------------------------------------------- PTX helpers
 __device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
@@ -273,6 +285,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int rank = CG == 2 ? (int)cluster_ctarank() : 0;
   const int cid = blockIdx.x / CG, ncl = gridDim.x / CG;   // pair (or CTA) index and count
+  if (threadIdx.x == 0) trace_stamp(p, 0);
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < STAGES; ++s) {
@@ -294,6 +307,10 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
   if (CG == 2) cluster_sync_all();   // the peer's barriers exist before any remote arrive
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
+  // the prologue above overlaps the previous kernel (PDL); global memory only after this point
+  pdl_wait();
+  pdl_trigger();
+  if (threadIdx.x == 0) trace_stamp(p, 1);
 
   if (warp == 0) {
     // ===================== TMA producer (both CTAs load their own halves) =====================
@@ -318,6 +335,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
             }
             if (MODE == DX) tma_3d(&tmB, sB, &full[stage], kb * BK, t.n * p.Bt, 0);
             if (MODE == ENC) tma_2d(&tmB, sB, &full[stage], kb * BK, t.n * p.BN);
+            if (it == 0) trace_stamp(p, 2);
           } else {
             if (rank == 0) mbar_expect_tx(&full[stage], 2u * ((uint32_t)A_STAGE + bytes_b));
             if (!A_MN) {
@@ -348,6 +366,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
           const uint32_t ph = (it / STAGES) & 1;
           mbar_wait(&full[stage], ph);
           tc_fence_after();
+          if (it == 0) trace_stamp(p, 3);
           const uint32_t sA = smem_u32(smem + stage * STAGE_BYTES);
           const uint32_t sB = sA + A_STAGE;
 #pragma unroll
@@ -362,6 +381,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         }
         if (CG == 2) mma_commit_pair(&tfull[a]);
         else mma_commit(&tfull[a]);
+        if (titer == 0) trace_stamp(p, 4);
       }
     }
   } else if (warp < EPI_WARP0) {
@@ -493,6 +513,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       const uint32_t a = titer & 1, aph = (titer >> 1) & 1;
       mbar_wait(&tfull[a], aph);
       tc_fence_after();
+      if (titer == 0 && warp == EPI_WARP0 && lane == 0) trace_stamp(p, 6);
       const uint32_t taddr = tmem + ((uint32_t)(32 * q) << 16) + a * 256;
       const int row = t.m * BM + 32 * q + lane;  // neuron index (M)
       if (MODE == FWD) {
@@ -516,13 +537,26 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
           for (int oc = 0; oc < NOC; ++oc)
 #pragma unroll
             for (int i = 0; i < 4; ++i) { qo[oc][i] = 0u; qh[oc][i] = 0u; }
-          for (int tt = 0; tt < p.T; ++tt) {
+          // TMEM loads of CH timesteps are issued together and waited once (trace r01: one
+          // load + wait per step left the epilogue latency-bound at small batch)
+          constexpr int CH = HB >= 16 ? 1 : 32 / HB;   // BT = 32: registers are the limit
+          for (int t0 = 0; t0 < p.T; t0 += CH) {
+          uint32_t rr[CH][HB / 8][8];
+#pragma unroll
+          for (int ci = 0; ci < CH; ++ci)
+            if (t0 + ci < p.T) {
+#pragma unroll
+              for (int j0 = 0; j0 < HB; j0 += 8) tmem_ld8(taddr + (t0 + ci) * BT + jb + j0, rr[ci][j0 / 8]);
+            }
+          tmem_ld_wait();
+#pragma unroll
+          for (int ci = 0; ci < CH; ++ci) {
+            const int tt = t0 + ci;
+            if (tt >= p.T) break;
             uint32_t hcur = 0;
 #pragma unroll
             for (int j0 = 0; j0 < HB; j0 += 8) {
-              uint32_t r[8];
-              tmem_ld8(taddr + tt * BT + jb + j0, r);
-              tmem_ld_wait();
+              const uint32_t (&r)[8] = rr[ci][j0 / 8];
               uint32_t wo = 0, wh = 0;
 #pragma unroll
               for (int jj = 0; jj < 8; ++jj) {
@@ -563,6 +597,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
               }
             }
           }
+          }
           if (p.counts && row < p.n3) {
 #pragma unroll
             for (int j = 0; j < HB; ++j) {
@@ -595,24 +630,28 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
           const bool full = b0 + HB <= p.B;
           const size_t bstr = (size_t)p.p_prev, tstr = (size_t)p.B * p.p_prev;
           __nv_bfloat16* const gbase = p.g_prev + (size_t)b0 * bstr + row;
-          for (int tt = p.T - 1; tt >= 0; --tt) {
-            if ((tt >> 4) != ch) {
-              ch = tt >> 4;
-              qo = nqo; qh = nqh;
-              if (ch > 0) { nqo = __ldg(bT + ch - 1); nqh = __ldg(mT + ch - 1); }
-            }
-            const uint32_t ow0 = byte_of(qo, tt & 15), hw0 = byte_of(qh, tt & 15);
-            __nv_bfloat16* gt = gbase + (size_t)tt * tstr;
+          // TMEM loads of 4 timesteps issued together, one wait (see the FWD epilogue)
+          for (int t1 = p.T - 1; t1 >= 0; t1 -= 4) {
+            uint32_t rr[4][8];
 #pragma unroll
-            for (int j0 = 0; j0 < HB; j0 += 8) {
-              uint32_t r[8];
-              tmem_ld8(taddr + tt * BT + jb + j0, r);
-              tmem_ld_wait();
+            for (int ci = 0; ci < 4; ++ci)
+              if (t1 - ci >= 0) tmem_ld8(taddr + (t1 - ci) * BT + jb, rr[ci]);
+            tmem_ld_wait();
 #pragma unroll
-              for (int jj = 0; jj < 8; ++jj) {
-                const int j = j0 + jj;
+            for (int ci = 0; ci < 4; ++ci) {
+              const int tt = t1 - ci;
+              if (tt < 0) break;
+              if ((tt >> 4) != ch) {
+                ch = tt >> 4;
+                qo = nqo; qh = nqh;
+                if (ch > 0) { nqo = __ldg(bT + ch - 1); nqh = __ldg(mT + ch - 1); }
+              }
+              const uint32_t ow0 = byte_of(qo, tt & 15), hw0 = byte_of(qh, tt & 15);
+              __nv_bfloat16* gt = gbase + (size_t)tt * tstr;
+#pragma unroll
+              for (int j = 0; j < HB; ++j) {
                 const bool o = (ow0 >> j) & 1u, h = (hw0 >> j) & 1u;
-                float G = lif_back_step(p.zh, p.kc.dv, p.kc.dc, __uint_as_float(r[jj]), o, h, dvn[j], dcn[j]);
+                float G = lif_back_step(p.zh, p.kc.dv, p.kc.dc, __uint_as_float(rr[ci][j]), o, h, dvn[j], dcn[j]);
                 if (!valid) G = 0.f;
                 gs[j] = __fadd_rn(gs[j], G);
                 if (full || b0 + j < p.B) *gt = __float2bfloat16_rn(G);
@@ -670,13 +709,18 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         const int c0 = g * (DW_BN / 2);
         float* dst = p.dw_part + (size_t)t.split * p.split_stride + (size_t)row * p.ldp + t.n * DW_BN + c0;
         if (t.n * DW_BN + c0 < p.ldp) {
-          for (int j0 = 0; j0 < DW_BN / 2; j0 += 8) {
-            uint32_t r[8];
-            tmem_ld8(taddr + c0 + j0, r);
+          for (int j1 = 0; j1 < DW_BN / 2; j1 += 32) {   // 4 loads in flight per wait
+            uint32_t rr[4][8];
+#pragma unroll
+            for (int ci = 0; ci < 4; ++ci) tmem_ld8(taddr + c0 + j1 + 8 * ci, rr[ci]);
             tmem_ld_wait();
-            float4* d4 = reinterpret_cast<float4*>(dst + j0);
-            d4[0] = make_float4(__uint_as_float(r[0]), __uint_as_float(r[1]), __uint_as_float(r[2]), __uint_as_float(r[3]));
-            d4[1] = make_float4(__uint_as_float(r[4]), __uint_as_float(r[5]), __uint_as_float(r[6]), __uint_as_float(r[7]));
+#pragma unroll
+            for (int ci = 0; ci < 4; ++ci) {
+              const uint32_t (&r)[8] = rr[ci];
+              float4* d4 = reinterpret_cast<float4*>(dst + j1 + 8 * ci);
+              d4[0] = make_float4(__uint_as_float(r[0]), __uint_as_float(r[1]), __uint_as_float(r[2]), __uint_as_float(r[3]));
+              d4[1] = make_float4(__uint_as_float(r[4]), __uint_as_float(r[5]), __uint_as_float(r[6]), __uint_as_float(r[7]));
+            }
           }
         }
       }
@@ -686,21 +730,26 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         if (CG == 2) mbar_arrive_leader(&tempty[a]);
         else mbar_arrive(&tempty[a]);
       }
+      if (titer == 0 && warp == EPI_WARP0 && lane == 0) trace_stamp(p, 7);
     }
   }
   tc_fence_before();
+  if (threadIdx.x == 0) trace_stamp(p, 8);
   __syncthreads();
   if (CG == 2) cluster_sync_all();   // no CTA of the pair releases smem / TMEM the other still uses
   if (warp == 1) {
     tc_fence_after();
     if (CG == 2) tmem_dealloc_cg2(tmem, TMEM_COLS);
     else tmem_dealloc(tmem, TMEM_COLS);
+    if (lane == 0) trace_stamp(p, 9);
   }
 }
 
 // dW[n][k] (master layout) = sum over splits (fixed order) of the partial tiles
 __global__ void dw_reduce_kernel(const float* __restrict__ part, int splits, long long split_stride, int ldp,
                                  int N, int K, float* __restrict__ dW, int accum) {
+  pdl_wait();
+  pdl_trigger();
   const long long total = (long long)N * K;
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < total; i += (long long)gridDim.x * blockDim.x) {
     const int n = (int)(i / K), k = (int)(i % K);
@@ -794,19 +843,21 @@ static int launch_cg(const CUtensorMap& ma, const CUtensorMap& mb, const Params&
   if (CG == 1) {
     const int ncta = num_sms();
     const int grid = p.n_units < ncta ? (int)p.n_units : ncta;
-    tc_kernel<MODE, BT, CG><<<grid, NUM_THREADS, SMEM_BYTES, st>>>(ma, mb, p);
+    pdl((tc_kernel<MODE, BT, CG>), grid, NUM_THREADS, SMEM_BYTES, st)(ma, mb, p);
   } else {
     cudaLaunchConfig_t cfg = {};
     cfg.blockDim = dim3(NUM_THREADS, 1, 1);
     cfg.dynamicSmemBytes = SMEM_BYTES;
     cfg.stream = st;
-    cudaLaunchAttribute at[1];
+    cudaLaunchAttribute at[2];
     at[0].id = cudaLaunchAttributeClusterDimension;
     at[0].val.clusterDim.x = CG;
     at[0].val.clusterDim.y = 1;
     at[0].val.clusterDim.z = 1;
+    at[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[1].val.programmaticStreamSerializationAllowed = pdl_enabled() ? 1 : 0;
     cfg.attrs = at;
-    cfg.numAttrs = 1;
+    cfg.numAttrs = 2;
     // A persistent grid larger than the number of co-resident pairs would run a second wave of
     // whole pairs; size it to what the GPCs can actually hold (not simply 148 / 2).
     const int slots = pair_slots();
@@ -819,8 +870,17 @@ static int launch_cg(const CUtensorMap& ma, const CUtensorMap& mb, const Params&
   return SPIKERL_OK;
 }
 
+static int g_launch_no = 0;
+static int trace_launch() {   // 1-based index of the launch to trace (0 = off)
+  static int v = -1;
+  if (v < 0) { const char* e = getenv("SPIKERL_TC_TRACE"); v = e ? atoi(e) : 0; }
+  return v;
+}
+
 template <int MODE, int BT>
-static int launch(const CUtensorMap& ma, const CUtensorMap& mb, const Params& p, cudaStream_t st) {
+static int launch(const CUtensorMap& ma, const CUtensorMap& mb, const Params& p0, cudaStream_t st) {
+  Params p = p0;
+  p.trace = (trace_launch() > 0 && ++g_launch_no == trace_launch()) ? 1 : 0;
   return p.cg == 2 ? launch_cg<MODE, BT, 2>(ma, mb, p, st) : launch_cg<MODE, BT, 1>(ma, mb, p, st);
 }
 
@@ -930,9 +990,23 @@ int launch_lif_dx_tc(const ActorDims& d, int l, int B, const void* Gl, const __n
   return launch_bt<DX>(p.Bt, ma, mb, p, st);
 }
 
+static int enc_cg(const ActorDims& d) { return (pairs_enabled() && (d.P[0] / BM) % 2 == 0) ? 2 : 1; }
+
+// batch columns per ENC unit: 256 when that still gives every SM (pair) a unit; smaller batches
+// use narrower units (>= 16) so the per-unit epilogue loop over the batch stays short (cfg1:
+// one 256-wide unit = 2 CTAs and an 8 us epilogue; 16-wide units = 16 pairs)
+static int enc_bn(const ActorDims& d, int B) {
+  const int cg = enc_cg(d);
+  const int m_tiles = d.P[0] / BM / cg;
+  const int slots = cg == 2 ? pair_slots() : num_sms();
+  int bn = 256;
+  while (bn > 16 && (long long)m_tiles * cdiv(B, bn) < slots) bn /= 2;
+  if (B < bn) bn = round_up(B, 16);
+  return bn;
+}
+
 size_t tc_enc_partial_bytes(const ActorDims& d, int B) {
-  const int BN = B >= 256 ? 256 : round_up(B, 16);
-  return sizeof(float) * 2 * 2 * (size_t)cdiv(B, BN) * d.K0;   // 2 epilogue groups per N tile
+  return sizeof(float) * 2 * 2 * (size_t)cdiv(B, enc_bn(d, B)) * d.K0;   // 2 epilogue groups per N tile
 }
 
 int launch_enc_grad_tc(const ActorDims& d, int B, const void* Gsum, const __nv_bfloat16* W1b16, const float* A,
@@ -941,8 +1015,8 @@ int launch_enc_grad_tc(const ActorDims& d, int B, const void* Gsum, const __nv_b
   ProfScope ps_("enc_grad_tc", PB_TENSOR, 2.0 * B * (double)d.N1 * d.K0, 0.0, st);
   Params p{};
   p.T = 1; p.B = B;
-  p.BN = B >= 256 ? 256 : round_up(B, 16);
-  p.cg = (pairs_enabled() && (d.P[0] / BM) % 2 == 0) ? 2 : 1;
+  p.BN = enc_bn(d, B);
+  p.cg = enc_cg(d);
   p.m_tiles = d.P[0] / BM / p.cg;
   p.n_tiles = cdiv(B, p.BN);
   p.k_blocks = d.P[1] / BK;
@@ -1025,9 +1099,14 @@ int launch_lif_dw_tc(const ActorDims& d, int l, int B, const void* Gl, const uin
   SPK_TRY(launch_bt<DW>(8, ma, mb, p, st));
   const long long total = (long long)d.N[l] * d.N[l - 1];
   const int grid = (int)((total + 255) / 256 < 148 * 8 ? (total + 255) / 256 : 148 * 8);
-  dw_reduce_kernel<<<grid, 256, 0, st>>>(part, splits, p.split_stride, p.ldp, d.N[l], d.N[l - 1], dW, accumulate);
+  pdl(dw_reduce_kernel, grid, 256, 0, st)(part, splits, p.split_stride, p.ldp, d.N[l], d.N[l - 1], dW, accumulate);
   SPK_LAUNCHED();
   return SPIKERL_OK;
 }
 
 }  // namespace spk
+
+extern "C" int spikerl_debug_tc_trace(unsigned long long* host16) {
+  if (cudaMemcpyFromSymbol(host16, spk::tc::g_trace, sizeof(unsigned long long) * 16) != cudaSuccess) return 5;
+  return 0;
+}

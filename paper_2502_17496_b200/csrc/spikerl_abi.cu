@@ -25,6 +25,18 @@ void set_error(const char* fmt, ...) {
 }
 void note_launch(int n) { g_launches += n; }
 
+static thread_local cudaError_t g_launch_err = cudaSuccess;
+void note_launch_error(cudaError_t e) { g_launch_err = e; }
+cudaError_t take_launch_error() {
+  const cudaError_t e = g_launch_err;
+  g_launch_err = cudaSuccess;
+  return e;
+}
+bool pdl_enabled() {
+  static const bool on = [] { const char* e = getenv("SPIKERL_PDL"); return !(e && e[0] == '0'); }();
+  return on;
+}
+
 static int resolve_engine(const spikerl_actor_cfg* c, ActorDims* d) {
   const bool bf = c->precision == SPIKERL_BF16;
   switch (c->engine) {
@@ -291,6 +303,8 @@ static Td3Ws td3_ws_layout(const ActorDims& ad, const CriticDims& cd, int B) {
 }
 
 __global__ void neg_mean_kernel(int B, const float* __restrict__ q, float* __restrict__ out) {
+  pdl_wait();
+  pdl_trigger();
   __shared__ float red[256];
   float s = 0.f;
   for (int b = threadIdx.x; b < B; b += 256) s = __fadd_rn(s, q[b]);
@@ -601,7 +615,7 @@ int spikerl_td3_update(const spikerl_actor_cfg* acfg, const spikerl_critic_cfg* 
     SPK_TRY(critic_fwd_bwd(cd, B, b->critic, cbf, s, ad.S, api, ad.A, nullptr, q, mma ? losses + 1 : nullptr, nullptr,
                            ga, -1.0f / (float)B, 1, cws, st));
     if (!mma) {
-      neg_mean_kernel<<<1, 256, 0, st>>>(B, q, losses + 1);
+      pdl(neg_mean_kernel, 1, 256, 0, st)(B, q, losses + 1);
       SPK_LAUNCHED();
     }
     SPK_TRY(actor_backward_impl(ad, B, b->actor, abf, s, tape, ga, b->grad_actor, 0, aws, st));
