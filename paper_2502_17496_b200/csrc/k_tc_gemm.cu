@@ -36,7 +36,13 @@ constexpr int EXP_WARP0 = 2, EPI_WARP0 = 2 + NUM_EXP_WARPS;
 constexpr int NUM_THREADS = (EPI_WARP0 + NUM_EPI_WARPS) * 32;  // 448
 constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + 1024 + 256;
 constexpr int TMEM_COLS = 512;
-constexpr int DW_BN = 256;
+constexpr int DW_BN = 256;   // N of one DW MMA
+// A DW unit of a CTA pair covers 2 x 256 output columns (two accumulators, sharing every A tile):
+// each G_l tile fetched from L2/HBM feeds twice the MMA work, which halves the G_l re-reads over
+// the K_{l-1} tiles (ncu r01: dW1 at cfg4 read 6.1 GB from DRAM for a 2.15 GB G_1, and with the
+// MMAs disabled its TMA loads alone took 7.3 ms). The epilogue only dumps partial tiles, so the
+// accumulator is not double-buffered for these units.
+__host__ __device__ constexpr int dw_unit_cols(int cg) { return DW_BN * cg; }
 
 struct Params {
   int T, B, Bt, BN;
@@ -56,6 +62,10 @@ struct Params {
   // DW
   const uint32_t* bits_dw; int w_dw; float* dw_part; long long split_stride; int ldp; int R;
   int trace;   // diagnostics: CTA 0 stamps %globaltimer at phase boundaries into g_trace
+  int dbg;     // diagnostics only (SPIKERL_TC_DBG, wrong results): 1 = expanders skip their smem
+               // stores, 2 = epilogue skips its work, 4 = MMA issuer skips the MMAs, 8 = DW
+               // expanders skip their global loads, 16 = TMA producer skips its loads (and the
+               // expect_tx, so the stage completes on the expanders' arrivals alone)
 };
 
 // Phase timeline of one launch (SPIKERL_TC_TRACE=<n>: the n-th tc launch of the process), read by
@@ -153,13 +163,24 @@ __device__ __forceinline__ void tmem_ld8(uint32_t taddr, uint32_t (&r)[8]) {
 }
 __device__ __forceinline__ void tmem_ld_wait() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
 
-// 8 spike bits -> 8 bf16 values {0, 1.0} (16 bytes)
+// 8 spike bits -> 8 bf16 values {0, 1.0} (16 bytes). A multiply moves bit i of each nibble to
+// the sign bit of byte i (the partial products never overlap, so no carries); prmt with the
+// sign-replicate selector bit turns byte pairs into 0x0000 / 0xFFFF halves, masked to 0x3F80 =
+// bf16 1.0: 12 instructions per 16 bytes instead of ~20 shift/select pairs (ncu r01: the DW
+// expanders were issue-latency bound).
+__device__ __forceinline__ uint32_t prmt_sx(uint32_t x, uint32_t sel) {
+  uint32_t r;
+  asm("prmt.b32 %0, %1, 0, %2;" : "=r"(r) : "r"(x), "r"(sel));
+  return r;
+}
 __device__ __forceinline__ uint4 expand_byte(uint32_t byte) {
+  const uint32_t zlo = (byte & 0x0Fu) * 0x10204080u;   // bit i     -> bit 8 i + 7
+  const uint32_t zhi = (byte & 0xF0u) * 0x01020408u;   // bit 4 + i -> bit 8 i + 7
   uint4 r;
-  r.x = ((byte & 1u) ? 0x3F80u : 0u) | ((byte & 2u) ? 0x3F800000u : 0u);
-  r.y = ((byte & 4u) ? 0x3F80u : 0u) | ((byte & 8u) ? 0x3F800000u : 0u);
-  r.z = ((byte & 16u) ? 0x3F80u : 0u) | ((byte & 32u) ? 0x3F800000u : 0u);
-  r.w = ((byte & 64u) ? 0x3F80u : 0u) | ((byte & 128u) ? 0x3F800000u : 0u);
+  r.x = prmt_sx(zlo, 0x9988u) & 0x3F803F80u;
+  r.y = prmt_sx(zlo, 0xBBAAu) & 0x3F803F80u;
+  r.z = prmt_sx(zhi, 0x9988u) & 0x3F803F80u;
+  r.w = prmt_sx(zhi, 0xBBAAu) & 0x3F803F80u;
   return r;
 }
 __device__ __forceinline__ void st_shared_v4(uint32_t addr, uint4 v) {
@@ -272,11 +293,19 @@ constexpr int PF = 4;
 template <int MODE, int BT, int CG>
 __global__ void __launch_bounds__(NUM_THREADS, 1)
     tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, const Params p) {
+  // A CTA of a pair holds at most 128 B rows (its half of the MMA's N), so its stages are 32 KB
+  // and the same shared memory holds 6 of them instead of 4 (ncu r01: the DW/FWD L1 MMA waited
+  // on TMA-filled stages with the ring 4 deep)
+  constexpr bool DW2 = (MODE == DW && CG == 2);   // two accumulators per unit, one buffer
+  constexpr int NST = CG == 2 && !DW2 ? 6 : STAGES;
+  constexpr int SB_ = A_STAGE + (DW2 ? B_STAGE : B_STAGE / CG);
+  constexpr int NBUF = DW2 ? 1 : 2;               // TMEM accumulator buffers
+  static_assert(NST * SB_ <= STAGES * STAGE_BYTES, "stage ring exceeds the shared-memory budget");
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
-  uint64_t* full = (uint64_t*)(smem + STAGES * STAGE_BYTES);
-  uint64_t* empty = full + STAGES;
-  uint64_t* tfull = empty + STAGES;
+  uint64_t* full = (uint64_t*)(smem + NST * SB_);
+  uint64_t* empty = full + NST;
+  uint64_t* tfull = empty + NST;
   uint64_t* tempty = tfull + 2;
   uint32_t* tmem_slot = (uint32_t*)(tempty + 2);
   constexpr bool B_EXPAND = (MODE == FWD || MODE == DW);
@@ -288,8 +317,8 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
   if (threadIdx.x == 0) trace_stamp(p, 0);
 
   if (threadIdx.x == 0) {
-    for (int s = 0; s < STAGES; ++s) {
-      mbar_init(&full[s], 1 + (B_EXPAND ? CG * NUM_EXP_WARPS : 0));
+    for (int s = 0; s < NST; ++s) {
+      mbar_init(&full[s], 1 + (B_EXPAND ? CG : 0));   // TMA + one expander warp per CTA
       mbar_init(&empty[s], 1);
     }
     for (int a = 0; a < 2; ++a) {
@@ -320,12 +349,14 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       for (int u = cid; u < p.n_units; u += ncl) {
         const Tile t = decode<MODE>(p, u, rank, CG);
         for (int kb = t.kb0; kb < t.kb1; ++kb, ++it) {
-          const int stage = it % STAGES;
-          const uint32_t ph = (it / STAGES) & 1;
+          const int stage = it % NST;
+          const uint32_t ph = (it / NST) & 1;
           mbar_wait(&empty[stage], ph ^ 1);
-          uint8_t* sA = smem + stage * STAGE_BYTES;
+          uint8_t* sA = smem + stage * SB_;
           uint8_t* sB = sA + A_STAGE;
-          if (CG == 1) {
+          if (p.dbg & 16) {
+            if (CG == 1 || rank == 0) mbar_arrive(&full[stage]);
+          } else if (CG == 1) {
             mbar_expect_tx(&full[stage], (uint32_t)A_STAGE + bytes_b);
             if (!A_MN) {
               tma_2d(&tmA, sA, &full[stage], kb * BK, t.m * BM);
@@ -357,24 +388,30 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       const uint32_t idesc = make_idesc(p.BN, A_MN ? 1 : 0, B_MN ? 1 : 0, BM * CG);
       for (int u = cid; u < p.n_units; u += ncl, ++titer) {
         const Tile t = decode<MODE>(p, u, rank, CG);
-        const uint32_t a = titer & 1, aph = (titer >> 1) & 1;
+        const uint32_t a = titer % NBUF, aph = (titer / NBUF) & 1;
         mbar_wait(&tempty[a], aph ^ 1);
         tc_fence_after();
         const uint32_t d_tmem = tmem + a * 256;
+        // DW2: the second accumulator's columns may lie wholly past the padded K_{l-1} width
+        const bool second = DW2 && t.n * dw_unit_cols(CG) + DW_BN < p.ldp;
         for (int kb = t.kb0; kb < t.kb1; ++kb, ++it) {
-          const int stage = it % STAGES;
-          const uint32_t ph = (it / STAGES) & 1;
+          const int stage = it % NST;
+          const uint32_t ph = (it / NST) & 1;
           mbar_wait(&full[stage], ph);
           tc_fence_after();
           if (it == 0) trace_stamp(p, 3);
-          const uint32_t sA = smem_u32(smem + stage * STAGE_BYTES);
+          const uint32_t sA = smem_u32(smem + stage * SB_);
           const uint32_t sB = sA + A_STAGE;
 #pragma unroll
           for (int kk = 0; kk < BK / 16; ++kk) {
             const uint64_t ad = A_MN ? make_desc(sA + kk * 2048, 8192, 1024) : make_desc(sA + kk * 32, 16, 1024);
             const uint64_t bd = B_MN ? make_desc(sB + kk * 2048, 8192, 1024) : make_desc(sB + kk * 32, 16, 1024);
+            if (p.dbg & 4) continue;
             if (CG == 2) mma_bf16_cg2(d_tmem, ad, bd, idesc, (kb > t.kb0 || kk > 0) ? 1u : 0u);
             else mma_bf16(d_tmem, ad, bd, idesc, (kb > t.kb0 || kk > 0) ? 1u : 0u);
+            if (DW2 && second)
+              mma_bf16_cg2(d_tmem + DW_BN, ad, make_desc(sB + 16384 + kk * 2048, 8192, 1024), idesc,
+                           (kb > t.kb0 || kk > 0) ? 1u : 0u);
           }
           if (CG == 2) mma_commit_pair(&empty[stage]);
           else mma_commit(&empty[stage]);
@@ -386,120 +423,140 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     }
   } else if (warp < EPI_WARP0) {
     // ===================== spike-bit expanders =====================
-    // Each thread owns fixed rows of the B tile for the whole unit and keeps the spike words of
-    // the next PF k-blocks in registers, so global-load latency overlaps the smem ring.
+    // Expander warp w fills every stage of ring iterations it = w, w + 4, w + 8, ... on its own:
+    // each stage is written, fenced (generic -> async proxy) and published by one warp, so the
+    // four warps keep four stages in flight and the fence latency of one overlaps the stores of
+    // the others (ncu r01: with all four warps splitting each stage, the stage-serial
+    // store -> fence -> arrive chain paced DW/FWD L1 at ~1600 clk per k-block, with the MMAs
+    // disabled). The spike words of the warp's next k-block are loaded one iteration ahead into
+    // the other half of a statically indexed double buffer.
     if (B_EXPAND) {
-      const int et = threadIdx.x - EXP_WARP0 * 32;
-      uint32_t it = 0;
+      const int ew = warp - EXP_WARP0;
+      uint32_t it = 0;   // ring iterations of all units so far (every warp counts all of them)
       for (int u = cid; u < p.n_units; u += ncl) {
         const Tile t = decode<MODE>(p, u, rank, CG);
+        const int nkb = t.kb1 - t.kb0;
         if (MODE == FWD) {
-          // K-major: row = t*Bt + j (spike row (t, b)), one k-block = 2 words = 8 chunks of 16 B;
-          // a CTA of a pair expands its half of the rows (the MMA's B columns) into local rows
+          // K-major: row = (t, j) spike row of the MMA's B columns this CTA holds; one k-block =
+          // 2 words per row = 8 chunks of 16 B. Lane l owns rows l + 32 i.
+          constexpr int RPL = CG == 2 ? 4 : 8;
           const int rows = p.T * p.Bt / CG;
-          const uint32_t* rp[2];
-          bool rv[2];
+          const uint32_t* rp[RPL];
 #pragma unroll
-          for (int i = 0; i < 2; ++i) {
-            const int row = et + 128 * i;
+          for (int i = 0; i < RPL; ++i) {
+            const int row = lane + 32 * i;
             const int rg = rank * rows + row;
             const int tt = rg / p.Bt, j = rg - tt * p.Bt;
             const int b = t.n * p.Bt + j;
-            rv[i] = row < rows && b < p.B;
-            rp[i] = rv[i] ? p.bits_in + ((size_t)tt * p.B + b) * p.w_in : p.bits_in;
+            rp[i] = (row < rows && b < p.B) ? p.bits_in + ((size_t)tt * p.B + b) * p.w_in : nullptr;
           }
-          uint2 q[PF][2];
+          uint2 q[2][RPL];
+          auto ld = [&](uint2 (&dst)[RPL], int kb) {
 #pragma unroll
-          for (int f = 0; f < PF; ++f)
-#pragma unroll
-            for (int i = 0; i < 2; ++i) {
-              const int kb = t.kb0 + f;
-              q[f][i] = (rv[i] && kb < t.kb1) ? __ldg(reinterpret_cast<const uint2*>(rp[i] + 2 * kb)) : make_uint2(0u, 0u);
-            }
-          for (int kb = t.kb0; kb < t.kb1; ++kb, ++it) {
-            const int stage = it % STAGES;
-            const uint32_t ph = (it / STAGES) & 1;
+            for (int i = 0; i < RPL; ++i)
+              dst[i] = (rp[i] && kb < t.kb1) ? __ldg(reinterpret_cast<const uint2*>(rp[i] + 2 * kb)) : make_uint2(0u, 0u);
+          };
+          auto body = [&](const uint2 (&cur)[RPL], uint32_t itx) {
+            const int stage = itx % NST;
+            const uint32_t ph = (itx / NST) & 1;
             mbar_wait(&empty[stage], ph ^ 1);
-            const uint32_t sB = smem_u32(smem + stage * STAGE_BYTES + A_STAGE);
+            const uint32_t sB = smem_u32(smem + stage * SB_ + A_STAGE);
 #pragma unroll
-            for (int i = 0; i < 2; ++i) {
-              const int row = et + 128 * i;
+            for (int i = 0; i < RPL; ++i) {
+              const int row = lane + 32 * i;
               if (row < rows) {
                 const uint32_t base = sB + row * 128;
                 const uint32_t sw = row & 7;
 #pragma unroll
                 for (int c = 0; c < 8; ++c) {
-                  const uint32_t w = c < 4 ? q[0][i].x : q[0][i].y;
-                  st_shared_v4(base + ((c ^ sw) << 4), expand_byte((w >> (8 * (c & 3))) & 0xFFu));
+                  const uint32_t w = c < 4 ? cur[i].x : cur[i].y;
+                  if (!(p.dbg & 1)) st_shared_v4(base + ((c ^ sw) << 4), expand_byte((w >> (8 * (c & 3))) & 0xFFu));
                 }
               }
             }
-#pragma unroll
-            for (int f = 0; f < PF - 1; ++f) { q[f][0] = q[f + 1][0]; q[f][1] = q[f + 1][1]; }
-#pragma unroll
-            for (int i = 0; i < 2; ++i) {
-              const int kn = kb + PF;
-              q[PF - 1][i] = (rv[i] && kn < t.kb1) ? __ldg(reinterpret_cast<const uint2*>(rp[i] + 2 * kn))
-                                                  : make_uint2(0u, 0u);
-            }
             fence_proxy_async();
             __syncwarp();
             if (lane == 0) {
               if (CG == 2) mbar_arrive_leader(&full[stage]);
               else mbar_arrive(&full[stage]);
-            }
-          }
-        } else {
-          // MN-major: K row r = one (t,b) row, 256 output columns = 8 words (4 atoms of 64); a CTA
-          // of a pair expands its 128 columns (2 atoms, 4 words). thread = (row, part)
-          constexpr int WPT = 4 / CG;                  // words per thread per k-block
-          const int r = et >> 1, part = et & 1;
-          const int wcol = t.n * (DW_BN / 32) + rank * 4 + WPT * part;
-          const bool cv = wcol < p.w_dw;
-          uint32_t q[PF][WPT];
-          auto ldw = [&](uint32_t (&dst)[WPT], int kb) {
-            const int rg = kb * BK + r;
-            const bool ok = cv && kb < t.kb1 && rg < p.R;
-            const uint32_t* src = p.bits_dw + (size_t)rg * p.w_dw + wcol;
-            if (WPT == 4) {
-              const uint4 v = ok ? __ldg(reinterpret_cast<const uint4*>(src)) : make_uint4(0u, 0u, 0u, 0u);
-              dst[0] = v.x; dst[1 % WPT] = v.y; dst[2 % WPT] = v.z; dst[3 % WPT] = v.w;
-            } else {
-              const uint2 v = ok ? __ldg(reinterpret_cast<const uint2*>(src)) : make_uint2(0u, 0u);
-              dst[0] = v.x; dst[1 % WPT] = v.y;
             }
           };
+          // this warp's k-blocks of the unit: local index j = ew, ew + 4, ... (global it + j)
+          const int j0 = (int)((ew - it % NUM_EXP_WARPS + NUM_EXP_WARPS) % NUM_EXP_WARPS);
+          if (j0 < nkb) ld(q[0], t.kb0 + j0);
+          for (int j = j0; j < nkb; j += 2 * NUM_EXP_WARPS) {
+            if (j + NUM_EXP_WARPS < nkb) ld(q[1], t.kb0 + j + NUM_EXP_WARPS);
+            body(q[0], it + j);
+            if (j + NUM_EXP_WARPS >= nkb) break;
+            if (j + 2 * NUM_EXP_WARPS < nkb) ld(q[0], t.kb0 + j + 2 * NUM_EXP_WARPS);
+            body(q[1], it + j + NUM_EXP_WARPS);
+          }
+        } else {
+          // MN-major: K row r = one (t,b) row; every CTA expands 256 columns = 8 words = 4 atoms of
+          // 64 per k-block: all 256 columns of its MMA (one CTA), or (pair) its 128-column half of
+          // each of the unit's two MMAs (atoms 0-1: MMA 0, atoms 2-3: MMA 1). Lane l owns K rows
+          // l and l + 32, both halves h (4 words each).
+          int wcol[2];
+          bool cv[2];
 #pragma unroll
-          for (int f = 0; f < PF; ++f) ldw(q[f], t.kb0 + f);
-          for (int kb = t.kb0; kb < t.kb1; ++kb, ++it) {
-            const int stage = it % STAGES;
-            const uint32_t ph = (it / STAGES) & 1;
+          for (int h = 0; h < 2; ++h) {
+            wcol[h] = CG == 2 ? t.n * (dw_unit_cols(CG) / 32) + 8 * h + rank * 4 : t.n * (DW_BN / 32) + 4 * h;
+            cv[h] = wcol[h] < p.w_dw;
+          }
+          uint4 q[2][2][2];   // [buffer][row half][h]
+          auto ld = [&](uint4 (&dst)[2][2], int kb) {
+#pragma unroll
+            for (int i = 0; i < 2; ++i) {
+              const int rg = kb * BK + lane + 32 * i;
+              const bool okr = kb < t.kb1 && rg < p.R && !(p.dbg & 8);
+#pragma unroll
+              for (int h = 0; h < 2; ++h)
+                dst[i][h] = (okr && cv[h]) ? __ldg(reinterpret_cast<const uint4*>(p.bits_dw + (size_t)rg * p.w_dw + wcol[h]))
+                                           : make_uint4(0u, 0u, 0u, 0u);
+            }
+          };
+          auto body = [&](const uint4 (&cur)[2][2], uint32_t itx) {
+            const int stage = itx % NST;
+            const uint32_t ph = (itx / NST) & 1;
             mbar_wait(&empty[stage], ph ^ 1);
-            const uint32_t sB = smem_u32(smem + stage * STAGE_BYTES + A_STAGE);
-            const uint32_t sw = r & 7;
+            const uint32_t sB = smem_u32(smem + stage * SB_ + A_STAGE);
 #pragma unroll
-            for (int wi = 0; wi < WPT; ++wi) {
-              const int atom = (WPT * part + wi) >> 1, hw = wi & 1;
-              const uint32_t base = sB + atom * 8192 + r * 128;
+            for (int i = 0; i < 2; ++i) {
+              const int r = lane + 32 * i;
+              const uint32_t sw = r & 7;
 #pragma unroll
-              for (int c = 0; c < 4; ++c) {
-                const int chunk = hw * 4 + c;
-                st_shared_v4(base + ((chunk ^ sw) << 4), expand_byte((q[0][wi] >> (8 * c)) & 0xFFu));
+              for (int h = 0; h < 2; ++h) {
+                const uint32_t wv[4] = {cur[i][h].x, cur[i][h].y, cur[i][h].z, cur[i][h].w};
+#pragma unroll
+                for (int wi = 0; wi < 4; ++wi) {
+                  const int atom = 2 * h + (wi >> 1), hw = wi & 1;
+                  const uint32_t base = sB + atom * 8192 + r * 128;
+#pragma unroll
+                  for (int c = 0; c < 4; ++c) {
+                    const int chunk = hw * 4 + c;
+                    if (!(p.dbg & 1)) st_shared_v4(base + ((chunk ^ sw) << 4), expand_byte((wv[wi] >> (8 * c)) & 0xFFu));
+                  }
+                }
               }
             }
-#pragma unroll
-            for (int f = 0; f < PF - 1; ++f)
-#pragma unroll
-              for (int wi = 0; wi < WPT; ++wi) q[f][wi] = q[f + 1][wi];
-            ldw(q[PF - 1], kb + PF);
             fence_proxy_async();
             __syncwarp();
             if (lane == 0) {
               if (CG == 2) mbar_arrive_leader(&full[stage]);
               else mbar_arrive(&full[stage]);
             }
+          };
+          const int j0 = (int)((ew - it % NUM_EXP_WARPS + NUM_EXP_WARPS) % NUM_EXP_WARPS);
+          if (j0 < nkb) ld(q[0], t.kb0 + j0);
+          for (int j = j0; j < nkb; j += 2 * NUM_EXP_WARPS) {
+            if (j + NUM_EXP_WARPS < nkb) ld(q[1], t.kb0 + j + NUM_EXP_WARPS);
+            body(q[0], it + j);
+            if (j + NUM_EXP_WARPS >= nkb) break;
+            if (j + 2 * NUM_EXP_WARPS < nkb) ld(q[0], t.kb0 + j + 2 * NUM_EXP_WARPS);
+            body(q[1], it + j + NUM_EXP_WARPS);
           }
         }
+        it += nkb;
       }
     }
   } else {
@@ -510,13 +567,14 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     uint32_t titer = 0;
     for (int u = cid; u < p.n_units; u += ncl, ++titer) {
       const Tile t = decode<MODE>(p, u, rank, CG);
-      const uint32_t a = titer & 1, aph = (titer >> 1) & 1;
+      const uint32_t a = titer % NBUF, aph = (titer / NBUF) & 1;
       mbar_wait(&tfull[a], aph);
       tc_fence_after();
       if (titer == 0 && warp == EPI_WARP0 && lane == 0) trace_stamp(p, 6);
       const uint32_t taddr = tmem + ((uint32_t)(32 * q) << 16) + a * 256;
       const int row = t.m * BM + 32 * q + lane;  // neuron index (M)
-      if (MODE == FWD) {
+      if (p.dbg & 2) {
+      } else if (MODE == FWD) {
         constexpr int HB = BT >= 16 ? BT / 2 : BT;  // batch rows per group
         if (BT >= 16 || g == 0) {
           const int jb = BT >= 16 ? g * HB : 0;
@@ -705,11 +763,13 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
           p.partial[(((size_t)t.n * 2 + g) * p.K0 + row) * 2 + 0] = __fdiv_rn(pm, sg2);
           p.partial[(((size_t)t.n * 2 + g) * p.K0 + row) * 2 + 1] = __fdiv_rn(ps, sg3);
         }
-      } else {  // DW: group g writes columns [128 g, 128 g + 128)
-        const int c0 = g * (DW_BN / 2);
-        float* dst = p.dw_part + (size_t)t.split * p.split_stride + (size_t)row * p.ldp + t.n * DW_BN + c0;
-        if (t.n * DW_BN + c0 < p.ldp) {
-          for (int j1 = 0; j1 < DW_BN / 2; j1 += 32) {   // 4 loads in flight per wait
+      } else {  // DW: group g writes columns [GC g, GC g + GC) of the unit (GC = 128, or 256 for DW2)
+        constexpr int GC = DW2 ? DW_BN : DW_BN / 2;
+        const int c0 = g * GC;
+        const int col0 = t.n * dw_unit_cols(CG) + c0;
+        float* dst = p.dw_part + (size_t)t.split * p.split_stride + (size_t)row * p.ldp + col0;
+        for (int j1 = 0; j1 < GC; j1 += 32) {   // 4 loads in flight per wait
+          if (col0 + j1 < p.ldp) {               // ldp is a multiple of 128
             uint32_t rr[4][8];
 #pragma unroll
             for (int ci = 0; ci < 4; ++ci) tmem_ld8(taddr + c0 + j1 + 8 * ci, rr[ci]);
@@ -881,6 +941,8 @@ template <int MODE, int BT>
 static int launch(const CUtensorMap& ma, const CUtensorMap& mb, const Params& p0, cudaStream_t st) {
   Params p = p0;
   p.trace = (trace_launch() > 0 && ++g_launch_no == trace_launch()) ? 1 : 0;
+  static const int dbg = [] { const char* e = getenv("SPIKERL_TC_DBG"); return e ? atoi(e) : 0; }();
+  p.dbg = dbg;
   return p.cg == 2 ? launch_cg<MODE, BT, 2>(ma, mb, p, st) : launch_cg<MODE, BT, 1>(ma, mb, p, st);
 }
 
@@ -1045,7 +1107,7 @@ static int dw_cg(const ActorDims& d, int l) { return (pairs_enabled() && (d.P[l]
 
 void tc_dw_plan(const ActorDims& d, int l, int B, int* splits, int* kps) {
   const int cg = dw_cg(d, l);
-  const int m_tiles = d.P[l] / BM / cg, n_tiles = cdiv(d.P[l - 1], DW_BN);
+  const int m_tiles = d.P[l] / BM / cg, n_tiles = cdiv(d.P[l - 1], dw_unit_cols(cg));
   const int k_blocks = cdiv((long long)d.T * B, BK);
   const long long mn = (long long)m_tiles * n_tiles;
   const int sms = cg == 2 ? pair_slots() : num_sms();   // concurrent units (CTA pairs when cg = 2)
@@ -1080,7 +1142,7 @@ int launch_lif_dw_tc(const ActorDims& d, int l, int B, const void* Gl, const uin
   p.R = d.T * B;
   p.cg = dw_cg(d, l);
   p.m_tiles = d.P[l] / BM / p.cg;
-  p.n_tiles = cdiv(d.P[l - 1], DW_BN);
+  p.n_tiles = cdiv(d.P[l - 1], dw_unit_cols(p.cg));
   p.k_blocks = cdiv(p.R, BK);
   int splits, kps;
   tc_dw_plan(d, l, B, &splits, &kps);

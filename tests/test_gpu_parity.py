@@ -146,6 +146,53 @@ def test_actor_bf16_cfg4_shape_subsample():
     print(st)
 
 
+def test_actor_bf16_cfg4_full_batch():
+    """configs[4] at its full batch (65 536 rows: the launch configuration bench.py times).
+    Forward: the oracle re-runs 96 sampled rows teacher forced (spikes, masks, actions, encoder).
+    Backward: every row's G_l is independent of the batch it runs in, so the full-batch gradient
+    (one split-K plan, 2048 N tiles per layer) must equal the fp64 sum of the gradients of four
+    16 384-row chunks (other plans); the 64-row oracle check above pins the per-row backward."""
+    import torch
+    import paper_2502_17496_b200 as pk
+    shape, _, Bg = sg.preset("cfg4")
+    p, s, g = _inputs(shape, Bg, seed=7)
+    actor = pk.SpikingActor(pk.actor_cfg_from(shape), Bg)
+    actor.load(p)
+    obs = torch.from_numpy(s).cuda()
+    ga = torch.from_numpy(np.ascontiguousarray(g, np.float32)).cuda()
+    a = actor.forward(obs)
+    full = actor.backward(obs, ga).double().cpu()
+    torch.cuda.synchronize()
+    rows = np.sort(np.random.default_rng(3).choice(Bg, 96, replace=False))
+    rt = torch.from_numpy(rows).cuda()
+    v = actor.tape_view()
+    N = [shape.obs_dim * shape.pop_enc, shape.n1, shape.n2, shape.act_dim * shape.pop_dec]
+    sp = {f"o{l}": pk.unpack_bits(v[f"bits{l}"][:, rt, :], N[l]) for l in range(4)}
+    sp.update({f"h{l}": pk.unpack_bits(v[f"mask{l}"][:, rt, :], N[l]) for l in (1, 2, 3)})
+    gpu = dict(a=a[rt].cpu().numpy().astype(np.float64), grads=None, sp=sp, A=v["A"][rt].cpu().numpy(),
+               counts=v["counts"][rt].cpu().numpy())
+    print(check_actor(gpu, shape, p, s[rows], None))
+    del actor, v
+    Bc = Bg // 4
+    chunk = pk.SpikingActor(pk.actor_cfg_from(shape), Bc)
+    chunk.load(p)
+    tot = torch.zeros_like(full)
+    for c in range(4):
+        tot += _fwd_bwd(chunk, obs[c * Bc:(c + 1) * Bc], ga[c * Bc:(c + 1) * Bc])
+    gf, gt = pk.unpack_actor(chunk.cfg, full.float()), pk.unpack_actor(chunk.cfg, tot.float())
+    for k in gf:
+        e = rel_l2(gf[k], gt[k])
+        assert e <= 1e-4, (k, e)
+
+
+def _fwd_bwd(actor, obs, ga):
+    import torch
+    actor.forward(obs)
+    out = actor.backward(obs, ga).double().cpu()
+    torch.cuda.synchronize()
+    return out
+
+
 @pytest.mark.parametrize("B", [100, 257])
 def test_neuron_major_planes_are_transposes(B):
     """tcgen05 engine: the octet-major spike/mask copies read by the fused dX epilogue hold

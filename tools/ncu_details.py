@@ -1,0 +1,20 @@
+"""Print the `details` page of one kernel (by ID) of an ncu report, section by section.
+
+  python tools/ncu_details.py <report.ncu-rep> <ID> [section-regex]
+"""
+import csv, re, subprocess, sys
+rep, kid = sys.argv[1], sys.argv[2]
+pat = re.compile(sys.argv[3] if len(sys.argv) > 3 else ".")
+out = subprocess.run(["ncu", "-i", rep, "--page", "details", "--csv"], capture_output=True, text=True).stdout
+rows = list(csv.reader(out.splitlines()))
+h = rows[0]
+I = {k: h.index(k) for k in ("ID", "Kernel Name", "Section Name", "Metric Name", "Metric Unit", "Metric Value")}
+name = None
+for r in rows[1:]:
+    if len(r) <= I["Metric Value"] or r[I["ID"]] != kid:
+        continue
+    if name is None:
+        name = r[I["Kernel Name"]]
+        print(name[:150])
+    if pat.search(r[I["Section Name"]]) and r[I["Metric Name"]]:
+        print(f"  {r[I['Section Name']][:28]:28s} {r[I['Metric Name']][:52]:52s} {r[I['Metric Value']]:>14s} {r[I['Metric Unit']]}")

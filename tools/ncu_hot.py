@@ -1,17 +1,41 @@
-"""Summarise an ncu --set full report: top SASS instructions by warp-stall samples."""
-import csv, subprocess, sys
-rep = sys.argv[1]; n = int(sys.argv[2]) if len(sys.argv) > 2 else 25
+"""Summarise an ncu --set full report: top SASS instructions by warp-stall samples.
+
+  python tools/ncu_hot.py <report.ncu-rep> [n_lines] [kernel-regex] [occurrence]
+
+The source page holds one table per profiled launch ("Kernel Name" line, then "Address" header);
+kernel-regex / occurrence pick the table (default: the first).
+"""
+import csv, re, subprocess, sys
+rep = sys.argv[1]
+n = int(sys.argv[2]) if len(sys.argv) > 2 else 25
+pat = re.compile(sys.argv[3]) if len(sys.argv) > 3 else None
+occ = int(sys.argv[4]) if len(sys.argv) > 4 else 0
 out = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-source", "sass"], capture_output=True, text=True).stdout
 rows = list(csv.reader(out.splitlines()))
-hi = [i for i, r in enumerate(rows) if r and r[0] == "Address"][0]
-h = rows[hi]
+tables, cur = [], None
+for r in rows:
+    if r and r[0] == "Kernel Name":
+        cur = [r[1], None, []]
+        tables.append(cur)
+    elif r and r[0] == "Address" and cur is not None:
+        cur[1] = r
+    elif cur is not None and cur[1] is not None and len(r) >= len(cur[1]) - 1:
+        cur[2].append(r)
+sel = [t for t in tables if pat is None or pat.search(t[0])]
+name, h, data = sel[occ]
+print(name[:140])
 si = h.index("Warp Stall Sampling (All Samples)"); ie = h.index("Instructions Executed")
-data = []
-for r in rows[hi + 1:]:
-    if len(r) != len(h): continue
-    try: data.append((float(r[si] or 0), r[0], r[1], r[ie]))
-    except ValueError: pass
-tot = sum(d[0] for d in data) or 1
+stalls = [i for i, c in enumerate(h) if c.startswith("stall_") and "Not Issued" not in c]
+recs = []
+for r in data:
+    try:
+        recs.append((float(r[si] or 0), r))
+    except ValueError:
+        pass
+tot = sum(x[0] for x in recs) or 1
 print("total samples", tot)
-for d in sorted(data, reverse=True)[:n]:
-    print(f"{100*d[0]/tot:5.1f}%  {d[1]}  {d[2][:90]:90s} exec={d[3]}")
+agg = {h[i]: sum(float(r[i] or 0) for _, r in recs) for i in stalls}
+print("stall mix:", ", ".join(f"{k[6:]} {100 * v / tot:.1f}%" for k, v in sorted(agg.items(), key=lambda kv: -kv[1])[:8]))
+for s, r in sorted(recs, key=lambda x: -x[0])[:n]:
+    top = sorted(((float(r[i] or 0), h[i][6:]) for i in stalls), reverse=True)[:2]
+    print(f"{100 * s / tot:5.1f}%  {r[0]}  {r[1][:80]:80s} exec={r[ie]} [{', '.join(f'{b} {a:.0f}' for a, b in top)}]")
