@@ -146,25 +146,27 @@ template <> struct GT<__nv_bfloat16> {
   __device__ __forceinline__ static float round(float v) { return bf16_round(v); }
 };
 
-// LIF scan step shared by every forward kernel (north_star equations).
-// Uses explicit round-to-nearest ops (no FMA contraction) so all engines agree bit-for-bit on
-// identical currents.
+// LIF scan step shared by every forward kernel (north_star equations), so all
+// engines agree bit-for-bit on identical currents. c and v each take one fused multiply-add
+// (one rounding, closer to the fp64 oracle than a rounded product plus a rounded sum); the
+// reset gate is exact: v = c when the neuron fired at t-1.
 struct LifConst { float dc, dv, vth, win; };
 __device__ __forceinline__ void lif_step(const LifConst& k, float I, float& c, float& v, bool& o,
                                          bool& h) {
-  c = __fadd_rn(__fmul_rn(k.dc, c), I);
-  float vv = o ? 0.0f : __fmul_rn(k.dv, v);   // d_v * v * (1 - o_prev), exact gate
-  v = __fadd_rn(vv, c);
+  c = __fmaf_rn(k.dc, c, I);
+  v = o ? c : __fmaf_rn(k.dv, v, c);   // d_v * v * (1 - o_prev) + c
   o = v > k.vth;
   h = fabsf(__fsub_rn(v, k.vth)) < k.win;
 }
 
 // Reverse-scan step (rho = 0; reset gate detached): given g_o(t), o_t, h_t (bits) and the
 // carried (dv_next, dc_next), returns G_t = delta_c_t.  SPEC.md:168-176; R11.
+//   delta_v_t = h_t z g_t + d_v (1 - o_t) delta_v_{t+1};  delta_c_t = delta_v_t + d_c delta_c_{t+1}
 __device__ __forceinline__ float lif_back_step(float zh, float dvc, float dcc, float g, bool o,
                                                bool h, float& dvn, float& dcn) {
-  float dvt = __fadd_rn(h ? __fmul_rn(zh, g) : 0.0f, o ? 0.0f : __fmul_rn(dvc, dvn));
-  float dct = __fadd_rn(dvt, __fmul_rn(dcc, dcn));
+  const float hg = h ? __fmul_rn(zh, g) : 0.0f;
+  const float dvt = o ? hg : __fmaf_rn(dvc, dvn, hg);
+  const float dct = __fmaf_rn(dcc, dcn, dvt);
   dvn = dvt;
   dcn = dct;
   return dct;

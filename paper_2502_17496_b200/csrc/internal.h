@@ -72,13 +72,31 @@ int launch_f32_to_bf16(const float* in, __nv_bfloat16* out, size_t n, cudaStream
 // bf16 working-copy views of an fp32 master vector: Adam / Polyak write the RNE bf16 value of every
 // element they update into each place the refresh kernels would put it (the zero padding, written
 // once by a full refresh, is never touched), so the TD3 step needs no separate refresh launches.
+// Unsigned 32-bit division by a runtime-invariant divisor without a divide instruction sequence:
+// q = (umulhi(x, mul) + x) >> shift with mul = floor(2^32 (2^shift - d) / d) + 1, shift =
+// ceil(log2 d) (Granlund-Montgomery; exact for every 32-bit x; the add is done in 64 bits).
+struct FastDiv {
+  uint32_t d, mul, shift;
+};
+inline FastDiv make_fastdiv(uint32_t d) {
+  FastDiv f{d, 0u, 0u};
+  while ((1ull << f.shift) < d) ++f.shift;
+  f.mul = (uint32_t)(((1ull << 32) * ((1ull << f.shift) - d)) / d + 1);
+  return f;
+}
+__device__ __forceinline__ uint32_t fdiv(uint32_t x, const FastDiv& f) {
+  return (uint32_t)(((unsigned long long)__umulhi(x, f.mul) + x) >> f.shift);
+}
+
 struct Bf16Views {
   int kind;                  // 0 none, 1 actor W1..W3, 2 critic twin (mma layout), 3 plain copy
   __nv_bfloat16* out;
   long long src[3], dst[3];  // actor: fp32 offset of W_l, bf16 offset of its padded copy
   int rows[3], cols[3], ldd[3];
+  FastDiv colsd[3];
   long long P, tb, oW1, oW2, W1p, W1T, W2T, W2c;   // critic (per-critic block after the [2][P] copy)
   int in, H1, H2, inp;
+  FastDiv Pd, ind, H1d;
 };
 Bf16Views actor_bf16_views(const ActorDims& d, __nv_bfloat16* out);
 Bf16Views critic_bf16_views(const CriticDims& c, __nv_bfloat16* out);

@@ -484,6 +484,7 @@ Bf16Views critic_bf16_views(const CriticDims& c, __nv_bfloat16* out) {
   if (!out || !c.bf16) return v;
   v.out = out;
   v.P = (long long)c.off[SPIKERL_CRITIC_NPARAM];
+  v.Pd = make_fastdiv((uint32_t)v.P);
   if (!critic_mma_ok(c)) { v.kind = 3; return v; }
   const MmaLayout L = mma_layout(c);
   v.kind = 2;
@@ -492,6 +493,7 @@ Bf16Views critic_bf16_views(const CriticDims& c, __nv_bfloat16* out) {
   v.oW2 = (long long)c.off[SPIKERL_CRITIC_W2];
   v.W1p = L.W1p; v.W1T = L.W1T; v.W2T = L.W2T; v.W2c = L.W2c;
   v.in = c.in; v.H1 = c.H1; v.H2 = c.H2; v.inp = L.inp;
+  v.Pd = make_fastdiv((uint32_t)v.P); v.ind = make_fastdiv((uint32_t)c.in); v.H1d = make_fastdiv((uint32_t)c.H1);
   return v;
 }
 

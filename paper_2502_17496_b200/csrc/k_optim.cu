@@ -70,40 +70,44 @@ Bf16Views actor_bf16_views(const ActorDims& d, __nv_bfloat16* out) {
     v.rows[l - 1] = d.N[l];
     v.cols[l - 1] = d.N[l - 1];
     v.ldd[l - 1] = d.P[l - 1];
+    v.colsd[l - 1] = make_fastdiv((uint32_t)d.N[l - 1]);
   }
   return v;
 }
 
+// Writes the RNE bf16 copy of the updated master element e into every working copy that holds
+// it. Element indices are < 2^31 (parameter counts), so row / column come from 32-bit
+// multiply-high divisions (a 64-bit division per element made Adam ~5x slower than its bytes).
 __device__ __forceinline__ void store_views(const Bf16Views& v, size_t e, float x) {
   if (v.kind == 0) return;
   const __nv_bfloat16 h = __float2bfloat16_rn(x);
-  const long long le = (long long)e;
   if (v.kind == 1) {
 #pragma unroll
     for (int l = 0; l < 3; ++l) {
-      const long long r = le - v.src[l];
+      const long long r = (long long)e - v.src[l];
       if (r >= 0 && r < (long long)v.rows[l] * v.cols[l]) {
-        const long long n = r / v.cols[l], k = r - n * v.cols[l];
-        v.out[v.dst[l] + n * v.ldd[l] + k] = h;
+        const uint32_t n = fdiv((uint32_t)r, v.colsd[l]), k = (uint32_t)r - n * (uint32_t)v.cols[l];
+        v.out[v.dst[l] + (long long)n * v.ldd[l] + k] = h;
       }
     }
     return;
   }
-  v.out[le] = h;   // [2][P] plain copy (kinds 2 and 3)
+  v.out[e] = h;   // [2][P] plain copy (kinds 2 and 3)
   if (v.kind != 2) return;
-  const long long z = le / v.P, l = le - z * v.P;
+  const uint32_t z = fdiv((uint32_t)e, v.Pd);
+  const long long l = (long long)e - (long long)z * v.P;
   __nv_bfloat16* blk = v.out + 2 * v.P + z * v.tb;
   long long r = l - v.oW1;
   if (r >= 0 && r < (long long)v.H1 * v.in) {          // W1[j][i] -> W1p[j][i], W1T[i][j]
-    const long long j = r / v.in, i = r - j * v.in;
-    blk[v.W1p + j * v.inp + i] = h;
-    blk[v.W1T + i * v.H1 + j] = h;
+    const uint32_t j = fdiv((uint32_t)r, v.ind), i = (uint32_t)r - j * (uint32_t)v.in;
+    blk[v.W1p + (long long)j * v.inp + i] = h;
+    blk[v.W1T + (long long)i * v.H1 + j] = h;
     return;
   }
   r = l - v.oW2;
   if (r >= 0 && r < (long long)v.H2 * v.H1) {          // W2[j2][j1] -> W2T[j1][j2], W2c[j2][j1]
-    const long long j2 = r / v.H1, j1 = r - j2 * v.H1;
-    blk[v.W2T + j1 * v.H2 + j2] = h;
+    const uint32_t j2 = fdiv((uint32_t)r, v.H1d), j1 = (uint32_t)r - j2 * (uint32_t)v.H1;
+    blk[v.W2T + (long long)j1 * v.H2 + j2] = h;
     blk[v.W2c + r] = h;
   }
 }
@@ -119,11 +123,19 @@ __global__ void __launch_bounds__(256) adam_kernel(float* __restrict__ p, const 
                                                    const __grid_constant__ Bf16Views views) {
   pdl_wait();
   pdl_trigger();
-  const long long t = *(volatile long long*)counter + 1;
-  const double bc1 = 1.0 - pow((double)b1, (double)t);
-  const double bc2 = 1.0 - pow((double)b2, (double)t);
-  const float step_size = (float)((double)lr / bc1);
-  const float bc2_sqrt = (float)sqrt(bc2);
+  // bias corrections once per block (fp64 pow), not once per thread
+  __shared__ float s_coef[2];
+  __shared__ long long s_t;
+  if (threadIdx.x == 0) {
+    const long long tt = *(volatile long long*)counter + 1;
+    s_t = tt;
+    s_coef[0] = (float)((double)lr / (1.0 - pow((double)b1, (double)tt)));
+    s_coef[1] = (float)sqrt(1.0 - pow((double)b2, (double)tt));
+  }
+  __syncthreads();
+  const long long t = s_t;
+  const float step_size = s_coef[0];
+  const float bc2_sqrt = s_coef[1];
   const float omb1 = 1.0f - b1, omb2 = 1.0f - b2;
   const size_t n4 = n / 4;
   const size_t stride = (size_t)gridDim.x * blockDim.x;
