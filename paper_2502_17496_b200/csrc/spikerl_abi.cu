@@ -188,6 +188,8 @@ static int actor_forward_impl(const ActorDims& d, int B, const float* params,
   uint32_t* mask[4];
   for (int l = 0; l < 4; ++l) { bits[l] = (uint32_t*)(tape + L.bits[l]); mask[l] = (uint32_t*)(tape + L.mask[l]); }
   uint8_t* counts = (uint8_t*)(tape + L.counts);
+  if (fused_fwd_ok(d, B))   // small batch: one clustered launch instead of five
+    return launch_actor_fwd_fused(d, B, obs, params, pb16, L, tape, actions, st);
   SPK_TRY(launch_enc_fwd(d, B, obs, params + d.off[SPIKERL_ACTOR_MU], params + d.off[SPIKERL_ACTOR_SIGMA],
                          A, bits[0], st));
   for (int l = 1; l <= 3; ++l) {
