@@ -199,6 +199,13 @@ def build_td3(name, world, rank, engine, replay_size, seed=0):
     return td3, shape, B
 
 
+def l2_flush(buf):
+    """Evict L2 by READING a buffer twice its size (clean lines: a write flush would leave ~126 MB of
+    dirty lines whose write-back the next timed kernel pays for)."""
+    import torch
+    torch.sum(buf)
+
+
 def time_steps(run_step, K, flush_buf, world):
     """Per-step CUDA events on the launching stream; L2 flushed between steps (outside events)."""
     import torch
@@ -206,7 +213,7 @@ def time_steps(run_step, K, flush_buf, world):
     barrier(world)
     for k in range(K):
         if flush_buf is not None:
-            flush_buf.zero_()
+            l2_flush(flush_buf)
         evs[k][0].record()
         run_step(k)
         evs[k][1].record()
@@ -328,7 +335,7 @@ def run_td3(args, rank, world):
                                   f"{shape.obs_dim + shape.act_dim}->256->256->1",
                       "global_batch": B * world, "per_rank_batch": B, "replay_per_rank": args.replay_size,
                       "parallelism": f"dp{world}", "engine": args.engine,
-                      "l2": "flushed between timed steps (256 MB write, outside the events)" if flush is not None
+                      "l2": "flushed between timed steps (256 MB read, outside the events)" if flush is not None
                       else "not flushed", "cuda_graph": True},
            "clocks": clocks, "gpu_launches": int(gpu_launches)}
     # e2e: minibatch from pinned host memory every step + loss read-back, through the public API
@@ -437,6 +444,7 @@ def run_actor(args, rank, world):
     out["roofline"] = dominant_kernel(summ, peaks(), long_step=True)
     out["kernel_breakdown"] = sorted([{k: (round(v, 4) if isinstance(v, float) else v) for k, v in e.items()}
                                       for e in summ], key=lambda e: -e["total_ms"])[:12]
+    out["hbm_kernels"] = hbm_kernels(actor, summ)
     if not args.no_e2e:
         host_obs = obs.cpu().pin_memory(); host_ga = ga.cpu().pin_memory()
         grads_host = torch.empty(actor.n_params, dtype=torch.float32).pin_memory()
@@ -451,6 +459,50 @@ def run_actor(args, rank, world):
                       "h2d_bytes_per_step": B * (shape.obs_dim + shape.act_dim) * 4,
                       "d2h_bytes_per_step": actor.n_params * 4}
     return out
+
+
+def hbm_kernels(actor, summ, reps=20):
+    """The HBM-bound kernels of the path against the measured copy bandwidth (north_star: LIF scans
+    and Adam >= 70%): the output-layer reverse scan from the step's launch list, and Adam / Polyak
+    over the configs[4] actor's 5.08 M parameters (28 / 12 algorithmic bytes per parameter), each
+    launch timed alone with CUDA events on its stream, L2 flushed between launches."""
+    import torch
+    import paper_2502_17496_b200 as pk
+    pk_peaks = peaks()
+    res = {}
+    for e in summ:
+        if e["name"] == "dec_bwd_outscan":
+            gbs = e["bytes"] / (e["total_ms"] / 1e3) / 1e9
+            res["dec_bwd_outscan"] = {"achieved": round(gbs, 1), "unit": "GB/s", "peak": pk_peaks["hbm_gbs"],
+                                      "frac": round(gbs / pk_peaks["hbm_gbs"], 4),
+                                      "bytes_per_launch": e["bytes"] / e["launches"],
+                                      "us_per_launch": round(e["total_ms"] / e["launches"] * 1e3, 2)}
+    n = actor.n_params
+    f32 = dict(dtype=torch.float32, device="cuda")
+    p = actor.params.clone()
+    g = torch.randn(n, **f32) * 1e-3
+    m, v = torch.zeros(n, **f32), torch.zeros(n, **f32)
+    t = torch.zeros(2, dtype=torch.int64, device="cuda")
+    tgt = p.clone()
+    flush = torch.empty(64 * 1024 * 1024, **f32)
+    for name, bpp, fn in (("adam", 28.0, lambda: pk.adam(p, g, m, v, t, 1e-4)),
+                          ("polyak", 12.0, lambda: pk.polyak(tgt, p, 0.005))):
+        fn()
+        tot = 0.0
+        for _ in range(reps):
+            l2_flush(flush)
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            fn()
+            e1.record()
+            torch.cuda.synchronize()
+            tot += e0.elapsed_time(e1)
+        us = tot / reps * 1e3
+        gbs = bpp * n / (us / 1e6) / 1e9
+        res[name] = {"achieved": round(gbs, 1), "unit": "GB/s", "peak": pk_peaks["hbm_gbs"],
+                     "frac": round(gbs / pk_peaks["hbm_gbs"], 4), "bytes_per_launch": bpp * n,
+                     "us_per_launch": round(us, 2), "params": n}
+    return res
 
 
 def main():

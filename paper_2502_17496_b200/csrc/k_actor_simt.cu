@@ -118,68 +118,120 @@ int launch_dec_fwd(const ActorDims& d, int B, const uint8_t* counts, const float
 }
 
 // ------------------------------------------------------- decoder backward + output reverse scan
-// 32x32 bit-matrix transpose across a warp: lane i holds row i on entry, column i on exit
-// (five butterfly stages, each swapping the off-diagonal s x s blocks).
-__device__ __forceinline__ uint32_t warp_transpose32(uint32_t x, int lane) {
-  const uint32_t lo[5] = {0x0000FFFFu, 0x00FF00FFu, 0x0F0F0F0Fu, 0x33333333u, 0x55555555u};
-#pragma unroll
-  for (int k = 0, s = 16; k < 5; ++k, s >>= 1) {
-    const uint32_t y = __shfl_xor_sync(0xffffffffu, x, s);
-    x = (lane & s) ? ((x & ~lo[k]) | ((y & ~lo[k]) >> s)) : ((x & lo[k]) | ((y & lo[k]) << s));
+// Output-layer reverse scan (HBM-bound: writes G3, reads the spike / mask planes). A thread owns
+// 8 consecutive neurons of one batch row for all T steps: the 8 scans are independent chains,
+// each step's 8 results leave as one 16-byte store (bf16) and the step's spike / mask bits are one
+// byte of a word shared by 4 lanes. A warp covers 2 rows x 128 neurons; grid-strided over (row
+// pair, group of 4 words). ncu r01: the one-neuron-per-lane version issued ~36 instructions per element and
+// reached 31% of HBM bandwidth at configs[4].
+template <typename GTy> struct Pack8;
+template <> struct Pack8<__nv_bfloat16> {
+  __device__ __forceinline__ static void store(__nv_bfloat16* p, const float (&v)[8]) {
+    uint4 u;
+    u.x = bf2_bits(v[0], v[1]); u.y = bf2_bits(v[2], v[3]); u.z = bf2_bits(v[4], v[5]); u.w = bf2_bits(v[6], v[7]);
+    *reinterpret_cast<uint4*>(p) = u;
   }
-  return x;
-}
+  __device__ __forceinline__ static uint32_t bf2_bits(float a, float b) {
+    const __nv_bfloat162 h = __floats2bfloat162_rn(a, b);
+    return *reinterpret_cast<const uint32_t*>(&h);
+  }
+};
+template <> struct Pack8<float> {
+  __device__ __forceinline__ static void store(float* p, const float (&v)[8]) {
+    reinterpret_cast<float4*>(p)[0] = make_float4(v[0], v[1], v[2], v[3]);
+    reinterpret_cast<float4*>(p)[1] = make_float4(v[4], v[5], v[6], v[7]);
+  }
+};
 
-// One warp per (b, 32 output neurons), grid-strided over b. For T <= 32 lane t loads the spike
-// and mask words of step t and a warp bit transpose hands each neuron its bits over t, so the
-// reverse scan waits on no load (ncu r01: per-neuron redundant word loads and 64-bit index math
-// made this kernel ~50 instructions per element).
-template <typename GTy>
-__global__ void __launch_bounds__(128) dec_bwd_outscan_kernel(
-    int B, int T, int A, int D, int P3, int W3, float dcc, float dvc, float zh,
+template <typename GTy, int TT>
+__global__ void __launch_bounds__(256, 4) dec_bwd_outscan_kernel(
+    int B, int T, int A, int D, int N3, int W3, float dcc, float dvc, float zh,
     const float* __restrict__ grad_a, const float* __restrict__ act, const float* __restrict__ Wd,
     const uint32_t* __restrict__ bits3, const uint32_t* __restrict__ mask3, GTy* __restrict__ G3,
-    float* __restrict__ g_pre_out) {
+    float* __restrict__ g_pre_out, int write_pad) {
   pdl_wait();
   pdl_trigger();
-  const int n = blockIdx.y * 128 + threadIdx.x;
-  const int lane = threadIdx.x & 31;
-  const int N3 = A * D;
-  const bool nv = n < N3;
-  const int j = nv ? n / D : 0, e = nv ? n % D : 0;
-  const float wd = nv ? Wd[j * D + e] : 0.f;
-  const size_t ts = (size_t)B * W3;   // bit-plane stride between timesteps
-  const size_t gts = (size_t)B * P3;  // G3 stride between timesteps
-  for (int b = blockIdx.x; b < B; b += gridDim.x) {
-    float g = 0.f;
-    if (nv) {
-      const float a = act[(size_t)b * A + j];
-      const float gp = __fmul_rn(grad_a[(size_t)b * A + j], __fsub_rn(1.0f, __fmul_rn(a, a)));
-      if (e == 0) g_pre_out[(size_t)b * A + j] = gp;
-      g = __fdiv_rn(__fmul_rn(gp, wd), (float)T);  // g_o3 = g_fr / T, constant in t
+  // lane = (row jr of 2, word wq of 4, octet oct of 4): a warp stores 2 rows x 128 neurons, i.e.
+  // whole 128-byte lines of G3 (bf16), per step
+  const int lane = threadIdx.x & 31, jr = lane >> 4, wq = (lane >> 2) & 3, oct = lane & 3;
+  const int WG = W3 / 4;   // groups of 4 words (P3 is a multiple of 128)
+  const long long units = (long long)((B + 1) / 2) * WG;
+  const int P3 = 32 * W3;
+  const size_t ts = (size_t)B * W3;    // bit-plane stride between timesteps
+  const size_t gts = (size_t)B * P3;   // G3 stride between timesteps
+  for (long long u = (long long)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); u < units;
+       u += (long long)gridDim.x * (blockDim.x >> 5)) {
+    const int w = (int)(u % WG) * 4 + wq, b = (int)(u / WG) * 2 + jr;
+    if (b >= B) continue;   // (no warp-collective operations below)
+    const int n0 = 32 * w + 8 * oct;
+    // padded neurons (n >= N3) have G = 0: with the tcgen05 engine their columns are never read
+    // (TMA zero-fills past N3), so those lanes store nothing
+    const bool live = n0 < N3 || write_pad;
+    // g_o3 = g_fr / T = g_pre_a Wd[a][d] / T, constant in t; g_pre written once per (b, action)
+    float g[8];
+    int a = n0 / D, e = n0 - a * D;
+    float gp = 0.f;
+    if (n0 < N3) {
+      const float av = act[(size_t)b * A + a];
+      gp = __fmul_rn(grad_a[(size_t)b * A + a], __fsub_rn(1.0f, __fmul_rn(av, av)));
     }
-    float dvn = 0.f, dcn = 0.f;
-    GTy* gt = G3 + (size_t)b * P3 + n;
-    const uint32_t* po = bits3 + (size_t)b * W3 + (n >> 5);
-    const uint32_t* ph = mask3 + (size_t)b * W3 + (n >> 5);
-    if (T <= 32) {
-      uint32_t wo = 0u, wh = 0u;
-      if (lane < T) { wo = __ldg(po + lane * ts); wh = __ldg(ph + lane * ts); }
-      const uint32_t om = warp_transpose32(wo, lane), hm = warp_transpose32(wh, lane);
-      gt += (size_t)(T - 1) * gts;
-      for (int t = T - 1; t >= 0; --t, gt -= gts) {
-        const float Gt = lif_back_step(zh, dvc, dcc, g, (om >> t) & 1u, (hm >> t) & 1u, dvn, dcn);
-        GT<GTy>::store(gt, nv ? Gt : 0.f);
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      g[i] = 0.f;
+      if (n0 + i < N3) {
+        if (e == 0) g_pre_out[(size_t)b * A + a] = gp;
+        g[i] = __fmul_rn(zh, __fdiv_rn(__fmul_rn(gp, Wd[a * D + e]), (float)T));   // h z g (h applied below)
       }
-      continue;
+      if (++e == D && n0 + i + 1 < N3) {   // next action's population
+        e = 0;
+        ++a;
+        const float av = act[(size_t)b * A + a];
+        gp = __fmul_rn(grad_a[(size_t)b * A + a], __fsub_rn(1.0f, __fmul_rn(av, av)));
+      }
     }
-    for (int t = T - 1; t >= 0; --t) {
-      float Gt = 0.f;
-      if (nv) {
-        const uint32_t ow = __ldg(po + t * ts), hw = __ldg(ph + t * ts);
-        Gt = lif_back_step(zh, dvc, dcc, g, (ow >> lane) & 1u, (hw >> lane) & 1u, dvn, dcn);
+    float dvn[8], dcn[8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) { dvn[i] = 0.f; dcn[i] = 0.f; }
+    const uint32_t* po = bits3 + (size_t)b * W3 + w;
+    const uint32_t* ph = mask3 + (size_t)b * W3 + w;
+    GTy* gq = G3 + (size_t)b * P3 + n0 + (size_t)(T - 1) * gts;   // step T-1; walks back by gts
+    auto step = [&](uint32_t ow, uint32_t hw) {
+      const uint32_t o8 = (ow >> (8 * oct)) & 0xFFu, h8 = (hw >> (8 * oct)) & 0xFFu;
+      float G[8];
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        // lif_back_step with the window factor z folded into g (z is a constant per layer)
+        const float hg = ((h8 >> i) & 1u) ? g[i] : 0.0f;
+        const float dvt = ((o8 >> i) & 1u) ? hg : __fmaf_rn(dvc, dvn[i], hg);
+        const float dct = __fmaf_rn(dcc, dcn[i], dvt);
+        dvn[i] = dvt;
+        dcn[i] = dct;
+        G[i] = dct;
       }
-      GT<GTy>::store(gt + (size_t)t * gts, Gt);
+      if (live) Pack8<GTy>::store(gq, G);
+      gq -= gts;
+    };
+    if constexpr (TT > 0) {
+      // T known: the words of up to 8 steps are requested together before their scan steps (one
+      // memory latency per chunk; 8, not 16, keeps 4 blocks per SM resident without spills)
+      constexpr int CH = TT > 8 ? 8 : TT;
+      static_assert(TT % CH == 0, "T must be a multiple of the chunk");
+#pragma unroll
+      for (int c0 = TT - CH; c0 >= 0; c0 -= CH) {
+        uint32_t ow[CH], hw[CH];
+        const uint32_t *qo = po + (size_t)c0 * ts, *qh = ph + (size_t)c0 * ts;
+#pragma unroll
+        for (int k = 0; k < CH; ++k, qo += ts, qh += ts) { ow[k] = __ldg(qo); hw[k] = __ldg(qh); }
+#pragma unroll
+        for (int k = CH - 1; k >= 0; --k) step(ow[k], hw[k]);
+      }
+    } else {
+      uint32_t ow = __ldg(po + (size_t)(T - 1) * ts), hw = __ldg(ph + (size_t)(T - 1) * ts);
+      for (int t = T - 1; t >= 0; --t) {
+        const uint32_t o = ow, h = hw;
+        if (t > 0) { ow = __ldg(po + (size_t)(t - 1) * ts); hw = __ldg(ph + (size_t)(t - 1) * ts); }
+        step(o, h);
+      }
     }
   }
 }
@@ -187,21 +239,26 @@ __global__ void __launch_bounds__(128) dec_bwd_outscan_kernel(
 int launch_dec_bwd_outscan(const ActorDims& d, int B, const float* grad_a, const float* act,
                            const uint8_t* counts, const float* Wd, const uint32_t* bits3,
                            const uint32_t* mask3, void* G3, float* g_pre, cudaStream_t st) {
-  ProfScope ps_("dec_bwd_outscan", PB_HBM, 0.0, (double)d.T * B * (d.P[3] * (d.bf16 ? 2.0 : 4.0) + 2.0 * d.Wd[3] * 4), st);
+  // algorithmic bytes: G3 written for the N3 real neurons (tcgen05: padding never written), both
+  // bit planes read
+  const double gcols = d.engine == SPIKERL_ENGINE_TCGEN05 ? d.N3 : d.P[3];
+  ProfScope ps_("dec_bwd_outscan", PB_HBM, 0.0, (double)d.T * B * (gcols * (d.bf16 ? 2.0 : 4.0) + 2.0 * d.Wd[3] * 4), st);
   (void)counts;
-  // grid-strided over b: one 128-thread block per (b, 128 neurons) was block-scheduling bound
-  const int gy = d.P[3] / 128;
-  int gx = (num_sms() * 16 + gy - 1) / gy;
-  if (gx > B) gx = B;
-  dim3 grid(gx, gy);
-  if (d.bf16)
-    pdl((dec_bwd_outscan_kernel<__nv_bfloat16>), grid, 128, 0, st)(
-        B, d.T, d.A, d.D, d.P[3], d.Wd[3], d.dc, d.dv, d.zh, grad_a, act, Wd, bits3, mask3,
-        (__nv_bfloat16*)G3, g_pre);
-  else
-    pdl((dec_bwd_outscan_kernel<float>), grid, 128, 0, st)(B, d.T, d.A, d.D, d.P[3], d.Wd[3], d.dc,
-                                                        d.dv, d.zh, grad_a, act, Wd, bits3, mask3,
-                                                        (float*)G3, g_pre);
+  const long long units = (long long)cdiv(B, 2) * (d.Wd[3] / 4);   // warps of work
+  const int wpad = d.engine == SPIKERL_ENGINE_TCGEN05 ? 0 : 1;     // SIMT kernels read P3 columns
+  long long blocks = cdiv(units, 8);
+  if (blocks > (long long)num_sms() * 8) blocks = (long long)num_sms() * 8;
+  if (d.bf16) {
+    if (d.T == 16) pdl((dec_bwd_outscan_kernel<__nv_bfloat16, 16>), (int)blocks, 256, 0, st)(
+        B, d.T, d.A, d.D, d.N3, d.Wd[3], d.dc, d.dv, d.zh, grad_a, act, Wd, bits3, mask3, (__nv_bfloat16*)G3, g_pre, wpad);
+    else if (d.T == 5) pdl((dec_bwd_outscan_kernel<__nv_bfloat16, 5>), (int)blocks, 256, 0, st)(
+        B, d.T, d.A, d.D, d.N3, d.Wd[3], d.dc, d.dv, d.zh, grad_a, act, Wd, bits3, mask3, (__nv_bfloat16*)G3, g_pre, wpad);
+    else pdl((dec_bwd_outscan_kernel<__nv_bfloat16, 0>), (int)blocks, 256, 0, st)(
+        B, d.T, d.A, d.D, d.N3, d.Wd[3], d.dc, d.dv, d.zh, grad_a, act, Wd, bits3, mask3, (__nv_bfloat16*)G3, g_pre, wpad);
+  } else {
+    pdl((dec_bwd_outscan_kernel<float, 0>), (int)blocks, 256, 0, st)(
+        B, d.T, d.A, d.D, d.N3, d.Wd[3], d.dc, d.dv, d.zh, grad_a, act, Wd, bits3, mask3, (float*)G3, g_pre, 1);
+  }
   SPK_LAUNCHED();
   return SPIKERL_OK;
 }

@@ -139,25 +139,40 @@ __global__ void __launch_bounds__(256) adam_kernel(float* __restrict__ p, const 
   const float omb1 = 1.0f - b1, omb2 = 1.0f - b2;
   const size_t n4 = n / 4;
   const size_t stride = (size_t)gridDim.x * blockDim.x;
-  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n4; i += stride) {
-    float4 pp = reinterpret_cast<float4*>(p)[i];
-    const float4 gg = reinterpret_cast<const float4*>(g)[i];
-    float4 mm = reinterpret_cast<float4*>(m)[i];
-    float4 vv = reinterpret_cast<float4*>(v)[i];
-    float* pa = &pp.x; const float* ga = &gg.x; float* ma = &mm.x; float* va = &vv.x;
+  // two float4 groups per thread and iteration, every load issued before any arithmetic (more
+  // bytes in flight per thread: 128 B)
+  for (size_t i0 = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i0 < n4; i0 += 2 * stride) {
+    float4 pp[2], gg[2], mm[2], vv[2];
+    const bool two = i0 + stride < n4;
 #pragma unroll
-    for (int j = 0; j < 4; ++j) {
-      ma[j] = __fadd_rn(__fmul_rn(b1, ma[j]), __fmul_rn(omb1, ga[j]));
-      va[j] = __fadd_rn(__fmul_rn(b2, va[j]), __fmul_rn(__fmul_rn(omb2, ga[j]), ga[j]));
-      const float denom = __fadd_rn(__fdiv_rn(sqrtf(va[j]), bc2_sqrt), eps);
-      pa[j] = __fsub_rn(pa[j], __fmul_rn(step_size, __fdiv_rn(ma[j], denom)));
-      const size_t e = 4 * i + j;
-      if (e >= clo && e < chi) pa[j] = fmaxf(pa[j], cmin);
-      store_views(views, e, pa[j]);
+    for (int u = 0; u < 2; ++u) {
+      const size_t i = i0 + u * stride;
+      if (u == 0 || two) {
+        pp[u] = reinterpret_cast<float4*>(p)[i];
+        gg[u] = reinterpret_cast<const float4*>(g)[i];
+        mm[u] = reinterpret_cast<float4*>(m)[i];
+        vv[u] = reinterpret_cast<float4*>(v)[i];
+      }
     }
-    reinterpret_cast<float4*>(p)[i] = pp;
-    reinterpret_cast<float4*>(m)[i] = mm;
-    reinterpret_cast<float4*>(v)[i] = vv;
+#pragma unroll
+    for (int u = 0; u < 2; ++u) {
+      if (u == 1 && !two) break;
+      const size_t i = i0 + u * stride;
+      float* pa = &pp[u].x; const float* ga = &gg[u].x; float* ma = &mm[u].x; float* va = &vv[u].x;
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        ma[j] = __fadd_rn(__fmul_rn(b1, ma[j]), __fmul_rn(omb1, ga[j]));
+        va[j] = __fadd_rn(__fmul_rn(b2, va[j]), __fmul_rn(__fmul_rn(omb2, ga[j]), ga[j]));
+        const float denom = __fadd_rn(__fdiv_rn(sqrtf(va[j]), bc2_sqrt), eps);
+        pa[j] = __fsub_rn(pa[j], __fmul_rn(step_size, __fdiv_rn(ma[j], denom)));
+        const size_t e = 4 * i + j;
+        if (e >= clo && e < chi) pa[j] = fmaxf(pa[j], cmin);
+        store_views(views, e, pa[j]);
+      }
+      reinterpret_cast<float4*>(p)[i] = pp[u];
+      reinterpret_cast<float4*>(m)[i] = mm[u];
+      reinterpret_cast<float4*>(v)[i] = vv[u];
+    }
   }
   for (size_t e = 4 * n4 + blockIdx.x * (size_t)blockDim.x + threadIdx.x; e < n; e += stride) {
     float mm = __fadd_rn(__fmul_rn(b1, m[e]), __fmul_rn(omb1, g[e]));
@@ -202,8 +217,20 @@ __global__ void polyak_kernel(float* __restrict__ t, const float* __restrict__ s
   pdl_wait();
   pdl_trigger();
   const float omt = 1.0f - tau;
-  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n;
-       i += (size_t)gridDim.x * blockDim.x) {
+  const size_t n4 = (((uintptr_t)t | (uintptr_t)s) & 15) ? 0 : n / 4;   // float4 body when aligned
+  const size_t stride = (size_t)gridDim.x * blockDim.x;
+  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n4; i += stride) {
+    const float4 sv = reinterpret_cast<const float4*>(s)[i];
+    float4 tv = reinterpret_cast<float4*>(t)[i];
+    tv.x = __fadd_rn(__fmul_rn(tau, sv.x), __fmul_rn(omt, tv.x));
+    tv.y = __fadd_rn(__fmul_rn(tau, sv.y), __fmul_rn(omt, tv.y));
+    tv.z = __fadd_rn(__fmul_rn(tau, sv.z), __fmul_rn(omt, tv.z));
+    tv.w = __fadd_rn(__fmul_rn(tau, sv.w), __fmul_rn(omt, tv.w));
+    reinterpret_cast<float4*>(t)[i] = tv;
+    store_views(views, 4 * i, tv.x); store_views(views, 4 * i + 1, tv.y);
+    store_views(views, 4 * i + 2, tv.z); store_views(views, 4 * i + 3, tv.w);
+  }
+  for (size_t i = 4 * n4 + blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n; i += stride) {
     const float x = __fadd_rn(__fmul_rn(tau, s[i]), __fmul_rn(omt, t[i]));
     t[i] = x;
     store_views(views, i, x);
@@ -213,7 +240,7 @@ __global__ void polyak_kernel(float* __restrict__ t, const float* __restrict__ s
 int launch_polyak(float* t, const float* s, size_t n, float tau, const Bf16Views* views, cudaStream_t st) {
   const Bf16Views none{};
   ProfScope ps_("polyak", PB_HBM, 0.0, 12.0 * n, st);
-  pdl(polyak_kernel, ew_grid(n, 1), 256, 0, st)(t, s, n, tau, views ? *views : none);
+  pdl(polyak_kernel, ew_grid(n, 4), 256, 0, st)(t, s, n, tau, views ? *views : none);
   SPK_LAUNCHED();
   return SPIKERL_OK;
 }

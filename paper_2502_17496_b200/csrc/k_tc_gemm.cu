@@ -1043,8 +1043,9 @@ int launch_lif_dx_tc(const ActorDims& d, int l, int B, const void* Gl, const __n
     const uint32_t box[2] = {64, 64};
     SPK_TRY(make_map(&ma, Wb16, 2, dims, strides, box));
   }
-  {  // B = G_l [T][B][P_l]: rows (t, b) t-major per tile, K = P_l
-    const uint64_t dims[3] = {(uint64_t)d.P[l], (uint64_t)B, (uint64_t)d.T};
+  {  // B = G_l [T][B][P_l]: rows (t, b) t-major per tile, K = P_l. The map ends at N_3 for G_3:
+     // TMA zero-fills columns past it (the output-layer scan does not write G_3's padding)
+    const uint64_t dims[3] = {(uint64_t)(l == 3 ? d.N[3] : d.P[l]), (uint64_t)B, (uint64_t)d.T};
     const uint64_t strides[2] = {(uint64_t)d.P[l] * 2, (uint64_t)d.P[l] * 2 * B};
     const uint32_t box[3] = {64, (uint32_t)p.Bt, (uint32_t)(d.T / p.cg)};
     SPK_TRY(make_map(&mb, Gl, 3, dims, strides, box));
@@ -1151,8 +1152,8 @@ int launch_lif_dw_tc(const ActorDims& d, int l, int B, const void* Gl, const uin
   p.bits_dw = bits_prev; p.w_dw = d.Wd[l - 1];
   p.dw_part = part; p.ldp = d.P[l - 1]; p.split_stride = (long long)d.P[l] * d.P[l - 1];
   CUtensorMap ma, mb;
-  {  // A = G_l viewed [T*B][P_l]: M = P_l contiguous (MN-major), K = rows
-    const uint64_t dims[2] = {(uint64_t)d.P[l], (uint64_t)p.R};
+  {  // A = G_l viewed [T*B][P_l]: M = P_l contiguous (MN-major), K = rows (ends at N_3 for G_3, as above)
+    const uint64_t dims[2] = {(uint64_t)(l == 3 ? d.N[3] : d.P[l]), (uint64_t)p.R};
     const uint64_t strides[1] = {(uint64_t)d.P[l] * 2};
     const uint32_t box[2] = {64, 64};
     SPK_TRY(make_map(&ma, Gl, 2, dims, strides, box));
