@@ -66,8 +66,53 @@ __device__ __forceinline__ void warp_mma(float (&acc)[NT][4], const __nv_bfloat1
   }
 }
 
-// bf16 twin buffer: [2][P] (fp32 layout; P may be odd), then one block per critic holding every
-// operand the MMA path reads with 32-bit fragment loads (even offsets): W1p | W1T | W2T | W2
+// Same contraction with B in shared memory too (rows n, k-contiguous, row stride ldb elements).
+template <int NT>
+__device__ __forceinline__ void warp_mma_ss(float (&acc)[NT][4], const __nv_bfloat16* A, int lda,
+                                            const __nv_bfloat16* Bs, int ldb, int K) {
+  const int lane = threadIdx.x & 31, g = lane >> 2, t = lane & 3;
+  const __nv_bfloat16* a0 = A + g * lda + 2 * t;
+  const __nv_bfloat16* a1 = A + (g + 8) * lda + 2 * t;
+  const __nv_bfloat16* bp = Bs + g * ldb + 2 * t;
+#pragma unroll 4
+  for (int k0 = 0; k0 < K; k0 += 16) {
+    const uint32_t a[4] = {ld32(a0 + k0), ld32(a1 + k0), ld32(a0 + k0 + 8), ld32(a1 + k0 + 8)};
+#pragma unroll
+    for (int nt = 0; nt < NT; ++nt)
+      mma16816(acc[nt], a, ld32(bp + nt * 8 * ldb + k0), ld32(bp + nt * 8 * ldb + k0 + 8));
+  }
+}
+
+// A weight matrix [HW rows][K] bf16 staged into shared memory (row stride K + SPAD) by bulk
+// copies (one per row, issued by warp 0 right after the PDL wait), completing on an mbarrier.
+__device__ __forceinline__ uint32_t smem_addr(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void stage_rows(__nv_bfloat16* dst, const __nv_bfloat16* src, int rows, int K, uint64_t* bar) {
+  // every thread issues (at most) one row: a single warp issuing all of them stalled on the copy
+  // queue and held up the whole CTA at the next barrier (trace r01)
+  const uint32_t b = smem_addr(bar);
+  if (threadIdx.x == 0)
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(b), "r"((uint32_t)(rows * K * 2)) : "memory");
+  for (int r = threadIdx.x; r < rows; r += blockDim.x)
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                     smem_addr(dst + (size_t)r * (K + SPAD))),
+                 "l"(src + (size_t)r * K), "r"((uint32_t)(K * 2)), "r"(b)
+                 : "memory");
+}
+__device__ __forceinline__ void stage_wait(uint64_t* bar) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n"
+      "WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], 0;\n\t"
+      "@!p bra WAIT_%=;\n}" ::"r"(smem_addr(bar))
+      : "memory");
+}
+constexpr size_t kW2Smem = (size_t)HW * (HW + SPAD) * 2;   // staged W2 / W2T (135 KB)
+
+// bf16 twin buffer: [2][P] (fp32 layout; P may be odd), then (from element blk_base(P), a multiple
+// of 8 so every row is 16-byte aligned for bulk copies) one block per critic holding every operand
+// the MMA path reads: W1p | W1T | W2T | W2
+__host__ __device__ inline long long blk_base(long long P) { return (2 * P + 7) & ~7LL; }
+
 struct MmaLayout {
   long long P, W1p, W1T, W2T, W2c, tb;
   int inp, inq;          // in rounded to 16 (K of L1) and to 64 (+32 rows of W1T / XT)
@@ -124,8 +169,19 @@ __global__ void __launch_bounds__(256) critic_fwd_mma_kernel(
     long long oW3, const float* __restrict__ params, long long oB1, long long oB2, long long oB3,
     __nv_bfloat16* __restrict__ XT, __nv_bfloat16* __restrict__ H1T, float* __restrict__ Z1,
     float* __restrict__ Z2, float* __restrict__ Hh2, float* __restrict__ q, int store, unsigned int* ticket) {
+  extern __shared__ __align__(128) uint8_t dsm[];
+  __nv_bfloat16* const w2s = (__nv_bfloat16*)dsm;    // this critic's W2 staged: [HW][HW + SPAD]
+  __shared__ __align__(8) uint64_t wbar;
+  if (threadIdx.x == 0) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_addr(&wbar)) : "memory");
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
   pdl_wait();
   pdl_trigger();
+  // W2 into shared memory while the input tile and layer 1 run (the K = 256 layer-2 contraction
+  // then reads no operand from L2)
+  stage_rows(w2s, pb + blk_base(P) + blockIdx.y * tb + oW2, HW, HW, &wbar);
   __shared__ __align__(16) __nv_bfloat16 xs[RB * (512 + SPAD)];
   __shared__ __align__(16) __nv_bfloat16 h1s[RB * (HW + SPAD)];
   __shared__ float red[NWARP][RB];
@@ -134,6 +190,7 @@ __global__ void __launch_bounds__(256) critic_fwd_mma_kernel(
   const int in = S + A, ldx = inp + SPAD, ldh = HW + SPAD;
   if (ticket && blockIdx.x == 0 && z == 0 && tid == 0) *ticket = 0u;   // for the backward launch
   // X tile (bf16-rounded [s; a]); the z == 0 CTAs also write X^T (zeros beyond in / B) for dW1
+#pragma unroll 4
   for (int idx = tid; idx < RB * inp; idx += 256) {
     const int r = idx / inp, i = idx - r * inp, b = r0 + r;
     float v = 0.f;
@@ -147,20 +204,22 @@ __global__ void __launch_bounds__(256) critic_fwd_mma_kernel(
       XT[(size_t)i * Bp + r0 + r] = i < inp ? xs[r * ldx + i] : __float2bfloat16_rn(0.f);
     }
   }
-  const __nv_bfloat16* W1p = pb + 2 * P + z * tb + oW1p;
-  const __nv_bfloat16* W2 = pb + 2 * P + z * tb + oW2;
+  const __nv_bfloat16* W1p = pb + blk_base(P) + z * tb + oW1p;
   const float* b1 = params + z * P + oB1;
   const float* b2 = params + z * P + oB2;
   const int n0 = warp * NTW * 8;
   {
     float acc[NTW][4] = {};
+    float bias[NTW][2];   // requested before the MMAs (latency hidden behind them)
+#pragma unroll
+    for (int nt = 0; nt < NTW; ++nt) { bias[nt][0] = b1[n0 + nt * 8 + 2 * t]; bias[nt][1] = b1[n0 + nt * 8 + 2 * t + 1]; }
     warp_mma<NTW>(acc, xs, ldx, W1p + (size_t)n0 * inp, inp, inp);
 #pragma unroll
     for (int nt = 0; nt < NTW; ++nt) {
 #pragma unroll
       for (int e = 0; e < 4; ++e) {
         const int r = g + (e >> 1) * 8, col = n0 + nt * 8 + 2 * t + (e & 1), b = r0 + r;
-        const float zz = __fadd_rn(acc[nt][e], b1[col]);
+        const float zz = __fadd_rn(acc[nt][e], bias[nt][e & 1]);
         h1s[r * ldh + col] = b < B ? __float2bfloat16_rn(fmaxf(zz, 0.f)) : __float2bfloat16_rn(0.f);
         if (store && b < B) Z1[((size_t)z * B + b) * HW + col] = zz;
       }
@@ -177,15 +236,24 @@ __global__ void __launch_bounds__(256) critic_fwd_mma_kernel(
   float qp[2] = {0.f, 0.f};
   {
     float acc[NTW][4] = {};
-    warp_mma<NTW>(acc, h1s, ldh, W2 + (size_t)n0 * HW, HW, HW);
+    float bias[NTW][2], w3v[NTW][2];   // requested before the MMAs
+#pragma unroll
+    for (int nt = 0; nt < NTW; ++nt)
+#pragma unroll
+      for (int u = 0; u < 2; ++u) {
+        bias[nt][u] = b2[n0 + nt * 8 + 2 * t + u];
+        w3v[nt][u] = __bfloat162float(W3[n0 + nt * 8 + 2 * t + u]);
+      }
+    stage_wait(&wbar);
+    warp_mma_ss<NTW>(acc, h1s, ldh, w2s + (size_t)n0 * (HW + SPAD), HW + SPAD, HW);
 #pragma unroll
     for (int nt = 0; nt < NTW; ++nt) {
 #pragma unroll
       for (int e = 0; e < 4; ++e) {
         const int r = g + (e >> 1) * 8, col = n0 + nt * 8 + 2 * t + (e & 1), b = r0 + r;
-        const float zz = __fadd_rn(acc[nt][e], b2[col]);
+        const float zz = __fadd_rn(acc[nt][e], bias[nt][e & 1]);
         const float h = bf16_round(fmaxf(zz, 0.f));
-        qp[e >> 1] = __fmaf_rn(h, __bfloat162float(W3[col]), qp[e >> 1]);
+        qp[e >> 1] = __fmaf_rn(h, w3v[nt][e & 1], qp[e >> 1]);
         if (store && b < B) {
           Z2[((size_t)z * B + b) * HW + col] = zz;
           Hh2[((size_t)z * B + b) * HW + col] = h;
@@ -209,6 +277,16 @@ __global__ void __launch_bounds__(256) critic_fwd_mma_kernel(
   }
 }
 
+// phase timeline of CTA (0, 0) of the last data-backward launch (diagnostics; spikerl_debug_critic_trace)
+__device__ unsigned long long g_ctrace[8];
+__device__ __forceinline__ void cstamp(int i) {
+  if (blockIdx.x == 0 && blockIdx.y == 0 && threadIdx.x == 0) {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    g_ctrace[i] = t;
+  }
+}
+
 // ------------------------------------------------------------------ data backward
 // dZ2 = round(dQ w3 [Z2 > 0]); dZ1 = round((dZ2 W2) [Z1 > 0]); grad_act = (dZ1 W1)[:, S:S+A]
 // dQ is formed here (no separate loss launch): mode 0 (critic update) dQ_z[b] = 2 (Q_z - y)/B and
@@ -223,8 +301,9 @@ __global__ void __launch_bounds__(256) critic_bwd_data_mma_kernel(
     long long P, long long tb, long long oW3, long long oW1T, long long oW2T, const float* __restrict__ Z1,
     const float* __restrict__ Z2, __nv_bfloat16* __restrict__ dZ2T, __nv_bfloat16* __restrict__ dZ1T,
     float* __restrict__ grad_act, int store_t) {
-  pdl_wait();
-  pdl_trigger();
+  extern __shared__ __align__(128) uint8_t dsm[];
+  __nv_bfloat16* const w2s = (__nv_bfloat16*)dsm;    // W2T staged: [HW][HW + SPAD]
+  __shared__ __align__(8) uint64_t wbar;
   __shared__ __align__(16) __nv_bfloat16 d2s[RB * (HW + SPAD)];
   __shared__ __align__(16) __nv_bfloat16 d1s[RB * (HW + SPAD)];
   __shared__ float dqs[RB];
@@ -232,6 +311,18 @@ __global__ void __launch_bounds__(256) critic_bwd_data_mma_kernel(
   const int z = blockIdx.y, r0 = blockIdx.x * RB, tid = threadIdx.x, warp = tid >> 5;
   const int lane = tid & 31, g = lane >> 2, t = lane & 3;
   const int ldh = HW + SPAD;
+  if (tid == 0) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_addr(&wbar)) : "memory");
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  cstamp(0);
+  pdl_wait();
+  pdl_trigger();
+  cstamp(1);
+  // W2T into shared memory while the dQ / dZ2 phase runs (trace r01: the K = 256 contraction
+  // with its B fragments fetched from L2 took 6 us of this launch's 18)
+  stage_rows(w2s, pb + blk_base(P) + z * tb + oW2T, HW, HW, &wbar);
   const __nv_bfloat16* W3 = pb + z * P + oW3;
   if (warp == 0) {
     float d = 0.f, c = 0.f;
@@ -261,11 +352,15 @@ __global__ void __launch_bounds__(256) critic_bwd_data_mma_kernel(
     }
   }
   __syncthreads();
-  for (int idx = tid; idx < RB * HW; idx += 256) {   // coalesced along j
-    const int r = idx / HW, j = idx - r * HW, b = r0 + r;
-    float d = 0.f;
-    if (b < B && Z2[((size_t)z * B + b) * HW + j] > 0.f) d = __fmul_rn(dqs[r], __bfloat162float(W3[j]));
-    d2s[r * ldh + j] = __float2bfloat16_rn(d);
+  {   // thread = column j (HW == blockDim): w3_j once, the 16 rows' Z2 loads issued together
+    static_assert(HW == 256, "one thread per hidden unit");
+    const int j = tid;
+    const float w3 = __bfloat162float(W3[j]);
+    float zz[RB];
+#pragma unroll
+    for (int r = 0; r < RB; ++r) zz[r] = (r0 + r < B) ? Z2[((size_t)z * B + r0 + r) * HW + j] : 0.f;
+#pragma unroll
+    for (int r = 0; r < RB; ++r) d2s[r * ldh + j] = __float2bfloat16_rn(zz[r] > 0.f ? __fmul_rn(dqs[r], w3) : 0.f);
   }
   if (tid == 0) {   // publish the partial; the last CTA reduces all of them in (z, block) order
     __threadfence();
@@ -284,52 +379,74 @@ __global__ void __launch_bounds__(256) critic_bwd_data_mma_kernel(
     if (last) *ticket = 0u;
   }
   __syncthreads();
+  cstamp(2);
   if (store_t) {
     for (int idx = tid; idx < RB * HW; idx += 256) {
       const int j = idx / RB, r = idx - j * RB;
       dZ2T[((size_t)z * HW + j) * Bp + r0 + r] = d2s[r * ldh + j];
     }
   }
-  const __nv_bfloat16* W2T = pb + 2 * P + z * tb + oW2T;
+  cstamp(3);
   const int n0 = warp * NTW * 8;
   {
     float acc[NTW][4] = {};
-    warp_mma<NTW>(acc, d2s, ldh, W2T + (size_t)n0 * HW, HW, HW);
+    // the ReLU masks are requested before the MMAs so their latency hides behind them
+    float z1v[NTW][4];
+#pragma unroll
+    for (int nt = 0; nt < NTW; ++nt)
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        const int r = g + (e >> 1) * 8, col = n0 + nt * 8 + 2 * t + (e & 1), b = r0 + r;
+        z1v[nt][e] = b < B ? Z1[((size_t)z * B + b) * HW + col] : 0.f;
+      }
+    stage_wait(&wbar);
+    warp_mma_ss<NTW>(acc, d2s, ldh, w2s + (size_t)n0 * ldh, ldh, HW);
 #pragma unroll
     for (int nt = 0; nt < NTW; ++nt) {
 #pragma unroll
       for (int e = 0; e < 4; ++e) {
-        const int r = g + (e >> 1) * 8, col = n0 + nt * 8 + 2 * t + (e & 1), b = r0 + r;
-        float d = 0.f;
-        if (b < B && Z1[((size_t)z * B + b) * HW + col] > 0.f) d = acc[nt][e];
-        d1s[r * ldh + col] = __float2bfloat16_rn(d);
+        const int r = g + (e >> 1) * 8, col = n0 + nt * 8 + 2 * t + (e & 1);
+        d1s[r * ldh + col] = __float2bfloat16_rn(z1v[nt][e] > 0.f ? acc[nt][e] : 0.f);
       }
     }
   }
   __syncthreads();
+  cstamp(4);
   if (store_t) {
     for (int idx = tid; idx < RB * HW; idx += 256) {
       const int j = idx / RB, r = idx - j * RB;
       dZ1T[((size_t)z * HW + j) * Bp + r0 + r] = d1s[r * ldh + j];
     }
   }
+  cstamp(5);
   if (grad_act == nullptr || z != 0) return;
-  if (warp == 0) {   // columns [S, S+A) of dZ1 W1 = dZ1 (W1T)^T, in n-tiles of 8 from S rounded down
-    const __nv_bfloat16* W1T = pb + 2 * P + oW1T;
+  // columns [S, S+A) of dZ1 W1 = dZ1 (W1T)^T in n-tiles of 8 from S rounded down, 32 at a time;
+  // each warp takes 32 of the 256 k (2 k-steps) and the partial sums meet in shared memory
+  // (trace r01: one warp walking all 16 k-steps made this tail 3 us)
+  {
+    __shared__ float gpart[NWARP][RB][32];
+    const __nv_bfloat16* W1T = pb + blk_base(P) + oW1T;
     const int c0 = S & ~7;
     for (int cb = c0; cb < S + A; cb += 32) {
       float acc[4][4] = {};
-      warp_mma<4>(acc, d1s, ldh, W1T + (size_t)cb * HW, HW, HW);
+      const int kw = warp * (HW / NWARP);
+      warp_mma<4, 2>(acc, d1s + kw, ldh, W1T + (size_t)cb * HW + kw, HW, HW / NWARP);
 #pragma unroll
-      for (int nt = 0; nt < 4; ++nt) {
+      for (int nt = 0; nt < 4; ++nt)
 #pragma unroll
-        for (int e = 0; e < 4; ++e) {
-          const int r = g + (e >> 1) * 8, col = cb + nt * 8 + 2 * t + (e & 1), b = r0 + r;
-          if (b < B && col >= S && col < S + A) grad_act[(size_t)b * A + (col - S)] = acc[nt][e];
-        }
+        for (int e = 0; e < 4; ++e) gpart[warp][g + (e >> 1) * 8][nt * 8 + 2 * t + (e & 1)] = acc[nt][e];
+      __syncthreads();
+      for (int idx = tid; idx < RB * 32; idx += 256) {
+        const int r = idx >> 5, cl = idx & 31, col = cb + cl, b = r0 + r;
+        float sum = 0.f;
+#pragma unroll
+        for (int w = 0; w < NWARP; ++w) sum = __fadd_rn(sum, gpart[w][r][cl]);
+        if (b < B && col >= S && col < S + A) grad_act[(size_t)b * A + (col - S)] = sum;
       }
+      __syncthreads();
     }
   }
+  cstamp(6);
 }
 
 // ------------------------------------------------------------------ weight gradients
@@ -407,13 +524,15 @@ __global__ void critic_refresh_kernel(const float* __restrict__ params, long lon
                                       __nv_bfloat16* __restrict__ out) {
   pdl_wait();
   pdl_trigger();
-  const long long total = 2 * P + 2 * tb;
+  const long long bb = blk_base(P), total = bb + 2 * tb;
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < total; i += (long long)gridDim.x * blockDim.x) {
     float v;
     if (i < 2 * P) {
       v = params[i];
+    } else if (i < bb) {
+      v = 0.f;   // alignment gap
     } else {
-      const long long f = i - 2 * P;
+      const long long f = i - bb;
       const int z = (int)(f / tb);
       long long e = f - z * tb;
       const float* W1 = params + z * P + oW1;
@@ -470,7 +589,7 @@ bool critic_mma_ok(const CriticDims& c) { return c.bf16 && c.H1 == HW && c.H2 ==
 size_t critic_bf16_elems(const CriticDims& c) {
   if (!critic_mma_ok(c)) return 2 * c.off[SPIKERL_CRITIC_NPARAM];
   const MmaLayout L = mma_layout(c);
-  return 2 * L.P + 2 * L.tb;
+  return blk_base(L.P) + 2 * L.tb;
 }
 
 size_t critic_mma_ws_bytes(const CriticDims& c, int B) {
@@ -501,7 +620,7 @@ int launch_critic_refresh(const CriticDims& c, const float* params2, __nv_bfloat
   ProfScope ps_("critic_refresh_bf16", PB_HBM, 0.0, 6.0 * critic_bf16_elems(c), st);
   if (!critic_mma_ok(c)) return launch_f32_to_bf16(params2, out, 2 * c.off[SPIKERL_CRITIC_NPARAM], st);
   const MmaLayout L = mma_layout(c);
-  const long long total = 2 * L.P + 2 * L.tb;
+  const long long total = blk_base(L.P) + 2 * L.tb;
   pdl(critic_refresh_kernel, (int)(cdiv(total, 256) < 1184 ? cdiv(total, 256) : 1184), 256, 0, st)(
       params2, L.P, c.in, c.H1, c.H2, L.inp, L.inq, (long long)c.off[SPIKERL_CRITIC_W1],
       (long long)c.off[SPIKERL_CRITIC_W2], L.tb, out);
@@ -522,7 +641,13 @@ int critic_mma_fwd_bwd(const CriticDims& c, int B, const float* params2, const _
   {
     ProfScope ps_("critic_fwd_mma", PB_TENSOR, 2.0 * B * nz * ((double)c.in * HW + (double)HW * HW + HW), 0.0, st);
     dim3 grid(Bp / RB, nz);
-    pdl(critic_fwd_mma_kernel, grid, 256, 0, st)(
+    static bool attr = false;
+    if (!attr) {
+      SPK_CHECK_CUDA(cudaFuncSetAttribute(critic_fwd_mma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                          (int)kW2Smem));
+      attr = true;
+    }
+    pdl(critic_fwd_mma_kernel, grid, 256, kW2Smem, st)(
         B, Bp, S, A, L.inp, L.inq, obs, act, pb, L.P, L.tb, L.W1p, L.W2c, oW3, params2,
         (long long)c.off[SPIKERL_CRITIC_B1], (long long)c.off[SPIKERL_CRITIC_B2], (long long)c.off[SPIKERL_CRITIC_B3],
         w.XT, w.H1T, w.Z1, w.Z2, w.Hh2, q, need_bwd ? 1 : 0, need_bwd ? w.ticket : nullptr);
@@ -542,7 +667,13 @@ int critic_mma_fwd_bwd(const CriticDims& c, int B, const float* params2, const _
   {
     ProfScope ps_("critic_bwd_data_mma", PB_TENSOR, 2.0 * B * nb * ((double)HW * HW), 0.0, st);
     dim3 grid(Bp / RB, nb);
-    pdl(critic_bwd_data_mma_kernel, grid, 256, 0, st)(
+    static bool attr = false;
+    if (!attr) {
+      SPK_CHECK_CUDA(cudaFuncSetAttribute(critic_bwd_data_mma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                          (int)kW2Smem));
+      attr = true;
+    }
+    pdl(critic_bwd_data_mma_kernel, grid, 256, kW2Smem, st)(
         B, Bp, S, A, L.inp, q, y, mode, act_scale, w.dq, w.part, w.ticket, fused_scalar ? loss : nullptr, pb, L.P, L.tb,
         oW3, L.W1T, L.W2T, w.Z1, w.Z2, w.dZ2T, w.dZ1T, grad_act, want_params ? 1 : 0);
     SPK_LAUNCHED();
@@ -571,3 +702,8 @@ int critic_mma_fwd_bwd(const CriticDims& c, int B, const float* params2, const _
 }
 
 }  // namespace spk
+
+extern "C" int spikerl_debug_critic_trace(unsigned long long* host8) {
+  if (cudaMemcpyFromSymbol(host8, spk::g_ctrace, sizeof(unsigned long long) * 8) != cudaSuccess) return 5;
+  return 0;
+}

@@ -96,7 +96,7 @@ __device__ __forceinline__ void store_views(const Bf16Views& v, size_t e, float 
   if (v.kind != 2) return;
   const uint32_t z = fdiv((uint32_t)e, v.Pd);
   const long long l = (long long)e - (long long)z * v.P;
-  __nv_bfloat16* blk = v.out + 2 * v.P + z * v.tb;
+  __nv_bfloat16* blk = v.out + ((2 * v.P + 7) & ~7LL) + z * v.tb;   // blk_base (k_critic_mma.cu)
   long long r = l - v.oW1;
   if (r >= 0 && r < (long long)v.H1 * v.in) {          // W1[j][i] -> W1p[j][i], W1T[i][j]
     const uint32_t j = fdiv((uint32_t)r, v.ind), i = (uint32_t)r - j * (uint32_t)v.in;
