@@ -76,6 +76,8 @@ class ClockSampler:
             self.nvml = None
 
     def start(self):
+        self.e0 = self._energy_mj()
+        self.t0 = time.time()
         if self.nvml is not None:
             self.samples, self.reasons, self.stop_flag = [], 0, False
             nv = self.nvml
@@ -121,6 +123,21 @@ class ClockSampler:
     def _read(self):
         for line in self.proc.stdout:
             self.lines.append(line.strip())
+
+    def _energy_mj(self):
+        try:
+            return self.nvml.nvmlDeviceGetTotalEnergyConsumption(self.h) if self.nvml is not None else None
+        except Exception:
+            return None
+
+    def energy(self):
+        """GPU energy over the sampled window (NVML total-energy counter, mJ; PAPER.md GPS-UP context)."""
+        e1, t1 = self._energy_mj(), time.time()
+        if self.e0 is None or e1 is None:
+            return None
+        j = (e1 - self.e0) / 1e3
+        return {"joules": round(j, 4), "seconds": round(t1 - self.t0, 4),
+                "avg_watts": round(j / max(t1 - self.t0, 1e-9), 1), "source": "nvml total energy counter"}
 
     def stop(self):
         if self.nvml is not None:
@@ -328,6 +345,7 @@ def run_td3(args, rank, world):
     clk = ClockSampler(int(os.environ.get("LOCAL_RANK", "0")))
     clk.start()
     total_ms = time_steps(graph_step, args.steps, flush, world)
+    energy = clk.energy()
     clocks = clk.stop()
     gpu_launches = sum(launches[(step0[0] + k) % 2] for k in range(args.steps))
     step0[0] += args.steps
@@ -346,6 +364,9 @@ def run_td3(args, rank, world):
                       "l2": "flushed between timed steps (256 MB read, outside the events)" if flush is not None
                       else "not flushed", "cuda_graph": True},
            "clocks": clocks, "gpu_launches": int(gpu_launches)}
+    if energy:   # rank 0's GPU; the window includes the L2 flushes between timed steps
+        energy["joules_per_update"] = round(energy["joules"] / args.steps, 6)
+        out["energy"] = energy
     # e2e: minibatch from pinned host memory every step + loss read-back, through the public API
     if not args.no_e2e:
         out["e2e"] = e2e_td3(args, rank, world, td3, shape, B)
@@ -432,6 +453,7 @@ def run_actor(args, rank, world):
     clk = ClockSampler(int(os.environ.get("LOCAL_RANK", "0")))
     clk.start()
     total_ms = time_steps(step, args.steps, None, world)
+    energy = clk.energy()
     clocks = clk.stop()
     n_launch = lib.spikerl_launch_count(1)
     secs = total_ms / 1e3
@@ -444,6 +466,10 @@ def run_actor(args, rank, world):
                       "parallelism": f"dp{world}", "engine": args.engine,
                       "l2": "inputs and tape (GBs) exceed L2"},
            "clocks": clocks, "gpu_launches": int(n_launch)}
+    if energy:
+        energy["joules_per_step"] = round(energy["joules"] / args.steps, 5)
+        energy["samples_per_joule"] = round(args.steps * B / max(energy["joules"], 1e-9), 1)
+        out["energy"] = energy
     _lib.prof_enable(True)
     step(0)
     torch.cuda.synchronize()

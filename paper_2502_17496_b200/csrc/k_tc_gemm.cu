@@ -1102,8 +1102,11 @@ int launch_enc_grad_tc(const ActorDims& d, int B, const void* Gsum, const __nv_b
   return launch_enc_grad_reduce(d, 2 * p.n_tiles, partial, dmu, dsigma, accumulate, st);
 }
 
-// split-K plan for dW_l: at least two waves of units, splits chosen to minimise the idle tail of
-// the last wave (persistent grid = #SMs); never an empty split.
+// split-K plan for dW_l: pick the split count s minimising a simple cost model in units of one
+// k-block of MMAs: waves(s) x (k-blocks per unit + dump) + the fixed-order reduction of the s
+// partial tiles spread over the GPU. A unit's epilogue (dumping a 256 x 512 fp32 partial tile) costs
+// about 8 k-blocks and is not overlapped for pair units (single TMEM buffer). (The previous
+// wave-efficiency-only rule chose 320 one-k-block units for dW3 at configs[3] B = 4096: 278 us.)
 static int dw_cg(const ActorDims& d, int l) { return (pairs_enabled() && (d.P[l] / BM) % 2 == 0) ? 2 : 1; }
 
 void tc_dw_plan(const ActorDims& d, int l, int B, int* splits, int* kps) {
@@ -1111,18 +1114,18 @@ void tc_dw_plan(const ActorDims& d, int l, int B, int* splits, int* kps) {
   const int m_tiles = d.P[l] / BM / cg, n_tiles = cdiv(d.P[l - 1], dw_unit_cols(cg));
   const int k_blocks = cdiv((long long)d.T * B, BK);
   const long long mn = (long long)m_tiles * n_tiles;
-  const int sms = cg == 2 ? pair_slots() : num_sms();   // concurrent units (CTA pairs when cg = 2)
-  int s_lo = (int)cdiv(2LL * sms, mn);
-  if (s_lo < 1) s_lo = 1;
-  int best_s = s_lo;
-  double best_eff = -1.0;
-  for (int s = s_lo; s <= 4 * s_lo && s <= k_blocks; ++s) {
+  const int slots = cg == 2 ? pair_slots() : num_sms();   // concurrent units (CTA pairs when cg = 2)
+  constexpr double kDump = 8.0;
+  int best_s = 1;
+  double best = 1e300;
+  const int s_max = k_blocks < 8 * slots ? k_blocks : 8 * slots;
+  for (int s = 1; s <= s_max; ++s) {
     const int per = cdiv(k_blocks, s), ss = cdiv(k_blocks, per);
+    if (ss != s) continue;   // the same partition as a smaller s
     const long long units = mn * ss;
-    const double eff = (double)units / ((double)cdiv(units, sms) * sms);
-    if (eff > best_eff + 1e-3) { best_eff = eff; best_s = s; }
+    const double cost = (double)cdiv(units, slots) * (per + kDump) + (double)units * kDump / slots;
+    if (cost < best - 1e-9) { best = cost; best_s = s; }
   }
-  if (best_s > k_blocks) best_s = k_blocks;
   const int per = cdiv(k_blocks, best_s);
   *kps = per;
   *splits = cdiv(k_blocks, per);
