@@ -76,8 +76,6 @@ class ClockSampler:
             self.nvml = None
 
     def start(self):
-        self.e0 = self._energy_mj()
-        self.t0 = time.time()
         if self.nvml is not None:
             self.samples, self.reasons, self.stop_flag = [], 0, False
             nv = self.nvml
@@ -129,15 +127,6 @@ class ClockSampler:
             return self.nvml.nvmlDeviceGetTotalEnergyConsumption(self.h) if self.nvml is not None else None
         except Exception:
             return None
-
-    def energy(self):
-        """GPU energy over the sampled window (NVML total-energy counter, mJ; PAPER.md GPS-UP context)."""
-        e1, t1 = self._energy_mj(), time.time()
-        if self.e0 is None or e1 is None:
-            return None
-        j = (e1 - self.e0) / 1e3
-        return {"joules": round(j, 4), "seconds": round(t1 - self.t0, 4),
-                "avg_watts": round(j / max(t1 - self.t0, 1e-9), 1), "source": "nvml total energy counter"}
 
     def stop(self):
         if self.nvml is not None:
@@ -221,6 +210,29 @@ def l2_flush(buf):
     dirty lines whose write-back the next timed kernel pays for)."""
     import torch
     torch.sum(buf)
+
+
+def energy_window(run_step, sampler, seconds=1.5):
+    """GPU energy per step (NVML total-energy counter, mJ; it updates too coarsely for the short timed
+    region): steps run back to back for >= `seconds` after the timed region, energy difference over
+    that window / steps. PAPER.md §IV-B GPS-UP context (B200 side only)."""
+    import torch
+    torch.cuda.synchronize()
+    e0 = sampler._energy_mj()
+    if e0 is None:
+        return None
+    t0 = time.time()
+    n = 0
+    while time.time() - t0 < seconds or n < 3:
+        run_step(n)
+        n += 1
+        if n % 16 == 0:
+            torch.cuda.synchronize()
+    torch.cuda.synchronize()
+    dt, e1 = time.time() - t0, sampler._energy_mj()
+    j = (e1 - e0) / 1e3
+    return {"joules": round(j, 3), "steps": n, "seconds": round(dt, 3), "avg_watts": round(j / dt, 1),
+            "source": "nvml total energy counter, steps back to back after the timed region"}
 
 
 def time_steps(run_step, K, flush_buf, world):
@@ -345,10 +357,8 @@ def run_td3(args, rank, world):
     clk = ClockSampler(int(os.environ.get("LOCAL_RANK", "0")))
     clk.start()
     total_ms = time_steps(graph_step, args.steps, flush, world)
-    energy = clk.energy()
     clocks = clk.stop()
     gpu_launches = sum(launches[(step0[0] + k) % 2] for k in range(args.steps))
-    step0[0] += args.steps
     secs = total_ms / 1e3
     value = args.steps * B * world / secs
     out = {"metric": METRIC, "value": round(value, 2), "unit": "samples/s", "n_gpus": world, "steps": args.steps,
@@ -364,9 +374,13 @@ def run_td3(args, rank, world):
                       "l2": "flushed between timed steps (256 MB read, outside the events)" if flush is not None
                       else "not flushed", "cuda_graph": True},
            "clocks": clocks, "gpu_launches": int(gpu_launches)}
-    if energy:   # rank 0's GPU; the window includes the L2 flushes between timed steps
-        energy["joules_per_update"] = round(energy["joules"] / args.steps, 6)
-        out["energy"] = energy
+    step0[0] += args.steps
+    en = energy_window(lambda k: td3.replay_graph(step0[0] + k), clk)
+    if en:
+        step0[0] += en["steps"]
+        en["joules_per_update"] = round(en["joules"] / en["steps"], 6)
+        en["samples_per_joule"] = round(en["steps"] * B / max(en["joules"], 1e-9), 1)
+        out["energy"] = en
     # e2e: minibatch from pinned host memory every step + loss read-back, through the public API
     if not args.no_e2e:
         out["e2e"] = e2e_td3(args, rank, world, td3, shape, B)
@@ -453,7 +467,6 @@ def run_actor(args, rank, world):
     clk = ClockSampler(int(os.environ.get("LOCAL_RANK", "0")))
     clk.start()
     total_ms = time_steps(step, args.steps, None, world)
-    energy = clk.energy()
     clocks = clk.stop()
     n_launch = lib.spikerl_launch_count(1)
     secs = total_ms / 1e3
@@ -466,10 +479,11 @@ def run_actor(args, rank, world):
                       "parallelism": f"dp{world}", "engine": args.engine,
                       "l2": "inputs and tape (GBs) exceed L2"},
            "clocks": clocks, "gpu_launches": int(n_launch)}
-    if energy:
-        energy["joules_per_step"] = round(energy["joules"] / args.steps, 5)
-        energy["samples_per_joule"] = round(args.steps * B / max(energy["joules"], 1e-9), 1)
-        out["energy"] = energy
+    en = energy_window(step, clk)
+    if en:
+        en["joules_per_step"] = round(en["joules"] / en["steps"], 5)
+        en["samples_per_joule"] = round(en["steps"] * Bg / max(en["joules"], 1e-9), 1)
+        out["energy"] = en
     _lib.prof_enable(True)
     step(0)
     torch.cuda.synchronize()
