@@ -136,7 +136,12 @@ struct MmaWs {
   float *Z1, *Z2, *Hh2, *q, *dq;           // [2][B][H] x3, [2][B] x2
   float* part;                             // [2][Bp/RB] loss partials
   unsigned int* ticket;
+  float* wpart;                            // [splits][2][HW*HW + HW*inq] split-K weight-gradient partials
 };
+
+// Large batches: the weight-gradient GEMMs (K = batch) run as 64 x 128 tiles split over K (the
+// 16 x 256 row tiles re-read the whole B operand per 16 rows: 137 us at configs[3] B = 4096).
+inline int wgrad_splits(int B) { return B <= 512 ? 0 : (B >= 2048 ? 4 : 2); }   // 0 = small-batch kernel
 
 MmaWs mma_carve(const CriticDims& c, int B, void* base, size_t* total) {
   const MmaLayout L = mma_layout(c);
@@ -145,7 +150,9 @@ MmaWs mma_carve(const CriticDims& c, int B, void* base, size_t* total) {
   char* p = (char*)base;
   size_t off = 0;
   auto take = [&](size_t bytes) { char* r = p ? p + off : nullptr; off += align_up(bytes, 256); return r; };
-  w.XT = (__nv_bfloat16*)take(2 * (size_t)L.inq * Bp);
+  // (rows up to a multiple of 64: the split weight-gradient kernel's last 64-column warp may read
+  // past inq; those rows are never written and only feed columns that are never stored)
+  w.XT = (__nv_bfloat16*)take(2 * (size_t)round_up(L.inq, 64) * Bp);
   w.H1T = (__nv_bfloat16*)take(2 * 2 * (size_t)c.H1 * Bp);
   w.dZ2T = (__nv_bfloat16*)take(2 * 2 * (size_t)c.H2 * Bp);
   w.dZ1T = (__nv_bfloat16*)take(2 * 2 * (size_t)c.H1 * Bp);
@@ -156,6 +163,8 @@ MmaWs mma_carve(const CriticDims& c, int B, void* base, size_t* total) {
   w.dq = (float*)take(4 * 2 * (size_t)B);
   w.part = (float*)take(4 * 2 * (Bp / RB));
   w.ticket = (unsigned int*)take(4);
+  const int ws = wgrad_splits(B);
+  w.wpart = (float*)take(ws > 1 ? sizeof(float) * ws * 2 * ((size_t)HW * HW + (size_t)HW * L.inq) : 0);
   if (total) *total = off;
   return w;
 }
@@ -483,6 +492,64 @@ __global__ void __launch_bounds__(256) critic_wgrad_mma_kernel(
   }
 }
 
+// Large-batch weight gradients: blockIdx.x = (matrix, 64-row block, 128-column block) flattened,
+// blockIdx.y = K split, blockIdx.z = critic. Warp w: rows 16 (w & 3) of the block, 64 columns
+// (w >> 2). K split s covers batch rows [s Kc, (s+1) Kc). With one split the tile goes straight to
+// the fp32 master layout; otherwise to wpart[s] (reduced in a fixed order by the next kernel).
+__global__ void __launch_bounds__(256) critic_wgrad_split_kernel(
+    int Bp, int in, int inq, int Kc, long long P, long long oW1, long long oW2, const __nv_bfloat16* __restrict__ XT,
+    const __nv_bfloat16* __restrict__ H1T, const __nv_bfloat16* __restrict__ dZ2T,
+    const __nv_bfloat16* __restrict__ dZ1T, float* __restrict__ grad2, float* __restrict__ wpart) {
+  pdl_wait();
+  pdl_trigger();
+  const int z = blockIdx.z, ks = blockIdx.y, warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31, g = lane >> 2, t = lane & 3;
+  const int cb2 = HW / 128, cb1 = (inq + 127) / 128;   // column blocks of dW2, dW1
+  int blk = blockIdx.x;
+  const bool w2 = blk < (HW / 64) * cb2;
+  if (!w2) blk -= (HW / 64) * cb2;
+  const int cb = w2 ? cb2 : cb1;
+  const int m0 = (blk / cb) * 64 + 16 * (warp & 3), n0 = (blk % cb) * 128 + 64 * (warp >> 2);
+  const int ncols = w2 ? HW : in;
+  const int k0 = ks * Kc;
+  const __nv_bfloat16* Am = (w2 ? dZ2T : dZ1T) + ((size_t)z * HW + m0) * Bp + k0;
+  const __nv_bfloat16* Bm = (w2 ? H1T + (size_t)z * HW * Bp : XT) + (size_t)n0 * Bp + k0;
+  if (!w2 && n0 >= inq) return;   // (inq is a multiple of 32 >= in; XT rows past in are zero)
+  float acc[8][4] = {};
+  warp_mma<8, 2>(acc, Am, Bp, Bm, Bp, min(Kc, Bp - k0));   // the last split may be shorter
+  const size_t msz = (size_t)HW * HW + (size_t)HW * inq;
+  float* dst = gridDim.y == 1 ? grad2 + z * P + (w2 ? oW2 : oW1)
+                              : wpart + ((size_t)ks * 2 + z) * msz + (w2 ? 0 : (size_t)HW * HW);
+  const int ld = gridDim.y == 1 ? ncols : (w2 ? HW : inq);
+#pragma unroll
+  for (int nt = 0; nt < 8; ++nt)
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      const int r = m0 + g + (e >> 1) * 8, col = n0 + nt * 8 + 2 * t + (e & 1);
+      if (col < (gridDim.y == 1 ? ncols : ld)) dst[(size_t)r * ld + col] = acc[nt][e];
+    }
+}
+
+// grad2[z][W] = sum over splits (fixed order) of the partial tiles (true widths only)
+__global__ void critic_wgrad_reduce_kernel(int splits, int in, int inq, long long P, long long oW1, long long oW2,
+                                           const float* __restrict__ wpart, float* __restrict__ grad2) {
+  pdl_wait();
+  pdl_trigger();
+  const size_t msz = (size_t)HW * HW + (size_t)HW * inq;
+  const long long n2 = (long long)HW * HW, n1 = (long long)HW * in, per = n2 + n1;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < 2 * per; i += (long long)gridDim.x * blockDim.x) {
+    const int z = (int)(i / per);
+    const long long e = i - z * per;
+    size_t src;
+    float* dst;
+    if (e < n2) { src = (size_t)e; dst = grad2 + z * P + oW2 + e; }
+    else { const long long f = e - n2, r = f / in, c = f - r * in; src = (size_t)n2 + r * inq + c; dst = grad2 + z * P + oW1 + f; }
+    float sum = 0.f;
+    for (int s = 0; s < splits; ++s) sum = __fadd_rn(sum, wpart[((size_t)s * 2 + z) * msz + src]);
+    *dst = sum;
+  }
+}
+
 // db1 = rowsum dZ1T, db2 = rowsum dZ2T, dW3 = dQ^T H2, db3 = sum dQ: one warp per output
 __global__ void __launch_bounds__(256) critic_bias_grads_kernel(int B, int Bp, long long P, long long oB1,
                                                                 long long oB2, long long oW3, long long oB3,
@@ -690,11 +757,27 @@ int critic_mma_fwd_bwd(const CriticDims& c, int B, const float* params2, const _
     SPK_LAUNCHED();
     {
       ProfScope ps_("critic_wgrad_mma", PB_TENSOR, 2.0 * B * nz * ((double)HW * HW + (double)HW * c.in), 0.0, st);
-      dim3 grid(cdiv(L.inq > HW ? L.inq : HW, 256), 2 * (HW / RB), nz);
-      pdl(critic_wgrad_mma_kernel, grid, 256, 0, st)(Bp, c.in, L.inq, L.P, (long long)c.off[SPIKERL_CRITIC_W1],
-                                                    (long long)c.off[SPIKERL_CRITIC_W2], w.XT, w.H1T, w.dZ2T, w.dZ1T,
-                                                    grad2);
-      SPK_LAUNCHED();
+      const int ws = wgrad_splits(B);
+      if (ws == 0) {
+        dim3 grid(cdiv(L.inq > HW ? L.inq : HW, 256), 2 * (HW / RB), nz);
+        pdl(critic_wgrad_mma_kernel, grid, 256, 0, st)(Bp, c.in, L.inq, L.P, (long long)c.off[SPIKERL_CRITIC_W1],
+                                                      (long long)c.off[SPIKERL_CRITIC_W2], w.XT, w.H1T, w.dZ2T, w.dZ1T,
+                                                      grad2);
+        SPK_LAUNCHED();
+      } else {
+        // K split in multiples of 16 batch rows (Bp is a multiple of RB = 16)
+        const int kc = round_up(cdiv(Bp, ws), 16), splits = cdiv(Bp, kc);
+        const int blocks = (HW / 64) * (HW / 128) + (HW / 64) * cdiv(L.inq, 128);
+        pdl(critic_wgrad_split_kernel, dim3(blocks, splits, nz), 256, 0, st)(
+            Bp, c.in, L.inq, kc, L.P, (long long)c.off[SPIKERL_CRITIC_W1], (long long)c.off[SPIKERL_CRITIC_W2], w.XT,
+            w.H1T, w.dZ2T, w.dZ1T, grad2, w.wpart);
+        SPK_LAUNCHED();
+        if (splits > 1) {
+          pdl(critic_wgrad_reduce_kernel, 148 * 4, 256, 0, st)(splits, c.in, L.inq, L.P, (long long)c.off[SPIKERL_CRITIC_W1],
+                                                             (long long)c.off[SPIKERL_CRITIC_W2], w.wpart, grad2);
+          SPK_LAUNCHED();
+        }
+      }
     }
     SPK_TRY(stream_after(st, sb, aux->ev[17]));
   }

@@ -277,7 +277,8 @@ def test_forward_deterministic_and_accumulate():
 
 # ------------------------------------------------------------------ critic
 @pytest.mark.parametrize("prec,B,S,A", [("fp32", 100, 17, 6), ("bf16", 256, 17, 6), ("bf16", 4096, 17, 6),
-                                        ("bf16", 100, 376, 17), ("bf16", 512, 111, 8), ("bf16", 37, 17, 6)])
+                                        ("bf16", 100, 376, 17), ("bf16", 512, 111, 8), ("bf16", 37, 17, 6),
+                                        ("bf16", 1040, 376, 17), ("bf16", 4096, 376, 17)])
 def test_critic_parity(prec, B, S, A):
     import torch
     import paper_2502_17496_b200 as pk
