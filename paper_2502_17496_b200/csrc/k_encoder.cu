@@ -13,7 +13,8 @@ namespace spk {
 
 // TT > 0: T == TT known at compile time (T <= 32), the time loop fully unrolled: per step one
 // FADD, FSETP, predicated FADD, VOTE and a lane select (ncu r01: the runtime-T loop cost 14
-// instructions per step and 59% of the kernel). TT == 0: any T, in chunks of 32 steps.
+// instructions per step and 59% of the kernel; a lane-0 shared-memory variant measured slower).
+// TT == 0: any T, in chunks of 32 steps.
 template <int TT>
 __global__ void __launch_bounds__(256) enc_fwd_kernel(int B, int S, int E, int K0, int W0, int T,
                                                       const float* __restrict__ obs,
@@ -31,11 +32,18 @@ __global__ void __launch_bounds__(256) enc_fwd_kernel(int B, int S, int E, int K
   const double m = kv ? (double)__ldg(mu + k) : 0.0;
   const double sg = kv ? (double)__ldg(sigma + k) : 1.0;
   const double den = __dmul_rn(2.0, __dmul_rn(sg, sg));
-  const size_t wk = (size_t)(k >> 5);
+  // q / den as a correctly rounded quotient from the hoisted correctly rounded reciprocal:
+  // q0 = RN(q inv) is within one ulp, r = q - den q0 is exact (FMA), RN(q0 + r inv) = RN(q / den)
+  // (Markstein). Same value as __ddiv_rn(q, den) (the bit-exact encoder tests pin it against the
+  // oracle's IEEE division) at 3 instead of ~12 double operations per element.
+  const double inv = __ddiv_rn(1.0, den);
   const size_t tstride = (size_t)B * W0;
+  const size_t arow = (size_t)gridDim.x * K0, brow = (size_t)gridDim.x * W0;   // per-iteration strides
   int b = blockIdx.x;
+  float* ap = A_out + (size_t)b * K0 + k;
+  uint32_t* out = bits0 + (size_t)b * W0 + (k >> 5) + (size_t)lane * tstride;
   float s_next = (kv && b < B) ? __ldg(obs + (size_t)b * S + i) : 0.f;
-  for (; b < B; b += gridDim.x) {
+  for (; b < B; b += gridDim.x, ap += arow, out += brow) {
     const float s = s_next;
     const int bn = b + gridDim.x;
     if (kv && bn < B) s_next = __ldg(obs + (size_t)bn * S + i);
@@ -43,11 +51,12 @@ __global__ void __launch_bounds__(256) enc_fwd_kernel(int B, int S, int E, int K
     if (kv) {
       const double dd = __dsub_rn((double)s, m);
       const double q = __dmul_rn(dd, dd);
-      A = (float)exp(-__ddiv_rn(q, den));  // RNE double -> float
-      A_out[(size_t)b * K0 + k] = A;
+      const double q0 = __dmul_rn(q, inv);
+      const double r = __fma_rn(-q0, den, q);
+      A = (float)exp(-__fma_rn(r, inv, q0));  // RNE double -> float
+      *ap = A;
     }
     float acc = 0.0f;
-    uint32_t* out = bits0 + (size_t)b * W0 + wk + (size_t)lane * tstride;
     if constexpr (TT > 0) {
       // lane t keeps the ballot word of timestep t; one store instruction for all T words
       uint32_t mine = 0;

@@ -51,6 +51,21 @@ def test_encoder_edge_values():
     assert check_encoder(gpu, shape, p, s) == 0
 
 
+def test_encoder_quotient_stress():
+    """A = RN32(exp(-(s-mu)^2 / (2 sigma^2))) bit-exact over a wide spread of sigma (log-uniform
+    1e-3..30, learnable: DESIGN.md R12) and s (N(0, 3^2)): pins the kernel's reciprocal-based
+    correctly rounded quotient against the oracle's IEEE division."""
+    shape = sg.ActorShape(3, 2, pop_enc=64, pop_dec=4, n1=32, n2=32, T=16, precision="bf16")
+    rng = np.random.default_rng(11)
+    p = sg.actor_params(shape, rng)
+    p["sigma"] = np.exp(rng.uniform(np.log(1e-3), np.log(30.0), p["sigma"].shape)).astype(np.float32)
+    p["mu"] = rng.normal(0, 3, p["mu"].shape).astype(np.float32)
+    s = rng.normal(0, 3, (2048, 3)).astype(np.float32)
+    gpu = run_gpu_actor(shape, 2048, p, s, None, engine="simt")
+    from tests._parity import check_encoder
+    assert check_encoder(gpu, shape, p, s) == 0
+
+
 @pytest.mark.parametrize("T", [7, 32, 33, 70])
 def test_encoder_timesteps(T):
     """Unrolled (T in the compiled set) and runtime-T (chunks of 32 steps) encoder variants."""
