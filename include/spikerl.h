@@ -131,9 +131,10 @@ size_t spikerl_td3_workspace_bytes(const spikerl_actor_cfg* acfg, const spikerl_
  *   mask_l u32  [T][B][Pl/32]  surrogate window bits [|v - v_th| < window], layer l = 1..3
  *   counts u8   [B][N3]        output spike counts
  *   act    fp32 [B][A]         decoded actions (for the decoder backward)
- *   bitsT_l, maskT_l u8 [ceil32(B)/8][P_l][tpad]  (tcgen05 engine, l = 1, 2; else offset 0)
- *                              octet-major copies of the hidden planes: bit j of byte
- *                              (o, n, t) is batch row 8o + j (read by the fused dX epilogue) */
+ *   bitsT_l, maskT_l u8 [ceil32(B)/4][P_l][tpad/2]  (tcgen05 engine, l = 1, 2; else offset 0)
+ *                              quad-major copies of the hidden planes: one little-endian u64 per
+ *                              16 steps, bit 4 (t mod 16) + j of word (q, n, t / 16) is batch row
+ *                              4q + j at step t (read by the fused dX epilogue) */
 typedef struct {
   size_t A, bits[4], mask[4], counts, act, total;
   int padded[4];           /* P0..P3                                                        */

@@ -178,9 +178,13 @@ class SpikingActor:
                 out[f"mask{l}"] = seg(lay.mask[l], 4 * T * B * W, torch.int32, (T, B, W))
             if l and lay.bitsT[l]:
                 P = lay.padded[l]
-                O = (B + 31) // 32 * 4
-                out[f"bitsT{l}"] = seg(lay.bitsT[l], O * P * lay.tpad, torch.uint8, (O, P, lay.tpad))
-                out[f"maskT{l}"] = seg(lay.maskT[l], O * P * lay.tpad, torch.uint8, (O, P, lay.tpad))
+                Q = (B + 31) // 32 * 8          # batch quads
+                nb = Q * P * (lay.tpad // 2)
+                out[f"bitsT{l}"] = seg(lay.bitsT[l], nb, torch.uint8, (Q, P, lay.tpad // 2))
+                out[f"maskT{l}"] = seg(lay.maskT[l], nb, torch.uint8, (Q, P, lay.tpad // 2))
+                # the tcgen05 engine keeps the hidden layers' window bits only quad-major (the
+                # dX epilogue's input); this diagnostic view re-packs them batch-major
+                out[f"mask{l}"] = _quads_to_words(out[f"maskT{l}"], T, B)
         out["counts"] = seg(lay.counts, B * N3, torch.uint8, (B, N3))
         out["act"] = seg(lay.act, 4 * B * cfg.act_dim, torch.float32, (B, cfg.act_dim))
         return out
@@ -193,6 +197,18 @@ class SpikingActor:
         o = {f"o{l}": unpack_bits(v[f"bits{l}"], N[l]) for l in range(4)}
         o.update({f"h{l}": unpack_bits(v[f"mask{l}"], N[l]) for l in (1, 2, 3)})
         return o
+
+
+def _quads_to_words(qt, T, B):
+    """Diagnostics only (tape views for tests): quad-major bytes [Q][P][Tpad/2] (nibble s of a
+    (quad, neuron) row = its 4 batch rows at step s) -> batch-major int32 words [T][B][P/32]."""
+    Q, P, half = qt.shape
+    sh = torch.arange(8, device=qt.device, dtype=torch.uint8)
+    bits = (qt.unsqueeze(-1) >> sh) & 1                               # [Q][P][Tpad/2][8]
+    bits = bits.reshape(Q, P, 2 * half, 4).permute(2, 0, 3, 1)        # [Tpad][Q][4][P]
+    bits = bits.reshape(2 * half, 4 * Q, P)[:T, :B].to(torch.int64)   # [T][B][P]
+    w = (bits.reshape(T, B, P // 32, 32) << torch.arange(32, device=qt.device)).sum(-1)
+    return torch.where(w >= 2 ** 31, w - 2 ** 32, w).to(torch.int32)
 
 
 # ------------------------------------------------------------------------------------ critic

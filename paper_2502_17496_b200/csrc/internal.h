@@ -1,5 +1,6 @@
 // internal.h — launchers shared between the ABI layer and the kernel files.
 #pragma once
+#include <cuda.h>
 #include "common.cuh"
 
 namespace spk {
@@ -57,7 +58,10 @@ int launch_enc_grad_tc(const ActorDims& d, int B, const void* Gsum, const __nv_b
 int launch_lif_dw_tc(const ActorDims& d, int l, int B, const void* Gl, const uint32_t* bits_prev,
                      float* dW, float* part, int accumulate, cudaStream_t st);
 size_t tc_enc_partial_bytes(const ActorDims& d, int B);
-size_t tc_dw_partial_bytes(const ActorDims& d, int B, int l);   // split-K partials of dW_l
+size_t tc_dw_partial_bytes(const ActorDims& d, int B, int l);
+// 3-D u32 tensor map (dims / box innermost first, strides in bytes), no swizzle, OOB zero fill
+int make_u32_map3(CUtensorMap* m, const void* base, const uint64_t* dims, const uint64_t* strides,
+                  const uint32_t* box);   // split-K partials of dW_l
 int launch_enc_grad_reduce(const ActorDims& d, int nchunk, const float* partial, float* dmu,
                            float* dsigma, int accumulate, cudaStream_t st);
 

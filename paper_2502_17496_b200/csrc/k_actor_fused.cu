@@ -10,7 +10,7 @@
 // all T steps of its (b, neuron) accumulators: the LIF scan never leaves registers. The slice of
 // spikes is then pushed to the 3 peer CTAs with bulk DSMEM copies (cp.async.bulk ... shared::cluster)
 // completing on the peers' mbarriers, so the next layer reads the whole spike operand from local
-// shared memory. The tape written is exactly the tcgen05 engine's (A, bit / mask planes, octet-major
+// shared memory. The tape written is exactly the tcgen05 engine's (A, bit / mask planes, quad-major
 // copies, counts, actions), so the backward is unchanged.
 #include "internal.h"
 
@@ -239,26 +239,27 @@ __device__ __forceinline__ void pack_planes(const Params& p, int l, int c, int q
   }
 }
 
-// octet-major copies of this CTA's neurons (layers 1, 2; read by the tcgen05 DX epilogue)
-__device__ __forceinline__ void pack_octets(const Params& p, int l, int c, int q, const uint8_t* flags, int tid) {
+// quad-major copies of this CTA's neurons (layers 1, 2; read by the tcgen05 DX epilogue): one
+// 64-bit word per (batch quad, neuron), nibble t = the quad's bits at step t (T <= 16)
+__device__ __forceinline__ void pack_quads(const Params& p, int l, int c, int q, const uint8_t* flags, int tid) {
   const int S = slice(p, l);
-  if (tid >= 2 * S) return;
-  const int nl = tid % S, oct = tid / S, n = c * S + nl;
-  uint32_t wo[4] = {0u, 0u, 0u, 0u}, wh[4] = {0u, 0u, 0u, 0u};
+  if (tid >= 4 * S) return;
+  const int nl = tid % S, qd = tid / S, n = c * S + nl;
+  unsigned long long wo = 0ull, wh = 0ull;
   for (int t = 0; t < p.T; ++t) {
     uint32_t bo = 0, bh = 0;
 #pragma unroll
-    for (int j = 0; j < 8; ++j) {
-      const uint32_t f = flags[(t * RB + 8 * oct + j) * S + nl];
+    for (int j = 0; j < 4; ++j) {
+      const uint32_t f = flags[(t * RB + 4 * qd + j) * S + nl];
       bo |= (f & 1u) << j;
       bh |= ((f >> 1) & 1u) << j;
     }
-    wo[t >> 2] |= bo << (8 * (t & 3));
-    wh[t >> 2] |= bh << (8 * (t & 3));
+    wo |= (unsigned long long)bo << (4 * t);
+    wh |= (unsigned long long)bh << (4 * t);
   }
-  const size_t off = ((size_t)(2 * q + oct) * p.P[l] + n) * p.tpad;
-  *reinterpret_cast<uint4*>(p.bitsT[l] + off) = make_uint4(wo[0], wo[1], wo[2], wo[3]);
-  *reinterpret_cast<uint4*>(p.maskT[l] + off) = make_uint4(wh[0], wh[1], wh[2], wh[3]);
+  const size_t off = ((size_t)(4 * q + qd) * p.P[l] + n) * (p.tpad >> 1);
+  *reinterpret_cast<unsigned long long*>(p.bitsT[l] + off) = wo;
+  *reinterpret_cast<unsigned long long*>(p.maskT[l] + off) = wh;
 }
 
 template <int TT>
@@ -351,7 +352,7 @@ __global__ void __launch_bounds__(NTH, 1) actor_fwd_fused_kernel(const __grid_co
     fstamp(3 + 3 * li);
     const bool own = li <= 2 && !repl(p, li);   // words from this CTA's own flags: pack while copies fly
     if (own) pack_planes(p, li, c, q, sm + L.flags[li], warp, lane);
-    if (li == 1 || li == 2) pack_octets(p, li, c, q, flags_of(li, c), tid);
+    if (li == 1 || li == 2) pack_quads(p, li, c, q, flags_of(li, c), tid);
     mbar_wait(bar0 + 8 * li, 0);        // all 7 peer slices of layer li have landed
     fstamp(4 + 3 * li);
     if (li <= 2 && !own) pack_planes(p, li, c, q, sm + L.flags[li], warp, lane);
@@ -435,7 +436,7 @@ bool fused_fwd_ok(const ActorDims& d, int B) {
     const int nt = d.P[l] / C / 8;   // n-tiles per CTA must divide the 8 warps (k-split)
     if (l && NWARP % nt != 0) return false;
   }
-  if (round_up(d.T, 16) != 16) return false;          // octet planes: one uint4 per (octet, neuron)
+  if (round_up(d.T, 16) != 16) return false;          // quad planes: one u64 per (quad, neuron)
   const Params p = fused_params(d, B);
   return smem_layout(p).total <= 220 * 1024;
 }

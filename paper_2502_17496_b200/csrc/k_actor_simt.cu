@@ -236,6 +236,146 @@ __global__ void __launch_bounds__(256, 4) dec_bwd_outscan_kernel(
   }
 }
 
+// TMA-staged variant (the default whenever its stage fits in shared memory): a block owns R batch
+// rows x the live octets of the output layer (no dead lanes: N_3 = 170 uses 22 of a row's 32
+// octets), one thread per (row, octet). The spike and mask planes of the block's next R rows and
+// all T steps arrive by two 3-D TMA copies ([T][R][W3] boxes, rows past B zero-filled) into the
+// other half of a double buffer while the current rows are scanned, so the scan never waits on a
+// global load (ncu r01: the direct-load kernel above stalled on long-scoreboard 7.6 cycles per
+// issued instruction and reached 29-37% of the copy peak at configs[4]).
+namespace osc {
+__device__ __forceinline__ uint32_t su32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void bar_init(uint64_t* b, uint32_t c) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(su32(b)), "r"(c) : "memory");
+}
+__device__ __forceinline__ void bar_expect(uint64_t* b, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(su32(b)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void bar_wait(uint64_t* b, uint32_t parity) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n"
+      "OSC_WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+      "@!p bra OSC_WAIT_%=;\n}" ::"r"(su32(b)),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void tma3(const CUtensorMap* m, void* dst, uint64_t* b, int c0, int c1, int c2) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4, %5}], [%2];" ::"r"(
+          su32(dst)),
+      "l"(m), "r"(su32(b)), "r"(c0), "r"(c1), "r"(c2)
+      : "memory");
+}
+}  // namespace osc
+
+template <typename GTy>
+__global__ void __launch_bounds__(256) dec_bwd_outscan_tma_kernel(
+    const __grid_constant__ CUtensorMap map_o, const __grid_constant__ CUtensorMap map_h, int B, int T, int A,
+    int D, int N3, int W3, int NO, int R, int planeS, float dcc, float dvc, float zh,
+    const float* __restrict__ grad_a, const float* __restrict__ act, const float* __restrict__ Wd,
+    GTy* __restrict__ G3, float* __restrict__ g_pre_out, int write_pad) {
+  extern __shared__ __align__(128) uint8_t osm[];
+  uint32_t* sbuf = reinterpret_cast<uint32_t*>(osm);              // [2 buffers][2 planes][planeS]
+  uint64_t* bar = reinterpret_cast<uint64_t*>(osm + (size_t)16 * planeS);
+  const int tid = threadIdx.x;
+  const int units = (B + R - 1) / R;
+  if (tid == 0) {
+    osc::bar_init(&bar[0], 1);
+    osc::bar_init(&bar[1], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  pdl_wait();
+  pdl_trigger();
+  const uint32_t txb = 2u * (uint32_t)T * (uint32_t)R * (uint32_t)W3 * 4u;   // whole boxes (OOB rows count)
+  auto issue = [&](int unit, int bi) {
+    uint32_t* d0 = sbuf + (size_t)(2 * bi) * planeS;
+    osc::bar_expect(&bar[bi], txb);
+    osc::tma3(&map_o, d0, &bar[bi], 0, unit * R, 0);
+    osc::tma3(&map_h, d0 + planeS, &bar[bi], 0, unit * R, 0);
+  };
+  if (tid == 0 && (int)blockIdx.x < units) issue(blockIdx.x, 0);
+  const int o = tid % NO, r = tid / NO;
+  const int n0 = 8 * o, w = o >> 2, sh = 8 * (o & 3);
+  const int P3 = 32 * W3;
+  const bool live = n0 < N3 || write_pad;
+  const size_t gts = (size_t)B * P3;
+  const int tstr = R * W3;
+  int it = 0;
+  for (int u = blockIdx.x; u < units; u += gridDim.x, ++it) {
+    const int bi = it & 1;
+    if (tid == 0 && u + (int)gridDim.x < units) {
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");   // prior generic reads of buffer bi^1
+      issue(u + gridDim.x, bi ^ 1);
+    }
+    const int b = u * R + r;
+    // g_o3 = g_fr / T = g_pre_a Wd[a][d] / T (constant in t), window factor z folded in; the
+    // loads overlap the TMA copy of this unit's planes
+    float g[8];
+    if (b < B) {
+      int a = n0 / D, e = n0 - a * D;
+      float gp = 0.f;
+      if (n0 < N3) {
+        const float av = act[(size_t)b * A + a];
+        gp = __fmul_rn(grad_a[(size_t)b * A + a], __fsub_rn(1.0f, __fmul_rn(av, av)));
+      }
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        g[i] = 0.f;
+        if (n0 + i < N3) {
+          if (e == 0) g_pre_out[(size_t)b * A + a] = gp;
+          g[i] = __fmul_rn(zh, __fdiv_rn(__fmul_rn(gp, Wd[a * D + e]), (float)T));
+        }
+        if (++e == D && n0 + i + 1 < N3) {
+          e = 0;
+          ++a;
+          const float av = act[(size_t)b * A + a];
+          gp = __fmul_rn(grad_a[(size_t)b * A + a], __fsub_rn(1.0f, __fmul_rn(av, av)));
+        }
+      }
+    }
+    osc::bar_wait(&bar[bi], (uint32_t)(it >> 1) & 1u);
+    if (b < B) {
+      const uint32_t* so = sbuf + (size_t)(2 * bi) * planeS + r * W3 + w;
+      const uint32_t* sm = so + planeS;
+      float dvn[8], dcn[8];
+#pragma unroll
+      for (int i = 0; i < 8; ++i) { dvn[i] = 0.f; dcn[i] = 0.f; }
+      GTy* gq = G3 + (size_t)b * P3 + n0 + (size_t)(T - 1) * gts;
+#pragma unroll 2
+      for (int t = T - 1; t >= 0; --t) {
+        const uint32_t o8 = (so[t * tstr] >> sh) & 0xFFu, h8 = (sm[t * tstr] >> sh) & 0xFFu;
+        float G[8];
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+          const float hg = ((h8 >> i) & 1u) ? g[i] : 0.0f;
+          const float dvt = ((o8 >> i) & 1u) ? hg : __fmaf_rn(dvc, dvn[i], hg);
+          const float dct = __fmaf_rn(dcc, dcn[i], dvt);
+          dvn[i] = dvt;
+          dcn[i] = dct;
+          G[i] = dct;
+        }
+        if (live) Pack8<GTy>::store(gq, G);
+        gq -= gts;
+      }
+    }
+    __syncthreads();   // buffer bi is refilled at the top of the next-but-one iteration
+  }
+}
+
+// shared-memory plan of the staged scan: R rows per unit, the padded plane size in words (128-byte
+// aligned TMA destinations); R = 0 when even one row per unit does not fit the budget
+static void outscan_plan(const ActorDims& d, int wpad, int* NO, int* R, int* planeS) {
+  const int nl = wpad ? d.P[3] : d.N3;
+  *NO = (nl + 7) / 8;
+  int r = 256 / *NO;
+  constexpr size_t kBudget = 96 * 1024;
+  while (r > 0 && 16 * (size_t)round_up(d.T * r * d.Wd[3], 32) + 16 > kBudget) --r;
+  *R = r;
+  *planeS = round_up(d.T * (r > 0 ? r : 1) * d.Wd[3], 32);
+}
+
 int launch_dec_bwd_outscan(const ActorDims& d, int B, const float* grad_a, const float* act,
                            const uint8_t* counts, const float* Wd, const uint32_t* bits3,
                            const uint32_t* mask3, void* G3, float* g_pre, cudaStream_t st) {
@@ -244,8 +384,42 @@ int launch_dec_bwd_outscan(const ActorDims& d, int B, const float* grad_a, const
   const double gcols = d.engine == SPIKERL_ENGINE_TCGEN05 ? d.N3 : d.P[3];
   ProfScope ps_("dec_bwd_outscan", PB_HBM, 0.0, (double)d.T * B * (gcols * (d.bf16 ? 2.0 : 4.0) + 2.0 * d.Wd[3] * 4), st);
   (void)counts;
-  const long long units = (long long)cdiv(B, 2) * (d.Wd[3] / 4);   // warps of work
   const int wpad = d.engine == SPIKERL_ENGINE_TCGEN05 ? 0 : 1;     // SIMT kernels read P3 columns
+  int NO, R, planeS;
+  outscan_plan(d, wpad, &NO, &R, &planeS);
+  static const bool direct = [] { const char* e = getenv("SPIKERL_OUTSCAN_DIRECT"); return e && e[0] == '1'; }();
+  if (R > 0 && !direct) {
+    CUtensorMap mo, mh;
+    const uint64_t dims[3] = {(uint64_t)d.Wd[3], (uint64_t)B, (uint64_t)d.T};
+    const uint64_t strides[2] = {(uint64_t)d.Wd[3] * 4, (uint64_t)B * d.Wd[3] * 4};
+    const uint32_t box[3] = {(uint32_t)d.Wd[3], (uint32_t)R, (uint32_t)d.T};
+    SPK_TRY(make_u32_map3(&mo, bits3, dims, strides, box));
+    SPK_TRY(make_u32_map3(&mh, mask3, dims, strides, box));
+    const size_t smem = (size_t)16 * planeS + 16;
+    const int threads = NO * R;
+    auto launch = [&](auto kern, auto* G) -> int {
+      static bool attr = false;
+      if (!attr) {
+        SPK_CHECK_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 100 * 1024));
+        attr = true;
+      }
+      int per_sm = 0;
+      if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, threads, smem) != cudaSuccess || per_sm < 1) {
+        cudaGetLastError();
+        per_sm = 1;
+      }
+      const int units = cdiv(B, R), cap = num_sms() * per_sm;
+      const int waves = cdiv(units, cap);
+      const int blocks = cdiv(units, waves);   // every block gets `waves` units (the last one fewer)
+      pdl(kern, blocks, threads, smem, st)(mo, mh, B, d.T, d.A, d.D, d.N3, d.Wd[3], NO, R, planeS, d.dc, d.dv,
+                                            d.zh, grad_a, act, Wd, G, g_pre, wpad);
+      SPK_LAUNCHED();
+      return SPIKERL_OK;
+    };
+    if (d.bf16) return launch(dec_bwd_outscan_tma_kernel<__nv_bfloat16>, (__nv_bfloat16*)G3);
+    return launch(dec_bwd_outscan_tma_kernel<float>, (float*)G3);
+  }
+  const long long units = (long long)cdiv(B, 2) * (d.Wd[3] / 4);   // warps of work
   long long blocks = cdiv(units, 8);
   if (blocks > (long long)num_sms() * 8) blocks = (long long)num_sms() * 8;
   if (d.bf16) {

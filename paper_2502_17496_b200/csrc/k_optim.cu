@@ -15,6 +15,24 @@ static int ew_grid(size_t n, int per_thread) {
   return (int)(blocks < cap ? (blocks > 0 ? blocks : 1) : cap);
 }
 
+// Streaming kernels (Adam, Polyak): exactly one wave of resident blocks, never more. A grid of
+// 8 blocks per SM with 3 resident ran 2.67 waves (ncu r01: Adam at configs[4] size 66% of the
+// copy peak, the partial last wave and the ramp of each wave exposed).
+template <typename K>
+static int stream_grid(K kernel, size_t n, int per_thread) {
+  static int per_sm = 0;
+  if (!per_sm) {
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, 256, 0) != cudaSuccess || per_sm < 1) {
+      cudaGetLastError();
+      per_sm = 2;
+    }
+  }
+  const size_t threads = (n + per_thread - 1) / per_thread;
+  const size_t blocks = (threads + 255) / 256;
+  const size_t cap = (size_t)num_sms() * per_sm;
+  return (int)(blocks < cap ? (blocks > 0 ? blocks : 1) : cap);
+}
+
 // ------------------------------------------------------------------ bf16 working copies
 // Actor: W_l (fp32 [N_l][N_{l-1}]) -> bf16 [P_l][P_{l-1}], zero padded. One thread per padded
 // element so the padding is (re)written with zeros every refresh.
@@ -205,30 +223,42 @@ int launch_adam(float* p, const float* g, float* m, float* v, size_t n, long lon
     set_error("adam: buffers must be 16-byte aligned");
     return SPIKERL_E_ARG;
   }
-  pdl(adam_kernel, ew_grid(n, 4), 256, 0, st)(p, g, m, v, n, counter, lr, b1, b2, eps, clo, chi,
+  pdl(adam_kernel, stream_grid(adam_kernel, n, 8), 256, 0, st)(p, g, m, v, n, counter, lr, b1, b2, eps, clo, chi,
                                              cmin, ticket, views ? *views : none);
   SPK_LAUNCHED();
   return SPIKERL_OK;
 }
 
 // ------------------------------------------------------------------ Polyak
-__global__ void polyak_kernel(float* __restrict__ t, const float* __restrict__ s, size_t n,
-                              float tau, const __grid_constant__ Bf16Views views) {
+__global__ void __launch_bounds__(256, 4) polyak_kernel(float* __restrict__ t, const float* __restrict__ s,
+                                                      size_t n, float tau, const __grid_constant__ Bf16Views views) {
   pdl_wait();
   pdl_trigger();
   const float omt = 1.0f - tau;
   const size_t n4 = (((uintptr_t)t | (uintptr_t)s) & 15) ? 0 : n / 4;   // float4 body when aligned
   const size_t stride = (size_t)gridDim.x * blockDim.x;
-  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n4; i += stride) {
-    const float4 sv = reinterpret_cast<const float4*>(s)[i];
-    float4 tv = reinterpret_cast<float4*>(t)[i];
-    tv.x = __fadd_rn(__fmul_rn(tau, sv.x), __fmul_rn(omt, tv.x));
-    tv.y = __fadd_rn(__fmul_rn(tau, sv.y), __fmul_rn(omt, tv.y));
-    tv.z = __fadd_rn(__fmul_rn(tau, sv.z), __fmul_rn(omt, tv.z));
-    tv.w = __fadd_rn(__fmul_rn(tau, sv.w), __fmul_rn(omt, tv.w));
-    reinterpret_cast<float4*>(t)[i] = tv;
-    store_views(views, 4 * i, tv.x); store_views(views, 4 * i + 1, tv.y);
-    store_views(views, 4 * i + 2, tv.z); store_views(views, 4 * i + 3, tv.w);
+  // two float4 groups per thread and iteration, all four loads issued before the arithmetic
+  for (size_t i0 = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i0 < n4; i0 += 2 * stride) {
+    const bool two = i0 + stride < n4;
+    float4 sv[2], tv[2];
+#pragma unroll
+    for (int u = 0; u < 2; ++u)
+      if (u == 0 || two) {
+        sv[u] = reinterpret_cast<const float4*>(s)[i0 + u * stride];
+        tv[u] = reinterpret_cast<float4*>(t)[i0 + u * stride];
+      }
+#pragma unroll
+    for (int u = 0; u < 2; ++u) {
+      if (u == 1 && !two) break;
+      const size_t i = i0 + u * stride;
+      float* ta = &tv[u].x;
+      const float* sa = &sv[u].x;
+#pragma unroll
+      for (int j = 0; j < 4; ++j) ta[j] = __fadd_rn(__fmul_rn(tau, sa[j]), __fmul_rn(omt, ta[j]));
+      reinterpret_cast<float4*>(t)[i] = tv[u];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) store_views(views, 4 * i + j, ta[j]);
+    }
   }
   for (size_t i = 4 * n4 + blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n; i += stride) {
     const float x = __fadd_rn(__fmul_rn(tau, s[i]), __fmul_rn(omt, t[i]));
@@ -240,7 +270,7 @@ __global__ void polyak_kernel(float* __restrict__ t, const float* __restrict__ s
 int launch_polyak(float* t, const float* s, size_t n, float tau, const Bf16Views* views, cudaStream_t st) {
   const Bf16Views none{};
   ProfScope ps_("polyak", PB_HBM, 0.0, 12.0 * n, st);
-  pdl(polyak_kernel, ew_grid(n, 4), 256, 0, st)(t, s, n, tau, views ? *views : none);
+  pdl(polyak_kernel, stream_grid(polyak_kernel, n, 8), 256, 0, st)(t, s, n, tau, views ? *views : none);
   SPK_LAUNCHED();
   return SPIKERL_OK;
 }

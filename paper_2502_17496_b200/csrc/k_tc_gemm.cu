@@ -13,7 +13,9 @@
 //   warps 2-5   spike-bit expanders: u32 spike words -> bf16 {0,1} tiles in the 128B-swizzled
 //               UMMA layout (K-major for FWD, MN-major for DW)
 //   warps 6-13  epilogue, 2 groups x 4 warps: tcgen05.ld (32x32b) of the TMEM accumulator, one
-//               thread per neuron, each group owning half of the tile's columns
+//               thread per neuron, each group owning half of the tile's columns (4 groups of 4
+//               warps measured no faster: the FWD / DX epilogues are bound by their instruction
+//               count, not by latency hiding)
 // Pipelines: 4-stage smem ring (full/empty mbarriers), 2-stage TMEM accumulator (2 x 256 cols).
 // Neurons sit on TMEM lanes (MMA M) and (t,b) on columns (MMA N) with t-major order, so a
 // thread owns every timestep of its neuron: the LIF scans never leave registers, and one
@@ -25,17 +27,29 @@
 namespace spk {
 namespace tc {
 
-enum Mode { FWD = 0, DX = 1, ENC = 2, DW = 3 };
+// FWD: hidden layers (batch-major spike plane + quad-major spike / mask planes for the DX epilogue);
+// FWDO: output layer (batch-major spike and mask planes + spike counts)
+enum Mode { FWD = 0, DX = 1, ENC = 2, DW = 3, FWDO = 4 };
+__host__ __device__ constexpr bool is_fwd(int m) { return m == FWD || m == FWDO; }
 
 constexpr int BM = 128, BK = 64, STAGES = 4;
 constexpr int A_STAGE = BM * BK * 2;             // 16 KB
 constexpr int B_STAGE = 256 * BK * 2;            // 32 KB
 constexpr int STAGE_BYTES = A_STAGE + B_STAGE;   // 48 KB
-constexpr int NUM_EXP_WARPS = 4, NUM_EPI_WARPS = 8;
+constexpr int NUM_EXP_WARPS = 4, NUM_EPI_WARPS = 8, NUM_EPI_GROUPS = NUM_EPI_WARPS / 4;
 constexpr int EXP_WARP0 = 2, EPI_WARP0 = 2 + NUM_EXP_WARPS;
 constexpr int NUM_THREADS = (EPI_WARP0 + NUM_EPI_WARPS) * 32;  // 448
+// batch rows of a (t, b) tile per epilogue group (FWD / DX): a quarter of the tile, at least 4 (one
+// quad of the neuron-major planes); groups past BT / epi_hb(BT) idle
+__host__ __device__ constexpr int epi_hb(int bt) { return bt / NUM_EPI_GROUPS > 4 ? bt / NUM_EPI_GROUPS : 4; }
 constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + 1024 + 256;
 constexpr int TMEM_COLS = 512;
+// DX: the epilogue stages G_{l-1} in shared memory, DX_CH steps at a time ([t][b][128 neurons] bf16,
+// double-buffered), and one thread stores each chunk with a TMA tensor store (rows past B and steps
+// past T are clipped by the tensor map). ncu r01: per-element 2-byte global stores with their 64-bit
+// address arithmetic were over half of the DX epilogue's instructions.
+constexpr int DX_CH = 4;
+constexpr int DX_STG = 128 * 16 * DX_CH * 2;   // bytes per staging buffer (Bt <= 16)
 constexpr int DW_BN = 256;   // N of one DW MMA
 // A DW unit of a CTA pair covers 2 x 256 output columns (two accumulators, sharing every A tile):
 // each G_l tile fetched from L2/HBM feeds twice the MMA work, which halves the G_l re-reads over
@@ -51,9 +65,9 @@ struct Params {
   // FWD
   const uint32_t* bits_in; int w_in;
   uint32_t* bits_out; uint32_t* mask_out; int w_out; uint8_t* counts; int n_valid; int n3;
-  uint8_t* bitsT_out; uint8_t* maskT_out; int p_out;   // octet-major copies (may be null)
+  uint8_t* bitsT_out; uint8_t* maskT_out; int p_out;   // quad-major copies (may be null)
   LifConst kc; float zh;
-  int tpad;                                              // bytes per (octet, neuron) row = T rounded to 16
+  int tpad;                                              // T rounded to 16 (tpad / 2 bytes per (quad, neuron))
   // DX
   const uint8_t* bitsT_prev; const uint8_t* maskT_prev;
   __nv_bfloat16* g_prev; int p_prev; __nv_bfloat16* g_sum;
@@ -120,6 +134,20 @@ __device__ __forceinline__ void tma_3d(const CUtensorMap* map, void* dst, uint64
       : "memory");
 }
 
+__device__ __forceinline__ void tma_store_3d(const CUtensorMap* map, const void* src, int c0, int c1, int c2) {
+  asm volatile("cp.async.bulk.tensor.3d.global.shared::cta.bulk_group [%0, {%2, %3, %4}], [%1];" ::"l"(map),
+               "r"(smem_u32(src)), "r"(c0), "r"(c1), "r"(c2)
+               : "memory");
+}
+__device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void bulk_wait_read1() { asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory"); }
+__device__ __forceinline__ void bulk_wait_all() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
+// named barrier of the epilogue warps only (barrier 0 is __syncthreads)
+__device__ __forceinline__ void epi_bar_sync() { asm volatile("bar.sync 1, %0;" ::"n"(NUM_EPI_WARPS * 32) : "memory"); }
+__device__ __forceinline__ void st_shared_u16(uint32_t addr, uint16_t v) {
+  asm volatile("st.shared.b16 [%0], %1;" ::"r"(addr), "h"(v) : "memory");
+}
+
 __device__ __forceinline__ void tmem_alloc(uint32_t* dst, uint32_t ncols) {
   asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(dst)), "r"(ncols)
                : "memory");
@@ -161,6 +189,18 @@ __device__ __forceinline__ void tmem_ld8(uint32_t taddr, uint32_t (&r)[8]) {
                : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7])
                : "r"(taddr));
 }
+__device__ __forceinline__ void tmem_ld4(uint32_t taddr, uint32_t (&r)[4]) {
+  asm volatile("tcgen05.ld.sync.aligned.32x32b.x4.b32 {%0, %1, %2, %3}, [%4];"
+               : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3])
+               : "r"(taddr));
+}
+template <int N> __device__ __forceinline__ void tmem_ldn(uint32_t taddr, uint32_t (&r)[N]);
+template <> __device__ __forceinline__ void tmem_ldn<4>(uint32_t taddr, uint32_t (&r)[4]) { tmem_ld4(taddr, r); }
+template <> __device__ __forceinline__ void tmem_ldn<8>(uint32_t taddr, uint32_t (&r)[8]) { tmem_ld8(taddr, r); }
+template <> __device__ __forceinline__ void tmem_ldn<16>(uint32_t taddr, uint32_t (&r)[16]) {
+  tmem_ld8(taddr, *reinterpret_cast<uint32_t(*)[8]>(&r[0]));
+  tmem_ld8(taddr + 8, *reinterpret_cast<uint32_t(*)[8]>(&r[8]));
+}
 __device__ __forceinline__ void tmem_ld_wait() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
 
 // 8 spike bits -> 8 bf16 values {0, 1.0} (16 bytes). A multiply moves bit i of each nibble to
@@ -188,17 +228,6 @@ __device__ __forceinline__ void st_shared_v4(uint32_t addr, uint4 v) {
                : "memory");
 }
 
-// 16-byte shift register: the newest byte enters at the top (byte 15)
-__device__ __forceinline__ void shift_in(uint32_t (&q)[4], uint32_t byte) {
-  q[0] = __funnelshift_r(q[0], q[1], 8);
-  q[1] = __funnelshift_r(q[1], q[2], 8);
-  q[2] = __funnelshift_r(q[2], q[3], 8);
-  q[3] = (q[3] >> 8) | (byte << 24);
-}
-__device__ __forceinline__ uint32_t byte_of(const uint4& q, int i) {
-  const uint32_t w = i < 8 ? (i < 4 ? q.x : q.y) : (i < 12 ? q.z : q.w);
-  return (w >> ((i & 3) * 8)) & 0xFFu;
-}
 
 // ---- CTA-pair (cta_group::2) helpers: M = 256 per pair, A split by rows, B split by columns
 __device__ __forceinline__ uint32_t cluster_ctarank() {
@@ -292,24 +321,27 @@ constexpr int PF = 4;
 // MMA commits multicast back to both CTAs.
 template <int MODE, int BT, int CG>
 __global__ void __launch_bounds__(NUM_THREADS, 1)
-    tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, const Params p) {
+    tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+              const __grid_constant__ CUtensorMap tmC, const Params p) {
   // A CTA of a pair holds at most 128 B rows (its half of the MMA's N), so its stages are 32 KB
   // and the same shared memory holds 6 of them instead of 4 (ncu r01: the DW/FWD L1 MMA waited
   // on TMA-filled stages with the ring 4 deep)
   constexpr bool DW2 = (MODE == DW && CG == 2);   // two accumulators per unit, one buffer
-  constexpr int NST = CG == 2 && !DW2 ? 6 : STAGES;
   constexpr int SB_ = A_STAGE + (DW2 ? B_STAGE : B_STAGE / CG);
+  constexpr int STG_ = MODE == DX ? 2 * DX_STG : 0;   // DX output staging
+  constexpr int NST = ((CG == 2 && !DW2) ? 6 : STAGES) - (STG_ + SB_ - 1) / SB_;
   constexpr int NBUF = DW2 ? 1 : 2;               // TMEM accumulator buffers
-  static_assert(NST * SB_ <= STAGES * STAGE_BYTES, "stage ring exceeds the shared-memory budget");
+  static_assert(NST * SB_ + STG_ <= STAGES * STAGE_BYTES, "stage ring exceeds the shared-memory budget");
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
-  uint64_t* full = (uint64_t*)(smem + NST * SB_);
+  uint8_t* stg = smem + NST * SB_;   // DX staging (1024-aligned: SB_ is a multiple of 16 KB)
+  uint64_t* full = (uint64_t*)(smem + NST * SB_ + STG_);
   uint64_t* empty = full + NST;
   uint64_t* tfull = empty + NST;
   uint64_t* tempty = tfull + 2;
   uint32_t* tmem_slot = (uint32_t*)(tempty + 2);
-  constexpr bool B_EXPAND = (MODE == FWD || MODE == DW);
-  constexpr bool A_MN = (MODE != FWD);
+  constexpr bool B_EXPAND = (is_fwd(MODE) || MODE == DW);
+  constexpr bool A_MN = !is_fwd(MODE);
   constexpr bool B_MN = (MODE == DW);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int rank = CG == 2 ? (int)cluster_ctarank() : 0;
@@ -436,7 +468,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       for (int u = cid; u < p.n_units; u += ncl) {
         const Tile t = decode<MODE>(p, u, rank, CG);
         const int nkb = t.kb1 - t.kb0;
-        if (MODE == FWD) {
+        if (is_fwd(MODE)) {
           // K-major: row = (t, j) spike row of the MMA's B columns this CTA holds; one k-block =
           // 2 words per row = 8 chunks of 16 B. Lane l owns rows l + 32 i.
           constexpr int RPL = CG == 2 ? 4 : 8;
@@ -565,164 +597,206 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     const int q = warp & 3;
     const int g = (warp - EPI_WARP0) >> 2;
     uint32_t titer = 0;
+    uint32_t dx_chunk = 0;   // DX staging chunks issued so far (buffer parity)
+    (void)dx_chunk;
+    constexpr int DX_NQ = MODE == DX ? epi_hb(BT) / 4 : 1;
+    unsigned long long nq_o[DX_NQ], nq_h[DX_NQ];
+    auto dx_quad_load = [&](const Tile& tn, unsigned long long (&o)[DX_NQ], unsigned long long (&h)[DX_NQ]) {
+      const int b0 = tn.n * BT + g * epi_hb(BT);
+      const int rw = tn.m * BM + 32 * q + lane;
+      const size_t rb = (p.tpad >> 1) / 8;   // u64 words per (quad, neuron) row
+      const int ch = (p.T - 1) >> 4;
+#pragma unroll
+      for (int qi = 0; qi < DX_NQ; ++qi) {
+        const size_t w = ((size_t)((b0 >> 2) + qi) * p.p_prev + rw) * rb + ch;
+        o[qi] = __ldg(reinterpret_cast<const unsigned long long*>(p.bitsT_prev) + w);
+        h[qi] = __ldg(reinterpret_cast<const unsigned long long*>(p.maskT_prev) + w);
+      }
+    };
+    if constexpr (MODE == DX) {
+      if (cid < p.n_units) dx_quad_load(decode<MODE>(p, cid, rank, CG), nq_o, nq_h);
+    }
     for (int u = cid; u < p.n_units; u += ncl, ++titer) {
       const Tile t = decode<MODE>(p, u, rank, CG);
       const uint32_t a = titer % NBUF, aph = (titer / NBUF) & 1;
+      const int row = t.m * BM + 32 * q + lane;  // neuron index (M)
+      // DX: this thread's spike / mask bits of the last 16-step chunk (quad-major planes
+      // [B/4][P][Tpad/2]) were requested during the previous unit; the next unit's are requested now,
+      // so the load latency hides behind a whole unit (ncu r01: loaded at the unit start, they stalled
+      // the epilogue on long-scoreboard once per unit)
+      unsigned long long dq_o[DX_NQ], dq_h[DX_NQ];
+      if constexpr (MODE == DX) {
+#pragma unroll
+        for (int qi = 0; qi < DX_NQ; ++qi) { dq_o[qi] = nq_o[qi]; dq_h[qi] = nq_h[qi]; }
+        if (u + ncl < p.n_units) dx_quad_load(decode<MODE>(p, u + ncl, rank, CG), nq_o, nq_h);
+      }
       mbar_wait(&tfull[a], aph);
       tc_fence_after();
       if (titer == 0 && warp == EPI_WARP0 && lane == 0) trace_stamp(p, 6);
       const uint32_t taddr = tmem + ((uint32_t)(32 * q) << 16) + a * 256;
-      const int row = t.m * BM + 32 * q + lane;  // neuron index (M)
       if (p.dbg & 2) {
-      } else if (MODE == FWD) {
-        constexpr int HB = BT >= 16 ? BT / 2 : BT;  // batch rows per group
-        if (BT >= 16 || g == 0) {
-          const int jb = BT >= 16 ? g * HB : 0;
-          const bool valid = row < p.n_valid;
+      } else if constexpr (is_fwd(MODE)) {
+        // LIF forward scan of HB batch rows of one neuron, all T steps in registers. Padding
+        // neurons (zero weight rows) and padding batch rows (zero spikes) see I = 0 and never fire
+        // or enter the window (v = 0 sits on its lower edge), so no validity masking is needed.
+        // The reset gate is kept as a factor rv = d_v (1 - o_{t-1}): v = fma(rv, v, c) is exactly
+        // c after a spike (ncu r01: the bit-tracked select form cost ~27 instructions per
+        // neuron-step with the batch-major mask plane; the hidden layers' mask plane is not written
+        // any more, the DX epilogue reads the quad-major copy)
+        constexpr int HB = epi_hb(BT);            // batch rows of this group
+        constexpr bool OUT = MODE == FWDO;
+        if (g < BT / HB) {
+          const int jb = g * HB;
           const int b0 = t.n * BT + jb;
-          float c[HB], v[HB];
+          const float dc = p.kc.dc, dv = p.kc.dv, vth = p.kc.vth, win = p.kc.win;
+          float c[HB], v[HB], rv[HB];
           int cnt[HB];
-          uint32_t oprev = 0;
 #pragma unroll
-          for (int j = 0; j < HB; ++j) { c[j] = 0.f; v[j] = 0.f; cnt[j] = 0; }
-          const size_t wcol = (size_t)(t.m * BM + 32 * q) >> 5;
-          // octet-major copy (DX epilogue input): per batch octet, the byte of step t is shifted
-          // into a 16-byte register window and written once per 16 steps (coalesced uint4)
-          constexpr int NOC = HB / 8;
-          const bool wT = p.bitsT_out != nullptr;
-          uint32_t qo[NOC][4], qh[NOC][4];
+          for (int j = 0; j < HB; ++j) { c[j] = 0.f; v[j] = 0.f; rv[j] = dv; cnt[j] = 0; }
+          // lanes < HB store the step's words of rows b0 + lane: one pointer each, + B W per step
+          const bool st_lane = lane < HB && b0 + lane < p.B;
+          const size_t wofs = (size_t)(b0 + (lane < HB ? lane : 0)) * p.w_out + ((size_t)(t.m * BM + 32 * q) >> 5);
+          const size_t tstride = (size_t)p.B * p.w_out;
+          // quad-major copy (DX epilogue input): per batch quad, the nibble of step t enters a
+          // 64-bit word (16 steps) written once per 16 steps
+          constexpr int NQ = HB / 4;
+          unsigned long long qo[NQ], qh[NQ];
 #pragma unroll
-          for (int oc = 0; oc < NOC; ++oc)
-#pragma unroll
-            for (int i = 0; i < 4; ++i) { qo[oc][i] = 0u; qh[oc][i] = 0u; }
-          // TMEM loads of CH timesteps are issued together and waited once (trace r01: one
-          // load + wait per step left the epilogue latency-bound at small batch)
-          constexpr int CH = HB >= 16 ? 1 : 32 / HB;   // BT = 32: registers are the limit
+          for (int qi = 0; qi < NQ; ++qi) { qo[qi] = 0ull; qh[qi] = 0ull; }
+          // TMEM loads of CH timesteps are issued together and waited once
+          constexpr int CH = HB >= 16 ? 2 : (HB >= 8 ? 4 : 8);
           for (int t0 = 0; t0 < p.T; t0 += CH) {
-          uint32_t rr[CH][HB / 8][8];
+            uint32_t rr[CH][HB];
 #pragma unroll
-          for (int ci = 0; ci < CH; ++ci)
-            if (t0 + ci < p.T) {
+            for (int ci = 0; ci < CH; ++ci)
+              if (t0 + ci < p.T) tmem_ldn<HB>(taddr + (t0 + ci) * BT + jb, rr[ci]);
+            tmem_ld_wait();
 #pragma unroll
-              for (int j0 = 0; j0 < HB; j0 += 8) tmem_ld8(taddr + (t0 + ci) * BT + jb + j0, rr[ci][j0 / 8]);
-            }
-          tmem_ld_wait();
+            for (int ci = 0; ci < CH; ++ci) {
+              const int tt = t0 + ci;
+              if (tt >= p.T) break;
+              uint32_t ocur = 0, hcur = 0, wo = 0, wh = 0;
 #pragma unroll
-          for (int ci = 0; ci < CH; ++ci) {
-            const int tt = t0 + ci;
-            if (tt >= p.T) break;
-            uint32_t hcur = 0;
-#pragma unroll
-            for (int j0 = 0; j0 < HB; j0 += 8) {
-              const uint32_t (&r)[8] = rr[ci][j0 / 8];
-              uint32_t wo = 0, wh = 0;
-#pragma unroll
-              for (int jj = 0; jj < 8; ++jj) {
-                const int j = j0 + jj;
-                bool o = (oprev >> j) & 1u, h;
-                lif_step(p.kc, __uint_as_float(r[jj]), c[j], v[j], o, h);
-                if (!valid) { o = false; h = false; }
-                oprev = o ? (oprev | (1u << j)) : (oprev & ~(1u << j));
-                hcur |= h ? (1u << j) : 0u;
-                cnt[j] += o ? 1 : 0;
-                const uint32_t ob = __ballot_sync(0xffffffffu, o), hb = __ballot_sync(0xffffffffu, h);
-                if (lane == jj) { wo = ob; wh = hb; }
-              }
-              const int b = b0 + j0 + lane;
-              if (lane < 8 && b < p.B) {
-                const size_t wi = ((size_t)tt * p.B + b) * p.w_out + wcol;
-                p.bits_out[wi] = wo;
-                p.mask_out[wi] = wh;
-              }
-            }
-            if (wT) {
-#pragma unroll
-              for (int oc = 0; oc < NOC; ++oc) {
-                shift_in(qo[oc], (oprev >> (8 * oc)) & 0xFFu);
-                shift_in(qh[oc], (hcur >> (8 * oc)) & 0xFFu);
-              }
-              if ((tt & 15) == 15 || tt == p.T - 1) {
-                for (int k = (tt & 15) + 1; k < 16; ++k) {
-#pragma unroll
-                  for (int oc = 0; oc < NOC; ++oc) { shift_in(qo[oc], 0u); shift_in(qh[oc], 0u); }
+              for (int j = 0; j < HB; ++j) {
+                c[j] = __fmaf_rn(dc, c[j], __uint_as_float(rr[ci][j]));
+                v[j] = __fmaf_rn(rv[j], v[j], c[j]);
+                const bool o = v[j] > vth;
+                const bool h = fabsf(__fsub_rn(v[j], vth)) < win;
+                rv[j] = o ? 0.0f : dv;
+                if (o) ocur |= 1u << j;
+                if (h) hcur |= 1u << j;
+                const uint32_t ob = __ballot_sync(0xffffffffu, o);
+                if (lane == j) wo = ob;
+                if constexpr (OUT) {
+                  cnt[j] += o ? 1 : 0;
+                  const uint32_t hb = __ballot_sync(0xffffffffu, h);
+                  if (lane == j) wh = hb;
                 }
+              }
+              if (st_lane) {
+                p.bits_out[wofs + (size_t)tt * tstride] = wo;
+                if constexpr (OUT) p.mask_out[wofs + (size_t)tt * tstride] = wh;
+              }
+              if constexpr (!OUT) {
+                const int sh = 4 * (tt & 15);
 #pragma unroll
-                for (int oc = 0; oc < NOC; ++oc) {
-                  const size_t off = ((size_t)((b0 >> 3) + oc) * p.p_out + row) * p.tpad + (tt & ~15);
-                  *reinterpret_cast<uint4*>(p.bitsT_out + off) = make_uint4(qo[oc][0], qo[oc][1], qo[oc][2], qo[oc][3]);
-                  *reinterpret_cast<uint4*>(p.maskT_out + off) = make_uint4(qh[oc][0], qh[oc][1], qh[oc][2], qh[oc][3]);
+                for (int qi = 0; qi < NQ; ++qi) {
+                  qo[qi] |= (unsigned long long)((ocur >> (4 * qi)) & 0xFu) << sh;
+                  qh[qi] |= (unsigned long long)((hcur >> (4 * qi)) & 0xFu) << sh;
+                }
+                if ((tt & 15) == 15 || tt == p.T - 1) {
+#pragma unroll
+                  for (int qi = 0; qi < NQ; ++qi) {
+                    const size_t off = ((size_t)((b0 >> 2) + qi) * p.p_out + row) * (p.tpad >> 1) + ((tt >> 4) << 3);
+                    *reinterpret_cast<unsigned long long*>(p.bitsT_out + off) = qo[qi];
+                    *reinterpret_cast<unsigned long long*>(p.maskT_out + off) = qh[qi];
+                    qo[qi] = 0ull;
+                    qh[qi] = 0ull;
+                  }
                 }
               }
             }
           }
-          }
-          if (p.counts && row < p.n3) {
+          if constexpr (OUT) {
+            if (row < p.n3) {
 #pragma unroll
-            for (int j = 0; j < HB; ++j) {
-              const int b = b0 + j;
-              if (b < p.B) p.counts[(size_t)b * p.n3 + row] = (uint8_t)cnt[j];
+              for (int j = 0; j < HB; ++j) {
+                const int b = b0 + j;
+                if (b < p.B) p.counts[(size_t)b * p.n3 + row] = (uint8_t)cnt[j];
+              }
             }
           }
         }
       } else if constexpr (MODE == DX) {
-        constexpr int HB = BT >= 16 ? BT / 2 : BT;
-        if (BT >= 16 || g == 0) {
-          const int jb = BT >= 16 ? g * HB : 0;
-          const bool valid = row < p.n_valid;
-          const int b0 = t.n * BT + jb;
-          float dvn[HB], dcn[HB], gs[HB];
+        // reverse LIF scan of layer l-1 for HB batch rows of one neuron. Padding neurons have
+        // g = 0 (zero weight columns) and no spike / window bits, so G = 0 there without masking.
+        // G_{l-1} leaves through shared memory: DX_CH steps x BT rows x 128 neurons per TMA store.
+        constexpr int HB = epi_hb(BT);
+        constexpr int NQ = HB / 4;
+        static_assert(BT / HB == NUM_EPI_GROUPS, "every DX epilogue group owns HB batch rows");
+        const int jb = g * HB;
+        const int b0 = t.n * BT + jb;
+        const float zh = p.zh, dvc = p.kc.dv, dcc = p.kc.dc;
+        float dvn[HB], dcn[HB], gs[HB];
 #pragma unroll
-          for (int j = 0; j < HB; ++j) { dvn[j] = 0.f; dcn[j] = 0.f; gs[j] = 0.f; }
-          // this thread's own spike / mask bits for (t, b0..b0+7) come from the octet-major planes
-          // [B/8][P][Tpad] written by the forward epilogue: one coalesced uint4 per 16 steps
-          // (the next lower 16-step chunk is prefetched)
-          static_assert(HB == 8, "DX epilogue reads one batch octet per (t, neuron)");
-          const uint4* bT = reinterpret_cast<const uint4*>(p.bitsT_prev + ((size_t)(b0 >> 3) * p.p_prev + row) * p.tpad);
-          const uint4* mT = reinterpret_cast<const uint4*>(p.maskT_prev + ((size_t)(b0 >> 3) * p.p_prev + row) * p.tpad);
-          int ch = (p.T - 1) >> 4;
-          uint4 qo = __ldg(bT + ch), qh = __ldg(mT + ch);
-          uint4 nqo = ch > 0 ? __ldg(bT + ch - 1) : make_uint4(0u, 0u, 0u, 0u);
-          uint4 nqh = ch > 0 ? __ldg(mT + ch - 1) : make_uint4(0u, 0u, 0u, 0u);
-          // G_{l-1}[t][b][row]: one base pointer per thread, strides added per (t, j) (ncu r01: the
-          // per-element 64-bit index math and b < B branch were half of the epilogue's instructions)
-          const bool full = b0 + HB <= p.B;
-          const size_t bstr = (size_t)p.p_prev, tstr = (size_t)p.B * p.p_prev;
-          __nv_bfloat16* const gbase = p.g_prev + (size_t)b0 * bstr + row;
-          // TMEM loads of 4 timesteps issued together, one wait (see the FWD epilogue)
-          for (int t1 = p.T - 1; t1 >= 0; t1 -= 4) {
-            uint32_t rr[4][8];
+        for (int j = 0; j < HB; ++j) { dvn[j] = 0.f; dcn[j] = 0.f; gs[j] = 0.f; }
+        const size_t qstride = (size_t)p.p_prev * (p.tpad >> 1) / 8;   // u64 words between quads
+        const unsigned long long* bT = reinterpret_cast<const unsigned long long*>(
+            p.bitsT_prev + ((size_t)(b0 >> 2) * p.p_prev + row) * (p.tpad >> 1));
+        const unsigned long long* mT = reinterpret_cast<const unsigned long long*>(
+            p.maskT_prev + ((size_t)(b0 >> 2) * p.p_prev + row) * (p.tpad >> 1));
+        int ch = (p.T - 1) >> 4;
+        unsigned long long qo[NQ], qh[NQ];
 #pragma unroll
-            for (int ci = 0; ci < 4; ++ci)
-              if (t1 - ci >= 0) tmem_ld8(taddr + (t1 - ci) * BT + jb, rr[ci]);
-            tmem_ld_wait();
+        for (int qi = 0; qi < NQ; ++qi) { qo[qi] = dq_o[qi]; qh[qi] = dq_h[qi]; }
+        const bool leader = warp == EPI_WARP0 && lane == 0;
+        const uint32_t soff = (uint32_t)((jb * 128 + 32 * q + lane) * 2);
+        for (int c = (p.T - 1) / DX_CH; c >= 0; --c, ++dx_chunk) {
+          const uint32_t buf = dx_chunk & 1u;
+          if (leader) bulk_wait_read1();   // the store issued from this buffer two chunks ago has read it
+          epi_bar_sync();
+          const int tb = c * DX_CH;
+          uint32_t rr[DX_CH][HB];
 #pragma unroll
-            for (int ci = 0; ci < 4; ++ci) {
-              const int tt = t1 - ci;
-              if (tt < 0) break;
-              if ((tt >> 4) != ch) {
-                ch = tt >> 4;
-                qo = nqo; qh = nqh;
-                if (ch > 0) { nqo = __ldg(bT + ch - 1); nqh = __ldg(mT + ch - 1); }
-              }
-              const uint32_t ow0 = byte_of(qo, tt & 15), hw0 = byte_of(qh, tt & 15);
-              __nv_bfloat16* gt = gbase + (size_t)tt * tstr;
+          for (int ci = 0; ci < DX_CH; ++ci)
+            if (tb + ci < p.T) tmem_ldn<HB>(taddr + (tb + ci) * BT + jb, rr[ci]);
+          tmem_ld_wait();
+          const uint32_t sb = smem_u32(stg + buf * DX_STG) + soff;
 #pragma unroll
-              for (int j = 0; j < HB; ++j) {
-                const bool o = (ow0 >> j) & 1u, h = (hw0 >> j) & 1u;
-                float G = lif_back_step(p.zh, p.kc.dv, p.kc.dc, __uint_as_float(rr[ci][j]), o, h, dvn[j], dcn[j]);
-                if (!valid) G = 0.f;
-                gs[j] = __fadd_rn(gs[j], G);
-                if (full || b0 + j < p.B) *gt = __float2bfloat16_rn(G);
-                gt += bstr;
-              }
+          for (int ci = DX_CH - 1; ci >= 0; --ci) {
+            const int tt = tb + ci;
+            if (tt >= p.T) continue;
+            if ((tt >> 4) != ch) {
+              ch = tt >> 4;
+#pragma unroll
+              for (int qi = 0; qi < NQ; ++qi) { qo[qi] = __ldg(bT + qi * qstride + ch); qh[qi] = __ldg(mT + qi * qstride + ch); }
             }
-          }
-          if (p.g_sum) {
+            const int sh = 4 * (tt & 15);
+            uint32_t ow = 0, hw = 0;
+#pragma unroll
+            for (int qi = 0; qi < NQ; ++qi) {
+              ow |= ((uint32_t)(qo[qi] >> sh) & 0xFu) << (4 * qi);
+              hw |= ((uint32_t)(qh[qi] >> sh) & 0xFu) << (4 * qi);
+            }
 #pragma unroll
             for (int j = 0; j < HB; ++j) {
-              const int b = b0 + j;
-              if (b < p.B) p.g_sum[(size_t)b * p.p_prev + row] = __float2bfloat16_rn(gs[j]);
+              const float G = lif_back_step(zh, dvc, dcc, __uint_as_float(rr[ci][j]), (ow >> j) & 1u, (hw >> j) & 1u, dvn[j], dcn[j]);
+              gs[j] = __fadd_rn(gs[j], G);
+              st_shared_u16(sb + (uint32_t)((ci * BT + j) * 256), __bfloat16_as_ushort(__float2bfloat16_rn(G)));
             }
+          }
+          fence_proxy_async();   // generic-proxy smem writes -> the TMA store
+          epi_bar_sync();
+          if (leader) {
+            tma_store_3d(&tmC, stg + buf * DX_STG, t.m * BM, t.n * BT, tb);
+            bulk_commit();
+          }
+        }
+        if (p.g_sum) {
+#pragma unroll
+          for (int j = 0; j < HB; ++j) {
+            const int b = b0 + j;
+            if (b < p.B) p.g_sum[(size_t)b * p.p_prev + row] = __float2bfloat16_rn(gs[j]);
           }
         }
       } else if (MODE == ENC) {
@@ -731,10 +805,10 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         const int rr = valid ? row : 0;
         const float m = p.mu[rr];
         const int i = rr / p.E;
-        const int half = p.BN >> 1;
-        const int c0 = g * half;
+        const int qc = p.BN / NUM_EPI_GROUPS;   // BN is a multiple of 16: qc of 8
+        const int c0 = g * qc;
         float pm = 0.f, ps = 0.f;
-        for (int j0 = 0; j0 < half; j0 += 8) {
+        for (int j0 = 0; j0 < qc; j0 += 8) {
           uint32_t r[8];
           tmem_ld8(taddr + c0 + j0, r);
           float av[8], sv[8];
@@ -760,11 +834,11 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         if (valid) {
           const float sg = p.sigma[row];
           const float sg2 = __fmul_rn(sg, sg), sg3 = __fmul_rn(sg2, sg);
-          p.partial[(((size_t)t.n * 2 + g) * p.K0 + row) * 2 + 0] = __fdiv_rn(pm, sg2);
-          p.partial[(((size_t)t.n * 2 + g) * p.K0 + row) * 2 + 1] = __fdiv_rn(ps, sg3);
+          p.partial[(((size_t)t.n * NUM_EPI_GROUPS + g) * p.K0 + row) * 2 + 0] = __fdiv_rn(pm, sg2);
+          p.partial[(((size_t)t.n * NUM_EPI_GROUPS + g) * p.K0 + row) * 2 + 1] = __fdiv_rn(ps, sg3);
         }
-      } else {  // DW: group g writes columns [GC g, GC g + GC) of the unit (GC = 128, or 256 for DW2)
-        constexpr int GC = DW2 ? DW_BN : DW_BN / 2;
+      } else {  // DW: group g writes columns [GC g, GC g + GC) of the unit (GC = 64, or 128 for DW2)
+        constexpr int GC = (DW2 ? 2 * DW_BN : DW_BN) / NUM_EPI_GROUPS;
         const int c0 = g * GC;
         const int col0 = t.n * dw_unit_cols(CG) + c0;
         float* dst = p.dw_part + (size_t)t.split * p.split_stride + (size_t)row * p.ldp + col0;
@@ -792,6 +866,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       }
       if (titer == 0 && warp == EPI_WARP0 && lane == 0) trace_stamp(p, 7);
     }
+    if (MODE == DX && warp == EPI_WARP0 && lane == 0) bulk_wait_all();   // staged stores done before exit
   }
   tc_fence_before();
   if (threadIdx.x == 0) trace_stamp(p, 8);
@@ -840,7 +915,7 @@ static EncodeTiledFn encode_fn() {
 
 // bf16 tensor map, 128B swizzle, dims/strides listed innermost first (strides in bytes, rank-1 of them)
 static int make_map(CUtensorMap* m, const void* base, int rank, const uint64_t* dims, const uint64_t* strides,
-                    const uint32_t* box) {
+                    const uint32_t* box, CUtensorMapSwizzle swz = CU_TENSOR_MAP_SWIZZLE_128B) {
   EncodeTiledFn fn = encode_fn();
   if (!fn) { set_error("cuTensorMapEncodeTiled unavailable"); return SPIKERL_E_CUDA; }
   cuuint64_t gd[3], gs[2];
@@ -848,11 +923,28 @@ static int make_map(CUtensorMap* m, const void* base, int rank, const uint64_t* 
   for (int i = 0; i < rank; ++i) { gd[i] = dims[i]; bx[i] = box[i]; }
   for (int i = 0; i < rank - 1; ++i) gs[i] = strides[i];
   CUresult r = fn(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, rank, const_cast<void*>(base), gd, gs, bx, es,
-                  CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                  CU_TENSOR_MAP_INTERLEAVE_NONE, swz, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) { set_error("cuTensorMapEncodeTiled failed (%d)", (int)r); return SPIKERL_E_CUDA; }
   return SPIKERL_OK;
 }
+
+}  // namespace tc
+
+// u32 tensor map without swizzle (bit planes staged by TMA outside the GEMM engine)
+int make_u32_map3(CUtensorMap* m, const void* base, const uint64_t* dims, const uint64_t* strides, const uint32_t* box) {
+  tc::EncodeTiledFn fn = tc::encode_fn();
+  if (!fn) { set_error("cuTensorMapEncodeTiled unavailable"); return SPIKERL_E_CUDA; }
+  cuuint64_t gd[3] = {dims[0], dims[1], dims[2]}, gs[2] = {strides[0], strides[1]};
+  cuuint32_t bx[3] = {box[0], box[1], box[2]}, es[3] = {1, 1, 1};
+  CUresult r = fn(m, CU_TENSOR_MAP_DATA_TYPE_UINT32, 3, const_cast<void*>(base), gd, gs, bx, es,
+                  CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+                  CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) { set_error("cuTensorMapEncodeTiled (u32) failed (%d)", (int)r); return SPIKERL_E_CUDA; }
+  return SPIKERL_OK;
+}
+
+namespace tc {
 
 // Co-resident CTA pairs: every tc_kernel instance uses one CTA per SM (SMEM_BYTES), so one query
 // answers for all; cached so the split-K plan and the launch always agree.
@@ -892,7 +984,7 @@ static bool pairs_enabled() {
 }
 
 template <int MODE, int BT, int CG>
-static int launch_cg(const CUtensorMap& ma, const CUtensorMap& mb, const Params& p, cudaStream_t st) {
+static int launch_cg(const CUtensorMap& ma, const CUtensorMap& mb, const CUtensorMap& mc, const Params& p, cudaStream_t st) {
   static bool attr = false;
   if (!attr) {
     cudaError_t e =
@@ -903,7 +995,7 @@ static int launch_cg(const CUtensorMap& ma, const CUtensorMap& mb, const Params&
   if (CG == 1) {
     const int ncta = num_sms();
     const int grid = p.n_units < ncta ? (int)p.n_units : ncta;
-    pdl((tc_kernel<MODE, BT, CG>), grid, NUM_THREADS, SMEM_BYTES, st)(ma, mb, p);
+    pdl((tc_kernel<MODE, BT, CG>), grid, NUM_THREADS, SMEM_BYTES, st)(ma, mb, mc, p);
   } else {
     cudaLaunchConfig_t cfg = {};
     cfg.blockDim = dim3(NUM_THREADS, 1, 1);
@@ -923,7 +1015,7 @@ static int launch_cg(const CUtensorMap& ma, const CUtensorMap& mb, const Params&
     const int slots = pair_slots();
     const long long grid = p.n_units < slots ? p.n_units : slots;
     cfg.gridDim = dim3((unsigned)(grid * CG), 1, 1);
-    cudaError_t e = cudaLaunchKernelEx(&cfg, tc_kernel<MODE, BT, CG>, ma, mb, p);
+    cudaError_t e = cudaLaunchKernelEx(&cfg, tc_kernel<MODE, BT, CG>, ma, mb, mc, p);
     if (e != cudaSuccess) { set_error("cudaLaunchKernelEx (pair): %s", cudaGetErrorString(e)); return SPIKERL_E_CUDA; }
   }
   SPK_LAUNCHED();
@@ -938,22 +1030,24 @@ static int trace_launch() {   // 1-based index of the launch to trace (0 = off)
 }
 
 template <int MODE, int BT>
-static int launch(const CUtensorMap& ma, const CUtensorMap& mb, const Params& p0, cudaStream_t st) {
+static int launch(const CUtensorMap& ma, const CUtensorMap& mb, const CUtensorMap& mc, const Params& p0, cudaStream_t st) {
   Params p = p0;
   p.trace = (trace_launch() > 0 && ++g_launch_no == trace_launch()) ? 1 : 0;
   static const int dbg = [] { const char* e = getenv("SPIKERL_TC_DBG"); return e ? atoi(e) : 0; }();
   p.dbg = dbg;
-  return p.cg == 2 ? launch_cg<MODE, BT, 2>(ma, mb, p, st) : launch_cg<MODE, BT, 1>(ma, mb, p, st);
+  return p.cg == 2 ? launch_cg<MODE, BT, 2>(ma, mb, mc, p, st) : launch_cg<MODE, BT, 1>(ma, mb, mc, p, st);
 }
 
 template <int MODE>
-static int launch_bt(int bt, const CUtensorMap& ma, const CUtensorMap& mb, const Params& p, cudaStream_t st) {
-  if (MODE == ENC || MODE == DW) return launch<MODE, 8>(ma, mb, p, st);
+static int launch_bt(int bt, const CUtensorMap& ma, const CUtensorMap& mb, const Params& p, cudaStream_t st,
+                     const CUtensorMap* mc = nullptr) {
+  const CUtensorMap& c = mc ? *mc : ma;   // store map (DX only)
+  if (MODE == ENC || MODE == DW) return launch<MODE, 8>(ma, mb, c, p, st);
   switch (bt) {
-    case 8: return launch<MODE, 8>(ma, mb, p, st);
-    case 16: return launch<MODE, 16>(ma, mb, p, st);
+    case 8: return launch<MODE, 8>(ma, mb, c, p, st);
+    case 16: return launch<MODE, 16>(ma, mb, c, p, st);
     case 32:
-      if constexpr (MODE == FWD) return launch<MODE, 32>(ma, mb, p, st);
+      if constexpr (is_fwd(MODE)) return launch<MODE, 32>(ma, mb, c, p, st);
       break;
   }
   set_error("unsupported batch tile %d", bt);
@@ -1013,7 +1107,7 @@ int launch_lif_fwd_tc(const ActorDims& d, int l, int B, const uint32_t* bits_in,
   const uint32_t box[2] = {64, 128};
   SPK_TRY(make_map(&ma, Wb16, 2, dims, strides, box));
   mb = ma;
-  return launch_bt<FWD>(p.Bt, ma, mb, p, st);
+  return l == 3 ? launch_bt<FWDO>(p.Bt, ma, mb, p, st) : launch_bt<FWD>(p.Bt, ma, mb, p, st);
 }
 
 // dX of layer l fused with the reverse scan of layer l-1 (G_l bf16 [T][B][P_l])
@@ -1050,7 +1144,14 @@ int launch_lif_dx_tc(const ActorDims& d, int l, int B, const void* Gl, const __n
     const uint32_t box[3] = {64, (uint32_t)p.Bt, (uint32_t)(d.T / p.cg)};
     SPK_TRY(make_map(&mb, Gl, 3, dims, strides, box));
   }
-  return launch_bt<DX>(p.Bt, ma, mb, p, st);
+  CUtensorMap mc;
+  {  // C = G_{l-1} [T][B][P_{l-1}]: the epilogue's staged chunks of DX_CH steps x Bt rows x 128 neurons
+    const uint64_t dims[3] = {(uint64_t)d.P[l - 1], (uint64_t)B, (uint64_t)d.T};
+    const uint64_t strides[2] = {(uint64_t)d.P[l - 1] * 2, (uint64_t)d.P[l - 1] * 2 * B};
+    const uint32_t box[3] = {128, (uint32_t)p.Bt, (uint32_t)DX_CH};
+    SPK_TRY(make_map(&mc, Gprev, 3, dims, strides, box, CU_TENSOR_MAP_SWIZZLE_NONE));
+  }
+  return launch_bt<DX>(p.Bt, ma, mb, p, st, &mc);
 }
 
 static int enc_cg(const ActorDims& d) { return (pairs_enabled() && (d.P[0] / BM) % 2 == 0) ? 2 : 1; }
@@ -1069,7 +1170,7 @@ static int enc_bn(const ActorDims& d, int B) {
 }
 
 size_t tc_enc_partial_bytes(const ActorDims& d, int B) {
-  return sizeof(float) * 2 * 2 * (size_t)cdiv(B, enc_bn(d, B)) * d.K0;   // 2 epilogue groups per N tile
+  return sizeof(float) * 2 * NUM_EPI_GROUPS * (size_t)cdiv(B, enc_bn(d, B)) * d.K0;   // per epilogue group and N tile
 }
 
 int launch_enc_grad_tc(const ActorDims& d, int B, const void* Gsum, const __nv_bfloat16* W1b16, const float* A,
@@ -1099,7 +1200,7 @@ int launch_enc_grad_tc(const ActorDims& d, int B, const void* Gsum, const __nv_b
     SPK_TRY(make_map(&mb, Gsum, 2, dims, strides, box));
   }
   SPK_TRY(launch_bt<ENC>(8, ma, mb, p, st));
-  return launch_enc_grad_reduce(d, 2 * p.n_tiles, partial, dmu, dsigma, accumulate, st);
+  return launch_enc_grad_reduce(d, NUM_EPI_GROUPS * p.n_tiles, partial, dmu, dsigma, accumulate, st);
 }
 
 // split-K plan for dW_l: pick the split count s minimising a simple cost model in units of one

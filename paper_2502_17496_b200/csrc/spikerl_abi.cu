@@ -120,10 +120,10 @@ TapeLayout tape_layout(const ActorDims& d, int B) {
   L.tpad = round_up(d.T, 16);
   for (int l = 0; l < 4; ++l) { L.bitsT[l] = 0; L.maskT[l] = 0; }
   if (d.engine == SPIKERL_ENGINE_TCGEN05) {
-    const size_t octets = (size_t)round_up(B, 32) / 8;
+    const size_t quads = (size_t)round_up(B, 32) / 4;
     for (int l = 1; l <= 2; ++l) {
-      L.bitsT[l] = take(octets * d.P[l] * L.tpad);
-      L.maskT[l] = take(octets * d.P[l] * L.tpad);
+      L.bitsT[l] = take(quads * d.P[l] * (L.tpad / 2));
+      L.maskT[l] = take(quads * d.P[l] * (L.tpad / 2));
     }
   }
   L.total = o;

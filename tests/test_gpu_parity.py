@@ -234,7 +234,7 @@ def test_fused_small_batch_forward_subprocess():
 
 @pytest.mark.parametrize("B", [100, 257])
 def test_neuron_major_planes_are_transposes(B):
-    """tcgen05 engine: the octet-major spike/mask copies read by the fused dX epilogue hold
+    """tcgen05 engine: the quad-major spike/mask copies read by the fused dX epilogue hold
     exactly the transposed bits of the batch-major planes (bit-exact, ragged batch)."""
     import torch
     import paper_2502_17496_b200 as pk
@@ -248,9 +248,11 @@ def test_neuron_major_planes_are_transposes(B):
     for l in (1, 2):
         for a, bname in ((f"bits{l}", f"bitsT{l}"), (f"mask{l}", f"maskT{l}")):
             bm = pk.unpack_bits(v[a], v[a].shape[-1] * 32)              # [T][B][P]
-            raw = v[bname].cpu().numpy()                                # [O][P][tpad] bytes
-            bits = np.unpackbits(raw[..., None], axis=-1, bitorder="little")   # [O][P][tpad][8]
-            nm = bits.transpose(2, 1, 0, 3).reshape(raw.shape[2], raw.shape[1], -1)  # [tpad][P][O*8]
+            raw = v[bname].cpu().numpy()                                # [Q][P][tpad/2] bytes
+            bits = np.unpackbits(raw[..., None], axis=-1, bitorder="little")   # [Q][P][tpad/2][8]
+            Q, P = raw.shape[0], raw.shape[1]
+            bits = bits.reshape(Q, P, raw.shape[2] * 2, 4)               # nibble s = step s
+            nm = bits.transpose(2, 1, 0, 3).reshape(raw.shape[2] * 2, P, -1)  # [tpad][P][Q*4]
             T = shape.T
             assert np.array_equal(nm[:T, :, :B], bm.transpose(0, 2, 1)), (l, a)
             assert not nm[:T, :, B:].any() and not nm[T:].any()
