@@ -16,8 +16,8 @@ bash tools/profile_cfg1.sh > $O/plain1.log 2>&1 && \
 bash tools/profile_cfg4.sh > $O/plain4.log 2>&1 && \
   ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file $O/launches_cfg4.csv bash tools/profile_cfg4.sh > $O/ncu_l4.log 2>&1
 # full captures: FWD L1, DW L1, DX L2, enc_fwd, outscan, adam (the HBM kernels run by bench's hbm_kernels)
-bash tools/profile_cfg4_tc.sh fwd1:0:0 dw1:3:2 dx2:1:1
-for k in enc_fwd dec_bwd_outscan adam_kernel; do
+bash tools/profile_cfg4_tc.sh fwd1:0:0 fwd2:0:1 dw1:3:2 dx2:1:1 dx3:1:0
+for k in enc_fwd dec_bwd_outscan adam_kernel polyak_kernel; do
   ncu --set full --clock-control none --import-source on -k regex:$k -c 1 -o $O/prof_$k bash tools/profile_cfg4.sh > $O/ncu_$k.log 2>&1
 done
 ls -la $O
