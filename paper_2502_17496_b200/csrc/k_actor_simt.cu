@@ -269,7 +269,7 @@ __device__ __forceinline__ void tma3(const CUtensorMap* m, void* dst, uint64_t* 
 }
 }  // namespace osc
 
-template <typename GTy>
+template <typename GTy, int TT>
 __global__ void __launch_bounds__(256) dec_bwd_outscan_tma_kernel(
     const __grid_constant__ CUtensorMap map_o, const __grid_constant__ CUtensorMap map_h, int B, int T, int A,
     int D, int N3, int W3, int NO, int R, int planeS, float dcc, float dvc, float zh,
@@ -288,6 +288,7 @@ __global__ void __launch_bounds__(256) dec_bwd_outscan_tma_kernel(
   __syncthreads();
   pdl_wait();
   pdl_trigger();
+  if (TT > 0) T = TT;   // compile-time T: the step loop unrolls completely
   const uint32_t txb = 2u * (uint32_t)T * (uint32_t)R * (uint32_t)W3 * 4u;   // whole boxes (OOB rows count)
   auto issue = [&](int unit, int bi) {
     uint32_t* d0 = sbuf + (size_t)(2 * bi) * planeS;
@@ -302,6 +303,28 @@ __global__ void __launch_bounds__(256) dec_bwd_outscan_tma_kernel(
   const bool live = n0 < N3 || write_pad;
   const size_t gts = (size_t)B * P3;
   const int tstr = R * W3;
+  // This thread's octet is fixed: with D >= 8 it spans at most two action populations (a0 for
+  // i < split, a0 + 1 after), so its 8 decoder weights are loaded once and each row needs only the
+  // pre-activation gradients of two actions, requested one unit ahead (ncu r01: the per-unit loads
+  // of act / grad_a and the per-neuron action walk were ~45% of the kernel's stall samples)
+  const bool two_max = D >= 8;
+  const int a0 = n0 / D, split = D - (n0 - a0 * D);
+  const bool has1 = two_max && split < 8 && n0 + split < N3;
+  float w8[8];
+#pragma unroll
+  for (int i = 0; i < 8; ++i) w8[i] = (two_max && n0 + i < N3) ? Wd[n0 + i] : 0.f;   // Wd[a][e] at a D + e = n
+  const bool pow2T = (T & (T - 1)) == 0;   // g / T is then an exact multiply
+  const float invT = 1.0f / (float)T;
+  float nav0 = 0.f, nga0 = 0.f, nav1 = 0.f, nga1 = 0.f;   // next unit's act / grad_a of a0, a0 + 1
+  auto prefetch = [&](int unit) {
+    const int bn = unit * R + r;
+    if (two_max && unit < units && bn < B && n0 < N3) {
+      nav0 = act[(size_t)bn * A + a0];
+      nga0 = grad_a[(size_t)bn * A + a0];
+      if (has1) { nav1 = act[(size_t)bn * A + a0 + 1]; nga1 = grad_a[(size_t)bn * A + a0 + 1]; }
+    }
+  };
+  prefetch(blockIdx.x);
   int it = 0;
   for (int u = blockIdx.x; u < units; u += gridDim.x, ++it) {
     const int bi = it & 1;
@@ -310,10 +333,20 @@ __global__ void __launch_bounds__(256) dec_bwd_outscan_tma_kernel(
       issue(u + gridDim.x, bi ^ 1);
     }
     const int b = u * R + r;
-    // g_o3 = g_fr / T = g_pre_a Wd[a][d] / T (constant in t), window factor z folded in; the
-    // loads overlap the TMA copy of this unit's planes
+    // g_o3 = g_fr / T = g_pre_a Wd[a][d] / T (constant in t), window factor z folded in
     float g[8];
-    if (b < B) {
+    if (b < B && two_max) {
+      const float gp0 = __fmul_rn(nga0, __fsub_rn(1.0f, __fmul_rn(nav0, nav0)));
+      const float gp1 = __fmul_rn(nga1, __fsub_rn(1.0f, __fmul_rn(nav1, nav1)));
+      prefetch(u + gridDim.x);
+      if (n0 < N3 && split == D) g_pre_out[(size_t)b * A + a0] = gp0;       // the octet starts action a0
+      if (has1) g_pre_out[(size_t)b * A + a0 + 1] = gp1;                    // ... or contains a0 + 1's start
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        const float x = __fmul_rn(i < split ? gp0 : gp1, w8[i]);
+        g[i] = __fmul_rn(zh, pow2T ? __fmul_rn(x, invT) : __fdiv_rn(x, (float)T));
+      }
+    } else if (b < B) {
       int a = n0 / D, e = n0 - a * D;
       float gp = 0.f;
       if (n0 < N3) {
@@ -343,7 +376,7 @@ __global__ void __launch_bounds__(256) dec_bwd_outscan_tma_kernel(
 #pragma unroll
       for (int i = 0; i < 8; ++i) { dvn[i] = 0.f; dcn[i] = 0.f; }
       GTy* gq = G3 + (size_t)b * P3 + n0 + (size_t)(T - 1) * gts;
-#pragma unroll 2
+#pragma unroll (TT > 0 ? TT : 2)
       for (int t = T - 1; t >= 0; --t) {
         const uint32_t o8 = (so[t * tstr] >> sh) & 0xFFu, h8 = (sm[t * tstr] >> sh) & 0xFFu;
         float G[8];
@@ -398,11 +431,9 @@ int launch_dec_bwd_outscan(const ActorDims& d, int B, const float* grad_a, const
     const size_t smem = (size_t)16 * planeS + 16;
     const int threads = NO * R;
     auto launch = [&](auto kern, auto* G) -> int {
-      static bool attr = false;
-      if (!attr) {
-        SPK_CHECK_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 100 * 1024));
-        attr = true;
-      }
+      // per launch: the T-specialised kernels share one function-pointer type, so a static "done"
+      // flag here would cover only the first of them
+      SPK_CHECK_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 100 * 1024));
       int per_sm = 0;
       if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, threads, smem) != cudaSuccess || per_sm < 1) {
         cudaGetLastError();
@@ -416,8 +447,12 @@ int launch_dec_bwd_outscan(const ActorDims& d, int B, const float* grad_a, const
       SPK_LAUNCHED();
       return SPIKERL_OK;
     };
-    if (d.bf16) return launch(dec_bwd_outscan_tma_kernel<__nv_bfloat16>, (__nv_bfloat16*)G3);
-    return launch(dec_bwd_outscan_tma_kernel<float>, (float*)G3);
+    if (d.bf16) {
+      if (d.T == 16) return launch(dec_bwd_outscan_tma_kernel<__nv_bfloat16, 16>, (__nv_bfloat16*)G3);
+      if (d.T == 5) return launch(dec_bwd_outscan_tma_kernel<__nv_bfloat16, 5>, (__nv_bfloat16*)G3);
+      return launch(dec_bwd_outscan_tma_kernel<__nv_bfloat16, 0>, (__nv_bfloat16*)G3);
+    }
+    return launch(dec_bwd_outscan_tma_kernel<float, 0>, (float*)G3);
   }
   const long long units = (long long)cdiv(B, 2) * (d.Wd[3] / 4);   // warps of work
   long long blocks = cdiv(units, 8);

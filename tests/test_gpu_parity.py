@@ -486,3 +486,32 @@ def test_device_replay_and_rng():
     assert set(np.unique(d)) <= {0.0, 1.0} and abs(d.mean() - 0.01) < 0.002
     r2 = pk.replay_fill(n, 17, 6, seed=5, rank=1)
     assert not torch.equal(r.s, r2.s)
+
+
+@pytest.mark.parametrize("preset,B,T", [("cfg1", 256, 5), ("cfg3s", 100, 16), ("cfg0", 37, 7)])
+def test_staged_output_scan_matches_direct_subprocess(preset, B, T, tmp_path):
+    """The TMA-staged output-layer reverse scan (default) and the direct-load kernel
+    (SPIKERL_OUTSCAN_DIRECT=1, a subprocess) produce bit-identical actor gradients: same per-element
+    arithmetic, only the staging of the spike / mask words and the action gradients differs."""
+    import os, subprocess, sys
+    shape, _, _ = sg.preset(preset)
+    shape = sg.with_(shape, T=T)
+    p, s, g = _inputs(shape, B)
+    here = run_gpu_actor(shape, B, p, s, g)
+    code = (
+        "import numpy as np, pickle, synthgen as sg\n"
+        "from tests._parity import run_gpu_actor\n"
+        f"shape, _, _ = sg.preset({preset!r}); shape = sg.with_(shape, T={T})\n"
+        f"d = pickle.load(open({str(tmp_path / 'in.pkl')!r}, 'rb'))\n"
+        f"out = run_gpu_actor(shape, {B}, d['p'], d['s'], d['g'])\n"
+        f"pickle.dump(out['grads'], open({str(tmp_path / 'out.pkl')!r}, 'wb'))\n"
+        "print('direct ok')\n")
+    import pickle
+    pickle.dump(dict(p=p, s=s, g=g), open(tmp_path / "in.pkl", "wb"))
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    r = subprocess.run([sys.executable, "-c", code], cwd=root, capture_output=True, text=True, timeout=600,
+                       env=dict(os.environ, SPIKERL_OUTSCAN_DIRECT="1", PYTHONPATH=root))
+    assert r.returncode == 0 and "direct ok" in r.stdout, r.stdout[-2000:] + r.stderr[-2000:]
+    other = pickle.load(open(tmp_path / "out.pkl", "rb"))
+    for k in here["grads"]:
+        assert np.array_equal(here["grads"][k], other[k]), k
