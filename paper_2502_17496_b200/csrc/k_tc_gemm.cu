@@ -733,8 +733,8 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         // G_{l-1} leaves through shared memory: DX_CH steps x BT rows x 128 neurons per TMA store.
         constexpr int HB = epi_hb(BT);
         constexpr int NQ = HB / 4;
-        static_assert(BT / HB == NUM_EPI_GROUPS, "every DX epilogue group owns HB batch rows");
-        const int jb = g * HB;
+        const bool act = g < BT / HB;   // idle groups (BT = 8 with 4 groups) still join the barriers
+        const int jb = act ? g * HB : 0;
         const int b0 = t.n * BT + jb;
         const float zh = p.zh, dvc = p.kc.dv, dcc = p.kc.dc;
         float dvn[HB], dcn[HB], gs[HB];
@@ -765,7 +765,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
 #pragma unroll
           for (int ci = DX_CH - 1; ci >= 0; --ci) {
             const int tt = tb + ci;
-            if (tt >= p.T) continue;
+            if (tt >= p.T || !act) continue;
             if ((tt >> 4) != ch) {
               ch = tt >> 4;
 #pragma unroll
@@ -792,7 +792,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
             bulk_commit();
           }
         }
-        if (p.g_sum) {
+        if (p.g_sum && act) {
 #pragma unroll
           for (int j = 0; j < HB; ++j) {
             const int b = b0 + j;
@@ -805,15 +805,16 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         const int rr = valid ? row : 0;
         const float m = p.mu[rr];
         const int i = rr / p.E;
-        const int qc = p.BN / NUM_EPI_GROUPS;   // BN is a multiple of 16: qc of 8
+        constexpr int EJ = NUM_EPI_GROUPS == 2 ? 8 : 4;   // BN is a multiple of 16: qc of EJ
+        const int qc = p.BN / NUM_EPI_GROUPS;
         const int c0 = g * qc;
         float pm = 0.f, ps = 0.f;
-        for (int j0 = 0; j0 < qc; j0 += 8) {
-          uint32_t r[8];
-          tmem_ld8(taddr + c0 + j0, r);
-          float av[8], sv[8];
+        for (int j0 = 0; j0 < qc; j0 += EJ) {
+          uint32_t r[EJ];
+          tmem_ldn<EJ>(taddr + c0 + j0, r);
+          float av[EJ], sv[EJ];
 #pragma unroll
-          for (int jj = 0; jj < 8; ++jj) {
+          for (int jj = 0; jj < EJ; ++jj) {
             const int b = t.n * p.BN + c0 + j0 + jj;
             const int bb = b < p.B ? b : 0;
             av[jj] = __ldg(p.A + (size_t)bb * p.K0 + rr);
@@ -821,7 +822,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
           }
           tmem_ld_wait();
 #pragma unroll
-          for (int jj = 0; jj < 8; ++jj) {
+          for (int jj = 0; jj < EJ; ++jj) {
             const int b = t.n * p.BN + c0 + j0 + jj;
             if (b < p.B) {
               const float dd = __fsub_rn(sv[jj], m);
