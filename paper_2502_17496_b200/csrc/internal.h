@@ -20,8 +20,9 @@ int launch_dec_fwd(const ActorDims& d, int B, const uint8_t* counts, const float
 int launch_dec_bwd_outscan(const ActorDims& d, int B, const float* grad_a, const float* act,
                            const uint8_t* counts, const float* Wd, const uint32_t* bits3,
                            const uint32_t* mask3, void* G3, float* g_pre, cudaStream_t st);
+int dec_param_chunks(int B);   // row chunks of the decoder parameter gradient (partials: chunks x (N3 + A))
 int launch_dec_param_grads(const ActorDims& d, int B, const float* g_pre, const uint8_t* counts,
-                           float* dWd, float* dbd, int accumulate, cudaStream_t st);
+                           float* dWd, float* dbd, float* part, int accumulate, cudaStream_t st);
 // dX of layer l (3 or 2) fused with the reverse scan of layer l-1 -> G_{l-1} (+Gsum if l==2)
 int launch_lif_dx_simt(const ActorDims& d, int l, int B, const void* Gl, const float* Wf32,
                        const __nv_bfloat16* Wb16, const uint32_t* bits_prev,

@@ -472,8 +472,73 @@ int launch_dec_bwd_outscan(const ActorDims& d, int B, const float* grad_a, const
   return SPIKERL_OK;
 }
 
-// dbd[j] = sum_b g_pre[b][j];  dWd[j][e] = sum_b g_pre[b][j] * cnt[b][jD+e] / T.
-// One block per (j, e) (e == D row computes dbd); fixed-order block tree reduction.
+// dbd[j] = sum_b g_pre[b][j];  dWd[j][e] = sum_b g_pre[b][j] * cnt[b][jD+e] / T  (SPEC.md:168-176).
+// Large B: two fixed-order passes (run-to-run deterministic): a block sums a contiguous chunk of rows for
+// every output column (thread = column: the count bytes of a row are read coalesced, g_pre words
+// broadcast), then one thread per column adds the chunk partials in chunk order. One chunk writes
+// the result directly. (ncu r01: the former one-block-per-(j, e) kernel read the counts with a
+// 170-byte stride and ran a 256-long dependent sum per thread: 0.17 ms at configs[4].)
+constexpr int kDecRows = 128;   // rows per chunk (at least; chunks are capped at 4 per SM)
+int dec_param_chunks(int B) {
+  if (B <= 2048) return 1;   // latency regime: one block, no second launch
+  const int c = cdiv(B, kDecRows), cap = 4 * num_sms();
+  return c < cap ? c : cap;
+}
+
+__global__ void __launch_bounds__(256) dec_param_partial_kernel(int B, int A, int D, int T, int rows,
+                                                                const float* __restrict__ g_pre,
+                                                                const uint8_t* __restrict__ counts,
+                                                                float* __restrict__ part, float* __restrict__ dWd,
+                                                                float* __restrict__ dbd, int accum) {
+  pdl_wait();
+  pdl_trigger();
+  // thread = (column c of a 32-column group, row lane rl of 8): a lane sums every 8th row of the
+  // chunk (4 rows' loads in flight), the 8 lanes are added in lane order through shared memory
+  __shared__ float red[8][33];
+  const int N3 = A * D, NC = N3 + A;
+  const int c = threadIdx.x & 31, rl = threadIdx.x >> 5;
+  const int b0 = blockIdx.x * rows, b1 = min(B, b0 + rows);
+  for (int n0 = 0; n0 < NC; n0 += 32) {
+    const int n = n0 + c;
+    const bool live = n < NC, bias = n >= N3;
+    const int j = bias ? n - N3 : n / D;
+    float s = 0.f;
+    if (live) {
+      int b = b0 + rl;
+      for (; b + 24 < b1; b += 32) {
+        float gp[4], cn[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          gp[u] = g_pre[(size_t)(b + 8 * u) * A + j];
+          cn[u] = bias ? 1.f : (float)counts[(size_t)(b + 8 * u) * N3 + n];
+        }
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+          s = bias ? __fadd_rn(s, gp[u]) : __fadd_rn(s, __fmul_rn(gp[u], cn[u] / (float)T));
+      }
+      for (; b < b1; b += 8) {
+        const float gp = g_pre[(size_t)b * A + j];
+        s = bias ? __fadd_rn(s, gp) : __fadd_rn(s, __fmul_rn(gp, (float)counts[(size_t)b * N3 + n] / (float)T));
+      }
+    }
+    red[rl][c] = s;
+    __syncthreads();
+    if (rl == 0 && live) {
+      float t = 0.f;
+#pragma unroll
+      for (int q = 0; q < 8; ++q) t = __fadd_rn(t, red[q][c]);
+      if (gridDim.x == 1) {
+        float* dst = bias ? (dbd + j) : (dWd + n);   // Wd[j][e] sits at j D + e = n
+        *dst = accum ? __fadd_rn(*dst, t) : t;
+      } else {
+        part[(size_t)blockIdx.x * NC + n] = t;
+      }
+    }
+    __syncthreads();
+  }
+}
+
+// latency regime (B <= 2048): one block per (j, e), e == D the bias; fixed-order tree reduction
 __global__ void __launch_bounds__(256) dec_param_grads_kernel(int B, int A, int D, int T,
                                                               const float* __restrict__ g_pre,
                                                               const uint8_t* __restrict__ counts,
@@ -502,12 +567,36 @@ __global__ void __launch_bounds__(256) dec_param_grads_kernel(int B, int A, int 
   }
 }
 
+__global__ void dec_param_reduce_kernel(int A, int D, int chunks, const float* __restrict__ part,
+                                        float* __restrict__ dWd, float* __restrict__ dbd, int accum) {
+  pdl_wait();
+  pdl_trigger();
+  const int N3 = A * D, NC = N3 + A;
+  const int n = blockIdx.x * blockDim.x + threadIdx.x;
+  if (n >= NC) return;
+  float s = 0.f;
+  for (int c = 0; c < chunks; ++c) s = __fadd_rn(s, part[(size_t)c * NC + n]);
+  float* dst = n >= N3 ? (dbd + (n - N3)) : (dWd + n);
+  *dst = accum ? __fadd_rn(*dst, s) : s;
+}
+
 int launch_dec_param_grads(const ActorDims& d, int B, const float* g_pre, const uint8_t* counts,
-                           float* dWd, float* dbd, int accumulate, cudaStream_t st) {
+                           float* dWd, float* dbd, float* part, int accumulate, cudaStream_t st) {
   ProfScope ps_("dec_param_grads", PB_LATENCY, 0.0, (double)B * (4.0 * d.A + d.N3), st);
-  dim3 grid(d.A, d.D + 1);
-  pdl(dec_param_grads_kernel, grid, 256, 0, st)(B, d.A, d.D, d.T, g_pre, counts, dWd, dbd, accumulate);
+  const int chunks = dec_param_chunks(B), rows = cdiv(B, chunks), NC = d.N3 + d.A;
+  if (chunks == 1) {
+    pdl(dec_param_grads_kernel, dim3(d.A, d.D + 1), 256, 0, st)(B, d.A, d.D, d.T, g_pre, counts, dWd, dbd,
+                                                               accumulate);
+    SPK_LAUNCHED();
+    return SPIKERL_OK;
+  }
+  pdl(dec_param_partial_kernel, chunks, 256, 0, st)(B, d.A, d.D, d.T, rows, g_pre, counts, part, dWd, dbd,
+                                                   accumulate);
   SPK_LAUNCHED();
+  if (chunks > 1) {
+    pdl(dec_param_reduce_kernel, cdiv(NC, 256), 256, 0, st)(d.A, d.D, chunks, part, dWd, dbd, accumulate);
+    SPK_LAUNCHED();
+  }
   return SPIKERL_OK;
 }
 

@@ -809,26 +809,42 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         const int qc = p.BN / NUM_EPI_GROUPS;
         const int c0 = g * qc;
         float pm = 0.f, ps = 0.f;
-        for (int j0 = 0; j0 < qc; j0 += EJ) {
-          uint32_t r[EJ];
-          tmem_ldn<EJ>(taddr + c0 + j0, r);
-          float av[EJ], sv[EJ];
+        // A and s for the columns of chunk c + PD - 1 are requested while chunk c is summed (ncu r01:
+        // loaded right before use, one HBM latency per 8-column chunk paced this epilogue at ~15 us
+        // per unit); the sum stays in increasing b
+        constexpr int PD = 3;
+        const int nch = qc / EJ;
+        float av[PD][EJ], sv[PD][EJ];
+        auto ldc = [&](float (&a)[EJ], float (&sx)[EJ], int ch) {
 #pragma unroll
           for (int jj = 0; jj < EJ; ++jj) {
-            const int b = t.n * p.BN + c0 + j0 + jj;
+            const int b = t.n * p.BN + c0 + ch * EJ + jj;
             const int bb = b < p.B ? b : 0;
-            av[jj] = __ldg(p.A + (size_t)bb * p.K0 + rr);
-            sv[jj] = __ldg(p.obs + (size_t)bb * p.S + i);
+            a[jj] = __ldg(p.A + (size_t)bb * p.K0 + rr);
+            sx[jj] = __ldg(p.obs + (size_t)bb * p.S + i);
           }
-          tmem_ld_wait();
+        };
 #pragma unroll
-          for (int jj = 0; jj < EJ; ++jj) {
-            const int b = t.n * p.BN + c0 + j0 + jj;
-            if (b < p.B) {
-              const float dd = __fsub_rn(sv[jj], m);
-              const float gad = __fmul_rn(__fmul_rn(__uint_as_float(r[jj]), av[jj]), dd);
-              pm = __fadd_rn(pm, gad);
-              ps = __fadd_rn(ps, __fmul_rn(gad, dd));
+        for (int s2 = 0; s2 < PD - 1; ++s2)
+          if (s2 < nch) ldc(av[s2], sv[s2], s2);
+        for (int ch0 = 0; ch0 < nch; ch0 += PD) {
+#pragma unroll
+          for (int s2 = 0; s2 < PD; ++s2) {
+            const int ch = ch0 + s2;
+            if (ch >= nch) break;
+            if (ch + PD - 1 < nch) ldc(av[(s2 + PD - 1) % PD], sv[(s2 + PD - 1) % PD], ch + PD - 1);
+            uint32_t r[EJ];
+            tmem_ldn<EJ>(taddr + c0 + ch * EJ, r);
+            tmem_ld_wait();
+#pragma unroll
+            for (int jj = 0; jj < EJ; ++jj) {
+              const int b = t.n * p.BN + c0 + ch * EJ + jj;
+              if (b < p.B) {
+                const float dd = __fsub_rn(sv[s2][jj], m);
+                const float gad = __fmul_rn(__fmul_rn(__uint_as_float(r[jj]), av[s2][jj]), dd);
+                pm = __fadd_rn(pm, gad);
+                ps = __fadd_rn(ps, __fmul_rn(gad, dd));
+              }
             }
           }
         }

@@ -155,6 +155,7 @@ struct ActorWs {
   size_t G[4];      // G1..G3 [T][B][P_l] (fp32 or bf16); G[0] unused
   size_t Gsum;      // [B][P1]
   size_t g_pre;     // [B][A] fp32
+  size_t dec_part;  // decoder parameter-gradient chunk partials
   size_t enc_part;  // encoder partials
   size_t dw_part[4];   // tcgen05 split-K dW_l partials (one region per layer: the dW run concurrently)
   size_t total;
@@ -170,6 +171,7 @@ static ActorWs actor_ws_layout(const ActorDims& d, int B) {
   for (int l = 1; l <= 3; ++l) w.G[l] = take(gsz * (size_t)d.T * B * d.P[l]);
   w.Gsum = take(gsz * (size_t)B * d.P[1]);
   w.g_pre = take(sizeof(float) * (size_t)B * d.A);
+  w.dec_part = take(sizeof(float) * (size_t)dec_param_chunks(B) * (d.N3 + d.A));
   const bool tc = d.engine == SPIKERL_ENGINE_TCGEN05;
   const size_t ep = enc_grad_partial_bytes(d, B), ept = tc ? tc_enc_partial_bytes(d, B) : 0;
   w.enc_part = take(ep > ept ? ep : ept);
@@ -243,7 +245,7 @@ static int actor_backward_impl(const ActorDims& d, int B, const float* params,
   };
   SPK_TRY(branch(sw[0], 0));
   SPK_TRY(launch_dec_param_grads(d, B, g_pre, counts, grads + d.off[SPIKERL_ACTOR_WD],
-                                 grads + d.off[SPIKERL_ACTOR_BD], accum, sw[0]));
+                                 grads + d.off[SPIKERL_ACTOR_BD], (float*)(ws + W.dec_part), accum, sw[0]));
   for (int l = 3; l >= 1; --l) {
     const float* Wf = params + d.off[SPIKERL_ACTOR_W1 + l - 1];
     const __nv_bfloat16* Wb = d.bf16 ? pb16 + d.boff[l - 1] : nullptr;
