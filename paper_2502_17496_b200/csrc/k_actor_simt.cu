@@ -270,7 +270,7 @@ __device__ __forceinline__ void tma3(const CUtensorMap* m, void* dst, uint64_t* 
 }  // namespace osc
 
 template <typename GTy, int TT>
-__global__ void __launch_bounds__(256) dec_bwd_outscan_tma_kernel(
+__global__ void __launch_bounds__(256, 4) dec_bwd_outscan_tma_kernel(
     const __grid_constant__ CUtensorMap map_o, const __grid_constant__ CUtensorMap map_h, int B, int T, int A,
     int D, int N3, int W3, int NO, int R, int planeS, float dcc, float dvc, float zh,
     const float* __restrict__ grad_a, const float* __restrict__ act, const float* __restrict__ Wd,
@@ -300,8 +300,7 @@ __global__ void __launch_bounds__(256) dec_bwd_outscan_tma_kernel(
   const int o = tid % NO, r = tid / NO;
   const int n0 = 8 * o, w = o >> 2, sh = 8 * (o & 3);
   const int P3 = 32 * W3;
-  const bool live = n0 < N3 || write_pad;
-  const size_t gts = (size_t)B * P3;
+  // every thread's octet is live: NO counts only the octets below N3 (or all of P3 with write_pad)
   const int tstr = R * W3;
   // This thread's octet is fixed: with D >= 8 it spans at most two action populations (a0 for
   // i < split, a0 + 1 after), so its 8 decoder weights are loaded once and each row needs only the
@@ -375,7 +374,9 @@ __global__ void __launch_bounds__(256) dec_bwd_outscan_tma_kernel(
       float dvn[8], dcn[8];
 #pragma unroll
       for (int i = 0; i < 8; ++i) { dvn[i] = 0.f; dcn[i] = 0.f; }
-      GTy* gq = G3 + (size_t)b * P3 + n0 + (size_t)(T - 1) * gts;
+      // G3 element offsets of this row: 32-bit (T B P3 < 2^32 is checked at launch)
+      const uint32_t gts32 = (uint32_t)B * (uint32_t)P3;
+      uint32_t go = (uint32_t)b * (uint32_t)P3 + (uint32_t)n0 + (uint32_t)(T - 1) * gts32;
 #pragma unroll (TT > 0 ? TT : 2)
       for (int t = T - 1; t >= 0; --t) {
         const uint32_t o8 = (so[t * tstr] >> sh) & 0xFFu, h8 = (sm[t * tstr] >> sh) & 0xFFu;
@@ -389,8 +390,8 @@ __global__ void __launch_bounds__(256) dec_bwd_outscan_tma_kernel(
           dcn[i] = dct;
           G[i] = dct;
         }
-        if (live) Pack8<GTy>::store(gq, G);
-        gq -= gts;
+        Pack8<GTy>::store(G3 + go, G);
+        go -= gts32;
       }
     }
     __syncthreads();   // buffer bi is refilled at the top of the next-but-one iteration
@@ -421,7 +422,7 @@ int launch_dec_bwd_outscan(const ActorDims& d, int B, const float* grad_a, const
   int NO, R, planeS;
   outscan_plan(d, wpad, &NO, &R, &planeS);
   static const bool direct = [] { const char* e = getenv("SPIKERL_OUTSCAN_DIRECT"); return e && e[0] == '1'; }();
-  if (R > 0 && !direct) {
+  if (R > 0 && !direct && (unsigned long long)d.T * B * d.P[3] < (1ull << 32)) {
     CUtensorMap mo, mh;
     const uint64_t dims[3] = {(uint64_t)d.Wd[3], (uint64_t)B, (uint64_t)d.T};
     const uint64_t strides[2] = {(uint64_t)d.Wd[3] * 4, (uint64_t)B * d.Wd[3] * 4};
