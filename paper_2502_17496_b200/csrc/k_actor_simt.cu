@@ -479,9 +479,9 @@ int launch_dec_bwd_outscan(const ActorDims& d, int B, const float* grad_a, const
 // broadcast), then one thread per column adds the chunk partials in chunk order. One chunk writes
 // the result directly. (ncu r01: the former one-block-per-(j, e) kernel read the counts with a
 // 170-byte stride and ran a 256-long dependent sum per thread: 0.17 ms at configs[4].)
-constexpr int kDecRows = 128;   // rows per chunk (at least; chunks are capped at 4 per SM)
+constexpr int kDecRows = 32;   // rows per chunk (at least; chunks are capped at 4 per SM)
 int dec_param_chunks(int B) {
-  if (B <= 2048) return 1;   // latency regime: one block, no second launch
+  if (B <= 1024) return 1;   // latency regime: one block per column, no second launch
   const int c = cdiv(B, kDecRows), cap = 4 * num_sms();
   return c < cap ? c : cap;
 }
@@ -539,7 +539,7 @@ __global__ void __launch_bounds__(256) dec_param_partial_kernel(int B, int A, in
   }
 }
 
-// latency regime (B <= 2048): one block per (j, e), e == D the bias; fixed-order tree reduction
+// latency regime (B <= 1024): one block per (j, e), e == D the bias; fixed-order tree reduction
 __global__ void __launch_bounds__(256) dec_param_grads_kernel(int B, int A, int D, int T,
                                                               const float* __restrict__ g_pre,
                                                               const uint8_t* __restrict__ counts,

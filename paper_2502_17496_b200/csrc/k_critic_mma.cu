@@ -194,10 +194,13 @@ __global__ void __launch_bounds__(256) critic_fwd_mma_kernel(
   __shared__ __align__(16) __nv_bfloat16 xs[RB * (512 + SPAD)];
   __shared__ __align__(16) __nv_bfloat16 h1s[RB * (HW + SPAD)];
   __shared__ float red[NWARP][RB];
-  const int z = blockIdx.y, r0 = blockIdx.x * RB, tid = threadIdx.x, warp = tid >> 5;
+  const int z = blockIdx.y, tid = threadIdx.x, warp = tid >> 5;
   const int lane = tid & 31, g = lane >> 2, t = lane & 3;
   const int in = S + A, ldx = inp + SPAD, ldh = HW + SPAD;
   if (ticket && blockIdx.x == 0 && z == 0 && tid == 0) *ticket = 0u;   // for the backward launch
+  // persistent over 16-row tiles: the staged W2 (135 KB, one CTA per SM) serves every tile of this
+  // CTA (large batches: one CTA per 16 rows re-staged W2 512 times per launch at configs[3] B = 4096)
+  for (int r0 = blockIdx.x * RB; r0 < Bp; r0 += gridDim.x * RB) {
   // X tile (bf16-rounded [s; a]); the z == 0 CTAs also write X^T (zeros beyond in / B) for dW1
 #pragma unroll 4
   for (int idx = tid; idx < RB * inp; idx += 256) {
@@ -283,6 +286,8 @@ __global__ void __launch_bounds__(256) critic_fwd_mma_kernel(
     float s = red[0][tid];
     for (int w = 1; w < NWARP; ++w) s = __fadd_rn(s, red[w][tid]);
     q[(size_t)z * B + r0 + tid] = __fadd_rn(s, params[z * P + oB3]);
+  }
+  __syncthreads();   // xs / h1s / red are rewritten by the next tile
   }
 }
 
@@ -707,7 +712,9 @@ int critic_mma_fwd_bwd(const CriticDims& c, int B, const float* params2, const _
   const long long oW3 = (long long)c.off[SPIKERL_CRITIC_W3];
   {
     ProfScope ps_("critic_fwd_mma", PB_TENSOR, 2.0 * B * nz * ((double)c.in * HW + (double)HW * HW + HW), 0.0, st);
-    dim3 grid(Bp / RB, nz);
+    // one CTA per SM fits (staged W2): at most num_sms / nz CTAs per critic, each looping over tiles
+    const int cap = num_sms() / nz > 0 ? num_sms() / nz : 1;
+    dim3 grid(Bp / RB < cap ? Bp / RB : cap, nz);
     static bool attr = false;
     if (!attr) {
       SPK_CHECK_CUDA(cudaFuncSetAttribute(critic_fwd_mma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,

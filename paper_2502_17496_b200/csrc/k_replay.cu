@@ -51,10 +51,12 @@ __global__ void replay_gather_kernel(int B, int S, int A, const float* __restric
                                      const unsigned long long* __restrict__ counter,
                                      float* __restrict__ s, float* __restrict__ a,
                                      float* __restrict__ r, float* __restrict__ s2,
-                                     float* __restrict__ d) {
+                                     float* __restrict__ d, unsigned long long* __restrict__ ctr_snap) {
   pdl_wait();
   pdl_trigger();
   const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
+  // the step's counter value for the later target-noise draws (which then advance the counter)
+  if (ctr_snap && blockIdx.x == 0 && threadIdx.x == 0) *ctr_snap = *counter;
   if (warp >= B) return;
   long long i = 0;
   if (lane == 0) {
@@ -83,26 +85,32 @@ __global__ void replay_gather_kernel(int B, int S, int A, const float* __restric
 int launch_replay_gather(int B, int S, int A, const float* rs, const float* ra, const float* rr,
                          const float* rs2, const float* rd, long long N, const long long* idx,
                          unsigned long long seed, int rank, const unsigned long long* counter,
-                         float* s, float* a, float* r, float* s2, float* d, cudaStream_t st) {
+                         float* s, float* a, float* r, float* s2, float* d, unsigned long long* ctr_snap,
+                         cudaStream_t st) {
   ProfScope ps_("replay_gather", PB_LATENCY, 0.0, 8.0 * B * (2.0 * S + A + 2), st);
   pdl(replay_gather_kernel, cdiv((long long)B * 32, 256), 256, 0, st)(B, S, A, rs, ra, rr, rs2, rd, N, idx,
-                                                                     seed, rank, counter, s, a, r, s2, d);
+                                                                     seed, rank, counter, s, a, r, s2, d,
+                                                                     ctr_snap);
   SPK_LAUNCHED();
   return SPIKERL_OK;
 }
 
-// a~ = clip(a2 + clip(eps, -c, c), -1, 1); single block; advances the Philox counter at the end.
-__global__ void __launch_bounds__(1024) target_action_kernel(int B, int A, const float* __restrict__ a2,
-                                                             const float* __restrict__ noise,
-                                                             float sigma, float clip,
-                                                             unsigned long long seed, int rank,
-                                                             unsigned long long* counter,
-                                                             float* __restrict__ at) {
+// a~ = clip(a2 + clip(eps, -c, c), -1, 1). The noise uses the step's counter value snapshotted by
+// the gather launch, so any number of blocks may run; block 0 advances the counter (a single
+// 1024-thread block took 60 us at configs[3] B = 4096, on the critic step's critical path).
+__global__ void __launch_bounds__(256) target_action_kernel(int B, int A, const float* __restrict__ a2,
+                                                            const float* __restrict__ noise,
+                                                            float sigma, float clip,
+                                                            unsigned long long seed, int rank,
+                                                            unsigned long long* counter,
+                                                            const unsigned long long* __restrict__ ctr_snap,
+                                                            float* __restrict__ at) {
   pdl_wait();
   pdl_trigger();
-  const unsigned long long ctr = *counter;
+  const unsigned long long ctr = *ctr_snap;
   const int n = B * A;
-  for (int i = threadIdx.x; i < n; i += blockDim.x) {
+  if (blockIdx.x == 0 && threadIdx.x == 0) *counter = ctr + 1;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
     float eps;
     if (noise) {
       eps = noise[i];
@@ -115,15 +123,15 @@ __global__ void __launch_bounds__(1024) target_action_kernel(int B, int A, const
     eps = fminf(fmaxf(eps, -clip), clip);
     at[i] = fminf(fmaxf(__fadd_rn(a2[i], eps), -1.0f), 1.0f);
   }
-  __syncthreads();
-  if (threadIdx.x == 0) *counter = ctr + 1;
 }
 
 int launch_target_action(int B, int A, const float* a2, const float* noise, float sigma, float clip,
-                         unsigned long long seed, int rank, unsigned long long* counter, float* at,
-                         cudaStream_t st) {
+                         unsigned long long seed, int rank, unsigned long long* counter,
+                         const unsigned long long* ctr_snap, float* at, cudaStream_t st) {
   ProfScope ps_("target_action", PB_LATENCY, 0.0, 12.0 * B * A, st);
-  pdl(target_action_kernel, 1, 1024, 0, st)(B, A, a2, noise, sigma, clip, seed, rank, counter, at);
+  const int blocks = cdiv((long long)B * A, 512);   // two elements (one Box-Muller pair) per thread
+  pdl(target_action_kernel, blocks < 148 ? (blocks > 0 ? blocks : 1) : 148, 256, 0, st)(
+      B, A, a2, noise, sigma, clip, seed, rank, counter, ctr_snap, at);
   SPK_LAUNCHED();
   return SPIKERL_OK;
 }

@@ -286,7 +286,7 @@ static int actor_backward_impl(const ActorDims& d, int B, const float* params,
 
 // ------------------------------------------------------------------ TD3 workspace layout
 struct Td3Ws {
-  size_t s, a, r, s2, d, a2, at, api, qt, q, y, ga, lossa, tape, actor_ws, critic_ws, critic_ws_t, total;
+  size_t s, a, r, s2, d, a2, at, api, qt, q, y, ga, lossa, ctr, tape, actor_ws, critic_ws, critic_ws_t, total;
 };
 
 static Td3Ws td3_ws_layout(const ActorDims& ad, const CriticDims& cd, int B) {
@@ -298,6 +298,7 @@ static Td3Ws td3_ws_layout(const ActorDims& ad, const CriticDims& cd, int B) {
   w.d = take(f * B); w.a2 = take(f * B * ad.A); w.at = take(f * B * ad.A); w.api = take(f * B * ad.A);
   w.qt = take(f * 2 * B); w.q = take(f * 2 * B); w.y = take(f * B); w.ga = take(f * B * ad.A);
   w.lossa = take(f * 4);
+  w.ctr = take(sizeof(unsigned long long));
   w.tape = take(tape_layout(ad, B).total);
   w.actor_ws = take(actor_ws_layout(ad, B).total);
   w.critic_ws = take(critic_ws_bytes(cd, B));
@@ -579,13 +580,14 @@ int spikerl_td3_update(const spikerl_actor_cfg* acfg, const spikerl_critic_cfg* 
   void* cws_t = ws + W.critic_ws_t;
 
   // K9: sample (s, a, r, s', d)
+  unsigned long long* ctr_snap = (unsigned long long*)(ws + W.ctr);
   SPK_TRY(launch_replay_gather(B, ad.S, ad.A, b->rs, b->ra, b->rr, b->rs2, b->rd, b->replay_size, indices, seed,
-                               rank, b->rng_counter, s, a, r, s2, dn, st));
+                               rank, b->rng_counter, s, a, r, s2, dn, ctr_snap, st));
   // branch A: target path. 1. a~ = clip(pi'(s') + clip(eps), -1, 1); 2. y = r + gamma (1 - d) min(Q1', Q2')(s', a~)
   SPK_TRY(stream_after(sA, st, aux->ev[0]));
   SPK_TRY(actor_forward_impl(ad, B, b->actor_t, atbf, s2, a2, aws + actor_ws_layout(ad, B).tape, sA));
-  SPK_TRY(launch_target_action(B, ad.A, a2, noise, hp->policy_noise, hp->noise_clip, seed, rank, b->rng_counter, at,
-                               sA));
+  SPK_TRY(launch_target_action(B, ad.A, a2, noise, hp->policy_noise, hp->noise_clip, seed, rank, b->rng_counter,
+                               ctr_snap, at, sA));
   SPK_TRY(critic_fwd_bwd(cd, B, b->critic_t, ctbf, s2, ad.S, at, ad.A, nullptr, qt, nullptr, nullptr, nullptr, 0.f,
                          2, cws_t, sA));
   SPK_TRY(launch_td_target(B, r, dn, qt, hp->gamma, y, sA));
