@@ -60,6 +60,10 @@ int launch_lif_dw_tc(const ActorDims& d, int l, int B, const void* Gl, const uin
                      float* dW, float* part, int accumulate, cudaStream_t st);
 size_t tc_enc_partial_bytes(const ActorDims& d, int B);
 size_t tc_dw_partial_bytes(const ActorDims& d, int B, int l);
+// critic weight gradients on the tcgen05 engine (stacked K-major operands; see k_tc_gemm.cu)
+int tc_wgrad_splits(int Bp, int inq);
+int launch_critic_wgrad_tc(int Bp, int inq, int xtr, const __nv_bfloat16* dZT, const __nv_bfloat16* XTH,
+                           float* part, long long msz, cudaStream_t st);
 // 3-D u32 tensor map (dims / box innermost first, strides in bytes), no swizzle, OOB zero fill
 int make_u32_map3(CUtensorMap* m, const void* base, const uint64_t* dims, const uint64_t* strides,
                   const uint32_t* box);   // split-K partials of dW_l

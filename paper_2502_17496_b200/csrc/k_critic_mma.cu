@@ -164,7 +164,9 @@ MmaWs mma_carve(const CriticDims& c, int B, void* base, size_t* total) {
   w.part = (float*)take(4 * 2 * (Bp / RB));
   w.ticket = (unsigned int*)take(4);
   const int ws = wgrad_splits(B);
-  w.wpart = (float*)take(ws > 1 ? sizeof(float) * ws * 2 * ((size_t)HW * HW + (size_t)HW * L.inq) : 0);
+  const int wt = ws > 0 ? tc_wgrad_splits((int)Bp, L.inq) : 0;   // tcgen05 weight-gradient partials
+  const int wmax = ws > wt ? ws : wt;
+  w.wpart = (float*)take(wmax > 1 ? sizeof(float) * wmax * 2 * ((size_t)HW * HW + (size_t)HW * L.inq) : 0);
   if (total) *total = off;
   return w;
 }
@@ -700,6 +702,17 @@ int launch_critic_refresh(const CriticDims& c, const float* params2, __nv_bfloat
   return SPIKERL_OK;
 }
 
+// the tcgen05 weight-gradient launch reads the transposed operands as two stacked maps: dZ1T right
+// after dZ2T, H1T right after XT's 64-rounded rows (mma_carve's order); SPIKERL_CRITIC_WG_TC=0 forces
+// the mma.sync split kernel
+static bool tc_wgrad_ok(const CriticDims& c, const MmaWs& w, int Bp) {
+  static const int env = [] { const char* e = getenv("SPIKERL_CRITIC_WG_TC"); return e ? atoi(e) : 1; }();
+  const MmaLayout L = mma_layout(c);
+  return env != 0 && c.H1 == HW && c.H2 == HW && L.inq <= 3 * 256 &&
+         (const char*)w.dZ1T == (const char*)w.dZ2T + (size_t)2 * 2 * HW * Bp &&
+         (const char*)w.H1T == (const char*)w.XT + (size_t)2 * round_up(L.inq, 64) * Bp;
+}
+
 int critic_mma_fwd_bwd(const CriticDims& c, int B, const float* params2, const __nv_bfloat16* pb, const float* obs,
                        int S, const float* act, int A, const float* y, float* q, float* loss, float* grad2,
                        float* grad_act, float act_scale, int nz, void* ws, cudaStream_t st,
@@ -770,6 +783,15 @@ int critic_mma_fwd_bwd(const CriticDims& c, int B, const float* params2, const _
         pdl(critic_wgrad_mma_kernel, grid, 256, 0, st)(Bp, c.in, L.inq, L.P, (long long)c.off[SPIKERL_CRITIC_W1],
                                                       (long long)c.off[SPIKERL_CRITIC_W2], w.XT, w.H1T, w.dZ2T, w.dZ1T,
                                                       grad2);
+        SPK_LAUNCHED();
+      } else if (tc_wgrad_ok(c, w, Bp)) {
+        // tcgen05: both weight gradients of both critics as one split-K launch of K-major operand
+        // tiles (the mma.sync split kernel below took 104 us at configs[3] B = 4096)
+        const long long msz = (long long)HW * HW + (long long)HW * L.inq;
+        SPK_TRY(launch_critic_wgrad_tc(Bp, L.inq, round_up(L.inq, 64), w.dZ2T, w.XT, w.wpart, msz, st));
+        const int splits = tc_wgrad_splits(Bp, L.inq);
+        pdl(critic_wgrad_reduce_kernel, 148 * 4, 256, 0, st)(splits, c.in, L.inq, L.P, (long long)c.off[SPIKERL_CRITIC_W1],
+                                                           (long long)c.off[SPIKERL_CRITIC_W2], w.wpart, grad2);
         SPK_LAUNCHED();
       } else {
         // K split in multiples of 16 batch rows (Bp is a multiple of RB = 16)

@@ -29,7 +29,9 @@ namespace tc {
 
 // FWD: hidden layers (batch-major spike plane + quad-major spike / mask planes for the DX epilogue);
 // FWDO: output layer (batch-major spike and mask planes + spike counts)
-enum Mode { FWD = 0, DX = 1, ENC = 2, DW = 3, FWDO = 4 };
+// WG: the critic's weight-gradient GEMMs dW = dZ^T X (both operands K-major bf16 by TMA, K = batch),
+// split over K, fp32 partial tiles per (job, split)
+enum Mode { FWD = 0, DX = 1, ENC = 2, DW = 3, FWDO = 4, WG = 5 };
 __host__ __device__ constexpr bool is_fwd(int m) { return m == FWD || m == FWDO; }
 
 constexpr int BM = 128, BK = 64, STAGES = 4;
@@ -75,6 +77,9 @@ struct Params {
   const float* A; const float* obs; const float* mu; const float* sigma; float* partial; int K0, S, E;
   // DW
   const uint32_t* bits_dw; int w_dw; float* dw_part; long long split_stride; int ldp; int R;
+  // WG jobs (critic weight gradients): A / B row bases in the stacked operand maps, partial offset
+  // (elements, within one split), row stride and valid columns of the output tile
+  int wg_njobs; int wg_arow[8], wg_brow[8], wg_ld[8], wg_ncol[8]; long long wg_off[8];
   int trace;   // diagnostics: CTA 0 stamps %globaltimer at phase boundaries into g_trace
   int dbg;     // diagnostics only (SPIKERL_TC_DBG, wrong results): 1 = expanders skip their smem
                // stores, 2 = epilogue skips its work, 4 = MMA issuer skips the MMAs, 8 = DW
@@ -297,7 +302,7 @@ __device__ __forceinline__ Tile decode(const Params& p, int u, int rank, int CG)
   Tile t;
   t.m = (u % p.m_tiles) * CG + rank;
   int rest = u / p.m_tiles;
-  if (MODE == DW) {
+  if (MODE == DW || MODE == WG) {
     t.n = rest % p.n_tiles;
     t.split = rest / p.n_tiles;
     t.kb0 = t.split * p.kps;
@@ -341,7 +346,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
   uint64_t* tempty = tfull + 2;
   uint32_t* tmem_slot = (uint32_t*)(tempty + 2);
   constexpr bool B_EXPAND = (is_fwd(MODE) || MODE == DW);
-  constexpr bool A_MN = !is_fwd(MODE);
+  constexpr bool A_MN = !is_fwd(MODE) && MODE != WG;
   constexpr bool B_MN = (MODE == DW);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int rank = CG == 2 ? (int)cluster_ctarank() : 0;
@@ -377,7 +382,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     // ===================== TMA producer (both CTAs load their own halves) =====================
     if (lane == 0) {
       uint32_t it = 0;
-      const uint32_t bytes_b = (MODE == DX) ? 128u * p.T * p.Bt / CG : (MODE == ENC ? 128u * p.BN / CG : 0u);
+      const uint32_t bytes_b = (MODE == DX) ? 128u * p.T * p.Bt / CG : ((MODE == ENC || MODE == WG) ? 128u * p.BN / CG : 0u);
       for (int u = cid; u < p.n_units; u += ncl) {
         const Tile t = decode<MODE>(p, u, rank, CG);
         for (int kb = t.kb0; kb < t.kb1; ++kb, ++it) {
@@ -399,6 +404,10 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
             if (MODE == DX) tma_3d(&tmB, sB, &full[stage], kb * BK, t.n * p.Bt, 0);
             if (MODE == ENC) tma_2d(&tmB, sB, &full[stage], kb * BK, t.n * p.BN);
             if (it == 0) trace_stamp(p, 2);
+          } else if (MODE == WG) {
+            if (rank == 0) mbar_expect_tx(&full[stage], 2u * ((uint32_t)A_STAGE + bytes_b));
+            tma_2d_cg2(&tmA, sA, &full[stage], kb * BK, p.wg_arow[t.n] + rank * BM);
+            tma_2d_cg2(&tmB, sB, &full[stage], kb * BK, p.wg_brow[t.n] + rank * (p.BN / 2));
           } else {
             if (rank == 0) mbar_expect_tx(&full[stage], 2u * ((uint32_t)A_STAGE + bytes_b));
             if (!A_MN) {
@@ -854,6 +863,28 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
           p.partial[(((size_t)t.n * NUM_EPI_GROUPS + g) * p.K0 + row) * 2 + 0] = __fdiv_rn(pm, sg2);
           p.partial[(((size_t)t.n * NUM_EPI_GROUPS + g) * p.K0 + row) * 2 + 1] = __fdiv_rn(ps, sg3);
         }
+      } else if constexpr (MODE == WG) {
+        // dump the fp32 tile of this (job, split): row = output row within the job's 256, group g
+        // covers columns [128 g, 128 g + 128); columns past the job's width are not stored
+        constexpr int GC = DW_BN / NUM_EPI_GROUPS;
+        const int c0 = g * GC, ld = p.wg_ld[t.n], nc = p.wg_ncol[t.n];
+        float* dst = p.dw_part + (size_t)t.split * p.split_stride + p.wg_off[t.n] +
+                     (size_t)(rank * BM + 32 * q + lane) * ld + c0;
+        for (int j1 = 0; j1 < GC; j1 += 32) {
+          if (c0 + j1 < nc) {   // nc is a multiple of 32
+            uint32_t rr[4][8];
+#pragma unroll
+            for (int ci = 0; ci < 4; ++ci) tmem_ld8(taddr + c0 + j1 + 8 * ci, rr[ci]);
+            tmem_ld_wait();
+#pragma unroll
+            for (int ci = 0; ci < 4; ++ci) {
+              const uint32_t (&r)[8] = rr[ci];
+              float4* d4 = reinterpret_cast<float4*>(dst + j1 + 8 * ci);
+              d4[0] = make_float4(__uint_as_float(r[0]), __uint_as_float(r[1]), __uint_as_float(r[2]), __uint_as_float(r[3]));
+              d4[1] = make_float4(__uint_as_float(r[4]), __uint_as_float(r[5]), __uint_as_float(r[6]), __uint_as_float(r[7]));
+            }
+          }
+        }
       } else {  // DW: group g writes columns [GC g, GC g + GC) of the unit (GC = 64, or 128 for DW2)
         constexpr int GC = (DW2 ? 2 * DW_BN : DW_BN) / NUM_EPI_GROUPS;
         const int c0 = g * GC;
@@ -1059,7 +1090,7 @@ template <int MODE>
 static int launch_bt(int bt, const CUtensorMap& ma, const CUtensorMap& mb, const Params& p, cudaStream_t st,
                      const CUtensorMap* mc = nullptr) {
   const CUtensorMap& c = mc ? *mc : ma;   // store map (DX only)
-  if (MODE == ENC || MODE == DW) return launch<MODE, 8>(ma, mb, c, p, st);
+  if (MODE == ENC || MODE == DW || MODE == WG) return launch<MODE, 8>(ma, mb, c, p, st);
   switch (bt) {
     case 8: return launch<MODE, 8>(ma, mb, c, p, st);
     case 16: return launch<MODE, 16>(ma, mb, c, p, st);
@@ -1286,6 +1317,65 @@ int launch_lif_dw_tc(const ActorDims& d, int l, int B, const void* Gl, const uin
   pdl(dw_reduce_kernel, grid, 256, 0, st)(part, splits, p.split_stride, p.ldp, d.N[l], d.N[l - 1], dW, accumulate);
   SPK_LAUNCHED();
   return SPIKERL_OK;
+}
+
+// ---- critic weight gradients on the tcgen05 engine (large batches)
+// Operands (mma critic workspace): A = [dZ2T z0 | dZ2T z1 | dZ1T z0 | dZ1T z1] rows of Bp bf16 (one
+// stacked 2-D map), B = [XT (xtr rows) | H1T z0 | H1T z1]. Jobs: per critic z, dW2 (A rows z 256,
+// B = H1T z) and dW1 in 256-column tiles (A rows 512 + z 256, B = XT rows n 256). Output: fp32
+// partials in the layout critic_wgrad_reduce_kernel adds up: part[(s 2 + z) msz + ...].
+int tc_wgrad_splits(int Bp, int inq) {
+  const int jobs = 2 * (1 + cdiv(inq, 256));
+  const int kblocks = cdiv(Bp, BK);
+  int s = pairs_enabled() ? pair_slots() / jobs : 1;
+  if (s < 1) s = 1;
+  if (s > kblocks) s = kblocks;
+  const int kps = cdiv(kblocks, s);
+  return cdiv(kblocks, kps);
+}
+
+int launch_critic_wgrad_tc(int Bp, int inq, int xtr, const __nv_bfloat16* dZT, const __nv_bfloat16* XTH,
+                           float* part, long long msz, cudaStream_t st) {
+  if (!pairs_enabled()) { set_error("critic wgrad tc: needs CTA pairs"); return SPIKERL_E_UNSUPPORTED; }
+  constexpr int HWc = 256;
+  Params p{};
+  p.BN = 256;
+  p.cg = 2;
+  p.m_tiles = 1;
+  p.k_blocks = cdiv(Bp, BK);
+  const int splits = tc_wgrad_splits(Bp, inq);
+  p.kps = cdiv(p.k_blocks, splits);
+  int nj = 0;
+  for (int z = 0; z < 2; ++z) {
+    p.wg_arow[nj] = z * HWc; p.wg_brow[nj] = xtr + z * HWc; p.wg_ld[nj] = HWc; p.wg_ncol[nj] = HWc;
+    p.wg_off[nj] = (long long)z * msz; ++nj;
+    for (int n = 0; n * 256 < inq; ++n) {
+      p.wg_arow[nj] = 2 * HWc + z * HWc; p.wg_brow[nj] = n * 256; p.wg_ld[nj] = inq;
+      p.wg_ncol[nj] = inq - n * 256 < 256 ? inq - n * 256 : 256;
+      p.wg_off[nj] = (long long)z * msz + (long long)HWc * HWc + n * 256; ++nj;
+    }
+  }
+  if (nj > 8) { set_error("critic wgrad tc: input width too large"); return SPIKERL_E_UNSUPPORTED; }
+  p.wg_njobs = nj;
+  p.n_tiles = nj;
+  p.n_units = nj * cdiv(p.k_blocks, p.kps);
+  p.dw_part = part;
+  p.split_stride = 2 * msz;
+  CUtensorMap ma, mb;
+  {
+    const uint64_t dims[2] = {(uint64_t)Bp, (uint64_t)(4 * HWc)};
+    const uint64_t strides[1] = {(uint64_t)Bp * 2};
+    const uint32_t box[2] = {64, 128};
+    SPK_TRY(make_map(&ma, dZT, 2, dims, strides, box));
+  }
+  {
+    const uint64_t dims[2] = {(uint64_t)Bp, (uint64_t)(xtr + 2 * HWc)};
+    const uint64_t strides[1] = {(uint64_t)Bp * 2};
+    const uint32_t box[2] = {64, 128};
+    SPK_TRY(make_map(&mb, XTH, 2, dims, strides, box));
+  }
+  ProfScope ps_("critic_wgrad_tc", PB_TENSOR, 2.0 * 2 * Bp * ((double)HWc * HWc + (double)HWc * inq), 0.0, st);
+  return launch_bt<WG>(8, ma, mb, p, st);
 }
 
 }  // namespace spk
