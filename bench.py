@@ -25,6 +25,9 @@ import time
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
+# diagnostics: SPIKERL_BENCH_COMM=1 runs the N > 1 code path (NCCL communicator, allreduce inside the
+# captured graph) on a single GPU with a world-size-1 communicator
+FORCE_COMM = os.environ.get("SPIKERL_BENCH_COMM", "0") == "1"
 METRIC = "TD3 spiking-actor updates/sec at 1/2/4/8 B200; actor fwd+bwd samples/sec"
 SIMT_FP32_PEAK_TFLOPS = 148 * 128 * 2 * 1.965e9 / 1e12  # guide: 148 SMs x 128 FP32 lanes x FMA x max clock
 
@@ -198,7 +201,7 @@ def build_td3(name, world, rank, engine, replay_size, seed=0):
     acfg = pk.actor_cfg_from(shape, engine=engine)
     ccfg = pk.critic_cfg(cshape.in_dim, precision=shape.precision)
     replay = pk.replay_fill(replay_size, shape.obs_dim, shape.act_dim, seed=seed, rank=rank)
-    comm = pk.Comm(rank, world) if world > 1 else None
+    comm = pk.Comm(rank, world) if (world > 1 or FORCE_COMM) else None
     td3 = pk.TD3(acfg, ccfg, pk.td3_cfg(B), replay, seed=seed, comm=comm)
     rng = np.random.default_rng(seed)
     td3.load(sg.actor_params(shape, rng), sg.critic_params(cshape, rng), sg.critic_params(cshape, rng))
@@ -446,7 +449,7 @@ def run_actor(args, rank, world):
     actor = pk.SpikingActor(pk.actor_cfg_from(shape, engine=args.engine), B)
     rng = np.random.default_rng(0)
     actor.load(sg.actor_params(shape, rng))
-    comm = pk.Comm(rank, world) if world > 1 else None
+    comm = pk.Comm(rank, world) if (world > 1 or FORCE_COMM) else None
     if comm:
         comm.broadcast(actor.params)
         actor.refresh()

@@ -515,3 +515,48 @@ def test_staged_output_scan_matches_direct_subprocess(preset, B, T, tmp_path):
     other = pickle.load(open(tmp_path / "out.pkl", "rb"))
     for k in here["grads"]:
         assert np.array_equal(here["grads"][k], other[k]), k
+
+
+def test_nccl_single_rank_comm():
+    """The NCCL path on one GPU (a world-size-1 communicator): the mean allreduce and the broadcast
+    leave their buffers bit-identical, and TD3 updates with the communicator (eager and replayed
+    from a captured graph, NCCL calls inside the capture) equal the updates without it bitwise."""
+    import torch
+    import paper_2502_17496_b200 as pk
+    comm = pk.Comm(0, 1)
+    x = torch.randn(1 << 20, device="cuda")
+    y = x.clone()
+    comm.allreduce_mean(y)
+    comm.broadcast(y, 0)
+    torch.cuda.synchronize()
+    assert torch.equal(x, y)
+    shape, _, B = sg.preset("cfg1")
+    replay = pk.replay_fill(20000, 17, 6, seed=3)
+    outs = []
+    for use_comm, mode in ((False, "eager"), (True, "eager"), (True, "graph")):
+        rng = np.random.default_rng(8)
+        actor = sg.actor_params(shape, rng)
+        cs = sg.CriticShape(23, precision="bf16")
+        c1, c2 = sg.critic_params(cs, rng), sg.critic_params(cs, rng)
+        td3 = pk.TD3(pk.actor_cfg_from(shape), pk.critic_cfg(23), pk.td3_cfg(B), replay, seed=11,
+                     comm=comm if use_comm else None)
+        td3.load(actor, c1, c2)
+        if mode == "graph":
+            snap = [t.clone() for t in (td3.actor, td3.critic, td3.actor_t, td3.critic_t)]
+            td3.capture()
+            for t, sn in zip((td3.actor, td3.critic, td3.actor_t, td3.critic_t), snap):
+                t.copy_(sn)
+            td3.refresh()
+            for t in (td3.m_actor, td3.v_actor, td3.m_critic, td3.v_critic, td3.adam_steps, td3.rng_counter):
+                t.zero_()
+            for k in range(1, 5):
+                td3.replay_graph(k)
+        else:
+            for k in range(1, 5):
+                td3.update(k)
+        torch.cuda.synchronize()
+        outs.append([t.cpu().clone() for t in (td3.actor, td3.critic, td3.actor_t, td3.losses)])
+    for other in outs[1:]:
+        for a, b in zip(outs[0], other):
+            assert torch.equal(a, b)
+    comm.close()
