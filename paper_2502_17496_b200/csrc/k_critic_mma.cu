@@ -201,17 +201,37 @@ __global__ void __launch_bounds__(256) critic_fwd_mma_kernel(
   const int in = S + A, ldx = inp + SPAD, ldh = HW + SPAD;
   if (ticket && blockIdx.x == 0 && z == 0 && tid == 0) *ticket = 0u;   // for the backward launch
   // persistent over 16-row tiles: the staged W2 (135 KB, one CTA per SM) serves every tile of this
-  // CTA (large batches: one CTA per 16 rows re-staged W2 512 times per launch at configs[3] B = 4096)
+  // CTA (large batches: one CTA per 16 rows re-staged W2 512 times per launch at configs[3] B = 4096).
+  // The next tile's [s; a] values are requested while the current tile runs (warp = rows warp and
+  // warp + 8, lane = every 32nd input column: no index division; ncu r01: the X-tile build waited on
+  // its loads for ~54% of the launch's stall samples at B = 4096)
+  static_assert(RB == 16 && NWARP == 8, "X tile: two rows per warp");
+  float xv[2][16];
+  auto load_x = [&](int rt) {
+#pragma unroll
+    for (int rr = 0; rr < 2; ++rr) {
+      const int b = rt + warp + 8 * rr;
+#pragma unroll
+      for (int cc = 0; cc < 16; ++cc) {
+        const int i = lane + 32 * cc;
+        float v = 0.f;
+        if (b < B && i < in) v = i < S ? obs[(size_t)b * S + i] : act[(size_t)b * A + (i - S)];
+        xv[rr][cc] = v;
+      }
+    }
+  };
+  if (blockIdx.x * RB < Bp) load_x(blockIdx.x * RB);
   for (int r0 = blockIdx.x * RB; r0 < Bp; r0 += gridDim.x * RB) {
   // X tile (bf16-rounded [s; a]); the z == 0 CTAs also write X^T (zeros beyond in / B) for dW1
-#pragma unroll 4
-  for (int idx = tid; idx < RB * inp; idx += 256) {
-    const int r = idx / inp, i = idx - r * inp, b = r0 + r;
-    float v = 0.f;
-    if (b < B && i < in) v = i < S ? obs[(size_t)b * S + i] : act[(size_t)b * A + (i - S)];
-    xs[r * ldx + i] = __float2bfloat16_rn(v);
-  }
+#pragma unroll
+  for (int rr = 0; rr < 2; ++rr)
+#pragma unroll
+    for (int cc = 0; cc < 16; ++cc) {
+      const int i = lane + 32 * cc;
+      if (i < inp) xs[(warp + 8 * rr) * ldx + i] = __float2bfloat16_rn(xv[rr][cc]);
+    }
   __syncthreads();
+  if (r0 + (int)gridDim.x * RB < Bp) load_x(r0 + gridDim.x * RB);
   if (store && z == 0) {
     for (int idx = tid; idx < RB * inq; idx += 256) {
       const int i = idx / RB, r = idx - i * RB;
