@@ -39,6 +39,8 @@ def parse():
     ap.add_argument("--warmup", type=int, default=20)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--workload", default="cfg1", choices=["cfg1", "cfg2", "cfg3s", "cfg3L", "cfg4"])
+    ap.add_argument("--single-graphs", action="store_true",
+                    help="TD3: replay one graph per update instead of overlapped update pairs")
     ap.add_argument("--engine", default="auto", choices=["auto", "simt", "tcgen05"])
     ap.add_argument("--no-flush", action="store_true", help="do not flush L2 between timed steps")
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -340,15 +342,24 @@ def run_td3(args, rank, world):
     from paper_2502_17496_b200 import _lib
     td3, shape, B = build_td3(args.workload, world, rank, args.engine, args.replay_size)
     td3.capture()
+    # updates 2j+1, 2j+2 as one overlapped graph (spikerl_td3_update_pair: bitwise the same state as
+    # the two single-update graphs, tested) unless --single-graphs
+    pair = td3.hp.policy_delay == 2 and not args.single_graphs
+    if pair:
+        td3.capture_pair()
     launches = {}
     lib = pk.lib()
     for k in (1, 2):            # launches per phase, counted from an eager enqueue
         lib.spikerl_launch_count(1)
         td3.update(k)
         launches[k % 2] = lib.spikerl_launch_count(1)
+    if pair:
+        lib.spikerl_launch_count(1)
+        td3.update_pair(3)
+        launches["pair"] = lib.spikerl_launch_count(1)
     torch.cuda.synchronize()
     flush = None if args.no_flush else torch.empty(64 * 1024 * 1024, dtype=torch.float32, device="cuda")  # 256 MB > L2
-    step0 = [2]
+    step0 = [4 if pair else 2]
 
     def graph_step(k):
         td3.replay_graph(step0[0] + k)
@@ -356,12 +367,24 @@ def run_td3(args, rank, world):
     for k in range(args.warmup):
         graph_step(k)
     step0[0] += args.warmup
+    if pair and step0[0] % 2 == 1:   # pairs start at an odd update
+        graph_step(0)
+        step0[0] += 1
     torch.cuda.synchronize()
     clk = ClockSampler(int(os.environ.get("LOCAL_RANK", "0")))
     clk.start()
-    total_ms = time_steps(graph_step, args.steps, flush, world)
+    if pair:
+        npair = args.steps // 2
+        total_ms = time_steps(lambda k: td3.replay_pair(), npair, flush, world) if npair else 0.0
+        if args.steps % 2:
+            step0[0] += 2 * npair
+            total_ms += time_steps(graph_step, 1, flush, world)
+            step0[0] -= 2 * npair
+        gpu_launches = npair * launches["pair"] + (launches[1] if args.steps % 2 else 0)
+    else:
+        total_ms = time_steps(graph_step, args.steps, flush, world)
+        gpu_launches = sum(launches[(step0[0] + k) % 2] for k in range(args.steps))
     clocks = clk.stop()
-    gpu_launches = sum(launches[(step0[0] + k) % 2] for k in range(args.steps))
     secs = total_ms / 1e3
     value = args.steps * B * world / secs
     out = {"metric": METRIC, "value": round(value, 2), "unit": "samples/s", "n_gpus": world, "steps": args.steps,
@@ -374,11 +397,18 @@ def run_td3(args, rank, world):
                                   f"{shape.obs_dim + shape.act_dim}->256->256->1",
                       "global_batch": B * world, "per_rank_batch": B, "replay_per_rank": args.replay_size,
                       "parallelism": f"dp{world}", "engine": args.engine,
-                      "l2": "flushed between timed steps (256 MB read, outside the events)" if flush is not None
-                      else "not flushed", "cuda_graph": True},
+                      "l2": ("flushed between timed pairs of updates (256 MB read, outside the events)" if pair
+                             else "flushed between timed steps (256 MB read, outside the events)")
+                      if flush is not None else "not flushed", "cuda_graph": True,
+                      "graph": "update pairs (k odd, k + 1 overlapped)" if pair else "one graph per update"},
            "clocks": clocks, "gpu_launches": int(gpu_launches)}
     step0[0] += args.steps
-    en = energy_window(lambda k: td3.replay_graph(step0[0] + k), clk)
+    if pair and step0[0] % 2 == 0:
+        en = energy_window(lambda k: td3.replay_pair(), clk)   # each call = two updates
+        if en:
+            en["steps"] *= 2
+    else:
+        en = energy_window(lambda k: td3.replay_graph(step0[0] + k), clk)
     if en:
         step0[0] += en["steps"]
         en["joules_per_update"] = round(en["joules"] / en["steps"], 6)

@@ -236,6 +236,20 @@ int spikerl_td3_update(const spikerl_actor_cfg* acfg, const spikerl_critic_cfg* 
                        spikerl_comm* comm, float* losses, void* workspace,
                        spikerl_stream_t stream);
 
+/* Two consecutive updates k, k + 1 (k odd, policy_delay 2: a critic-only update then a critic +
+ * actor + targets update) as one fork/join DAG: update k + 1's target path and its pi(s) forward
+ * read only parameters update k leaves unchanged (the actor and the targets), so they overlap
+ * update k. Bitwise the same result as spikerl_td3_update(k) followed by spikerl_td3_update(k + 1)
+ * (SPEC.md:235-259 order; R15). indices [2][B] / noise [2][B][A] (device) or NULL;
+ * workspace: spikerl_td3_pair_workspace_bytes. E_ARG unless policy_delay == 2 and k is odd. */
+int spikerl_td3_update_pair(const spikerl_actor_cfg* acfg, const spikerl_critic_cfg* ccfg,
+                            const spikerl_td3_cfg* hp, const spikerl_td3_bufs* bufs, long long step,
+                            unsigned long long seed, const long long* indices, const float* noise,
+                            spikerl_comm* comm, float* losses, void* workspace,
+                            spikerl_stream_t stream);
+size_t spikerl_td3_pair_workspace_bytes(const spikerl_actor_cfg* acfg, const spikerl_critic_cfg* ccfg,
+                                        int batch);
+
 /* Fill a replay shard on the device: s,s2 ~ N(0,1) clip +-5, a ~ U[-1,1], r ~ N(0,1),
  * done ~ Bernoulli(p_done) (configs[1]); Philox keyed by (seed, rank). */
 int spikerl_replay_fill(float* s, float* a, float* r, float* s2, float* d, long long n, int obs_dim,

@@ -106,6 +106,7 @@ _SIGS = {
     "spikerl_actor_workspace_bytes": (SZ, [C.POINTER(ActorCfg), I]),
     "spikerl_critic_workspace_bytes": (SZ, [C.POINTER(CriticCfg), I]),
     "spikerl_td3_workspace_bytes": (SZ, [C.POINTER(ActorCfg), C.POINTER(CriticCfg), I]),
+    "spikerl_td3_pair_workspace_bytes": (SZ, [C.POINTER(ActorCfg), C.POINTER(CriticCfg), I]),
     "spikerl_actor_tape_layout": (I, [C.POINTER(ActorCfg), I, C.POINTER(TapeLayout)]),
     "spikerl_actor_refresh_bf16": (I, [C.POINTER(ActorCfg), P, P, P]),
     "spikerl_critic_refresh_bf16": (I, [C.POINTER(CriticCfg), I, P, P, P]),
@@ -116,6 +117,8 @@ _SIGS = {
     "spikerl_polyak": (I, [P, P, SZ, F, P]),
     "spikerl_td3_update": (I, [C.POINTER(ActorCfg), C.POINTER(CriticCfg), C.POINTER(TD3Cfg),
                                C.POINTER(TD3Bufs), LL, ULL, P, P, P, P, P, P]),
+    "spikerl_td3_update_pair": (I, [C.POINTER(ActorCfg), C.POINTER(CriticCfg), C.POINTER(TD3Cfg),
+                                    C.POINTER(TD3Bufs), LL, ULL, P, P, P, P, P, P]),
     "spikerl_replay_fill": (I, [P, P, P, P, P, LL, I, I, F, ULL, I, P]),
     "spikerl_comm_get_unique_id": (I, [P]),
     "spikerl_comm_init": (I, [I, I, P, C.POINTER(P)]),

@@ -329,6 +329,8 @@ class TD3:
             self.grad_actor, self.grad_critic, self.adam_steps, self.rng_counter, replay.s, replay.a, replay.r,
             replay.s2, replay.d)], replay.size)
         self.graphs = {}
+        self.ws_pair = None
+        self.pair_graph = None
 
     def load(self, actor: dict, critic1: dict, critic2: dict):
         a = pack_actor(self.acfg, actor, self.device)
@@ -354,6 +356,34 @@ class TD3:
                                        step, self.seed, _p(indices), _p(noise),
                                        self.comm.handle if self.comm is not None else None, _p(self.losses),
                                        _p(self.ws), _stream()), "td3_update")
+
+    def update_pair(self, step: int, indices: torch.Tensor | None = None, noise: torch.Tensor | None = None):
+        """Updates step (odd) and step + 1 as one overlapped DAG (policy_delay 2); bitwise the same
+        as update(step); update(step + 1). indices [2][B], noise [2][B][A] or None."""
+        if self.ws_pair is None:
+            self.ws_pair = _alloc(lib().spikerl_td3_pair_workspace_bytes(C.byref(self.acfg), C.byref(self.ccfg),
+                                                                          self.hp.batch), self.device)
+        check(lib().spikerl_td3_update_pair(C.byref(self.acfg), C.byref(self.ccfg), C.byref(self.hp),
+                                            C.byref(self._bufs), step, self.seed, _p(indices), _p(noise),
+                                            self.comm.handle if self.comm is not None else None, _p(self.losses),
+                                            _p(self.ws_pair), _stream()), "td3_update_pair")
+
+    def capture_pair(self):
+        """Capture the overlapped two-update DAG (steps 2j + 1, 2j + 2) as one CUDA graph."""
+        if self.ws_pair is None:
+            self.ws_pair = _alloc(lib().spikerl_td3_pair_workspace_bytes(C.byref(self.acfg), C.byref(self.ccfg),
+                                                                          self.hp.batch), self.device)
+        s = torch.cuda.Stream()
+        s.wait_stream(torch.cuda.current_stream())
+        with torch.cuda.stream(s):
+            g = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g, stream=s):
+                self.update_pair(1)
+            self.pair_graph = g
+        torch.cuda.current_stream().wait_stream(s)
+
+    def replay_pair(self):
+        self.pair_graph.replay()
 
     def capture(self):
         """Capture one CUDA graph per phase of the policy delay (critic-only / critic+actor)."""

@@ -143,13 +143,13 @@ int launch_replay_gather(int B, int S, int A, const float* rs, const float* ra, 
                          const float* rs2, const float* rd, long long N, const long long* idx,
                          unsigned long long seed, int rank, const unsigned long long* counter,
                          float* s, float* a, float* r, float* s2, float* d, unsigned long long* ctr_snap,
-                         cudaStream_t st);
+                         cudaStream_t st, unsigned long long ctr_add = 0);
 // ctr_snap: the step's Philox counter value, written by the gather launch (block 0) and read by
 // the target-noise launch, which advances *counter
 int launch_target_action(int B, int A, const float* a2, const float* noise, float sigma,
                          float clip, unsigned long long seed, int rank,
                          unsigned long long* counter, const unsigned long long* ctr_snap, float* at,
-                         cudaStream_t st);
+                         cudaStream_t st, int advance = 1);   // advance: *counter = snapshot + 1
 int launch_td_target(int B, const float* r, const float* d, const float* q2, float gamma,
                      float* y, cudaStream_t st);
 int launch_scale(float* x, size_t n, float s, cudaStream_t st);

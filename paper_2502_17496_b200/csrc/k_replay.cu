@@ -51,19 +51,21 @@ __global__ void replay_gather_kernel(int B, int S, int A, const float* __restric
                                      const unsigned long long* __restrict__ counter,
                                      float* __restrict__ s, float* __restrict__ a,
                                      float* __restrict__ r, float* __restrict__ s2,
-                                     float* __restrict__ d, unsigned long long* __restrict__ ctr_snap) {
+                                     float* __restrict__ d, unsigned long long* __restrict__ ctr_snap,
+                                     unsigned long long ctr_add) {
   pdl_wait();
   pdl_trigger();
   const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
-  // the step's counter value for the later target-noise draws (which then advance the counter)
-  if (ctr_snap && blockIdx.x == 0 && threadIdx.x == 0) *ctr_snap = *counter;
+  // the step's counter value (the device counter + ctr_add: the second update of a pair draws with
+  // the value the first one advanced to) for the later target-noise draws
+  if (ctr_snap && blockIdx.x == 0 && threadIdx.x == 0) *ctr_snap = *counter + ctr_add;
   if (warp >= B) return;
   long long i = 0;
   if (lane == 0) {
     if (idx) {
       i = idx[warp];
     } else {
-      const unsigned long long ctr = *counter;
+      const unsigned long long ctr = *counter + ctr_add;
       const uint4 x = Philox::gen(make_uint4((uint32_t)warp, P_INDEX, (uint32_t)ctr, (uint32_t)(ctr >> 32)),
                                   philox_key(seed, rank));
       const unsigned long long u = ((unsigned long long)x.x << 32) | x.y;
@@ -86,11 +88,11 @@ int launch_replay_gather(int B, int S, int A, const float* rs, const float* ra, 
                          const float* rs2, const float* rd, long long N, const long long* idx,
                          unsigned long long seed, int rank, const unsigned long long* counter,
                          float* s, float* a, float* r, float* s2, float* d, unsigned long long* ctr_snap,
-                         cudaStream_t st) {
+                         cudaStream_t st, unsigned long long ctr_add) {
   ProfScope ps_("replay_gather", PB_LATENCY, 0.0, 8.0 * B * (2.0 * S + A + 2), st);
   pdl(replay_gather_kernel, cdiv((long long)B * 32, 256), 256, 0, st)(B, S, A, rs, ra, rr, rs2, rd, N, idx,
                                                                      seed, rank, counter, s, a, r, s2, d,
-                                                                     ctr_snap);
+                                                                     ctr_snap, ctr_add);
   SPK_LAUNCHED();
   return SPIKERL_OK;
 }
@@ -104,12 +106,12 @@ __global__ void __launch_bounds__(256) target_action_kernel(int B, int A, const 
                                                             unsigned long long seed, int rank,
                                                             unsigned long long* counter,
                                                             const unsigned long long* __restrict__ ctr_snap,
-                                                            float* __restrict__ at) {
+                                                            float* __restrict__ at, int advance) {
   pdl_wait();
   pdl_trigger();
   const unsigned long long ctr = *ctr_snap;
   const int n = B * A;
-  if (blockIdx.x == 0 && threadIdx.x == 0) *counter = ctr + 1;
+  if (advance && blockIdx.x == 0 && threadIdx.x == 0) *counter = ctr + 1;
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
     float eps;
     if (noise) {
@@ -127,11 +129,11 @@ __global__ void __launch_bounds__(256) target_action_kernel(int B, int A, const 
 
 int launch_target_action(int B, int A, const float* a2, const float* noise, float sigma, float clip,
                          unsigned long long seed, int rank, unsigned long long* counter,
-                         const unsigned long long* ctr_snap, float* at, cudaStream_t st) {
+                         const unsigned long long* ctr_snap, float* at, cudaStream_t st, int advance) {
   ProfScope ps_("target_action", PB_LATENCY, 0.0, 12.0 * B * A, st);
   const int blocks = cdiv((long long)B * A, 512);   // two elements (one Box-Muller pair) per thread
   pdl(target_action_kernel, blocks < 148 ? (blocks > 0 ? blocks : 1) : 148, 256, 0, st)(
-      B, A, a2, noise, sigma, clip, seed, rank, counter, ctr_snap, at);
+      B, A, a2, noise, sigma, clip, seed, rank, counter, ctr_snap, at, advance);
   SPK_LAUNCHED();
   return SPIKERL_OK;
 }

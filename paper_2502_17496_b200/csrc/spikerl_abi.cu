@@ -635,4 +635,132 @@ int spikerl_td3_update(const spikerl_actor_cfg* acfg, const spikerl_critic_cfg* 
   return SPIKERL_OK;
 }
 
+// Two consecutive updates k (critic only) and k + 1 (critic + actor + targets) with policy_delay 2,
+// enqueued as one fork/join DAG. Update k + 1's target path (pi'(s'), smoothing, Q'(s', a~), y) and
+// its pi(s) forward read only the targets and the actor, which update k does not change, so they run
+// concurrently with update k instead of after it; every kernel and operand is the one the two
+// sequential calls use, so the result is bitwise the same (tested). Workspace: two update
+// workspaces back to back (spikerl_td3_pair_workspace_bytes).
+int spikerl_td3_update_pair(const spikerl_actor_cfg* acfg, const spikerl_critic_cfg* ccfg, const spikerl_td3_cfg* hp,
+                            const spikerl_td3_bufs* b, long long step, unsigned long long seed,
+                            const long long* indices, const float* noise, spikerl_comm* comm, float* losses,
+                            void* workspace, spikerl_stream_t stream) {
+  ActorDims ad;
+  CriticDims cd;
+  SPK_TRY(actor_dims(acfg, &ad));
+  SPK_TRY(critic_dims(ccfg, &cd));
+  if (!hp || !b || !workspace || !losses || step < 1) {
+    set_error("spikerl_td3_update_pair: bad arguments");
+    return SPIKERL_E_ARG;
+  }
+  if (hp->policy_delay != 2 || step % 2 != 1) {
+    set_error("spikerl_td3_update_pair: needs policy_delay 2 and an odd first step (got %d, %lld)", hp->policy_delay,
+              step);
+    return SPIKERL_E_ARG;
+  }
+  const int B = hp->batch;
+  if (B < 1 || cd.in != ad.S + ad.A || cd.bf16 != ad.bf16) {
+    set_error("spikerl_td3_update_pair: inconsistent configs");
+    return SPIKERL_E_ARG;
+  }
+  if (!b->actor || !b->actor_t || !b->critic || !b->critic_t || !b->m_actor || !b->v_actor || !b->m_critic ||
+      !b->v_critic || !b->grad_actor || !b->grad_critic || !b->adam_steps || !b->rng_counter || !b->rs ||
+      !b->ra || !b->rr || !b->rs2 || !b->rd ||
+      (ad.bf16 && (!b->actor_bf16 || !b->actor_t_bf16 || !b->critic_bf16 || !b->critic_t_bf16))) {
+    set_error("spikerl_td3_update_pair: null buffer");
+    return SPIKERL_E_ARG;
+  }
+  if (b->replay_size < B) {
+    set_error("replay holds %lld < batch %d transitions", b->replay_size, B);
+    return SPIKERL_E_NOTREADY;
+  }
+  cudaStream_t st = (cudaStream_t)stream;
+  const Td3Ws W = td3_ws_layout(ad, cd, B);
+  struct Slot {
+    float *s, *a, *r, *s2, *dn, *a2, *at, *api, *qt, *q, *y, *ga;
+    char *tape, *aws;
+    void *cws, *cws_t;
+    unsigned long long* snap;
+  } sl[2];
+  for (int i = 0; i < 2; ++i) {
+    char* ws = (char*)workspace + (size_t)i * W.total;
+    Slot& x = sl[i];
+    x.s = (float*)(ws + W.s); x.a = (float*)(ws + W.a); x.r = (float*)(ws + W.r); x.s2 = (float*)(ws + W.s2);
+    x.dn = (float*)(ws + W.d); x.a2 = (float*)(ws + W.a2); x.at = (float*)(ws + W.at); x.api = (float*)(ws + W.api);
+    x.qt = (float*)(ws + W.qt); x.q = (float*)(ws + W.q); x.y = (float*)(ws + W.y); x.ga = (float*)(ws + W.ga);
+    x.tape = ws + W.tape; x.aws = ws + W.actor_ws; x.cws = ws + W.critic_ws; x.cws_t = ws + W.critic_ws_t;
+    x.snap = (unsigned long long*)(ws + W.ctr);
+  }
+  const int rank = spikerl_comm_rank(comm);
+  const size_t Pa = ad.off[SPIKERL_ACTOR_NPARAM];
+  const size_t Pc = cd.off[SPIKERL_CRITIC_NPARAM];
+  const __nv_bfloat16* abf = (const __nv_bfloat16*)b->actor_bf16;
+  const __nv_bfloat16* atbf = (const __nv_bfloat16*)b->actor_t_bf16;
+  const __nv_bfloat16* cbf = (const __nv_bfloat16*)b->critic_bf16;
+  const __nv_bfloat16* ctbf = (const __nv_bfloat16*)b->critic_t_bf16;
+  AuxPool* aux = nullptr;
+  SPK_TRY(aux_pool(&aux));
+  cudaStream_t sA[2] = {aux->side[0], aux->side[7]}, sB = aux->side[1], sC = aux->side[2];
+  cudaEvent_t evA[2] = {aux->ev[1], aux->ev[7]};
+  // sample both minibatches (update k + 1 draws with the counter value update k advances to)
+  for (int i = 0; i < 2; ++i)
+    SPK_TRY(launch_replay_gather(B, ad.S, ad.A, b->rs, b->ra, b->rr, b->rs2, b->rd, b->replay_size,
+                                 indices ? indices + (size_t)i * B : nullptr, seed, rank, b->rng_counter, sl[i].s,
+                                 sl[i].a, sl[i].r, sl[i].s2, sl[i].dn, sl[i].snap, st, (unsigned long long)i));
+  // target paths of both updates, concurrently (branches A0, A1); only the second advances the counter
+  for (int i = 0; i < 2; ++i) {
+    const Slot& x = sl[i];
+    SPK_TRY(stream_after(sA[i], st, aux->ev[i == 0 ? 0 : 6]));
+    SPK_TRY(actor_forward_impl(ad, B, b->actor_t, atbf, x.s2, x.a2, x.aws + actor_ws_layout(ad, B).tape, sA[i]));
+    SPK_TRY(launch_target_action(B, ad.A, x.a2, noise ? noise + (size_t)i * B * ad.A : nullptr, hp->policy_noise,
+                                 hp->noise_clip, seed, rank, b->rng_counter, x.snap, x.at, sA[i], i == 1 ? 1 : 0));
+    SPK_TRY(critic_fwd_bwd(cd, B, b->critic_t, ctbf, x.s2, ad.S, x.at, ad.A, nullptr, x.qt, nullptr, nullptr, nullptr,
+                           0.f, 2, x.cws_t, sA[i]));
+    SPK_TRY(launch_td_target(B, x.r, x.dn, x.qt, hp->gamma, x.y, sA[i]));
+    SPK_CHECK_CUDA(cudaEventRecord(evA[i], sA[i]));
+  }
+  // branch B: pi(s) of update k + 1 (the actor is unchanged by update k)
+  SPK_TRY(stream_after(sB, st, aux->ev[2]));
+  SPK_TRY(actor_forward_impl(ad, B, b->actor, abf, sl[1].s, sl[1].api, sl[1].tape, sB));
+  SPK_CHECK_CUDA(cudaEventRecord(aux->ev[3], sB));
+  const Bf16Views cv = critic_bf16_views(cd, ad.bf16 ? (__nv_bfloat16*)b->critic_bf16 : nullptr);
+  const Bf16Views ctv = critic_bf16_views(cd, ad.bf16 ? (__nv_bfloat16*)b->critic_t_bf16 : nullptr);
+  const Bf16Views av = actor_bf16_views(ad, ad.bf16 ? (__nv_bfloat16*)b->actor_bf16 : nullptr);
+  const Bf16Views atv = actor_bf16_views(ad, ad.bf16 ? (__nv_bfloat16*)b->actor_t_bf16 : nullptr);
+  // the two critic updates, in order
+  for (int i = 0; i < 2; ++i) {
+    const Slot& x = sl[i];
+    SPK_TRY(critic_fwd_bwd(cd, B, b->critic, cbf, x.s, ad.S, x.a, ad.A, x.y, x.q, losses, b->grad_critic, nullptr,
+                           0.f, 2, x.cws, st, evA[i]));
+    SPK_TRY(spikerl_allreduce_grads(comm, b->grad_critic, 2 * Pc, stream));
+    SPK_TRY(launch_adam(b->critic, b->grad_critic, b->m_critic, b->v_critic, 2 * Pc, b->adam_steps, hp->lr_critic,
+                        hp->beta1, hp->beta2, hp->eps, 0, 0, 0.f, (unsigned int*)(b->adam_steps + 1), &cv, st));
+  }
+  // delayed actor update + targets (update k + 1), exactly as spikerl_td3_update's actor step
+  const Slot& x = sl[1];
+  SPK_TRY(stream_after(sC, st, aux->ev[4]));
+  SPK_TRY(launch_polyak(b->critic_t, b->critic, 2 * Pc, hp->tau, &ctv, sC));
+  SPK_CHECK_CUDA(cudaEventRecord(aux->ev[5], sC));
+  SPK_CHECK_CUDA(cudaStreamWaitEvent(st, aux->ev[3], 0));
+  const bool mma = critic_mma_ok(cd);
+  SPK_TRY(critic_fwd_bwd(cd, B, b->critic, cbf, x.s, ad.S, x.api, ad.A, nullptr, x.q, mma ? losses + 1 : nullptr,
+                         nullptr, x.ga, -1.0f / (float)B, 1, x.cws, st));
+  if (!mma) {
+    pdl(neg_mean_kernel, 1, 256, 0, st)(B, x.q, losses + 1);
+    SPK_LAUNCHED();
+  }
+  SPK_TRY(actor_backward_impl(ad, B, b->actor, abf, x.s, x.tape, x.ga, b->grad_actor, 0, x.aws, st));
+  SPK_TRY(spikerl_allreduce_grads(comm, b->grad_actor, Pa, stream));
+  SPK_TRY(launch_adam(b->actor, b->grad_actor, b->m_actor, b->v_actor, Pa, b->adam_steps + 2, hp->lr_actor, hp->beta1,
+                      hp->beta2, hp->eps, ad.off[SPIKERL_ACTOR_SIGMA], ad.off[SPIKERL_ACTOR_W1], ad.sigma_floor,
+                      (unsigned int*)(b->adam_steps + 3), &av, st));
+  SPK_TRY(launch_polyak(b->actor_t, b->actor, Pa, hp->tau, &atv, st));
+  SPK_CHECK_CUDA(cudaStreamWaitEvent(st, aux->ev[5], 0));
+  return SPIKERL_OK;
+}
+
+size_t spikerl_td3_pair_workspace_bytes(const spikerl_actor_cfg* acfg, const spikerl_critic_cfg* ccfg, int batch) {
+  return 2 * spikerl_td3_workspace_bytes(acfg, ccfg, batch);
+}
+
 }  // extern "C"

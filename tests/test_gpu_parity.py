@@ -560,3 +560,54 @@ def test_nccl_single_rank_comm():
         for a, b in zip(outs[0], other):
             assert torch.equal(a, b)
     comm.close()
+
+
+@pytest.mark.parametrize("preset", ["cfg1", "cfg3L"])
+def test_td3_pair_matches_sequential(preset):
+    """spikerl_td3_update_pair(k) (update k + 1's target path and pi(s) overlapping update k) leaves
+    bitwise the same state as update(k); update(k + 1): with injected minibatches / noise, with the
+    device Philox draws (counter advanced by two), and replayed from a captured graph."""
+    import torch
+    import paper_2502_17496_b200 as pk
+    shape, cs_, B = sg.preset(preset)
+    replay = pk.replay_fill(20000, shape.obs_dim, shape.act_dim, seed=3)
+    g = torch.Generator(device="cuda").manual_seed(5)
+    idx = torch.randint(0, 20000, (2, B), device="cuda", generator=g, dtype=torch.int64)
+    nz = torch.randn(2, B, shape.act_dim, device="cuda", generator=g)
+    outs = {}
+    for mode in ("seq", "pair", "seq_rng", "pair_rng", "pair_graph"):
+        rng = np.random.default_rng(8)
+        actor = sg.actor_params(shape, rng)
+        cs = sg.CriticShape(cs_.in_dim, precision="bf16")
+        c1, c2 = sg.critic_params(cs, rng), sg.critic_params(cs, rng)
+        td3 = pk.TD3(pk.actor_cfg_from(shape), pk.critic_cfg(cs_.in_dim), pk.td3_cfg(B), replay, seed=11)
+        td3.load(actor, c1, c2)
+        for j in range(2):          # steps 1..4
+            k = 2 * j + 1
+            if mode == "seq":
+                td3.update(k, idx[0], nz[0]); td3.update(k + 1, idx[1], nz[1])
+            elif mode == "pair":
+                td3.update_pair(k, idx, nz)
+            elif mode == "seq_rng":
+                td3.update(k); td3.update(k + 1)
+            elif mode == "pair_rng":
+                td3.update_pair(k)
+            else:
+                if j == 0:
+                    snap = [t.clone() for t in (td3.actor, td3.critic, td3.actor_t, td3.critic_t)]
+                    td3.capture_pair()
+                    for t, sn in zip((td3.actor, td3.critic, td3.actor_t, td3.critic_t), snap):
+                        t.copy_(sn)
+                    td3.refresh()
+                    for t in (td3.m_actor, td3.v_actor, td3.m_critic, td3.v_critic, td3.adam_steps,
+                              td3.rng_counter):
+                        t.zero_()
+                td3.replay_pair()
+        torch.cuda.synchronize()
+        outs[mode] = [t.cpu().clone() for t in (td3.actor, td3.critic, td3.actor_t, td3.critic_t, td3.losses,
+                                                 td3.m_actor, td3.v_critic, td3.rng_counter)]
+    for a, b in zip(outs["seq"], outs["pair"]):
+        assert torch.equal(a, b)
+    for other in ("pair_rng", "pair_graph"):
+        for a, b in zip(outs["seq_rng"], outs[other]):
+            assert torch.equal(a, b), other

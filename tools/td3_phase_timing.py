@@ -26,4 +26,15 @@ for k, label in ((1, "critic_only"), (2, "critic_and_actor")):
     e1.record()
     torch.cuda.synchronize()
     out[label] = round(e0.elapsed_time(e1) / 200 * 1000, 2)
+td3.capture_pair()
+for _ in range(20):
+    td3.replay_pair()
+torch.cuda.synchronize()
+e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+e0.record()
+for _ in range(100):
+    td3.replay_pair()
+e1.record()
+torch.cuda.synchronize()
+out["pair_per_update"] = round(e0.elapsed_time(e1) / 200 * 1000, 2)
 print(json.dumps({"workload": name, "us_per_step": out, "serial": os.environ.get("SPIKERL_TD3_SERIAL", "0")}))
