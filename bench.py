@@ -416,7 +416,7 @@ def run_td3(args, rank, world):
         out["energy"] = en
     # e2e: minibatch from pinned host memory every step + loss read-back, through the public API
     if not args.no_e2e:
-        out["e2e"] = e2e_td3(args, rank, world, td3, shape, B)
+        out["e2e"] = e2e_td3(args, rank, world, td3, shape, B, pair=pair)
     # roofline: eager profiling pass (CUDA events around every launch on its own stream)
     _lib.prof_enable(True)
     for k in range(8):
@@ -430,7 +430,12 @@ def run_td3(args, rank, world):
     return out
 
 
-def e2e_td3(args, rank, world, td3_dev, shape, B):
+def e2e_td3(args, rank, world, td3_dev, shape, B, pair=False):
+    """End to end through the public API: every update's minibatch is copied from pinned host memory
+    (5 H2D copies per update) and the losses are read back to pinned host memory; the timed region
+    contains the copies. pair: each timed iteration is one captured graph of [H2D copies of two
+    minibatches -> spikerl_td3_update_pair -> D2H of the losses] (one graph per pair of host buffers);
+    otherwise an eager TD3.update per update."""
     import numpy as np
     import torch
     import paper_2502_17496_b200 as pk
@@ -441,30 +446,83 @@ def e2e_td3(args, rank, world, td3_dev, shape, B):
     host = [pk.replay_from_host(__import__("synthgen").replay_batch(rng, B, S, A), device="cpu") for _ in range(nbuf)]
     host = [pk.ReplayShard(*(t.pin_memory() for t in (h.s, h.a, h.r, h.s2, h.d))) for h in host]
     f32 = dict(dtype=torch.float32, device="cuda")
-    rs = pk.ReplayShard(torch.empty(B, S, **f32), torch.empty(B, A, **f32), torch.empty(B, **f32),
-                        torch.empty(B, S, **f32), torch.empty(B, **f32))   # device staging = a replay of size B
+    nb = 2 if pair else 1
+    # device staging = a replay of nb B rows whose five arrays are views of ONE buffer, so a pinned
+    # host buffer with the same layout arrives in a single H2D copy
+    dev = torch.empty(nb * B * per, **f32)
+
+    def views(buf):
+        n, o, out = nb * B, 0, []
+        for w in (S, A, 1, S, 1):
+            v = buf[o:o + n * w]
+            out.append(v.view(n, w) if w > 1 else v)
+            o += n * w
+        return pk.ReplayShard(*out)
+
+    rs = views(dev)
+    if pair:   # pinned host buffers, one per pair of pool minibatches, in the staging layout
+        packed = []
+        for g_i in range(nbuf // 2):
+            hb = torch.empty(nb * B * per, dtype=torch.float32).pin_memory()
+            hv = views(hb)
+            for j in range(2):
+                h = host[2 * g_i + j]
+                for src, dst in ((h.s, hv.s), (h.a, hv.a), (h.r, hv.r), (h.s2, hv.s2), (h.d, hv.d)):
+                    dst[j * B:(j + 1) * B].copy_(src)
+            packed.append(hb)
     td3 = pk.TD3(td3_dev.acfg, td3_dev.ccfg, td3_dev.hp, rs, seed=1, comm=td3_dev.comm)
     for t_src, t_dst in ((td3_dev.actor, td3.actor), (td3_dev.actor_t, td3.actor_t), (td3_dev.critic, td3.critic),
                          (td3_dev.critic_t, td3.critic_t)):
         t_dst.copy_(t_src)
     td3.refresh()
-    idx = torch.arange(B, dtype=torch.int64, device="cuda")
+    idx = torch.arange(nb * B, dtype=torch.int64, device="cuda").view(nb, B)
     loss_host = torch.empty(2, dtype=torch.float32).pin_memory()
 
-    def step(k):
-        h = host[k % nbuf]
+    def h2d(h, j):
         for src, dst in ((h.s, rs.s), (h.a, rs.a), (h.r, rs.r), (h.s2, rs.s2), (h.d, rs.d)):
-            dst.copy_(src, non_blocking=True)          # one cudaMemcpyAsync H2D each
-        td3.update(k + 1, indices=idx)
-        loss_host.copy_(td3.losses, non_blocking=True)
+            dst[j * B:(j + 1) * B].copy_(src, non_blocking=True)          # one cudaMemcpyAsync H2D each
 
-    for k in range(args.warmup):
-        step(k)
-    total_ms = time_steps(step, args.steps, None, world)
-    torch.cuda.synchronize()
-    return {"value": round(args.steps * B * world / (total_ms / 1e3), 2), "unit": "samples/s",
-            "h2d_bytes_per_step": B * per * 4, "d2h_bytes_per_step": 8,
-            "path": "TD3.update (eager C-ABI call) fed from pinned host minibatches; losses read back"}
+    if pair:
+        graphs = []
+        cs = torch.cuda.Stream()
+        cs.wait_stream(torch.cuda.current_stream())
+        with torch.cuda.stream(cs):
+            for g_i in range(nbuf // 2):
+                g = torch.cuda.CUDAGraph()
+                with torch.cuda.graph(g, stream=cs):
+                    dev.copy_(packed[g_i], non_blocking=True)      # both minibatches: one H2D copy
+                    td3.update_pair(1, indices=idx)
+                    loss_host.copy_(td3.losses, non_blocking=True)
+                graphs.append(g)
+        torch.cuda.current_stream().wait_stream(cs)
+        torch.cuda.synchronize()
+
+        def step(k):
+            graphs[k % len(graphs)].replay()
+
+        for k in range(max(1, args.warmup // 2)):
+            step(k)
+        npair = max(1, args.steps // 2)
+        total_ms = time_steps(step, npair, None, world)
+        torch.cuda.synchronize()
+        n_upd = 2 * npair
+        path = ("graph of [one H2D copy of two packed pinned host minibatches -> spikerl_td3_update_pair -> D2H "
+                "of the losses] per two updates (TD3.update_pair through the C ABI)")
+    else:
+        def step(k):
+            h2d(host[k % nbuf], 0)
+            td3.update(k + 1, indices=idx[0])
+            loss_host.copy_(td3.losses, non_blocking=True)
+
+        for k in range(args.warmup):
+            step(k)
+        total_ms = time_steps(step, args.steps, None, world)
+        torch.cuda.synchronize()
+        n_upd = args.steps
+        path = "TD3.update (eager C-ABI call) fed from pinned host minibatches; losses read back"
+    return {"value": round(n_upd * B * world / (total_ms / 1e3), 2), "unit": "samples/s",
+            "h2d_bytes_per_step": B * per * 4, "d2h_bytes_per_step": 8 // nb if pair else 8,
+            "path": path}
 
 
 def run_actor(args, rank, world):
