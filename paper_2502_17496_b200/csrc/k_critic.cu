@@ -300,11 +300,9 @@ int critic_fwd_bwd(const CriticDims& c, int B, const float* params2, const __nv_
   CriticWs w = carve(c, B, ws);
   const bool bf = c.bf16 != 0;
   const long long P = (long long)c.off[SPIKERL_CRITIC_NPARAM];
-  const void* Wbase = bf ? (const void*)pb16 : (const void*)params2;
   auto Wp = [&](int idx) -> const void* {
     return bf ? (const void*)(pb16 + c.off[idx]) : (const void*)(params2 + c.off[idx]);
   };
-  (void)Wbase;
   const int in = c.in, H1 = c.H1, H2 = c.H2;
   pdl(build_x_kernel, cdiv((long long)B * in, 256) < 1184 ? cdiv((long long)B * in, 256) : 1184, 256, 0, st)(
       B, S, A, obs, act, bf, w.X);

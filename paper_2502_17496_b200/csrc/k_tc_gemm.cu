@@ -317,8 +317,6 @@ __device__ __forceinline__ Tile decode(const Params& p, int u, int rank, int CG)
 }
 
 // ------------------------------------------------------------------------- the kernel
-// Expander prefetch depth (k-blocks of spike words kept in registers ahead of the smem ring).
-constexpr int PF = 4;
 
 // CG = 1: one CTA computes a 128-row tile. CG = 2: a CTA pair (cluster of 2) computes a 256-row
 // tile with tcgen05.mma.cta_group::2 issued by rank 0: each CTA holds its 128 rows of A and half
