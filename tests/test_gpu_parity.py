@@ -533,7 +533,7 @@ def test_nccl_single_rank_comm():
     shape, _, B = sg.preset("cfg1")
     replay = pk.replay_fill(20000, 17, 6, seed=3)
     outs = []
-    for use_comm, mode in ((False, "eager"), (True, "eager"), (True, "graph")):
+    for use_comm, mode in ((False, "eager"), (True, "eager"), (True, "graph"), (True, "pair")):
         rng = np.random.default_rng(8)
         actor = sg.actor_params(shape, rng)
         cs = sg.CriticShape(23, precision="bf16")
@@ -551,6 +551,9 @@ def test_nccl_single_rank_comm():
                 t.zero_()
             for k in range(1, 5):
                 td3.replay_graph(k)
+        elif mode == "pair":
+            td3.update_pair(1)
+            td3.update_pair(3)
         else:
             for k in range(1, 5):
                 td3.update(k)
