@@ -139,11 +139,17 @@ int critic_fwd_bwd(const CriticDims& c, int B, const float* params2, const __nv_
                    void* ws, cudaStream_t st, cudaEvent_t wait_before_loss = nullptr);
 
 // ---- replay / TD3 glue (k_replay.cu)
+// minibatch destinations of one gather launch (1 slot, or the 2 updates of a pair); idx[slot] = NULL:
+// indices drawn on the device with the counter value *counter + slot (snapshotted into snap[slot])
+struct GatherSlots {
+  int n;
+  float *s[2], *a[2], *r[2], *s2[2], *d[2];
+  unsigned long long* snap[2];
+  const long long* idx[2];
+};
 int launch_replay_gather(int B, int S, int A, const float* rs, const float* ra, const float* rr,
-                         const float* rs2, const float* rd, long long N, const long long* idx,
-                         unsigned long long seed, int rank, const unsigned long long* counter,
-                         float* s, float* a, float* r, float* s2, float* d, unsigned long long* ctr_snap,
-                         cudaStream_t st, unsigned long long ctr_add = 0);
+                         const float* rs2, const float* rd, long long N, unsigned long long seed, int rank,
+                         const unsigned long long* counter, const GatherSlots& gs, cudaStream_t st);
 // ctr_snap: the step's Philox counter value, written by the gather launch (block 0) and read by
 // the target-noise launch, which advances *counter
 int launch_target_action(int B, int A, const float* a2, const float* noise, float sigma,

@@ -43,56 +43,53 @@ __device__ __forceinline__ float2 box_muller(uint32_t a, uint32_t b) {
 enum Purpose : uint32_t { P_INDEX = 1, P_NOISE = 2, P_FILL = 3 };
 
 // one warp per sampled row: lane 0 draws the index, the warp copies the row's columns
+// one warp per sampled row: lane 0 draws the index, the warp copies the row's columns. Up to two
+// minibatches (the two updates of a pair) in one launch: warp w < nslots B samples row w % B of
+// slot w / B, whose draws use the device counter + slot (the second update of a pair draws with the
+// value the first one advances to); block 0 snapshots those values for the target-noise launches.
 __global__ void replay_gather_kernel(int B, int S, int A, const float* __restrict__ rs,
                                      const float* __restrict__ ra, const float* __restrict__ rr,
                                      const float* __restrict__ rs2, const float* __restrict__ rd,
-                                     long long N, const long long* __restrict__ idx,
-                                     unsigned long long seed, int rank,
-                                     const unsigned long long* __restrict__ counter,
-                                     float* __restrict__ s, float* __restrict__ a,
-                                     float* __restrict__ r, float* __restrict__ s2,
-                                     float* __restrict__ d, unsigned long long* __restrict__ ctr_snap,
-                                     unsigned long long ctr_add) {
+                                     long long N, unsigned long long seed, int rank,
+                                     const unsigned long long* __restrict__ counter, const GatherSlots gs) {
   pdl_wait();
   pdl_trigger();
   const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
-  // the step's counter value (the device counter + ctr_add: the second update of a pair draws with
-  // the value the first one advanced to) for the later target-noise draws
-  if (ctr_snap && blockIdx.x == 0 && threadIdx.x == 0) *ctr_snap = *counter + ctr_add;
-  if (warp >= B) return;
+  if (blockIdx.x == 0 && threadIdx.x < gs.n && gs.snap[threadIdx.x])
+    *gs.snap[threadIdx.x] = *counter + threadIdx.x;
+  if (warp >= gs.n * B) return;
+  const int slot = warp / B, row = warp - slot * B;
   long long i = 0;
   if (lane == 0) {
-    if (idx) {
-      i = idx[warp];
+    if (gs.idx[slot]) {
+      i = gs.idx[slot][row];
     } else {
-      const unsigned long long ctr = *counter + ctr_add;
-      const uint4 x = Philox::gen(make_uint4((uint32_t)warp, P_INDEX, (uint32_t)ctr, (uint32_t)(ctr >> 32)),
+      const unsigned long long ctr = *counter + slot;
+      const uint4 x = Philox::gen(make_uint4((uint32_t)row, P_INDEX, (uint32_t)ctr, (uint32_t)(ctr >> 32)),
                                   philox_key(seed, rank));
       const unsigned long long u = ((unsigned long long)x.x << 32) | x.y;
       i = (long long)(u % (unsigned long long)N);
     }
   }
   i = __shfl_sync(0xffffffffu, i, 0);
+  float* const s = gs.s[slot]; float* const s2 = gs.s2[slot]; float* const a = gs.a[slot];
   for (int c = lane; c < S; c += 32) {
-    s[(size_t)warp * S + c] = rs[(size_t)i * S + c];
-    s2[(size_t)warp * S + c] = rs2[(size_t)i * S + c];
+    s[(size_t)row * S + c] = rs[(size_t)i * S + c];
+    s2[(size_t)row * S + c] = rs2[(size_t)i * S + c];
   }
-  for (int c = lane; c < A; c += 32) a[(size_t)warp * A + c] = ra[(size_t)i * A + c];
+  for (int c = lane; c < A; c += 32) a[(size_t)row * A + c] = ra[(size_t)i * A + c];
   if (lane == 0) {
-    r[warp] = rr[i];
-    d[warp] = rd[i];
+    gs.r[slot][row] = rr[i];
+    gs.d[slot][row] = rd[i];
   }
 }
 
 int launch_replay_gather(int B, int S, int A, const float* rs, const float* ra, const float* rr,
-                         const float* rs2, const float* rd, long long N, const long long* idx,
-                         unsigned long long seed, int rank, const unsigned long long* counter,
-                         float* s, float* a, float* r, float* s2, float* d, unsigned long long* ctr_snap,
-                         cudaStream_t st, unsigned long long ctr_add) {
-  ProfScope ps_("replay_gather", PB_LATENCY, 0.0, 8.0 * B * (2.0 * S + A + 2), st);
-  pdl(replay_gather_kernel, cdiv((long long)B * 32, 256), 256, 0, st)(B, S, A, rs, ra, rr, rs2, rd, N, idx,
-                                                                     seed, rank, counter, s, a, r, s2, d,
-                                                                     ctr_snap, ctr_add);
+                         const float* rs2, const float* rd, long long N, unsigned long long seed, int rank,
+                         const unsigned long long* counter, const GatherSlots& gs, cudaStream_t st) {
+  ProfScope ps_("replay_gather", PB_LATENCY, 0.0, 8.0 * gs.n * B * (2.0 * S + A + 2), st);
+  pdl(replay_gather_kernel, cdiv((long long)gs.n * B * 32, 256), 256, 0, st)(B, S, A, rs, ra, rr, rs2, rd, N, seed,
+                                                                            rank, counter, gs);
   SPK_LAUNCHED();
   return SPIKERL_OK;
 }

@@ -581,8 +581,13 @@ int spikerl_td3_update(const spikerl_actor_cfg* acfg, const spikerl_critic_cfg* 
 
   // K9: sample (s, a, r, s', d)
   unsigned long long* ctr_snap = (unsigned long long*)(ws + W.ctr);
-  SPK_TRY(launch_replay_gather(B, ad.S, ad.A, b->rs, b->ra, b->rr, b->rs2, b->rd, b->replay_size, indices, seed,
-                               rank, b->rng_counter, s, a, r, s2, dn, ctr_snap, st));
+  {
+    GatherSlots gs{};
+    gs.n = 1;
+    gs.s[0] = s; gs.a[0] = a; gs.r[0] = r; gs.s2[0] = s2; gs.d[0] = dn; gs.snap[0] = ctr_snap; gs.idx[0] = indices;
+    SPK_TRY(launch_replay_gather(B, ad.S, ad.A, b->rs, b->ra, b->rr, b->rs2, b->rd, b->replay_size, seed, rank,
+                                 b->rng_counter, gs, st));
+  }
   // branch A: target path. 1. a~ = clip(pi'(s') + clip(eps), -1, 1); 2. y = r + gamma (1 - d) min(Q1', Q2')(s', a~)
   SPK_TRY(stream_after(sA, st, aux->ev[0]));
   SPK_TRY(actor_forward_impl(ad, B, b->actor_t, atbf, s2, a2, aws + actor_ws_layout(ad, B).tape, sA));
@@ -702,11 +707,18 @@ int spikerl_td3_update_pair(const spikerl_actor_cfg* acfg, const spikerl_critic_
   SPK_TRY(aux_pool(&aux));
   cudaStream_t sA[2] = {aux->side[0], aux->side[7]}, sB = aux->side[1], sC = aux->side[2];
   cudaEvent_t evA[2] = {aux->ev[1], aux->ev[7]};
-  // sample both minibatches (update k + 1 draws with the counter value update k advances to)
-  for (int i = 0; i < 2; ++i)
-    SPK_TRY(launch_replay_gather(B, ad.S, ad.A, b->rs, b->ra, b->rr, b->rs2, b->rd, b->replay_size,
-                                 indices ? indices + (size_t)i * B : nullptr, seed, rank, b->rng_counter, sl[i].s,
-                                 sl[i].a, sl[i].r, sl[i].s2, sl[i].dn, sl[i].snap, st, (unsigned long long)i));
+  // sample both minibatches in one launch (update k + 1 draws with the counter value update k
+  // advances to)
+  {
+    GatherSlots gs{};
+    gs.n = 2;
+    for (int i = 0; i < 2; ++i) {
+      gs.s[i] = sl[i].s; gs.a[i] = sl[i].a; gs.r[i] = sl[i].r; gs.s2[i] = sl[i].s2; gs.d[i] = sl[i].dn;
+      gs.snap[i] = sl[i].snap; gs.idx[i] = indices ? indices + (size_t)i * B : nullptr;
+    }
+    SPK_TRY(launch_replay_gather(B, ad.S, ad.A, b->rs, b->ra, b->rr, b->rs2, b->rd, b->replay_size, seed, rank,
+                                 b->rng_counter, gs, st));
+  }
   // target paths of both updates, concurrently (branches A0, A1); only the second advances the counter
   for (int i = 0; i < 2; ++i) {
     const Slot& x = sl[i];
