@@ -91,6 +91,10 @@ typedef struct {
   int policy_delay;                           /* 2                                            */
   float lr_actor, lr_critic, beta1, beta2, eps; /* 1e-4, 1e-3, 0.9, 0.999, 1e-8             */
   int batch;                                  /* per-rank batch B                             */
+  /* dynamic loss scaling (PAPER.md:164-167 GradScaler; used when bufs->amp != NULL):
+   * scale *= amp_growth after amp_interval consecutive finite steps, *= amp_backoff on overflow */
+  float amp_growth, amp_backoff;              /* 2.0, 0.5                                      */
+  int amp_interval;                           /* 2000                                          */
 } spikerl_td3_cfg;
 
 /* ------------------------------------------------------------------------------------------
@@ -216,6 +220,13 @@ typedef struct {
   unsigned long long* rng_counter; /* device [1]: Philox counter, advanced every update       */
   const float *rs, *ra, *rr, *rs2, *rd; /* replay shard SoA: s[N][S] a[N][A] r[N] s2[N][S] d[N] */
   long long replay_size;           /* (host) N valid transitions                               */
+  /* device [8] or NULL (no scaling): GradScaler state of the critic at [0..3] and of the actor at
+   * [4..7] = {loss scale, finite steps since the last scale change, found_inf, unused}. The loss
+   * gradient is multiplied by the scale; before each Adam step the gradient is checked for inf /
+   * NaN: if any, the optimizer step is skipped (parameters, moments and its step count unchanged)
+   * and the scale backs off; otherwise the gradient is unscaled inside the Adam kernel. The caller
+   * initialises the scales (e.g. 65536) and zeroes the rest. */
+  float* amp;
 } spikerl_td3_bufs;
 
 struct spikerl_comm;

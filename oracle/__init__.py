@@ -13,6 +13,7 @@ Modules (each cites the passages it follows):
   critic.py    twin ReLU critic forward/backward (configs[1]) — pinned (FD)
   td3.py       TD3 update, Adam, Polyak          — pinned (arithmetic)
   dual.py      forward-mode dual-number second oracle for BPTT
+  amp.py       dynamic loss scaling (GradScaler) state machine — pinned
 Unpinned: learning dynamics / rewards (no environment; PAPER.md Figs 5a-c missing) — out of
 scope, "parity unpinned" (DESIGN.md).
 """
@@ -21,3 +22,4 @@ from .actor import (gaussian_stim, encode_spikes, lif_layer_forward, decode, act
                     surrogate, lif_reverse_scan, actor_backward, counts)
 from .critic import critic_forward, critic_backward  # noqa: F401
 from .td3 import adam_update, polyak, init_state, td3_update  # noqa: F401
+from .amp import amp_step, unscale, all_finite  # noqa: F401

@@ -41,7 +41,8 @@ class TD3Cfg(C.Structure):
     _fields_ = [("gamma", C.c_float), ("tau", C.c_float), ("policy_noise", C.c_float),
                 ("noise_clip", C.c_float), ("policy_delay", C.c_int), ("lr_actor", C.c_float),
                 ("lr_critic", C.c_float), ("beta1", C.c_float), ("beta2", C.c_float), ("eps", C.c_float),
-                ("batch", C.c_int)]
+                ("batch", C.c_int), ("amp_growth", C.c_float), ("amp_backoff", C.c_float),
+                ("amp_interval", C.c_int)]
 
 
 class TapeLayout(C.Structure):
@@ -63,7 +64,7 @@ class TD3Bufs(C.Structure):
                 ("v_actor", C.c_void_p), ("m_critic", C.c_void_p), ("v_critic", C.c_void_p),
                 ("grad_actor", C.c_void_p), ("grad_critic", C.c_void_p), ("adam_steps", C.c_void_p),
                 ("rng_counter", C.c_void_p), ("rs", C.c_void_p), ("ra", C.c_void_p), ("rr", C.c_void_p),
-                ("rs2", C.c_void_p), ("rd", C.c_void_p), ("replay_size", C.c_longlong)]
+                ("rs2", C.c_void_p), ("rd", C.c_void_p), ("replay_size", C.c_longlong), ("amp", C.c_void_p)]
 
 
 class ProfEntry(C.Structure):

@@ -48,9 +48,10 @@ def critic_cfg(in_dim, hidden1=256, hidden2=256, precision="bf16") -> L.CriticCf
 
 
 def td3_cfg(batch, gamma=0.99, tau=0.005, policy_noise=0.2, noise_clip=0.5, policy_delay=2, lr_actor=1e-4,
-            lr_critic=1e-3, beta1=0.9, beta2=0.999, eps=1e-8) -> L.TD3Cfg:
+            lr_critic=1e-3, beta1=0.9, beta2=0.999, eps=1e-8, amp_growth=2.0, amp_backoff=0.5,
+            amp_interval=2000) -> L.TD3Cfg:
     return L.TD3Cfg(gamma, tau, policy_noise, noise_clip, policy_delay, lr_actor, lr_critic, beta1, beta2, eps,
-                    batch)
+                    batch, amp_growth, amp_backoff, amp_interval)
 
 
 def actor_offsets(cfg):
@@ -300,7 +301,7 @@ class TD3:
     """Device-resident TD3 state + the C-ABI update."""
 
     def __init__(self, acfg: L.ActorCfg, ccfg: L.CriticCfg, hp: L.TD3Cfg, replay: ReplayShard, device="cuda",
-                 seed=0, comm: Comm | None = None):
+                 seed=0, comm: Comm | None = None, loss_scale: float | None = None):
         self.acfg, self.ccfg, self.hp, self.replay, self.device, self.seed, self.comm = \
             acfg, ccfg, hp, replay, device, seed, comm
         lb = lib()
@@ -322,12 +323,18 @@ class TD3:
         self.adam_steps = torch.zeros(4, dtype=torch.int64, device=device)
         self.rng_counter = torch.zeros(1, dtype=torch.int64, device=device)
         self.losses = torch.zeros(2, **f32)
+        # dynamic loss scaling state (None: no scaling): {scale, finite steps, found_inf, -} x {critic, actor}
+        self.amp = None
+        if loss_scale is not None:
+            self.amp = torch.zeros(8, **f32)
+            self.amp[0] = loss_scale
+            self.amp[4] = loss_scale
         self.ws = _alloc(lb.spikerl_td3_workspace_bytes(C.byref(acfg), C.byref(ccfg), hp.batch), device)
         self._bufs = L.TD3Bufs(*[t.data_ptr() if t is not None else None for t in (
             self.actor, self.actor_t, self.actor_bf16, self.actor_t_bf16, self.critic, self.critic_t,
             self.critic_bf16, self.critic_t_bf16, self.m_actor, self.v_actor, self.m_critic, self.v_critic,
             self.grad_actor, self.grad_critic, self.adam_steps, self.rng_counter, replay.s, replay.a, replay.r,
-            replay.s2, replay.d)], replay.size)
+            replay.s2, replay.d)], replay.size, self.amp.data_ptr() if self.amp is not None else None)
         self.graphs = {}
         self.ws_pair = None
         self.pair_graph = None

@@ -118,7 +118,10 @@ Bf16Views actor_bf16_views(const ActorDims& d, __nv_bfloat16* out);
 Bf16Views critic_bf16_views(const CriticDims& c, __nv_bfloat16* out);
 int launch_adam(float* p, const float* g, float* m, float* v, size_t n, long long* counter,
                 float lr, float b1, float b2, float eps, size_t clo, size_t chi, float cmin,
-                unsigned int* done_ticket, const Bf16Views* views, cudaStream_t st);
+                unsigned int* done_ticket, const Bf16Views* views, cudaStream_t st, float* amp = nullptr,
+                float amp_growth = 2.f, float amp_backoff = 0.5f, int amp_interval = 2000);
+// dynamic loss scaling: amp[2] = 1 when g holds a non-finite element (amp: {scale, count, found, -})
+int launch_amp_check(const float* g, size_t n, float* amp, cudaStream_t st);
 int launch_polyak(float* t, const float* s, size_t n, float tau, const Bf16Views* views, cudaStream_t st);
 
 // ---- critic (k_critic.cu)
@@ -130,13 +133,14 @@ size_t critic_mma_ws_bytes(const CriticDims& c, int B);
 int critic_mma_fwd_bwd(const CriticDims& c, int B, const float* params2, const __nv_bfloat16* pb, const float* obs,
                        int S, const float* act, int A, const float* y, float* q, float* loss, float* grad2,
                        float* grad_act, float act_scale, int nz, void* ws, cudaStream_t st,
-                       cudaEvent_t wait_before_loss = nullptr);
+                       cudaEvent_t wait_before_loss = nullptr, const float* dq_scale = nullptr);
 // wait_before_loss (optional): the stream waits on this event after the forward and before the
 // loss (the TD target y is produced concurrently on another stream).
 int critic_fwd_bwd(const CriticDims& c, int B, const float* params2, const __nv_bfloat16* pb16,
                    const float* obs, int S, const float* act, int A, const float* y, float* q,
                    float* loss, float* grad2, float* grad_act, float act_scale, int n_critics,
-                   void* ws, cudaStream_t st, cudaEvent_t wait_before_loss = nullptr);
+                   void* ws, cudaStream_t st, cudaEvent_t wait_before_loss = nullptr,
+                   const float* dq_scale = nullptr);   // dq_scale: device loss scale applied to dQ
 
 // ---- replay / TD3 glue (k_replay.cu)
 // minibatch destinations of one gather launch (1 slot, or the 2 updates of a pair); idx[slot] = NULL:

@@ -293,10 +293,11 @@ size_t critic_ws_bytes(const CriticDims& c, int B) {
 int critic_fwd_bwd(const CriticDims& c, int B, const float* params2, const __nv_bfloat16* pb16,
                    const float* obs, int S, const float* act, int A, const float* y, float* q,
                    float* loss, float* grad2, float* grad_act, float act_scale, int nz, void* ws,
-                   cudaStream_t st, cudaEvent_t wait_before_loss) {
+                   cudaStream_t st, cudaEvent_t wait_before_loss, const float* dq_scale) {
   if (critic_mma_ok(c))
     return critic_mma_fwd_bwd(c, B, params2, pb16, obs, S, act, A, y, q, loss, grad2, grad_act, act_scale, nz, ws, st,
-                              wait_before_loss);
+                              wait_before_loss, dq_scale);
+  if (dq_scale) { set_error("critic: loss scaling needs the bf16 mma critic"); return SPIKERL_E_UNSUPPORTED; }
   CriticWs w = carve(c, B, ws);
   const bool bf = c.bf16 != 0;
   const long long P = (long long)c.off[SPIKERL_CRITIC_NPARAM];

@@ -336,7 +336,7 @@ __global__ void __launch_bounds__(256) critic_bwd_data_mma_kernel(
     float* __restrict__ loss, const __nv_bfloat16* __restrict__ pb,
     long long P, long long tb, long long oW3, long long oW1T, long long oW2T, const float* __restrict__ Z1,
     const float* __restrict__ Z2, __nv_bfloat16* __restrict__ dZ2T, __nv_bfloat16* __restrict__ dZ1T,
-    float* __restrict__ grad_act, int store_t) {
+    float* __restrict__ grad_act, int store_t, const float* __restrict__ dq_scale) {
   extern __shared__ __align__(128) uint8_t dsm[];
   __nv_bfloat16* const w2s = (__nv_bfloat16*)dsm;    // W2T staged: [HW][HW + SPAD]
   __shared__ __align__(8) uint64_t wbar;
@@ -373,6 +373,7 @@ __global__ void __launch_bounds__(256) critic_bwd_data_mma_kernel(
         d = act_scale;
         c = qv;
       }
+      if (dq_scale) d = __fmul_rn(d, *dq_scale);   // dynamic loss scaling (the loss scalar stays unscaled)
       dq[(size_t)z * B + b] = d;
     }
     if (lane < RB) dqs[lane] = d;
@@ -736,7 +737,7 @@ static bool tc_wgrad_ok(const CriticDims& c, const MmaWs& w, int Bp) {
 int critic_mma_fwd_bwd(const CriticDims& c, int B, const float* params2, const __nv_bfloat16* pb, const float* obs,
                        int S, const float* act, int A, const float* y, float* q, float* loss, float* grad2,
                        float* grad_act, float act_scale, int nz, void* ws, cudaStream_t st,
-                       cudaEvent_t wait_before_loss) {
+                       cudaEvent_t wait_before_loss, const float* dq_scale) {
   const MmaLayout L = mma_layout(c);
   MmaWs w = mma_carve(c, B, ws, nullptr);
   const int Bp = round_up(B, RB);
@@ -782,7 +783,7 @@ int critic_mma_fwd_bwd(const CriticDims& c, int B, const float* params2, const _
     }
     pdl(critic_bwd_data_mma_kernel, grid, 256, kW2Smem, st)(
         B, Bp, S, A, L.inp, q, y, mode, act_scale, w.dq, w.part, w.ticket, fused_scalar ? loss : nullptr, pb, L.P, L.tb,
-        oW3, L.W1T, L.W2T, w.Z1, w.Z2, w.dZ2T, w.dZ1T, grad_act, want_params ? 1 : 0);
+        oW3, L.W1T, L.W2T, w.Z1, w.Z2, w.dZ2T, w.dZ1T, grad_act, want_params ? 1 : 0, dq_scale);
     SPK_LAUNCHED();
   }
   if (want_params) {

@@ -138,28 +138,35 @@ __global__ void __launch_bounds__(256) adam_kernel(float* __restrict__ p, const 
                                                    size_t n, long long* counter, float lr, float b1,
                                                    float b2, float eps, size_t clo, size_t chi,
                                                    float cmin, unsigned int* ticket,
-                                                   const __grid_constant__ Bf16Views views) {
+                                                   const __grid_constant__ Bf16Views views, float* amp,
+                                                   float amp_growth, float amp_backoff, int amp_interval) {
   pdl_wait();
   pdl_trigger();
   // bias corrections once per block (fp64 pow), not once per thread
-  __shared__ float s_coef[2];
+  __shared__ float s_coef[3];
   __shared__ long long s_t;
+  __shared__ int s_skip;
   if (threadIdx.x == 0) {
     const long long tt = *(volatile long long*)counter + 1;
     s_t = tt;
     s_coef[0] = (float)((double)lr / (1.0 - pow((double)b1, (double)tt)));
     s_coef[1] = (float)sqrt(1.0 - pow((double)b2, (double)tt));
+    // loss scaling: skip the step on a non-finite gradient, else unscale by 1 / scale
+    s_skip = amp ? (*(volatile float*)(amp + 2) != 0.0f) : 0;
+    s_coef[2] = amp ? __frcp_rn(*(volatile float*)amp) : 1.0f;
   }
   __syncthreads();
   const long long t = s_t;
   const float step_size = s_coef[0];
   const float bc2_sqrt = s_coef[1];
+  const float inv_scale = s_coef[2];
+  const bool skip = s_skip != 0;
   const float omb1 = 1.0f - b1, omb2 = 1.0f - b2;
   const size_t n4 = n / 4;
   const size_t stride = (size_t)gridDim.x * blockDim.x;
   // two float4 groups per thread and iteration, every load issued before any arithmetic (more
   // bytes in flight per thread: 128 B)
-  for (size_t i0 = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i0 < n4; i0 += 2 * stride) {
+  for (size_t i0 = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i0 < n4 && !skip; i0 += 2 * stride) {
     float4 pp[2], gg[2], mm[2], vv[2];
     const bool two = i0 + stride < n4;
 #pragma unroll
@@ -176,9 +183,10 @@ __global__ void __launch_bounds__(256) adam_kernel(float* __restrict__ p, const 
     for (int u = 0; u < 2; ++u) {
       if (u == 1 && !two) break;
       const size_t i = i0 + u * stride;
-      float* pa = &pp[u].x; const float* ga = &gg[u].x; float* ma = &mm[u].x; float* va = &vv[u].x;
+      float* pa = &pp[u].x; float* ga = &gg[u].x; float* ma = &mm[u].x; float* va = &vv[u].x;
 #pragma unroll
       for (int j = 0; j < 4; ++j) {
+        if (amp) ga[j] = __fmul_rn(ga[j], inv_scale);
         ma[j] = __fadd_rn(__fmul_rn(b1, ma[j]), __fmul_rn(omb1, ga[j]));
         va[j] = __fadd_rn(__fmul_rn(b2, va[j]), __fmul_rn(__fmul_rn(omb2, ga[j]), ga[j]));
         const float denom = __fadd_rn(__fdiv_rn(sqrtf(va[j]), bc2_sqrt), eps);
@@ -192,9 +200,10 @@ __global__ void __launch_bounds__(256) adam_kernel(float* __restrict__ p, const 
       reinterpret_cast<float4*>(v)[i] = vv[u];
     }
   }
-  for (size_t e = 4 * n4 + blockIdx.x * (size_t)blockDim.x + threadIdx.x; e < n; e += stride) {
-    float mm = __fadd_rn(__fmul_rn(b1, m[e]), __fmul_rn(omb1, g[e]));
-    float vv = __fadd_rn(__fmul_rn(b2, v[e]), __fmul_rn(__fmul_rn(omb2, g[e]), g[e]));
+  for (size_t e = 4 * n4 + blockIdx.x * (size_t)blockDim.x + threadIdx.x; e < n && !skip; e += stride) {
+    const float ge = amp ? __fmul_rn(g[e], inv_scale) : g[e];
+    float mm = __fadd_rn(__fmul_rn(b1, m[e]), __fmul_rn(omb1, ge));
+    float vv = __fadd_rn(__fmul_rn(b2, v[e]), __fmul_rn(__fmul_rn(omb2, ge), ge));
     const float denom = __fadd_rn(__fdiv_rn(sqrtf(vv), bc2_sqrt), eps);
     float pp = __fsub_rn(p[e], __fmul_rn(step_size, __fdiv_rn(mm, denom)));
     if (e >= clo && e < chi) pp = fmaxf(pp, cmin);
@@ -207,16 +216,44 @@ __global__ void __launch_bounds__(256) adam_kernel(float* __restrict__ p, const 
     __threadfence();
     const unsigned int done = atomicAdd(ticket, 1u);
     if (done == gridDim.x - 1) {
-      *counter = t;
+      if (!skip) *counter = t;   // a skipped step does not count (PyTorch GradScaler semantics)
+      if (amp) {                 // scale update: back off on overflow, grow after amp_interval finite steps
+        if (skip) {
+          amp[0] = __fmul_rn(amp[0], amp_backoff);
+          amp[1] = 0.0f;
+        } else {
+          amp[1] = __fadd_rn(amp[1], 1.0f);
+          if (amp[1] >= (float)amp_interval) { amp[0] = __fmul_rn(amp[0], amp_growth); amp[1] = 0.0f; }
+        }
+        amp[2] = 0.0f;
+      }
       *ticket = 0u;
       __threadfence();
     }
   }
 }
 
+// found_inf of dynamic loss scaling: any non-finite gradient element sets amp[2]
+__global__ void amp_check_kernel(const float* __restrict__ g, size_t n, float* __restrict__ amp) {
+  pdl_wait();
+  pdl_trigger();
+  bool bad = false;
+  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x)
+    bad |= !isfinite(g[i]);
+  if (__any_sync(0xffffffffu, bad) && (threadIdx.x & 31) == 0) amp[2] = 1.0f;
+}
+
+int launch_amp_check(const float* g, size_t n, float* amp, cudaStream_t st) {
+  ProfScope ps_("amp_check", PB_HBM, 0.0, 4.0 * n, st);
+  pdl(amp_check_kernel, ew_grid(n, 4), 256, 0, st)(g, n, amp);
+  SPK_LAUNCHED();
+  return SPIKERL_OK;
+}
+
 int launch_adam(float* p, const float* g, float* m, float* v, size_t n, long long* counter,
                 float lr, float b1, float b2, float eps, size_t clo, size_t chi, float cmin,
-                unsigned int* ticket, const Bf16Views* views, cudaStream_t st) {
+                unsigned int* ticket, const Bf16Views* views, cudaStream_t st, float* amp, float amp_growth,
+                float amp_backoff, int amp_interval) {
   ProfScope ps_("adam", PB_HBM, 0.0, 28.0 * n, st);
   const Bf16Views none{};
   if (((uintptr_t)p | (uintptr_t)g | (uintptr_t)m | (uintptr_t)v) & 15) {
@@ -224,7 +261,8 @@ int launch_adam(float* p, const float* g, float* m, float* v, size_t n, long lon
     return SPIKERL_E_ARG;
   }
   pdl(adam_kernel, stream_grid(adam_kernel, n, 8), 256, 0, st)(p, g, m, v, n, counter, lr, b1, b2, eps, clo, chi,
-                                             cmin, ticket, views ? *views : none);
+                                             cmin, ticket, views ? *views : none, amp, amp_growth, amp_backoff,
+                                             amp_interval);
   SPK_LAUNCHED();
   return SPIKERL_OK;
 }

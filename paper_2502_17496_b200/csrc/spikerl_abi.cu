@@ -609,11 +609,14 @@ int spikerl_td3_update(const spikerl_actor_cfg* acfg, const spikerl_critic_cfg* 
   const Bf16Views ctv = critic_bf16_views(cd, ad.bf16 ? (__nv_bfloat16*)b->critic_t_bf16 : nullptr);
   const Bf16Views av = actor_bf16_views(ad, ad.bf16 ? (__nv_bfloat16*)b->actor_bf16 : nullptr);
   const Bf16Views atv = actor_bf16_views(ad, ad.bf16 ? (__nv_bfloat16*)b->actor_t_bf16 : nullptr);
+  float* const amp_c = b->amp, * const amp_a = b->amp ? b->amp + 4 : nullptr;   // loss scaling (or none)
   SPK_TRY(critic_fwd_bwd(cd, B, b->critic, cbf, s, ad.S, a, ad.A, y, q, losses, b->grad_critic, nullptr, 0.f, 2,
-                         cws, st, aux->ev[1]));
+                         cws, st, aux->ev[1], amp_c));
   SPK_TRY(spikerl_allreduce_grads(comm, b->grad_critic, 2 * Pc, stream));
+  if (amp_c) SPK_TRY(launch_amp_check(b->grad_critic, 2 * Pc, amp_c, st));
   SPK_TRY(launch_adam(b->critic, b->grad_critic, b->m_critic, b->v_critic, 2 * Pc, b->adam_steps, hp->lr_critic,
-                      hp->beta1, hp->beta2, hp->eps, 0, 0, 0.f, (unsigned int*)(b->adam_steps + 1), &cv, st));
+                      hp->beta1, hp->beta2, hp->eps, 0, 0, 0.f, (unsigned int*)(b->adam_steps + 1), &cv, st, amp_c,
+                      hp->amp_growth, hp->amp_backoff, hp->amp_interval));
   // 4. delayed actor update + targets
   if (actor_step) {
     // branch C: the critic targets only need the updated critic
@@ -624,16 +627,18 @@ int spikerl_td3_update(const spikerl_actor_cfg* acfg, const spikerl_critic_cfg* 
     // actor loss -mean Q1(s, pi(s)): formed by the mma critic's data-backward launch itself
     const bool mma = critic_mma_ok(cd);
     SPK_TRY(critic_fwd_bwd(cd, B, b->critic, cbf, s, ad.S, api, ad.A, nullptr, q, mma ? losses + 1 : nullptr, nullptr,
-                           ga, -1.0f / (float)B, 1, cws, st));
+                           ga, -1.0f / (float)B, 1, cws, st, nullptr, amp_a));
     if (!mma) {
       pdl(neg_mean_kernel, 1, 256, 0, st)(B, q, losses + 1);
       SPK_LAUNCHED();
     }
     SPK_TRY(actor_backward_impl(ad, B, b->actor, abf, s, tape, ga, b->grad_actor, 0, aws, st));
     SPK_TRY(spikerl_allreduce_grads(comm, b->grad_actor, Pa, stream));
+    if (amp_a) SPK_TRY(launch_amp_check(b->grad_actor, Pa, amp_a, st));
     SPK_TRY(launch_adam(b->actor, b->grad_actor, b->m_actor, b->v_actor, Pa, b->adam_steps + 2, hp->lr_actor,
                         hp->beta1, hp->beta2, hp->eps, ad.off[SPIKERL_ACTOR_SIGMA], ad.off[SPIKERL_ACTOR_W1],
-                        ad.sigma_floor, (unsigned int*)(b->adam_steps + 3), &av, st));
+                        ad.sigma_floor, (unsigned int*)(b->adam_steps + 3), &av, st, amp_a, hp->amp_growth,
+                        hp->amp_backoff, hp->amp_interval));
     SPK_TRY(launch_polyak(b->actor_t, b->actor, Pa, hp->tau, &atv, st));
     SPK_CHECK_CUDA(cudaStreamWaitEvent(st, aux->ev[5], 0));   // join branch C
   }
@@ -739,14 +744,17 @@ int spikerl_td3_update_pair(const spikerl_actor_cfg* acfg, const spikerl_critic_
   const Bf16Views ctv = critic_bf16_views(cd, ad.bf16 ? (__nv_bfloat16*)b->critic_t_bf16 : nullptr);
   const Bf16Views av = actor_bf16_views(ad, ad.bf16 ? (__nv_bfloat16*)b->actor_bf16 : nullptr);
   const Bf16Views atv = actor_bf16_views(ad, ad.bf16 ? (__nv_bfloat16*)b->actor_t_bf16 : nullptr);
+  float* const amp_c = b->amp, * const amp_a = b->amp ? b->amp + 4 : nullptr;   // loss scaling (or none)
   // the two critic updates, in order
   for (int i = 0; i < 2; ++i) {
     const Slot& x = sl[i];
     SPK_TRY(critic_fwd_bwd(cd, B, b->critic, cbf, x.s, ad.S, x.a, ad.A, x.y, x.q, losses, b->grad_critic, nullptr,
-                           0.f, 2, x.cws, st, evA[i]));
+                           0.f, 2, x.cws, st, evA[i], amp_c));
     SPK_TRY(spikerl_allreduce_grads(comm, b->grad_critic, 2 * Pc, stream));
+    if (amp_c) SPK_TRY(launch_amp_check(b->grad_critic, 2 * Pc, amp_c, st));
     SPK_TRY(launch_adam(b->critic, b->grad_critic, b->m_critic, b->v_critic, 2 * Pc, b->adam_steps, hp->lr_critic,
-                        hp->beta1, hp->beta2, hp->eps, 0, 0, 0.f, (unsigned int*)(b->adam_steps + 1), &cv, st));
+                        hp->beta1, hp->beta2, hp->eps, 0, 0, 0.f, (unsigned int*)(b->adam_steps + 1), &cv, st, amp_c,
+                        hp->amp_growth, hp->amp_backoff, hp->amp_interval));
   }
   // delayed actor update + targets (update k + 1), exactly as spikerl_td3_update's actor step
   const Slot& x = sl[1];
@@ -756,16 +764,18 @@ int spikerl_td3_update_pair(const spikerl_actor_cfg* acfg, const spikerl_critic_
   SPK_CHECK_CUDA(cudaStreamWaitEvent(st, aux->ev[3], 0));
   const bool mma = critic_mma_ok(cd);
   SPK_TRY(critic_fwd_bwd(cd, B, b->critic, cbf, x.s, ad.S, x.api, ad.A, nullptr, x.q, mma ? losses + 1 : nullptr,
-                         nullptr, x.ga, -1.0f / (float)B, 1, x.cws, st));
+                         nullptr, x.ga, -1.0f / (float)B, 1, x.cws, st, nullptr, amp_a));
   if (!mma) {
     pdl(neg_mean_kernel, 1, 256, 0, st)(B, x.q, losses + 1);
     SPK_LAUNCHED();
   }
   SPK_TRY(actor_backward_impl(ad, B, b->actor, abf, x.s, x.tape, x.ga, b->grad_actor, 0, x.aws, st));
   SPK_TRY(spikerl_allreduce_grads(comm, b->grad_actor, Pa, stream));
+  if (amp_a) SPK_TRY(launch_amp_check(b->grad_actor, Pa, amp_a, st));
   SPK_TRY(launch_adam(b->actor, b->grad_actor, b->m_actor, b->v_actor, Pa, b->adam_steps + 2, hp->lr_actor, hp->beta1,
                       hp->beta2, hp->eps, ad.off[SPIKERL_ACTOR_SIGMA], ad.off[SPIKERL_ACTOR_W1], ad.sigma_floor,
-                      (unsigned int*)(b->adam_steps + 3), &av, st));
+                      (unsigned int*)(b->adam_steps + 3), &av, st, amp_a, hp->amp_growth, hp->amp_backoff,
+                      hp->amp_interval));
   SPK_TRY(launch_polyak(b->actor_t, b->actor, Pa, hp->tau, &atv, st));
   SPK_CHECK_CUDA(cudaStreamWaitEvent(st, aux->ev[5], 0));
   return SPIKERL_OK;

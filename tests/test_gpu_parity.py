@@ -614,3 +614,79 @@ def test_td3_pair_matches_sequential(preset):
     for other in ("pair_rng", "pair_graph"):
         for a, b in zip(outs["seq_rng"], outs[other]):
             assert torch.equal(a, b), other
+
+
+def _amp_td3(pk, shape, B, replay, loss_scale, interval=2000):
+    rng = np.random.default_rng(8)
+    actor = sg.actor_params(shape, rng)
+    cs = sg.CriticShape(shape.obs_dim + shape.act_dim, precision="bf16")
+    c1, c2 = sg.critic_params(cs, rng), sg.critic_params(cs, rng)
+    td3 = pk.TD3(pk.actor_cfg_from(shape), pk.critic_cfg(cs.in_dim), pk.td3_cfg(B, amp_interval=interval), replay,
+                 seed=11, loss_scale=loss_scale)
+    td3.load(actor, c1, c2)
+    return td3
+
+
+def test_td3_loss_scaling_matches_unscaled():
+    """Dynamic loss scaling with a power-of-two scale and no overflow changes
+    nothing: dQ * 2^16 flows through bf16 roundings and fp32 sums exactly scaled, the Adam kernel
+    unscales exactly; four updates (single and pair form) leave the same parameters as without it,
+    and the scaler counts its finite steps (oracle state machine)."""
+    import torch
+    import paper_2502_17496_b200 as pk
+    shape, _, B = sg.preset("cfg1")
+    replay = pk.replay_fill(20000, 17, 6, seed=3)
+    g = torch.Generator(device="cuda").manual_seed(5)
+    idx = torch.randint(0, 20000, (4, B), device="cuda", generator=g, dtype=torch.int64)
+    nz = torch.randn(4, B, 6, device="cuda", generator=g)
+    outs = []
+    for scale, pair in ((None, False), (65536.0, False), (65536.0, True)):
+        td3 = _amp_td3(pk, shape, B, replay, scale)
+        if pair:
+            td3.update_pair(1, idx[:2], nz[:2]); td3.update_pair(3, idx[2:], nz[2:])
+        else:
+            for k in range(1, 5):
+                td3.update(k, idx[k - 1], nz[k - 1])
+        torch.cuda.synchronize()
+        outs.append([t.cpu().clone() for t in (td3.actor, td3.critic, td3.actor_t, td3.critic_t, td3.losses)])
+        if scale is not None:
+            st_c, st_a = (scale, 0), (scale, 0)
+            for k in range(1, 5):
+                st_c, _ = oracle.amp_step(st_c, True)
+                if k % 2 == 0:
+                    st_a, _ = oracle.amp_step(st_a, True)
+            amp = td3.amp.cpu().numpy()
+            assert (amp[0], amp[1], amp[2]) == (st_c[0], st_c[1], 0.0)
+            assert (amp[4], amp[5], amp[6]) == (st_a[0], st_a[1], 0.0)
+    for other in outs[1:]:
+        for a, b in zip(outs[0], other):
+            assert torch.equal(a, b)
+
+
+def test_td3_loss_scaling_overflow_skips_and_backs_off():
+    """A non-finite critic gradient (an infinite reward in the minibatch) skips the critic's Adam
+    step (parameters, moments and its step count unchanged) and halves the critic's scale; the
+    following finite updates proceed and the scale grows back after amp_interval finite steps."""
+    import torch
+    import paper_2502_17496_b200 as pk
+    shape, _, B = sg.preset("cfg1")
+    replay = pk.replay_fill(20000, 17, 6, seed=3)
+    replay.r[:B] = float("inf")
+    td3 = _amp_td3(pk, shape, B, replay, 1024.0, interval=2)
+    bad = torch.arange(B, device="cuda", dtype=torch.int64)
+    good = torch.arange(B, 2 * B, device="cuda", dtype=torch.int64)
+    c0, m0 = td3.critic.clone(), td3.m_critic.clone()
+    td3.update(1, bad)
+    torch.cuda.synchronize()
+    assert torch.equal(td3.critic, c0) and torch.equal(td3.m_critic, m0)
+    assert int(td3.adam_steps[0]) == 0
+    assert td3.amp[0].item() == 512.0 and td3.amp[1].item() == 0.0 and td3.amp[2].item() == 0.0
+    td3.update(2, good)     # critic + actor: finite
+    torch.cuda.synchronize()
+    assert not torch.equal(td3.critic, c0) and int(td3.adam_steps[0]) == 1 and int(td3.adam_steps[2]) == 1
+    assert td3.amp[0].item() == 512.0 and td3.amp[1].item() == 1.0
+    assert td3.amp[4].item() == 1024.0 and td3.amp[5].item() == 1.0
+    td3.update(3, good)     # second finite critic step in a row: grow
+    torch.cuda.synchronize()
+    assert td3.amp[0].item() == 1024.0 and td3.amp[1].item() == 0.0
+    assert all(torch.isfinite(t).all() for t in (td3.critic, td3.actor, td3.m_critic, td3.v_critic))

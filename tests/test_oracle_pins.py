@@ -479,3 +479,22 @@ def test_actor_invariants_cfg0_shape():
     # workload structure: He-uniform gives non-degenerate densities
     dens = [float(O.mean()) for O in tape["O"]]
     assert 0.05 < dens[0] < 0.5 and 0.05 < dens[2] < 0.6, dens
+
+
+def test_grad_scaler_state_machine():
+    """GradScaler rule (PyTorch GradScaler): hand-worked sequences."""
+    st = (65536.0, 0)
+    st, took = oracle.amp_step(st, True, interval=3)
+    assert took and st == (65536.0, 1)
+    st, took = oracle.amp_step(st, False, interval=3)        # overflow: skip, back off, reset
+    assert not took and st == (32768.0, 0)
+    for _ in range(2):
+        st, took = oracle.amp_step(st, True, interval=3)
+    assert st == (32768.0, 2)
+    st, took = oracle.amp_step(st, True, interval=3)         # third finite step in a row: grow
+    assert took and st == (65536.0, 0)
+    # unscaling by a power-of-two scale is exact; non-finite detection
+    g = np.array([1.5, -3.0e-20, 7.0], np.float32)
+    assert np.array_equal(oracle.unscale(g * np.float32(65536.0), 65536.0), g)
+    assert oracle.all_finite(g) and not oracle.all_finite(np.array([1.0, np.inf], np.float32))
+    assert not oracle.all_finite(np.array([np.nan], np.float32))
