@@ -57,7 +57,11 @@ enum spikerl_status {
 
 enum spikerl_precision {
   SPIKERL_FP32 = 0,          /* true fp32 (no TF32) SIMT path; configs[0]                      */
-  SPIKERL_BF16 = 1           /* bf16 operands, fp32 accumulate, fp32 master */
+  SPIKERL_BF16 = 1,          /* bf16 operands, fp32 accumulate, fp32 master */
+  SPIKERL_FP16 = 2           /* actor only, tcgen05 engine: fp16 operands ("FP16 (half
+                                precision)" AMP), fp32 accumulate, fp32 master; pair it with dynamic
+                                loss scaling (spikerl_td3_bufs.amp). The 16-bit working copy has the
+                                bf16 copy's layout and size. */
 };
 
 enum spikerl_engine {

@@ -25,6 +25,13 @@ def bf16(x):
     return r.view(np.float32).astype(np.float64)
 
 
+def fp16(x):
+    """RNE to IEEE binary16 of fp32(x) (subnormals kept, +-inf on overflow); returned as float64.
+    PAPER.md:164 ("FP16 (half precision)" AMP); numpy's float32 -> float16 cast rounds to nearest even."""
+    x32 = np.asarray(x, dtype=np.float64).astype(np.float32)
+    return x32.astype(np.float16).astype(np.float64)
+
+
 def identity(x):
     return np.asarray(x, dtype=np.float64)
 
@@ -33,6 +40,8 @@ def rounder(precision: str):
     """Operand rounding for a GEMM operand at a DESIGN.md R20 rounding point."""
     if precision == "bf16":
         return bf16
+    if precision == "fp16":
+        return fp16
     if precision == "fp32":
         return identity
     raise ValueError(f"unknown precision {precision!r}")

@@ -13,7 +13,7 @@ LIB_PATH = os.path.join(_HERE, "libspikerl.so")
 
 OK, E_ARG, E_DOMAIN, E_STATE, E_NOTREADY, E_CUDA, E_NCCL, E_UNSUPPORTED = range(8)
 STATUS_NAMES = ["OK", "E_ARG", "E_DOMAIN", "E_STATE", "E_NOTREADY", "E_CUDA", "E_NCCL", "E_UNSUPPORTED"]
-FP32, BF16 = 0, 1
+FP32, BF16, FP16 = 0, 1, 2
 ENGINE_AUTO, ENGINE_SIMT, ENGINE_TCGEN05 = 0, 1, 2
 ACTOR_PARAMS = ("mu", "sigma", "W1", "W2", "W3", "Wd", "bd")
 CRITIC_PARAMS = ("W1", "b1", "W2", "b2", "W3", "b3")

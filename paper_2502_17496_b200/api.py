@@ -15,7 +15,7 @@ import torch
 from . import _lib as L
 from ._lib import check, lib
 
-_PREC = {"fp32": L.FP32, "bf16": L.BF16}
+_PREC = {"fp32": L.FP32, "bf16": L.BF16, "fp16": L.FP16}
 _ENG = {"auto": L.ENGINE_AUTO, "simt": L.ENGINE_SIMT, "tcgen05": L.ENGINE_TCGEN05}
 
 
@@ -129,7 +129,7 @@ class SpikingActor:
         self.offsets = actor_offsets(cfg)
         self.n_params = self.offsets[-1]
         self.params = torch.zeros(self.n_params, dtype=torch.float32, device=device)
-        self.bf16 = cfg.precision == L.BF16
+        self.bf16 = cfg.precision in (L.BF16, L.FP16)
         self.params_bf16 = _alloc(lib().spikerl_actor_bf16_bytes(C.byref(cfg)), device) if self.bf16 else None
         self.tape_buf = _alloc(lib().spikerl_actor_tape_bytes(C.byref(cfg), batch), device)
         self.ws = _alloc(lib().spikerl_actor_workspace_bytes(C.byref(cfg), batch), device)
@@ -219,7 +219,7 @@ class TwinCritic:
         self.offsets = critic_offsets(cfg)
         self.P = self.offsets[-1]
         self.params = torch.zeros(2 * self.P, dtype=torch.float32, device=device)
-        self.bf16 = cfg.precision == L.BF16
+        self.bf16 = cfg.precision in (L.BF16, L.FP16)
         self.params_bf16 = _alloc(lib().spikerl_critic_bf16_bytes(C.byref(cfg)), device) if self.bf16 else None
         self.ws = _alloc(lib().spikerl_critic_workspace_bytes(C.byref(cfg), batch), device)
         self.q = torch.zeros(2, batch, dtype=torch.float32, device=device)
@@ -313,7 +313,7 @@ class TD3:
         self.m_actor, self.v_actor = torch.zeros(self.Pa, **f32), torch.zeros(self.Pa, **f32)
         self.m_critic, self.v_critic = torch.zeros(2 * self.Pc, **f32), torch.zeros(2 * self.Pc, **f32)
         self.grad_actor, self.grad_critic = torch.zeros(self.Pa, **f32), torch.zeros(2 * self.Pc, **f32)
-        self.bf16 = acfg.precision == L.BF16
+        self.bf16 = acfg.precision in (L.BF16, L.FP16)
         ab = lb.spikerl_actor_bf16_bytes(C.byref(acfg))
         cb = lb.spikerl_critic_bf16_bytes(C.byref(ccfg))
         self.actor_bf16 = _alloc(ab, device) if self.bf16 else None

@@ -2,6 +2,7 @@
 #pragma once
 #include <cuda_runtime.h>
 #include <cuda_bf16.h>
+#include <cuda_fp16.h>
 #include <cstdint>
 #include <cstddef>
 #include "spikerl.h"
@@ -107,7 +108,8 @@ struct ActorDims {
   size_t off[SPIKERL_ACTOR_NPARAM + 1];
   size_t boff[4]; // bf16 copy element offsets of W1, W2, W3 ([P_l][P_{l-1}] each); boff[3] = total
   float dc, dv, vth, win, zh, sigma_floor;
-  int bf16;       // precision == BF16
+  int bf16;       // 16-bit GEMM operands (precision BF16 or FP16)
+  int f16;        // ... and they are fp16 (precision FP16: tcgen05 engine only)
   int engine;     // resolved: SPIKERL_ENGINE_SIMT or SPIKERL_ENGINE_TCGEN05
 };
 int actor_dims(const spikerl_actor_cfg* cfg, ActorDims* d);
@@ -130,6 +132,10 @@ struct CriticDims {
 int critic_dims(const spikerl_critic_cfg* cfg, CriticDims* d);
 
 // ----------------------------------------------------------------------------- device helpers
+// the 16-bit operand bits of x: RNE to fp16 (f16) or to bf16
+__device__ __forceinline__ unsigned short op16_bits(float x, bool f16) {
+  return f16 ? __half_as_ushort(__float2half_rn(x)) : __bfloat16_as_ushort(__float2bfloat16_rn(x));
+}
 __device__ __forceinline__ float bf16_round(float x) {
   return __bfloat162float(__float2bfloat16_rn(x));
 }

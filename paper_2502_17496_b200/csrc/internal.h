@@ -106,6 +106,7 @@ __device__ __forceinline__ uint32_t fdiv(uint32_t x, const FastDiv& f) {
 
 struct Bf16Views {
   int kind;                  // 0 none, 1 actor W1..W3, 2 critic twin (mma layout), 3 plain copy
+  int f16;                   // the 16-bit copy holds fp16 (actor FP16 precision), else bf16
   __nv_bfloat16* out;
   long long src[3], dst[3];  // actor: fp32 offset of W_l, bf16 offset of its padded copy
   int rows[3], cols[3], ldd[3];

@@ -424,6 +424,7 @@ static Params fused_params(const ActorDims& d, int B) {
 }
 
 bool fused_fwd_ok(const ActorDims& d, int B) {
+  if (d.f16) return false;   // bf16 operands only
   // opt-in (SPIKERL_FUSED_FWD=1): measured on B200 at configs[1] (B = 256) one launch takes
   // 34.6 us against 28.8 us for the five-kernel chain it replaces (one CTA of 8 warps per SM
   // leaves every phase latency-bound), so the chain stays the default

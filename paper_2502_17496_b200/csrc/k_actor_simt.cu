@@ -136,6 +136,17 @@ template <> struct Pack8<__nv_bfloat16> {
     return *reinterpret_cast<const uint32_t*>(&h);
   }
 };
+template <> struct Pack8<__half> {
+  __device__ __forceinline__ static void store(__half* p, const float (&v)[8]) {
+    uint4 u;
+    u.x = h2_bits(v[0], v[1]); u.y = h2_bits(v[2], v[3]); u.z = h2_bits(v[4], v[5]); u.w = h2_bits(v[6], v[7]);
+    *reinterpret_cast<uint4*>(p) = u;
+  }
+  __device__ __forceinline__ static uint32_t h2_bits(float a, float b) {
+    const __half2 h = __floats2half2_rn(a, b);
+    return *reinterpret_cast<const uint32_t*>(&h);
+  }
+};
 template <> struct Pack8<float> {
   __device__ __forceinline__ static void store(float* p, const float (&v)[8]) {
     reinterpret_cast<float4*>(p)[0] = make_float4(v[0], v[1], v[2], v[3]);
@@ -448,6 +459,11 @@ int launch_dec_bwd_outscan(const ActorDims& d, int B, const float* grad_a, const
       SPK_LAUNCHED();
       return SPIKERL_OK;
     };
+    if (d.f16) {
+      if (d.T == 16) return launch(dec_bwd_outscan_tma_kernel<__half, 16>, (__half*)G3);
+      if (d.T == 5) return launch(dec_bwd_outscan_tma_kernel<__half, 5>, (__half*)G3);
+      return launch(dec_bwd_outscan_tma_kernel<__half, 0>, (__half*)G3);
+    }
     if (d.bf16) {
       if (d.T == 16) return launch(dec_bwd_outscan_tma_kernel<__nv_bfloat16, 16>, (__nv_bfloat16*)G3);
       if (d.T == 5) return launch(dec_bwd_outscan_tma_kernel<__nv_bfloat16, 5>, (__nv_bfloat16*)G3);
@@ -458,7 +474,10 @@ int launch_dec_bwd_outscan(const ActorDims& d, int B, const float* grad_a, const
   const long long units = (long long)cdiv(B, 2) * (d.Wd[3] / 4);   // warps of work
   long long blocks = cdiv(units, 8);
   if (blocks > (long long)num_sms() * 8) blocks = (long long)num_sms() * 8;
-  if (d.bf16) {
+  if (d.f16) {
+    pdl((dec_bwd_outscan_kernel<__half, 0>), (int)blocks, 256, 0, st)(
+        B, d.T, d.A, d.D, d.N3, d.Wd[3], d.dc, d.dv, d.zh, grad_a, act, Wd, bits3, mask3, (__half*)G3, g_pre, wpad);
+  } else if (d.bf16) {
     if (d.T == 16) pdl((dec_bwd_outscan_kernel<__nv_bfloat16, 16>), (int)blocks, 256, 0, st)(
         B, d.T, d.A, d.D, d.N3, d.Wd[3], d.dc, d.dv, d.zh, grad_a, act, Wd, bits3, mask3, (__nv_bfloat16*)G3, g_pre, wpad);
     else if (d.T == 5) pdl((dec_bwd_outscan_kernel<__nv_bfloat16, 5>), (int)blocks, 256, 0, st)(

@@ -37,7 +37,7 @@ static int stream_grid(K kernel, size_t n, int per_thread) {
 // Actor: W_l (fp32 [N_l][N_{l-1}]) -> bf16 [P_l][P_{l-1}], zero padded. One thread per padded
 // element so the padding is (re)written with zeros every refresh.
 __global__ void actor_refresh_kernel(const float* __restrict__ W, int N, int K, int P, int Pk,
-                                     __nv_bfloat16* __restrict__ out) {
+                                     __nv_bfloat16* __restrict__ out, int f16) {
   pdl_wait();
   pdl_trigger();
   const size_t total = (size_t)P * Pk;
@@ -45,7 +45,7 @@ __global__ void actor_refresh_kernel(const float* __restrict__ W, int N, int K, 
        i += (size_t)gridDim.x * blockDim.x) {
     const int n = (int)(i / Pk), k = (int)(i % Pk);
     const float v = (n < N && k < K) ? W[(size_t)n * K + k] : 0.0f;
-    out[i] = __float2bfloat16_rn(v);
+    reinterpret_cast<unsigned short*>(out)[i] = op16_bits(v, f16 != 0);
   }
 }
 
@@ -56,7 +56,7 @@ int launch_actor_refresh_bf16(const ActorDims& d, const float* params, __nv_bflo
     const size_t total = (size_t)d.P[l] * d.P[l - 1];
     pdl(actor_refresh_kernel, ew_grid(total, 4), 256, 0, st)(
         params + d.off[SPIKERL_ACTOR_W1 + l - 1], d.N[l], d.N[l - 1], d.P[l], d.P[l - 1],
-        out + d.boff[l - 1]);
+        out + d.boff[l - 1], d.f16);
     SPK_LAUNCHED();
   }
   return SPIKERL_OK;
@@ -81,6 +81,7 @@ int launch_f32_to_bf16(const float* in, __nv_bfloat16* out, size_t n, cudaStream
 Bf16Views actor_bf16_views(const ActorDims& d, __nv_bfloat16* out) {
   Bf16Views v{};
   v.kind = out ? 1 : 0;
+  v.f16 = d.f16;
   v.out = out;
   for (int l = 1; l <= 3; ++l) {
     v.src[l - 1] = (long long)d.off[SPIKERL_ACTOR_W1 + l - 1];
@@ -98,7 +99,7 @@ Bf16Views actor_bf16_views(const ActorDims& d, __nv_bfloat16* out) {
 // multiply-high divisions (a 64-bit division per element made Adam ~5x slower than its bytes).
 __device__ __forceinline__ void store_views(const Bf16Views& v, size_t e, float x) {
   if (v.kind == 0) return;
-  const __nv_bfloat16 h = __float2bfloat16_rn(x);
+  const __nv_bfloat16 h = __ushort_as_bfloat16(op16_bits(x, v.f16 != 0));   // fp16 bits when v.f16
   if (v.kind == 1) {
 #pragma unroll
     for (int l = 0; l < 3; ++l) {

@@ -80,6 +80,8 @@ struct Params {
   // WG jobs (critic weight gradients): A / B row bases in the stacked operand maps, partial offset
   // (elements, within one split), row stride and valid columns of the output tile
   int wg_njobs; int wg_arow[8], wg_brow[8], wg_ld[8], wg_ncol[8]; long long wg_off[8];
+  int f16;          // 16-bit operands are fp16 (actor FP16 precision), else bf16
+  uint32_t one2;    // two 16-bit 1.0 values: 0x3F803F80 (bf16) / 0x3C003C00 (fp16), the expanded spike
   int trace;   // diagnostics: CTA 0 stamps %globaltimer at phase boundaries into g_trace
   int dbg;     // diagnostics only (SPIKERL_TC_DBG, wrong results): 1 = expanders skip their smem
                // stores, 2 = epilogue skips its work, 4 = MMA issuer skips the MMAs, 8 = DW
@@ -173,8 +175,9 @@ __device__ __forceinline__ uint64_t make_desc(uint32_t saddr, uint32_t lbo_bytes
   return d;
 }
 // instruction descriptor: bf16 x bf16 -> f32, M = 128 (one CTA) or 256 (CTA pair)
-__host__ __device__ constexpr uint32_t make_idesc(int N, int a_mn, int b_mn, int M = BM) {
-  return (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)a_mn << 15) | ((uint32_t)b_mn << 16) |
+__host__ __device__ constexpr uint32_t make_idesc(int N, int a_mn, int b_mn, int M = BM, int f16 = 0) {
+  // A / B formats (bits 7-9, 10-12): 1 = bf16, 0 = fp16; accumulator fp32 (bit 4)
+  return (1u << 4) | ((f16 ? 0u : 1u) << 7) | ((f16 ? 0u : 1u) << 10) | ((uint32_t)a_mn << 15) | ((uint32_t)b_mn << 16) |
          ((uint32_t)(N >> 3) << 17) | ((uint32_t)(M >> 4) << 24);
 }
 __device__ __forceinline__ void mma_bf16(uint32_t d_tmem, uint64_t adesc, uint64_t bdesc, uint32_t idesc, uint32_t acc) {
@@ -218,14 +221,14 @@ __device__ __forceinline__ uint32_t prmt_sx(uint32_t x, uint32_t sel) {
   asm("prmt.b32 %0, %1, 0, %2;" : "=r"(r) : "r"(x), "r"(sel));
   return r;
 }
-__device__ __forceinline__ uint4 expand_byte(uint32_t byte) {
+__device__ __forceinline__ uint4 expand_byte(uint32_t byte, uint32_t one2) {
   const uint32_t zlo = (byte & 0x0Fu) * 0x10204080u;   // bit i     -> bit 8 i + 7
   const uint32_t zhi = (byte & 0xF0u) * 0x01020408u;   // bit 4 + i -> bit 8 i + 7
   uint4 r;
-  r.x = prmt_sx(zlo, 0x9988u) & 0x3F803F80u;
-  r.y = prmt_sx(zlo, 0xBBAAu) & 0x3F803F80u;
-  r.z = prmt_sx(zhi, 0x9988u) & 0x3F803F80u;
-  r.w = prmt_sx(zhi, 0xBBAAu) & 0x3F803F80u;
+  r.x = prmt_sx(zlo, 0x9988u) & one2;
+  r.y = prmt_sx(zlo, 0xBBAAu) & one2;
+  r.z = prmt_sx(zhi, 0x9988u) & one2;
+  r.w = prmt_sx(zhi, 0xBBAAu) & one2;
   return r;
 }
 __device__ __forceinline__ void st_shared_v4(uint32_t addr, uint4 v) {
@@ -424,7 +427,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     // ===================== MMA issuer (rank 0 of a pair) =====================
     if (lane == 0 && rank == 0) {
       uint32_t it = 0, titer = 0;
-      const uint32_t idesc = make_idesc(p.BN, A_MN ? 1 : 0, B_MN ? 1 : 0, BM * CG);
+      const uint32_t idesc = make_idesc(p.BN, A_MN ? 1 : 0, B_MN ? 1 : 0, BM * CG, p.f16);
       for (int u = cid; u < p.n_units; u += ncl, ++titer) {
         const Tile t = decode<MODE>(p, u, rank, CG);
         const uint32_t a = titer % NBUF, aph = (titer / NBUF) & 1;
@@ -509,7 +512,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
 #pragma unroll
                 for (int c = 0; c < 8; ++c) {
                   const uint32_t w = c < 4 ? cur[i].x : cur[i].y;
-                  if (!(p.dbg & 1)) st_shared_v4(base + ((c ^ sw) << 4), expand_byte((w >> (8 * (c & 3))) & 0xFFu));
+                  if (!(p.dbg & 1)) st_shared_v4(base + ((c ^ sw) << 4), expand_byte((w >> (8 * (c & 3))) & 0xFFu, p.one2));
                 }
               }
             }
@@ -573,7 +576,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
 #pragma unroll
                   for (int c = 0; c < 4; ++c) {
                     const int chunk = hw * 4 + c;
-                    if (!(p.dbg & 1)) st_shared_v4(base + ((chunk ^ sw) << 4), expand_byte((wv[wi] >> (8 * c)) & 0xFFu));
+                    if (!(p.dbg & 1)) st_shared_v4(base + ((chunk ^ sw) << 4), expand_byte((wv[wi] >> (8 * c)) & 0xFFu, p.one2));
                   }
                 }
               }
@@ -789,7 +792,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
             for (int j = 0; j < HB; ++j) {
               const float G = lif_back_step(zh, dvc, dcc, __uint_as_float(rr[ci][j]), (ow >> j) & 1u, (hw >> j) & 1u, dvn[j], dcn[j]);
               gs[j] = __fadd_rn(gs[j], G);
-              st_shared_u16(sb + (uint32_t)((ci * BT + j) * 256), __bfloat16_as_ushort(__float2bfloat16_rn(G)));
+              st_shared_u16(sb + (uint32_t)((ci * BT + j) * 256), op16_bits(G, p.f16 != 0));
             }
           }
           fence_proxy_async();   // generic-proxy smem writes -> the TMA store
@@ -803,7 +806,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
 #pragma unroll
           for (int j = 0; j < HB; ++j) {
             const int b = b0 + j;
-            if (b < p.B) p.g_sum[(size_t)b * p.p_prev + row] = __float2bfloat16_rn(gs[j]);
+            if (b < p.B) p.g_sum[(size_t)b * p.p_prev + row] = __ushort_as_bfloat16(op16_bits(gs[j], p.f16 != 0));
           }
         }
       } else if (MODE == ENC) {
@@ -961,14 +964,15 @@ static EncodeTiledFn encode_fn() {
 
 // bf16 tensor map, 128B swizzle, dims/strides listed innermost first (strides in bytes, rank-1 of them)
 static int make_map(CUtensorMap* m, const void* base, int rank, const uint64_t* dims, const uint64_t* strides,
-                    const uint32_t* box, CUtensorMapSwizzle swz = CU_TENSOR_MAP_SWIZZLE_128B) {
+                    const uint32_t* box, CUtensorMapSwizzle swz = CU_TENSOR_MAP_SWIZZLE_128B, bool f16 = false) {
   EncodeTiledFn fn = encode_fn();
   if (!fn) { set_error("cuTensorMapEncodeTiled unavailable"); return SPIKERL_E_CUDA; }
   cuuint64_t gd[3], gs[2];
   cuuint32_t bx[3], es[3] = {1, 1, 1};
   for (int i = 0; i < rank; ++i) { gd[i] = dims[i]; bx[i] = box[i]; }
   for (int i = 0; i < rank - 1; ++i) gs[i] = strides[i];
-  CUresult r = fn(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, rank, const_cast<void*>(base), gd, gs, bx, es,
+  CUresult r = fn(m, f16 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT16 : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, rank,
+                  const_cast<void*>(base), gd, gs, bx, es,
                   CU_TENSOR_MAP_INTERLEAVE_NONE, swz, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) { set_error("cuTensorMapEncodeTiled failed (%d)", (int)r); return SPIKERL_E_CUDA; }
@@ -1133,6 +1137,7 @@ int launch_lif_fwd_tc(const ActorDims& d, int l, int B, const uint32_t* bits_in,
   ProfScope ps_(l == 1 ? "lif_fwd_tc_L1" : (l == 2 ? "lif_fwd_tc_L2" : "lif_fwd_tc_L3"), PB_TENSOR,
                 2.0 * d.T * B * (double)d.N[l] * d.N[l - 1], 0.0, st);
   Params p{};
+  p.f16 = d.f16; p.one2 = d.f16 ? 0x3C003C00u : 0x3F803F80u;
   p.T = d.T; p.B = B;
   const int mt = d.P[l] / BM;
   p.Bt = choose_bt(d.T, B, mt, FWD_MAX_BT);
@@ -1151,7 +1156,7 @@ int launch_lif_fwd_tc(const ActorDims& d, int l, int B, const uint32_t* bits_in,
   const uint64_t dims[2] = {(uint64_t)d.P[l - 1], (uint64_t)d.P[l]};
   const uint64_t strides[1] = {(uint64_t)d.P[l - 1] * 2};
   const uint32_t box[2] = {64, 128};
-  SPK_TRY(make_map(&ma, Wb16, 2, dims, strides, box));
+  SPK_TRY(make_map(&ma, Wb16, 2, dims, strides, box, CU_TENSOR_MAP_SWIZZLE_128B, d.f16));
   mb = ma;
   return l == 3 ? launch_bt<FWDO>(p.Bt, ma, mb, p, st) : launch_bt<FWD>(p.Bt, ma, mb, p, st);
 }
@@ -1163,6 +1168,7 @@ int launch_lif_dx_tc(const ActorDims& d, int l, int B, const void* Gl, const __n
   ProfScope ps_(l == 3 ? "lif_dx_tc_L3" : "lif_dx_tc_L2", PB_TENSOR, 2.0 * d.T * B * (double)d.N[l] * d.N[l - 1],
                 0.0, st);
   Params p{};
+  p.f16 = d.f16; p.one2 = d.f16 ? 0x3C003C00u : 0x3F803F80u;
   p.T = d.T; p.B = B;
   const int mt = d.P[l - 1] / BM;
   p.Bt = choose_bt(d.T, B, mt, DX_MAX_BT);
@@ -1181,21 +1187,21 @@ int launch_lif_dx_tc(const ActorDims& d, int l, int B, const void* Gl, const __n
     const uint64_t dims[2] = {(uint64_t)d.P[l - 1], (uint64_t)d.P[l]};
     const uint64_t strides[1] = {(uint64_t)d.P[l - 1] * 2};
     const uint32_t box[2] = {64, 64};
-    SPK_TRY(make_map(&ma, Wb16, 2, dims, strides, box));
+    SPK_TRY(make_map(&ma, Wb16, 2, dims, strides, box, CU_TENSOR_MAP_SWIZZLE_128B, d.f16));
   }
   {  // B = G_l [T][B][P_l]: rows (t, b) t-major per tile, K = P_l. The map ends at N_3 for G_3:
      // TMA zero-fills columns past it (the output-layer scan does not write G_3's padding)
     const uint64_t dims[3] = {(uint64_t)(l == 3 ? d.N[3] : d.P[l]), (uint64_t)B, (uint64_t)d.T};
     const uint64_t strides[2] = {(uint64_t)d.P[l] * 2, (uint64_t)d.P[l] * 2 * B};
     const uint32_t box[3] = {64, (uint32_t)p.Bt, (uint32_t)(d.T / p.cg)};
-    SPK_TRY(make_map(&mb, Gl, 3, dims, strides, box));
+    SPK_TRY(make_map(&mb, Gl, 3, dims, strides, box, CU_TENSOR_MAP_SWIZZLE_128B, d.f16));
   }
   CUtensorMap mc;
   {  // C = G_{l-1} [T][B][P_{l-1}]: the epilogue's staged chunks of DX_CH steps x Bt rows x 128 neurons
     const uint64_t dims[3] = {(uint64_t)d.P[l - 1], (uint64_t)B, (uint64_t)d.T};
     const uint64_t strides[2] = {(uint64_t)d.P[l - 1] * 2, (uint64_t)d.P[l - 1] * 2 * B};
     const uint32_t box[3] = {128, (uint32_t)p.Bt, (uint32_t)DX_CH};
-    SPK_TRY(make_map(&mc, Gprev, 3, dims, strides, box, CU_TENSOR_MAP_SWIZZLE_NONE));
+    SPK_TRY(make_map(&mc, Gprev, 3, dims, strides, box, CU_TENSOR_MAP_SWIZZLE_NONE, d.f16));
   }
   return launch_bt<DX>(p.Bt, ma, mb, p, st, &mc);
 }
@@ -1224,6 +1230,7 @@ int launch_enc_grad_tc(const ActorDims& d, int B, const void* Gsum, const __nv_b
                        float* dsigma, int accumulate, cudaStream_t st) {
   ProfScope ps_("enc_grad_tc", PB_TENSOR, 2.0 * B * (double)d.N1 * d.K0, 0.0, st);
   Params p{};
+  p.f16 = d.f16; p.one2 = d.f16 ? 0x3C003C00u : 0x3F803F80u;
   p.T = 1; p.B = B;
   p.BN = enc_bn(d, B);
   p.cg = enc_cg(d);
@@ -1237,13 +1244,13 @@ int launch_enc_grad_tc(const ActorDims& d, int B, const void* Gsum, const __nv_b
     const uint64_t dims[2] = {(uint64_t)d.P[0], (uint64_t)d.P[1]};
     const uint64_t strides[1] = {(uint64_t)d.P[0] * 2};
     const uint32_t box[2] = {64, 64};
-    SPK_TRY(make_map(&ma, W1b16, 2, dims, strides, box));
+    SPK_TRY(make_map(&ma, W1b16, 2, dims, strides, box, CU_TENSOR_MAP_SWIZZLE_128B, d.f16));
   }
   {
     const uint64_t dims[2] = {(uint64_t)d.P[1], (uint64_t)B};
     const uint64_t strides[1] = {(uint64_t)d.P[1] * 2};
     const uint32_t box[2] = {64, (uint32_t)(p.BN / p.cg)};
-    SPK_TRY(make_map(&mb, Gsum, 2, dims, strides, box));
+    SPK_TRY(make_map(&mb, Gsum, 2, dims, strides, box, CU_TENSOR_MAP_SWIZZLE_128B, d.f16));
   }
   SPK_TRY(launch_bt<ENC>(8, ma, mb, p, st));
   return launch_enc_grad_reduce(d, NUM_EPI_GROUPS * p.n_tiles, partial, dmu, dsigma, accumulate, st);
@@ -1289,6 +1296,7 @@ int launch_lif_dw_tc(const ActorDims& d, int l, int B, const void* Gl, const uin
   ProfScope ps_(l == 1 ? "lif_dw_tc_L1" : (l == 2 ? "lif_dw_tc_L2" : "lif_dw_tc_L3"), PB_TENSOR,
                 2.0 * d.T * B * (double)d.N[l] * d.N[l - 1], 0.0, st);
   Params p{};
+  p.f16 = d.f16; p.one2 = d.f16 ? 0x3C003C00u : 0x3F803F80u;
   p.T = d.T; p.B = B; p.BN = DW_BN;
   p.R = d.T * B;
   p.cg = dw_cg(d, l);
@@ -1306,7 +1314,7 @@ int launch_lif_dw_tc(const ActorDims& d, int l, int B, const void* Gl, const uin
     const uint64_t dims[2] = {(uint64_t)(l == 3 ? d.N[3] : d.P[l]), (uint64_t)p.R};
     const uint64_t strides[1] = {(uint64_t)d.P[l] * 2};
     const uint32_t box[2] = {64, 64};
-    SPK_TRY(make_map(&ma, Gl, 2, dims, strides, box));
+    SPK_TRY(make_map(&ma, Gl, 2, dims, strides, box, CU_TENSOR_MAP_SWIZZLE_128B, d.f16));
   }
   mb = ma;
   SPK_TRY(launch_bt<DW>(8, ma, mb, p, st));
@@ -1337,6 +1345,7 @@ int launch_critic_wgrad_tc(int Bp, int inq, int xtr, const __nv_bfloat16* dZT, c
   if (!pairs_enabled()) { set_error("critic wgrad tc: needs CTA pairs"); return SPIKERL_E_UNSUPPORTED; }
   constexpr int HWc = 256;
   Params p{};
+  p.one2 = 0x3F803F80u;
   p.BN = 256;
   p.cg = 2;
   p.m_tiles = 1;

@@ -38,7 +38,15 @@ bool pdl_enabled() {
 }
 
 static int resolve_engine(const spikerl_actor_cfg* c, ActorDims* d) {
-  const bool bf = c->precision == SPIKERL_BF16;
+  const bool bf = c->precision == SPIKERL_BF16 || c->precision == SPIKERL_FP16;
+  if (c->precision == SPIKERL_FP16) {   // fp16 operands exist on the tcgen05 engine only
+    if (c->engine == SPIKERL_ENGINE_SIMT || !tc_supported(*d)) {
+      set_error("FP16 precision needs the tcgen05 engine and a shape it supports");
+      return SPIKERL_E_UNSUPPORTED;
+    }
+    d->engine = SPIKERL_ENGINE_TCGEN05;
+    return SPIKERL_OK;
+  }
   switch (c->engine) {
     case SPIKERL_ENGINE_SIMT: d->engine = SPIKERL_ENGINE_SIMT; return SPIKERL_OK;
     case SPIKERL_ENGINE_TCGEN05:
@@ -72,7 +80,7 @@ int actor_dims(const spikerl_actor_cfg* c, ActorDims* d) {
               c->surr_window);
     return SPIKERL_E_DOMAIN;
   }
-  if (c->precision != SPIKERL_FP32 && c->precision != SPIKERL_BF16) {
+  if (c->precision != SPIKERL_FP32 && c->precision != SPIKERL_BF16 && c->precision != SPIKERL_FP16) {
     set_error("unknown precision %d", c->precision);
     return SPIKERL_E_ARG;
   }
@@ -96,7 +104,8 @@ int actor_dims(const spikerl_actor_cfg* c, ActorDims* d) {
   d->boff[3] = bo;
   d->dc = c->d_c; d->dv = c->d_v; d->vth = c->v_th; d->win = c->surr_window; d->zh = c->surr_height;
   d->sigma_floor = c->sigma_floor;
-  d->bf16 = c->precision == SPIKERL_BF16;
+  d->bf16 = c->precision == SPIKERL_BF16 || c->precision == SPIKERL_FP16;
+  d->f16 = c->precision == SPIKERL_FP16;
   return resolve_engine(c, d);
 }
 

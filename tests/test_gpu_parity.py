@@ -690,3 +690,48 @@ def test_td3_loss_scaling_overflow_skips_and_backs_off():
     torch.cuda.synchronize()
     assert td3.amp[0].item() == 1024.0 and td3.amp[1].item() == 0.0
     assert all(torch.isfinite(t).all() for t in (td3.critic, td3.actor, td3.m_critic, td3.v_critic))
+
+
+# ------------------------------------------------------------------ fp16 actor (PAPER.md:164 FP16 AMP)
+@pytest.mark.parametrize("name,B", [("cfg1", 256), ("cfg3L", 1024), ("cfg4", 64)])
+def test_actor_fp16(name, B):
+    """FP16 operands on the tcgen05 engine: the oracle rounds the same GEMM operands (R20 points)
+    to binary16 instead of bf16; same tolerances as bf16 (actions 2e-2, gradients 1e-2 rel. L2)."""
+    shape = sg.with_(sg.preset(name)[0], precision="fp16")
+    p, s, g = _inputs(shape, B, seed=4)
+    st = check_actor(run_gpu_actor(shape, B, p, s, g, engine="tcgen05"), shape, p, s, g)
+    print(name, B, st)
+
+
+@pytest.mark.parametrize("T,B", [(5, 33), (16, 19)])
+def test_actor_fp16_edges(T, B):
+    shape = sg.ActorShape(5, 3, pop_enc=7, pop_dec=9, n1=45, n2=161, T=T, precision="fp16")
+    p, s, g = _inputs(shape, B, seed=20 + T)
+    check_actor(run_gpu_actor(shape, B, p, s, g, engine="tcgen05"), shape, p, s, g)
+
+
+def test_td3_fp16_actor_with_loss_scaling():
+    """TD3 with the fp16 actor (bf16 critic) and dynamic loss scaling: updates run in both the
+    single and the pair form with the same result, everything stays finite, the scalers count
+    their finite steps, and the FP16 engine rules are enforced (no SIMT engine)."""
+    import torch
+    import paper_2502_17496_b200 as pk
+    shape = sg.with_(sg.preset("cfg1")[0], precision="fp16")
+    B = 256
+    replay = pk.replay_fill(20000, 17, 6, seed=3)
+    outs = []
+    for pair in (False, True):
+        td3 = _amp_td3(pk, shape, B, replay, 65536.0)
+        if pair:
+            td3.update_pair(1); td3.update_pair(3)
+        else:
+            for k in range(1, 5):
+                td3.update(k)
+        torch.cuda.synchronize()
+        assert all(torch.isfinite(t).all() for t in (td3.actor, td3.critic, td3.actor_t, td3.losses))
+        assert td3.amp[1].item() == 4.0 and td3.amp[5].item() == 2.0
+        outs.append([t.cpu().clone() for t in (td3.actor, td3.critic, td3.actor_t)])
+    for a, b in zip(*outs):
+        assert torch.equal(a, b)
+    with pytest.raises(pk.SpikeRLError):
+        pk.SpikingActor(pk.actor_cfg_from(shape, engine="simt"), 8)

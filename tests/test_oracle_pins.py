@@ -498,3 +498,17 @@ def test_grad_scaler_state_machine():
     assert np.array_equal(oracle.unscale(g * np.float32(65536.0), 65536.0), g)
     assert oracle.all_finite(g) and not oracle.all_finite(np.array([1.0, np.inf], np.float32))
     assert not oracle.all_finite(np.array([np.nan], np.float32))
+
+
+def test_fp16_rne_laws():
+    """fp16 operand rounding (PAPER.md:164 FP16 AMP): IEEE binary16 round-to-nearest-even from fp32."""
+    from oracle.numerics import fp16
+    assert fp16(1.0 + 2.0 ** -11) == 1.0                 # tie -> even
+    assert fp16(1.0 + 3 * 2.0 ** -11) == 1.0 + 2.0 ** -9  # tie -> even (upwards)
+    assert fp16(2.0 ** -25) == 0.0                       # half the smallest subnormal -> 0 (even)
+    assert fp16(3 * 2.0 ** -25) == 2.0 ** -23            # tie between 2^-24 and 2^-23 -> even
+    assert np.isinf(fp16(65520.0)) and fp16(65504.0) == 65504.0
+    x = np.random.default_rng(0).normal(0, 10, 1000)
+    r = fp16(x)
+    assert np.array_equal(fp16(r), r)                    # idempotent
+    assert np.all(np.abs(r - x) <= np.maximum(np.abs(x) * 2.0 ** -11, 2.0 ** -25))
