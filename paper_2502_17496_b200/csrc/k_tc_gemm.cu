@@ -325,7 +325,7 @@ __device__ __forceinline__ Tile decode(const Params& p, int u, int rank, int CG)
 // tile with tcgen05.mma.cta_group::2 issued by rank 0: each CTA holds its 128 rows of A and half
 // of the B columns, every TMA / expander / epilogue completion signals rank 0's barriers, and the
 // MMA commits multicast back to both CTAs.
-template <int MODE, int BT, int CG>
+template <int MODE, int BT, int CG, bool F16 = false>
 __global__ void __launch_bounds__(NUM_THREADS, 1)
     tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
               const __grid_constant__ CUtensorMap tmC, const Params p) {
@@ -427,7 +427,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     // ===================== MMA issuer (rank 0 of a pair) =====================
     if (lane == 0 && rank == 0) {
       uint32_t it = 0, titer = 0;
-      const uint32_t idesc = make_idesc(p.BN, A_MN ? 1 : 0, B_MN ? 1 : 0, BM * CG, p.f16);
+      const uint32_t idesc = make_idesc(p.BN, A_MN ? 1 : 0, B_MN ? 1 : 0, BM * CG, F16 ? 1 : 0);
       for (int u = cid; u < p.n_units; u += ncl, ++titer) {
         const Tile t = decode<MODE>(p, u, rank, CG);
         const uint32_t a = titer % NBUF, aph = (titer / NBUF) & 1;
@@ -792,7 +792,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
             for (int j = 0; j < HB; ++j) {
               const float G = lif_back_step(zh, dvc, dcc, __uint_as_float(rr[ci][j]), (ow >> j) & 1u, (hw >> j) & 1u, dvn[j], dcn[j]);
               gs[j] = __fadd_rn(gs[j], G);
-              st_shared_u16(sb + (uint32_t)((ci * BT + j) * 256), op16_bits(G, p.f16 != 0));
+              st_shared_u16(sb + (uint32_t)((ci * BT + j) * 256), op16_bits(G, F16));
             }
           }
           fence_proxy_async();   // generic-proxy smem writes -> the TMA store
@@ -806,7 +806,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
 #pragma unroll
           for (int j = 0; j < HB; ++j) {
             const int b = b0 + j;
-            if (b < p.B) p.g_sum[(size_t)b * p.p_prev + row] = __ushort_as_bfloat16(op16_bits(gs[j], p.f16 != 0));
+            if (b < p.B) p.g_sum[(size_t)b * p.p_prev + row] = __ushort_as_bfloat16(op16_bits(gs[j], F16));
           }
         }
       } else if (MODE == ENC) {
@@ -1033,19 +1033,19 @@ static bool pairs_enabled() {
   return v == 1;
 }
 
-template <int MODE, int BT, int CG>
+template <int MODE, int BT, int CG, bool F16>
 static int launch_cg(const CUtensorMap& ma, const CUtensorMap& mb, const CUtensorMap& mc, const Params& p, cudaStream_t st) {
   static bool attr = false;
   if (!attr) {
     cudaError_t e =
-        cudaFuncSetAttribute(tc_kernel<MODE, BT, CG>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES);
+        cudaFuncSetAttribute(tc_kernel<MODE, BT, CG, F16>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES);
     if (e != cudaSuccess) { set_error("cudaFuncSetAttribute: %s", cudaGetErrorString(e)); return SPIKERL_E_CUDA; }
     attr = true;
   }
   if (CG == 1) {
     const int ncta = num_sms();
     const int grid = p.n_units < ncta ? (int)p.n_units : ncta;
-    pdl((tc_kernel<MODE, BT, CG>), grid, NUM_THREADS, SMEM_BYTES, st)(ma, mb, mc, p);
+    pdl((tc_kernel<MODE, BT, CG, F16>), grid, NUM_THREADS, SMEM_BYTES, st)(ma, mb, mc, p);
   } else {
     cudaLaunchConfig_t cfg = {};
     cfg.blockDim = dim3(NUM_THREADS, 1, 1);
@@ -1065,7 +1065,7 @@ static int launch_cg(const CUtensorMap& ma, const CUtensorMap& mb, const CUtenso
     const int slots = pair_slots();
     const long long grid = p.n_units < slots ? p.n_units : slots;
     cfg.gridDim = dim3((unsigned)(grid * CG), 1, 1);
-    cudaError_t e = cudaLaunchKernelEx(&cfg, tc_kernel<MODE, BT, CG>, ma, mb, mc, p);
+    cudaError_t e = cudaLaunchKernelEx(&cfg, tc_kernel<MODE, BT, CG, F16>, ma, mb, mc, p);
     if (e != cudaSuccess) { set_error("cudaLaunchKernelEx (pair): %s", cudaGetErrorString(e)); return SPIKERL_E_CUDA; }
   }
   SPK_LAUNCHED();
@@ -1085,7 +1085,11 @@ static int launch(const CUtensorMap& ma, const CUtensorMap& mb, const CUtensorMa
   p.trace = (trace_launch() > 0 && ++g_launch_no == trace_launch()) ? 1 : 0;
   static const int dbg = [] { const char* e = getenv("SPIKERL_TC_DBG"); return e ? atoi(e) : 0; }();
   p.dbg = dbg;
-  return p.cg == 2 ? launch_cg<MODE, BT, 2>(ma, mb, mc, p, st) : launch_cg<MODE, BT, 1>(ma, mb, mc, p, st);
+  // fp16 operands (actor FP16 precision) are a separate instantiation: the G conversions and the
+  // MMA instruction descriptor are then compile-time (a runtime switch cost ~2% at configs[4])
+  if (MODE != WG && p.f16)
+    return p.cg == 2 ? launch_cg<MODE, BT, 2, true>(ma, mb, mc, p, st) : launch_cg<MODE, BT, 1, true>(ma, mb, mc, p, st);
+  return p.cg == 2 ? launch_cg<MODE, BT, 2, false>(ma, mb, mc, p, st) : launch_cg<MODE, BT, 1, false>(ma, mb, mc, p, st);
 }
 
 template <int MODE>
