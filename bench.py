@@ -258,18 +258,24 @@ def time_steps(run_step, K, flush_buf, world):
 
 
 def dominant_kernel(summary, pk_peaks, long_step, clocks=None):
-    """Largest kernel of the step against its roofline. Tensor-bound kernels take the burst bf16
-    peak unless the step is long AND the SM clock measured during it sagged below 95% of max (the
-    sustained figure was measured at ~1320 MHz under the power cap; a step that held 1965 MHz is
-    judged against the burst figure)."""
+    """Largest kernel of the step against its roofline. Tensor-bound kernels are judged against the
+    burst bf16 peak (cuBLAS 8192^3 at full clock), the stricter of the two measured figures: the
+    sustained one was measured at a ~1320 MHz median SM clock under the power cap, which the actor's
+    FWD L1 beats at the 1.8-1.97 GHz it holds, so a frac against it would read above 1. For a long
+    step whose sampled clock sagged below 95% of max, the sustained figure and the frac against it
+    are reported beside (`peak_sustained`, `frac_vs_sustained`) as context, not as the headline."""
     from paper_2502_17496_b200 import _lib
     best = max(summary, key=lambda e: e["total_ms"])
     avg_s = best["total_ms"] / best["launches"] / 1e3
+    extra = {}
     if best["bound"] == "tensor":
         per = best["flops"] / best["launches"]
         sagged = bool(clocks and clocks.get("sm_mhz") and clocks.get("sm_max_mhz")
                       and clocks["sm_mhz"] < 0.95 * clocks["sm_max_mhz"])
-        peak = pk_peaks["bf16_tflops_sustained" if (long_step and sagged) else "bf16_tflops"]
+        peak = pk_peaks["bf16_tflops"]
+        if long_step and sagged and pk_peaks.get("bf16_tflops_sustained"):
+            ps = pk_peaks["bf16_tflops_sustained"]
+            extra = {"peak_sustained": ps, "frac_vs_sustained": round(per / avg_s / 1e12 / ps, 5)}
         ach, unit, bound = per / avg_s / 1e12, "TFLOP/s", "tensor"
     elif best["bound"] == "alu":
         per = best["flops"] / best["launches"]
@@ -290,8 +296,7 @@ def dominant_kernel(summary, pk_peaks, long_step, clocks=None):
             "frac": round(ach / peak, 5), "traffic": traffic, "work_per_launch": per,
             "avg_launch_us": round(avg_s * 1e6, 3), "share_of_step": round(best["total_ms"] / total, 4),
             "peak_src": pk_peaks["src"] if bound != "alu" else "derived (guide: 148 SM x 128 lanes x 2 x 1.965 GHz)",
-            "peak_kind": ("sustained" if peak == pk_peaks.get("bf16_tflops_sustained") else "burst") if bound == "tensor"
-            else ("copy" if bound == "hbm" else "derived")}
+            "peak_kind": "burst" if bound == "tensor" else ("copy" if bound == "hbm" else "derived"), **extra}
 
 
 def cpu_baseline_td3(name, seconds=12.0, min_steps=4):
