@@ -29,7 +29,8 @@ def fp16(x):
     """RNE to IEEE binary16 of fp32(x) (subnormals kept, +-inf on overflow); returned as float64.
     PAPER.md:164 ("FP16 (half precision)" AMP); numpy's float32 -> float16 cast rounds to nearest even."""
     x32 = np.asarray(x, dtype=np.float64).astype(np.float32)
-    return x32.astype(np.float16).astype(np.float64)
+    with np.errstate(over="ignore"):   # overflow to +-inf is the defined result, not an error
+        return x32.astype(np.float16).astype(np.float64)
 
 
 def identity(x):
