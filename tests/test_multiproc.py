@@ -73,7 +73,7 @@ def test_nccl_unique_id_rendezvous_over_gloo():
     assert res[0][2] == res[1][2] and len(res[0][2]) == 128 and any(res[0][2])
 
 
-def _worker_td3(rank, world, port, q, n_steps):
+def _worker_td3(rank, world, port, q, n_steps, scheme="A"):
     import sys
     sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
     _init(rank, world, port)
@@ -86,16 +86,42 @@ def _worker_td3(rank, world, port, q, n_steps):
             o = {}
             for k, v in d.items():
                 t = torch.from_numpy(np.ascontiguousarray(v, dtype=np.float64))
-                dist.all_reduce(t)
-                o[k] = (t / world).numpy()
+                if scheme == "B":      # DDP: gradients pre-divided by the world size, then summed
+                    t = t / world
+                    dist.all_reduce(t)
+                    o[k] = t.numpy()
+                else:                  # MPI average_gradients: sum over ranks, then divide
+                    dist.all_reduce(t)
+                    o[k] = (t / world).numpy()
             out.append(o)
         return out
 
     shape = sg.ActorShape(3, 2, pop_enc=5, pop_dec=4, n1=12, n2=10, T=5, precision="fp32")
     cs = sg.CriticShape(5, 16, 16, precision="fp32")
     hp = sg.TD3Hyper()
-    rng = np.random.default_rng(0)             # same init on every rank (broadcast_weights)
+    # scheme A: each rank draws its own init and rank 0's is broadcast (PAPER.md:135
+    # broadcast_weights); scheme B: every rank builds the same seeded init (DDP's start state)
+    rng = np.random.default_rng(0 if scheme == "B" else 77 * rank)
     st = oracle.init_state(sg.actor_params(shape, rng), sg.critic_params(cs, rng), sg.critic_params(cs, rng))
+    if scheme == "A":
+        rng0 = np.random.default_rng(0)
+        ref = oracle.init_state(sg.actor_params(shape, rng0), sg.critic_params(cs, rng0), sg.critic_params(cs, rng0))
+
+        def bcast(a):
+            t = torch.from_numpy(np.ascontiguousarray(a) if rank == 0 else np.zeros_like(a))
+            dist.broadcast(t, 0)
+            return t.numpy()
+
+        def walk(x):
+            if isinstance(x, dict):
+                return {k: walk(v) for k, v in x.items()}
+            if isinstance(x, (list, tuple)):
+                return type(x)(walk(v) for v in x)
+            if isinstance(x, np.ndarray):
+                return bcast(x)
+            return x
+        st = walk(st)
+        assert all(np.array_equal(st["actor"][k], ref["actor"][k]) for k in ref["actor"])
     B = 6
     for k in range(1, n_steps + 1):
         brng = np.random.default_rng(1000 + k)  # the global batch of step k, split by rank
@@ -140,6 +166,26 @@ def test_data_parallel_td3_equivalence():
     flat = np.concatenate([np.ravel(st["actor"][kk]) for kk in sorted(st["actor"])] +
                           [np.ravel(c[kk]) for c in st["c"] for kk in sorted(c)])
     assert np.allclose(res[0], flat, rtol=1e-5, atol=1e-9)
+
+
+def test_scheme_a_equals_scheme_b():
+    """PAPER.md:135 (MPI: broadcast_weights + average_gradients) and PAPER.md:144 (DDP: same init,
+    gradients pre-divided then summed) give bit-identical replicas at world size 2: division by 2
+    is exact, so sum-then-divide and divide-then-sum round identically (SURVEY 8(f) #3)."""
+    ctx = mp.get_context("spawn")
+    out = {}
+    for scheme in ("A", "B"):
+        q = ctx.Queue()
+        port = _free_port()
+        ps = [ctx.Process(target=_worker_td3, args=(r, 2, port, q, 3, scheme)) for r in range(2)]
+        for p in ps:
+            p.start()
+        res = dict(q.get(timeout=300) for _ in range(2))
+        for p in ps:
+            p.join(timeout=60)
+        assert np.array_equal(res[0], res[1])
+        out[scheme] = res[0]
+    assert np.array_equal(out["A"], out["B"])
 
 
 def test_bench_sharding_arithmetic():
