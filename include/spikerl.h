@@ -65,9 +65,13 @@ enum spikerl_precision {
 };
 
 enum spikerl_engine {
-  SPIKERL_ENGINE_AUTO = 0,   /* bf16 -> tcgen05 tensor-core GEMMs; fp32 -> SIMT              */
-  SPIKERL_ENGINE_SIMT = 1,   /* plain SIMT kernels (fp32 FFMA), any precision                 */
-  SPIKERL_ENGINE_TCGEN05 = 2 /* force tcgen05 (bf16 only)                                     */
+  SPIKERL_ENGINE_AUTO = 0,   /* bf16/fp16 -> tcgen05 tensor-core GEMMs; fp32 -> SIMT. Never
+                                switches engine silently: a bf16 shape tcgen05 cannot tile (odd
+                                T > 16, T > 32) is SPIKERL_E_UNSUPPORTED (north_star: no
+                                multi-backend dispatch)                                        */
+  SPIKERL_ENGINE_SIMT = 1,   /* plain SIMT kernels (fp32 FFMA), fp32 or bf16 operands; only when
+                                asked for                                                       */
+  SPIKERL_ENGINE_TCGEN05 = 2 /* tcgen05 (bf16/fp16 only)                                       */
 };
 
 /* Actor problem statement (PAPER.md:131 + north_star): obs dim S, action dim A, encoder
@@ -191,7 +195,10 @@ int spikerl_actor_backward(const spikerl_actor_cfg* cfg, int batch, const float*
  * params2 [2][P] fp32 (+ bf16 copy iff precision=BF16). q [2][B] receives Q1, Q2.
  * If target_y [B] != NULL: loss (device scalar, may be NULL) = mean(Q1-y)^2 + mean(Q2-y)^2 and,
  * if grad_params2 != NULL, its gradient w.r.t. both critics (overwritten).
- * If grad_act [B][A] != NULL: grad_act = act_grad_scale * dQ1/da (per sample). */
+ * If grad_act [B][A] != NULL: grad_act = act_grad_scale * dQ1/da (per sample).
+ * BF16 critics run on the tensor-core kernels, which need hidden widths 256-256 and in_dim <= 512
+ * (configs[1..3]); other bf16 shapes are SPIKERL_E_UNSUPPORTED (checked before anything is
+ * enqueued). FP32 critics run on SIMT GEMMs (any shape). */
 int spikerl_critic_fwd_bwd(const spikerl_critic_cfg* cfg, int batch, const float* params2,
                            const void* params2_bf16, const float* obs, int obs_dim,
                            const float* act, int act_dim, const float* target_y, float* q,
@@ -280,7 +287,9 @@ int spikerl_comm_init(int rank, int world, const void* id128 /* host */, spikerl
 int spikerl_comm_destroy(spikerl_comm* comm);
 int spikerl_comm_world(const spikerl_comm* comm);
 int spikerl_comm_rank(const spikerl_comm* comm);
-/* in place: grads <- mean over ranks (ncclAvg, fp32)  — PAPER.md:135 average_gradients */
+/* in place: grads <- mean over ranks (ncclAvg, fp32)  — PAPER.md:135 average_gradients.
+ * comm == NULL: identity, nothing enqueued. A one-rank communicator still calls NCCL (identity
+ * result), so the one-GPU path runs the same NCCL kernels, graph-capturable. */
 int spikerl_allreduce_grads(spikerl_comm* comm, float* grads, size_t count,
                             spikerl_stream_t stream);
 /* params <- params of `root`  — PAPER.md:135 broadcast_weights */

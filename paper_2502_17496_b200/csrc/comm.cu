@@ -115,7 +115,9 @@ int spikerl_comm_rank(const spikerl_comm* comm) { return comm ? comm->rank : 0; 
 int spikerl_allreduce_grads(spikerl_comm* comm, float* grads, size_t count, spikerl_stream_t stream) {
   if (!comm) return SPIKERL_OK;  // one GPU: identity
   if (!grads && count) { spk::set_error("null grads"); return SPIKERL_E_ARG; }
-  if (comm->world == 1 || count == 0) return SPIKERL_OK;
+  if (count == 0) return SPIKERL_OK;
+  // world 1 included: NCCL runs one-rank communicators (the mean is the identity), so the one-GPU
+  // path exercises the same calls, inside graph captures too
   return spk::nccl_status(spk::api().allReduce(grads, grads, count, ncclFloat32, ncclAvg, comm->comm,
                                                (cudaStream_t)stream),
                           "ncclAllReduce");
@@ -128,7 +130,7 @@ int spikerl_broadcast_params(spikerl_comm* comm, float* params, size_t count, in
     spk::set_error("spikerl_broadcast_params: bad arguments");
     return SPIKERL_E_ARG;
   }
-  if (comm->world == 1 || count == 0) return SPIKERL_OK;
+  if (count == 0) return SPIKERL_OK;
   return spk::nccl_status(spk::api().broadcast(params, params, count, ncclFloat32, root, comm->comm,
                                                (cudaStream_t)stream),
                           "ncclBroadcast");

@@ -9,16 +9,24 @@
 
 namespace spk {
 
-// SM count of the current device (cached; grids of persistent / grid-strided kernels are sized by it)
+// Current device index (per-device caches below are keyed by it; a process may drive several GPUs).
+inline int cur_device() {
+  int dev = 0;
+  cudaGetDevice(&dev);
+  return dev & 31;
+}
+
+// SM count of the current device (cached per device; grids of persistent / grid-strided kernels are
+// sized by it)
 inline int num_sms() {
-  static int n = 0;
-  if (!n) {
-    int dev = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
-    if (n <= 0) n = 148;
+  static int n[32] = {};
+  const int dev = cur_device();
+  if (!n[dev]) {
+    int v = 0;
+    cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev);
+    n[dev] = v > 0 ? v : 148;
   }
-  return n;
+  return n[dev];
 }
 
 // ----------------------------------------------------------------------------- errors
@@ -52,6 +60,19 @@ cudaError_t take_launch_error();
   do {                                                                               \
     int s_ = (expr);                                                                 \
     if (s_ != SPIKERL_OK) return s_;                                                 \
+  } while (0)
+
+// Opt a kernel into > 48 KB of dynamic shared memory once per (call site, device): the attribute
+// is per device, so a process driving several GPUs sets it on each before the first launch there.
+#define SPK_SMEM_ATTR(kernel, bytes)                                                  \
+  do {                                                                               \
+    static unsigned done_mask_ = 0u;                                                 \
+    const unsigned bit_ = 1u << ::spk::cur_device();                                 \
+    if (!(__atomic_load_n(&done_mask_, __ATOMIC_ACQUIRE) & bit_)) {                  \
+      SPK_CHECK_CUDA(cudaFuncSetAttribute((kernel),                                  \
+                     cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(bytes)));    \
+      __atomic_fetch_or(&done_mask_, bit_, __ATOMIC_ACQ_REL);                        \
+    }                                                                                \
   } while (0)
 
 // ----------------------------------------------------------------------------- PDL

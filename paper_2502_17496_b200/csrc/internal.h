@@ -37,15 +37,9 @@ int launch_enc_grad_simt(const ActorDims& d, int B, const void* Gsum, const floa
                          float* dsigma, int accumulate, cudaStream_t st);
 size_t enc_grad_partial_bytes(const ActorDims& d, int B);
 
-// ---- latency-regime fused actor forward (k_actor_fused.cu): encoder + 3 LIF layers + decoder in
-// one clustered launch for small batches; writes the tcgen05 engine's tape layout
-bool fused_fwd_ok(const ActorDims& d, int B);
-int launch_actor_fwd_fused(const ActorDims& d, int B, const float* obs, const float* params,
-                           const __nv_bfloat16* pb16, const TapeLayout& L, char* tape, float* actions,
-                           cudaStream_t st);
-
 // ---- tcgen05 engine (k_tc_gemm.cu)
 bool tc_supported(const ActorDims& d);
+bool tc_pairs_enabled();   // CTA pairs (cta_group::2) in use (SPIKERL_TC_PAIR=0 turns them off)
 int launch_lif_fwd_tc(const ActorDims& d, int l, int B, const uint32_t* bits_in,
                       const __nv_bfloat16* Wb16, uint32_t* bits_out, uint32_t* mask_out,
                       uint8_t* counts, uint8_t* bitsT_out, uint8_t* maskT_out, int row_bytes,

@@ -289,7 +289,7 @@ size_t critic_ws_bytes(const CriticDims& c, int B) {
   return n > m ? n : m;
 }
 
-// SIMT GEMM path: fp32 precision (configs[0]-style critics) and shapes outside the mma path.
+// SIMT GEMM path: fp32 precision only (bf16 critics run on the tensor-core kernels).
 int critic_fwd_bwd(const CriticDims& c, int B, const float* params2, const __nv_bfloat16* pb16,
                    const float* obs, int S, const float* act, int A, const float* y, float* q,
                    float* loss, float* grad2, float* grad_act, float act_scale, int nz, void* ws,
@@ -297,7 +297,12 @@ int critic_fwd_bwd(const CriticDims& c, int B, const float* params2, const __nv_
   if (critic_mma_ok(c))
     return critic_mma_fwd_bwd(c, B, params2, pb16, obs, S, act, A, y, q, loss, grad2, grad_act, act_scale, nz, ws, st,
                               wait_before_loss, dq_scale);
-  if (dq_scale) { set_error("critic: loss scaling needs the bf16 mma critic"); return SPIKERL_E_UNSUPPORTED; }
+  if (c.bf16) {   // no silent switch of engine (north_star: no multi-backend dispatch)
+    set_error("bf16 critic: the tensor-core critic needs hidden widths 256-256 and in_dim <= 512 (got %d-%d, %d)",
+              c.H1, c.H2, c.in);
+    return SPIKERL_E_UNSUPPORTED;
+  }
+  if (dq_scale) { set_error("critic: loss scaling needs the bf16 tensor-core critic"); return SPIKERL_E_UNSUPPORTED; }
   CriticWs w = carve(c, B, ws);
   const bool bf = c.bf16 != 0;
   const long long P = (long long)c.off[SPIKERL_CRITIC_NPARAM];

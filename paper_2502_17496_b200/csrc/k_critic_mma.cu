@@ -729,7 +729,7 @@ int launch_critic_refresh(const CriticDims& c, const float* params2, __nv_bfloat
 static bool tc_wgrad_ok(const CriticDims& c, const MmaWs& w, int Bp) {
   static const int env = [] { const char* e = getenv("SPIKERL_CRITIC_WG_TC"); return e ? atoi(e) : 1; }();
   const MmaLayout L = mma_layout(c);
-  return env != 0 && c.H1 == HW && c.H2 == HW && L.inq <= 3 * 256 &&
+  return env != 0 && tc_pairs_enabled() && c.H1 == HW && c.H2 == HW && L.inq <= 3 * 256 &&
          (const char*)w.dZ1T == (const char*)w.dZ2T + (size_t)2 * 2 * HW * Bp &&
          (const char*)w.H1T == (const char*)w.XT + (size_t)2 * round_up(L.inq, 64) * Bp;
 }
@@ -749,12 +749,7 @@ int critic_mma_fwd_bwd(const CriticDims& c, int B, const float* params2, const _
     // one CTA per SM fits (staged W2): at most num_sms / nz CTAs per critic, each looping over tiles
     const int cap = num_sms() / nz > 0 ? num_sms() / nz : 1;
     dim3 grid(Bp / RB < cap ? Bp / RB : cap, nz);
-    static bool attr = false;
-    if (!attr) {
-      SPK_CHECK_CUDA(cudaFuncSetAttribute(critic_fwd_mma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                          (int)kW2Smem));
-      attr = true;
-    }
+    SPK_SMEM_ATTR(critic_fwd_mma_kernel, kW2Smem);
     pdl(critic_fwd_mma_kernel, grid, 256, kW2Smem, st)(
         B, Bp, S, A, L.inp, L.inq, obs, act, pb, L.P, L.tb, L.W1p, L.W2c, oW3, params2,
         (long long)c.off[SPIKERL_CRITIC_B1], (long long)c.off[SPIKERL_CRITIC_B2], (long long)c.off[SPIKERL_CRITIC_B3],
@@ -775,12 +770,7 @@ int critic_mma_fwd_bwd(const CriticDims& c, int B, const float* params2, const _
   {
     ProfScope ps_("critic_bwd_data_mma", PB_TENSOR, 2.0 * B * nb * ((double)HW * HW), 0.0, st);
     dim3 grid(Bp / RB, nb);
-    static bool attr = false;
-    if (!attr) {
-      SPK_CHECK_CUDA(cudaFuncSetAttribute(critic_bwd_data_mma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                          (int)kW2Smem));
-      attr = true;
-    }
+    SPK_SMEM_ATTR(critic_bwd_data_mma_kernel, kW2Smem);
     pdl(critic_bwd_data_mma_kernel, grid, 256, kW2Smem, st)(
         B, Bp, S, A, L.inp, q, y, mode, act_scale, w.dq, w.part, w.ticket, fused_scalar ? loss : nullptr, pb, L.P, L.tb,
         oW3, L.W1T, L.W2T, w.Z1, w.Z2, w.dZ2T, w.dZ1T, grad_act, want_params ? 1 : 0, dq_scale);

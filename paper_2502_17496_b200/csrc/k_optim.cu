@@ -20,12 +20,15 @@ static int ew_grid(size_t n, int per_thread) {
 // copy peak, the partial last wave and the ramp of each wave exposed).
 template <typename K>
 static int stream_grid(K kernel, size_t n, int per_thread) {
-  static int per_sm = 0;
+  static int cache[32] = {};   // per device
+  int& per_sm = cache[cur_device()];
   if (!per_sm) {
-    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, 256, 0) != cudaSuccess || per_sm < 1) {
+    int v = 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&v, kernel, 256, 0) != cudaSuccess || v < 1) {
       cudaGetLastError();
-      per_sm = 2;
+      v = 2;
     }
+    per_sm = v;
   }
   const size_t threads = (n + per_thread - 1) / per_thread;
   const size_t blocks = (threads + 255) / 256;

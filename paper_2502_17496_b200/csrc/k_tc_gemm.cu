@@ -999,9 +999,12 @@ namespace tc {
 // Co-resident CTA pairs: every tc_kernel instance uses one CTA per SM (SMEM_BYTES), so one query
 // answers for all; cached so the split-K plan and the launch always agree.
 static int pair_slots() {
-  static int slots = 0;
-  if (!slots) {
-    cudaFuncSetAttribute(tc_kernel<FWD, 8, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES);
+  static int slots[32] = {};
+  const int dev = cur_device();
+  if (!slots[dev]) {
+    if (cudaFuncSetAttribute(tc_kernel<FWD, 8, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES) !=
+        cudaSuccess)
+      cudaGetLastError();
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(num_sms() / 2 * 2, 1, 1);
     cfg.blockDim = dim3(NUM_THREADS, 1, 1);
@@ -1018,9 +1021,9 @@ static int pair_slots() {
       cudaGetLastError();
       nc = num_sms() / 2;
     }
-    slots = nc;
+    slots[dev] = nc;
   }
-  return slots;
+  return slots[dev];
 }
 
 // CTA pairs (cta_group::2) are used when the tile count allows; SPIKERL_TC_PAIR=0 forces single CTAs.
@@ -1035,13 +1038,7 @@ static bool pairs_enabled() {
 
 template <int MODE, int BT, int CG, bool F16>
 static int launch_cg(const CUtensorMap& ma, const CUtensorMap& mb, const CUtensorMap& mc, const Params& p, cudaStream_t st) {
-  static bool attr = false;
-  if (!attr) {
-    cudaError_t e =
-        cudaFuncSetAttribute(tc_kernel<MODE, BT, CG, F16>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES);
-    if (e != cudaSuccess) { set_error("cudaFuncSetAttribute: %s", cudaGetErrorString(e)); return SPIKERL_E_CUDA; }
-    attr = true;
-  }
+  SPK_SMEM_ATTR((tc_kernel<MODE, BT, CG, F16>), SMEM_BYTES);
   if (CG == 1) {
     const int ncta = num_sms();
     const int grid = p.n_units < ncta ? (int)p.n_units : ncta;
@@ -1127,6 +1124,8 @@ constexpr int FWD_MAX_BT = 32, DX_MAX_BT = 16;
 }  // namespace tc
 
 using namespace tc;
+
+bool tc_pairs_enabled() { return pairs_enabled(); }
 
 bool tc_supported(const ActorDims& d) {
   if (!d.bf16) return false;

@@ -55,10 +55,15 @@ static int resolve_engine(const spikerl_actor_cfg* c, ActorDims* d) {
       if (!tc_supported(*d)) { set_error("tcgen05 engine does not support this shape"); return SPIKERL_E_UNSUPPORTED; }
       return SPIKERL_OK;
     case SPIKERL_ENGINE_AUTO:
-      d->engine = SPIKERL_ENGINE_SIMT;
-      if (bf) {
-        d->engine = SPIKERL_ENGINE_TCGEN05;
-        if (!tc_supported(*d)) d->engine = SPIKERL_ENGINE_SIMT;
+      // fp32 runs on the SIMT engine (the only fp32 engine); bf16 runs on tcgen05, and a shape it
+      // cannot tile is an error, not a silent switch of engine (north_star: no multi-backend
+      // dispatch). ENGINE_SIMT may still be requested explicitly for bf16.
+      if (!bf) { d->engine = SPIKERL_ENGINE_SIMT; return SPIKERL_OK; }
+      d->engine = SPIKERL_ENGINE_TCGEN05;
+      if (!tc_supported(*d)) {
+        set_error("bf16 actor: the tcgen05 engine cannot tile T=%d (needs T <= 16, or even T <= 32); request "
+                  "SPIKERL_ENGINE_SIMT explicitly", d->T);
+        return SPIKERL_E_UNSUPPORTED;
       }
       return SPIKERL_OK;
     default: set_error("unknown engine %d", c->engine); return SPIKERL_E_ARG;
@@ -158,6 +163,20 @@ int critic_dims(const spikerl_critic_cfg* c, CriticDims* d) {
   return SPIKERL_OK;
 }
 
+// compute-time checks of a critic config, made on the host before anything is enqueued
+static int critic_supported(const CriticDims& c, bool loss_scaling) {
+  if (c.bf16 && !critic_mma_ok(c)) {
+    set_error("bf16 critic: the tensor-core critic needs hidden widths 256-256 and in_dim <= 512 (got %d-%d, %d)",
+              c.H1, c.H2, c.in);
+    return SPIKERL_E_UNSUPPORTED;
+  }
+  if (loss_scaling && !c.bf16) {
+    set_error("dynamic loss scaling needs the bf16 tensor-core critic");
+    return SPIKERL_E_UNSUPPORTED;
+  }
+  return SPIKERL_OK;
+}
+
 // ------------------------------------------------------------------ actor workspace layout
 struct ActorWs {
   size_t tape;      // inference-only spike planes (TapeLayout at offset 0)
@@ -199,8 +218,6 @@ static int actor_forward_impl(const ActorDims& d, int B, const float* params,
   uint32_t* mask[4];
   for (int l = 0; l < 4; ++l) { bits[l] = (uint32_t*)(tape + L.bits[l]); mask[l] = (uint32_t*)(tape + L.mask[l]); }
   uint8_t* counts = (uint8_t*)(tape + L.counts);
-  if (fused_fwd_ok(d, B))   // small batch: one clustered launch instead of five
-    return launch_actor_fwd_fused(d, B, obs, params, pb16, L, tape, actions, st);
   SPK_TRY(launch_enc_fwd(d, B, obs, params + d.off[SPIKERL_ACTOR_MU], params + d.off[SPIKERL_ACTOR_SIGMA],
                          A, bits[0], st));
   for (int l = 1; l <= 3; ++l) {
@@ -513,6 +530,7 @@ int spikerl_critic_fwd_bwd(const spikerl_critic_cfg* cfg, int batch, const float
     set_error("spikerl_critic_fwd_bwd: bad arguments");
     return SPIKERL_E_ARG;
   }
+  SPK_TRY(critic_supported(c, false));
   return critic_fwd_bwd(c, batch, params2, (const __nv_bfloat16*)params2_bf16, obs, obs_dim, act, act_dim, target_y,
                         q, target_y ? loss : nullptr, grad_params2, grad_act, act_grad_scale, 2, workspace,
                         (cudaStream_t)stream);
@@ -558,6 +576,7 @@ int spikerl_td3_update(const spikerl_actor_cfg* acfg, const spikerl_critic_cfg* 
     set_error("spikerl_td3_update: null buffer");
     return SPIKERL_E_ARG;
   }
+  SPK_TRY(critic_supported(cd, b->amp != nullptr));
   if (b->replay_size < B) {
     set_error("replay holds %lld < batch %d transitions", b->replay_size, B);
     return SPIKERL_E_NOTREADY;
@@ -689,6 +708,7 @@ int spikerl_td3_update_pair(const spikerl_actor_cfg* acfg, const spikerl_critic_
     set_error("spikerl_td3_update_pair: null buffer");
     return SPIKERL_E_ARG;
   }
+  SPK_TRY(critic_supported(cd, b->amp != nullptr));
   if (b->replay_size < B) {
     set_error("replay holds %lld < batch %d transitions", b->replay_size, B);
     return SPIKERL_E_NOTREADY;

@@ -73,6 +73,38 @@ def test_tcgen05_needs_bf16(L):
     assert L.lib().spikerl_actor_cfg_check(C.byref(c)) == L.E_UNSUPPORTED
 
 
+@pytest.mark.parametrize("T,status", [(5, 0), (16, 0), (24, 0), (17, 7), (33, 7)])
+def test_auto_engine_never_switches_silently(L, T, status):
+    """bf16 with ENGINE_AUTO runs on tcgen05; a shape it cannot tile is E_UNSUPPORTED (no silent drop
+    to another engine: north_star "no multi-backend dispatch"); ENGINE_SIMT must then be asked for."""
+    c = cfg(precision="bf16", T=T)
+    assert L.lib().spikerl_actor_cfg_check(C.byref(c)) == status, L.last_error()
+    assert L.lib().spikerl_actor_cfg_check(C.byref(cfg(precision="bf16", T=T, engine="simt"))) == 0
+
+
+def test_bf16_critic_shape_not_silently_rerouted(L):
+    """A bf16 critic outside the tensor-core kernels' shapes (hidden 256-256, in <= 512) is rejected on
+    the host before anything is enqueued; fp32 critics run on the SIMT GEMMs; loss scaling needs bf16."""
+    lib = L.lib()
+    from paper_2502_17496_b200 import critic_cfg, td3_cfg
+    for cc, st_expect in ((critic_cfg(23, hidden1=128, hidden2=128), L.E_UNSUPPORTED),
+                          (critic_cfg(600), L.E_UNSUPPORTED)):
+        z = C.c_void_p(256)
+        st = lib.spikerl_critic_fwd_bwd(C.byref(cc), 8, z, z, z, cc.in_dim - 6, z, 6, None, z, None, None, None,
+                                        0.0, z, None)
+        assert st == st_expect, L.last_error()
+    c = cfg(precision="fp32")
+    cc = critic_cfg(23, precision="fp32")
+    bufs = L.TD3Bufs()
+    for f, _ in L.TD3Bufs._fields_[:-1]:
+        setattr(bufs, f, 256)
+    bufs.replay_size = 1000
+    bufs.amp = 256
+    st = lib.spikerl_td3_update(C.byref(c), C.byref(cc), C.byref(td3_cfg(256)), C.byref(bufs), 1, 0, None, None,
+                                None, C.c_void_p(256), C.c_void_p(256), None)
+    assert st == L.E_UNSUPPORTED, L.last_error()
+
+
 def test_tape_layout_sizes(L):
     c = cfg(precision="bf16")
     lay = L.TapeLayout()
