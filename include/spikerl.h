@@ -272,6 +272,21 @@ int spikerl_td3_update_pair(const spikerl_actor_cfg* acfg, const spikerl_critic_
 size_t spikerl_td3_pair_workspace_bytes(const spikerl_actor_cfg* acfg, const spikerl_critic_cfg* ccfg,
                                         int batch);
 
+/* Byte offsets, inside one update's workspace (the pair workspace holds two such blocks back to
+ * back, update k then k + 1), of the intermediates a TD3 update leaves behind (read by the parity
+ * tests' teacher-forced protocol; host call, no device work). After spikerl_td3_update(k):
+ *   s, a, r, s2, d  fp32 the gathered minibatch ([B][S], [B][A], [B], [B][S], [B])
+ *   a2   fp32 [B][A]  target-policy actions pi'(s');   at fp32 [B][A]  smoothed a~
+ *   y    fp32 [B]     TD target;                        api fp32 [B][A]  pi(s) (actor steps)
+ *   ga   fp32 [B][A]  -(1/B) dQ1/da at (s, pi(s)) (actor steps; times the actor loss scale)
+ *   tape_pi, tape_target  tape buffers (spikerl_tape_layout) of the pi(s) / pi'(s') forwards
+ * SPEC.md:235-252 (compute_target, train_step). */
+typedef struct {
+  size_t s, a, r, s2, d, a2, at, api, y, ga, tape_pi, tape_target, total;
+} spikerl_td3_ws_layout;
+int spikerl_td3_workspace_layout(const spikerl_actor_cfg* acfg, const spikerl_critic_cfg* ccfg, int batch,
+                                 spikerl_td3_ws_layout* out);
+
 /* Fill a replay shard on the device: s,s2 ~ N(0,1) clip +-5, a ~ U[-1,1], r ~ N(0,1),
  * done ~ Bernoulli(p_done) (configs[1]); Philox keyed by (seed, rank). */
 int spikerl_replay_fill(float* s, float* a, float* r, float* s2, float* d, long long n, int obs_dim,

@@ -18,7 +18,7 @@ Unpinned: learning dynamics / rewards (no environment; PAPER.md Figs 5a-c missin
 scope, "parity unpinned" (DESIGN.md).
 """
 from .numerics import bf16, fp32, rounder  # noqa: F401
-from .actor import (gaussian_stim, encode_spikes, lif_layer_forward, decode, actor_forward,  # noqa: F401
+from .actor import (gaussian_stim, gaussian_stim_f64, encode_spikes, lif_layer_forward, decode, actor_forward,  # noqa: F401
                     surrogate, lif_reverse_scan, actor_backward, counts)
 from .critic import critic_forward, critic_backward  # noqa: F401
 from .td3 import adam_update, polyak, init_state, td3_update  # noqa: F401

@@ -41,6 +41,12 @@ def gaussian_stim(s, mu, sigma):
     inputs with the op sequence d=s-mu; q=d*d; den=2*(sigma*sigma); exp(-(q/den)) (R4),
     then one rounding to fp32. Flattening k = i*E + e (R1).
     """
+    return gaussian_stim_f64(s, mu, sigma).astype(np.float32)
+
+
+def gaussian_stim_f64(s, mu, sigma):
+    """The fp64 value gaussian_stim rounds to fp32 (same op sequence, R4), [B][S*E]; the parity
+    protocol's encoder exemption (C-4 step 2) is decided on it."""
     s64 = np.asarray(s, np.float32).astype(F64)
     mu64 = np.asarray(mu, np.float32).astype(F64)
     sg64 = np.asarray(sigma, np.float32).astype(F64)
@@ -50,7 +56,7 @@ def gaussian_stim(s, mu, sigma):
     q = d * d
     den = 2.0 * (sg64 * sg64)
     A = np.exp(-(q / den[None, :, :]))
-    return A.astype(np.float32).reshape(s64.shape[0], -1)
+    return A.reshape(s64.shape[0], -1)
 
 
 def encode_spikes(A, T):

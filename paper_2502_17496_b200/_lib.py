@@ -67,6 +67,11 @@ class TD3Bufs(C.Structure):
                 ("rs2", C.c_void_p), ("rd", C.c_void_p), ("replay_size", C.c_longlong), ("amp", C.c_void_p)]
 
 
+class TD3WsLayout(C.Structure):
+    _fields_ = [(n, C.c_size_t) for n in ("s", "a", "r", "s2", "d", "a2", "at", "api", "y", "ga", "tape_pi",
+                                         "tape_target", "total")]
+
+
 class ProfEntry(C.Structure):
     _fields_ = [("name", C.c_char * 48), ("bound", C.c_int), ("launches", C.c_longlong),
                 ("total_ms", C.c_double), ("flops", C.c_double), ("bytes", C.c_double)]
@@ -109,6 +114,7 @@ _SIGS = {
     "spikerl_td3_workspace_bytes": (SZ, [C.POINTER(ActorCfg), C.POINTER(CriticCfg), I]),
     "spikerl_td3_pair_workspace_bytes": (SZ, [C.POINTER(ActorCfg), C.POINTER(CriticCfg), I]),
     "spikerl_actor_tape_layout": (I, [C.POINTER(ActorCfg), I, C.POINTER(TapeLayout)]),
+    "spikerl_td3_workspace_layout": (I, [C.POINTER(ActorCfg), C.POINTER(CriticCfg), I, C.POINTER(TD3WsLayout)]),
     "spikerl_actor_refresh_bf16": (I, [C.POINTER(ActorCfg), P, P, P]),
     "spikerl_critic_refresh_bf16": (I, [C.POINTER(CriticCfg), I, P, P, P]),
     "spikerl_actor_forward": (I, [C.POINTER(ActorCfg), I, P, P, P, P, C.POINTER(Tape), P, P]),

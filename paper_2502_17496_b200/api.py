@@ -164,40 +164,49 @@ class SpikingActor:
 
     # tape views (for parity tests / diagnostics)
     def tape_view(self):
-        cfg, B, lay = self.cfg, self.batch, self.layout
-        T = cfg.T
-        K0, N3 = cfg.obs_dim * cfg.pop_enc, cfg.act_dim * cfg.pop_dec
-        buf = self.tape_buf
-
-        def seg(off, nbytes, dtype, shape):
-            return buf[off:off + nbytes].view(dtype).view(*shape)
-        out = {"A": seg(lay.A, 4 * B * K0, torch.float32, (B, K0))}
-        for l in range(4):
-            W = lay.padded[l] // 32
-            out[f"bits{l}"] = seg(lay.bits[l], 4 * T * B * W, torch.int32, (T, B, W))
-            if l:
-                out[f"mask{l}"] = seg(lay.mask[l], 4 * T * B * W, torch.int32, (T, B, W))
-            if l and lay.bitsT[l]:
-                P = lay.padded[l]
-                Q = (B + 31) // 32 * 8          # batch quads
-                nb = Q * P * (lay.tpad // 2)
-                out[f"bitsT{l}"] = seg(lay.bitsT[l], nb, torch.uint8, (Q, P, lay.tpad // 2))
-                out[f"maskT{l}"] = seg(lay.maskT[l], nb, torch.uint8, (Q, P, lay.tpad // 2))
-                # the tcgen05 engine keeps the hidden layers' window bits only quad-major (the
-                # dX epilogue's input); this diagnostic view re-packs them batch-major
-                out[f"mask{l}"] = _quads_to_words(out[f"maskT{l}"], T, B)
-        out["counts"] = seg(lay.counts, B * N3, torch.uint8, (B, N3))
-        out["act"] = seg(lay.act, 4 * B * cfg.act_dim, torch.float32, (B, cfg.act_dim))
-        return out
+        return tape_view(self.cfg, self.batch, self.tape_buf, 0)
 
     def spikes(self):
         """Host copies of the spike / mask planes as uint8 [T][B][N_l]."""
-        v = self.tape_view()
-        N = [self.cfg.obs_dim * self.cfg.pop_enc, self.cfg.hidden1, self.cfg.hidden2,
-             self.cfg.act_dim * self.cfg.pop_dec]
-        o = {f"o{l}": unpack_bits(v[f"bits{l}"], N[l]) for l in range(4)}
-        o.update({f"h{l}": unpack_bits(v[f"mask{l}"], N[l]) for l in (1, 2, 3)})
-        return o
+        return tape_spikes(self.cfg, self.tape_view())
+
+
+def tape_view(cfg, B, buf, base=0):
+    """Typed views of a tape held in the uint8 device buffer ``buf`` at byte offset ``base``
+    (spikerl_actor_tape_layout), for parity tests / diagnostics."""
+    lay = L.TapeLayout()
+    check(lib().spikerl_actor_tape_layout(C.byref(cfg), B, C.byref(lay)), "tape layout")
+    T = cfg.T
+    K0, N3 = cfg.obs_dim * cfg.pop_enc, cfg.act_dim * cfg.pop_dec
+
+    def seg(off, nbytes, dtype, shape):
+        return buf[base + off:base + off + nbytes].view(dtype).view(*shape)
+    out = {"A": seg(lay.A, 4 * B * K0, torch.float32, (B, K0))}
+    for l in range(4):
+        W = lay.padded[l] // 32
+        out[f"bits{l}"] = seg(lay.bits[l], 4 * T * B * W, torch.int32, (T, B, W))
+        if l:
+            out[f"mask{l}"] = seg(lay.mask[l], 4 * T * B * W, torch.int32, (T, B, W))
+        if l and lay.bitsT[l]:
+            P = lay.padded[l]
+            Q = (B + 31) // 32 * 8          # batch quads
+            nb = Q * P * (lay.tpad // 2)
+            out[f"bitsT{l}"] = seg(lay.bitsT[l], nb, torch.uint8, (Q, P, lay.tpad // 2))
+            out[f"maskT{l}"] = seg(lay.maskT[l], nb, torch.uint8, (Q, P, lay.tpad // 2))
+            # the tcgen05 engine keeps the hidden layers' window bits only quad-major (the
+            # dX epilogue's input); this diagnostic view re-packs them batch-major
+            out[f"mask{l}"] = _quads_to_words(out[f"maskT{l}"], T, B)
+    out["counts"] = seg(lay.counts, B * N3, torch.uint8, (B, N3))
+    out["act"] = seg(lay.act, 4 * B * cfg.act_dim, torch.float32, (B, cfg.act_dim))
+    return out
+
+
+def tape_spikes(cfg, v):
+    """Host copies of a tape view's spike / mask planes as uint8 [T][B][N_l]."""
+    N = [cfg.obs_dim * cfg.pop_enc, cfg.hidden1, cfg.hidden2, cfg.act_dim * cfg.pop_dec]
+    o = {f"o{l}": unpack_bits(v[f"bits{l}"], N[l]) for l in range(4)}
+    o.update({f"h{l}": unpack_bits(v[f"mask{l}"], N[l]) for l in (1, 2, 3)})
+    return o
 
 
 def _quads_to_words(qt, T, B):
@@ -406,6 +415,25 @@ class TD3:
 
     def replay_graph(self, step: int):
         self.graphs[step % self.hp.policy_delay].replay()
+
+    def ws_view(self, pair=False, slot=0):
+        """Typed views of the intermediates the last update left in its workspace
+        (spikerl_td3_workspace_layout); pair=True: the pair workspace, slot 0 / 1 = update k / k + 1."""
+        lay = L.TD3WsLayout()
+        B, S, A = self.hp.batch, self.acfg.obs_dim, self.acfg.act_dim
+        check(lib().spikerl_td3_workspace_layout(C.byref(self.acfg), C.byref(self.ccfg), B, C.byref(lay)), "ws layout")
+        buf = self.ws_pair if pair else self.ws
+        base = slot * lay.total if pair else 0
+
+        def f32(off, *shape):
+            n = int(np.prod(shape))
+            return buf[base + off:base + off + 4 * n].view(torch.float32).view(*shape)
+        out = dict(s=f32(lay.s, B, S), a=f32(lay.a, B, A), r=f32(lay.r, B), s2=f32(lay.s2, B, S), d=f32(lay.d, B),
+                   a2=f32(lay.a2, B, A), at=f32(lay.at, B, A), api=f32(lay.api, B, A), y=f32(lay.y, B),
+                   ga=f32(lay.ga, B, A))
+        out["tape_pi"] = tape_view(self.acfg, B, buf, base + lay.tape_pi)
+        out["tape_target"] = tape_view(self.acfg, B, buf, base + lay.tape_target)
+        return out
 
 
 def replay_fill(n, obs_dim, act_dim, seed=0, rank=0, p_done=0.01, device="cuda") -> ReplayShard:

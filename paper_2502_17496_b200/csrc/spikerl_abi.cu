@@ -810,6 +810,21 @@ int spikerl_td3_update_pair(const spikerl_actor_cfg* acfg, const spikerl_critic_
   return SPIKERL_OK;
 }
 
+int spikerl_td3_workspace_layout(const spikerl_actor_cfg* acfg, const spikerl_critic_cfg* ccfg, int batch,
+                                 spikerl_td3_ws_layout* out) {
+  ActorDims ad;
+  CriticDims cd;
+  SPK_TRY(actor_dims(acfg, &ad));
+  SPK_TRY(critic_dims(ccfg, &cd));
+  if (!out || batch < 1) { set_error("spikerl_td3_workspace_layout: bad arguments"); return SPIKERL_E_ARG; }
+  const Td3Ws W = td3_ws_layout(ad, cd, batch);
+  out->s = W.s; out->a = W.a; out->r = W.r; out->s2 = W.s2; out->d = W.d; out->a2 = W.a2; out->at = W.at;
+  out->api = W.api; out->y = W.y; out->ga = W.ga; out->tape_pi = W.tape;
+  out->tape_target = W.actor_ws + actor_ws_layout(ad, batch).tape;
+  out->total = W.total;
+  return SPIKERL_OK;
+}
+
 size_t spikerl_td3_pair_workspace_bytes(const spikerl_actor_cfg* acfg, const spikerl_critic_cfg* ccfg, int batch) {
   return 2 * spikerl_td3_workspace_bytes(acfg, ccfg, batch);
 }

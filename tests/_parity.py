@@ -36,17 +36,35 @@ def run_gpu_actor(shape, B, p, s, g_a, engine="auto"):
     return out
 
 
+def near_fp32_midpoint(a64, ulps=2):
+    """True where the fp64 value lies within `ulps` fp64 ulps of a midpoint between two adjacent
+    fp32 values: only there may libm's and CUDA's fp64 exp (each within 1 ulp64) round to different
+    fp32 results."""
+    a64 = np.asarray(a64, np.float64)
+    lo = a64.astype(np.float32)
+    lo = np.where(lo.astype(np.float64) > a64, np.nextafter(lo, np.float32(-np.inf)), lo)
+    hi = np.nextafter(lo, np.float32(np.inf))
+    mid = (lo.astype(np.float64) + hi.astype(np.float64)) / 2.0
+    return np.abs(a64 - mid) <= ulps * np.spacing(np.abs(a64))
+
+
 def check_encoder(gpu, shape, p, s):
+    """Stimulation A and encoder spikes bit-exact (north_star). The only exemption is an element whose
+    fp64 value sits within 2 ulp64 of an fp32 rounding midpoint; there A may differ by 1 ulp32 and
+    that element's column of spikes is compared against the oracle's rule applied to the GPU's A.
+    Expected (and observed) exemption count: 0."""
     A_ref = oracle.gaussian_stim(s, p["mu"], p["sigma"])
     O0 = oracle.encode_spikes(A_ref, shape.T)
     diffA = gpu["A"].view(np.uint32).astype(np.int64) - A_ref.view(np.uint32).astype(np.int64)
-    # exemption: libm vs CUDA exp may differ by 1 ulp when the fp64 value sits on an fp32
-    # rounding midpoint (DESIGN.md parity protocol step 2); expected count 0
-    assert np.abs(diffA).max(initial=0) <= 1, "encoder stimulation differs by more than 1 ulp"
-    n_ex = int((diffA != 0).sum())
-    assert n_ex <= max(1, 1e-6 * diffA.size), n_ex
-    ok_cols = (diffA == 0)
-    assert np.array_equal(gpu["sp"]["o0"][:, ok_cols], O0[:, ok_cols]), "encoder spikes not bit-exact"
+    bad = diffA != 0
+    n_ex = int(bad.sum())
+    if n_ex:
+        assert np.abs(diffA).max() <= 1, "encoder stimulation differs by more than 1 ulp"
+        mid = near_fp32_midpoint(oracle.gaussian_stim_f64(s, p["mu"], p["sigma"]))
+        assert np.all(mid[bad]), "encoder stimulation differs away from an fp32 rounding midpoint"
+        O0_gpuA = oracle.encode_spikes(gpu["A"], shape.T)
+        assert np.array_equal(gpu["sp"]["o0"][:, bad], O0_gpuA[:, bad])
+    assert np.array_equal(gpu["sp"]["o0"][:, ~bad], O0[:, ~bad]), "encoder spikes not bit-exact"
     return n_ex
 
 
@@ -86,7 +104,8 @@ def check_actor(gpu, shape, p, s, g_a, grad_tol=None, act_tol=None):
         assert not np.any(mh & ~near_h), f"layer {l}: surrogate-mask disagreement away from the window edge"
     stats["spike_exempt"] = n_exempt
     stats["spikes"] = n_spk
-    assert n_exempt <= max(1e-5 * n_spk, 1.0), stats
+    # north_star: at most 1e-5 of the (oracle's) spikes, strictly (no rounding up to one)
+    assert n_exempt <= 1e-5 * n_spk, stats
     # actions: rows without free-running disagreement against the free oracle; all rows against the
     # oracle decoder applied to the GPU's own counts (= a_tf, decoder of forced O3)
     a = gpu["a"]

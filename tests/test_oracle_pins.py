@@ -512,3 +512,83 @@ def test_fp16_rne_laws():
     r = fp16(x)
     assert np.array_equal(fp16(r), r)                    # idempotent
     assert np.all(np.abs(r - x) <= np.maximum(np.abs(x) * 2.0 ** -11, 2.0 ** -25))
+
+
+# ------------------------------------------------------------------ R20: where the bf16 roundings sit
+def _r20_tape():
+    """A hand-made tape (the backward is a function of the tape): T = 2, one neuron
+    per layer, every hidden/output neuron fires at both steps with V = (0.6, 0.9) (inside the window,
+    h = 1), encoder spikes (0, 1) from A = RN32(exp(-1/2)) (s = 1, mu = 0, sigma = 1), a = 0.5, fr = 1."""
+    V = np.array([[[0.6]], [[0.9]]])
+    O = np.ones((2, 1, 1), np.uint8)
+    A = np.array([[np.float32(np.exp(-0.5))]], np.float32)
+    tape = dict(A=A, O0=np.array([[[0]], [[1]]], np.uint8), O=[O, O, O], V=[V, V, V],
+                a=np.array([[0.5]]), fr=np.array([[1.0]]), s=np.array([[1.0]], np.float32))
+    w = 1.0 + 2.0 ** -7 + 2.0 ** -9                      # exact in fp32, not in bf16
+    p = dict(mu=np.zeros((1, 1), np.float32), sigma=np.ones((1, 1), np.float32),
+             W1=np.full((1, 1), 0.75, np.float32), W2=np.full((1, 1), 0.7, np.float32),
+             W3=np.full((1, 1), 0.6, np.float32), Wd=np.full((1, 1), w, np.float32), bd=np.zeros(1, np.float32))
+    return p, tape
+
+
+def test_r20_actor_rounding_points_hand_worked():
+    """DESIGN.md R20 for the actor backward, by hand (g_a = 1, d_c = 0.5, rho = 0; o = 1 everywhere so
+    the d_v term vanishes):
+      g_pre = 1 (1 - 0.5^2) = 0.75; dWd = dbd = 0.75 (fr = 1; the decoder is never rounded)
+      g_o3 = 0.75 w / T = 0.375 w;  G3 = (g + d_c g, g) = (0.5625 w, 0.375 w) = (0.5679931640625, 0.378662109375)
+      bf16: RN(G3) = (0.56640625, 0.37890625)  [1.0010001|01101b x 2^-1 down; 1.1000001|111b x 2^-2 up]
+      dW3 = sum_t RN(G3_t) o2_t = 0.9453125        (unrounded G3 would give 0.9466552734375)
+      RN(W3 = 0.6f) = 0.6015625;  g_o2 = RN(G3) RN(W3) = (0.340728759765625, 0.227935791015625)
+      G2 = (g_o2[1] + 0.5 g_o2[2], g_o2[2]) = (0.4546966552734375, 0.227935791015625) -> RN (0.455078125, 0.2275390625)
+      dW2 = 0.6826171875;  RN(W2 = 0.7f) = 0.69921875;  g_o1 = RN(G2) RN(W2)
+      G1 = (0.3977489471435547, 0.15909957885742188) -> RN (0.3984375, 0.1591796875)
+      dW1 = RN(G1_2) o0_2 = 0.1591796875   (o0 = (0, 1))
+      encoder: RN(sum_t G1) = RN(0.5568485260009766) = 0.55859375 -- the SUM is rounded once (rounding
+      each G1_t first would give 0.5576171875); dL/dA = 0.55859375 RN(W1 = 0.75) = 0.4189453125;
+      dmu = dL/dA A (s - mu) / sigma^2 = 0.4189453125 RN32(exp(-1/2)) = dsigma (s - mu = sigma = 1)."""
+    p, tape = _r20_tape()
+    g = oracle.actor_backward(p, cfg_ns(T=2, precision="bf16"), tape, np.array([[1.0]]))
+    A = float(np.float32(np.exp(-0.5)))
+    assert g["Wd"][0, 0] == 0.75 and g["bd"][0] == 0.75
+    assert g["W3"][0, 0] == 0.9453125
+    assert g["W2"][0, 0] == 0.6826171875
+    assert g["W1"][0, 0] == 0.1591796875
+    assert g["mu"][0, 0] == 0.4189453125 * A and g["sigma"][0, 0] == 0.4189453125 * A
+    # fp32 mode: nothing rounded; dW3 = 0.9375 w exactly
+    g32 = oracle.actor_backward(p, cfg_ns(T=2, precision="fp32"), tape, np.array([[1.0]]))
+    assert g32["W3"][0, 0] == 0.9375 * (1.0 + 2.0 ** -7 + 2.0 ** -9)
+
+
+def test_r20_critic_rounding_points_hand_worked():
+    """DESIGN.md R20 for the critic, by hand: in = 2, one hidden unit per layer, x = [1 + 2^-9, 0.5],
+    W1 = [1, 1], W2 = w = 1 + 2^-7 + 2^-9, W3 = 1, biases 0, dL/dQ = 1 + 2^-9.
+      RN(x) = [1, 0.5] (2^-9 < half an ulp) -> z1 = 1.5 = h1;  RN(w) = 1.0078125;  z2 = 1.51171875
+      h2 = RN(z2) = 1.515625 (65.5/128: tie to even 66);  Q = 1.515625
+      dh2 = dQ W3 = 1 + 2^-9 -> dz2 = RN(.) = 1;  dz1 = RN(dz2 RN(w)) = 1.0078125;  dx = dz1 RN(W1)
+      dW3 = dQ h2 = 1.518585205078125;  db3 = dQ;  dW2 = dz2 h1 = 1.5;  db2 = 1
+      dW1 = dz1 RN(x) = [1.0078125, 0.50390625];  db1 = 1.0078125."""
+    w = 1.0 + 2.0 ** -7 + 2.0 ** -9
+    p = dict(W1=np.ones((1, 2), np.float32), b1=np.zeros(1, np.float32), W2=np.full((1, 1), w, np.float32),
+             b2=np.zeros(1, np.float32), W3=np.ones((1, 1), np.float32), b3=np.zeros(1, np.float32))
+    x = np.array([[1.0 + 2.0 ** -9, 0.5]])
+    q, cache = oracle.critic_forward(p, x, "bf16")
+    assert q[0] == 1.515625
+    dQ = 1.0 + 2.0 ** -9
+    g, dx = oracle.critic_backward(p, cache, np.array([dQ]), "bf16")
+    assert g["W3"][0, 0] == 1.518585205078125 and g["b3"][0] == dQ
+    assert g["W2"][0, 0] == 1.5 and g["b2"][0] == 1.0
+    assert np.array_equal(g["W1"], [[1.0078125, 0.50390625]]) and g["b1"][0] == 1.0078125
+    assert np.array_equal(dx, [[1.0078125, 1.0078125]])
+    # fp32 mode: x kept, Q = (1 + 2^-9 + 0.5) w
+    q32, _ = oracle.critic_forward(p, x, "fp32")
+    assert q32[0] == (1.5 + 2.0 ** -9) * w
+
+
+def test_encoder_exemption_condition():
+    """The parity protocol's encoder exemption (C-4 step 2) holds only within 2 ulp64 of an fp32
+    rounding midpoint."""
+    from tests._parity import near_fp32_midpoint
+    mid = 1.0 + 2.0 ** -24                                   # halfway between 1 and 1 + 2^-23
+    u = 2.0 ** -52
+    vals = np.array([mid, mid + 2 * u, mid - 2 * u, mid + 3 * u, 1.0, 0.75 + 2.0 ** -25, 0.6065306597126334])
+    assert near_fp32_midpoint(vals).tolist() == [True, True, True, False, False, True, False]
