@@ -1,16 +1,20 @@
 #!/usr/bin/env python
 """Benchmark of the SpikeRL hot path on B200 (contract: see DESIGN.md "Measurement").
 
-  python bench.py [--gpus N --steps K --warmup W] [--workload cfg1|cfg2|cfg3s|cfg3L|cfg4]
+  python bench.py [--gpus N --steps K --warmup W] [--workload cfg0|cfg1|cfg2|cfg3s|cfg3L|cfg4]
   python -m torch.distributed.run --nproc-per-node N ... bench.py --gpus N   (data parallel)
   python bench.py --impl reference      (the CPU oracle, timed on the host cores)
 
-One JSON line on rank 0. A "step" is one TD3 update (configs[1..3]: replay sample -> target
-actor -> target critics -> critic fwd/bwd -> allreduce -> Adam -> [delayed actor fwd/BPTT,
-allreduce, Adam, Polyak]) or, for cfg4, one actor forward + BPTT + gradient allreduce over the
-rank's shard. Inputs are device-resident when the timed region starts (replay shard filled on
-the device); `e2e` re-times the same step through the public API with the minibatch copied
-from pinned host memory and the losses read back every step.
+One JSON line on rank 0. The default workload is configs[4] (BASELINE.json's large-batch
+config, the largest that fits one GPU): a step is one actor forward + surrogate-gradient BPTT +
+gradient allreduce over the rank's shard of the 65 536-row global batch (strong scaling). The same
+line carries, under "td3", configs[3] at per-rank batch 4096 (the TD3 throughput regime, weak
+scaling): a step there is one TD3 update (replay sample -> target actor -> target critics -> critic
+fwd/bwd -> allreduce -> Adam -> [delayed actor fwd/BPTT, allreduce, Adam, Polyak]). Inputs are
+device-resident when the timed region starts; `e2e` re-times the same step through the public
+API with its inputs copied from pinned host memory and its result read back every step. The
+roofline kernel is timed live inside the timed region (event pairs around its launches on its own
+stream, recorded as graph event nodes).
 """
 from __future__ import annotations
 
@@ -38,7 +42,9 @@ def parse():
     ap.add_argument("--steps", type=int, default=200)
     ap.add_argument("--warmup", type=int, default=20)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--workload", default="cfg1", choices=["cfg1", "cfg2", "cfg3s", "cfg3L", "cfg4"])
+    ap.add_argument("--workload", default="cfg4", choices=["cfg0", "cfg1", "cfg2", "cfg3s", "cfg3L", "cfg4"])
+    ap.add_argument("--no-td3-extra", action="store_true", help="cfg4: skip the configs[3] B=4096 TD3 keys")
+    ap.add_argument("--eager", action="store_true", help="actor workloads: eager launches instead of a graph")
     ap.add_argument("--single-graphs", action="store_true",
                     help="TD3: replay one graph per update instead of overlapped update pairs")
     ap.add_argument("--engine", default="auto", choices=["auto", "simt", "tcgen05"])
@@ -240,8 +246,10 @@ def energy_window(run_step, sampler, seconds=1.5):
             "source": "nvml total energy counter, steps back to back after the timed region"}
 
 
-def time_steps(run_step, K, flush_buf, world):
-    """Per-step CUDA events on the launching stream; L2 flushed between steps (outside events)."""
+def time_steps(run_step, K, flush_buf, world, after_step=None):
+    """Per-step CUDA events on the launching stream; L2 flushed between steps (outside events).
+    after_step (optional) runs after each step's end event, outside the timed interval (the live
+    kernel watch synchronises there and reads its event pairs)."""
     import torch
     evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(K)]
     barrier(world)
@@ -251,22 +259,24 @@ def time_steps(run_step, K, flush_buf, world):
         evs[k][0].record()
         run_step(k)
         evs[k][1].record()
+        if after_step is not None:
+            after_step(k)
     torch.cuda.synchronize()
     barrier(world)
     total_ms = sum(a.elapsed_time(b) for a, b in evs)
     return max_over_ranks(total_ms, world)
 
 
-def dominant_kernel(summary, pk_peaks, long_step, clocks=None):
-    """Largest kernel of the step against its roofline. Tensor-bound kernels are judged against the
-    burst bf16 peak (cuBLAS 8192^3 at full clock), the stricter of the two measured figures: the
-    sustained one was measured at a ~1320 MHz median SM clock under the power cap, which the actor's
-    FWD L1 beats at the 1.8-1.97 GHz it holds, so a frac against it would read above 1. For a long
-    step whose sampled clock sagged below 95% of max, the sustained figure and the frac against it
-    are reported beside (`peak_sustained`, `frac_vs_sustained`) as context, not as the headline."""
-    from paper_2502_17496_b200 import _lib
+def dominant_kernel(summary, pk_peaks, live, timed_ms, clocks=None, long_step=False):
+    """The largest kernel of the step (by the profiling pass's launch list) against its roofline.
+    `live` = (launches, total_ms) of that kernel measured inside the timed region (Watch); the
+    algorithmic work per launch is the launcher's attribution (flops or bytes). Tensor-bound
+    kernels are judged against the burst bf16 peak (cuBLAS 8192^3 at full clock), the stricter of
+    the two measured figures; for a long step whose sampled clock sagged below 95% of max the
+    sustained figure and the frac against it are reported beside as context."""
     best = max(summary, key=lambda e: e["total_ms"])
-    avg_s = best["total_ms"] / best["launches"] / 1e3
+    n_live, ms_live = live
+    avg_s = ms_live / n_live / 1e3
     extra = {}
     if best["bound"] == "tensor":
         per = best["flops"] / best["launches"]
@@ -291,10 +301,13 @@ def dominant_kernel(summary, pk_peaks, long_step, clocks=None):
             traffic = json.load(f).get(best["name"])
     except Exception:
         pass
-    total = sum(e["total_ms"] for e in summary)
     return {"kernel": best["name"], "bound": bound, "achieved": round(ach, 3), "peak": peak, "unit": unit,
             "frac": round(ach / peak, 5), "traffic": traffic, "work_per_launch": per,
-            "avg_launch_us": round(avg_s * 1e6, 3), "share_of_step": round(best["total_ms"] / total, 4),
+            "avg_launch_us": round(avg_s * 1e6, 3), "launches_timed": n_live,
+            "timing": "live: CUDA event pair around every launch of this kernel inside the timed region, on its "
+                      "launch stream (graph event nodes); in a DAG with concurrent branches a launch's interval "
+                      "includes sharing the GPU with the kernels overlapping it",
+            "share_of_step": round(ms_live / max(timed_ms, 1e-12), 4),
             "peak_src": pk_peaks["src"] if bound != "alu" else "derived (guide: 148 SM x 128 lanes x 2 x 1.965 GHz)",
             "peak_kind": "burst" if bound == "tensor" else ("copy" if bound == "hbm" else "derived"), **extra}
 
@@ -341,54 +354,108 @@ def cpu_baseline_actor(name, B_sample=16, seconds=12.0):
 
 
 # ---------------------------------------------------------------------------------- ours
-def run_td3(args, rank, world):
+def _profile_pass(fn):
+    """Eager pass with CUDA events around every library launch: which kernel dominates and the
+    algorithmic work its launcher attributes to it (the timing itself is re-measured live)."""
+    import torch
+    from paper_2502_17496_b200 import _lib
+    torch.cuda.synchronize()
+    _lib.prof_enable(True)
+    fn()
+    torch.cuda.synchronize()
+    summ = _lib.prof_summary()
+    _lib.prof_enable(False)
+    return summ
+
+
+def _breakdown(summ):
+    return sorted([{k: (round(v, 4) if isinstance(v, float) else v) for k, v in e.items()} for e in summ],
+                  key=lambda e: -e["total_ms"])[:12]
+
+
+def _capture(fn):
+    import torch
+    s = torch.cuda.Stream()
+    s.wait_stream(torch.cuda.current_stream())
+    with torch.cuda.stream(s):
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g, stream=s):
+            fn()
+    torch.cuda.current_stream().wait_stream(s)
+    torch.cuda.synchronize()
+    return g
+
+
+def run_td3(args, rank, world, workload):
     import torch
     import paper_2502_17496_b200 as pk
     from paper_2502_17496_b200 import _lib
-    td3, shape, B = build_td3(args.workload, world, rank, args.engine, args.replay_size)
-    td3.capture()
+    td3, shape, B = build_td3(workload, world, rank, args.engine, args.replay_size)
     # updates 2j+1, 2j+2 as one overlapped graph (spikerl_td3_update_pair: bitwise the same state as
-    # the two single-update graphs, tested) unless --single-graphs
+    # two sequential updates, tested) unless --single-graphs
     pair = td3.hp.policy_delay == 2 and not args.single_graphs
-    if pair:
-        td3.capture_pair()
-    launches = {}
     lib = pk.lib()
-    for k in (1, 2):            # launches per phase, counted from an eager enqueue
-        lib.spikerl_launch_count(1)
-        td3.update(k)
-        launches[k % 2] = lib.spikerl_launch_count(1)
+    launches = {}
+
+    td3.update(1)                   # first launches (module loading, tensor maps) outside the profile
+    td3.update(2)
     if pair:
-        lib.spikerl_launch_count(1)
         td3.update_pair(3)
-        launches["pair"] = lib.spikerl_launch_count(1)
+
+    def prof_fn():
+        for k in (1, 2):            # launches per phase, counted from an eager enqueue
+            lib.spikerl_launch_count(1)
+            td3.update(k)
+            launches[k % 2] = lib.spikerl_launch_count(1)
+        if pair:
+            lib.spikerl_launch_count(1)
+            td3.update_pair(3)
+            launches["pair"] = lib.spikerl_launch_count(1)
+    summ = _profile_pass(prof_fn)
+    dom = max(summ, key=lambda e: e["total_ms"])["name"]
+    watch = _lib.Watch(dom, 64)
+    td3.capture()
+    if pair:
+        watch.arm()
+        td3.capture_pair()
+        per = watch.used()
+        _lib.Watch.off()
     torch.cuda.synchronize()
     flush = None if args.no_flush else torch.empty(64 * 1024 * 1024, dtype=torch.float32, device="cuda")  # 256 MB > L2
-    step0 = [4 if pair else 2]
+    step0 = [6 if pair else 2]
 
     def graph_step(k):
         td3.replay_graph(step0[0] + k)
 
-    for k in range(args.warmup):
-        graph_step(k)
-    step0[0] += args.warmup
-    if pair and step0[0] % 2 == 1:   # pairs start at an odd update
-        graph_step(0)
-        step0[0] += 1
+    if pair:
+        for k in range(max(1, args.warmup // 2)):
+            td3.replay_pair()
+        step0[0] += 2 * max(1, args.warmup // 2)
+    else:
+        for k in range(args.warmup):
+            graph_step(k)
+        step0[0] += args.warmup
     torch.cuda.synchronize()
     clk = ClockSampler(int(os.environ.get("LOCAL_RANK", "0")))
     clk.start()
+    live = None
     if pair:
         npair = args.steps // 2
-        total_ms = time_steps(lambda k: td3.replay_pair(), npair, flush, world) if npair else 0.0
+
+        def after(k):
+            torch.cuda.synchronize()
+            watch.collect(per)
+        total_ms = time_steps(lambda k: td3.replay_pair(), npair, flush, world, after_step=after) if npair else 0.0
+        step0[0] += 2 * npair
         if args.steps % 2:
-            step0[0] += 2 * npair
             total_ms += time_steps(graph_step, 1, flush, world)
-            step0[0] -= 2 * npair
+            step0[0] += 1
         gpu_launches = npair * launches["pair"] + (launches[1] if args.steps % 2 else 0)
+        live = (watch.launches, watch.total_ms)
     else:
         total_ms = time_steps(graph_step, args.steps, flush, world)
         gpu_launches = sum(launches[(step0[0] + k) % 2] for k in range(args.steps))
+        step0[0] += args.steps
     clocks = clk.stop()
     secs = total_ms / 1e3
     value = args.steps * B * world / secs
@@ -397,7 +464,7 @@ def run_td3(args, rank, world):
            "scaling": "weak", "vs_baseline": None, "dtype": "bf16" if shape.precision == "bf16" else "f32",
            "data": "synthetic (device-resident replay shard filled with Philox; configs[1] distributions)",
            "updates_per_s": round(args.steps / secs, 3),
-           "config": {"workload": f"{args.workload}: TD3 update, spiking actor obs {shape.obs_dim} act "
+           "config": {"workload": f"{workload}: TD3 update, spiking actor obs {shape.obs_dim} act "
                                   f"{shape.act_dim} pop 10/10 hidden {shape.n1}-{shape.n2} T={shape.T}, twin critics "
                                   f"{shape.obs_dim + shape.act_dim}->256->256->1",
                       "global_batch": B * world, "per_rank_batch": B, "replay_per_rank": args.replay_size,
@@ -407,7 +474,6 @@ def run_td3(args, rank, world):
                       if flush is not None else "not flushed", "cuda_graph": True,
                       "graph": "update pairs (k odd, k + 1 overlapped)" if pair else "one graph per update"},
            "clocks": clocks, "gpu_launches": int(gpu_launches)}
-    step0[0] += args.steps
     if pair and step0[0] % 2 == 0:
         en = energy_window(lambda k: td3.replay_pair(), clk)   # each call = two updates
         if en:
@@ -422,16 +488,13 @@ def run_td3(args, rank, world):
     # e2e: minibatch from pinned host memory every step + loss read-back, through the public API
     if not args.no_e2e:
         out["e2e"] = e2e_td3(args, rank, world, td3, shape, B, pair=pair)
-    # roofline: eager profiling pass (CUDA events around every launch on its own stream)
-    _lib.prof_enable(True)
-    for k in range(8):
-        td3.update(step0[0] + k)
-    torch.cuda.synchronize()
-    summ = _lib.prof_summary()
-    _lib.prof_enable(False)
-    out["roofline"] = dominant_kernel(summ, peaks(), long_step=False)
-    out["kernel_breakdown"] = sorted([{k: (round(v, 4) if isinstance(v, float) else v) for k, v in e.items()}
-                                      for e in summ], key=lambda e: -e["total_ms"])[:12]
+    if live is None:   # --single-graphs (diagnostic): no live watch; the eager profiling pass stands in
+        d = [e for e in summ if e["name"] == dom][0]
+        live = (d["launches"], d["total_ms"])
+    out["roofline"] = dominant_kernel(summ, peaks(), live, total_ms)
+    if not pair:
+        out["roofline"]["timing"] = "eager profiling pass (events around every launch); --single-graphs diagnostic"
+    out["kernel_breakdown"] = _breakdown(summ)
     return out
 
 
@@ -530,15 +593,18 @@ def e2e_td3(args, rank, world, td3_dev, shape, B, pair=False):
             "path": path}
 
 
-def run_actor(args, rank, world):
-    """cfg4: actor forward + BPTT + gradient allreduce over the rank's shard (strong scaling)."""
+def run_actor(args, rank, world, workload):
+    """configs[4]: actor forward + BPTT + gradient allreduce over the rank's shard of the 65 536-row
+    global batch (strong scaling); configs[0]: the fp32 actor forward + backward at B = 100 per rank
+    (weak scaling). The step is captured as one CUDA graph (NCCL call included) unless --eager."""
     import numpy as np
     import torch
     import synthgen as sg
     import paper_2502_17496_b200 as pk
     from paper_2502_17496_b200 import _lib
-    shape, _, Bg = sg.preset("cfg4")
-    B = Bg // world
+    shape, _, Bg = sg.preset(workload)
+    strong = workload == "cfg4"
+    B = Bg // world if strong else Bg
     actor = pk.SpikingActor(pk.actor_cfg_from(shape, engine=args.engine), B)
     rng = np.random.default_rng(0)
     actor.load(sg.actor_params(shape, rng))
@@ -550,59 +616,105 @@ def run_actor(args, rank, world):
     obs = torch.clamp(torch.randn(B, shape.obs_dim, device="cuda", generator=g), -5, 5)
     ga = torch.randn(B, shape.act_dim, device="cuda", generator=g)
 
-    def step(k):
+    def step(k=0):
         actor.forward(obs)
         actor.backward(obs, ga)
         if comm:
             comm.allreduce_mean(actor.grads)
 
-    for k in range(args.warmup):
-        step(k)
     lib = pk.lib()
+    step()                          # first launches (module loading, tensor maps) outside the profile
+    summ = _profile_pass(step)
+    dom = max(summ, key=lambda e: e["total_ms"])["name"]
     lib.spikerl_launch_count(1)
+    step()
+    n_launch = lib.spikerl_launch_count(1)
+    watch = _lib.Watch(dom, 16)
+    if args.eager:
+        def run(k):
+            watch.arm()
+            step(k)
+        per = None
+    else:
+        watch.arm()
+        graph = _capture(step)
+        per = watch.used()
+        _lib.Watch.off()
+
+        def run(k):
+            graph.replay()
+    for k in range(args.warmup):
+        run(k)
+    torch.cuda.synchronize()
+    flush = None if (strong or args.no_flush) else torch.empty(64 * 1024 * 1024, dtype=torch.float32, device="cuda")
+
+    def after(k):
+        torch.cuda.synchronize()
+        watch.collect(per if per is not None else watch.used())
     clk = ClockSampler(int(os.environ.get("LOCAL_RANK", "0")))
     clk.start()
-    total_ms = time_steps(step, args.steps, None, world)
+    total_ms = time_steps(run, args.steps, flush, world, after_step=after)
     clocks = clk.stop()
-    n_launch = lib.spikerl_launch_count(1)
+    _lib.Watch.off()
     secs = total_ms / 1e3
-    out = {"metric": METRIC, "value": round(args.steps * Bg / secs, 2), "unit": "samples/s", "n_gpus": world,
+    gsum = Bg if strong else B * world
+    out = {"metric": METRIC, "value": round(args.steps * gsum / secs, 2), "unit": "samples/s", "n_gpus": world,
            "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(total_ms / args.steps, 4),
-           "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "bf16",
+           "higher_is_better": True, "scaling": "strong" if strong else "weak", "vs_baseline": None,
+           "dtype": "bf16" if shape.precision == "bf16" else "f32",
            "data": "synthetic observations ~N(0,1) clipped +-5, upstream grads ~N(0,1)",
-           "config": {"workload": "cfg4: spiking actor fwd+BPTT (+allreduce), obs 376 act 17 pop 10/10 hidden "
-                                  "1024-1024 T=16", "global_batch": Bg, "per_rank_batch": B,
+           "config": {"workload": f"{workload}: spiking actor fwd+BPTT (+allreduce), obs {shape.obs_dim} act "
+                                  f"{shape.act_dim} pop 10/10 hidden {shape.n1}-{shape.n2} T={shape.T} "
+                                  f"{shape.precision}", "global_batch": gsum, "per_rank_batch": B,
                       "parallelism": f"dp{world}", "engine": args.engine,
-                      "l2": "inputs and tape (GBs) exceed L2"},
-           "clocks": clocks, "gpu_launches": int(n_launch)}
-    en = energy_window(step, clk)
+                      "cuda_graph": not args.eager,
+                      "l2": "inputs and tape (GBs) exceed L2" if strong else
+                      ("flushed between timed steps (256 MB read, outside the events)" if flush is not None
+                       else "not flushed")},
+           "clocks": clocks, "gpu_launches": int(n_launch) * args.steps}
+    en = energy_window(run, clk)
     if en:
         en["joules_per_step"] = round(en["joules"] / en["steps"], 5)
-        en["samples_per_joule"] = round(en["steps"] * Bg / max(en["joules"], 1e-9), 1)
+        en["samples_per_joule"] = round(en["steps"] * gsum / max(en["joules"], 1e-9), 1)
         out["energy"] = en
-    _lib.prof_enable(True)
-    step(0)
-    torch.cuda.synchronize()
-    summ = _lib.prof_summary()
-    _lib.prof_enable(False)
-    out["roofline"] = dominant_kernel(summ, peaks(), long_step=True, clocks=clocks)
-    out["kernel_breakdown"] = sorted([{k: (round(v, 4) if isinstance(v, float) else v) for k, v in e.items()}
-                                      for e in summ], key=lambda e: -e["total_ms"])[:12]
-    out["hbm_kernels"] = hbm_kernels(actor, summ)
+    out["roofline"] = dominant_kernel(summ, peaks(), (watch.launches, watch.total_ms), total_ms, long_step=strong,
+                                      clocks=clocks)
+    out["kernel_breakdown"] = _breakdown(summ)
+    if strong:
+        out["hbm_kernels"] = hbm_kernels(actor, summ)
     if not args.no_e2e:
-        host_obs = obs.cpu().pin_memory(); host_ga = ga.cpu().pin_memory()
-        grads_host = torch.empty(actor.n_params, dtype=torch.float32).pin_memory()
-
-        def e2e_step(k):
-            obs.copy_(host_obs, non_blocking=True); ga.copy_(host_ga, non_blocking=True)
-            step(k)
-            grads_host.copy_(actor.grads, non_blocking=True)
-        total = time_steps(e2e_step, max(3, args.steps // 4), None, world)
-        n = max(3, args.steps // 4)
-        out["e2e"] = {"value": round(n * Bg / (total / 1e3), 2), "unit": "samples/s",
-                      "h2d_bytes_per_step": B * (shape.obs_dim + shape.act_dim) * 4,
-                      "d2h_bytes_per_step": actor.n_params * 4}
+        out["e2e"] = e2e_actor(args, world, actor, step, obs, ga, gsum, shape)
     return out
+
+
+def e2e_actor(args, world, actor, step, obs, ga, gsum, shape):
+    """End to end through the public API: every step copies its observations and upstream action
+    gradients from pinned host memory and reads the parameter gradients back into pinned host
+    memory; one captured graph of [H2D, H2D -> forward -> backward (-> allreduce) -> D2H]."""
+    import torch
+    host_obs = obs.cpu().pin_memory()
+    host_ga = ga.cpu().pin_memory()
+    grads_host = torch.empty(actor.n_params, dtype=torch.float32).pin_memory()
+
+    def e2e_step(k=0):
+        obs.copy_(host_obs, non_blocking=True)
+        ga.copy_(host_ga, non_blocking=True)
+        step(k)
+        grads_host.copy_(actor.grads, non_blocking=True)
+    if args.eager:
+        run = e2e_step
+    else:
+        g = _capture(e2e_step)
+        run = lambda k: g.replay()
+    n = max(3, args.steps // 2)
+    for k in range(max(1, args.warmup // 2)):
+        run(k)
+    total = time_steps(run, n, None, world)
+    B = obs.shape[0]
+    return {"value": round(n * gsum / (total / 1e3), 2), "unit": "samples/s",
+            "h2d_bytes_per_step": B * (shape.obs_dim + shape.act_dim) * 4, "d2h_bytes_per_step": actor.n_params * 4,
+            "path": ("graph" if not args.eager else "eager") + " of [H2D obs + upstream grads from pinned host -> "
+                    "spikerl_actor_forward -> spikerl_actor_backward (-> allreduce) -> D2H of the gradients]"}
 
 
 def hbm_kernels(actor, summ, reps=20):
@@ -655,12 +767,17 @@ def main():
         return reference(args)
     import torch
     rank, world, local = dist_init(args)
-    if args.workload == "cfg4":
-        out = run_actor(args, rank, world)
+    if args.workload in ("cfg0", "cfg4"):
+        out = run_actor(args, rank, world, args.workload)
+        if args.workload == "cfg4" and not args.no_td3_extra:
+            # configs[3] at per-rank batch 4096: the TD3 updates/s throughput regime (weak scaling)
+            td = run_td3(args, rank, world, "cfg3L")
+            td.pop("metric", None)
+            out["td3"] = td
         if rank == 0 and world == 1 and not args.no_cpu_baseline:
-            out["cpu_baseline"] = cpu_baseline_actor("cfg4")
+            out["cpu_baseline"] = cpu_baseline_actor(args.workload, B_sample=16 if args.workload == "cfg4" else 100)
     else:
-        out = run_td3(args, rank, world)
+        out = run_td3(args, rank, world, args.workload)
         if rank == 0 and world == 1 and not args.no_cpu_baseline:
             out["cpu_baseline"] = cpu_baseline_td3(args.workload)
     if rank == 0:
@@ -672,7 +789,8 @@ def main():
 
 
 def reference(args):
-    """The oracle, as it stands, on the host cores: same metric/unit/config as our arm."""
+    """The oracle, as it stands, on the host cores: same metric/unit/config as our arm. Exactly
+    --warmup untimed steps, then up to --steps timed steps (stops early at a time budget and says so)."""
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
@@ -682,15 +800,17 @@ def reference(args):
     name = args.workload
     shape, cs, B = sg.preset(name)
     rng = np.random.default_rng(0)
-    if name == "cfg4":
+    if name in ("cfg0", "cfg4"):
         p = sg.actor_params(shape, rng)
-        Bs = 8
+        Bs = 8 if name == "cfg4" else B
 
         def step(k):
             s = sg.observations(rng, Bs, shape.obs_dim)
             a, tape = oracle.actor_forward(p, shape, s)
             oracle.actor_backward(p, shape, tape, sg.action_grads(rng, Bs, shape.act_dim))
-        per_step, sample = Bs, f"each step = {Bs} rows of cfg4 actor fwd+BPTT (value extrapolates linearly in B)"
+        per_step = Bs
+        sample = (f"each step = {Bs} rows of cfg4 actor fwd+BPTT (value extrapolates linearly in B)" if name == "cfg4"
+                  else f"each step = the full cfg0 batch of {B} rows, actor fwd+BPTT")
     else:
         st = [oracle.init_state(sg.actor_params(shape, rng), sg.critic_params(cs, rng), sg.critic_params(cs, rng))]
         hp = sg.TD3Hyper()
@@ -701,7 +821,7 @@ def reference(args):
         per_step, sample = B, f"each step = one full TD3 update of {name} at B={B}"
     budget = 150.0
     t_start = time.time()
-    for k in range(min(args.warmup, 3)):
+    for k in range(args.warmup):
         step(k)
     t0 = time.time()
     done = 0
@@ -714,8 +834,8 @@ def reference(args):
     v = done * per_step / dt
     cores = len(os.sched_getaffinity(0))
     out = {"impl": "reference", "metric": METRIC, "value": round(v, 3), "unit": "samples/s", "n_gpus": args.gpus,
-           "steps": done, "warmup": min(args.warmup, 3), "ms_per_step": round(dt / done * 1e3, 3),
-           "higher_is_better": True, "scaling": "weak" if name != "cfg4" else "strong", "vs_baseline": None,
+           "steps": done, "warmup": args.warmup, "ms_per_step": round(dt / done * 1e3, 3),
+           "higher_is_better": True, "scaling": "weak" if name not in ("cfg4",) else "strong", "vs_baseline": None,
            "dtype": "f64", "data": "synthetic", "config": {"workload": name, "per_rank_batch": B},
            "cpu_baseline": {"value": round(v, 3), "unit": "samples/s", "cores": cores, "kind": "oracle",
                             "sample": sample + (f"; stopped after {done} of {args.steps} steps (time budget)"

@@ -332,6 +332,14 @@ typedef struct {
 } spikerl_prof_entry;
 void spikerl_prof_enable(int on);
 int spikerl_prof_summary(spikerl_prof_entry* out, int max_entries);
+/* Live watch of one kernel inside a timed region (bench.py's roofline): every launch named `name`
+ * (the names spikerl_prof_summary reports) is bracketed by the next caller-owned event pair
+ * (cudaEvent_t created with timing), ev_begin[i] / ev_end[i], i = 0..n-1, recorded on the stream
+ * the kernel is launched on; inside a stream capture the records become event nodes of the graph,
+ * re-recorded at every replay. name == NULL turns the watch off. watch_count() = pairs used since
+ * the last spikerl_prof_watch (re-arming resets it). */
+int spikerl_prof_watch(const char* name, void* const* ev_begin, void* const* ev_end, int n);
+int spikerl_prof_watch_count(void);
 
 #ifdef __cplusplus
 }

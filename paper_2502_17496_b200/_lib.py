@@ -84,6 +84,39 @@ def prof_enable(on: bool):
     lib().spikerl_prof_enable(1 if on else 0)
 
 
+class Watch:
+    """Live timing of one named kernel inside a timed region (spikerl_prof_watch): up to n launches
+    per arming, each bracketed by its own timing-event pair on the stream it is launched on."""
+
+    def __init__(self, name: str, n: int):
+        import torch
+        self.name, self.n = name, n
+        self.ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(n)]
+        for a, b in self.ev:   # torch creates the CUDA event lazily, at its first record
+            a.record()
+            b.record()
+        torch.cuda.synchronize()
+        self.total_ms, self.launches = 0.0, 0
+
+    def arm(self):
+        b = (P * self.n)(*[C.c_void_p(e[0].cuda_event) for e in self.ev])
+        e = (P * self.n)(*[C.c_void_p(x[1].cuda_event) for x in self.ev])
+        check(lib().spikerl_prof_watch(self.name.encode(), b, e, self.n), "prof_watch")
+
+    def used(self) -> int:
+        return lib().spikerl_prof_watch_count()
+
+    @staticmethod
+    def off():
+        lib().spikerl_prof_watch(None, None, None, 0)
+
+    def collect(self, k: int):
+        """Add the durations of the first k pairs (their launches have completed: call after a sync)."""
+        for a, b in self.ev[:k]:
+            self.total_ms += a.elapsed_time(b)
+        self.launches += k
+
+
 def prof_summary():
     n = lib().spikerl_prof_summary(None, 0)
     if n < 0:
@@ -139,6 +172,8 @@ _SIGS = {
     "spikerl_launch_count": (LL, [I]),
     "spikerl_prof_enable": (None, [I]),
     "spikerl_prof_summary": (I, [P, I]),
+    "spikerl_prof_watch": (I, [C.c_char_p, C.POINTER(P), C.POINTER(P), I]),
+    "spikerl_prof_watch_count": (I, []),
 }
 EXPORTS = tuple(_SIGS)
 

@@ -210,6 +210,7 @@ enum ProfBound { PB_HBM = 0, PB_TENSOR = 1, PB_ALU = 2, PB_LATENCY = 3 };
 bool prof_on();
 struct ProfScope {
   int slot = -1;
+  int wslot = -1;   // live watch (spikerl_prof_watch): index of the event pair around this launch
   cudaStream_t st;
   ProfScope(const char* name, int bound, double flops, double bytes, cudaStream_t s);
   ~ProfScope();

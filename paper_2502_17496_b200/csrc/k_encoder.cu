@@ -3,112 +3,211 @@
 //   PAPER.md:131 (§III-A "populations use Gaussian distributions to transform continuous input
 //   values into spike trains"); north_star ("deterministic soft-reset encoder spikes");
 //   SPEC.md:123-140; R4 (fp64 exponent, RNE to fp32, no FTZ) and R5 (acc >= 1).
-// A warp owns 32 consecutive encoder neurons k, so one __ballot_sync per timestep yields exactly
-// one u32 word of bits0[t][b][:]. Each thread keeps its neuron's constants (obs index, mu, the
-// fp64 2 sigma^2) in registers and walks a strided set of batch rows, prefetching the next
-// observation, so the grid is a few blocks per SM instead of one block per (b, 128 neurons).
+//
+// Design. A thread owns one encoder neuron k (its constants mu, den = 2 sigma^2 and 1/den stay in
+// registers) and a warp 32 consecutive neurons, i.e. one u32 word of every bits0[t][b] row; a
+// block of 8 warps owns 256 neurons and walks tiles of R batch rows:
+//   1. every element: A = RN32(exp(-(q/den))) in fp64 (Markstein-corrected quotient from the
+//      hoisted reciprocal), stored coalesced;
+//   2. the accumulate-and-fire loop (R5) runs only for the elements that can fire at all. With the
+//      paper's receptive fields (sigma = 0.15 against a mu spacing of 0.667) about 90% of the
+//      elements have A < 1/T, yet every warp of 32 consecutive neurons holds a few that do not, so
+//      a per-row loop over the warp (one ballot per step) paid the T steps for all 32 lanes. Instead
+//      each warp queues its (row, lane, A) candidates in shared memory and then runs the loop with
+//      one candidate per lane, OR-ing the spikes into its own words of the tile (shared atomics);
+//   3. the tile's words leave with full 32-byte sectors (the 8 warps' words of one (t, row) are
+//      adjacent).
+// No-fire bound (conservative, so skipping is exact): no spike at any t <= T when
+// A < thr = 1 / (T (1 + T 2^-22)): the fp32 accumulator after t steps without a spike is at most
+// t A (1 + 2^-24)^t < 1.
 #include "internal.h"
 
 namespace spk {
 
-// TT > 0: T == TT known at compile time (T <= 32), the time loop fully unrolled: per step one
-// FADD, FSETP, predicated FADD, VOTE and a lane select (ncu r01: the runtime-T loop cost 14
-// instructions per step and 59% of the kernel; a lane-0 shared-memory variant measured slower).
-// TT == 0: any T, in chunks of 32 steps.
-template <int TT>
-__global__ void __launch_bounds__(256) enc_fwd_kernel(int B, int S, int E, int K0, int W0, int T,
-                                                      const float* __restrict__ obs,
-                                                      const float* __restrict__ mu,
-                                                      const float* __restrict__ sigma,
-                                                      float* __restrict__ A_out,
-                                                      uint32_t* __restrict__ bits0) {
-  pdl_wait();
-  pdl_trigger();
-  const int k = blockIdx.y * blockDim.x + threadIdx.x;
-  const int lane = threadIdx.x & 31;
-  if ((k >> 5) >= W0) return;   // whole warp past the padded width
+namespace {
+constexpr int kEncThreads = 256;   // = neurons per tile (8 warps, 8 words)
+constexpr int kEncWarps = kEncThreads / 32;
+
+// dynamic shared memory for R rows and T steps: bit words [T][R][8] + per-warp queues of R*32
+// (entry = row << 5 | lane as u16, and the element's A)
+inline size_t enc_smem_bytes(int R, int T) {
+  return (size_t)T * R * kEncWarps * 4 + (size_t)kEncWarps * R * 32 * (4 + 2);
+}
+}  // namespace
+
+// exp(-z) in fp64 for 0 <= z <= 110 (within one ulp of libm's exp over the encoder's range, checked
+// bit-for-bit after the RNE to fp32 by the encoder parity tests). z = n ln2 - r with n = round(z / ln2)
+// (the 1.5 * 2^52 shifter), r from a two-part ln2 (Cody-Waite; ln2_hi has 21 trailing zero bits so
+// n ln2_hi is exact), exp(r) by the degree-13 Taylor polynomial in Horner form (|r| <= ln2/2: the
+// remainder is below 5e-18), 2^-n added to the exponent (the result stays a normal double). The
+// coefficients come from the constant bank (no per-use register materialisation); the library exp
+// spent ~35 instructions per element on range checks this range never needs.
+__constant__ double kExpC[12] = {
+    1.6059043836821613e-10, 2.08767569878681e-09, 2.505210838544172e-08, 2.755731922398589e-07,
+    2.7557319223985893e-06, 2.48015873015873e-05,  0.0001984126984126984, 0.001388888888888889,
+    0.008333333333333333,   0.041666666666666664,  0.16666666666666666,   0.5};
+__device__ __forceinline__ double exp_neg(double z) {
+  z = fmin(z, 110.0);                                               // exp(-110) still rounds to fp32 0
+  const double t = __fma_rn(-z, 1.4426950408889634, 6755399441055744.0);
+  const double nd = __dsub_rn(t, 6755399441055744.0);               // round(-z / ln2), exactly
+  double r = __fma_rn(nd, -0x1.62e42fee00000p-1, -z);              // -z - n ln2_hi (exact)
+  r = __fma_rn(nd, -0x1.a39ef35793c76p-33, r);                      //   - n ln2_lo
+  double p = kExpC[0];
+#pragma unroll
+  for (int j = 1; j < 12; ++j) p = __fma_rn(p, r, kExpC[j]);
+  p = __fma_rn(p, r, 1.0);
+  p = __fma_rn(p, r, 1.0);
+  return __longlong_as_double(__double_as_longlong(p) + ((long long)__double2loint(t) << 52));
+}
+
+// TT > 0: T == TT at compile time (unrolled accumulate-and-fire); TT == 0: runtime T. RR rows per
+// tile (compile time: the tile index math is shifts).
+template <int TT, int RR>
+__global__ void __launch_bounds__(kEncThreads) enc_fwd_kernel(int B, int S, int E, int K0, int W0, int T,
+                                                              float thr, const float* __restrict__ obs,
+                                                              const float* __restrict__ mu,
+                                                              const float* __restrict__ sigma,
+                                                              float* __restrict__ A_out,
+                                                              uint32_t* __restrict__ bits0) {
+  extern __shared__ __align__(16) unsigned char esm[];
+  const int Tn = TT > 0 ? TT : T;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int nw = Tn * RR * kEncWarps;                                              // words of a tile
+  uint32_t* w_sh = reinterpret_cast<uint32_t*>(esm);                               // [T][RR][8]
+  float* qA = reinterpret_cast<float*>(w_sh + nw) + warp * RR * 32;                // per-warp queue
+  uint16_t* qe = reinterpret_cast<uint16_t*>(reinterpret_cast<float*>(w_sh + nw) + kEncWarps * RR * 32) +
+                 warp * RR * 32;
+  const uint32_t lt = (1u << lane) - 1u;
+  const int k = blockIdx.y * kEncThreads + tid;
   const bool kv = k < K0;
   const int i = kv ? k / E : 0;
+  const int w0 = blockIdx.y * kEncWarps;
+  const int tstep = gridDim.x * RR;
+  pdl_wait();     // mu / sigma may have just been written by the optimiser
+  pdl_trigger();
+  // per-neuron constants (fp64, as the oracle's op sequence R4): den = 2 sigma^2 and its reciprocal
   const double m = kv ? (double)__ldg(mu + k) : 0.0;
   const double sg = kv ? (double)__ldg(sigma + k) : 1.0;
   const double den = __dmul_rn(2.0, __dmul_rn(sg, sg));
-  // q / den as a correctly rounded quotient from the hoisted correctly rounded reciprocal:
-  // q0 = RN(q inv) is within one ulp, r = q - den q0 is exact (FMA), RN(q0 + r inv) = RN(q / den)
-  // (Markstein). Same value as __ddiv_rn(q, den) (the bit-exact encoder tests pin it against the
-  // oracle's IEEE division) at 3 instead of ~12 double operations per element.
   const double inv = __ddiv_rn(1.0, den);
-  const size_t tstride = (size_t)B * W0;
-  const size_t arow = (size_t)gridDim.x * K0, brow = (size_t)gridDim.x * W0;   // per-iteration strides
-  int b = blockIdx.x;
-  float* ap = A_out + (size_t)b * K0 + k;
-  uint32_t* out = bits0 + (size_t)b * W0 + (k >> 5) + (size_t)lane * tstride;
-  float s_next = (kv && b < B) ? __ldg(obs + (size_t)b * S + i) : 0.f;
-  for (; b < B; b += gridDim.x, ap += arow, out += brow) {
-    const float s = s_next;
-    const int bn = b + gridDim.x;
-    if (kv && bn < B) s_next = __ldg(obs + (size_t)bn * S + i);
-    float A = 0.0f;
-    if (kv) {
-      const double dd = __dsub_rn((double)s, m);
-      const double q = __dmul_rn(dd, dd);
-      const double q0 = __dmul_rn(q, inv);
-      const double r = __fma_rn(-q0, den, q);
-      A = (float)exp(-__fma_rn(r, inv, q0));  // RNE double -> float
-      *ap = A;
-    }
-    float acc = 0.0f;
-    if constexpr (TT > 0) {
-      // lane t keeps the ballot word of timestep t; one store instruction for all T words
-      uint32_t mine = 0;
+  for (int b0 = blockIdx.x * RR; b0 < B; b0 += tstep) {
+    for (int j = tid; j < nw / 4; j += kEncThreads) reinterpret_cast<uint4*>(w_sh)[j] = make_uint4(0u, 0u, 0u, 0u);
+    // the tile's observation values, requested together (rows past B read row B - 1: never used)
+    float sv[RR];
+    const float* op = obs + i;
 #pragma unroll
-      for (int t = 0; t < TT; ++t) {
-        acc = __fadd_rn(acc, A);
-        const bool fire = acc >= 1.0f;
-        if (fire) acc = __fsub_rn(acc, 1.0f);
-        const uint32_t w = __ballot_sync(0xffffffffu, fire);
-        mine = (lane == t) ? w : mine;
+    for (int r = 0; r < RR; ++r) sv[r] = __ldg(op + (size_t)min(b0 + r, B - 1) * S);
+    __syncthreads();   // zeroed words; the previous tile's words have been written out
+    // ---- 1. stimulation A for every element of the tile, candidates queued per warp
+    int cnt = 0;
+    float* ap = A_out + (size_t)b0 * K0 + k;
+#pragma unroll
+    for (int r = 0; r < RR; ++r, ap += K0) {
+      const bool live = kv && b0 + r < B;
+      float A = 0.0f;
+      if (live) {
+        const double dd = __dsub_rn((double)sv[r], m);
+        const double q = __dmul_rn(dd, dd);
+        // q / den as a correctly rounded quotient from the correctly rounded reciprocal:
+        // q0 = RN(q inv) is within one ulp, r = q - den q0 is exact (FMA), RN(q0 + r inv) = RN(q / den)
+        // (Markstein); the bit-exact encoder tests pin it against the oracle's IEEE division
+        const double q0 = __dmul_rn(q, inv);
+        const double rr = __fma_rn(-q0, den, q);
+        A = (float)exp_neg(__fma_rn(rr, inv, q0));   // RNE double -> float
+        *ap = A;
       }
-      if (lane < TT) *out = mine;
-    } else {
-      for (int t0 = 0; t0 < T; t0 += 32) {
-        const int n = T - t0 < 32 ? T - t0 : 32;
-        uint32_t mine = 0;
-        for (int j = 0; j < n; ++j) {
-          acc = __fadd_rn(acc, A);
-          const bool fire = acc >= 1.0f;
-          if (fire) acc = __fsub_rn(acc, 1.0f);
-          const uint32_t w = __ballot_sync(0xffffffffu, fire);
-          mine = (lane == j) ? w : mine;
+      const bool cand = A >= thr;
+      const uint32_t bal = __ballot_sync(0xffffffffu, cand);
+      if (cand) {
+        const int j = cnt + __popc(bal & lt);
+        qA[j] = A;
+        qe[j] = (uint16_t)((r << 5) | lane);
+      }
+      cnt += __popc(bal);
+    }
+    __syncwarp();
+    // ---- 2. accumulate-and-fire (R5: fp32 acc += A; spike iff acc >= 1; acc -= 1), one candidate
+    // per lane; each spike is OR-ed into its (t, row) word of the warp
+    for (int j = lane; j < cnt; j += 32) {
+      const float A = qA[j];
+      const int e = qe[j];
+      const uint32_t bit = 1u << (e & 31);
+      uint32_t* wp = w_sh + (e >> 5) * kEncWarps + warp;   // + step * RR * 8
+      float acc = 0.0f;
+#pragma unroll
+      for (int st = 0; st < (TT > 0 ? TT : 1); ++st) {
+        if (TT == 0) break;
+        acc = __fadd_rn(acc, A);
+        if (acc >= 1.0f) {
+          acc = __fsub_rn(acc, 1.0f);
+          atomicOr(wp + st * RR * kEncWarps, bit);
         }
-        if (lane < n) out[(size_t)t0 * tstride] = mine;
+      }
+      if constexpr (TT == 0) {
+        for (int st = 0; st < Tn; ++st) {
+          acc = __fadd_rn(acc, A);
+          if (acc >= 1.0f) {
+            acc = __fsub_rn(acc, 1.0f);
+            atomicOr(wp + st * RR * kEncWarps, bit);
+          }
+        }
+      }
+    }
+    __syncthreads();
+    // ---- 3. the tile's bit words: the 8 words of one (t, row) are one 32-byte sector, written as
+    // two 16-byte stores (W0 = P0 / 32 and w0 are multiples of 4 words)
+    {
+      const int q = tid & 1, r = (tid >> 1) % RR;   // this thread's quarter-sector and row
+      const int b = b0 + r;
+      if (b < B && w0 + 4 * q < W0) {
+        uint4* gp = reinterpret_cast<uint4*>(bits0 + ((size_t)b * W0 + w0 + 4 * q));
+        const size_t gstep = (size_t)B * W0 / 4;          // one step t, in uint4
+        constexpr int kPer = 2 * RR;                     // threads per step
+        for (int st = tid / kPer; st < Tn; st += kEncThreads / kPer)
+          gp[(size_t)st * gstep] = reinterpret_cast<const uint4*>(w_sh)[(st * RR + r) * 2 + q];
       }
     }
   }
 }
 
-template <int TT>
-static void enc_launch(dim3 grid, cudaStream_t st, const ActorDims& d, int B, const float* obs, const float* mu,
-                       const float* sigma, float* A, uint32_t* bits0) {
-  pdl((enc_fwd_kernel<TT>), grid, 256, 0, st)(B, d.S, d.E, d.K0, d.Wd[0], d.T, obs, mu, sigma, A, bits0);
+template <int TT, int RR>
+static int enc_launch(cudaStream_t st, const ActorDims& d, int B, float thr, const float* obs, const float* mu,
+                      const float* sigma, float* A, uint32_t* bits0) {
+  const size_t smem = enc_smem_bytes(RR, d.T);
+  if (smem > 160 * 1024) { set_error("encoder: T = %d too long for the shared tile", d.T); return SPIKERL_E_UNSUPPORTED; }
+  SPK_SMEM_ATTR((enc_fwd_kernel<TT, RR>), 160 * 1024);   // an upper bound; each launch asks for its own size
+  // one wave of resident blocks (a second partial wave of row-walking blocks would double the time)
+  int per_sm = 0;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, enc_fwd_kernel<TT, RR>, kEncThreads, smem) !=
+          cudaSuccess || per_sm < 1) {
+    cudaGetLastError();
+    per_sm = 1;
+  }
+  const int ky = (d.P[0] + kEncThreads - 1) / kEncThreads;
+  int bx = num_sms() * per_sm / ky;
+  if (bx > cdiv(B, RR)) bx = cdiv(B, RR);
+  if (bx < 1) bx = 1;
+  pdl((enc_fwd_kernel<TT, RR>), dim3((unsigned)bx, (unsigned)ky), kEncThreads, smem, st)(
+      B, d.S, d.E, d.K0, d.Wd[0], d.T, thr, obs, mu, sigma, A, bits0);
+  return SPIKERL_OK;
 }
 
 int launch_enc_fwd(const ActorDims& d, int B, const float* obs, const float* mu, const float* sigma,
                    float* A, uint32_t* bits0, cudaStream_t st) {
   ProfScope ps_("enc_fwd", PB_HBM, 0.0, 4.0 * B * (d.S + d.K0 + (double)d.T * d.Wd[0]), st);
-  // 256-thread blocks: the 8 warps of a block write 8 consecutive words (one full 32-byte sector)
-  // of each bits0[t][b] row, instead of half sectors (ncu r01: 1.89 GB written for 1.49 GB).
-  const int ky = (d.P[0] + 255) / 256;
-  int bx = (148 * 8 + ky - 1) / ky;  // ~8 resident 256-thread blocks per SM in total
-  if (bx > B) bx = B;
-  if (bx < 1) bx = 1;
-  dim3 grid(bx, ky);
+  // no-fire bound (see the file header), rounded down to fp32
+  const double thr64 = 1.0 / ((double)d.T * (1.0 + (double)d.T * 0x1p-22));
+  float thr = (float)thr64;
+  if ((double)thr > thr64) thr = nextafterf(thr, 0.0f);
+  // 8 rows per tile for the compiled T (a T = 32 tile is ~20 KB: eight resident blocks); 2 rows
+  // for any other T (up to 255: 16 KB of words)
   switch (d.T) {
 #define SPK_ENC_T(n) \
-  case n: enc_launch<n>(grid, st, d, B, obs, mu, sigma, A, bits0); break;
-    SPK_ENC_T(1) SPK_ENC_T(2) SPK_ENC_T(3) SPK_ENC_T(4) SPK_ENC_T(5) SPK_ENC_T(6) SPK_ENC_T(8) SPK_ENC_T(10)
-    SPK_ENC_T(12) SPK_ENC_T(16) SPK_ENC_T(20) SPK_ENC_T(24) SPK_ENC_T(32)
+  case n: SPK_TRY((enc_launch<n, 8>(st, d, B, thr, obs, mu, sigma, A, bits0))); break;
+    SPK_ENC_T(1) SPK_ENC_T(2) SPK_ENC_T(3) SPK_ENC_T(4) SPK_ENC_T(5) SPK_ENC_T(8) SPK_ENC_T(10) SPK_ENC_T(16)
+    SPK_ENC_T(32)
 #undef SPK_ENC_T
-    default: enc_launch<0>(grid, st, d, B, obs, mu, sigma, A, bits0); break;
+    default: SPK_TRY((enc_launch<0, 2>(st, d, B, thr, obs, mu, sigma, A, bits0))); break;
   }
   SPK_LAUNCHED();
   return SPIKERL_OK;

@@ -1,4 +1,6 @@
-// prof.cu — opt-in launch timing with CUDA events (never active inside a graph capture).
+// prof.cu — opt-in launch timing with CUDA events: (1) the profiling pass (every launch bracketed by
+// events; never inside a graph capture) and (2) the live watch of one kernel inside a benchmark's
+// timed region (event pairs supplied by the caller, recorded as event nodes when captured).
 #include <cstring>
 #include <map>
 #include <mutex>
@@ -17,11 +19,32 @@ struct Rec {
 std::mutex g_mu;
 std::vector<Rec> g_recs;
 bool g_on = false;
+struct Watch {
+  std::string name;
+  std::vector<cudaEvent_t> b, e;
+  int next = 0;
+} g_watch;
+bool g_watch_on = false;
+
+cudaError_t record(cudaEvent_t ev, cudaStream_t s) {
+  cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+  if (cudaStreamIsCapturing(s, &cs) != cudaSuccess) cs = cudaStreamCaptureStatusNone;
+  // inside a capture the record must become an event node of the graph (timed at every replay)
+  return cudaEventRecordWithFlags(ev, s, cs == cudaStreamCaptureStatusActive ? cudaEventRecordExternal
+                                                                               : cudaEventRecordDefault);
+}
 }  // namespace
 
-bool prof_on() { return g_on; }
+bool prof_on() { return g_on || g_watch_on; }
 
 ProfScope::ProfScope(const char* name, int bound, double flops, double bytes, cudaStream_t s) : st(s) {
+  if (g_watch_on) {
+    std::lock_guard<std::mutex> lk(g_mu);
+    if (g_watch.next < (int)g_watch.b.size() && g_watch.name == name) {
+      wslot = g_watch.next++;
+      record(g_watch.b[wslot], s);
+    }
+  }
   if (!g_on) return;
   cudaStreamCaptureStatus cs;
   if (cudaStreamIsCapturing(s, &cs) != cudaSuccess || cs != cudaStreamCaptureStatusNone) return;
@@ -35,6 +58,10 @@ ProfScope::ProfScope(const char* name, int bound, double flops, double bytes, cu
 }
 
 ProfScope::~ProfScope() {
+  if (wslot >= 0) {
+    std::lock_guard<std::mutex> lk(g_mu);
+    record(g_watch.e[wslot], st);
+  }
   if (slot < 0) return;
   std::lock_guard<std::mutex> lk(g_mu);
   cudaEventRecord(g_recs[slot].e1, st);
@@ -49,6 +76,27 @@ void spikerl_prof_enable(int on) {
   for (auto& r : spk::g_recs) { cudaEventDestroy(r.e0); cudaEventDestroy(r.e1); }
   spk::g_recs.clear();
   spk::g_on = on != 0;
+}
+
+int spikerl_prof_watch(const char* name, void* const* ev_begin, void* const* ev_end, int n) {
+  std::lock_guard<std::mutex> lk(spk::g_mu);
+  spk::g_watch = spk::Watch{};
+  spk::g_watch_on = false;
+  if (!name) return SPIKERL_OK;
+  if (n < 1 || !ev_begin || !ev_end) { spk::set_error("spikerl_prof_watch: bad arguments"); return SPIKERL_E_ARG; }
+  spk::g_watch.name = name;
+  for (int i = 0; i < n; ++i) {
+    if (!ev_begin[i] || !ev_end[i]) { spk::set_error("spikerl_prof_watch: null event"); return SPIKERL_E_ARG; }
+    spk::g_watch.b.push_back((cudaEvent_t)ev_begin[i]);
+    spk::g_watch.e.push_back((cudaEvent_t)ev_end[i]);
+  }
+  spk::g_watch_on = true;
+  return SPIKERL_OK;
+}
+
+int spikerl_prof_watch_count(void) {
+  std::lock_guard<std::mutex> lk(spk::g_mu);
+  return spk::g_watch.next;
 }
 
 int spikerl_prof_summary(spikerl_prof_entry* out, int max_entries) {

@@ -62,12 +62,19 @@ def _actor(pk, td3, flat):
     return {k: v.astype(np.float64) for k, v in pk.unpack_actor(td3.acfg, flat).items()}
 
 
+def _f32(x):
+    """A hyper-parameter as the fp32 value the C ABI passes the kernels (spikerl_td3_cfg is fp32)."""
+    return float(np.float32(x))
+
+
 def check_adam(p_pre, g, m_pre, v_pre, t, lr, p, m, v, clamp=None, what=""):
     """Oracle Adam (fp64) on the GPU's fp32 gradient and pre-state vs the GPU's fp32 result (R30):
     m, v within 4 ulp of the magnitude of their two terms, p within 2 ulp of |p| plus 1e-5 of the
     step lr (the step's own fp32 rounding: a quotient, a square root, a bias correction)."""
     f = lambda x: np.asarray(x, np.float64)
-    pr, mr, vr = oracle.adam_update(f(p_pre), f(g), f(m_pre), f(v_pre), t, lr)
+    hp = sg.TD3Hyper()
+    pr, mr, vr = oracle.adam_update(f(p_pre), f(g), f(m_pre), f(v_pre), t, _f32(lr), _f32(hp.beta1), _f32(hp.beta2),
+                                    _f32(hp.eps))
     if clamp is not None:
         lo, hi, cmin = clamp
         pr[lo:hi] = np.maximum(pr[lo:hi], cmin)
@@ -83,6 +90,7 @@ def check_adam(p_pre, g, m_pre, v_pre, t, lr, p, m, v, clamp=None, what=""):
 def check_polyak(tgt_pre, src, tau, tgt, what=""):
     """theta' <- tau theta + (1 - tau) theta' (fp32: two products and a sum) within 3 ulp of its terms."""
     f = lambda x: np.asarray(x, np.float64)
+    tau = _f32(tau)
     ref = oracle.polyak(f(tgt_pre), f(src), tau)
     e = 3 * ULP32 * (tau * np.abs(f(src)) + (1 - tau) * np.abs(f(tgt_pre))) + 1e-38
     d = np.abs(f(tgt) - ref)
