@@ -22,6 +22,7 @@
 // __ballot_sync per (t,b) yields exactly one u32 word of the next layer's bit plane.
 #include <cuda.h>
 #include <mutex>
+#include <type_traits>
 #include "internal.h"
 
 namespace spk {
@@ -741,8 +742,12 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         // reverse LIF scan of layer l-1 for HB batch rows of one neuron. Padding neurons have
         // g = 0 (zero weight columns) and no spike / window bits, so G = 0 there without masking.
         // G_{l-1} leaves through shared memory: DX_CH steps x BT rows x 128 neurons per TMA store.
+        // The chunk's spike / window bits are gathered once into one 32-bit word each (quad qi's 16
+        // bits = 4 steps x 4 rows at bits 16 qi), so every (step, row) test is one LOP3 against a
+        // compile-time mask (ncu r02: 17 instructions per element before, 547 per 4-step chunk)
         constexpr int HB = epi_hb(BT);
         constexpr int NQ = HB / 4;
+        static_assert(DX_CH == 4 && NQ <= 2, "one 16-bit field of 4 steps x 4 rows per quad");
         const bool act = g < BT / HB;   // idle groups (BT = 8 with 4 groups) still join the barriers
         const int jb = act ? g * HB : 0;
         const int b0 = t.n * BT + jb;
@@ -761,52 +766,61 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         for (int qi = 0; qi < NQ; ++qi) { qo[qi] = dq_o[qi]; qh[qi] = dq_h[qi]; }
         const bool leader = warp == EPI_WARP0 && lane == 0;
         const uint32_t soff = (uint32_t)((jb * 128 + 32 * q + lane) * 2);
-        for (int c = (p.T - 1) / DX_CH; c >= 0; --c, ++dx_chunk) {
-          const uint32_t buf = dx_chunk & 1u;
-          if (leader) bulk_wait_read1();   // the store issued from this buffer two chunks ago has read it
-          epi_bar_sync();
-          const int tb = c * DX_CH;
-          uint32_t rr[DX_CH][HB];
+        {
+          for (int c = (p.T - 1) / DX_CH; c >= 0; --c, ++dx_chunk) {
+            const uint32_t buf = dx_chunk & 1u;
+            if (leader) bulk_wait_read1();   // the store issued from this buffer two chunks ago has read it
+            epi_bar_sync();
+            const int tb = c * DX_CH;
+            uint32_t rr[DX_CH][HB];
 #pragma unroll
-          for (int ci = 0; ci < DX_CH; ++ci)
-            if (tb + ci < p.T) tmem_ldn<HB>(taddr + (tb + ci) * BT + jb, rr[ci]);
-          tmem_ld_wait();
-          const uint32_t sb = smem_u32(stg + buf * DX_STG) + soff;
-#pragma unroll
-          for (int ci = DX_CH - 1; ci >= 0; --ci) {
-            const int tt = tb + ci;
-            if (tt >= p.T || !act) continue;
-            if ((tt >> 4) != ch) {
-              ch = tt >> 4;
+            for (int ci = 0; ci < DX_CH; ++ci)
+              if (tb + ci < p.T) tmem_ldn<HB>(taddr + (tb + ci) * BT + jb, rr[ci]);
+            if ((tb >> 4) != ch) {
+              ch = tb >> 4;
 #pragma unroll
               for (int qi = 0; qi < NQ; ++qi) { qo[qi] = __ldg(bT + qi * qstride + ch); qh[qi] = __ldg(mT + qi * qstride + ch); }
             }
-            const int sh = 4 * (tt & 15);
-            uint32_t ow = 0, hw = 0;
+            const int sh = 4 * (tb & 15);   // 0, 16, 32 or 48: the chunk's aligned 16-bit field
+            uint32_t xo = 0, xh = 0;
 #pragma unroll
             for (int qi = 0; qi < NQ; ++qi) {
-              ow |= ((uint32_t)(qo[qi] >> sh) & 0xFu) << (4 * qi);
-              hw |= ((uint32_t)(qh[qi] >> sh) & 0xFu) << (4 * qi);
+              xo |= ((uint32_t)(qo[qi] >> sh) & 0xFFFFu) << (16 * qi);
+              xh |= ((uint32_t)(qh[qi] >> sh) & 0xFFFFu) << (16 * qi);
             }
+            tmem_ld_wait();
+            const uint32_t sb = smem_u32(stg + buf * DX_STG) + soff;
+#pragma unroll
+            for (int ci = DX_CH - 1; ci >= 0; --ci) {
+              if (tb + ci >= p.T || !act) continue;
+#pragma unroll
+              for (int j = 0; j < HB; ++j) {
+                const uint32_t bm = 1u << (16 * (j >> 2) + 4 * ci + (j & 3));
+                const float gv = __uint_as_float(rr[ci][j]);
+                // lif_back_step (common.cuh), same operations: delta_v = h z g + d_v (1 - o) delta_v',
+                // delta_c = delta_v + d_c delta_c'
+                const float hg = (xh & bm) ? __fmul_rn(zh, gv) : 0.0f;
+                const float dvt = (xo & bm) ? hg : __fmaf_rn(dvc, dvn[j], hg);
+                const float dct = __fmaf_rn(dcc, dcn[j], dvt);
+                dvn[j] = dvt;
+                dcn[j] = dct;
+                gs[j] = __fadd_rn(gs[j], dct);
+                st_shared_u16(sb + (uint32_t)((ci * BT + j) * 256), op16_bits(dct, F16));
+              }
+            }
+            fence_proxy_async();   // generic-proxy smem writes -> the TMA store
+            epi_bar_sync();
+            if (leader) {
+              tma_store_3d(&tmC, stg + buf * DX_STG, t.m * BM, t.n * BT, tb);
+              bulk_commit();
+            }
+          }
+          if (p.g_sum && act) {
 #pragma unroll
             for (int j = 0; j < HB; ++j) {
-              const float G = lif_back_step(zh, dvc, dcc, __uint_as_float(rr[ci][j]), (ow >> j) & 1u, (hw >> j) & 1u, dvn[j], dcn[j]);
-              gs[j] = __fadd_rn(gs[j], G);
-              st_shared_u16(sb + (uint32_t)((ci * BT + j) * 256), op16_bits(G, F16));
+              const int b = b0 + j;
+              if (b < p.B) p.g_sum[(size_t)b * p.p_prev + row] = __ushort_as_bfloat16(op16_bits(gs[j], F16));
             }
-          }
-          fence_proxy_async();   // generic-proxy smem writes -> the TMA store
-          epi_bar_sync();
-          if (leader) {
-            tma_store_3d(&tmC, stg + buf * DX_STG, t.m * BM, t.n * BT, tb);
-            bulk_commit();
-          }
-        }
-        if (p.g_sum && act) {
-#pragma unroll
-          for (int j = 0; j < HB; ++j) {
-            const int b = b0 + j;
-            if (b < p.B) p.g_sum[(size_t)b * p.p_prev + row] = __ushort_as_bfloat16(op16_bits(gs[j], F16));
           }
         }
       } else if (MODE == ENC) {
