@@ -74,6 +74,10 @@ enum spikerl_engine {
   SPIKERL_ENGINE_TCGEN05 = 2 /* tcgen05 (bf16/fp16 only)                                       */
 };
 
+/* Opaque NCCL communicator owned by the library (spikerl_comm_init / spikerl_comm_destroy). */
+struct spikerl_comm;
+typedef struct spikerl_comm spikerl_comm;
+
 /* Actor problem statement (PAPER.md:131 + north_star): obs dim S, action dim A, encoder
  * population E, decoder population D, hidden widths N1, N2, T timesteps, LIF constants. */
 typedef struct {
@@ -191,6 +195,21 @@ int spikerl_actor_backward(const spikerl_actor_cfg* cfg, int batch, const float*
                            const float* grad_actions, float* grad_params, int accumulate,
                            void* workspace, spikerl_stream_t stream);
 
+/* Actor backward fused with the data-parallel gradient mean (PAPER.md:135 average_gradients,
+ * PAPER.md:144 DDP "gradient synchronization ... during backpropagation"): as
+ * spikerl_actor_backward, and grad_params ends as the mean over the ranks of comm. The mean runs
+ * per bucket (spikerl_actor_grad_buckets, completion order: W3|Wd|bd, W2, mu|sigma|W1) on the
+ * library's comm stream as soon as the bucket is computed, overlapping the rest of the backward;
+ * `stream` waits for the last bucket before the call's work ends (graph-capturable). comm == NULL:
+ * exactly spikerl_actor_backward. Every rank must make the same calls in the same order. */
+int spikerl_actor_backward_dp(const spikerl_actor_cfg* cfg, int batch, const float* params,
+                              const void* params_bf16, const float* obs, const spikerl_tape* tape,
+                              const float* grad_actions, float* grad_params, int accumulate,
+                              spikerl_comm* comm, void* workspace, spikerl_stream_t stream);
+/* Bucket bounds of the flat actor gradient (host call): bounds[4] = {0, off W2, off W3, total};
+ * buckets [bounds[i], bounds[i+1]). */
+int spikerl_actor_grad_buckets(const spikerl_actor_cfg* cfg, size_t* bounds);
+
 /* Twin critic forward (+ backward). x = [obs ; act] with obs_dim + act_dim == in_dim.
  * params2 [2][P] fp32 (+ bf16 copy iff precision=BF16). q [2][B] receives Q1, Q2.
  * If target_y [B] != NULL: loss (device scalar, may be NULL) = mean(Q1-y)^2 + mean(Q2-y)^2 and,
@@ -240,8 +259,6 @@ typedef struct {
   float* amp;
 } spikerl_td3_bufs;
 
-struct spikerl_comm;
-typedef struct spikerl_comm spikerl_comm;
 
 /* One TD3 update. step = 1-based k; the actor and all targets are updated when
  * k % policy_delay == 0. indices [B] (device int64) / noise [B][A] (device fp32 raw eps, before
@@ -332,6 +349,14 @@ typedef struct {
 } spikerl_prof_entry;
 void spikerl_prof_enable(int on);
 int spikerl_prof_summary(spikerl_prof_entry* out, int max_entries);
+/* The profiling pass's launches in enqueue order, each with its start / end (ms) relative to the
+ * first recorded launch's start (events on the launch's own stream: concurrent branches show as
+ * overlapping intervals). Returns the number of launches (or -1). */
+typedef struct {
+  char name[48];
+  double start_ms, end_ms;
+} spikerl_prof_span;
+int spikerl_prof_timeline(spikerl_prof_span* out, int max_entries);
 /* Live watch of one kernel inside a timed region (bench.py's roofline): every launch named `name`
  * (the names spikerl_prof_summary reports) is bracketed by the next caller-owned event pair
  * (cudaEvent_t created with timing), ev_begin[i] / ev_end[i], i = 0..n-1, recorded on the stream

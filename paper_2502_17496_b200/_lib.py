@@ -77,6 +77,10 @@ class ProfEntry(C.Structure):
                 ("total_ms", C.c_double), ("flops", C.c_double), ("bytes", C.c_double)]
 
 
+class ProfSpan(C.Structure):
+    _fields_ = [("name", C.c_char * 48), ("start_ms", C.c_double), ("end_ms", C.c_double)]
+
+
 BOUND_NAMES = ("hbm", "tensor", "alu", "latency")
 
 
@@ -117,6 +121,16 @@ class Watch:
         self.launches += k
 
 
+def prof_timeline():
+    """Launches of the profiling pass in enqueue order: [(name, start_ms, end_ms)]."""
+    n = lib().spikerl_prof_timeline(None, 0)
+    if n < 0:
+        raise SpikeRLError(E_CUDA, last_error())
+    arr = (ProfSpan * max(n, 1))()
+    lib().spikerl_prof_timeline(arr, n)
+    return [(e.name.decode(), e.start_ms, e.end_ms) for e in arr[:n]]
+
+
 def prof_summary():
     n = lib().spikerl_prof_summary(None, 0)
     if n < 0:
@@ -152,6 +166,8 @@ _SIGS = {
     "spikerl_critic_refresh_bf16": (I, [C.POINTER(CriticCfg), I, P, P, P]),
     "spikerl_actor_forward": (I, [C.POINTER(ActorCfg), I, P, P, P, P, C.POINTER(Tape), P, P]),
     "spikerl_actor_backward": (I, [C.POINTER(ActorCfg), I, P, P, P, C.POINTER(Tape), P, P, I, P, P]),
+    "spikerl_actor_backward_dp": (I, [C.POINTER(ActorCfg), I, P, P, P, C.POINTER(Tape), P, P, I, P, P, P]),
+    "spikerl_actor_grad_buckets": (I, [C.POINTER(ActorCfg), C.POINTER(SZ)]),
     "spikerl_critic_fwd_bwd": (I, [C.POINTER(CriticCfg), I, P, P, P, I, P, I, P, P, P, P, P, F, P, P]),
     "spikerl_adam": (I, [P, P, P, P, SZ, P, F, F, F, F, SZ, SZ, F, P]),
     "spikerl_polyak": (I, [P, P, SZ, F, P]),
@@ -172,6 +188,7 @@ _SIGS = {
     "spikerl_launch_count": (LL, [I]),
     "spikerl_prof_enable": (None, [I]),
     "spikerl_prof_summary": (I, [P, I]),
+    "spikerl_prof_timeline": (I, [P, I]),
     "spikerl_prof_watch": (I, [C.c_char_p, C.POINTER(P), C.POINTER(P), I]),
     "spikerl_prof_watch_count": (I, []),
 }

@@ -156,11 +156,25 @@ class SpikingActor:
                                           _p(self.ws), _stream()), "actor_forward")
         return self.actions
 
-    def backward(self, obs: torch.Tensor, grad_actions: torch.Tensor, accumulate=False) -> torch.Tensor:
-        check(lib().spikerl_actor_backward(C.byref(self.cfg), self.batch, _p(self.params), _p(self.params_bf16),
-                                           _p(obs), C.byref(self.tape), _p(grad_actions), _p(self.grads),
-                                           int(accumulate), _p(self.ws), _stream()), "actor_backward")
+    def backward(self, obs: torch.Tensor, grad_actions: torch.Tensor, accumulate=False, comm=None) -> torch.Tensor:
+        """BPTT; with `comm` the gradient ends as the mean over ranks, allreduced per bucket while the
+        backward still runs (spikerl_actor_backward_dp)."""
+        if comm is None:
+            check(lib().spikerl_actor_backward(C.byref(self.cfg), self.batch, _p(self.params), _p(self.params_bf16),
+                                               _p(obs), C.byref(self.tape), _p(grad_actions), _p(self.grads),
+                                               int(accumulate), _p(self.ws), _stream()), "actor_backward")
+        else:
+            check(lib().spikerl_actor_backward_dp(C.byref(self.cfg), self.batch, _p(self.params),
+                                                  _p(self.params_bf16), _p(obs), C.byref(self.tape),
+                                                  _p(grad_actions), _p(self.grads), int(accumulate), comm.handle,
+                                                  _p(self.ws), _stream()), "actor_backward_dp")
         return self.grads
+
+    def grad_buckets(self):
+        """[0, off W2, off W3, total): the allreduce buckets of the flat gradient."""
+        b = (C.c_size_t * 4)()
+        check(lib().spikerl_actor_grad_buckets(C.byref(self.cfg), b), "grad_buckets")
+        return list(b)
 
     # tape views (for parity tests / diagnostics)
     def tape_view(self):

@@ -67,10 +67,11 @@ int launch_enc_grad_reduce(const ActorDims& d, int nchunk, const float* partial,
 // ---- auxiliary streams (prof.cu): per device, created once outside any graph capture (the
 // workspace-size queries create them). Kernels forked onto them are joined back before the
 // forking call returns, so a graph capture of the call records a DAG with parallel branches.
-// Slots: TD3 step side 0-2 / ev 0-7; actor backward side 3-5 / ev 8-15; critic side 6 / ev 16-19.
+// Slots: TD3 step side 0-2, 7 / ev 0-7; actor backward side 3-5 / ev 8-15; critic side 6 / ev 16-19;
+// bucketed gradient allreduce of the actor backward: side 8 (the comm stream) / ev 20-27.
 struct AuxPool {
-  cudaStream_t side[8];
-  cudaEvent_t ev[24];
+  cudaStream_t side[10];
+  cudaEvent_t ev[32];
 };
 int aux_pool(AuxPool** out);
 int stream_after(cudaStream_t dst, cudaStream_t src, cudaEvent_t ev);   // dst waits for src's work so far

@@ -99,6 +99,29 @@ int spikerl_prof_watch_count(void) {
   return spk::g_watch.next;
 }
 
+int spikerl_prof_timeline(spikerl_prof_span* out, int max_entries) {
+  std::lock_guard<std::mutex> lk(spk::g_mu);
+  if (spk::g_recs.empty()) return 0;
+  cudaEvent_t t0 = spk::g_recs[0].e0;
+  for (auto& r : spk::g_recs)
+    if (cudaEventSynchronize(r.e1) != cudaSuccess) { spk::set_error("prof: event sync failed"); return -1; }
+  int n = 0;
+  for (auto& r : spk::g_recs) {
+    if (out && n < max_entries) {
+      spikerl_prof_span& e = out[n];
+      memset(&e, 0, sizeof(e));
+      strncpy(e.name, r.name, sizeof(e.name) - 1);
+      float a = 0.f, b = 0.f;
+      cudaEventElapsedTime(&a, t0, r.e0);
+      cudaEventElapsedTime(&b, t0, r.e1);
+      e.start_ms = a;
+      e.end_ms = b;
+    }
+    ++n;
+  }
+  return n;
+}
+
 int spikerl_prof_summary(spikerl_prof_entry* out, int max_entries) {
   std::lock_guard<std::mutex> lk(spk::g_mu);
   std::map<std::string, spikerl_prof_entry> agg;

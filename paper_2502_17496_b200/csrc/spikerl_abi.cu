@@ -236,10 +236,24 @@ static int actor_forward_impl(const ActorDims& d, int B, const float* params,
   return SPIKERL_OK;
 }
 
+// Gradient buckets of the actor's flat layout mu|sigma|W1|W2|W3|Wd|bd, in the order the backward
+// completes them: tail = W3|Wd|bd (dW3 + decoder), W2 (dW2), head = mu|sigma|W1 (dW1 + encoder).
+// Bounds: [0, off W2, off W3, total).
+static void actor_grad_buckets(const ActorDims& d, size_t out[4]) {
+  out[0] = 0;
+  out[1] = d.off[SPIKERL_ACTOR_W2];
+  out[2] = d.off[SPIKERL_ACTOR_W3];
+  out[3] = d.off[SPIKERL_ACTOR_NPARAM];
+}
+
+// comm != NULL: the gradient mean over ranks (PAPER.md:135 average_gradients, PAPER.md:144 DDP
+// "during backpropagation") runs per bucket on the library's comm stream as soon as the bucket's
+// producers finish, overlapping the rest of the backward (the tail and W2 buckets run while dX2,
+// dW1 and the encoder gradient compute); the call's stream joins the comm stream at the end.
 static int actor_backward_impl(const ActorDims& d, int B, const float* params,
                                const __nv_bfloat16* pb16, const float* obs, const char* tape,
                                const float* grad_a, float* grads, int accum, char* ws,
-                               cudaStream_t st) {
+                               cudaStream_t st, spikerl_comm* comm = nullptr) {
   const TapeLayout L = tape_layout(d, B);
   const ActorWs W = actor_ws_layout(d, B);
   const uint32_t* bits[4];
@@ -269,6 +283,23 @@ static int actor_backward_impl(const ActorDims& d, int B, const float* params,
     if (s == st) return SPIKERL_OK;
     return stream_after(s, st, aux->ev[8 + e]);
   };
+  size_t bk[4];
+  actor_grad_buckets(d, bk);
+  cudaStream_t sc = aux->side[8];
+  int nev = 0;
+  // bucket [lo, hi) allreduced on the comm stream after the producers' work enqueued so far
+  // (np producers: the stream handles themselves may be 0, the legacy default stream)
+  auto bucket = [&](size_t lo, size_t hi, cudaStream_t p0, cudaStream_t p1, int np) -> int {
+    if (!comm) return SPIKERL_OK;
+    const cudaStream_t prod[2] = {p0, p1};
+    for (int i = 0; i < np; ++i) {
+      SPK_TRY(stream_after(sc, prod[i], aux->ev[20 + nev]));
+      ++nev;
+    }
+    static const char* names[3] = {"allreduce_bucket_head", "allreduce_bucket_W2", "allreduce_bucket_tail"};
+    ProfScope ps_(names[lo == bk[0] ? 0 : (lo == bk[1] ? 1 : 2)], PB_LATENCY, 0.0, 8.0 * (hi - lo), sc);
+    return spikerl_allreduce_grads(comm, grads + lo, hi - lo, sc);
+  };
   SPK_TRY(branch(sw[0], 0));
   SPK_TRY(launch_dec_param_grads(d, B, g_pre, counts, grads + d.off[SPIKERL_ACTOR_WD],
                                  grads + d.off[SPIKERL_ACTOR_BD], (float*)(ws + W.dec_part), accum, sw[0]));
@@ -281,6 +312,8 @@ static int actor_backward_impl(const ActorDims& d, int B, const float* params,
       SPK_TRY(launch_lif_dw_tc(d, l, B, G[l], bits[l - 1], dW, (float*)(ws + W.dw_part[l]), accum, sw[l]));
     else
       SPK_TRY(launch_lif_dw_simt(d, l, B, G[l], bits[l - 1], dW, accum, sw[l]));
+    if (l == 3) SPK_TRY(bucket(bk[2], bk[3], sw[3], sw[0], sw[0] != sw[3] ? 2 : 1));
+    if (l == 2) SPK_TRY(bucket(bk[1], bk[2], sw[2], sw[2], 1));
     if (l >= 2) {
       if (tc)
         SPK_TRY(launch_lif_dx_tc(d, l, B, G[l], Wb, (const uint8_t*)(tape + L.bitsT[l - 1]),
@@ -301,12 +334,14 @@ static int actor_backward_impl(const ActorDims& d, int B, const float* params,
                                  A, obs, params + d.off[SPIKERL_ACTOR_MU], params + d.off[SPIKERL_ACTOR_SIGMA],
                                  (float*)(ws + W.enc_part), grads + d.off[SPIKERL_ACTOR_MU],
                                  grads + d.off[SPIKERL_ACTOR_SIGMA], accum, st));
+  SPK_TRY(bucket(bk[0], bk[1], sw[1], st, sw[1] != st ? 2 : 1));
   if (fork) {   // join every side stream back into st
     for (int i = 3; i <= 5; ++i) {
       SPK_CHECK_CUDA(cudaEventRecord(aux->ev[8 + i], aux->side[i]));
       SPK_CHECK_CUDA(cudaStreamWaitEvent(st, aux->ev[8 + i], 0));
     }
   }
+  if (comm) SPK_TRY(stream_after(st, sc, aux->ev[27]));   // join the comm stream
   return SPIKERL_OK;
 }
 
@@ -519,6 +554,34 @@ int spikerl_actor_backward(const spikerl_actor_cfg* cfg, int batch, const float*
                              (cudaStream_t)stream);
 }
 
+int spikerl_actor_backward_dp(const spikerl_actor_cfg* cfg, int batch, const float* params,
+                              const void* params_bf16, const float* obs, const spikerl_tape* tape,
+                              const float* grad_actions, float* grad_params, int accumulate, spikerl_comm* comm,
+                              void* workspace, spikerl_stream_t stream) {
+  ActorDims d;
+  SPK_TRY(actor_dims(cfg, &d));
+  if (batch < 1 || !params || !obs || !tape || !grad_actions || !grad_params || !workspace ||
+      (d.bf16 && !params_bf16)) {
+    set_error("spikerl_actor_backward_dp: bad arguments");
+    return SPIKERL_E_ARG;
+  }
+  if (tape->magic != kTapeMagic || tape->cfg_hash != actor_cfg_hash(cfg) || tape->batch != batch || !tape->dev) {
+    set_error("tape does not belong to this (cfg, batch)");
+    return SPIKERL_E_STATE;
+  }
+  return actor_backward_impl(d, batch, params, (const __nv_bfloat16*)params_bf16, obs, (const char*)tape->dev,
+                             grad_actions, grad_params, accumulate ? 1 : 0, (char*)workspace, (cudaStream_t)stream,
+                             comm);
+}
+
+int spikerl_actor_grad_buckets(const spikerl_actor_cfg* cfg, size_t* bounds) {
+  ActorDims d;
+  SPK_TRY(actor_dims(cfg, &d));
+  if (!bounds) { set_error("null bounds"); return SPIKERL_E_ARG; }
+  actor_grad_buckets(d, bounds);
+  return SPIKERL_OK;
+}
+
 int spikerl_critic_fwd_bwd(const spikerl_critic_cfg* cfg, int batch, const float* params2,
                            const void* params2_bf16, const float* obs, int obs_dim, const float* act, int act_dim,
                            const float* target_y, float* q, float* loss, float* grad_params2, float* grad_act,
@@ -660,8 +723,7 @@ int spikerl_td3_update(const spikerl_actor_cfg* acfg, const spikerl_critic_cfg* 
       pdl(neg_mean_kernel, 1, 256, 0, st)(B, q, losses + 1);
       SPK_LAUNCHED();
     }
-    SPK_TRY(actor_backward_impl(ad, B, b->actor, abf, s, tape, ga, b->grad_actor, 0, aws, st));
-    SPK_TRY(spikerl_allreduce_grads(comm, b->grad_actor, Pa, stream));
+    SPK_TRY(actor_backward_impl(ad, B, b->actor, abf, s, tape, ga, b->grad_actor, 0, aws, st, comm));
     if (amp_a) SPK_TRY(launch_amp_check(b->grad_actor, Pa, amp_a, st));
     SPK_TRY(launch_adam(b->actor, b->grad_actor, b->m_actor, b->v_actor, Pa, b->adam_steps + 2, hp->lr_actor,
                         hp->beta1, hp->beta2, hp->eps, ad.off[SPIKERL_ACTOR_SIGMA], ad.off[SPIKERL_ACTOR_W1],
@@ -798,8 +860,7 @@ int spikerl_td3_update_pair(const spikerl_actor_cfg* acfg, const spikerl_critic_
     pdl(neg_mean_kernel, 1, 256, 0, st)(B, x.q, losses + 1);
     SPK_LAUNCHED();
   }
-  SPK_TRY(actor_backward_impl(ad, B, b->actor, abf, x.s, x.tape, x.ga, b->grad_actor, 0, x.aws, st));
-  SPK_TRY(spikerl_allreduce_grads(comm, b->grad_actor, Pa, stream));
+  SPK_TRY(actor_backward_impl(ad, B, b->actor, abf, x.s, x.tape, x.ga, b->grad_actor, 0, x.aws, st, comm));
   if (amp_a) SPK_TRY(launch_amp_check(b->grad_actor, Pa, amp_a, st));
   SPK_TRY(launch_adam(b->actor, b->grad_actor, b->m_actor, b->v_actor, Pa, b->adam_steps + 2, hp->lr_actor, hp->beta1,
                       hp->beta2, hp->eps, ad.off[SPIKERL_ACTOR_SIGMA], ad.off[SPIKERL_ACTOR_W1], ad.sigma_floor,

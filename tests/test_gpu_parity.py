@@ -494,6 +494,44 @@ def test_nccl_single_rank_comm():
     comm.close()
 
 
+@pytest.mark.parametrize("preset,B", [("cfg1", 256), ("cfg3L", 8192)])
+def test_actor_backward_dp_buckets_world1(preset, B):
+    """The bucketed gradient mean (spikerl_actor_backward_dp: W3|Wd|bd, W2, mu|sigma|W1 allreduced on
+    the comm stream as each is produced) through a one-rank NCCL communicator, eager and captured in
+    a CUDA graph: bitwise the plain backward's gradient (ncclAvg over one rank is the identity), in
+    the side-stream schedule (T B <= 32768) and the one-stream schedule."""
+    import torch
+    import paper_2502_17496_b200 as pk
+    shape, _, _ = sg.preset(preset)
+    p, s, g = _inputs(shape, B, seed=31)
+    comm = pk.Comm(0, 1)
+    actor = pk.SpikingActor(pk.actor_cfg_from(shape), B)
+    actor.load(p)
+    b = actor.grad_buckets()
+    assert b[0] == 0 and b[-1] == actor.n_params and b == sorted(b)
+    obs = torch.from_numpy(s).cuda()
+    ga = torch.from_numpy(np.ascontiguousarray(g, np.float32)).cuda()
+    actor.forward(obs)
+    ref = actor.backward(obs, ga).clone()
+    actor.grads.zero_()
+    got = actor.backward(obs, ga, comm=comm).clone()
+    torch.cuda.synchronize()
+    assert torch.equal(ref, got)
+    st = torch.cuda.Stream()
+    st.wait_stream(torch.cuda.current_stream())
+    with torch.cuda.stream(st):
+        graph = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(graph, stream=st):
+            actor.forward(obs)
+            actor.backward(obs, ga, comm=comm)
+    torch.cuda.current_stream().wait_stream(st)
+    actor.grads.zero_()
+    graph.replay()
+    torch.cuda.synchronize()
+    assert torch.equal(ref, actor.grads)
+    comm.close()
+
+
 @pytest.mark.parametrize("preset", ["cfg1", "cfg3L"])
 def test_td3_pair_matches_sequential(preset):
     """spikerl_td3_update_pair(k) (update k + 1's target path and pi(s) overlapping update k) leaves

@@ -188,6 +188,77 @@ def test_scheme_a_equals_scheme_b():
     assert np.array_equal(out["A"], out["B"])
 
 
+def _worker_buckets(rank, world, port, q):
+    import sys
+    sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+    _init(rank, world, port)
+    import ctypes as C
+    import oracle
+    import synthgen as sg
+    from paper_2502_17496_b200 import _lib, actor_cfg_from, pack_actor
+    shape = sg.ActorShape(3, 2, pop_enc=5, pop_dec=4, n1=12, n2=10, T=5, precision="fp32")
+    cfg = actor_cfg_from(shape)
+    bounds = (C.c_size_t * 4)()
+    assert _lib.lib().spikerl_actor_grad_buckets(C.byref(cfg), bounds) == 0
+    rng = np.random.default_rng(0)
+    p = sg.randomize_actor(shape, rng)
+    s = sg.observations(rng, 8, 3)
+    g = sg.action_grads(rng, 8, 2)
+    sl = slice(4 * rank, 4 * rank + 4)
+    _, tape = oracle.actor_forward(p, shape, s[sl])
+    grad = oracle.actor_backward(p, shape, tape, g[sl])
+    flat = pack_actor(cfg, {k: v.astype(np.float32) for k, v in grad.items()}, device="cpu").double()
+    whole = flat.clone()
+    dist.all_reduce(whole)
+    whole /= world
+    bucketed = flat.clone()
+    for i in (2, 1, 0):            # the library's completion order: W3|Wd|bd, W2, mu|sigma|W1
+        seg = bucketed[bounds[i]:bounds[i + 1]]
+        dist.all_reduce(seg)
+        seg /= world
+    q.put((rank, list(bounds), whole.numpy(), bucketed.numpy()))
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def test_bucketed_allreduce_matches_whole():
+    """The library's gradient buckets (spikerl_actor_grad_buckets: host logic) tile the flat actor
+    gradient in order, and a mean allreduced bucket by bucket in the library's completion order equals
+    the whole-vector mean bitwise on both ranks, which equals the fp32-packed oracle gradient of the
+    concatenated batch over 2 (PAPER.md:135 average_gradients)."""
+    import oracle
+    import synthgen as sg
+    from paper_2502_17496_b200 import actor_cfg_from, pack_actor, _lib
+    if not os.path.exists(_lib.LIB_PATH):
+        import __graft_entry__
+        __graft_entry__.build()
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    ps = [ctx.Process(target=_worker_buckets, args=(r, 2, port, q)) for r in range(2)]
+    for p in ps:
+        p.start()
+    res = dict((r, rest) for r, *rest in (q.get(timeout=120) for _ in range(2)))
+    for p in ps:
+        p.join(timeout=60)
+    bounds = res[0][0]
+    shape = sg.ActorShape(3, 2, pop_enc=5, pop_dec=4, n1=12, n2=10, T=5, precision="fp32")
+    cfg = actor_cfg_from(shape)
+    n = pack_actor(cfg, sg.actor_params(shape, np.random.default_rng(0)), device="cpu").numel()
+    assert bounds[0] == 0 and bounds[-1] == n and all(a < b for a, b in zip(bounds, bounds[1:]))
+    for r in (0, 1):
+        assert np.array_equal(res[r][1], res[r][2])
+    assert np.array_equal(res[0][2], res[1][2])
+    rng = np.random.default_rng(0)
+    p = sg.randomize_actor(shape, rng)
+    s = sg.observations(rng, 8, 3)
+    g = sg.action_grads(rng, 8, 2)
+    _, tape = oracle.actor_forward(p, shape, s)
+    full = oracle.actor_backward(p, shape, tape, g)
+    ref = pack_actor(cfg, {k: (v / 2).astype(np.float32) for k, v in full.items()}, device="cpu").double().numpy()
+    assert np.allclose(res[0][2], ref, rtol=1e-6, atol=1e-7)
+
+
 def test_bench_sharding_arithmetic():
     """bench.py's per-rank split of configs[4] and weak-scaling accounting."""
     import bench
