@@ -58,6 +58,12 @@ size_t tc_dw_partial_bytes(const ActorDims& d, int B, int l);
 int tc_wgrad_splits(int Bp, int inq);
 int launch_critic_wgrad_tc(int Bp, int inq, int xtr, const __nv_bfloat16* dZT, const __nv_bfloat16* XTH,
                            float* part, long long msz, cudaStream_t st);
+// twin-critic contractions at large batch on the tcgen05 engine: mode 6 = CF1 (X W1^T -> H1T),
+// 7 = CF2 (H1 W2^T -> H2T, q), 8 = CB1 (dZ2 W2 -> dZ1T); see k_tc_gemm.cu
+int launch_critic_tc(int mode, int B, int Bp, int nz, const __nv_bfloat16* A, int a_rows, int aoff,
+                     const __nv_bfloat16* Bw0, const __nv_bfloat16* Bw1, int bk, int ldb, const float* bias,
+                     const __nv_bfloat16* w3, const float* b3, long long ps, __nv_bfloat16* out, long long os,
+                     const __nv_bfloat16* mask, float* q, cudaStream_t st);
 // 3-D u32 tensor map (dims / box innermost first, strides in bytes), no swizzle, OOB zero fill
 int make_u32_map3(CUtensorMap* m, const void* base, const uint64_t* dims, const uint64_t* strides,
                   const uint32_t* box);   // split-K partials of dW_l

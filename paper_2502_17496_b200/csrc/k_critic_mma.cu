@@ -133,6 +133,7 @@ MmaLayout mma_layout(const CriticDims& c) {
 
 struct MmaWs {
   __nv_bfloat16 *XT, *H1T, *dZ2T, *dZ1T;   // [inq][Bp], [2][H][Bp] x3
+  __nv_bfloat16* H2T;                      // [2][H][Bp] (tcgen05 path: h2 for dW3 and the dZ2 mask)
   float *Z1, *Z2, *Hh2, *q, *dq;           // [2][B][H] x3, [2][B] x2
   float* part;                             // [2][Bp/RB] loss partials
   unsigned int* ticket;
@@ -156,6 +157,7 @@ MmaWs mma_carve(const CriticDims& c, int B, void* base, size_t* total) {
   w.H1T = (__nv_bfloat16*)take(2 * 2 * (size_t)c.H1 * Bp);
   w.dZ2T = (__nv_bfloat16*)take(2 * 2 * (size_t)c.H2 * Bp);
   w.dZ1T = (__nv_bfloat16*)take(2 * 2 * (size_t)c.H1 * Bp);
+  w.H2T = (__nv_bfloat16*)take(2 * 2 * (size_t)c.H2 * Bp);
   w.Z1 = (float*)take(4 * 2 * (size_t)B * c.H1);
   w.Z2 = (float*)take(4 * 2 * (size_t)B * c.H2);
   w.Hh2 = (float*)take(4 * 2 * (size_t)B * c.H2);
@@ -169,6 +171,29 @@ MmaWs mma_carve(const CriticDims& c, int B, void* base, size_t* total) {
   w.wpart = (float*)take(wmax > 1 ? sizeof(float) * wmax * 2 * ((size_t)HW * HW + (size_t)HW * L.inq) : 0);
   if (total) *total = off;
   return w;
+}
+
+// Loss of the last block to finish (the caller's `last`, block-uniform): per critic z a fixed-order
+// sum over the blocks' partials (each thread a strided subset, all its loads in flight, then a
+// fixed tree over the 256 threads), then the critics in order: deterministic. (The serial chain of
+// one volatile L2 load per partial it replaces cost ~0.3 us per block.) blockDim.x == 256.
+__device__ __forceinline__ void final_loss(const float* part, int nb, int nz, int mode, int B, float* loss) {
+  __shared__ float red[256];
+  float tot = 0.f;
+  for (int z = 0; z < nz; ++z) {
+    float s = 0.f;
+    for (int i = threadIdx.x; i < nb; i += 256) s = __fadd_rn(s, *(volatile const float*)&part[z * nb + i]);
+    red[threadIdx.x] = s;
+    __syncthreads();
+    for (int w = 128; w > 0; w >>= 1) {
+      if (threadIdx.x < w) red[threadIdx.x] = __fadd_rn(red[threadIdx.x], red[threadIdx.x + w]);
+      __syncthreads();
+    }
+    const float sz = __fdiv_rn(red[0], (float)B);
+    tot = mode == 0 ? __fadd_rn(tot, sz) : __fsub_rn(tot, sz);
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) *loss = tot;
 }
 
 // ------------------------------------------------------------------ forward (both critics)
@@ -399,23 +424,17 @@ __global__ void __launch_bounds__(256) critic_bwd_data_mma_kernel(
 #pragma unroll
     for (int r = 0; r < RB; ++r) d2s[r * ldh + j] = __float2bfloat16_rn(zz[r] > 0.f ? __fmul_rn(dqs[r], w3) : 0.f);
   }
-  if (tid == 0) {   // publish the partial; the last CTA reduces all of them in (z, block) order
+  if (tid == 0) {   // publish the partial; the last CTA reduces all of them
     __threadfence();
     const unsigned int n = gridDim.x * gridDim.y;
     last = atomicAdd(ticket, 1u) == n - 1;
-    if (last && loss) {
-      __threadfence();
-      float tot = 0.f;
-      for (int zz = 0; zz < (int)gridDim.y; ++zz) {
-        float sz = 0.f;
-        for (int bx = 0; bx < (int)gridDim.x; ++bx) sz = __fadd_rn(sz, *(volatile float*)&part[zz * gridDim.x + bx]);
-        tot = mode == 0 ? __fadd_rn(tot, __fdiv_rn(sz, (float)B)) : __fsub_rn(tot, __fdiv_rn(sz, (float)B));
-      }
-      *loss = tot;
-    }
-    if (last) *ticket = 0u;
   }
   __syncthreads();
+  if (last) {
+    __threadfence();
+    if (loss) final_loss(part, gridDim.x, gridDim.y, mode, B, loss);
+    if (tid == 0) *ticket = 0u;
+  }
   cstamp(2);
   if (store_t) {
     for (int idx = tid; idx < RB * HW; idx += 256) {
@@ -578,32 +597,100 @@ __global__ void critic_wgrad_reduce_kernel(int splits, int in, int inq, long lon
   }
 }
 
-// db1 = rowsum dZ1T, db2 = rowsum dZ2T, dW3 = dQ^T H2, db3 = sum dQ: one warp per output
+// db1 = rowsum dZ1T, db2 = rowsum dZ2T, dW3 = dQ^T H2, db3 = sum dQ. Small batches: one warp per
+// output (blockIdx.x * 8 + warp); large batches (B > 1024): one block per output, each thread a
+// strided subset of the rows with four partial sums, then a fixed tree (ncu r02: the warp-per-output
+// form took 18-26 us at B = 4096). Both orders are fixed: deterministic.
+__device__ __forceinline__ float bias_row_term(int o, int z, int b, int Bp, int B, const __nv_bfloat16* dZ1T,
+                                               const __nv_bfloat16* dZ2T, const float* dq, const float* Hh2,
+                                               const __nv_bfloat16* H2T) {
+  if (o < HW) return __bfloat162float(dZ1T[((size_t)z * HW + o) * Bp + b]);
+  if (o < 2 * HW) return __bfloat162float(dZ2T[((size_t)z * HW + o - HW) * Bp + b]);
+  if (o < 3 * HW) {
+    const int j = o - 2 * HW;
+    const float h = H2T ? __bfloat162float(H2T[((size_t)z * HW + j) * Bp + b]) : Hh2[((size_t)z * B + b) * HW + j];
+    return __fmul_rn(dq[(size_t)z * B + b], h);
+  }
+  return dq[(size_t)z * B + b];
+}
+
 __global__ void __launch_bounds__(256) critic_bias_grads_kernel(int B, int Bp, long long P, long long oB1,
                                                                 long long oB2, long long oW3, long long oB3,
                                                                 const __nv_bfloat16* __restrict__ dZ1T,
                                                                 const __nv_bfloat16* __restrict__ dZ2T,
                                                                 const float* __restrict__ dq,
                                                                 const float* __restrict__ Hh2,
+                                                                const __nv_bfloat16* __restrict__ H2T,
                                                                 float* __restrict__ grad2) {
   pdl_wait();
   pdl_trigger();
   const int z = blockIdx.y;
-  const int o = blockIdx.x * 8 + (threadIdx.x >> 5), lane = threadIdx.x & 31;
   const int nout = 3 * HW + 1;
-  if (o >= nout) return;
-  float s = 0.f;
-  if (o < 2 * HW) {
-    const __nv_bfloat16* row = (o < HW ? dZ1T + ((size_t)z * HW + o) * Bp : dZ2T + ((size_t)z * HW + o - HW) * Bp);
-    for (int b = lane; b < B; b += 32) s = __fadd_rn(s, __bfloat162float(row[b]));
-  } else if (o < 3 * HW) {
-    const int j = o - 2 * HW;
-    for (int b = lane; b < B; b += 32)
-      s = __fmaf_rn(dq[(size_t)z * B + b], Hh2[((size_t)z * B + b) * HW + j], s);
-  } else {
-    for (int b = lane; b < B; b += 32) s = __fadd_rn(s, dq[(size_t)z * B + b]);
+  const bool big = gridDim.x == (unsigned)nout;   // one block per output
+  if (big && H2T) {
+    // tcgen05 path (rows transposed, Bp a multiple of 16): each thread 8 consecutive rows per
+    // 16-byte load, every load of the row issued before the sums; rows past B are zero in dZ1T /
+    // dZ2T / H2T, and dq is only read below B
+    const int o = blockIdx.x;
+    const __nv_bfloat16* row = o < HW ? dZ1T + ((size_t)z * HW + o) * Bp
+                             : (o < 2 * HW ? dZ2T + ((size_t)z * HW + o - HW) * Bp
+                                           : (o < 3 * HW ? H2T + ((size_t)z * HW + o - 2 * HW) * Bp : nullptr));
+    float sacc = 0.f;
+    for (int b0 = 8 * threadIdx.x; b0 < Bp; b0 += 4 * 2048) {
+      uint4 v[4];
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+        v[i] = (row && b0 + 2048 * i < Bp) ? *reinterpret_cast<const uint4*>(row + b0 + 2048 * i) : make_uint4(0u, 0u, 0u, 0u);
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        const int bb = b0 + 2048 * i;
+        if (bb >= Bp) break;
+        const uint32_t* w = &v[i].x;
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+          const float x = __uint_as_float(k & 1 ? (w[k >> 1] & 0xFFFF0000u) : (w[k >> 1] << 16));
+          const int b = bb + k;
+          if (o < 2 * HW) sacc = __fadd_rn(sacc, x);
+          else if (b < B) sacc = o < 3 * HW ? __fmaf_rn(dq[(size_t)z * B + b], x, sacc) : __fadd_rn(sacc, dq[(size_t)z * B + b]);
+        }
+      }
+    }
+    for (int off = 16; off > 0; off >>= 1) sacc = __fadd_rn(sacc, __shfl_xor_sync(0xffffffffu, sacc, off));
+    __shared__ float red2[8];
+    if ((threadIdx.x & 31) == 0) red2[threadIdx.x >> 5] = sacc;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      float t = 0.f;
+      for (int w = 0; w < 8; ++w) t = __fadd_rn(t, red2[w]);
+      float* base = grad2 + z * P;
+      if (o < HW) base[oB1 + o] = t;
+      else if (o < 2 * HW) base[oB2 + (o - HW)] = t;
+      else if (o < 3 * HW) base[oW3 + (o - 2 * HW)] = t;
+      else base[oB3] = t;
+    }
+    return;
   }
+  const int o = big ? blockIdx.x : blockIdx.x * 8 + (threadIdx.x >> 5);
+  const int lane = big ? threadIdx.x : threadIdx.x & 31, nl = big ? 256 : 32;
+  if (o >= nout) return;
+  float s4[4] = {0.f, 0.f, 0.f, 0.f};
+  int b = lane;
+  for (; b + 3 * nl < B; b += 4 * nl) {
+#pragma unroll
+    for (int k = 0; k < 4; ++k) s4[k] = __fadd_rn(s4[k], bias_row_term(o, z, b + k * nl, Bp, B, dZ1T, dZ2T, dq, Hh2, H2T));
+  }
+  for (int k = 0; b < B; b += nl, ++k) s4[k & 3] = __fadd_rn(s4[k & 3], bias_row_term(o, z, b, Bp, B, dZ1T, dZ2T, dq, Hh2, H2T));
+  float s = __fadd_rn(__fadd_rn(s4[0], s4[1]), __fadd_rn(s4[2], s4[3]));
   for (int off = 16; off > 0; off >>= 1) s = __fadd_rn(s, __shfl_xor_sync(0xffffffffu, s, off));
+  if (big) {
+    __shared__ float red[8];
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = s;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      s = 0.f;
+      for (int w = 0; w < 8; ++w) s = __fadd_rn(s, red[w]);
+    }
+  }
   if (lane == 0) {
     float* base = grad2 + z * P;
     if (o < HW) base[oB1 + o] = s;
@@ -677,6 +764,166 @@ __global__ void __launch_bounds__(256) critic_loss_mma_kernel(int B, int nz, con
   if (threadIdx.x == 0 && loss) *loss = tot;
 }
 
+// ------------------------------------------------------------------ large batches (tcgen05 engine)
+// X^T = bf16([s; a])^T [inq64][Bp] (zero past in and past B), through a 32 x 32 shared tile (reads
+// coalesced along the input, writes along the batch); block (0, 0) also zeroes the loss ticket of
+// the data-backward launch.
+__global__ void __launch_bounds__(256) critic_xt_kernel(int B, int Bp, int S, int A, int rows,
+                                                        const float* __restrict__ obs, const float* __restrict__ act,
+                                                        __nv_bfloat16* __restrict__ XT, unsigned int* ticket) {
+  pdl_wait();
+  pdl_trigger();
+  __shared__ float tile[32][33];
+  const int b0 = blockIdx.x * 32, i0 = blockIdx.y * 32, tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
+  const int in = S + A;
+  if (ticket && blockIdx.x == 0 && blockIdx.y == 0 && threadIdx.x == 0) *ticket = 0u;
+#pragma unroll
+  for (int r = ty; r < 32; r += 8) {
+    const int b = b0 + r, i = i0 + tx;
+    float v = 0.f;
+    if (b < B && i < in) v = i < S ? obs[(size_t)b * S + i] : act[(size_t)b * A + (i - S)];
+    tile[r][tx] = v;
+  }
+  __syncthreads();
+#pragma unroll
+  for (int r = ty; r < 32; r += 8) {
+    const int i = i0 + r, b = b0 + tx;
+    if (i < rows && b < Bp) XT[(size_t)i * Bp + b] = __float2bfloat16_rn(tile[tx][r]);
+  }
+}
+
+// dQ (mode 0: 2 (Q_z - y)/B and the MSE; mode 1: act_scale, the actor loss -mean Q), then
+// dZ2^T = RN_bf16(dQ w3 [h2 > 0]) [z][H2][Bp]. A block owns 64 batch rows of one critic (thread =
+// row (tid & 63), hidden units tid >> 6 + 4 i); its loss partial is summed in row order and the
+// last block (ticket) adds the partials in (z, block) order: deterministic.
+__global__ void __launch_bounds__(256) critic_dz2_kernel(int B, int Bp, const float* __restrict__ q,
+                                                         const float* __restrict__ y, int mode, float act_scale,
+                                                         const float* __restrict__ dq_scale, float* __restrict__ dq,
+                                                         float* __restrict__ part, unsigned int* __restrict__ ticket,
+                                                         float* __restrict__ loss, const __nv_bfloat16* __restrict__ pb,
+                                                         long long P, long long oW3, const __nv_bfloat16* __restrict__ H2T,
+                                                         __nv_bfloat16* __restrict__ dZ2T) {
+  pdl_wait();
+  pdl_trigger();
+  __shared__ float dqs[64], cs[64], w3s[HW];
+  __shared__ bool last;
+  const int z = blockIdx.y, r = threadIdx.x & 63, b = blockIdx.x * 64 + r;
+  // w3 in shared memory (ncu r02: read from global inside the store loop, every hidden unit waited
+  // on its own L2 round trip: 38 us at B = 4096)
+  w3s[threadIdx.x] = __bfloat162float(pb[z * P + oW3 + threadIdx.x]);
+  if (threadIdx.x < 64) {
+    float d = 0.f, c = 0.f;
+    if (b < B) {
+      const float qv = q[(size_t)z * B + b];
+      if (mode == 0) {
+        const float e = __fsub_rn(qv, y[b]);
+        d = __fdiv_rn(__fmul_rn(2.0f, e), (float)B);
+        c = __fmul_rn(e, e);
+      } else {
+        d = act_scale;
+        c = qv;
+      }
+      if (dq_scale) d = __fmul_rn(d, *dq_scale);   // dynamic loss scaling (the loss stays unscaled)
+      dq[(size_t)z * B + b] = d;
+    }
+    dqs[r] = d;
+    cs[r] = c;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    float sum = 0.f;
+    for (int k = 0; k < 64; ++k) sum = __fadd_rn(sum, cs[k]);
+    part[z * gridDim.x + blockIdx.x] = sum;
+    __threadfence();
+    const unsigned int n = gridDim.x * gridDim.y;
+    last = atomicAdd(ticket, 1u) == n - 1;
+  }
+  __syncthreads();
+  if (last) {
+    __threadfence();
+    if (loss) final_loss(part, gridDim.x, gridDim.y, mode, B, loss);
+    if (threadIdx.x == 0) *ticket = 0u;
+  }
+  __syncthreads();   // dqs / w3s complete
+  // the block's 64 rows x 256 hidden units as 16-byte chunks of 8 rows: 8 chunks per thread, all
+  // loads issued before any store (ncu r02: one 2-byte load in flight per thread made this launch
+  // 35-38 us at configs[3] B = 4096)
+  const int b0 = blockIdx.x * 64;
+  uint4 hv[8];
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {
+    const int c = threadIdx.x + 256 * i, j = c >> 3, bo = (c & 7) * 8;
+    hv[i] = b0 + bo < Bp ? *reinterpret_cast<const uint4*>(H2T + ((size_t)z * HW + j) * Bp + b0 + bo)
+                         : make_uint4(0u, 0u, 0u, 0u);
+  }
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {
+    const int c = threadIdx.x + 256 * i, j = c >> 3, bo = (c & 7) * 8;
+    if (b0 + bo >= Bp) continue;
+    const uint32_t* hw = &hv[i].x;
+    uint32_t ow[4];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const float h0 = __uint_as_float(hw[k] << 16), h1 = __uint_as_float(hw[k] & 0xFFFF0000u);
+      const float v0 = h0 > 0.f ? __fmul_rn(dqs[bo + 2 * k], w3s[j]) : 0.f;
+      const float v1 = h1 > 0.f ? __fmul_rn(dqs[bo + 2 * k + 1], w3s[j]) : 0.f;
+      ow[k] = (uint32_t)__bfloat16_as_ushort(__float2bfloat16_rn(v0)) |
+              ((uint32_t)__bfloat16_as_ushort(__float2bfloat16_rn(v1)) << 16);
+    }
+    *reinterpret_cast<uint4*>(dZ2T + ((size_t)z * HW + j) * Bp + b0 + bo) = make_uint4(ow[0], ow[1], ow[2], ow[3]);
+  }
+}
+
+// grad_act[b][a] = sum_j dZ1[b][j] W1[j][S + a] (critic 0). A block owns 32 rows; warp w sums hidden
+// units [32 w, 32 w + 32) for every action of its lane's row (the W1T slice staged in shared memory,
+// read as warp-wide broadcasts), and the 8 partial sums meet in shared memory in warp order.
+constexpr int kGactMaxA = 32;
+__global__ void __launch_bounds__(256) critic_gact_kernel(int B, int Bp, int S, int A, const __nv_bfloat16* __restrict__ dZ1T,
+                                                          const __nv_bfloat16* __restrict__ W1T, float* __restrict__ grad_act) {
+  pdl_wait();
+  pdl_trigger();
+  // one buffer: first the W1T slice wsl[j][a] = W1[j][S + a], then the partial sums part[w][r][a]
+  __shared__ float sbuf[NWARP * 32 * (kGactMaxA + 1)];
+  static_assert(HW * kGactMaxA <= NWARP * 32 * (kGactMaxA + 1), "shared buffer");
+  float (*wsl)[kGactMaxA] = reinterpret_cast<float (*)[kGactMaxA]>(sbuf);
+  float (*part)[32][kGactMaxA + 1] = reinterpret_cast<float (*)[32][kGactMaxA + 1]>(sbuf);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  {   // the W1T slice, all loads issued before the shared-memory stores
+    float wv[kGactMaxA];
+#pragma unroll
+    for (int a = 0; a < kGactMaxA; ++a) wv[a] = a < A ? __bfloat162float(W1T[(size_t)(S + a) * HW + threadIdx.x]) : 0.f;
+#pragma unroll
+    for (int a = 0; a < kGactMaxA; ++a) wsl[threadIdx.x][a] = wv[a];
+  }
+  __syncthreads();
+  const int b = blockIdx.x * 32 + lane;
+  float acc[kGactMaxA];
+#pragma unroll
+  for (int a = 0; a < kGactMaxA; ++a) acc[a] = 0.f;
+  float dv[32];
+#pragma unroll
+  for (int u = 0; u < 32; ++u) dv[u] = b < Bp ? __bfloat162float(dZ1T[(size_t)(32 * warp + u) * Bp + b]) : 0.f;
+#pragma unroll
+  for (int u = 0; u < 32; ++u) {
+    const int j = 32 * warp + u;
+#pragma unroll
+    for (int a = 0; a < kGactMaxA; ++a)
+      if (a < A) acc[a] = __fmaf_rn(dv[u], wsl[j][a], acc[a]);
+  }
+  __syncthreads();   // every warp is done with wsl
+#pragma unroll
+  for (int a = 0; a < kGactMaxA; ++a)
+    if (a < A) part[warp][lane][a] = acc[a];
+  __syncthreads();
+  for (int i = threadIdx.x; i < 32 * A; i += 256) {
+    const int r = i / A, a = i - r * A, bb = blockIdx.x * 32 + r;
+    float s = 0.f;
+#pragma unroll
+    for (int w = 0; w < NWARP; ++w) s = __fadd_rn(s, part[w][r][a]);
+    if (bb < B) grad_act[(size_t)bb * A + a] = s;
+  }
+}
+
 }  // namespace
 
 bool critic_mma_ok(const CriticDims& c) { return c.bf16 && c.H1 == HW && c.H2 == HW && c.in <= 512; }
@@ -734,10 +981,98 @@ static bool tc_wgrad_ok(const CriticDims& c, const MmaWs& w, int Bp) {
          (const char*)w.H1T == (const char*)w.XT + (size_t)2 * round_up(L.inq, 64) * Bp;
 }
 
+// Large batches run the critic's contractions on the tcgen05 engine (batch on the MMA's M, the 256
+// hidden units on its N): ~50 us per forward of the warp-MMA kernels at configs[3] B = 4096, whose
+// 16-row tiles re-read W1 from L2 per tile (SPIKERL_CRITIC_TC=0 keeps the warp-MMA path).
+static bool critic_tc_ok(const CriticDims& c, int B) {
+  static const int env = [] { const char* e = getenv("SPIKERL_CRITIC_TC"); return e ? atoi(e) : 1; }();
+  return env != 0 && c.bf16 && c.H1 == HW && c.H2 == HW && B >= 1024;
+}
+
+static int critic_tc_fwd_bwd(const CriticDims& c, int B, const float* params2, const __nv_bfloat16* pb, const float* obs,
+                             int S, const float* act, int A, const float* y, float* q, float* loss, float* grad2,
+                             float* grad_act, float act_scale, int nz, void* ws, cudaStream_t st,
+                             cudaEvent_t wait_before_loss, const float* dq_scale) {
+  const MmaLayout L = mma_layout(c);
+  MmaWs w = mma_carve(c, B, ws, nullptr);
+  const int Bp = round_up(B, RB);
+  const bool want_params = (y != nullptr && grad2 != nullptr);
+  const bool need_bwd = want_params || grad_act != nullptr;
+  const long long oW3 = (long long)c.off[SPIKERL_CRITIC_W3];
+  const __nv_bfloat16* blk = pb + blk_base(L.P);
+  const int xrows = round_up(L.inq, 64);
+  const long long os = (long long)HW * Bp;
+  {
+    ProfScope ps_("critic_fwd_tc", PB_TENSOR, 2.0 * B * nz * ((double)c.in * HW + (double)HW * HW + HW), 0.0, st);
+    pdl(critic_xt_kernel, dim3((unsigned)cdiv(Bp, 32), (unsigned)cdiv(xrows, 32)), 256, 0, st)(
+        B, Bp, S, A, xrows, obs, act, w.XT, need_bwd ? w.ticket : nullptr);
+    SPK_LAUNCHED();
+    // layer 1: H1T = RN(relu(X W1^T + b1))^T
+    SPK_TRY(launch_critic_tc(6, B, Bp, nz, w.XT, xrows, 0, blk + L.W1p, blk + L.tb + L.W1p, L.inp, L.inp,
+                             params2 + c.off[SPIKERL_CRITIC_B1], nullptr, nullptr, L.P, w.H1T, os, nullptr, nullptr,
+                             st));
+    // layer 2 + output: H2T = RN(relu(H1 W2^T + b2))^T, q = h2 . w3 + b3
+    SPK_TRY(launch_critic_tc(7, B, Bp, nz, w.H1T, 2 * HW, HW, blk + L.W2c, blk + L.tb + L.W2c, HW, HW,
+                             params2 + c.off[SPIKERL_CRITIC_B2], pb + oW3, params2 + c.off[SPIKERL_CRITIC_B3], L.P,
+                             w.H2T, os, nullptr, q, st));
+  }
+  if (wait_before_loss) SPK_CHECK_CUDA(cudaStreamWaitEvent(st, wait_before_loss, 0));
+  if (!need_bwd) {
+    if (y) {
+      pdl(critic_loss_mma_kernel, 1, 256, 0, st)(B, nz, q, y, w.dq, loss);
+      SPK_LAUNCHED();
+    }
+    return SPIKERL_OK;
+  }
+  const int mode = want_params ? 0 : 1;
+  const int nb = want_params ? nz : 1;
+  {
+    ProfScope ps_("critic_bwd_data_tc", PB_TENSOR, 2.0 * B * nb * ((double)HW * HW), 0.0, st);
+    pdl(critic_dz2_kernel, dim3((unsigned)cdiv(Bp, 64), (unsigned)nb), 256, 0, st)(
+        B, Bp, q, y, mode, act_scale, dq_scale, w.dq, w.part, w.ticket, (want_params || !y) ? loss : nullptr, pb, L.P,
+        oW3, w.H2T, w.dZ2T);
+    SPK_LAUNCHED();
+    // dZ1T = RN(dZ2 W2 [h1 > 0])^T
+    SPK_TRY(launch_critic_tc(8, B, Bp, nb, w.dZ2T, 2 * HW, HW, blk + L.W2T, blk + L.tb + L.W2T, HW, HW, nullptr,
+                             nullptr, nullptr, L.P, w.dZ1T, os, w.H1T, nullptr, st));
+    if (grad_act) {
+      if (A > kGactMaxA) { set_error("critic tc path: action dim %d > %d", A, kGactMaxA); return SPIKERL_E_UNSUPPORTED; }
+      pdl(critic_gact_kernel, dim3((unsigned)cdiv(B, 32)), 256, 0, st)(B, Bp, S, A, w.dZ1T, blk + L.W1T, grad_act);
+      SPK_LAUNCHED();
+    }
+  }
+  if (want_params) {
+    AuxPool* aux = nullptr;
+    SPK_TRY(aux_pool(&aux));
+    cudaStream_t sb = aux->side[6];
+    SPK_TRY(stream_after(sb, st, aux->ev[16]));
+    pdl(critic_bias_grads_kernel, dim3(3 * HW + 1, nz), 256, 0, sb)(
+        B, Bp, L.P, (long long)c.off[SPIKERL_CRITIC_B1], (long long)c.off[SPIKERL_CRITIC_B2], oW3,
+        (long long)c.off[SPIKERL_CRITIC_B3], w.dZ1T, w.dZ2T, w.dq, (const float*)nullptr,
+        (const __nv_bfloat16*)w.H2T, grad2);
+    SPK_LAUNCHED();
+    {
+      ProfScope ps_("critic_wgrad_tc", PB_TENSOR, 2.0 * B * nz * ((double)HW * HW + (double)HW * c.in), 0.0, st);
+      if (!tc_wgrad_ok(c, w, Bp)) { set_error("critic tc path: weight-gradient operands not adjacent"); return SPIKERL_E_UNSUPPORTED; }
+      const long long msz = (long long)HW * HW + (long long)HW * L.inq;
+      SPK_TRY(launch_critic_wgrad_tc(Bp, L.inq, round_up(L.inq, 64), w.dZ2T, w.XT, w.wpart, msz, st));
+      const int splits = tc_wgrad_splits(Bp, L.inq);
+      pdl(critic_wgrad_reduce_kernel, 148 * 4, 256, 0, st)(splits, c.in, L.inq, L.P, (long long)c.off[SPIKERL_CRITIC_W1],
+                                                         (long long)c.off[SPIKERL_CRITIC_W2], w.wpart, grad2);
+      SPK_LAUNCHED();
+    }
+    SPK_TRY(stream_after(st, sb, aux->ev[17]));
+  }
+  return SPIKERL_OK;
+}
+
 int critic_mma_fwd_bwd(const CriticDims& c, int B, const float* params2, const __nv_bfloat16* pb, const float* obs,
                        int S, const float* act, int A, const float* y, float* q, float* loss, float* grad2,
                        float* grad_act, float act_scale, int nz, void* ws, cudaStream_t st,
                        cudaEvent_t wait_before_loss, const float* dq_scale) {
+  if (critic_tc_ok(c, B))
+    return critic_tc_fwd_bwd(c, B, params2, pb, obs, S, act, A, y, q, loss, grad2, grad_act, act_scale, nz, ws, st,
+                             wait_before_loss, dq_scale);
   const MmaLayout L = mma_layout(c);
   MmaWs w = mma_carve(c, B, ws, nullptr);
   const int Bp = round_up(B, RB);
@@ -784,7 +1119,7 @@ int critic_mma_fwd_bwd(const CriticDims& c, int B, const float* params2, const _
     SPK_TRY(stream_after(sb, st, aux->ev[16]));
     pdl(critic_bias_grads_kernel, dim3(cdiv(3 * HW + 1, 8), nz), 256, 0, sb)(
         B, Bp, L.P, (long long)c.off[SPIKERL_CRITIC_B1], (long long)c.off[SPIKERL_CRITIC_B2], oW3,
-        (long long)c.off[SPIKERL_CRITIC_B3], w.dZ1T, w.dZ2T, w.dq, w.Hh2, grad2);
+        (long long)c.off[SPIKERL_CRITIC_B3], w.dZ1T, w.dZ2T, w.dq, w.Hh2, (const __nv_bfloat16*)nullptr, grad2);
     SPK_LAUNCHED();
     {
       ProfScope ps_("critic_wgrad_mma", PB_TENSOR, 2.0 * B * nz * ((double)HW * HW + (double)HW * c.in), 0.0, st);

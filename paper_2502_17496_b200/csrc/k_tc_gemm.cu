@@ -32,8 +32,15 @@ namespace tc {
 // FWDO: output layer (batch-major spike and mask planes + spike counts)
 // WG: the critic's weight-gradient GEMMs dW = dZ^T X (both operands K-major bf16 by TMA, K = batch),
 // split over K, fp32 partial tiles per (job, split)
-enum Mode { FWD = 0, DX = 1, ENC = 2, DW = 3, FWDO = 4, WG = 5 };
+// CF1 / CF2 / CB1: the twin critic's large-batch contractions (batch on the MMA's M = TMEM lanes,
+// the 256 hidden units on its N), A = the batch-contiguous transposed activations (MN-major), B =
+// the critic's bf16 weights (K-major, one map per critic: tmB critic 0, tmC critic 1):
+//   CF1  Z1 = X W1^T     -> b1, ReLU, bf16: H1T [2][H1][Bp]
+//   CF2  Z2 = H1 W2^T    -> b2, ReLU, bf16: H2T [2][H2][Bp], q = h2 . w3 + b3
+//   CB1  dH1 = dZ2 W2    -> ReLU mask (h1 > 0), bf16: dZ1T [2][H1][Bp]
+enum Mode { FWD = 0, DX = 1, ENC = 2, DW = 3, FWDO = 4, WG = 5, CF1 = 6, CF2 = 7, CB1 = 8 };
 __host__ __device__ constexpr bool is_fwd(int m) { return m == FWD || m == FWDO; }
+__host__ __device__ constexpr bool is_crit(int m) { return m == CF1 || m == CF2 || m == CB1; }
 
 constexpr int BM = 128, BK = 64, STAGES = 4;
 constexpr int A_STAGE = BM * BK * 2;             // 16 KB
@@ -81,6 +88,11 @@ struct Params {
   // WG jobs (critic weight gradients): A / B row bases in the stacked operand maps, partial offset
   // (elements, within one split), row stride and valid columns of the output tile
   int wg_njobs; int wg_arow[8], wg_brow[8], wg_ld[8], wg_ncol[8]; long long wg_off[8];
+  // critic modes: per-critic fp32 biases / bf16 w3 (stride cr_ps elements between critics), the
+  // transposed bf16 output [2][256][Bp] (critic stride cr_os), CB1's ReLU mask source (H1T), q out,
+  // A's K-row offset per critic (H1T / dZ2T hold both critics' rows; XT is shared)
+  const float* cr_bias; const __nv_bfloat16* cr_w3; const float* cr_b3; long long cr_ps;
+  __nv_bfloat16* cr_out; long long cr_os; int cr_Bp; const __nv_bfloat16* cr_mask; float* cr_q; int cr_aoff;
   int f16;          // 16-bit operands are fp16 (actor FP16 precision), else bf16
   uint32_t one2;    // two 16-bit 1.0 values: 0x3F803F80 (bf16) / 0x3C003C00 (fp16), the expanded spike
   int trace;   // diagnostics: CTA 0 stamps %globaltimer at phase boundaries into g_trace
@@ -384,7 +396,8 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     // ===================== TMA producer (both CTAs load their own halves) =====================
     if (lane == 0) {
       uint32_t it = 0;
-      const uint32_t bytes_b = (MODE == DX) ? 128u * p.T * p.Bt / CG : ((MODE == ENC || MODE == WG) ? 128u * p.BN / CG : 0u);
+      const uint32_t bytes_b = (MODE == DX) ? 128u * p.T * p.Bt / CG
+                               : ((MODE == ENC || MODE == WG || is_crit(MODE)) ? 128u * p.BN / CG : 0u);
       for (int u = cid; u < p.n_units; u += ncl) {
         const Tile t = decode<MODE>(p, u, rank, CG);
         for (int kb = t.kb0; kb < t.kb1; ++kb, ++it) {
@@ -397,12 +410,15 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
             if (CG == 1 || rank == 0) mbar_arrive(&full[stage]);
           } else if (CG == 1) {
             mbar_expect_tx(&full[stage], (uint32_t)A_STAGE + bytes_b);
+            // critic modes: A's K rows of critic t.n start at t.n * cr_aoff (H1T / dZ2T stack both)
+            const int ka = kb * BK + (is_crit(MODE) ? t.n * p.cr_aoff : 0);
             if (!A_MN) {
               tma_2d(&tmA, sA, &full[stage], kb * BK, t.m * BM);
             } else {
-              tma_2d(&tmA, sA, &full[stage], t.m * BM, kb * BK);
-              tma_2d(&tmA, sA + 8192, &full[stage], t.m * BM + 64, kb * BK);
+              tma_2d(&tmA, sA, &full[stage], t.m * BM, ka);
+              tma_2d(&tmA, sA + 8192, &full[stage], t.m * BM + 64, ka);
             }
+            if (is_crit(MODE)) tma_2d(t.n == 0 ? &tmB : &tmC, sB, &full[stage], kb * BK, 0);
             if (MODE == DX) tma_3d(&tmB, sB, &full[stage], kb * BK, t.n * p.Bt, 0);
             if (MODE == ENC) tma_2d(&tmB, sB, &full[stage], kb * BK, t.n * p.BN);
             if (it == 0) trace_stamp(p, 2);
@@ -878,6 +894,54 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
           p.partial[(((size_t)t.n * NUM_EPI_GROUPS + g) * p.K0 + row) * 2 + 0] = __fdiv_rn(pm, sg2);
           p.partial[(((size_t)t.n * NUM_EPI_GROUPS + g) * p.K0 + row) * 2 + 1] = __fdiv_rn(ps, sg3);
         }
+      } else if constexpr (is_crit(MODE)) {
+        // thread = batch row b (TMEM lane), group g = hidden units [128 g, 128 g + 128); outputs are
+        // transposed [z][n][Bp] (lanes = consecutive rows: 64-byte coalesced stores per column)
+        const int z = t.n;
+        const int b = t.m * BM + 32 * q + lane;
+        const bool bv = b < p.B, bs = b < p.cr_Bp;
+        const int c0 = g * 128;
+        const float* bias = p.cr_bias + (size_t)z * p.cr_ps;
+        __nv_bfloat16* out = p.cr_out + (size_t)z * p.cr_os + (bs ? b : 0);
+        const __nv_bfloat16* msk = MODE == CB1 ? p.cr_mask + (size_t)z * p.cr_os + (bs ? b : 0) : nullptr;
+        const __nv_bfloat16* w3 = MODE == CF2 ? p.cr_w3 + (size_t)z * p.cr_ps : nullptr;
+        float qacc = 0.f;
+        for (int j1 = 0; j1 < 128; j1 += 32) {
+          uint32_t rr[4][8];
+#pragma unroll
+          for (int ci = 0; ci < 4; ++ci) tmem_ld8(taddr + c0 + j1 + 8 * ci, rr[ci]);
+          unsigned short mk[32];
+          if constexpr (MODE == CB1) {
+#pragma unroll
+            for (int e = 0; e < 32; ++e) mk[e] = bs ? __bfloat16_as_ushort(msk[(size_t)(c0 + j1 + e) * p.cr_Bp]) : 0;
+          }
+          tmem_ld_wait();
+#pragma unroll
+          for (int e = 0; e < 32; ++e) {
+            const int n = c0 + j1 + e;
+            const float v = __uint_as_float(rr[e >> 3][e & 7]);
+            __nv_bfloat16 o;
+            if constexpr (MODE == CB1) {
+              // relu'(z1) from the stored h1 = RN_bf16(relu(z1)) > 0 (R31)
+              const bool m = (mk[e] & 0x7FFFu) != 0 && !(mk[e] & 0x8000u);
+              o = __float2bfloat16_rn(bv && m ? v : 0.f);
+            } else {
+              const float zz = __fadd_rn(v, __ldg(bias + n));
+              const float h = bv ? fmaxf(zz, 0.f) : 0.f;
+              o = __float2bfloat16_rn(h);
+              if constexpr (MODE == CF2) qacc = __fmaf_rn(__bfloat162float(o), __bfloat162float(w3[n]), qacc);
+            }
+            if (bs) out[(size_t)n * p.cr_Bp] = o;
+          }
+        }
+        if constexpr (MODE == CF2) {
+          // q = (sum over units 0..127 + sum over 128..255) + b3, the halves meeting in shared memory
+          __shared__ float qx[BM];
+          if (g == 1) qx[32 * q + lane] = qacc;
+          epi_bar_sync();
+          if (g == 0 && bv) p.cr_q[(size_t)z * p.B + b] = __fadd_rn(__fadd_rn(qacc, qx[32 * q + lane]), p.cr_b3[(size_t)z * p.cr_ps]);
+          epi_bar_sync();
+        }
       } else if constexpr (MODE == WG) {
         // dump the fp32 tile of this (job, split): row = output row within the job's 256, group g
         // covers columns [128 g, 128 g + 128); columns past the job's width are not stored
@@ -1098,16 +1162,20 @@ static int launch(const CUtensorMap& ma, const CUtensorMap& mb, const CUtensorMa
   p.dbg = dbg;
   // fp16 operands (actor FP16 precision) are a separate instantiation: the G conversions and the
   // MMA instruction descriptor are then compile-time (a runtime switch cost ~2% at configs[4])
-  if (MODE != WG && p.f16)
-    return p.cg == 2 ? launch_cg<MODE, BT, 2, true>(ma, mb, mc, p, st) : launch_cg<MODE, BT, 1, true>(ma, mb, mc, p, st);
-  return p.cg == 2 ? launch_cg<MODE, BT, 2, false>(ma, mb, mc, p, st) : launch_cg<MODE, BT, 1, false>(ma, mb, mc, p, st);
+  if constexpr (is_crit(MODE)) {   // bf16, single CTAs only
+    return launch_cg<MODE, BT, 1, false>(ma, mb, mc, p, st);
+  } else {
+    if (MODE != WG && p.f16)
+      return p.cg == 2 ? launch_cg<MODE, BT, 2, true>(ma, mb, mc, p, st) : launch_cg<MODE, BT, 1, true>(ma, mb, mc, p, st);
+    return p.cg == 2 ? launch_cg<MODE, BT, 2, false>(ma, mb, mc, p, st) : launch_cg<MODE, BT, 1, false>(ma, mb, mc, p, st);
+  }
 }
 
 template <int MODE>
 static int launch_bt(int bt, const CUtensorMap& ma, const CUtensorMap& mb, const Params& p, cudaStream_t st,
                      const CUtensorMap* mc = nullptr) {
   const CUtensorMap& c = mc ? *mc : ma;   // store map (DX only)
-  if (MODE == ENC || MODE == DW || MODE == WG) return launch<MODE, 8>(ma, mb, c, p, st);
+  if (MODE == ENC || MODE == DW || MODE == WG || is_crit(MODE)) return launch<MODE, 8>(ma, mb, c, p, st);
   switch (bt) {
     case 8: return launch<MODE, 8>(ma, mb, c, p, st);
     case 16: return launch<MODE, 16>(ma, mb, c, p, st);
@@ -1400,6 +1468,47 @@ int launch_critic_wgrad_tc(int Bp, int inq, int xtr, const __nv_bfloat16* dZT, c
   }
   ProfScope ps_("critic_wgrad_tc", PB_TENSOR, 2.0 * 2 * Bp * ((double)HWc * HWc + (double)HWc * inq), 0.0, st);
   return launch_bt<WG>(8, ma, mb, p, st);
+}
+
+// ---- twin critic contractions at large batches (modes CF1 / CF2 / CB1; see the Mode enum)
+// A: bf16 [a_rows][Bp] (batch contiguous; critic z's K rows start at z * aoff); B: critic z's bf16
+// weight rows [256][ldb] (K extent bk), Bw0 / Bw1; outputs transposed [z][256][Bp] (stride os).
+int launch_critic_tc(int mode, int B, int Bp, int nz, const __nv_bfloat16* A, int a_rows, int aoff,
+                     const __nv_bfloat16* Bw0, const __nv_bfloat16* Bw1, int bk, int ldb, const float* bias,
+                     const __nv_bfloat16* w3, const float* b3, long long ps, __nv_bfloat16* out, long long os,
+                     const __nv_bfloat16* mask, float* q, cudaStream_t st) {
+  Params p{};
+  p.one2 = 0x3F803F80u;
+  p.B = B;
+  p.BN = 256;
+  p.cg = 1;
+  p.m_tiles = cdiv(Bp, BM);
+  p.n_tiles = nz;
+  p.k_blocks = cdiv(bk, BK);
+  p.n_units = p.m_tiles * nz;
+  p.cr_bias = bias; p.cr_w3 = w3; p.cr_b3 = b3; p.cr_ps = ps;
+  p.cr_out = out; p.cr_os = os; p.cr_Bp = Bp; p.cr_mask = mask; p.cr_q = q; p.cr_aoff = aoff;
+  CUtensorMap ma, mb, mc;
+  {
+    const uint64_t dims[2] = {(uint64_t)Bp, (uint64_t)a_rows};
+    const uint64_t strides[1] = {(uint64_t)Bp * 2};
+    const uint32_t box[2] = {64, 64};
+    SPK_TRY(make_map(&ma, A, 2, dims, strides, box));
+  }
+  {
+    const uint64_t dims[2] = {(uint64_t)bk, 256};
+    const uint64_t strides[1] = {(uint64_t)ldb * 2};
+    const uint32_t box[2] = {64, 256};
+    SPK_TRY(make_map(&mb, Bw0, 2, dims, strides, box));
+    SPK_TRY(make_map(&mc, Bw1 ? Bw1 : Bw0, 2, dims, strides, box));
+  }
+  switch (mode) {
+    case CF1: return launch_bt<CF1>(8, ma, mb, p, st, &mc);
+    case CF2: return launch_bt<CF2>(8, ma, mb, p, st, &mc);
+    case CB1: return launch_bt<CB1>(8, ma, mb, p, st, &mc);
+  }
+  set_error("launch_critic_tc: bad mode %d", mode);
+  return SPIKERL_E_ARG;
 }
 
 }  // namespace spk

@@ -275,8 +275,11 @@ def test_forward_deterministic_and_accumulate():
 # ------------------------------------------------------------------ critic
 @pytest.mark.parametrize("prec,B,S,A", [("fp32", 100, 17, 6), ("bf16", 256, 17, 6), ("bf16", 4096, 17, 6),
                                         ("bf16", 100, 376, 17), ("bf16", 512, 111, 8), ("bf16", 37, 17, 6),
-                                        ("bf16", 1040, 376, 17), ("bf16", 4096, 376, 17)])
+                                        ("bf16", 1040, 376, 17), ("bf16", 4096, 376, 17), ("bf16", 1500, 17, 6),
+                                        ("bf16", 1024, 111, 8)])
 def test_critic_parity(prec, B, S, A):
+    """fp32 SIMT critic, the warp-MMA bf16 critic (B < 1024) and the tcgen05 bf16 critic (B >= 1024:
+    configs[3] B = 4096, a ragged 1500, the 1024 threshold) against the oracle."""
     import torch
     import paper_2502_17496_b200 as pk
     rng = np.random.default_rng(5)
