@@ -982,11 +982,15 @@ static bool tc_wgrad_ok(const CriticDims& c, const MmaWs& w, int Bp) {
 }
 
 // Large batches run the critic's contractions on the tcgen05 engine (batch on the MMA's M, the 256
-// hidden units on its N): ~50 us per forward of the warp-MMA kernels at configs[3] B = 4096, whose
-// 16-row tiles re-read W1 from L2 per tile (SPIKERL_CRITIC_TC=0 keeps the warp-MMA path).
+// hidden units on its N). Measured crossover (tools/critic_timing.py, r02): at B = 4096 the update's
+// forward + backward takes 65 us against 183 us for the warp-MMA kernels (whose 16-row tiles re-read
+// W1 from L2 per tile) and the forward 25 against 39 us; at B = 1024 the warp-MMA kernels are still
+// ahead (83 against 102 us per TD3 update: each tcgen05 launch is one unit deep there), so the
+// engine switches at B >= 2048. SPIKERL_CRITIC_TC: 0 = never, 2 = from B = 512 on (tests; the
+// weight-gradient launch's split-K plan assumes a few 64-row k-blocks, so never below that).
 static bool critic_tc_ok(const CriticDims& c, int B) {
   static const int env = [] { const char* e = getenv("SPIKERL_CRITIC_TC"); return e ? atoi(e) : 1; }();
-  return env != 0 && c.bf16 && c.H1 == HW && c.H2 == HW && B >= 1024;
+  return env != 0 && c.bf16 && c.H1 == HW && c.H2 == HW && B >= (env == 2 ? 512 : 2048);
 }
 
 static int critic_tc_fwd_bwd(const CriticDims& c, int B, const float* params2, const __nv_bfloat16* pb, const float* obs,

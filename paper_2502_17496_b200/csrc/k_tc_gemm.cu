@@ -410,15 +410,17 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
             if (CG == 1 || rank == 0) mbar_arrive(&full[stage]);
           } else if (CG == 1) {
             mbar_expect_tx(&full[stage], (uint32_t)A_STAGE + bytes_b);
-            // critic modes: A's K rows of critic t.n start at t.n * cr_aoff (H1T / dZ2T stack both)
-            const int ka = kb * BK + (is_crit(MODE) ? t.n * p.cr_aoff : 0);
+            // critic modes: unit column t.n = critic z * (256 / BN) + hidden block; A's K rows of
+            // critic z start at z * cr_aoff (H1T / dZ2T stack both critics)
+            const int cz = is_crit(MODE) ? t.n / (256 / p.BN) : 0, ch = is_crit(MODE) ? t.n % (256 / p.BN) : 0;
+            const int ka = kb * BK + (is_crit(MODE) ? cz * p.cr_aoff : 0);
             if (!A_MN) {
               tma_2d(&tmA, sA, &full[stage], kb * BK, t.m * BM);
             } else {
               tma_2d(&tmA, sA, &full[stage], t.m * BM, ka);
               tma_2d(&tmA, sA + 8192, &full[stage], t.m * BM + 64, ka);
             }
-            if (is_crit(MODE)) tma_2d(t.n == 0 ? &tmB : &tmC, sB, &full[stage], kb * BK, 0);
+            if (is_crit(MODE)) tma_2d(cz == 0 ? &tmB : &tmC, sB, &full[stage], kb * BK, ch * p.BN);
             if (MODE == DX) tma_3d(&tmB, sB, &full[stage], kb * BK, t.n * p.Bt, 0);
             if (MODE == ENC) tma_2d(&tmB, sB, &full[stage], kb * BK, t.n * p.BN);
             if (it == 0) trace_stamp(p, 2);
@@ -897,28 +899,30 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       } else if constexpr (is_crit(MODE)) {
         // thread = batch row b (TMEM lane), group g = hidden units [128 g, 128 g + 128); outputs are
         // transposed [z][n][Bp] (lanes = consecutive rows: 64-byte coalesced stores per column)
-        const int z = t.n;
+        const int nh = 256 / p.BN;                  // hidden blocks per critic (CF1 / CB1: 2, CF2: 1)
+        const int z = t.n / nh, hb = t.n % nh;
         const int b = t.m * BM + 32 * q + lane;
         const bool bv = b < p.B, bs = b < p.cr_Bp;
-        const int c0 = g * 128;
+        const int gc = p.BN / NUM_EPI_GROUPS;       // accumulator columns of this group
+        const int c0 = g * gc, n0 = hb * p.BN + c0;  // TMEM column, hidden unit of the group's first
         const float* bias = p.cr_bias + (size_t)z * p.cr_ps;
         __nv_bfloat16* out = p.cr_out + (size_t)z * p.cr_os + (bs ? b : 0);
         const __nv_bfloat16* msk = MODE == CB1 ? p.cr_mask + (size_t)z * p.cr_os + (bs ? b : 0) : nullptr;
         const __nv_bfloat16* w3 = MODE == CF2 ? p.cr_w3 + (size_t)z * p.cr_ps : nullptr;
         float qacc = 0.f;
-        for (int j1 = 0; j1 < 128; j1 += 32) {
+        for (int j1 = 0; j1 < gc; j1 += 32) {
           uint32_t rr[4][8];
 #pragma unroll
           for (int ci = 0; ci < 4; ++ci) tmem_ld8(taddr + c0 + j1 + 8 * ci, rr[ci]);
           unsigned short mk[32];
           if constexpr (MODE == CB1) {
 #pragma unroll
-            for (int e = 0; e < 32; ++e) mk[e] = bs ? __bfloat16_as_ushort(msk[(size_t)(c0 + j1 + e) * p.cr_Bp]) : 0;
+            for (int e = 0; e < 32; ++e) mk[e] = bs ? __bfloat16_as_ushort(msk[(size_t)(n0 + j1 + e) * p.cr_Bp]) : 0;
           }
           tmem_ld_wait();
 #pragma unroll
           for (int e = 0; e < 32; ++e) {
-            const int n = c0 + j1 + e;
+            const int n = n0 + j1 + e;
             const float v = __uint_as_float(rr[e >> 3][e & 7]);
             __nv_bfloat16 o;
             if constexpr (MODE == CB1) {
@@ -1480,12 +1484,15 @@ int launch_critic_tc(int mode, int B, int Bp, int nz, const __nv_bfloat16* A, in
   Params p{};
   p.one2 = 0x3F803F80u;
   p.B = B;
-  p.BN = 256;
+  // CF1 / CB1 units cover half of the hidden units (N = 128: twice the CTAs, each with half the MMA
+  // and epilogue work: a launch is one unit deep at B = 4096, so this halves its latency); CF2 keeps
+  // N = 256 so its epilogue forms q = h2 . w3 over every hidden unit
+  p.BN = mode == CF2 ? 256 : 128;
   p.cg = 1;
   p.m_tiles = cdiv(Bp, BM);
-  p.n_tiles = nz;
+  p.n_tiles = nz * (256 / p.BN);
   p.k_blocks = cdiv(bk, BK);
-  p.n_units = p.m_tiles * nz;
+  p.n_units = p.m_tiles * p.n_tiles;
   p.cr_bias = bias; p.cr_w3 = w3; p.cr_b3 = b3; p.cr_ps = ps;
   p.cr_out = out; p.cr_os = os; p.cr_Bp = Bp; p.cr_mask = mask; p.cr_q = q; p.cr_aoff = aoff;
   CUtensorMap ma, mb, mc;
@@ -1498,7 +1505,7 @@ int launch_critic_tc(int mode, int B, int Bp, int nz, const __nv_bfloat16* A, in
   {
     const uint64_t dims[2] = {(uint64_t)bk, 256};
     const uint64_t strides[1] = {(uint64_t)ldb * 2};
-    const uint32_t box[2] = {64, 256};
+    const uint32_t box[2] = {64, (uint32_t)p.BN};
     SPK_TRY(make_map(&mb, Bw0, 2, dims, strides, box));
     SPK_TRY(make_map(&mc, Bw1 ? Bw1 : Bw0, 2, dims, strides, box));
   }

@@ -278,8 +278,8 @@ def test_forward_deterministic_and_accumulate():
                                         ("bf16", 1040, 376, 17), ("bf16", 4096, 376, 17), ("bf16", 1500, 17, 6),
                                         ("bf16", 1024, 111, 8)])
 def test_critic_parity(prec, B, S, A):
-    """fp32 SIMT critic, the warp-MMA bf16 critic (B < 1024) and the tcgen05 bf16 critic (B >= 1024:
-    configs[3] B = 4096, a ragged 1500, the 1024 threshold) against the oracle."""
+    """fp32 SIMT critic, the warp-MMA bf16 critic (B < 2048) and the tcgen05 bf16 critic (B >= 2048:
+    configs[3] B = 4096, configs[1] widths at 4096) against the oracle."""
     import torch
     import paper_2502_17496_b200 as pk
     rng = np.random.default_rng(5)
@@ -350,6 +350,23 @@ def test_adam_and_polyak():
 
 
 # ------------------------------------------------------------------ TD3 update (oracle parity: tests/test_gpu_td3_parity.py)
+def test_critic_tcgen05_small_and_ragged_subprocess():
+    """The tcgen05 critic forced below its default threshold (SPIKERL_CRITIC_TC=2: B >= 512, a
+    subprocess): configs[2] widths at 512, ragged batches whose last 128-row tile ends in a partly
+    (1500) or wholly (1450) out-of-bounds TMA box, against the oracle through the same checks."""
+    import os, subprocess, sys
+    code = (
+        "import sys; sys.argv = ['x']\n"
+        "import tests.test_gpu_parity as t\n"
+        "for args in (('bf16', 512, 111, 8), ('bf16', 1500, 376, 17), ('bf16', 1450, 17, 6)):\n"
+        "    t.test_critic_parity(*args)\n"
+        "print('tc critic ok')\n")
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    r = subprocess.run([sys.executable, "-c", code], cwd=root, capture_output=True, text=True, timeout=600,
+                       env=dict(os.environ, SPIKERL_CRITIC_TC="2", PYTHONPATH=root))
+    assert r.returncode == 0 and "tc critic ok" in r.stdout, r.stdout[-2000:] + r.stderr[-2000:]
+
+
 @pytest.mark.parametrize("obs,act", [(17, 6), (111, 8)])
 def test_td3_bf16_copies_track_masters(obs, act):
     """Adam / Polyak write the bf16 working copies in place (Bf16Views): after several updates they
