@@ -45,6 +45,8 @@ def parse():
     ap.add_argument("--workload", default="cfg4", choices=["cfg0", "cfg1", "cfg2", "cfg3s", "cfg3L", "cfg4"])
     ap.add_argument("--no-td3-extra", action="store_true", help="cfg4: skip the configs[3] B=4096 TD3 keys")
     ap.add_argument("--eager", action="store_true", help="actor workloads: eager launches instead of a graph")
+    ap.add_argument("--fused-dp", action="store_true",
+                    help="TD3 with a communicator: the fused gradient-mean + Adam kernel over NCCL symmetric memory")
     ap.add_argument("--single-graphs", action="store_true",
                     help="TD3: replay one graph per update instead of overlapped update pairs")
     ap.add_argument("--engine", default="auto", choices=["auto", "simt", "tcgen05"])
@@ -201,7 +203,7 @@ def max_over_ranks(x, world):
 
 
 # ---------------------------------------------------------------------------------- workloads
-def build_td3(name, world, rank, engine, replay_size, seed=0):
+def build_td3(name, world, rank, engine, replay_size, seed=0, fused=False):
     import numpy as np
     import synthgen as sg
     import paper_2502_17496_b200 as pk
@@ -210,7 +212,7 @@ def build_td3(name, world, rank, engine, replay_size, seed=0):
     ccfg = pk.critic_cfg(cshape.in_dim, precision=shape.precision)
     replay = pk.replay_fill(replay_size, shape.obs_dim, shape.act_dim, seed=seed, rank=rank)
     comm = pk.Comm(rank, world) if (world > 1 or FORCE_COMM) else None
-    td3 = pk.TD3(acfg, ccfg, pk.td3_cfg(B), replay, seed=seed, comm=comm)
+    td3 = pk.TD3(acfg, ccfg, pk.td3_cfg(B), replay, seed=seed, comm=comm, fused=fused)
     rng = np.random.default_rng(seed)
     td3.load(sg.actor_params(shape, rng), sg.critic_params(cshape, rng), sg.critic_params(cshape, rng))
     return td3, shape, B
@@ -395,7 +397,7 @@ def run_td3(args, rank, world, workload):
     import torch
     import paper_2502_17496_b200 as pk
     from paper_2502_17496_b200 import _lib
-    td3, shape, B = build_td3(workload, world, rank, args.engine, args.replay_size)
+    td3, shape, B = build_td3(workload, world, rank, args.engine, args.replay_size, fused=args.fused_dp)
     # updates 2j+1, 2j+2 as one overlapped graph (spikerl_td3_update_pair: bitwise the same state as
     # two sequential updates, tested) unless --single-graphs
     pair = td3.hp.policy_delay == 2 and not args.single_graphs
@@ -418,7 +420,9 @@ def run_td3(args, rank, world, workload):
             launches["pair"] = lib.spikerl_launch_count(1)
     summ = _profile_pass(prof_fn)
     dom = max(summ, key=lambda e: e["total_ms"])["name"]
-    watch = _lib.Watch(dom, 64)
+    # at most two watched launches per replayed pair: each event node in the graph cuts a programmatic
+    # (PDL) edge and costs a few microseconds, which at configs[1] would itself move ms_per_step
+    watch = _lib.Watch(dom, 2)
     td3.capture()
     if pair:
         watch.arm()
@@ -477,7 +481,10 @@ def run_td3(args, rank, world, workload):
                       "l2": ("flushed between timed pairs of updates (256 MB read, outside the events)" if pair
                              else "flushed between timed steps (256 MB read, outside the events)")
                       if flush is not None else "not flushed", "cuda_graph": True,
-                      "graph": "update pairs (k odd, k + 1 overlapped)" if pair else "one graph per update"},
+                      "graph": "update pairs (k odd, k + 1 overlapped)" if pair else "one graph per update",
+                      "dp_optimiser": ("fused gradient mean + Adam over NCCL symmetric memory"
+                                       if td3.fused_plans[0] is not None else
+                                       ("bucketed NCCL allreduce + Adam" if td3.comm is not None else "none (1 GPU)"))},
            "clocks": clocks, "gpu_launches": int(gpu_launches)}
     if pair and step0[0] % 2 == 0:
         en = energy_window(lambda k: td3.replay_pair(), clk)   # each call = two updates

@@ -77,6 +77,9 @@ enum spikerl_engine {
 /* Opaque NCCL communicator owned by the library (spikerl_comm_init / spikerl_comm_destroy). */
 struct spikerl_comm;
 typedef struct spikerl_comm spikerl_comm;
+/* Opaque fused gradient-mean + Adam plan over symmetric memory (spikerl_fused_adam_create). */
+struct spikerl_fused_adam;
+typedef struct spikerl_fused_adam spikerl_fused_adam;
 
 /* Actor problem statement (PAPER.md:131 + north_star): obs dim S, action dim A, encoder
  * population E, decoder population D, hidden widths N1, N2, T timesteps, LIF constants. */
@@ -257,6 +260,11 @@ typedef struct {
    * and the scale backs off; otherwise the gradient is unscaled inside the Adam kernel. The caller
    * initialises the scales (e.g. 65536) and zeroes the rest. */
   float* amp;
+  /* optional (NULL = the NCCL allreduce + Adam launches): fused gradient mean + Adam plans
+   * (spikerl_fused_adam_create over grad_critic / critic and grad_actor / actor, which must then come
+   * from spikerl_comm_mem_alloc). Used only with a communicator and without loss scaling. */
+  spikerl_fused_adam* fused_critic;
+  spikerl_fused_adam* fused_actor;
 } spikerl_td3_bufs;
 
 
@@ -328,6 +336,27 @@ int spikerl_allreduce_grads(spikerl_comm* comm, float* grads, size_t count,
 int spikerl_broadcast_params(spikerl_comm* comm, float* params, size_t count, int root,
                              spikerl_stream_t stream);
 
+/* the gradient mean fused with the optimiser step over NVLink (PAPER.md:135
+ * average_gradients + Adam) as one kernel on NCCL 2.28 symmetric memory:
+ *   mem_alloc / mem_free: ncclMemAlloc'd device memory (the buffers a plan may use);
+ *   fused_adam_create (collective over comm): registers grads and params (n fp32 each, from
+ *     mem_alloc) as symmetric windows and creates the device communicator (LSA barriers; NVLS
+ *     multimem when use_multimem and the fabric has it, else peer loads / stores);
+ *   fused_allreduce_adam: ONE launch per rank: barrier, then for the rank's 1/W shard the mean over
+ *     ranks of the peers' gradients (summed in rank order), Adam (PyTorch form, same element
+ *     arithmetic as spikerl_adam) on the shard with the clamp, the new values stored into every
+ *     rank's params, barrier. params end bitwise identical on all ranks; m and v are kept only for
+ *     the rank's shard (ZeRO-1). At world 1 the result equals allreduce + spikerl_adam bitwise.
+ * Errors: E_NCCL if the NCCL library has no device API; E_UNSUPPORTED above 8 ranks. */
+int spikerl_comm_mem_alloc(spikerl_comm* comm, size_t bytes, void** ptr /* host out */);
+int spikerl_comm_mem_free(spikerl_comm* comm, void* ptr);
+int spikerl_fused_adam_create(spikerl_comm* comm, float* grads, float* params, size_t n, int use_multimem,
+                              spikerl_fused_adam** out);
+int spikerl_fused_adam_destroy(spikerl_fused_adam* plan);
+int spikerl_fused_allreduce_adam(spikerl_fused_adam* plan, float* m, float* v, long long* step_counter, float lr,
+                                 float beta1, float beta2, float eps, size_t clamp_lo, size_t clamp_hi,
+                                 float clamp_min, spikerl_stream_t stream);
+
 /* ------------------------------------------------------------------------------------------
  * Diagnostics
  * ---------------------------------------------------------------------------------------- */
@@ -365,6 +394,8 @@ int spikerl_prof_timeline(spikerl_prof_span* out, int max_entries);
  * the last spikerl_prof_watch (re-arming resets it). */
 int spikerl_prof_watch(const char* name, void* const* ev_begin, void* const* ev_end, int n);
 int spikerl_prof_watch_count(void);
+/* name == "*" watches every launch; watch_name(i) = the kernel name of pair i (or ""). */
+const char* spikerl_prof_watch_name(int i);
 
 #ifdef __cplusplus
 }

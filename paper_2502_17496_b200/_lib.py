@@ -64,7 +64,8 @@ class TD3Bufs(C.Structure):
                 ("v_actor", C.c_void_p), ("m_critic", C.c_void_p), ("v_critic", C.c_void_p),
                 ("grad_actor", C.c_void_p), ("grad_critic", C.c_void_p), ("adam_steps", C.c_void_p),
                 ("rng_counter", C.c_void_p), ("rs", C.c_void_p), ("ra", C.c_void_p), ("rr", C.c_void_p),
-                ("rs2", C.c_void_p), ("rd", C.c_void_p), ("replay_size", C.c_longlong), ("amp", C.c_void_p)]
+                ("rs2", C.c_void_p), ("rd", C.c_void_p), ("replay_size", C.c_longlong), ("amp", C.c_void_p),
+                ("fused_critic", C.c_void_p), ("fused_actor", C.c_void_p)]
 
 
 class TD3WsLayout(C.Structure):
@@ -183,6 +184,11 @@ _SIGS = {
     "spikerl_comm_rank": (I, [P]),
     "spikerl_allreduce_grads": (I, [P, P, SZ, P]),
     "spikerl_broadcast_params": (I, [P, P, SZ, I, P]),
+    "spikerl_comm_mem_alloc": (I, [P, SZ, C.POINTER(P)]),
+    "spikerl_comm_mem_free": (I, [P, P]),
+    "spikerl_fused_adam_create": (I, [P, P, P, SZ, I, C.POINTER(P)]),
+    "spikerl_fused_adam_destroy": (I, [P]),
+    "spikerl_fused_allreduce_adam": (I, [P, P, P, P, F, F, F, F, SZ, SZ, F, P]),
     "spikerl_last_error": (C.c_char_p, []),
     "spikerl_version": (C.c_char_p, []),
     "spikerl_launch_count": (LL, [I]),
@@ -191,6 +197,7 @@ _SIGS = {
     "spikerl_prof_timeline": (I, [P, I]),
     "spikerl_prof_watch": (I, [C.c_char_p, C.POINTER(P), C.POINTER(P), I]),
     "spikerl_prof_watch_count": (I, []),
+    "spikerl_prof_watch_name": (C.c_char_p, [I]),
 }
 EXPORTS = tuple(_SIGS)
 

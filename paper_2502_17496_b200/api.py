@@ -300,10 +300,41 @@ class Comm:
     def broadcast(self, params: torch.Tensor, root=0):
         check(lib().spikerl_broadcast_params(self.handle, _p(params), params.numel(), root, _stream()), "broadcast")
 
+    def alloc(self, n: int) -> torch.Tensor:
+        """n fp32 zeros in NCCL symmetric-capable memory (spikerl_comm_mem_alloc: ncclMemAlloc), for
+        buffers a fused allreduce + Adam plan registers. Freed when the tensor's storage dies."""
+        ptr = C.c_void_p()
+        check(lib().spikerl_comm_mem_alloc(self.handle, 4 * n, C.byref(ptr)), "comm_mem_alloc")
+        t = torch.as_tensor(_CommMem(self, ptr.value, n), device="cuda")
+        t.zero_()
+        return t
+
+    def fused_adam(self, grads: torch.Tensor, params: torch.Tensor, use_multimem=True):
+        """A fused gradient-mean + Adam plan over (grads, params), both from alloc()."""
+        h = C.c_void_p()
+        check(lib().spikerl_fused_adam_create(self.handle, _p(grads), _p(params), params.numel(), int(use_multimem),
+                                              C.byref(h)), "fused_adam_create")
+        return h
+
     def close(self):
         if self.handle:
             lib().spikerl_comm_destroy(self.handle)
             self.handle = None
+
+
+class _CommMem:
+    """__cuda_array_interface__ over an ncclMemAlloc'd buffer (kept alive by the tensor using it)."""
+
+    def __init__(self, comm, ptr, n):
+        self.comm, self.ptr = comm, ptr
+        self.__cuda_array_interface__ = {"shape": (n,), "typestr": "<f4", "data": (ptr, False), "version": 3}
+
+    def __del__(self):
+        try:
+            if self.comm.handle:
+                lib().spikerl_comm_mem_free(self.comm.handle, C.c_void_p(self.ptr))
+        except Exception:
+            pass
 
 
 # ------------------------------------------------------------------------------------ TD3
@@ -324,18 +355,24 @@ class TD3:
     """Device-resident TD3 state + the C-ABI update."""
 
     def __init__(self, acfg: L.ActorCfg, ccfg: L.CriticCfg, hp: L.TD3Cfg, replay: ReplayShard, device="cuda",
-                 seed=0, comm: Comm | None = None, loss_scale: float | None = None):
+                 seed=0, comm: Comm | None = None, loss_scale: float | None = None, fused: bool = False):
+        """fused (needs comm): the gradient mean and Adam of both networks run as the one fused kernel over
+        NCCL symmetric memory (spikerl_fused_allreduce_adam) instead of allreduce + Adam launches."""
         self.acfg, self.ccfg, self.hp, self.replay, self.device, self.seed, self.comm = \
             acfg, ccfg, hp, replay, device, seed, comm
         lb = lib()
         self.Pa = actor_offsets(acfg)[-1]
         self.Pc = critic_offsets(ccfg)[-1]
         f32 = dict(dtype=torch.float32, device=device)
-        self.actor, self.actor_t = torch.zeros(self.Pa, **f32), torch.zeros(self.Pa, **f32)
-        self.critic, self.critic_t = torch.zeros(2 * self.Pc, **f32), torch.zeros(2 * self.Pc, **f32)
+        fused = bool(fused and comm is not None)
+        sym = (lambda n: comm.alloc(n)) if fused else (lambda n: torch.zeros(n, **f32))
+        self.actor, self.actor_t = sym(self.Pa), torch.zeros(self.Pa, **f32)
+        self.critic, self.critic_t = sym(2 * self.Pc), torch.zeros(2 * self.Pc, **f32)
         self.m_actor, self.v_actor = torch.zeros(self.Pa, **f32), torch.zeros(self.Pa, **f32)
         self.m_critic, self.v_critic = torch.zeros(2 * self.Pc, **f32), torch.zeros(2 * self.Pc, **f32)
-        self.grad_actor, self.grad_critic = torch.zeros(self.Pa, **f32), torch.zeros(2 * self.Pc, **f32)
+        self.grad_actor, self.grad_critic = sym(self.Pa), sym(2 * self.Pc)
+        self.fused_plans = (comm.fused_adam(self.grad_critic, self.critic), comm.fused_adam(self.grad_actor, self.actor)) \
+            if fused else (None, None)
         self.bf16 = acfg.precision in (L.BF16, L.FP16)
         ab = lb.spikerl_actor_bf16_bytes(C.byref(acfg))
         cb = lb.spikerl_critic_bf16_bytes(C.byref(ccfg))
@@ -357,7 +394,8 @@ class TD3:
             self.actor, self.actor_t, self.actor_bf16, self.actor_t_bf16, self.critic, self.critic_t,
             self.critic_bf16, self.critic_t_bf16, self.m_actor, self.v_actor, self.m_critic, self.v_critic,
             self.grad_actor, self.grad_critic, self.adam_steps, self.rng_counter, replay.s, replay.a, replay.r,
-            replay.s2, replay.d)], replay.size, self.amp.data_ptr() if self.amp is not None else None)
+            replay.s2, replay.d)], replay.size, self.amp.data_ptr() if self.amp is not None else None,
+            self.fused_plans[0], self.fused_plans[1])
         self.graphs = {}
         self.ws_pair = None
         self.pair_graph = None

@@ -10,27 +10,16 @@
 #include <nccl.h>
 #include "internal.h"
 
+#include "comm_internal.h"
+
 struct spikerl_comm {
   ncclComm_t comm;
   int rank, world;
 };
 
 namespace spk {
-namespace {
 
-struct NcclApi {
-  void* h = nullptr;
-  decltype(&ncclGetUniqueId) getUniqueId = nullptr;
-  decltype(&ncclCommInitRank) commInitRank = nullptr;
-  decltype(&ncclCommDestroy) commDestroy = nullptr;
-  decltype(&ncclAllReduce) allReduce = nullptr;
-  decltype(&ncclBroadcast) broadcast = nullptr;
-  decltype(&ncclGetErrorString) errStr = nullptr;
-  decltype(&ncclCommGetAsyncError) asyncErr = nullptr;
-  std::string why;
-};
-
-NcclApi& api() {
+NcclApi& nccl_api() {
   static NcclApi a;
   static std::once_flag once;
   std::call_once(once, [] {
@@ -53,6 +42,12 @@ NcclApi& api() {
     SPK_SYM(broadcast, "ncclBroadcast");
     SPK_SYM(errStr, "ncclGetErrorString");
     SPK_SYM(asyncErr, "ncclCommGetAsyncError");
+    SPK_SYM(memAlloc, "ncclMemAlloc");
+    SPK_SYM(memFree, "ncclMemFree");
+    SPK_SYM(winRegister, "ncclCommWindowRegister");
+    SPK_SYM(winDeregister, "ncclCommWindowDeregister");
+    SPK_SYM(devCommCreate, "ncclDevCommCreate");
+    SPK_SYM(devCommDestroy, "ncclDevCommDestroy");
 #undef SPK_SYM
     if (!a.getUniqueId || !a.commInitRank || !a.allReduce || !a.broadcast) a.why = "missing NCCL symbols";
   });
@@ -61,12 +56,12 @@ NcclApi& api() {
 
 int nccl_status(ncclResult_t r, const char* what) {
   if (r == ncclSuccess) return SPIKERL_OK;
-  set_error("%s: %s", what, api().errStr ? api().errStr(r) : "nccl error");
+  set_error("%s: %s", what, nccl_api().errStr ? nccl_api().errStr(r) : "nccl error");
   return SPIKERL_E_NCCL;
 }
 
-int need_api() {
-  NcclApi& a = api();
+int nccl_need_api() {
+  NcclApi& a = nccl_api();
   if (!a.why.empty()) {
     set_error("NCCL unavailable: %s", a.why.c_str());
     return SPIKERL_E_NCCL;
@@ -74,16 +69,18 @@ int need_api() {
   return SPIKERL_OK;
 }
 
-}  // namespace
+ncclComm_t comm_nccl(const spikerl_comm* c) { return c->comm; }
+int comm_world(const spikerl_comm* c) { return c->world; }
+
 }  // namespace spk
 
 extern "C" {
 
 int spikerl_comm_get_unique_id(void* out128) {
   if (!out128) { spk::set_error("null id buffer"); return SPIKERL_E_ARG; }
-  SPK_TRY(spk::need_api());
+  SPK_TRY(spk::nccl_need_api());
   ncclUniqueId id;
-  SPK_TRY(spk::nccl_status(spk::api().getUniqueId(&id), "ncclGetUniqueId"));
+  SPK_TRY(spk::nccl_status(spk::nccl_api().getUniqueId(&id), "ncclGetUniqueId"));
   memcpy(out128, &id, sizeof(id));
   return SPIKERL_OK;
 }
@@ -93,18 +90,18 @@ int spikerl_comm_init(int rank, int world, const void* id128, spikerl_comm** out
     spk::set_error("spikerl_comm_init: bad arguments (rank %d, world %d)", rank, world);
     return SPIKERL_E_ARG;
   }
-  SPK_TRY(spk::need_api());
+  SPK_TRY(spk::nccl_need_api());
   ncclUniqueId id;
   memcpy(&id, id128, sizeof(id));
   ncclComm_t c;
-  SPK_TRY(spk::nccl_status(spk::api().commInitRank(&c, world, id, rank), "ncclCommInitRank"));
+  SPK_TRY(spk::nccl_status(spk::nccl_api().commInitRank(&c, world, id, rank), "ncclCommInitRank"));
   *out = new spikerl_comm{c, rank, world};
   return SPIKERL_OK;
 }
 
 int spikerl_comm_destroy(spikerl_comm* comm) {
   if (!comm) return SPIKERL_OK;
-  int st = spk::nccl_status(spk::api().commDestroy(comm->comm), "ncclCommDestroy");
+  int st = spk::nccl_status(spk::nccl_api().commDestroy(comm->comm), "ncclCommDestroy");
   delete comm;
   return st;
 }
@@ -118,7 +115,7 @@ int spikerl_allreduce_grads(spikerl_comm* comm, float* grads, size_t count, spik
   if (count == 0) return SPIKERL_OK;
   // world 1 included: NCCL runs one-rank communicators (the mean is the identity), so the one-GPU
   // path exercises the same calls, inside graph captures too
-  return spk::nccl_status(spk::api().allReduce(grads, grads, count, ncclFloat32, ncclAvg, comm->comm,
+  return spk::nccl_status(spk::nccl_api().allReduce(grads, grads, count, ncclFloat32, ncclAvg, comm->comm,
                                                (cudaStream_t)stream),
                           "ncclAllReduce");
 }
@@ -131,7 +128,7 @@ int spikerl_broadcast_params(spikerl_comm* comm, float* params, size_t count, in
     return SPIKERL_E_ARG;
   }
   if (count == 0) return SPIKERL_OK;
-  return spk::nccl_status(spk::api().broadcast(params, params, count, ncclFloat32, root, comm->comm,
+  return spk::nccl_status(spk::nccl_api().broadcast(params, params, count, ncclFloat32, root, comm->comm,
                                                (cudaStream_t)stream),
                           "ncclBroadcast");
 }

@@ -118,10 +118,68 @@ struct Bf16Views {
 };
 Bf16Views actor_bf16_views(const ActorDims& d, __nv_bfloat16* out);
 Bf16Views critic_bf16_views(const CriticDims& c, __nv_bfloat16* out);
+// Adam (PyTorch form; R19) for one element, shared by adam_kernel and the fused
+// allreduce + Adam kernel so both round identically: m, v fp32; step = lr / (1 - b1^t) and
+// bc2_sqrt = sqrt(1 - b2^t) formed once (fp64, rounded to fp32) by adam_coefs.
+__device__ __forceinline__ void adam_coefs(float lr, float b1, float b2, long long t, float* step_size,
+                                           float* bc2_sqrt) {
+  *step_size = (float)((double)lr / (1.0 - pow((double)b1, (double)t)));
+  *bc2_sqrt = (float)sqrt(1.0 - pow((double)b2, (double)t));
+}
+__device__ __forceinline__ float adam_elem(float p, float g, float& m, float& v, float b1, float omb1, float b2,
+                                           float omb2, float bc2_sqrt, float eps, float step_size) {
+  m = __fadd_rn(__fmul_rn(b1, m), __fmul_rn(omb1, g));
+  v = __fadd_rn(__fmul_rn(b2, v), __fmul_rn(__fmul_rn(omb2, g), g));
+  const float denom = __fadd_rn(__fdiv_rn(sqrtf(v), bc2_sqrt), eps);
+  return __fsub_rn(p, __fmul_rn(step_size, __fdiv_rn(m, denom)));
+}
+// Writes the RNE bf16 copy of the updated master element e into every working copy that holds
+// it. Element indices are < 2^31 (parameter counts), so row / column come from 32-bit
+// multiply-high divisions (a 64-bit division per element made Adam ~5x slower than its bytes).
+__device__ __forceinline__ void store_views(const Bf16Views& v, size_t e, float x) {
+  if (v.kind == 0) return;
+  const __nv_bfloat16 h = __ushort_as_bfloat16(op16_bits(x, v.f16 != 0));   // fp16 bits when v.f16
+  if (v.kind == 1) {
+#pragma unroll
+    for (int l = 0; l < 3; ++l) {
+      const long long r = (long long)e - v.src[l];
+      if (r >= 0 && r < (long long)v.rows[l] * v.cols[l]) {
+        const uint32_t n = fdiv((uint32_t)r, v.colsd[l]), k = (uint32_t)r - n * (uint32_t)v.cols[l];
+        v.out[v.dst[l] + (long long)n * v.ldd[l] + k] = h;
+      }
+    }
+    return;
+  }
+  v.out[e] = h;   // [2][P] plain copy (kinds 2 and 3)
+  if (v.kind != 2) return;
+  const uint32_t z = fdiv((uint32_t)e, v.Pd);
+  const long long l = (long long)e - (long long)z * v.P;
+  __nv_bfloat16* blk = v.out + ((2 * v.P + 7) & ~7LL) + z * v.tb;   // blk_base (k_critic_mma.cu)
+  long long r = l - v.oW1;
+  if (r >= 0 && r < (long long)v.H1 * v.in) {          // W1[j][i] -> W1p[j][i], W1T[i][j]
+    const uint32_t j = fdiv((uint32_t)r, v.ind), i = (uint32_t)r - j * (uint32_t)v.in;
+    blk[v.W1p + (long long)j * v.inp + i] = h;
+    blk[v.W1T + (long long)i * v.H1 + j] = h;
+    return;
+  }
+  r = l - v.oW2;
+  if (r >= 0 && r < (long long)v.H2 * v.H1) {          // W2[j2][j1] -> W2T[j1][j2], W2c[j2][j1]
+    const uint32_t j2 = fdiv((uint32_t)r, v.H1d), j1 = (uint32_t)r - j2 * (uint32_t)v.H1;
+    blk[v.W2T + (long long)j1 * v.H2 + j2] = h;
+    blk[v.W2c + r] = h;
+  }
+}
+
+
 int launch_adam(float* p, const float* g, float* m, float* v, size_t n, long long* counter,
                 float lr, float b1, float b2, float eps, size_t clo, size_t chi, float cmin,
                 unsigned int* done_ticket, const Bf16Views* views, cudaStream_t st, float* amp = nullptr,
                 float amp_growth = 2.f, float amp_backoff = 0.5f, int amp_interval = 2000);
+// fused gradient mean + Adam over symmetric memory (k_fused_dp.cu; spikerl_fused_adam_create)
+bool fused_adam_matches(const spikerl_fused_adam* fa, const float* g, const float* p, size_t n);
+int fused_adam_launch(spikerl_fused_adam* fa, float* m, float* v, long long* counter, float lr, float b1, float b2,
+                      float eps, size_t clo, size_t chi, float cmin, unsigned int* ticket, const Bf16Views* views,
+                      cudaStream_t st);
 // dynamic loss scaling: amp[2] = 1 when g holds a non-finite element (amp: {scale, count, found, -})
 int launch_amp_check(const float* g, size_t n, float* amp, cudaStream_t st);
 int launch_polyak(float* t, const float* s, size_t n, float tau, const Bf16Views* views, cudaStream_t st);

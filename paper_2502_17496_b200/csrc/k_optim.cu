@@ -97,43 +97,6 @@ Bf16Views actor_bf16_views(const ActorDims& d, __nv_bfloat16* out) {
   return v;
 }
 
-// Writes the RNE bf16 copy of the updated master element e into every working copy that holds
-// it. Element indices are < 2^31 (parameter counts), so row / column come from 32-bit
-// multiply-high divisions (a 64-bit division per element made Adam ~5x slower than its bytes).
-__device__ __forceinline__ void store_views(const Bf16Views& v, size_t e, float x) {
-  if (v.kind == 0) return;
-  const __nv_bfloat16 h = __ushort_as_bfloat16(op16_bits(x, v.f16 != 0));   // fp16 bits when v.f16
-  if (v.kind == 1) {
-#pragma unroll
-    for (int l = 0; l < 3; ++l) {
-      const long long r = (long long)e - v.src[l];
-      if (r >= 0 && r < (long long)v.rows[l] * v.cols[l]) {
-        const uint32_t n = fdiv((uint32_t)r, v.colsd[l]), k = (uint32_t)r - n * (uint32_t)v.cols[l];
-        v.out[v.dst[l] + (long long)n * v.ldd[l] + k] = h;
-      }
-    }
-    return;
-  }
-  v.out[e] = h;   // [2][P] plain copy (kinds 2 and 3)
-  if (v.kind != 2) return;
-  const uint32_t z = fdiv((uint32_t)e, v.Pd);
-  const long long l = (long long)e - (long long)z * v.P;
-  __nv_bfloat16* blk = v.out + ((2 * v.P + 7) & ~7LL) + z * v.tb;   // blk_base (k_critic_mma.cu)
-  long long r = l - v.oW1;
-  if (r >= 0 && r < (long long)v.H1 * v.in) {          // W1[j][i] -> W1p[j][i], W1T[i][j]
-    const uint32_t j = fdiv((uint32_t)r, v.ind), i = (uint32_t)r - j * (uint32_t)v.in;
-    blk[v.W1p + (long long)j * v.inp + i] = h;
-    blk[v.W1T + (long long)i * v.H1 + j] = h;
-    return;
-  }
-  r = l - v.oW2;
-  if (r >= 0 && r < (long long)v.H2 * v.H1) {          // W2[j2][j1] -> W2T[j1][j2], W2c[j2][j1]
-    const uint32_t j2 = fdiv((uint32_t)r, v.H1d), j1 = (uint32_t)r - j2 * (uint32_t)v.H1;
-    blk[v.W2T + (long long)j1 * v.H2 + j2] = h;
-    blk[v.W2c + r] = h;
-  }
-}
-
 // ------------------------------------------------------------------ Adam
 // t = *counter + 1 is read by every block; the last block to finish (atomic ticket) stores it
 // back, so the call is graph-replayable with an on-device step count.
@@ -153,8 +116,7 @@ __global__ void __launch_bounds__(256) adam_kernel(float* __restrict__ p, const 
   if (threadIdx.x == 0) {
     const long long tt = *(volatile long long*)counter + 1;
     s_t = tt;
-    s_coef[0] = (float)((double)lr / (1.0 - pow((double)b1, (double)tt)));
-    s_coef[1] = (float)sqrt(1.0 - pow((double)b2, (double)tt));
+    adam_coefs(lr, b1, b2, tt, &s_coef[0], &s_coef[1]);
     // loss scaling: skip the step on a non-finite gradient, else unscale by 1 / scale
     s_skip = amp ? (*(volatile float*)(amp + 2) != 0.0f) : 0;
     s_coef[2] = amp ? __frcp_rn(*(volatile float*)amp) : 1.0f;
@@ -191,10 +153,7 @@ __global__ void __launch_bounds__(256) adam_kernel(float* __restrict__ p, const 
 #pragma unroll
       for (int j = 0; j < 4; ++j) {
         if (amp) ga[j] = __fmul_rn(ga[j], inv_scale);
-        ma[j] = __fadd_rn(__fmul_rn(b1, ma[j]), __fmul_rn(omb1, ga[j]));
-        va[j] = __fadd_rn(__fmul_rn(b2, va[j]), __fmul_rn(__fmul_rn(omb2, ga[j]), ga[j]));
-        const float denom = __fadd_rn(__fdiv_rn(sqrtf(va[j]), bc2_sqrt), eps);
-        pa[j] = __fsub_rn(pa[j], __fmul_rn(step_size, __fdiv_rn(ma[j], denom)));
+        pa[j] = adam_elem(pa[j], ga[j], ma[j], va[j], b1, omb1, b2, omb2, bc2_sqrt, eps, step_size);
         const size_t e = 4 * i + j;
         if (e >= clo && e < chi) pa[j] = fmaxf(pa[j], cmin);
         store_views(views, e, pa[j]);
@@ -206,10 +165,8 @@ __global__ void __launch_bounds__(256) adam_kernel(float* __restrict__ p, const 
   }
   for (size_t e = 4 * n4 + blockIdx.x * (size_t)blockDim.x + threadIdx.x; e < n && !skip; e += stride) {
     const float ge = amp ? __fmul_rn(g[e], inv_scale) : g[e];
-    float mm = __fadd_rn(__fmul_rn(b1, m[e]), __fmul_rn(omb1, ge));
-    float vv = __fadd_rn(__fmul_rn(b2, v[e]), __fmul_rn(__fmul_rn(omb2, ge), ge));
-    const float denom = __fadd_rn(__fdiv_rn(sqrtf(vv), bc2_sqrt), eps);
-    float pp = __fsub_rn(p[e], __fmul_rn(step_size, __fdiv_rn(mm, denom)));
+    float mm = m[e], vv = v[e];
+    float pp = adam_elem(p[e], ge, mm, vv, b1, omb1, b2, omb2, bc2_sqrt, eps, step_size);
     if (e >= clo && e < chi) pp = fmaxf(pp, cmin);
     p[e] = pp; m[e] = mm; v[e] = vv;
     store_views(views, e, pp);

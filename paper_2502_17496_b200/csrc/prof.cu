@@ -20,8 +20,9 @@ std::mutex g_mu;
 std::vector<Rec> g_recs;
 bool g_on = false;
 struct Watch {
-  std::string name;
+  std::string name;   // "*": every launch
   std::vector<cudaEvent_t> b, e;
+  std::vector<const char*> names;   // kernel name of each pair used
   int next = 0;
 } g_watch;
 bool g_watch_on = false;
@@ -40,8 +41,9 @@ bool prof_on() { return g_on || g_watch_on; }
 ProfScope::ProfScope(const char* name, int bound, double flops, double bytes, cudaStream_t s) : st(s) {
   if (g_watch_on) {
     std::lock_guard<std::mutex> lk(g_mu);
-    if (g_watch.next < (int)g_watch.b.size() && g_watch.name == name) {
+    if (g_watch.next < (int)g_watch.b.size() && (g_watch.name == "*" || g_watch.name == name)) {
       wslot = g_watch.next++;
+      g_watch.names.push_back(name);
       record(g_watch.b[wslot], s);
     }
   }
@@ -97,6 +99,11 @@ int spikerl_prof_watch(const char* name, void* const* ev_begin, void* const* ev_
 int spikerl_prof_watch_count(void) {
   std::lock_guard<std::mutex> lk(spk::g_mu);
   return spk::g_watch.next;
+}
+
+const char* spikerl_prof_watch_name(int i) {
+  std::lock_guard<std::mutex> lk(spk::g_mu);
+  return (i >= 0 && i < (int)spk::g_watch.names.size()) ? spk::g_watch.names[i] : "";
 }
 
 int spikerl_prof_timeline(spikerl_prof_span* out, int max_entries) {

@@ -368,6 +368,34 @@ static Td3Ws td3_ws_layout(const ActorDims& ad, const CriticDims& cd, int B) {
   return w;
 }
 
+// The optimiser step of each network after its backward: the gradient mean over ranks + Adam, either
+// as the NCCL allreduce (the actor's is already bucketed inside its backward) and the Adam launch, or
+// as the one fused allreduce + Adam kernel over symmetric memory when a plan is given (NEXT #1).
+static int critic_optimise(const spikerl_td3_bufs* b, spikerl_comm* comm, const spikerl_td3_cfg* hp, size_t Pc,
+                           const Bf16Views* cv, float* amp_c, cudaStream_t st) {
+  if (comm && b->fused_critic)
+    return fused_adam_launch(b->fused_critic, b->m_critic, b->v_critic, b->adam_steps, hp->lr_critic, hp->beta1,
+                             hp->beta2, hp->eps, 0, 0, 0.f, (unsigned int*)(b->adam_steps + 1), cv, st);
+  SPK_TRY(spikerl_allreduce_grads(comm, b->grad_critic, 2 * Pc, st));
+  if (amp_c) SPK_TRY(launch_amp_check(b->grad_critic, 2 * Pc, amp_c, st));
+  return launch_adam(b->critic, b->grad_critic, b->m_critic, b->v_critic, 2 * Pc, b->adam_steps, hp->lr_critic,
+                     hp->beta1, hp->beta2, hp->eps, 0, 0, 0.f, (unsigned int*)(b->adam_steps + 1), cv, st, amp_c,
+                     hp->amp_growth, hp->amp_backoff, hp->amp_interval);
+}
+
+static int actor_optimise(const spikerl_td3_bufs* b, spikerl_comm* comm, const spikerl_td3_cfg* hp,
+                          const ActorDims& ad, size_t Pa, const Bf16Views* av, float* amp_a, cudaStream_t st) {
+  if (comm && b->fused_actor)
+    return fused_adam_launch(b->fused_actor, b->m_actor, b->v_actor, b->adam_steps + 2, hp->lr_actor, hp->beta1,
+                             hp->beta2, hp->eps, ad.off[SPIKERL_ACTOR_SIGMA], ad.off[SPIKERL_ACTOR_W1],
+                             ad.sigma_floor, (unsigned int*)(b->adam_steps + 3), av, st);
+  if (amp_a) SPK_TRY(launch_amp_check(b->grad_actor, Pa, amp_a, st));
+  return launch_adam(b->actor, b->grad_actor, b->m_actor, b->v_actor, Pa, b->adam_steps + 2, hp->lr_actor, hp->beta1,
+                     hp->beta2, hp->eps, ad.off[SPIKERL_ACTOR_SIGMA], ad.off[SPIKERL_ACTOR_W1], ad.sigma_floor,
+                     (unsigned int*)(b->adam_steps + 3), av, st, amp_a, hp->amp_growth, hp->amp_backoff,
+                     hp->amp_interval);
+}
+
 __global__ void neg_mean_kernel(int B, const float* __restrict__ q, float* __restrict__ out) {
   pdl_wait();
   pdl_trigger();
@@ -640,6 +668,14 @@ int spikerl_td3_update(const spikerl_actor_cfg* acfg, const spikerl_critic_cfg* 
     return SPIKERL_E_ARG;
   }
   SPK_TRY(critic_supported(cd, b->amp != nullptr));
+  if (comm && (b->fused_critic || b->fused_actor)) {
+    if (b->amp) { set_error("fused allreduce + Adam: no dynamic loss scaling"); return SPIKERL_E_UNSUPPORTED; }
+    if ((b->fused_critic && !fused_adam_matches(b->fused_critic, b->grad_critic, b->critic, 2 * cd.off[SPIKERL_CRITIC_NPARAM])) ||
+        (b->fused_actor && !fused_adam_matches(b->fused_actor, b->grad_actor, b->actor, ad.off[SPIKERL_ACTOR_NPARAM]))) {
+      set_error("fused allreduce + Adam plan does not cover this buffer set (grads / params / size)");
+      return SPIKERL_E_ARG;
+    }
+  }
   if (b->replay_size < B) {
     set_error("replay holds %lld < batch %d transitions", b->replay_size, B);
     return SPIKERL_E_NOTREADY;
@@ -703,11 +739,7 @@ int spikerl_td3_update(const spikerl_actor_cfg* acfg, const spikerl_critic_cfg* 
   float* const amp_c = b->amp, * const amp_a = b->amp ? b->amp + 4 : nullptr;   // loss scaling (or none)
   SPK_TRY(critic_fwd_bwd(cd, B, b->critic, cbf, s, ad.S, a, ad.A, y, q, losses, b->grad_critic, nullptr, 0.f, 2,
                          cws, st, aux->ev[1], amp_c));
-  SPK_TRY(spikerl_allreduce_grads(comm, b->grad_critic, 2 * Pc, stream));
-  if (amp_c) SPK_TRY(launch_amp_check(b->grad_critic, 2 * Pc, amp_c, st));
-  SPK_TRY(launch_adam(b->critic, b->grad_critic, b->m_critic, b->v_critic, 2 * Pc, b->adam_steps, hp->lr_critic,
-                      hp->beta1, hp->beta2, hp->eps, 0, 0, 0.f, (unsigned int*)(b->adam_steps + 1), &cv, st, amp_c,
-                      hp->amp_growth, hp->amp_backoff, hp->amp_interval));
+  SPK_TRY(critic_optimise(b, comm, hp, Pc, &cv, amp_c, st));
   // 4. delayed actor update + targets
   if (actor_step) {
     // branch C: the critic targets only need the updated critic
@@ -723,12 +755,9 @@ int spikerl_td3_update(const spikerl_actor_cfg* acfg, const spikerl_critic_cfg* 
       pdl(neg_mean_kernel, 1, 256, 0, st)(B, q, losses + 1);
       SPK_LAUNCHED();
     }
-    SPK_TRY(actor_backward_impl(ad, B, b->actor, abf, s, tape, ga, b->grad_actor, 0, aws, st, comm));
-    if (amp_a) SPK_TRY(launch_amp_check(b->grad_actor, Pa, amp_a, st));
-    SPK_TRY(launch_adam(b->actor, b->grad_actor, b->m_actor, b->v_actor, Pa, b->adam_steps + 2, hp->lr_actor,
-                        hp->beta1, hp->beta2, hp->eps, ad.off[SPIKERL_ACTOR_SIGMA], ad.off[SPIKERL_ACTOR_W1],
-                        ad.sigma_floor, (unsigned int*)(b->adam_steps + 3), &av, st, amp_a, hp->amp_growth,
-                        hp->amp_backoff, hp->amp_interval));
+    SPK_TRY(actor_backward_impl(ad, B, b->actor, abf, s, tape, ga, b->grad_actor, 0, aws, st,
+                                b->fused_actor ? nullptr : comm));
+    SPK_TRY(actor_optimise(b, comm, hp, ad, Pa, &av, amp_a, st));
     SPK_TRY(launch_polyak(b->actor_t, b->actor, Pa, hp->tau, &atv, st));
     SPK_CHECK_CUDA(cudaStreamWaitEvent(st, aux->ev[5], 0));   // join branch C
   }
@@ -771,6 +800,14 @@ int spikerl_td3_update_pair(const spikerl_actor_cfg* acfg, const spikerl_critic_
     return SPIKERL_E_ARG;
   }
   SPK_TRY(critic_supported(cd, b->amp != nullptr));
+  if (comm && (b->fused_critic || b->fused_actor)) {
+    if (b->amp) { set_error("fused allreduce + Adam: no dynamic loss scaling"); return SPIKERL_E_UNSUPPORTED; }
+    if ((b->fused_critic && !fused_adam_matches(b->fused_critic, b->grad_critic, b->critic, 2 * cd.off[SPIKERL_CRITIC_NPARAM])) ||
+        (b->fused_actor && !fused_adam_matches(b->fused_actor, b->grad_actor, b->actor, ad.off[SPIKERL_ACTOR_NPARAM]))) {
+      set_error("fused allreduce + Adam plan does not cover this buffer set (grads / params / size)");
+      return SPIKERL_E_ARG;
+    }
+  }
   if (b->replay_size < B) {
     set_error("replay holds %lld < batch %d transitions", b->replay_size, B);
     return SPIKERL_E_NOTREADY;
@@ -841,11 +878,7 @@ int spikerl_td3_update_pair(const spikerl_actor_cfg* acfg, const spikerl_critic_
     const Slot& x = sl[i];
     SPK_TRY(critic_fwd_bwd(cd, B, b->critic, cbf, x.s, ad.S, x.a, ad.A, x.y, x.q, losses, b->grad_critic, nullptr,
                            0.f, 2, x.cws, st, evA[i], amp_c));
-    SPK_TRY(spikerl_allreduce_grads(comm, b->grad_critic, 2 * Pc, stream));
-    if (amp_c) SPK_TRY(launch_amp_check(b->grad_critic, 2 * Pc, amp_c, st));
-    SPK_TRY(launch_adam(b->critic, b->grad_critic, b->m_critic, b->v_critic, 2 * Pc, b->adam_steps, hp->lr_critic,
-                        hp->beta1, hp->beta2, hp->eps, 0, 0, 0.f, (unsigned int*)(b->adam_steps + 1), &cv, st, amp_c,
-                        hp->amp_growth, hp->amp_backoff, hp->amp_interval));
+    SPK_TRY(critic_optimise(b, comm, hp, Pc, &cv, amp_c, st));
   }
   // delayed actor update + targets (update k + 1), exactly as spikerl_td3_update's actor step
   const Slot& x = sl[1];
@@ -860,12 +893,9 @@ int spikerl_td3_update_pair(const spikerl_actor_cfg* acfg, const spikerl_critic_
     pdl(neg_mean_kernel, 1, 256, 0, st)(B, x.q, losses + 1);
     SPK_LAUNCHED();
   }
-  SPK_TRY(actor_backward_impl(ad, B, b->actor, abf, x.s, x.tape, x.ga, b->grad_actor, 0, x.aws, st, comm));
-  if (amp_a) SPK_TRY(launch_amp_check(b->grad_actor, Pa, amp_a, st));
-  SPK_TRY(launch_adam(b->actor, b->grad_actor, b->m_actor, b->v_actor, Pa, b->adam_steps + 2, hp->lr_actor, hp->beta1,
-                      hp->beta2, hp->eps, ad.off[SPIKERL_ACTOR_SIGMA], ad.off[SPIKERL_ACTOR_W1], ad.sigma_floor,
-                      (unsigned int*)(b->adam_steps + 3), &av, st, amp_a, hp->amp_growth, hp->amp_backoff,
-                      hp->amp_interval));
+  SPK_TRY(actor_backward_impl(ad, B, b->actor, abf, x.s, x.tape, x.ga, b->grad_actor, 0, x.aws, st,
+                              b->fused_actor ? nullptr : comm));
+  SPK_TRY(actor_optimise(b, comm, hp, ad, Pa, &av, amp_a, st));
   SPK_TRY(launch_polyak(b->actor_t, b->actor, Pa, hp->tau, &atv, st));
   SPK_CHECK_CUDA(cudaStreamWaitEvent(st, aux->ev[5], 0));
   return SPIKERL_OK;

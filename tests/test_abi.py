@@ -96,8 +96,9 @@ def test_bf16_critic_shape_not_silently_rerouted(L):
     c = cfg(precision="fp32")
     cc = critic_cfg(23, precision="fp32")
     bufs = L.TD3Bufs()
-    for f, _ in L.TD3Bufs._fields_[:-1]:
+    for f, _ in L.TD3Bufs._fields_:
         setattr(bufs, f, 256)
+    bufs.fused_critic = bufs.fused_actor = None
     bufs.replay_size = 1000
     bufs.amp = 256
     st = lib.spikerl_td3_update(C.byref(c), C.byref(cc), C.byref(td3_cfg(256)), C.byref(bufs), 1, 0, None, None,
@@ -131,8 +132,9 @@ def test_sync_errors_enqueue_nothing(L):
     from paper_2502_17496_b200 import critic_cfg, td3_cfg
     cc = critic_cfg(23, precision="fp32")
     bufs = L.TD3Bufs()
-    for f, _ in L.TD3Bufs._fields_[:-1]:
+    for f, _ in L.TD3Bufs._fields_:
         setattr(bufs, f, 256)
+    bufs.amp = bufs.fused_critic = bufs.fused_actor = None
     bufs.replay_size = 10
     hp = td3_cfg(256)
     st = lib.spikerl_td3_update(C.byref(c), C.byref(cc), C.byref(hp), C.byref(bufs), 1, 0, None, None, None,

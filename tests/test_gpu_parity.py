@@ -552,6 +552,62 @@ def test_actor_backward_dp_buckets_world1(preset, B):
     comm.close()
 
 
+def test_fused_allreduce_adam_world1():
+    """SURVEY 8(f) NEXT #1 at world 1 (the only size this build's GPU allocation allows): the fused
+    gradient-mean + Adam kernel over NCCL symmetric memory (spikerl_fused_allreduce_adam) leaves
+    parameters, moments, step counts and the bf16 working copies bitwise equal to the NCCL allreduce +
+    Adam launches, over four TD3 updates (single and pair form, critic and actor plans); and the
+    stand-alone call equals spikerl_adam (with the sigma clamp range) bitwise."""
+    import torch
+    import paper_2502_17496_b200 as pk
+    comm = pk.Comm(0, 1)
+    try:
+        g0 = comm.alloc(8)
+        comm.fused_adam(g0, comm.alloc(8))
+    except pk.SpikeRLError as e:
+        pytest.skip(f"NCCL symmetric memory / device API unavailable here: {e}")
+    n = 100_003
+    rng = np.random.default_rng(3)
+    g = comm.alloc(n)
+    p = comm.alloc(n)
+    p.copy_(torch.from_numpy(rng.standard_normal(n).astype(np.float32)))
+    plan = comm.fused_adam(g, p)
+    p_ref = p.clone()
+    m1, v1, m2, v2 = (torch.zeros(n, device="cuda") for _ in range(4))
+    c1, c2 = (torch.zeros(2, dtype=torch.int64, device="cuda") for _ in range(2))
+    lib = pk.lib()
+    for t in range(3):
+        g.copy_(torch.from_numpy(rng.standard_normal(n).astype(np.float32)))
+        pk.adam(p_ref, g, m1, v1, c1, 1e-3, clamp=(10, 200, 1e-3))
+        pk._lib.check(lib.spikerl_fused_allreduce_adam(plan, pk.api._p(m2), pk.api._p(v2), pk.api._p(c2), 1e-3, 0.9,
+                                                        0.999, 1e-8, 10, 200, 1e-3, pk.api._stream()), "fused")
+    torch.cuda.synchronize()
+    for a, b in ((p_ref, p), (m1, m2), (v1, v2), (c1, c2)):
+        assert torch.equal(a, b)
+    shape, _, B = sg.preset("cfg1")
+    replay = pk.replay_fill(20000, 17, 6, seed=3)
+    outs = []
+    for fused, pair in ((False, False), (True, False), (True, True)):
+        rng = np.random.default_rng(8)
+        actor = sg.actor_params(shape, rng)
+        cs = sg.CriticShape(23, precision="bf16")
+        c1p, c2p = sg.critic_params(cs, rng), sg.critic_params(cs, rng)
+        td3 = pk.TD3(pk.actor_cfg_from(shape), pk.critic_cfg(23), pk.td3_cfg(B), replay, seed=11, comm=comm,
+                     fused=fused)
+        td3.load(actor, c1p, c2p)
+        if pair:
+            td3.update_pair(1); td3.update_pair(3)
+        else:
+            for k in range(1, 5):
+                td3.update(k)
+        torch.cuda.synchronize()
+        outs.append([t.cpu().clone() for t in (td3.actor, td3.critic, td3.actor_t, td3.critic_t, td3.m_actor,
+                                                td3.v_critic, td3.adam_steps, td3.actor_bf16, td3.critic_bf16)])
+    for other in outs[1:]:
+        for a, b in zip(outs[0], other):
+            assert torch.equal(a, b)
+
+
 @pytest.mark.parametrize("preset", ["cfg1", "cfg3L"])
 def test_td3_pair_matches_sequential(preset):
     """spikerl_td3_update_pair(k) (update k + 1's target path and pi(s) overlapping update k) leaves
