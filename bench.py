@@ -336,23 +336,67 @@ def cpu_baseline_td3(name, seconds=12.0, min_steps=4):
             "sample": f"{k} full TD3 updates of {name} (B={B}, half with the delayed actor step), numpy fp64 oracle"}
 
 
-def cpu_baseline_actor(name, B_sample=16, seconds=12.0):
+class HostEnergy:
+    """Host CPU energy from the RAPL powercap counters (/sys/class/powercap/*/energy_uj), when the box
+    exposes them; None otherwise (the r01/r02 boxes do not)."""
+
+    def __init__(self):
+        import glob
+        self.files = [f for f in glob.glob("/sys/class/powercap/*/energy_uj") if os.access(f, os.R_OK)]
+
+    def read_j(self):
+        if not self.files:
+            return None
+        try:
+            return sum(int(open(f).read()) for f in self.files) / 1e6
+        except Exception:
+            return None
+
+
+def cpu_baseline_actor(name, B_sample=16, seconds=12.0, threads=None):
     import numpy as np
     import oracle
     import synthgen as sg
+    from threadpoolctl import threadpool_limits
     shape, _, B = sg.preset(name)
     rng = np.random.default_rng(0)
     p = sg.actor_params(shape, rng)
-    t0 = time.time()
-    n = 0
-    while n == 0 or time.time() - t0 < seconds:
-        s = sg.observations(rng, B_sample, shape.obs_dim)
-        a, tape = oracle.actor_forward(p, shape, s)
-        oracle.actor_backward(p, shape, tape, sg.action_grads(rng, B_sample, shape.act_dim))
-        n += B_sample
-    dt = time.time() - t0
-    return {"value": round(n / dt, 3), "unit": "samples/s", "cores": len(os.sched_getaffinity(0)), "kind": "oracle",
-            "sample": f"{n} samples of {name} actor fwd+BPTT in batches of {B_sample} (extrapolates linearly in B)"}
+    he = HostEnergy()
+    with threadpool_limits(limits=threads):
+        e0 = he.read_j()
+        t0 = time.time()
+        n = 0
+        while n == 0 or time.time() - t0 < seconds:
+            s = sg.observations(rng, B_sample, shape.obs_dim)
+            a, tape = oracle.actor_forward(p, shape, s)
+            oracle.actor_backward(p, shape, tape, sg.action_grads(rng, B_sample, shape.act_dim))
+            n += B_sample
+        dt = time.time() - t0
+        e1 = he.read_j()
+    out = {"value": round(n / dt, 3), "unit": "samples/s", "cores": threads or len(os.sched_getaffinity(0)),
+           "kind": "oracle",
+           "sample": f"{n} samples of {name} actor fwd+BPTT in batches of {B_sample} (extrapolates linearly in B)"}
+    if e0 is not None and e1 is not None:
+        out["host_joules_per_sample"] = round((e1 - e0) / n, 6)
+    return out
+
+
+def gps_up(gpu_value, energy, cpu):
+    """The paper's GPS-UP view (§IV-B; R29: phi labels the baseline):
+    Speedup = T_oracle / T_gpu, Powerup = P_oracle / P_gpu, Greenup = Speedup x Powerup = the energy
+    per sample ratio. The GPU side is measured (NVML counter); the host side needs RAPL counters,
+    which these boxes do not expose, so Powerup and Greenup stay null there. Context only."""
+    out = {"speedup": round(gpu_value / cpu["value"], 1) if cpu and cpu.get("value") else None,
+           "gpu_joules_per_sample": None, "host_joules_per_sample": cpu.get("host_joules_per_sample") if cpu else None,
+           "powerup": None, "greenup": None}
+    if energy and energy.get("samples_per_joule"):
+        out["gpu_joules_per_sample"] = round(1.0 / energy["samples_per_joule"], 9)
+    if out["gpu_joules_per_sample"] and out["host_joules_per_sample"]:
+        out["greenup"] = round(out["host_joules_per_sample"] / out["gpu_joules_per_sample"], 1)
+        out["powerup"] = round(out["greenup"] / out["speedup"], 3) if out["speedup"] else None
+    else:
+        out["why_null"] = "host CPU energy not observable on this box (no readable RAPL powercap counters)"
+    return out
 
 
 # ---------------------------------------------------------------------------------- ours
@@ -803,6 +847,10 @@ def main():
             out["td3"] = td
         if rank == 0 and world == 1 and not args.no_cpu_baseline:
             out["cpu_baseline"] = cpu_baseline_actor(args.workload, B_sample=16 if args.workload == "cfg4" else 100)
+            # the oracle on one host core as well (SURVEY D-5), a shorter sample
+            out["cpu_baseline"]["single_thread"] = cpu_baseline_actor(
+                args.workload, B_sample=16 if args.workload == "cfg4" else 100, seconds=5.0, threads=1)
+            out["gps_up"] = gps_up(out["value"], out.get("energy"), out["cpu_baseline"])
     else:
         out = run_td3(args, rank, world, args.workload)
         if rank == 0 and world == 1 and not args.no_cpu_baseline:
