@@ -120,11 +120,12 @@ Bf16Views actor_bf16_views(const ActorDims& d, __nv_bfloat16* out);
 Bf16Views critic_bf16_views(const CriticDims& c, __nv_bfloat16* out);
 // Adam (PyTorch form; R19) for one element, shared by adam_kernel and the fused
 // allreduce + Adam kernel so both round identically: m, v fp32; step = lr / (1 - b1^t) and
-// bc2_sqrt = sqrt(1 - b2^t) formed once (fp64, rounded to fp32) by adam_coefs.
-__device__ __forceinline__ void adam_coefs(float lr, float b1, float b2, long long t, float* step_size,
+// bc2_sqrt = sqrt(1 - b2^t) formed once (fp64, rounded to fp32) by adam_coefs, with b^t = exp(t ln b)
+// from ln b computed on the host (a device fp64 pow per launch cost ~5 us of latency in r01's Adam).
+__device__ __forceinline__ void adam_coefs(float lr, double lnb1, double lnb2, long long t, float* step_size,
                                            float* bc2_sqrt) {
-  *step_size = (float)((double)lr / (1.0 - pow((double)b1, (double)t)));
-  *bc2_sqrt = (float)sqrt(1.0 - pow((double)b2, (double)t));
+  *step_size = (float)((double)lr / (1.0 - exp((double)t * lnb1)));
+  *bc2_sqrt = (float)sqrt(1.0 - exp((double)t * lnb2));
 }
 __device__ __forceinline__ float adam_elem(float p, float g, float& m, float& v, float b1, float omb1, float b2,
                                            float omb2, float bc2_sqrt, float eps, float step_size) {

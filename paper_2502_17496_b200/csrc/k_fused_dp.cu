@@ -48,7 +48,7 @@ __device__ __forceinline__ void mm_st(float* mp, float x) {
 __global__ void __launch_bounds__(256) fused_allreduce_adam_kernel(
     ncclDevComm dev, ncclWindow_t gwin, ncclWindow_t pwin, size_t n, float* __restrict__ m, float* __restrict__ v,
     long long* counter, float lr, float b1, float b2, float eps, size_t clo, size_t chi, float cmin,
-    unsigned int* ticket, const __grid_constant__ Bf16Views views, int use_mm) {
+    unsigned int* ticket, const __grid_constant__ Bf16Views views, int use_mm, double lnb1, double lnb2) {
   pdl_wait();
   pdl_trigger();
   ncclLsaBarrierSession<ncclCoopCta> bar(ncclCoopCta(), dev, ncclTeamTagLsa(), blockIdx.x);
@@ -59,7 +59,7 @@ __global__ void __launch_bounds__(256) fused_allreduce_adam_kernel(
   __shared__ long long s_t;
   if (threadIdx.x == 0) {
     s_t = *(volatile long long*)counter + 1;
-    adam_coefs(lr, b1, b2, s_t, &s_coef[0], &s_coef[1]);
+    adam_coefs(lr, lnb1, lnb2, s_t, &s_coef[0], &s_coef[1]);
   }
   __syncthreads();
   const float step_size = s_coef[0], bc2_sqrt = s_coef[1];
@@ -123,7 +123,7 @@ int fused_adam_launch(spikerl_fused_adam* fa, float* m, float* v, long long* cou
   Bf16Views none{};
   pdl(fused_allreduce_adam_kernel, fa->blocks, 256, 0, st)(fa->dev, fa->gwin, fa->pwin, fa->n, m, v, counter, lr, b1,
                                                            b2, eps, clo, chi, cmin, ticket, views ? *views : none,
-                                                           fa->multimem);
+                                                           fa->multimem, log((double)b1), log((double)b2));
   SPK_LAUNCHED();
   return SPIKERL_OK;
 }

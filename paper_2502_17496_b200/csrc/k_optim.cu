@@ -106,17 +106,18 @@ __global__ void __launch_bounds__(256) adam_kernel(float* __restrict__ p, const 
                                                    float b2, float eps, size_t clo, size_t chi,
                                                    float cmin, unsigned int* ticket,
                                                    const __grid_constant__ Bf16Views views, float* amp,
-                                                   float amp_growth, float amp_backoff, int amp_interval) {
+                                                   float amp_growth, float amp_backoff, int amp_interval,
+                                                   double lnb1, double lnb2) {
   pdl_wait();
   pdl_trigger();
-  // bias corrections once per block (fp64 pow), not once per thread
+  // bias corrections once per block, not once per thread
   __shared__ float s_coef[3];
   __shared__ long long s_t;
   __shared__ int s_skip;
   if (threadIdx.x == 0) {
     const long long tt = *(volatile long long*)counter + 1;
     s_t = tt;
-    adam_coefs(lr, b1, b2, tt, &s_coef[0], &s_coef[1]);
+    adam_coefs(lr, lnb1, lnb2, tt, &s_coef[0], &s_coef[1]);
     // loss scaling: skip the step on a non-finite gradient, else unscale by 1 / scale
     s_skip = amp ? (*(volatile float*)(amp + 2) != 0.0f) : 0;
     s_coef[2] = amp ? __frcp_rn(*(volatile float*)amp) : 1.0f;
@@ -223,7 +224,7 @@ int launch_adam(float* p, const float* g, float* m, float* v, size_t n, long lon
   }
   pdl(adam_kernel, stream_grid(adam_kernel, n, 8), 256, 0, st)(p, g, m, v, n, counter, lr, b1, b2, eps, clo, chi,
                                              cmin, ticket, views ? *views : none, amp, amp_growth, amp_backoff,
-                                             amp_interval);
+                                             amp_interval, log((double)b1), log((double)b2));
   SPK_LAUNCHED();
   return SPIKERL_OK;
 }
