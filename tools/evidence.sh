@@ -34,6 +34,6 @@ for k in enc_fwd dec_bwd_outscan; do
       python tools/kernel_times.py cfg4 65536 1 > $O/ncu_$k.log 2>&1
 done
 python tools/small_kernels.py > $O/small.log 2>&1
-ncu --set full --clock-control none --import-source on -k regex:adam_kernel -s 40 -c 1 -o $O/prof_adam_kernel \
+ncu --set full --clock-control none --import-source on -k regex:adam_kernel -s 95 -c 1 -o $O/prof_adam_kernel \
     python tools/small_kernels.py > $O/ncu_adam.log 2>&1
 ls -la $O
