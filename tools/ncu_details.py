@@ -3,9 +3,11 @@
   python tools/ncu_details.py <report.ncu-rep> <ID> [section-regex]
 """
 import csv, re, subprocess, sys
+sys.path.insert(0, __import__("os").path.dirname(__import__("os").path.abspath(__file__)))
+from ncu_page import page  # noqa: E402
 rep, kid = sys.argv[1], sys.argv[2]
 pat = re.compile(sys.argv[3] if len(sys.argv) > 3 else ".")
-out = subprocess.run(["ncu", "-i", rep, "--page", "details", "--csv"], capture_output=True, text=True).stdout
+out = page(rep, "details")
 rows = list(csv.reader(out.splitlines()))
 h = rows[0]
 I = {k: h.index(k) for k in ("ID", "Kernel Name", "Section Name", "Metric Name", "Metric Unit", "Metric Value")}

@@ -2,10 +2,11 @@
 SASS lines with equal execution counts (basic blocks), largest first.
   python tools/ncu_groups.py <report.ncu-rep> <units> [n]   (units: divide counts by this, e.g. warp-elements)"""
 import csv, subprocess, sys
+sys.path.insert(0, __import__("os").path.dirname(__import__("os").path.abspath(__file__)))
+from ncu_page import page  # noqa: E402
 rep, units = sys.argv[1], float(sys.argv[2])
 n = int(sys.argv[3]) if len(sys.argv) > 3 else 14
-out = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-source", "sass"], capture_output=True,
-                     text=True).stdout
+out = page(rep, "source", ("--print-source", "sass"))
 h, data = None, []
 for r in csv.reader(out.splitlines()):
     if r and r[0] == "Address":

@@ -6,11 +6,13 @@ The source page holds one table per profiled launch ("Kernel Name" line, then "A
 kernel-regex / occurrence pick the table (default: the first).
 """
 import csv, re, subprocess, sys
+sys.path.insert(0, __import__("os").path.dirname(__import__("os").path.abspath(__file__)))
+from ncu_page import page  # noqa: E402
 rep = sys.argv[1]
 n = int(sys.argv[2]) if len(sys.argv) > 2 else 25
 pat = re.compile(sys.argv[3]) if len(sys.argv) > 3 else None
 occ = int(sys.argv[4]) if len(sys.argv) > 4 else 0
-out = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-source", "sass"], capture_output=True, text=True).stdout
+out = page(rep, "source", ("--print-source", "sass"))
 rows = list(csv.reader(out.splitlines()))
 tables, cur = [], None
 for r in rows:

@@ -12,6 +12,8 @@ import os
 import subprocess
 import sys
 from collections import defaultdict
+sys.path.insert(0, __import__("os").path.dirname(__import__("os").path.abspath(__file__)))
+from ncu_page import page  # noqa: E402
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 KEYS = ["gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.sum",
@@ -25,7 +27,7 @@ SCALE = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "ns": 1e-9, "us": 
 
 
 def raw(rep):
-    out = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
+    out = page(rep, "raw")
     rows = list(csv.reader(out.splitlines()))
     h, units, vals = rows[0], rows[1], rows[2]
     return {k: (vals[h.index(k)], units[h.index(k)]) for k in KEYS if k in h}, vals[h.index("Kernel Name")]
