@@ -92,6 +92,10 @@ typedef struct {
   float sigma_floor;                      /* sigma clamp after the actor Adam step (1e-3)     */
   int precision;                          /* enum spikerl_precision                           */
   int engine;                             /* enum spikerl_engine                              */
+  int reset_grad;                         /* rho: 0 = reset gate (1 - o_{t-1}) detached in BPTT
+                                             (default); 1 = differentiated through it:
+                                             delta_v_t = h_t (g_t - d_v v_t delta_v_{t+1}) +
+                                             d_v (1 - o_t) delta_v_{t+1} (needs fp32 v_t in the tape) */
 } spikerl_actor_cfg;
 
 /* Twin critic Q_i(s,a) = W3 relu(W2 relu(W1 [s;a] + b1) + b2) + b3 (configs[1]). */
@@ -159,6 +163,7 @@ typedef struct {
   int padded[4];           /* P0..P3                                                        */
   size_t bitsT[4], maskT[4];
   int tpad;                /* T rounded up to 16                                            */
+  size_t V[4];             /* reset_grad = 1: membrane potentials fp32 [T][B][P_l], l = 1..3 (else 0) */
 } spikerl_tape_layout;
 int spikerl_actor_tape_layout(const spikerl_actor_cfg* cfg, int batch, spikerl_tape_layout* out);
 

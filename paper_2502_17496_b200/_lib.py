@@ -30,7 +30,7 @@ class ActorCfg(C.Structure):
                 ("hidden1", C.c_int), ("hidden2", C.c_int), ("T", C.c_int),
                 ("d_c", C.c_float), ("d_v", C.c_float), ("v_th", C.c_float),
                 ("surr_window", C.c_float), ("surr_height", C.c_float), ("sigma_floor", C.c_float),
-                ("precision", C.c_int), ("engine", C.c_int)]
+                ("precision", C.c_int), ("engine", C.c_int), ("reset_grad", C.c_int)]
 
 
 class CriticCfg(C.Structure):
@@ -49,7 +49,7 @@ class TapeLayout(C.Structure):
     _fields_ = [("A", C.c_size_t), ("bits", C.c_size_t * 4), ("mask", C.c_size_t * 4),
                 ("counts", C.c_size_t), ("act", C.c_size_t), ("total", C.c_size_t),
                 ("padded", C.c_int * 4), ("bitsT", C.c_size_t * 4), ("maskT", C.c_size_t * 4),
-                ("tpad", C.c_int)]
+                ("tpad", C.c_int), ("V", C.c_size_t * 4)]
 
 
 class Tape(C.Structure):

@@ -31,16 +31,16 @@ def _stream(stream=None):
 # ------------------------------------------------------------------------------------ configs
 def actor_cfg(obs_dim, act_dim, pop_enc=10, pop_dec=10, hidden1=256, hidden2=256, T=5, d_c=0.5, d_v=0.75,
               v_th=0.5, surr_window=0.5, surr_height=1.0, sigma_floor=1e-3, precision="bf16",
-              engine="auto") -> L.ActorCfg:
+              engine="auto", reset_grad=0) -> L.ActorCfg:
     return L.ActorCfg(obs_dim, act_dim, pop_enc, pop_dec, hidden1, hidden2, T, d_c, d_v, v_th, surr_window,
-                      surr_height, sigma_floor, _PREC[precision], _ENG[engine])
+                      surr_height, sigma_floor, _PREC[precision], _ENG[engine], reset_grad)
 
 
-def actor_cfg_from(shape, engine="auto") -> L.ActorCfg:
+def actor_cfg_from(shape, engine="auto", reset_grad=0) -> L.ActorCfg:
     """From any object with the problem-statement attributes (obs_dim, act_dim, pop_enc, ...)."""
     return actor_cfg(shape.obs_dim, shape.act_dim, shape.pop_enc, shape.pop_dec, shape.n1, shape.n2, shape.T,
                      shape.d_c, shape.d_v, shape.v_th, shape.surr_window, shape.surr_height, shape.sigma_floor,
-                     shape.precision, engine)
+                     shape.precision, engine, reset_grad)
 
 
 def critic_cfg(in_dim, hidden1=256, hidden2=256, precision="bf16") -> L.CriticCfg:
@@ -210,6 +210,9 @@ def tape_view(cfg, B, buf, base=0):
             # the tcgen05 engine keeps the hidden layers' window bits only quad-major (the
             # dX epilogue's input); this diagnostic view re-packs them batch-major
             out[f"mask{l}"] = _quads_to_words(out[f"maskT{l}"], T, B)
+    for l in (1, 2, 3):
+        if lay.V[l]:
+            out[f"V{l}"] = seg(lay.V[l], 4 * T * B * lay.padded[l], torch.float32, (T, B, lay.padded[l]))
     out["counts"] = seg(lay.counts, B * N3, torch.uint8, (B, N3))
     out["act"] = seg(lay.act, 4 * B * cfg.act_dim, torch.float32, (B, cfg.act_dim))
     return out

@@ -132,6 +132,7 @@ struct ActorDims {
   int bf16;       // 16-bit GEMM operands (precision BF16 or FP16)
   int f16;        // ... and they are fp16 (precision FP16: tcgen05 engine only)
   int engine;     // resolved: SPIKERL_ENGINE_SIMT or SPIKERL_ENGINE_TCGEN05
+  int rho;        // reset_grad: BPTT through the reset gate (fp32 v_t kept in the tape)
 };
 int actor_dims(const spikerl_actor_cfg* cfg, ActorDims* d);
 unsigned long long actor_cfg_hash(const spikerl_actor_cfg* cfg);
@@ -143,6 +144,7 @@ struct TapeLayout {
   // written by the forward epilogue, read by the DX epilogue
   size_t bitsT[4], maskT[4];
   int tpad;   // T rounded up to 16
+  size_t V[4];   // rho = 1: fp32 membrane potentials [T][B][P_l], l = 1..3 (else 0)
 };
 TapeLayout tape_layout(const ActorDims& d, int B);
 
@@ -189,6 +191,12 @@ __device__ __forceinline__ void lif_step(const LifConst& k, float I, float& c, f
 // Reverse-scan step (rho = 0; reset gate detached): given g_o(t), o_t, h_t (bits) and the
 // carried (dv_next, dc_next), returns G_t = delta_c_t.  SPEC.md:168-176; R11.
 //   delta_v_t = h_t z g_t + d_v (1 - o_t) delta_v_{t+1};  delta_c_t = delta_v_t + d_c delta_c_{t+1}
+// rho = 1 (reset gate differentiated, SPEC.md:171 variant; R11): the upstream gradient of
+// step t becomes g - d_v v_t delta_v_{t+1} before the window factor: delta_v_t = h z (g - d_v v_t
+// delta_v_{t+1}) + d_v (1 - o_t) delta_v_{t+1}.
+__device__ __forceinline__ float rho_grad(float g, float dvc, float v, float dvn) {
+  return __fmaf_rn(-__fmul_rn(dvc, v), dvn, g);
+}
 __device__ __forceinline__ float lif_back_step(float zh, float dvc, float dcc, float g, bool o,
                                                bool h, float& dvn, float& dcn) {
   const float hg = h ? __fmul_rn(zh, g) : 0.0f;

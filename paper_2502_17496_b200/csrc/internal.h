@@ -13,20 +13,21 @@ int launch_enc_fwd(const ActorDims& d, int B, const float* obs, const float* mu,
 // forward layer l (1..3): bits_in [T][B][W_{l-1}] -> bits_out, mask_out [T][B][W_l] (+counts)
 int launch_lif_fwd_simt(const ActorDims& d, int l, int B, const uint32_t* bits_in,
                         const float* Wf32, const __nv_bfloat16* Wb16, uint32_t* bits_out,
-                        uint32_t* mask_out, uint8_t* counts, cudaStream_t st);
+                        uint32_t* mask_out, uint8_t* counts, float* v_out, cudaStream_t st);
 int launch_dec_fwd(const ActorDims& d, int B, const uint8_t* counts, const float* Wd,
                    const float* bd, float* act_out, float* act_tape, cudaStream_t st);
 // decoder backward + output-layer reverse scan -> G3 [T][B][P3] (fp32 or bf16 per precision)
 int launch_dec_bwd_outscan(const ActorDims& d, int B, const float* grad_a, const float* act,
                            const uint8_t* counts, const float* Wd, const uint32_t* bits3,
-                           const uint32_t* mask3, void* G3, float* g_pre, cudaStream_t st);
+                           const uint32_t* mask3, const float* v3, void* G3, float* g_pre, cudaStream_t st);
 int dec_param_chunks(int B);   // row chunks of the decoder parameter gradient (partials: chunks x (N3 + A))
 int launch_dec_param_grads(const ActorDims& d, int B, const float* g_pre, const uint8_t* counts,
                            float* dWd, float* dbd, float* part, int accumulate, cudaStream_t st);
 // dX of layer l (3 or 2) fused with the reverse scan of layer l-1 -> G_{l-1} (+Gsum if l==2)
 int launch_lif_dx_simt(const ActorDims& d, int l, int B, const void* Gl, const float* Wf32,
                        const __nv_bfloat16* Wb16, const uint32_t* bits_prev,
-                       const uint32_t* mask_prev, void* Gprev, void* Gsum, cudaStream_t st);
+                       const uint32_t* mask_prev, const float* v_prev, void* Gprev, void* Gsum,
+                       cudaStream_t st);
 // dW_l = sum_{t,b} G_l^T o_{l-1}  (fp32 [N_l][N_{l-1}] in the master layout)
 int launch_lif_dw_simt(const ActorDims& d, int l, int B, const void* Gl, const uint32_t* bits_prev,
                        float* dW, int accumulate, cudaStream_t st);
@@ -43,10 +44,10 @@ bool tc_pairs_enabled();   // CTA pairs (cta_group::2) in use (SPIKERL_TC_PAIR=0
 int launch_lif_fwd_tc(const ActorDims& d, int l, int B, const uint32_t* bits_in,
                       const __nv_bfloat16* Wb16, uint32_t* bits_out, uint32_t* mask_out,
                       uint8_t* counts, uint8_t* bitsT_out, uint8_t* maskT_out, int row_bytes,
-                      cudaStream_t st);
+                      float* v_out, cudaStream_t st);
 int launch_lif_dx_tc(const ActorDims& d, int l, int B, const void* Gl, const __nv_bfloat16* Wb16,
-                     const uint8_t* bitsT_prev, const uint8_t* maskT_prev, int row_bytes, void* Gprev,
-                     void* Gsum, cudaStream_t st);
+                     const uint8_t* bitsT_prev, const uint8_t* maskT_prev, int row_bytes,
+                     const float* v_prev, void* Gprev, void* Gsum, cudaStream_t st);
 int launch_enc_grad_tc(const ActorDims& d, int B, const void* Gsum, const __nv_bfloat16* W1b16,
                        const float* A, const float* obs, const float* mu, const float* sigma,
                        float* partial, float* dmu, float* dsigma, int accumulate, cudaStream_t st);

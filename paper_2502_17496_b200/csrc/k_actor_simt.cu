@@ -22,7 +22,7 @@ template <typename WT>
 __global__ void __launch_bounds__(128) lif_fwd_simt_kernel(
     int B, int T, int N, int Win, int Wout, const uint32_t* __restrict__ bits_in,
     const WT* __restrict__ W, int ldw_, LifConst kc, uint32_t* __restrict__ bits_out,
-    uint32_t* __restrict__ mask_out, uint8_t* __restrict__ counts) {
+    uint32_t* __restrict__ mask_out, uint8_t* __restrict__ counts, float* __restrict__ v_out, int P) {
   pdl_wait();
   pdl_trigger();
   extern __shared__ uint32_t s_words[];
@@ -52,6 +52,7 @@ __global__ void __launch_bounds__(128) lif_fwd_simt_kernel(
     if (n < N) {
       lif_step(kc, I, c, v, o, h);
     }
+    if (v_out) v_out[((size_t)t * B + b) * P + n] = v;   // rho = 1 tape (padding neurons: 0)
     const uint32_t ob = __ballot_sync(0xffffffffu, o);
     const uint32_t hb = __ballot_sync(0xffffffffu, h);
     if (lane == 0) {
@@ -67,7 +68,7 @@ __global__ void __launch_bounds__(128) lif_fwd_simt_kernel(
 
 int launch_lif_fwd_simt(const ActorDims& d, int l, int B, const uint32_t* bits_in,
                         const float* Wf32, const __nv_bfloat16* Wb16, uint32_t* bits_out,
-                        uint32_t* mask_out, uint8_t* counts, cudaStream_t st) {
+                        uint32_t* mask_out, uint8_t* counts, float* v_out, cudaStream_t st) {
   ProfScope ps_(l == 1 ? "lif_fwd_simt_L1" : (l == 2 ? "lif_fwd_simt_L2" : "lif_fwd_simt_L3"), PB_ALU,
                 2.0 * d.T * B * (double)d.N[l] * d.N[l - 1], 0.0, st);
   LifConst kc{d.dc, d.dv, d.vth, d.win};
@@ -76,10 +77,10 @@ int launch_lif_fwd_simt(const ActorDims& d, int l, int B, const uint32_t* bits_i
   const size_t smem = sizeof(uint32_t) * Win;
   if (d.bf16) {
     pdl((lif_fwd_simt_kernel<__nv_bfloat16>), grid, 128, smem, st)(
-        B, d.T, d.N[l], Win, Wout, bits_in, Wb16, d.P[l - 1], kc, bits_out, mask_out, counts);
+        B, d.T, d.N[l], Win, Wout, bits_in, Wb16, d.P[l - 1], kc, bits_out, mask_out, counts, v_out, d.P[l]);
   } else {
     pdl((lif_fwd_simt_kernel<float>), grid, 128, smem, st)(B, d.T, d.N[l], Win, Wout, bits_in, Wf32,
-                                                       d.N[l - 1], kc, bits_out, mask_out, counts);
+                                                       d.N[l - 1], kc, bits_out, mask_out, counts, v_out, d.P[l]);
   }
   SPK_LAUNCHED();
   return SPIKERL_OK;
@@ -158,8 +159,8 @@ template <typename GTy, int TT>
 __global__ void __launch_bounds__(256, 4) dec_bwd_outscan_kernel(
     int B, int T, int A, int D, int N3, int W3, float dcc, float dvc, float zh,
     const float* __restrict__ grad_a, const float* __restrict__ act, const float* __restrict__ Wd,
-    const uint32_t* __restrict__ bits3, const uint32_t* __restrict__ mask3, GTy* __restrict__ G3,
-    float* __restrict__ g_pre_out, int write_pad) {
+    const uint32_t* __restrict__ bits3, const uint32_t* __restrict__ mask3, const float* __restrict__ v3,
+    GTy* __restrict__ G3, float* __restrict__ g_pre_out, int write_pad) {
   pdl_wait();
   pdl_trigger();
   // lane = (row jr of 2, word wq of 4, octet oct of 4): a warp stores 2 rows x 128 neurons, i.e.
@@ -206,13 +207,22 @@ __global__ void __launch_bounds__(256, 4) dec_bwd_outscan_kernel(
     const uint32_t* po = bits3 + (size_t)b * W3 + w;
     const uint32_t* ph = mask3 + (size_t)b * W3 + w;
     GTy* gq = G3 + (size_t)b * P3 + n0 + (size_t)(T - 1) * gts;   // step T-1; walks back by gts
+    const float* vq = v3 ? v3 + (size_t)b * P3 + n0 + (size_t)(T - 1) * gts : nullptr;   // rho = 1
+    const float zdv = __fmul_rn(zh, dvc);
     auto step = [&](uint32_t ow, uint32_t hw) {
       const uint32_t o8 = (ow >> (8 * oct)) & 0xFFu, h8 = (hw >> (8 * oct)) & 0xFFu;
-      float G[8];
+      float G[8], vv[8];
+      if (vq) {
+        const float4 a = reinterpret_cast<const float4*>(vq)[0], c = reinterpret_cast<const float4*>(vq)[1];
+        vv[0] = a.x; vv[1] = a.y; vv[2] = a.z; vv[3] = a.w; vv[4] = c.x; vv[5] = c.y; vv[6] = c.z; vv[7] = c.w;
+        vq -= gts;
+      }
 #pragma unroll
       for (int i = 0; i < 8; ++i) {
-        // lif_back_step with the window factor z folded into g (z is a constant per layer)
-        const float hg = ((h8 >> i) & 1u) ? g[i] : 0.0f;
+        // lif_back_step with the window factor z folded into g (z is a constant per layer); rho = 1
+        // subtracts z d_v v_t delta_v_{t+1}
+        const float gi = vq ? __fmaf_rn(-__fmul_rn(zdv, vv[i]), dvn[i], g[i]) : g[i];
+        const float hg = ((h8 >> i) & 1u) ? gi : 0.0f;
         const float dvt = ((o8 >> i) & 1u) ? hg : __fmaf_rn(dvc, dvn[i], hg);
         const float dct = __fmaf_rn(dcc, dcn[i], dvt);
         dvn[i] = dvt;
@@ -285,7 +295,7 @@ __global__ void __launch_bounds__(256, 4) dec_bwd_outscan_tma_kernel(
     const __grid_constant__ CUtensorMap map_o, const __grid_constant__ CUtensorMap map_h, int B, int T, int A,
     int D, int N3, int W3, int NO, int R, int planeS, float dcc, float dvc, float zh,
     const float* __restrict__ grad_a, const float* __restrict__ act, const float* __restrict__ Wd,
-    GTy* __restrict__ G3, float* __restrict__ g_pre_out, int write_pad) {
+    const float* __restrict__ v3, GTy* __restrict__ G3, float* __restrict__ g_pre_out, int write_pad) {
   extern __shared__ __align__(128) uint8_t osm[];
   uint32_t* sbuf = reinterpret_cast<uint32_t*>(osm);              // [2 buffers][2 planes][planeS]
   uint64_t* bar = reinterpret_cast<uint64_t*>(osm + (size_t)16 * planeS);
@@ -388,13 +398,19 @@ __global__ void __launch_bounds__(256, 4) dec_bwd_outscan_tma_kernel(
       // G3 element offsets of this row: 32-bit (T B P3 < 2^32 is checked at launch)
       const uint32_t gts32 = (uint32_t)B * (uint32_t)P3;
       uint32_t go = (uint32_t)b * (uint32_t)P3 + (uint32_t)n0 + (uint32_t)(T - 1) * gts32;
+      const float zdv = __fmul_rn(zh, dvc);
 #pragma unroll (TT > 0 ? TT : 2)
       for (int t = T - 1; t >= 0; --t) {
         const uint32_t o8 = (so[t * tstr] >> sh) & 0xFFu, h8 = (sm[t * tstr] >> sh) & 0xFFu;
-        float G[8];
+        float G[8], vv[8];
+        if (v3) {   // rho = 1: v_t of the 8 neurons (same element offsets as G3)
+          const float4 a = reinterpret_cast<const float4*>(v3 + go)[0], c = reinterpret_cast<const float4*>(v3 + go)[1];
+          vv[0] = a.x; vv[1] = a.y; vv[2] = a.z; vv[3] = a.w; vv[4] = c.x; vv[5] = c.y; vv[6] = c.z; vv[7] = c.w;
+        }
 #pragma unroll
         for (int i = 0; i < 8; ++i) {
-          const float hg = ((h8 >> i) & 1u) ? g[i] : 0.0f;
+          const float gi = v3 ? __fmaf_rn(-__fmul_rn(zdv, vv[i]), dvn[i], g[i]) : g[i];
+          const float hg = ((h8 >> i) & 1u) ? gi : 0.0f;
           const float dvt = ((o8 >> i) & 1u) ? hg : __fmaf_rn(dvc, dvn[i], hg);
           const float dct = __fmaf_rn(dcc, dcn[i], dvt);
           dvn[i] = dvt;
@@ -423,7 +439,7 @@ static void outscan_plan(const ActorDims& d, int wpad, int* NO, int* R, int* pla
 
 int launch_dec_bwd_outscan(const ActorDims& d, int B, const float* grad_a, const float* act,
                            const uint8_t* counts, const float* Wd, const uint32_t* bits3,
-                           const uint32_t* mask3, void* G3, float* g_pre, cudaStream_t st) {
+                           const uint32_t* mask3, const float* v3, void* G3, float* g_pre, cudaStream_t st) {
   // algorithmic bytes: G3 written for the N3 real neurons (tcgen05: padding never written), both
   // bit planes read
   const double gcols = d.engine == SPIKERL_ENGINE_TCGEN05 ? d.N3 : d.P[3];
@@ -455,7 +471,7 @@ int launch_dec_bwd_outscan(const ActorDims& d, int B, const float* grad_a, const
       const int waves = cdiv(units, cap);
       const int blocks = cdiv(units, waves);   // every block gets `waves` units (the last one fewer)
       pdl(kern, blocks, threads, smem, st)(mo, mh, B, d.T, d.A, d.D, d.N3, d.Wd[3], NO, R, planeS, d.dc, d.dv,
-                                            d.zh, grad_a, act, Wd, G, g_pre, wpad);
+                                            d.zh, grad_a, act, Wd, v3, G, g_pre, wpad);
       SPK_LAUNCHED();
       return SPIKERL_OK;
     };
@@ -476,17 +492,17 @@ int launch_dec_bwd_outscan(const ActorDims& d, int B, const float* grad_a, const
   if (blocks > (long long)num_sms() * 8) blocks = (long long)num_sms() * 8;
   if (d.f16) {
     pdl((dec_bwd_outscan_kernel<__half, 0>), (int)blocks, 256, 0, st)(
-        B, d.T, d.A, d.D, d.N3, d.Wd[3], d.dc, d.dv, d.zh, grad_a, act, Wd, bits3, mask3, (__half*)G3, g_pre, wpad);
+        B, d.T, d.A, d.D, d.N3, d.Wd[3], d.dc, d.dv, d.zh, grad_a, act, Wd, bits3, mask3, v3, (__half*)G3, g_pre, wpad);
   } else if (d.bf16) {
     if (d.T == 16) pdl((dec_bwd_outscan_kernel<__nv_bfloat16, 16>), (int)blocks, 256, 0, st)(
-        B, d.T, d.A, d.D, d.N3, d.Wd[3], d.dc, d.dv, d.zh, grad_a, act, Wd, bits3, mask3, (__nv_bfloat16*)G3, g_pre, wpad);
+        B, d.T, d.A, d.D, d.N3, d.Wd[3], d.dc, d.dv, d.zh, grad_a, act, Wd, bits3, mask3, v3, (__nv_bfloat16*)G3, g_pre, wpad);
     else if (d.T == 5) pdl((dec_bwd_outscan_kernel<__nv_bfloat16, 5>), (int)blocks, 256, 0, st)(
-        B, d.T, d.A, d.D, d.N3, d.Wd[3], d.dc, d.dv, d.zh, grad_a, act, Wd, bits3, mask3, (__nv_bfloat16*)G3, g_pre, wpad);
+        B, d.T, d.A, d.D, d.N3, d.Wd[3], d.dc, d.dv, d.zh, grad_a, act, Wd, bits3, mask3, v3, (__nv_bfloat16*)G3, g_pre, wpad);
     else pdl((dec_bwd_outscan_kernel<__nv_bfloat16, 0>), (int)blocks, 256, 0, st)(
-        B, d.T, d.A, d.D, d.N3, d.Wd[3], d.dc, d.dv, d.zh, grad_a, act, Wd, bits3, mask3, (__nv_bfloat16*)G3, g_pre, wpad);
+        B, d.T, d.A, d.D, d.N3, d.Wd[3], d.dc, d.dv, d.zh, grad_a, act, Wd, bits3, mask3, v3, (__nv_bfloat16*)G3, g_pre, wpad);
   } else {
     pdl((dec_bwd_outscan_kernel<float, 0>), (int)blocks, 256, 0, st)(
-        B, d.T, d.A, d.D, d.N3, d.Wd[3], d.dc, d.dv, d.zh, grad_a, act, Wd, bits3, mask3, (float*)G3, g_pre, 1);
+        B, d.T, d.A, d.D, d.N3, d.Wd[3], d.dc, d.dv, d.zh, grad_a, act, Wd, bits3, mask3, v3, (float*)G3, g_pre, 1);
   }
   SPK_LAUNCHED();
   return SPIKERL_OK;
@@ -627,7 +643,8 @@ template <typename GTy, typename WT>
 __global__ void __launch_bounds__(128) lif_dx_simt_kernel(
     int B, int T, int Nl, int Pl, int Nprev, int Pprev, int Wprev, float dcc, float dvc, float zh,
     const GTy* __restrict__ Gl, const WT* __restrict__ W, int ldw_, const uint32_t* __restrict__ bits,
-    const uint32_t* __restrict__ mask, GTy* __restrict__ Gprev, GTy* __restrict__ Gsum) {
+    const uint32_t* __restrict__ mask, const float* __restrict__ vprev, GTy* __restrict__ Gprev,
+    GTy* __restrict__ Gsum) {
   pdl_wait();
   pdl_trigger();
   extern __shared__ float s_g[];
@@ -643,6 +660,7 @@ __global__ void __launch_bounds__(128) lif_dx_simt_kernel(
       float g = 0.f;
       for (int n = 0; n < Nl; ++n) g = __fmaf_rn(s_g[n], ldw<WT>(W + (size_t)n * ldw_ + k), g);
       const uint32_t ow = bits[row * Wprev + (k >> 5)], hw = mask[row * Wprev + (k >> 5)];
+      if (vprev) g = rho_grad(g, dvc, vprev[row * Pprev + k], dvn);   // rho = 1
       Gt = lif_back_step(zh, dvc, dcc, g, (ow >> (k & 31)) & 1u, (hw >> (k & 31)) & 1u, dvn, dcn);
       gs = __fadd_rn(gs, Gt);
     }
@@ -654,19 +672,20 @@ __global__ void __launch_bounds__(128) lif_dx_simt_kernel(
 
 int launch_lif_dx_simt(const ActorDims& d, int l, int B, const void* Gl, const float* Wf32,
                        const __nv_bfloat16* Wb16, const uint32_t* bits_prev,
-                       const uint32_t* mask_prev, void* Gprev, void* Gsum, cudaStream_t st) {
+                       const uint32_t* mask_prev, const float* v_prev, void* Gprev, void* Gsum,
+                       cudaStream_t st) {
   ProfScope ps_(l == 3 ? "lif_dx_simt_L3" : "lif_dx_simt_L2", PB_ALU, 2.0 * d.T * B * (double)d.N[l] * d.N[l - 1], 0.0, st);
   dim3 grid(B, d.P[l - 1] / 128);
   const size_t smem = sizeof(float) * d.N[l];
   if (d.bf16)
     pdl((lif_dx_simt_kernel<__nv_bfloat16, __nv_bfloat16>), grid, 128, smem, st)(
         B, d.T, d.N[l], d.P[l], d.N[l - 1], d.P[l - 1], d.Wd[l - 1], d.dc, d.dv, d.zh,
-        (const __nv_bfloat16*)Gl, Wb16, d.P[l - 1], bits_prev, mask_prev, (__nv_bfloat16*)Gprev,
+        (const __nv_bfloat16*)Gl, Wb16, d.P[l - 1], bits_prev, mask_prev, v_prev, (__nv_bfloat16*)Gprev,
         (__nv_bfloat16*)Gsum);
   else
     pdl((lif_dx_simt_kernel<float, float>), grid, 128, smem, st)(
         B, d.T, d.N[l], d.P[l], d.N[l - 1], d.P[l - 1], d.Wd[l - 1], d.dc, d.dv, d.zh,
-        (const float*)Gl, Wf32, d.N[l - 1], bits_prev, mask_prev, (float*)Gprev, (float*)Gsum);
+        (const float*)Gl, Wf32, d.N[l - 1], bits_prev, mask_prev, v_prev, (float*)Gprev, (float*)Gsum);
   SPK_LAUNCHED();
   return SPIKERL_OK;
 }

@@ -76,6 +76,7 @@ struct Params {
   const uint32_t* bits_in; int w_in;
   uint32_t* bits_out; uint32_t* mask_out; int w_out; uint8_t* counts; int n_valid; int n3;
   uint8_t* bitsT_out; uint8_t* maskT_out; int p_out;   // quad-major copies (may be null)
+  float* v_out; const float* v_prev;                     // rho = 1: fp32 membrane planes [T][B][P_l]
   LifConst kc; float zh;
   int tpad;                                              // T rounded to 16 (tpad / 2 bytes per (quad, neuron))
   // DX
@@ -338,7 +339,10 @@ __device__ __forceinline__ Tile decode(const Params& p, int u, int rank, int CG)
 // tile with tcgen05.mma.cta_group::2 issued by rank 0: each CTA holds its 128 rows of A and half
 // of the B columns, every TMA / expander / epilogue completion signals rank 0's barriers, and the
 // MMA commits multicast back to both CTAs.
-template <int MODE, int BT, int CG, bool F16 = false>
+// RHO: the reset-gate-gradient variant (R11, rho = 1): FWD / FWDO write the fp32 membrane
+// planes, DX reads the previous layer's; a separate instantiation, so the default path carries no
+// extra registers for it
+template <int MODE, int BT, int CG, bool F16 = false, bool RHO = false>
 __global__ void __launch_bounds__(NUM_THREADS, 1)
     tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
               const __grid_constant__ CUtensorMap tmC, const Params p) {
@@ -712,6 +716,9 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
                 const bool o = v[j] > vth;
                 const bool h = fabsf(__fsub_rn(v[j], vth)) < win;
                 rv[j] = o ? 0.0f : dv;
+                if constexpr (RHO) {
+                  if (b0 + j < p.B) p.v_out[((size_t)tt * p.B + b0 + j) * p.p_out + row] = v[j];
+                }
                 if (o) ocur |= 1u << j;
                 if (h) hcur |= 1u << j;
                 const uint32_t ob = __ballot_sync(0xffffffffu, o);
@@ -794,6 +801,16 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
 #pragma unroll
             for (int ci = 0; ci < DX_CH; ++ci)
               if (tb + ci < p.T) tmem_ldn<HB>(taddr + (tb + ci) * BT + jb, rr[ci]);
+            // rho = 1: the chunk's membrane potentials of this neuron (rows past B read as 0)
+            float vv[DX_CH][HB];
+            if constexpr (RHO) {
+#pragma unroll
+              for (int ci = 0; ci < DX_CH; ++ci)
+#pragma unroll
+                for (int j = 0; j < HB; ++j)
+                  vv[ci][j] = (tb + ci < p.T && b0 + j < p.B)
+                                  ? __ldg(p.v_prev + ((size_t)(tb + ci) * p.B + b0 + j) * p.p_prev + row) : 0.f;
+            }
             if ((tb >> 4) != ch) {
               ch = tb >> 4;
 #pragma unroll
@@ -814,7 +831,8 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
 #pragma unroll
               for (int j = 0; j < HB; ++j) {
                 const uint32_t bm = 1u << (16 * (j >> 2) + 4 * ci + (j & 3));
-                const float gv = __uint_as_float(rr[ci][j]);
+                float gv = __uint_as_float(rr[ci][j]);
+                if constexpr (RHO) gv = rho_grad(gv, dvc, vv[ci][j], dvn[j]);   // rho = 1
                 // lif_back_step (common.cuh), same operations: delta_v = h z g + d_v (1 - o) delta_v',
                 // delta_c = delta_v + d_c delta_c'
                 const float hg = (xh & bm) ? __fmul_rn(zh, gv) : 0.0f;
@@ -1118,13 +1136,13 @@ static bool pairs_enabled() {
   return v == 1;
 }
 
-template <int MODE, int BT, int CG, bool F16>
+template <int MODE, int BT, int CG, bool F16, bool RHO = false>
 static int launch_cg(const CUtensorMap& ma, const CUtensorMap& mb, const CUtensorMap& mc, const Params& p, cudaStream_t st) {
-  SPK_SMEM_ATTR((tc_kernel<MODE, BT, CG, F16>), SMEM_BYTES);
+  SPK_SMEM_ATTR((tc_kernel<MODE, BT, CG, F16, RHO>), SMEM_BYTES);
   if (CG == 1) {
     const int ncta = num_sms();
     const int grid = p.n_units < ncta ? (int)p.n_units : ncta;
-    pdl((tc_kernel<MODE, BT, CG, F16>), grid, NUM_THREADS, SMEM_BYTES, st)(ma, mb, mc, p);
+    pdl((tc_kernel<MODE, BT, CG, F16, RHO>), grid, NUM_THREADS, SMEM_BYTES, st)(ma, mb, mc, p);
   } else {
     cudaLaunchConfig_t cfg = {};
     cfg.blockDim = dim3(NUM_THREADS, 1, 1);
@@ -1144,7 +1162,7 @@ static int launch_cg(const CUtensorMap& ma, const CUtensorMap& mb, const CUtenso
     const int slots = pair_slots();
     const long long grid = p.n_units < slots ? p.n_units : slots;
     cfg.gridDim = dim3((unsigned)(grid * CG), 1, 1);
-    cudaError_t e = cudaLaunchKernelEx(&cfg, tc_kernel<MODE, BT, CG, F16>, ma, mb, mc, p);
+    cudaError_t e = cudaLaunchKernelEx(&cfg, tc_kernel<MODE, BT, CG, F16, RHO>, ma, mb, mc, p);
     if (e != cudaSuccess) { set_error("cudaLaunchKernelEx (pair): %s", cudaGetErrorString(e)); return SPIKERL_E_CUDA; }
   }
   SPK_LAUNCHED();
@@ -1168,6 +1186,14 @@ static int launch(const CUtensorMap& ma, const CUtensorMap& mb, const CUtensorMa
   // MMA instruction descriptor are then compile-time (a runtime switch cost ~2% at configs[4])
   if constexpr (is_crit(MODE)) {   // bf16, single CTAs only
     return launch_cg<MODE, BT, 1, false>(ma, mb, mc, p, st);
+  } else if constexpr (is_fwd(MODE) || MODE == DX) {
+    if (p.v_out || p.v_prev) {   // rho = 1 (bf16 operands only; checked by the caller)
+      return p.cg == 2 ? launch_cg<MODE, BT, 2, false, true>(ma, mb, mc, p, st)
+                       : launch_cg<MODE, BT, 1, false, true>(ma, mb, mc, p, st);
+    }
+    if (p.f16)
+      return p.cg == 2 ? launch_cg<MODE, BT, 2, true>(ma, mb, mc, p, st) : launch_cg<MODE, BT, 1, true>(ma, mb, mc, p, st);
+    return p.cg == 2 ? launch_cg<MODE, BT, 2, false>(ma, mb, mc, p, st) : launch_cg<MODE, BT, 1, false>(ma, mb, mc, p, st);
   } else {
     if (MODE != WG && p.f16)
       return p.cg == 2 ? launch_cg<MODE, BT, 2, true>(ma, mb, mc, p, st) : launch_cg<MODE, BT, 1, true>(ma, mb, mc, p, st);
@@ -1222,7 +1248,7 @@ bool tc_supported(const ActorDims& d) {
 
 int launch_lif_fwd_tc(const ActorDims& d, int l, int B, const uint32_t* bits_in, const __nv_bfloat16* Wb16,
                       uint32_t* bits_out, uint32_t* mask_out, uint8_t* counts, uint8_t* bitsT_out,
-                      uint8_t* maskT_out, int row_bytes, cudaStream_t st) {
+                      uint8_t* maskT_out, int row_bytes, float* v_out, cudaStream_t st) {
   ProfScope ps_(l == 1 ? "lif_fwd_tc_L1" : (l == 2 ? "lif_fwd_tc_L2" : "lif_fwd_tc_L3"), PB_TENSOR,
                 2.0 * d.T * B * (double)d.N[l] * d.N[l - 1], 0.0, st);
   Params p{};
@@ -1240,6 +1266,7 @@ int launch_lif_fwd_tc(const ActorDims& d, int l, int B, const uint32_t* bits_in,
   p.bits_out = bits_out; p.mask_out = mask_out; p.w_out = d.Wd[l];
   p.counts = counts; p.n_valid = d.N[l]; p.n3 = d.N[3];
   p.bitsT_out = bitsT_out; p.maskT_out = maskT_out; p.p_out = d.P[l]; p.tpad = row_bytes;
+  p.v_out = v_out;
   p.kc = LifConst{d.dc, d.dv, d.vth, d.win}; p.zh = d.zh;
   CUtensorMap ma, mb;
   const uint64_t dims[2] = {(uint64_t)d.P[l - 1], (uint64_t)d.P[l]};
@@ -1252,8 +1279,8 @@ int launch_lif_fwd_tc(const ActorDims& d, int l, int B, const uint32_t* bits_in,
 
 // dX of layer l fused with the reverse scan of layer l-1 (G_l bf16 [T][B][P_l])
 int launch_lif_dx_tc(const ActorDims& d, int l, int B, const void* Gl, const __nv_bfloat16* Wb16,
-                     const uint8_t* bitsT_prev, const uint8_t* maskT_prev, int row_bytes, void* Gprev,
-                     void* Gsum, cudaStream_t st) {
+                     const uint8_t* bitsT_prev, const uint8_t* maskT_prev, int row_bytes,
+                     const float* v_prev, void* Gprev, void* Gsum, cudaStream_t st) {
   ProfScope ps_(l == 3 ? "lif_dx_tc_L3" : "lif_dx_tc_L2", PB_TENSOR, 2.0 * d.T * B * (double)d.N[l] * d.N[l - 1],
                 0.0, st);
   Params p{};
@@ -1269,6 +1296,7 @@ int launch_lif_dx_tc(const ActorDims& d, int l, int B, const void* Gl, const __n
   p.n_units = p.m_tiles * p.n_tiles;
   p.bitsT_prev = bitsT_prev; p.maskT_prev = maskT_prev; p.tpad = row_bytes;
   p.g_prev = (__nv_bfloat16*)Gprev; p.p_prev = d.P[l - 1]; p.g_sum = (__nv_bfloat16*)Gsum;
+  p.v_prev = v_prev;
   p.n_valid = d.N[l - 1];
   p.kc = LifConst{d.dc, d.dv, d.vth, d.win}; p.zh = d.zh;
   CUtensorMap ma, mb;

@@ -85,6 +85,10 @@ int actor_dims(const spikerl_actor_cfg* c, ActorDims* d) {
               c->surr_window);
     return SPIKERL_E_DOMAIN;
   }
+  if (c->reset_grad != 0 && c->reset_grad != 1) {
+    set_error("reset_grad must be 0 (detached) or 1 (through the reset gate), got %d", c->reset_grad);
+    return SPIKERL_E_DOMAIN;
+  }
   if (c->precision != SPIKERL_FP32 && c->precision != SPIKERL_BF16 && c->precision != SPIKERL_FP16) {
     set_error("unknown precision %d", c->precision);
     return SPIKERL_E_ARG;
@@ -111,6 +115,11 @@ int actor_dims(const spikerl_actor_cfg* c, ActorDims* d) {
   d->sigma_floor = c->sigma_floor;
   d->bf16 = c->precision == SPIKERL_BF16 || c->precision == SPIKERL_FP16;
   d->f16 = c->precision == SPIKERL_FP16;
+  d->rho = c->reset_grad;
+  if (d->rho && d->f16) {
+    set_error("reset_grad = 1 is implemented for FP32 and BF16 precision (not FP16)");
+    return SPIKERL_E_UNSUPPORTED;
+  }
   return resolve_engine(c, d);
 }
 
@@ -132,7 +141,9 @@ TapeLayout tape_layout(const ActorDims& d, int B) {
   L.counts = take((size_t)B * d.N3);
   L.act = take(sizeof(float) * (size_t)B * d.A);
   L.tpad = round_up(d.T, 16);
-  for (int l = 0; l < 4; ++l) { L.bitsT[l] = 0; L.maskT[l] = 0; }
+  for (int l = 0; l < 4; ++l) { L.bitsT[l] = 0; L.maskT[l] = 0; L.V[l] = 0; }
+  if (d.rho)
+    for (int l = 1; l <= 3; ++l) L.V[l] = take(sizeof(float) * (size_t)d.T * B * d.P[l]);
   if (d.engine == SPIKERL_ENGINE_TCGEN05) {
     const size_t quads = (size_t)round_up(B, 32) / 4;
     for (int l = 1; l <= 2; ++l) {
@@ -224,12 +235,13 @@ static int actor_forward_impl(const ActorDims& d, int B, const float* params,
     const float* Wf = params + d.off[SPIKERL_ACTOR_W1 + l - 1];
     const __nv_bfloat16* Wb = d.bf16 ? pb16 + d.boff[l - 1] : nullptr;
     uint8_t* cnt = (l == 3) ? counts : nullptr;
+    float* vout = L.V[l] ? (float*)(tape + L.V[l]) : nullptr;
     if (d.engine == SPIKERL_ENGINE_TCGEN05)
       SPK_TRY(launch_lif_fwd_tc(d, l, B, bits[l - 1], Wb, bits[l], mask[l], cnt,
                                 L.bitsT[l] ? (uint8_t*)(tape + L.bitsT[l]) : nullptr,
-                                L.maskT[l] ? (uint8_t*)(tape + L.maskT[l]) : nullptr, L.tpad, st));
+                                L.maskT[l] ? (uint8_t*)(tape + L.maskT[l]) : nullptr, L.tpad, vout, st));
     else
-      SPK_TRY(launch_lif_fwd_simt(d, l, B, bits[l - 1], Wf, Wb, bits[l], mask[l], cnt, st));
+      SPK_TRY(launch_lif_fwd_simt(d, l, B, bits[l - 1], Wf, Wb, bits[l], mask[l], cnt, vout, st));
   }
   SPK_TRY(launch_dec_fwd(d, B, counts, params + d.off[SPIKERL_ACTOR_WD], params + d.off[SPIKERL_ACTOR_BD],
                          actions, (float*)(tape + L.act), st));
@@ -267,8 +279,10 @@ static int actor_backward_impl(const ActorDims& d, int B, const float* params,
   void* G[4] = {nullptr, ws + W.G[1], ws + W.G[2], ws + W.G[3]};
   void* Gsum = ws + W.Gsum;
   float* g_pre = (float*)(ws + W.g_pre);
+  const float* V[4] = {nullptr, nullptr, nullptr, nullptr};
+  for (int l = 1; l <= 3; ++l) V[l] = L.V[l] ? (const float*)(tape + L.V[l]) : nullptr;
   SPK_TRY(launch_dec_bwd_outscan(d, B, grad_a, act, counts, params + d.off[SPIKERL_ACTOR_WD], bits[3], mask[3],
-                                 G[3], g_pre, st));
+                                 V[3], G[3], g_pre, st));
   // Small problems (kernels far from filling the GPU): dW_l and the decoder parameter grads run
   // on side streams next to the dX chain, each as soon as its G_l exists; the critical path is
   // then outscan -> dX3 -> dX2 -> max(encoder grad, dW1). Large problems stay on one stream
@@ -317,10 +331,10 @@ static int actor_backward_impl(const ActorDims& d, int B, const float* params,
     if (l >= 2) {
       if (tc)
         SPK_TRY(launch_lif_dx_tc(d, l, B, G[l], Wb, (const uint8_t*)(tape + L.bitsT[l - 1]),
-                                 (const uint8_t*)(tape + L.maskT[l - 1]), L.tpad, G[l - 1],
+                                 (const uint8_t*)(tape + L.maskT[l - 1]), L.tpad, V[l - 1], G[l - 1],
                                  l == 2 ? Gsum : nullptr, st));
       else
-        SPK_TRY(launch_lif_dx_simt(d, l, B, G[l], Wf, Wb, bits[l - 1], mask[l - 1], G[l - 1],
+        SPK_TRY(launch_lif_dx_simt(d, l, B, G[l], Wf, Wb, bits[l - 1], mask[l - 1], V[l - 1], G[l - 1],
                                    l == 2 ? Gsum : nullptr, st));
     }
   }
@@ -506,6 +520,7 @@ int spikerl_actor_tape_layout(const spikerl_actor_cfg* cfg, int batch, spikerl_t
     out->bitsT[l] = L.bitsT[l]; out->maskT[l] = L.maskT[l];
   }
   out->tpad = L.tpad;
+  for (int l = 0; l < 4; ++l) out->V[l] = L.V[l];
   out->counts = L.counts; out->act = L.act; out->total = L.total;
   return SPIKERL_OK;
 }

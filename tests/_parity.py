@@ -18,10 +18,10 @@ def rel_l2(x, ref):
     return np.linalg.norm(x - ref) / den if den > 0 else np.linalg.norm(x)
 
 
-def run_gpu_actor(shape, B, p, s, g_a, engine="auto"):
+def run_gpu_actor(shape, B, p, s, g_a, engine="auto", reset_grad=0):
     import torch
     import paper_2502_17496_b200 as pk
-    actor = pk.SpikingActor(pk.actor_cfg_from(shape, engine=engine), B)
+    actor = pk.SpikingActor(pk.actor_cfg_from(shape, engine=engine, reset_grad=reset_grad), B)
     actor.load(p)
     obs = torch.from_numpy(np.ascontiguousarray(s)).cuda()
     a = actor.forward(obs).cpu().numpy().astype(np.float64)
@@ -68,8 +68,9 @@ def check_encoder(gpu, shape, p, s):
     return n_ex
 
 
-def check_actor(gpu, shape, p, s, g_a, grad_tol=None, act_tol=None):
-    """Free-running + teacher-forced comparison; returns a stats dict."""
+def check_actor(gpu, shape, p, s, g_a, grad_tol=None, act_tol=None, rho=0.0):
+    """Free-running + teacher-forced comparison; returns a stats dict. rho = 1: the reset-gate
+    gradient variant (oracle.lif_reverse_scan's rho)."""
     prec = shape.precision
     T = shape.T
     sp = gpu["sp"]
@@ -120,7 +121,7 @@ def check_actor(gpu, shape, p, s, g_a, grad_tol=None, act_tol=None):
     stats["max_da"] = float(np.abs(a - a_tf).max())
     # gradients on the GPU's spike tape, masks from the oracle's teacher-forced V
     if g_a is not None and gpu["grads"] is not None:
-        ref = oracle.actor_backward(p, shape, tape, g_a)
+        ref = oracle.actor_backward(p, shape, tape, g_a, rho=rho)
         gt = grad_tol if grad_tol is not None else (1e-4 if prec == "fp32" else 1e-2)
         errs = {}
         for k in ref:

@@ -68,6 +68,20 @@ def test_cfg_validation(L, field, value, status):
     assert L.lib().spikerl_actor_param_count(C.byref(c)) == 0
 
 
+def test_reset_grad_validation_and_tape(L):
+    """reset_grad (rho) is 0 or 1; rho = 1 adds the fp32 membrane planes [T][B][P_l] to the tape and
+    is not offered for FP16 operands."""
+    assert L.lib().spikerl_actor_cfg_check(C.byref(cfg(reset_grad=2))) == L.E_DOMAIN
+    assert L.lib().spikerl_actor_cfg_check(C.byref(cfg(precision="fp16", reset_grad=1))) == L.E_UNSUPPORTED
+    B = 64
+    l0, l1 = L.TapeLayout(), L.TapeLayout()
+    assert L.lib().spikerl_actor_tape_layout(C.byref(cfg(precision="bf16")), B, C.byref(l0)) == 0
+    assert L.lib().spikerl_actor_tape_layout(C.byref(cfg(precision="bf16", reset_grad=1)), B, C.byref(l1)) == 0
+    assert list(l0.V) == [0, 0, 0, 0] and all(l1.V[i] > 0 for i in (1, 2, 3))
+    extra = sum(4 * 5 * B * l1.padded[i] for i in (1, 2, 3))
+    assert l1.total - l0.total >= extra
+
+
 def test_tcgen05_needs_bf16(L):
     c = cfg(engine="tcgen05")
     assert L.lib().spikerl_actor_cfg_check(C.byref(c)) == L.E_UNSUPPORTED

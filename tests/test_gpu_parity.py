@@ -272,6 +272,29 @@ def test_forward_deterministic_and_accumulate():
     assert torch.allclose(g3, 2 * g1, rtol=1e-6, atol=0)
 
 
+# ------------------------------------------------------------------ reset-gate gradient (rho = 1)
+@pytest.mark.parametrize("name,B,prec,engine,T", [("cfg0", 100, "fp32", "auto", 5), ("cfg1", 256, "bf16", "auto", 5),
+                                                 ("cfg1", 256, "bf16", "simt", 5), ("cfg3L", 1024, "bf16", "auto", 5),
+                                                 ("cfg3L", 4096, "bf16", "auto", 5), ("cfg4", 64, "bf16", "auto", 16),
+                                                 ("odd", 33, "bf16", "auto", 16), ("odd", 19, "fp32", "auto", 7)])
+def test_actor_reset_grad(name, B, prec, engine, T):
+    """SPEC.md:171's variant with the reset gate differentiated (rho = 1, R11): the fp32
+    membrane potentials kept in the tape and the reverse scans (SIMT, tcgen05 DX epilogue, output-layer
+    scan) against the oracle's rho = 1 BPTT, teacher forced, at the rho = 0 tolerances; the variant
+    must matter (the rho = 0 gradient is far from it) and leave the forward unchanged."""
+    if name == "odd":
+        shape = sg.ActorShape(5, 3, pop_enc=7, pop_dec=9, n1=45, n2=161, T=T, precision=prec)
+    else:
+        shape = sg.with_(sg.preset(name)[0], precision=prec, T=T)
+    p, s, g = _inputs(shape, B, seed=40 + B)
+    gpu = run_gpu_actor(shape, B, p, s, g, engine=engine, reset_grad=1)
+    st = check_actor(gpu, shape, p, s, g, rho=1.0)
+    ref0 = run_gpu_actor(shape, B, p, s, g, engine=engine, reset_grad=0)
+    assert np.array_equal(ref0["a"], gpu["a"]) and all(np.array_equal(ref0["sp"][k], gpu["sp"][k]) for k in gpu["sp"])
+    assert max(rel_l2(gpu["grads"][k], ref0["grads"][k]) for k in ("W1", "W2", "W3")) > 0.05, "rho had no effect"
+    print(name, B, prec, st.get("grad_rel_l2"))
+
+
 # ------------------------------------------------------------------ critic
 @pytest.mark.parametrize("prec,B,S,A", [("fp32", 100, 17, 6), ("bf16", 256, 17, 6), ("bf16", 4096, 17, 6),
                                         ("bf16", 100, 376, 17), ("bf16", 512, 111, 8), ("bf16", 37, 17, 6),
