@@ -9,7 +9,8 @@ import ctypes as C
 import os
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libspikerl.so")
+# SPIKERL_LIB_PATH: diagnostics only (A/B timing of two builds of this library)
+LIB_PATH = os.environ.get("SPIKERL_LIB_PATH") or os.path.join(_HERE, "libspikerl.so")
 
 OK, E_ARG, E_DOMAIN, E_STATE, E_NOTREADY, E_CUDA, E_NCCL, E_UNSUPPORTED = range(8)
 STATUS_NAMES = ["OK", "E_ARG", "E_DOMAIN", "E_STATE", "E_NOTREADY", "E_CUDA", "E_NCCL", "E_UNSUPPORTED"]

@@ -40,21 +40,31 @@ inline size_t enc_smem_bytes(int R, int T) {
 // (the 1.5 * 2^52 shifter), r from a two-part ln2 (Cody-Waite; ln2_hi has 21 trailing zero bits so
 // n ln2_hi is exact), exp(r) by the degree-13 Taylor polynomial in Horner form (|r| <= ln2/2: the
 // remainder is below 5e-18), 2^-n added to the exponent (the result stays a normal double). The
-// coefficients come from the constant bank (no per-use register materialisation); the library exp
-// spent ~35 instructions per element on range checks this range never needs.
-__constant__ double kExpC[12] = {
+// library exp spent ~35 instructions per element on range checks this range never needs. The
+// coefficients are read once per thread into registers (ncu r02: taken from the constant bank they
+// cost 6 LDCU.128 + 4 UMOV per element, 10 % of the kernel's instructions).
+__device__ const double kExpC[12] = {
     1.6059043836821613e-10, 2.08767569878681e-09, 2.505210838544172e-08, 2.755731922398589e-07,
     2.7557319223985893e-06, 2.48015873015873e-05,  0.0001984126984126984, 0.001388888888888889,
     0.008333333333333333,   0.041666666666666664,  0.16666666666666666,   0.5};
-__device__ __forceinline__ double exp_neg(double z) {
+struct ExpCoefs {
+  double c[12], ln2_hi, ln2_lo;
+  __device__ __forceinline__ void load() {
+#pragma unroll
+    for (int j = 0; j < 12; ++j) c[j] = __ldg(kExpC + j);
+    ln2_hi = -0x1.62e42fee00000p-1;
+    ln2_lo = -0x1.a39ef35793c76p-33;
+  }
+};
+__device__ __forceinline__ double exp_neg(double z, const ExpCoefs& k) {
   z = fmin(z, 110.0);                                               // exp(-110) still rounds to fp32 0
   const double t = __fma_rn(-z, 1.4426950408889634, 6755399441055744.0);
   const double nd = __dsub_rn(t, 6755399441055744.0);               // round(-z / ln2), exactly
-  double r = __fma_rn(nd, -0x1.62e42fee00000p-1, -z);              // -z - n ln2_hi (exact)
-  r = __fma_rn(nd, -0x1.a39ef35793c76p-33, r);                      //   - n ln2_lo
-  double p = kExpC[0];
+  double r = __fma_rn(nd, k.ln2_hi, -z);                            // -z - n ln2_hi (exact)
+  r = __fma_rn(nd, k.ln2_lo, r);                                    //   - n ln2_lo
+  double p = k.c[0];
 #pragma unroll
-  for (int j = 1; j < 12; ++j) p = __fma_rn(p, r, kExpC[j]);
+  for (int j = 1; j < 12; ++j) p = __fma_rn(p, r, k.c[j]);
   p = __fma_rn(p, r, 1.0);
   p = __fma_rn(p, r, 1.0);
   return __longlong_as_double(__double_as_longlong(p) + ((long long)__double2loint(t) << 52));
@@ -90,33 +100,38 @@ __global__ void __launch_bounds__(kEncThreads) enc_fwd_kernel(int B, int S, int 
   const double sg = kv ? (double)__ldg(sigma + k) : 1.0;
   const double den = __dmul_rn(2.0, __dmul_rn(sg, sg));
   const double inv = __ddiv_rn(1.0, den);
+  ExpCoefs kx;
+  kx.load();
+  // the observation values of a tile are requested one tile ahead (ncu r02: loaded at the tile
+  // start, their latency was the kernel's top stall); rows past B read row B - 1 and are not stored
+  const float* op = obs + i;
+  float sv[RR];
+#pragma unroll
+  for (int r = 0; r < RR; ++r) sv[r] = __ldg(op + (size_t)min((int)blockIdx.x * RR + r, B - 1) * S);
   for (int b0 = blockIdx.x * RR; b0 < B; b0 += tstep) {
     for (int j = tid; j < nw / 4; j += kEncThreads) reinterpret_cast<uint4*>(w_sh)[j] = make_uint4(0u, 0u, 0u, 0u);
-    // the tile's observation values, requested together (rows past B read row B - 1: never used)
-    float sv[RR];
-    const float* op = obs + i;
+    float svn[RR];
 #pragma unroll
-    for (int r = 0; r < RR; ++r) sv[r] = __ldg(op + (size_t)min(b0 + r, B - 1) * S);
+    for (int r = 0; r < RR; ++r) svn[r] = __ldg(op + (size_t)min(b0 + tstep + r, B - 1) * S);
     __syncthreads();   // zeroed words; the previous tile's words have been written out
-    // ---- 1. stimulation A for every element of the tile, candidates queued per warp
+    // ---- 1. stimulation A for every element of the tile, candidates queued per warp. Padding
+    // neurons / rows compute on clamped inputs and only their stores are predicated off (no
+    // divergent branch around the fp64 chain).
     int cnt = 0;
     float* ap = A_out + (size_t)b0 * K0 + k;
 #pragma unroll
     for (int r = 0; r < RR; ++r, ap += K0) {
       const bool live = kv && b0 + r < B;
-      float A = 0.0f;
-      if (live) {
-        const double dd = __dsub_rn((double)sv[r], m);
-        const double q = __dmul_rn(dd, dd);
-        // q / den as a correctly rounded quotient from the correctly rounded reciprocal:
-        // q0 = RN(q inv) is within one ulp, r = q - den q0 is exact (FMA), RN(q0 + r inv) = RN(q / den)
-        // (Markstein); the bit-exact encoder tests pin it against the oracle's IEEE division
-        const double q0 = __dmul_rn(q, inv);
-        const double rr = __fma_rn(-q0, den, q);
-        A = (float)exp_neg(__fma_rn(rr, inv, q0));   // RNE double -> float
-        *ap = A;
-      }
-      const bool cand = A >= thr;
+      const double dd = __dsub_rn((double)sv[r], m);
+      const double q = __dmul_rn(dd, dd);
+      // q / den as a correctly rounded quotient from the correctly rounded reciprocal:
+      // q0 = RN(q inv) is within one ulp, r = q - den q0 is exact (FMA), RN(q0 + r inv) = RN(q / den)
+      // (Markstein); the bit-exact encoder tests pin it against the oracle's IEEE division
+      const double q0 = __dmul_rn(q, inv);
+      const double rr = __fma_rn(-q0, den, q);
+      const float A = (float)exp_neg(__fma_rn(rr, inv, q0), kx);   // RNE double -> float
+      if (live) *ap = A;
+      const bool cand = live && A >= thr;
       const uint32_t bal = __ballot_sync(0xffffffffu, cand);
       if (cand) {
         const int j = cnt + __popc(bal & lt);
@@ -127,7 +142,9 @@ __global__ void __launch_bounds__(kEncThreads) enc_fwd_kernel(int B, int S, int 
     }
     __syncwarp();
     // ---- 2. accumulate-and-fire (R5: fp32 acc += A; spike iff acc >= 1; acc -= 1), one candidate
-    // per lane; each spike is OR-ed into its (t, row) word of the warp
+    // per lane, each spike OR-ed into its (t, row) word of the warp (shared atomics). ncu r02: a
+    // branch-free variant that assembled whole words per lane from T-bit trains was 45 % slower
+    // (dependent shared loads)
     for (int j = lane; j < cnt; j += 32) {
       const float A = qA[j];
       const int e = qe[j];
@@ -135,21 +152,11 @@ __global__ void __launch_bounds__(kEncThreads) enc_fwd_kernel(int B, int S, int 
       uint32_t* wp = w_sh + (e >> 5) * kEncWarps + warp;   // + step * RR * 8
       float acc = 0.0f;
 #pragma unroll
-      for (int st = 0; st < (TT > 0 ? TT : 1); ++st) {
-        if (TT == 0) break;
+      for (int st = 0; st < (TT > 0 ? TT : Tn); ++st) {
         acc = __fadd_rn(acc, A);
         if (acc >= 1.0f) {
           acc = __fsub_rn(acc, 1.0f);
           atomicOr(wp + st * RR * kEncWarps, bit);
-        }
-      }
-      if constexpr (TT == 0) {
-        for (int st = 0; st < Tn; ++st) {
-          acc = __fadd_rn(acc, A);
-          if (acc >= 1.0f) {
-            acc = __fsub_rn(acc, 1.0f);
-            atomicOr(wp + st * RR * kEncWarps, bit);
-          }
         }
       }
     }
@@ -167,6 +174,8 @@ __global__ void __launch_bounds__(kEncThreads) enc_fwd_kernel(int B, int S, int 
           gp[(size_t)st * gstep] = reinterpret_cast<const uint4*>(w_sh)[(st * RR + r) * 2 + q];
       }
     }
+#pragma unroll
+    for (int r = 0; r < RR; ++r) sv[r] = svn[r];
   }
 }
 

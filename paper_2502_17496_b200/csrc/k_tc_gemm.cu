@@ -54,12 +54,14 @@ constexpr int NUM_THREADS = (EPI_WARP0 + NUM_EPI_WARPS) * 32;  // 448
 __host__ __device__ constexpr int epi_hb(int bt) { return bt / NUM_EPI_GROUPS > 4 ? bt / NUM_EPI_GROUPS : 4; }
 constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + 1024 + 256;
 constexpr int TMEM_COLS = 512;
-// DX: the epilogue stages G_{l-1} in shared memory, DX_CH steps at a time ([t][b][128 neurons] bf16,
-// double-buffered), and one thread stores each chunk with a TMA tensor store (rows past B and steps
-// past T are clipped by the tensor map). ncu r01: per-element 2-byte global stores with their 64-bit
-// address arithmetic were over half of the DX epilogue's instructions.
+// DX: each epilogue warp stages its part of G_{l-1} in shared memory, DX_CH steps at a time
+// ([t][HB rows][32 neurons] bf16, double-buffered per warp), and its lane 0 stores each chunk with a
+// TMA tensor store (rows past B and steps past T are clipped by the tensor map). ncu r01: per-element
+// 2-byte global stores with their 64-bit address arithmetic were over half of the DX epilogue's
+// instructions.
 constexpr int DX_CH = 4;
-constexpr int DX_STG = 128 * 16 * DX_CH * 2;   // bytes per staging buffer (Bt <= 16)
+constexpr int DX_WSTG = 32 * 8 * DX_CH * 2;   // bytes per warp staging buffer (32 neurons x HB <= 8 rows)
+constexpr int DX_STG = NUM_EPI_WARPS * DX_WSTG;   // both buffers of all epilogue warps: 2 x DX_STG
 constexpr int DW_BN = 256;   // N of one DW MMA
 // A DW unit of a CTA pair covers 2 x 256 output columns (two accumulators, sharing every A tile):
 // each G_l tile fetched from L2/HBM feeds twice the MMA work, which halves the G_l re-reads over
@@ -766,14 +768,14 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       } else if constexpr (MODE == DX) {
         // reverse LIF scan of layer l-1 for HB batch rows of one neuron. Padding neurons have
         // g = 0 (zero weight columns) and no spike / window bits, so G = 0 there without masking.
-        // G_{l-1} leaves through shared memory: DX_CH steps x BT rows x 128 neurons per TMA store.
+        // G_{l-1} leaves through shared memory: DX_CH steps x HB rows x 32 neurons per warp TMA store.
         // The chunk's spike / window bits are gathered once into one 32-bit word each (quad qi's 16
         // bits = 4 steps x 4 rows at bits 16 qi), so every (step, row) test is one LOP3 against a
         // compile-time mask (ncu r02: 17 instructions per element before, 547 per 4-step chunk)
         constexpr int HB = epi_hb(BT);
         constexpr int NQ = HB / 4;
         static_assert(DX_CH == 4 && NQ <= 2, "one 16-bit field of 4 steps x 4 rows per quad");
-        const bool act = g < BT / HB;   // idle groups (BT = 8 with 4 groups) still join the barriers
+        const bool act = g < BT / HB;   // idle groups (BT = 4: HB = 4 rows for group 0 only) skip the scan
         const int jb = act ? g * HB : 0;
         const int b0 = t.n * BT + jb;
         const float zh = p.zh, dvc = p.kc.dv, dcc = p.kc.dc;
@@ -789,13 +791,17 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         unsigned long long qo[NQ], qh[NQ];
 #pragma unroll
         for (int qi = 0; qi < NQ; ++qi) { qo[qi] = dq_o[qi]; qh[qi] = dq_h[qi]; }
-        const bool leader = warp == EPI_WARP0 && lane == 0;
-        const uint32_t soff = (uint32_t)((jb * 128 + 32 * q + lane) * 2);
-        {
+        // each warp stages its own 32 neurons x HB rows x DX_CH steps and stores them with its own
+        // TMA store (double-buffered per warp): no barrier between the eight epilogue warps (ncu r02:
+        // the two named barriers per chunk were 38 % of DX L3's stall samples)
+        uint8_t* const wbuf = stg + (warp - EPI_WARP0) * 2 * DX_WSTG;
+        const uint32_t wstg = smem_u32(wbuf);
+        const uint32_t soff = (uint32_t)lane * 2u;
+        if (act) {
           for (int c = (p.T - 1) / DX_CH; c >= 0; --c, ++dx_chunk) {
             const uint32_t buf = dx_chunk & 1u;
-            if (leader) bulk_wait_read1();   // the store issued from this buffer two chunks ago has read it
-            epi_bar_sync();
+            if (lane == 0) bulk_wait_read1();   // this warp's store from this buffer two chunks ago has read it
+            __syncwarp();
             const int tb = c * DX_CH;
             uint32_t rr[DX_CH][HB];
 #pragma unroll
@@ -824,10 +830,10 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
               xh |= ((uint32_t)(qh[qi] >> sh) & 0xFFFFu) << (16 * qi);
             }
             tmem_ld_wait();
-            const uint32_t sb = smem_u32(stg + buf * DX_STG) + soff;
+            const uint32_t sb = wstg + buf * DX_WSTG + soff;
 #pragma unroll
             for (int ci = DX_CH - 1; ci >= 0; --ci) {
-              if (tb + ci >= p.T || !act) continue;
+              if (tb + ci >= p.T) continue;
 #pragma unroll
               for (int j = 0; j < HB; ++j) {
                 const uint32_t bm = 1u << (16 * (j >> 2) + 4 * ci + (j & 3));
@@ -841,17 +847,17 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
                 dvn[j] = dvt;
                 dcn[j] = dct;
                 gs[j] = __fadd_rn(gs[j], dct);
-                st_shared_u16(sb + (uint32_t)((ci * BT + j) * 256), op16_bits(dct, F16));
+                st_shared_u16(sb + (uint32_t)((ci * HB + j) * 64), op16_bits(dct, F16));
               }
             }
             fence_proxy_async();   // generic-proxy smem writes -> the TMA store
-            epi_bar_sync();
-            if (leader) {
-              tma_store_3d(&tmC, stg + buf * DX_STG, t.m * BM, t.n * BT, tb);
+            __syncwarp();
+            if (lane == 0) {
+              tma_store_3d(&tmC, wbuf + buf * DX_WSTG, t.m * BM + 32 * q, b0, tb);
               bulk_commit();
             }
           }
-          if (p.g_sum && act) {
+          if (p.g_sum) {
 #pragma unroll
             for (int j = 0; j < HB; ++j) {
               const int b = b0 + j;
@@ -1015,7 +1021,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       }
       if (titer == 0 && warp == EPI_WARP0 && lane == 0) trace_stamp(p, 7);
     }
-    if (MODE == DX && warp == EPI_WARP0 && lane == 0) bulk_wait_all();   // staged stores done before exit
+    if (MODE == DX && lane == 0) bulk_wait_all();   // this warp's staged stores done before exit
   }
   tc_fence_before();
   if (threadIdx.x == 0) trace_stamp(p, 8);
@@ -1314,10 +1320,10 @@ int launch_lif_dx_tc(const ActorDims& d, int l, int B, const void* Gl, const __n
     SPK_TRY(make_map(&mb, Gl, 3, dims, strides, box, CU_TENSOR_MAP_SWIZZLE_128B, d.f16));
   }
   CUtensorMap mc;
-  {  // C = G_{l-1} [T][B][P_{l-1}]: the epilogue's staged chunks of DX_CH steps x Bt rows x 128 neurons
+  {  // C = G_{l-1} [T][B][P_{l-1}]: one epilogue warp's staged chunk of DX_CH steps x HB rows x 32 neurons
     const uint64_t dims[3] = {(uint64_t)d.P[l - 1], (uint64_t)B, (uint64_t)d.T};
     const uint64_t strides[2] = {(uint64_t)d.P[l - 1] * 2, (uint64_t)d.P[l - 1] * 2 * B};
-    const uint32_t box[3] = {128, (uint32_t)p.Bt, (uint32_t)DX_CH};
+    const uint32_t box[3] = {32, (uint32_t)epi_hb(p.Bt), (uint32_t)DX_CH};
     SPK_TRY(make_map(&mc, Gprev, 3, dims, strides, box, CU_TENSOR_MAP_SWIZZLE_NONE, d.f16));
   }
   return launch_bt<DX>(p.Bt, ma, mb, p, st, &mc);

@@ -39,6 +39,14 @@ for k in enc_fwd dec_bwd_outscan; do
       python tools/kernel_times.py cfg4 65536 1 > $O/ncu_$k.log 2>&1
   bash tools/ncu_export.sh $O/prof_$k.ncu-rep
 done
+# the tcgen05 critic at configs[3] B = 4096 (CF1 / CF2 / CB1 modes)
+for spec in cf1:6 cf2:7 cb1:8; do
+  IFS=: read name mode <<< "$spec"
+  ncu --set full --clock-control none --import-source on --kernel-name-base demangled \
+      -k regex:"tc_kernel<\\(int\\)$mode," -s 4 -c 1 -o $O/prof_$name \
+      python tools/td3_launches.py cfg3L 2 > $O/ncu_$name.log 2>&1
+  bash tools/ncu_export.sh $O/prof_$name.ncu-rep
+done
 python tools/small_kernels.py > $O/small.log 2>&1
 ncu --set full --clock-control none --import-source on -k regex:adam_kernel -s 95 -c 1 -o $O/prof_adam_kernel \
     python tools/small_kernels.py > $O/ncu_adam.log 2>&1
