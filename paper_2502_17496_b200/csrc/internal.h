@@ -14,8 +14,22 @@ int launch_enc_fwd(const ActorDims& d, int B, const float* obs, const float* mu,
 int launch_lif_fwd_simt(const ActorDims& d, int l, int B, const uint32_t* bits_in,
                         const float* Wf32, const __nv_bfloat16* Wb16, uint32_t* bits_out,
                         uint32_t* mask_out, uint8_t* counts, float* v_out, cudaStream_t st);
+// TD3 target-policy smoothing fused into the target actor's decoder launch (at != NULL):
+// at = clip(a + clip(eps, -c, c), -1, 1) with eps from the update's snapshotted Philox counter (or
+// the injected noise); advance: this launch moves *counter past the snapshot
+struct TargetSmooth {
+  const float* noise;
+  float sigma, clip;
+  unsigned long long seed;
+  int rank;
+  unsigned long long* counter;
+  const unsigned long long* ctr_snap;
+  float* at;
+  int advance;
+};
 int launch_dec_fwd(const ActorDims& d, int B, const uint8_t* counts, const float* Wd,
-                   const float* bd, float* act_out, float* act_tape, cudaStream_t st);
+                   const float* bd, float* act_out, float* act_tape, cudaStream_t st,
+                   const TargetSmooth* smooth = nullptr);
 // decoder backward + output-layer reverse scan -> G3 [T][B][P3] (fp32 or bf16 per precision)
 int launch_dec_bwd_outscan(const ActorDims& d, int B, const float* grad_a, const float* act,
                            const uint8_t* counts, const float* Wd, const uint32_t* bits3,
@@ -173,10 +187,18 @@ __device__ __forceinline__ void store_views(const Bf16Views& v, size_t e, float 
 }
 
 
+// Polyak soft update of a target network fused into the Adam launch of its source (TD3's actor step):
+// t <- tau p_new + (1 - tau) t right after p_new is formed, the same arithmetic as polyak_kernel
+struct PolyakFuse {
+  float* t;
+  float tau;
+  const Bf16Views* views;
+};
 int launch_adam(float* p, const float* g, float* m, float* v, size_t n, long long* counter,
                 float lr, float b1, float b2, float eps, size_t clo, size_t chi, float cmin,
                 unsigned int* done_ticket, const Bf16Views* views, cudaStream_t st, float* amp = nullptr,
-                float amp_growth = 2.f, float amp_backoff = 0.5f, int amp_interval = 2000);
+                float amp_growth = 2.f, float amp_backoff = 0.5f, int amp_interval = 2000,
+                const PolyakFuse* polyak = nullptr);
 // fused gradient mean + Adam over symmetric memory (k_fused_dp.cu; spikerl_fused_adam_create)
 bool fused_adam_matches(const spikerl_fused_adam* fa, const float* g, const float* p, size_t n);
 int fused_adam_launch(spikerl_fused_adam* fa, float* m, float* v, long long* counter, float lr, float b1, float b2,
@@ -187,19 +209,42 @@ int launch_amp_check(const float* g, size_t n, float* amp, cudaStream_t st);
 int launch_polyak(float* t, const float* s, size_t n, float tau, const Bf16Views* views, cudaStream_t st);
 
 // ---- critic (k_critic.cu)
+// The TD target of a critic update, read where the loss forms dQ: either given (y),
+// or formed there from the target critics' Q'(s', a~) [2][B] (qt), r, done and gamma as
+// y = r + gamma (1 - d) min(Q1', Q2') with the operations of the former separate td_target launch,
+// so the update is bitwise unchanged and one launch shorter.
+struct TdY {
+  const float* y;
+  const float* r;
+  const float* d;
+  const float* qt;
+  float gamma;
+  int B;
+  float* out;   // optional: the formed y is stored here (by the reads for critic 0)
+  __device__ __forceinline__ float at(int b) const {
+    if (y) return y[b];
+    return __fadd_rn(r[b], __fmul_rn(__fmul_rn(gamma, __fsub_rn(1.0f, d[b])), fminf(qt[b], qt[B + b])));
+  }
+  __device__ __forceinline__ float get(int b, int z) const {
+    const float v = at(b);
+    if (out && z == 0) out[b] = v;
+    return v;
+  }
+};
 size_t critic_ws_bytes(const CriticDims& c, int B);
 size_t critic_bf16_elems(const CriticDims& c);   // twin pair incl. the mma path's padded/transposed copies
 int launch_critic_refresh(const CriticDims& c, const float* params2, __nv_bfloat16* out, cudaStream_t st);
 bool critic_mma_ok(const CriticDims& c);
 size_t critic_mma_ws_bytes(const CriticDims& c, int B);
 int critic_mma_fwd_bwd(const CriticDims& c, int B, const float* params2, const __nv_bfloat16* pb, const float* obs,
-                       int S, const float* act, int A, const float* y, float* q, float* loss, float* grad2,
+                       int S, const float* act, int A, const TdY* y, float* q, float* loss, float* grad2,
                        float* grad_act, float act_scale, int nz, void* ws, cudaStream_t st,
                        cudaEvent_t wait_before_loss = nullptr, const float* dq_scale = nullptr);
-// wait_before_loss (optional): the stream waits on this event after the forward and before the
-// loss (the TD target y is produced concurrently on another stream).
+// y: the TD target (critic update) or NULL (forward / actor objective). wait_before_loss (optional):
+// the stream waits on this event after the forward and before the loss (the target critics' Q' are
+// produced concurrently on another stream).
 int critic_fwd_bwd(const CriticDims& c, int B, const float* params2, const __nv_bfloat16* pb16,
-                   const float* obs, int S, const float* act, int A, const float* y, float* q,
+                   const float* obs, int S, const float* act, int A, const TdY* y, float* q,
                    float* loss, float* grad2, float* grad_act, float act_scale, int n_critics,
                    void* ws, cudaStream_t st, cudaEvent_t wait_before_loss = nullptr,
                    const float* dq_scale = nullptr);   // dq_scale: device loss scale applied to dQ
@@ -216,14 +261,6 @@ struct GatherSlots {
 int launch_replay_gather(int B, int S, int A, const float* rs, const float* ra, const float* rr,
                          const float* rs2, const float* rd, long long N, unsigned long long seed, int rank,
                          const unsigned long long* counter, const GatherSlots& gs, cudaStream_t st);
-// ctr_snap: the step's Philox counter value, written by the gather launch (block 0) and read by
-// the target-noise launch, which advances *counter
-int launch_target_action(int B, int A, const float* a2, const float* noise, float sigma,
-                         float clip, unsigned long long seed, int rank,
-                         unsigned long long* counter, const unsigned long long* ctr_snap, float* at,
-                         cudaStream_t st, int advance = 1);   // advance: *counter = snapshot + 1
-int launch_td_target(int B, const float* r, const float* d, const float* q2, float gamma,
-                     float* y, cudaStream_t st);
 int launch_scale(float* x, size_t n, float s, cudaStream_t st);
 
 }  // namespace spk

@@ -8,6 +8,7 @@
 // [T][B][P_l] in fp32 (FP32 precision) or bf16 (BF16 precision, R20 rounding point).
 // All reductions run in a fixed order: results are run-to-run bitwise deterministic.
 #include "internal.h"
+#include "rng.cuh"
 
 namespace spk {
 
@@ -89,7 +90,7 @@ int launch_lif_fwd_simt(const ActorDims& d, int l, int B, const uint32_t* bits_i
 // ------------------------------------------------------------------------------ decoder forward
 __global__ void dec_fwd_kernel(int B, int A, int D, int T, const uint8_t* __restrict__ counts,
                                const float* __restrict__ Wd, const float* __restrict__ bd,
-                               float* __restrict__ act_out, float* __restrict__ act_tape) {
+                               float* __restrict__ act_out, float* __restrict__ act_tape, const TargetSmooth ts) {
   pdl_wait();
   pdl_trigger();
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
@@ -107,13 +108,20 @@ __global__ void dec_fwd_kernel(int B, int A, int D, int T, const uint8_t* __rest
   const float a = tanhf(pre);
   act_out[i] = a;
   if (act_tape) act_tape[i] = a;
+  if (ts.at) {   // target actor of a TD3 update: the smoothed target action (one launch less)
+    const unsigned long long ctr = *ts.ctr_snap;
+    if (ts.advance && i == 0) *ts.counter = ctr + 1;
+    ts.at[i] = smooth_action(a, i, ts.noise, ts.sigma, ts.clip, ts.seed, ts.rank, ctr);
+  }
 }
 
 int launch_dec_fwd(const ActorDims& d, int B, const uint8_t* counts, const float* Wd,
-                   const float* bd, float* act_out, float* act_tape, cudaStream_t st) {
-  ProfScope ps_("dec_fwd", PB_LATENCY, 0.0, (double)B * (d.N3 + 8.0 * d.A), st);
+                   const float* bd, float* act_out, float* act_tape, cudaStream_t st, const TargetSmooth* smooth) {
+  ProfScope ps_(smooth ? "dec_fwd_smooth" : "dec_fwd", PB_LATENCY, 0.0, (double)B * (d.N3 + 8.0 * d.A), st);
   const int n = B * d.A;
-  pdl(dec_fwd_kernel, cdiv(n, 256), 256, 0, st)(B, d.A, d.D, d.T, counts, Wd, bd, act_out, act_tape);
+  const TargetSmooth none{};
+  pdl(dec_fwd_kernel, cdiv(n, 256), 256, 0, st)(B, d.A, d.D, d.T, counts, Wd, bd, act_out, act_tape,
+                                                 smooth ? *smooth : none);
   SPK_LAUNCHED();
   return SPIKERL_OK;
 }

@@ -161,7 +161,7 @@ __global__ void critic_out_kernel(int B, int H2, const float* __restrict__ H, lo
 
 // loss = sum_z mean_b (Q_z - y)^2 ; dQ[z][b] = 2 (Q_z - y)/B. Single block, fixed order.
 __global__ void __launch_bounds__(256) critic_loss_kernel(int B, int nz, const float* __restrict__ q,
-                                                          const float* __restrict__ y,
+                                                          const TdY y,
                                                           float* __restrict__ dq,
                                                           float* __restrict__ loss) {
   pdl_wait();
@@ -171,7 +171,7 @@ __global__ void __launch_bounds__(256) critic_loss_kernel(int B, int nz, const f
   for (int z = 0; z < nz; ++z) {
     float s = 0.f;
     for (int b = threadIdx.x; b < B; b += 256) {
-      const float e = __fsub_rn(q[(size_t)z * B + b], y[b]);
+      const float e = __fsub_rn(q[(size_t)z * B + b], y.get(b, z));
       s = __fmaf_rn(e, e, s);
       dq[(size_t)z * B + b] = __fdiv_rn(__fmul_rn(2.0f, e), (float)B);
     }
@@ -291,7 +291,7 @@ size_t critic_ws_bytes(const CriticDims& c, int B) {
 
 // SIMT GEMM path: fp32 precision only (bf16 critics run on the tensor-core kernels).
 int critic_fwd_bwd(const CriticDims& c, int B, const float* params2, const __nv_bfloat16* pb16,
-                   const float* obs, int S, const float* act, int A, const float* y, float* q,
+                   const float* obs, int S, const float* act, int A, const TdY* y, float* q,
                    float* loss, float* grad2, float* grad_act, float act_scale, int nz, void* ws,
                    cudaStream_t st, cudaEvent_t wait_before_loss, const float* dq_scale) {
   if (critic_mma_ok(c))
@@ -349,7 +349,7 @@ int critic_fwd_bwd(const CriticDims& c, int B, const float* params2, const __nv_
   const bool want_params = (y != nullptr && grad2 != nullptr);
   if (wait_before_loss) SPK_CHECK_CUDA(cudaStreamWaitEvent(st, wait_before_loss, 0));
   if (y) {
-    pdl(critic_loss_kernel, 1, 256, 0, st)(B, nz, q, y, w.dq, loss);
+    pdl(critic_loss_kernel, 1, 256, 0, st)(B, nz, q, *y, w.dq, loss);
     SPK_LAUNCHED();
   }
   if (!want_params && !grad_act) return SPIKERL_OK;

@@ -356,7 +356,7 @@ __device__ __forceinline__ void cstamp(int i) {
 // the last CTA to finish (atomic ticket, zeroed by the forward launch) adds the partials in
 // a fixed order, so the scalar is deterministic.
 __global__ void __launch_bounds__(256) critic_bwd_data_mma_kernel(
-    int B, int Bp, int S, int A, int inp, const float* __restrict__ q, const float* __restrict__ y, int mode,
+    int B, int Bp, int S, int A, int inp, const float* __restrict__ q, const TdY y, int mode,
     float act_scale, float* __restrict__ dq, float* __restrict__ part, unsigned int* __restrict__ ticket,
     float* __restrict__ loss, const __nv_bfloat16* __restrict__ pb,
     long long P, long long tb, long long oW3, long long oW1T, long long oW2T, const float* __restrict__ Z1,
@@ -391,7 +391,7 @@ __global__ void __launch_bounds__(256) critic_bwd_data_mma_kernel(
     if (lane < RB && b < B) {
       const float qv = q[(size_t)z * B + b];
       if (mode == 0) {
-        const float e = __fsub_rn(qv, y[b]);
+        const float e = __fsub_rn(qv, y.get(b, z));
         d = __fdiv_rn(__fmul_rn(2.0f, e), (float)B);
         c = __fmul_rn(e, e);
       } else {
@@ -739,7 +739,7 @@ __global__ void critic_refresh_kernel(const float* __restrict__ params, long lon
 
 // loss = sum_z mean_b (Q_z - y)^2 ; dQ[z][b] = 2 (Q_z - y)/B. Single block, fixed order.
 __global__ void __launch_bounds__(256) critic_loss_mma_kernel(int B, int nz, const float* __restrict__ q,
-                                                              const float* __restrict__ y, float* __restrict__ dq,
+                                                              const TdY y, float* __restrict__ dq,
                                                               float* __restrict__ loss) {
   pdl_wait();
   pdl_trigger();
@@ -748,7 +748,7 @@ __global__ void __launch_bounds__(256) critic_loss_mma_kernel(int B, int nz, con
   for (int z = 0; z < nz; ++z) {
     float s = 0.f;
     for (int b = threadIdx.x; b < B; b += 256) {
-      const float e = __fsub_rn(q[(size_t)z * B + b], y[b]);
+      const float e = __fsub_rn(q[(size_t)z * B + b], y.get(b, z));
       s = __fmaf_rn(e, e, s);
       dq[(size_t)z * B + b] = __fdiv_rn(__fmul_rn(2.0f, e), (float)B);
     }
@@ -797,7 +797,7 @@ __global__ void __launch_bounds__(256) critic_xt_kernel(int B, int Bp, int S, in
 // row (tid & 63), hidden units tid >> 6 + 4 i); its loss partial is summed in row order and the
 // last block (ticket) adds the partials in (z, block) order: deterministic.
 __global__ void __launch_bounds__(256) critic_dz2_kernel(int B, int Bp, const float* __restrict__ q,
-                                                         const float* __restrict__ y, int mode, float act_scale,
+                                                         const TdY y, int mode, float act_scale,
                                                          const float* __restrict__ dq_scale, float* __restrict__ dq,
                                                          float* __restrict__ part, unsigned int* __restrict__ ticket,
                                                          float* __restrict__ loss, const __nv_bfloat16* __restrict__ pb,
@@ -816,7 +816,7 @@ __global__ void __launch_bounds__(256) critic_dz2_kernel(int B, int Bp, const fl
     if (b < B) {
       const float qv = q[(size_t)z * B + b];
       if (mode == 0) {
-        const float e = __fsub_rn(qv, y[b]);
+        const float e = __fsub_rn(qv, y.get(b, z));
         d = __fdiv_rn(__fmul_rn(2.0f, e), (float)B);
         c = __fmul_rn(e, e);
       } else {
@@ -994,7 +994,7 @@ static bool critic_tc_ok(const CriticDims& c, int B) {
 }
 
 static int critic_tc_fwd_bwd(const CriticDims& c, int B, const float* params2, const __nv_bfloat16* pb, const float* obs,
-                             int S, const float* act, int A, const float* y, float* q, float* loss, float* grad2,
+                             int S, const float* act, int A, const TdY* y, float* q, float* loss, float* grad2,
                              float* grad_act, float act_scale, int nz, void* ws, cudaStream_t st,
                              cudaEvent_t wait_before_loss, const float* dq_scale) {
   const MmaLayout L = mma_layout(c);
@@ -1023,7 +1023,7 @@ static int critic_tc_fwd_bwd(const CriticDims& c, int B, const float* params2, c
   if (wait_before_loss) SPK_CHECK_CUDA(cudaStreamWaitEvent(st, wait_before_loss, 0));
   if (!need_bwd) {
     if (y) {
-      pdl(critic_loss_mma_kernel, 1, 256, 0, st)(B, nz, q, y, w.dq, loss);
+      pdl(critic_loss_mma_kernel, 1, 256, 0, st)(B, nz, q, *y, w.dq, loss);
       SPK_LAUNCHED();
     }
     return SPIKERL_OK;
@@ -1033,7 +1033,7 @@ static int critic_tc_fwd_bwd(const CriticDims& c, int B, const float* params2, c
   {
     ProfScope ps_("critic_bwd_data_tc", PB_TENSOR, 2.0 * B * nb * ((double)HW * HW), 0.0, st);
     pdl(critic_dz2_kernel, dim3((unsigned)cdiv(Bp, 64), (unsigned)nb), 256, 0, st)(
-        B, Bp, q, y, mode, act_scale, dq_scale, w.dq, w.part, w.ticket, (want_params || !y) ? loss : nullptr, pb, L.P,
+        B, Bp, q, y ? *y : TdY{}, mode, act_scale, dq_scale, w.dq, w.part, w.ticket, (want_params || !y) ? loss : nullptr, pb, L.P,
         oW3, w.H2T, w.dZ2T);
     SPK_LAUNCHED();
     // dZ1T = RN(dZ2 W2 [h1 > 0])^T
@@ -1071,7 +1071,7 @@ static int critic_tc_fwd_bwd(const CriticDims& c, int B, const float* params2, c
 }
 
 int critic_mma_fwd_bwd(const CriticDims& c, int B, const float* params2, const __nv_bfloat16* pb, const float* obs,
-                       int S, const float* act, int A, const float* y, float* q, float* loss, float* grad2,
+                       int S, const float* act, int A, const TdY* y, float* q, float* loss, float* grad2,
                        float* grad_act, float act_scale, int nz, void* ws, cudaStream_t st,
                        cudaEvent_t wait_before_loss, const float* dq_scale) {
   if (critic_tc_ok(c, B))
@@ -1101,7 +1101,7 @@ int critic_mma_fwd_bwd(const CriticDims& c, int B, const float* params2, const _
   const int mode = want_params ? 0 : 1;
   const bool fused_scalar = need_bwd && (want_params || !y);
   if (y && !fused_scalar) {
-    pdl(critic_loss_mma_kernel, 1, 256, 0, st)(B, nz, q, y, w.dq, loss);
+    pdl(critic_loss_mma_kernel, 1, 256, 0, st)(B, nz, q, *y, w.dq, loss);
     SPK_LAUNCHED();
   }
   if (!need_bwd) return SPIKERL_OK;
@@ -1111,7 +1111,7 @@ int critic_mma_fwd_bwd(const CriticDims& c, int B, const float* params2, const _
     dim3 grid(Bp / RB, nb);
     SPK_SMEM_ATTR(critic_bwd_data_mma_kernel, kW2Smem);
     pdl(critic_bwd_data_mma_kernel, grid, 256, kW2Smem, st)(
-        B, Bp, S, A, L.inp, q, y, mode, act_scale, w.dq, w.part, w.ticket, fused_scalar ? loss : nullptr, pb, L.P, L.tb,
+        B, Bp, S, A, L.inp, q, y ? *y : TdY{}, mode, act_scale, w.dq, w.part, w.ticket, fused_scalar ? loss : nullptr, pb, L.P, L.tb,
         oW3, L.W1T, L.W2T, w.Z1, w.Z2, w.dZ2T, w.dZ1T, grad_act, want_params ? 1 : 0, dq_scale);
     SPK_LAUNCHED();
   }

@@ -107,7 +107,8 @@ __global__ void __launch_bounds__(256) adam_kernel(float* __restrict__ p, const 
                                                    float cmin, unsigned int* ticket,
                                                    const __grid_constant__ Bf16Views views, float* amp,
                                                    float amp_growth, float amp_backoff, int amp_interval,
-                                                   double lnb1, double lnb2) {
+                                                   double lnb1, double lnb2, float* __restrict__ tp, float tau,
+                                                   const __grid_constant__ Bf16Views tviews) {
   pdl_wait();
   pdl_trigger();
   // bias corrections once per block, not once per thread
@@ -129,12 +130,13 @@ __global__ void __launch_bounds__(256) adam_kernel(float* __restrict__ p, const 
   const float inv_scale = s_coef[2];
   const bool skip = s_skip != 0;
   const float omb1 = 1.0f - b1, omb2 = 1.0f - b2;
+  const float omt = 1.0f - tau;
   const size_t n4 = n / 4;
   const size_t stride = (size_t)gridDim.x * blockDim.x;
   // two float4 groups per thread and iteration, every load issued before any arithmetic (more
   // bytes in flight per thread: 128 B)
   for (size_t i0 = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i0 < n4 && !skip; i0 += 2 * stride) {
-    float4 pp[2], gg[2], mm[2], vv[2];
+    float4 pp[2], gg[2], mm[2], vv[2], tt[2];
     const bool two = i0 + stride < n4;
 #pragma unroll
     for (int u = 0; u < 2; ++u) {
@@ -144,6 +146,7 @@ __global__ void __launch_bounds__(256) adam_kernel(float* __restrict__ p, const 
         gg[u] = reinterpret_cast<const float4*>(g)[i];
         mm[u] = reinterpret_cast<float4*>(m)[i];
         vv[u] = reinterpret_cast<float4*>(v)[i];
+        if (tp) tt[u] = reinterpret_cast<float4*>(tp)[i];
       }
     }
 #pragma unroll
@@ -158,10 +161,16 @@ __global__ void __launch_bounds__(256) adam_kernel(float* __restrict__ p, const 
         const size_t e = 4 * i + j;
         if (e >= clo && e < chi) pa[j] = fmaxf(pa[j], cmin);
         store_views(views, e, pa[j]);
+        if (tp) {
+          float* ta = &tt[u].x;
+          ta[j] = __fadd_rn(__fmul_rn(tau, pa[j]), __fmul_rn(omt, ta[j]));
+          store_views(tviews, e, ta[j]);
+        }
       }
       reinterpret_cast<float4*>(p)[i] = pp[u];
       reinterpret_cast<float4*>(m)[i] = mm[u];
       reinterpret_cast<float4*>(v)[i] = vv[u];
+      if (tp) reinterpret_cast<float4*>(tp)[i] = tt[u];
     }
   }
   for (size_t e = 4 * n4 + blockIdx.x * (size_t)blockDim.x + threadIdx.x; e < n && !skip; e += stride) {
@@ -171,6 +180,11 @@ __global__ void __launch_bounds__(256) adam_kernel(float* __restrict__ p, const 
     if (e >= clo && e < chi) pp = fmaxf(pp, cmin);
     p[e] = pp; m[e] = mm; v[e] = vv;
     store_views(views, e, pp);
+    if (tp) {
+      const float x = __fadd_rn(__fmul_rn(tau, pp), __fmul_rn(omt, tp[e]));
+      tp[e] = x;
+      store_views(tviews, e, x);
+    }
   }
   // publish the new step count once every block has read the old one
   __syncthreads();
@@ -215,16 +229,20 @@ int launch_amp_check(const float* g, size_t n, float* amp, cudaStream_t st) {
 int launch_adam(float* p, const float* g, float* m, float* v, size_t n, long long* counter,
                 float lr, float b1, float b2, float eps, size_t clo, size_t chi, float cmin,
                 unsigned int* ticket, const Bf16Views* views, cudaStream_t st, float* amp, float amp_growth,
-                float amp_backoff, int amp_interval) {
-  ProfScope ps_("adam", PB_HBM, 0.0, 28.0 * n, st);
+                float amp_backoff, int amp_interval, const PolyakFuse* polyak) {
+  // a skipped (overflowing) loss-scaled step must still move the target: no fusion with the scaler
+  if (polyak && amp) { set_error("adam: a fused Polyak update needs amp == NULL"); return SPIKERL_E_ARG; }
+  ProfScope ps_(polyak ? "adam_polyak" : "adam", PB_HBM, 0.0, (polyak ? 40.0 : 28.0) * n, st);
   const Bf16Views none{};
-  if (((uintptr_t)p | (uintptr_t)g | (uintptr_t)m | (uintptr_t)v) & 15) {
+  if (((uintptr_t)p | (uintptr_t)g | (uintptr_t)m | (uintptr_t)v | (uintptr_t)(polyak ? polyak->t : nullptr)) & 15) {
     set_error("adam: buffers must be 16-byte aligned");
     return SPIKERL_E_ARG;
   }
   pdl(adam_kernel, stream_grid(adam_kernel, n, 8), 256, 0, st)(p, g, m, v, n, counter, lr, b1, b2, eps, clo, chi,
                                              cmin, ticket, views ? *views : none, amp, amp_growth, amp_backoff,
-                                             amp_interval, log((double)b1), log((double)b2));
+                                             amp_interval, log((double)b1), log((double)b2),
+                                             polyak ? polyak->t : nullptr, polyak ? polyak->tau : 0.f,
+                                             (polyak && polyak->views) ? *polyak->views : none);
   SPK_LAUNCHED();
   return SPIKERL_OK;
 }

@@ -6,41 +6,9 @@
 // Random numbers: counter-based Philox4x32-10 keyed by (seed, rank); the counter lives on the
 // device so a captured CUDA graph draws fresh numbers on every replay.
 #include "internal.h"
+#include "rng.cuh"
 
 namespace spk {
-
-struct Philox {
-  __device__ static uint4 round(uint4 c, uint2 k) {
-    const uint32_t M0 = 0xD2511F53u, M1 = 0xCD9E8D57u;
-    const uint32_t hi0 = __umulhi(M0, c.x), lo0 = M0 * c.x;
-    const uint32_t hi1 = __umulhi(M1, c.z), lo1 = M1 * c.z;
-    return make_uint4(hi1 ^ c.y ^ k.x, lo1, hi0 ^ c.w ^ k.y, lo0);
-  }
-  __device__ static uint4 gen(uint4 c, uint2 k) {
-#pragma unroll
-    for (int i = 0; i < 10; ++i) {
-      c = round(c, k);
-      k.x += 0x9E3779B9u;
-      k.y += 0xBB67AE85u;
-    }
-    return c;
-  }
-};
-
-__device__ __forceinline__ uint2 philox_key(unsigned long long seed, int rank) {
-  return make_uint2((uint32_t)seed, (uint32_t)(seed >> 32) ^ (0x85EBCA6Bu * (uint32_t)(rank + 1)));
-}
-__device__ __forceinline__ float u01(uint32_t x) {  // (0, 1]
-  return ((float)(x >> 8) + 1.0f) * (1.0f / 16777216.0f);
-}
-__device__ __forceinline__ float2 box_muller(uint32_t a, uint32_t b) {
-  const float r = sqrtf(-2.0f * logf(u01(a)));
-  float s, c;
-  sincospif(2.0f * u01(b), &s, &c);
-  return make_float2(r * c, r * s);
-}
-
-enum Purpose : uint32_t { P_INDEX = 1, P_NOISE = 2, P_FILL = 3 };
 
 // one warp per sampled row: lane 0 draws the index, the warp copies the row's columns
 // one warp per sampled row: lane 0 draws the index, the warp copies the row's columns. Up to two
@@ -90,65 +58,6 @@ int launch_replay_gather(int B, int S, int A, const float* rs, const float* ra, 
   ProfScope ps_("replay_gather", PB_LATENCY, 0.0, 8.0 * gs.n * B * (2.0 * S + A + 2), st);
   pdl(replay_gather_kernel, cdiv((long long)gs.n * B * 32, 256), 256, 0, st)(B, S, A, rs, ra, rr, rs2, rd, N, seed,
                                                                             rank, counter, gs);
-  SPK_LAUNCHED();
-  return SPIKERL_OK;
-}
-
-// a~ = clip(a2 + clip(eps, -c, c), -1, 1). The noise uses the step's counter value snapshotted by
-// the gather launch, so any number of blocks may run; block 0 advances the counter (a single
-// 1024-thread block took 60 us at configs[3] B = 4096, on the critic step's critical path).
-__global__ void __launch_bounds__(256) target_action_kernel(int B, int A, const float* __restrict__ a2,
-                                                            const float* __restrict__ noise,
-                                                            float sigma, float clip,
-                                                            unsigned long long seed, int rank,
-                                                            unsigned long long* counter,
-                                                            const unsigned long long* __restrict__ ctr_snap,
-                                                            float* __restrict__ at, int advance) {
-  pdl_wait();
-  pdl_trigger();
-  const unsigned long long ctr = *ctr_snap;
-  const int n = B * A;
-  if (advance && blockIdx.x == 0 && threadIdx.x == 0) *counter = ctr + 1;
-  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
-    float eps;
-    if (noise) {
-      eps = noise[i];
-    } else {
-      const uint4 x = Philox::gen(make_uint4((uint32_t)(i >> 1), P_NOISE, (uint32_t)ctr, (uint32_t)(ctr >> 32)),
-                                  philox_key(seed, rank));
-      const float2 z = box_muller(x.x, x.y);
-      eps = sigma * ((i & 1) ? z.y : z.x);
-    }
-    eps = fminf(fmaxf(eps, -clip), clip);
-    at[i] = fminf(fmaxf(__fadd_rn(a2[i], eps), -1.0f), 1.0f);
-  }
-}
-
-int launch_target_action(int B, int A, const float* a2, const float* noise, float sigma, float clip,
-                         unsigned long long seed, int rank, unsigned long long* counter,
-                         const unsigned long long* ctr_snap, float* at, cudaStream_t st, int advance) {
-  ProfScope ps_("target_action", PB_LATENCY, 0.0, 12.0 * B * A, st);
-  const int blocks = cdiv((long long)B * A, 512);   // two elements (one Box-Muller pair) per thread
-  pdl(target_action_kernel, blocks < 148 ? (blocks > 0 ? blocks : 1) : 148, 256, 0, st)(
-      B, A, a2, noise, sigma, clip, seed, rank, counter, ctr_snap, at, advance);
-  SPK_LAUNCHED();
-  return SPIKERL_OK;
-}
-
-__global__ void td_target_kernel(int B, const float* __restrict__ r, const float* __restrict__ d,
-                                 const float* __restrict__ q2, float gamma, float* __restrict__ y) {
-  pdl_wait();
-  pdl_trigger();
-  const int b = blockIdx.x * blockDim.x + threadIdx.x;
-  if (b >= B) return;
-  const float qmin = fminf(q2[b], q2[B + b]);
-  y[b] = __fadd_rn(r[b], __fmul_rn(__fmul_rn(gamma, __fsub_rn(1.0f, d[b])), qmin));
-}
-
-int launch_td_target(int B, const float* r, const float* d, const float* q2, float gamma, float* y,
-                     cudaStream_t st) {
-  ProfScope ps_("td_target", PB_LATENCY, 0.0, 20.0 * B, st);
-  pdl(td_target_kernel, cdiv(B, 256), 256, 0, st)(B, r, d, q2, gamma, y);
   SPK_LAUNCHED();
   return SPIKERL_OK;
 }

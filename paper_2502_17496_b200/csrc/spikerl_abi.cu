@@ -222,7 +222,7 @@ static ActorWs actor_ws_layout(const ActorDims& d, int B) {
 
 static int actor_forward_impl(const ActorDims& d, int B, const float* params,
                               const __nv_bfloat16* pb16, const float* obs, float* actions,
-                              char* tape, cudaStream_t st) {
+                              char* tape, cudaStream_t st, const TargetSmooth* smooth = nullptr) {
   const TapeLayout L = tape_layout(d, B);
   float* A = (float*)(tape + L.A);
   uint32_t* bits[4];
@@ -244,7 +244,7 @@ static int actor_forward_impl(const ActorDims& d, int B, const float* params,
       SPK_TRY(launch_lif_fwd_simt(d, l, B, bits[l - 1], Wf, Wb, bits[l], mask[l], cnt, vout, st));
   }
   SPK_TRY(launch_dec_fwd(d, B, counts, params + d.off[SPIKERL_ACTOR_WD], params + d.off[SPIKERL_ACTOR_BD],
-                         actions, (float*)(tape + L.act), st));
+                         actions, (float*)(tape + L.act), st, smooth));
   return SPIKERL_OK;
 }
 
@@ -385,29 +385,39 @@ static Td3Ws td3_ws_layout(const ActorDims& ad, const CriticDims& cd, int B) {
 // The optimiser step of each network after its backward: the gradient mean over ranks + Adam, either
 // as the NCCL allreduce (the actor's is already bucketed inside its backward) and the Adam launch, or
 // as the one fused allreduce + Adam kernel over symmetric memory when a plan is given (NEXT #1).
+// polyak (actor steps): the target soft update t <- tau p + (1 - tau) t of that network, fused into its
+// Adam launch (one launch less at the end of the update's critical path); with the fused allreduce
+// + Adam kernel or loss scaling it stays a launch of its own right after, same arithmetic.
 static int critic_optimise(const spikerl_td3_bufs* b, spikerl_comm* comm, const spikerl_td3_cfg* hp, size_t Pc,
-                           const Bf16Views* cv, float* amp_c, cudaStream_t st) {
-  if (comm && b->fused_critic)
-    return fused_adam_launch(b->fused_critic, b->m_critic, b->v_critic, b->adam_steps, hp->lr_critic, hp->beta1,
-                             hp->beta2, hp->eps, 0, 0, 0.f, (unsigned int*)(b->adam_steps + 1), cv, st);
+                           const Bf16Views* cv, float* amp_c, cudaStream_t st, const PolyakFuse* polyak = nullptr) {
+  if (comm && b->fused_critic) {
+    SPK_TRY(fused_adam_launch(b->fused_critic, b->m_critic, b->v_critic, b->adam_steps, hp->lr_critic, hp->beta1,
+                              hp->beta2, hp->eps, 0, 0, 0.f, (unsigned int*)(b->adam_steps + 1), cv, st));
+    return polyak ? launch_polyak(polyak->t, b->critic, 2 * Pc, polyak->tau, polyak->views, st) : SPIKERL_OK;
+  }
   SPK_TRY(spikerl_allreduce_grads(comm, b->grad_critic, 2 * Pc, st));
   if (amp_c) SPK_TRY(launch_amp_check(b->grad_critic, 2 * Pc, amp_c, st));
-  return launch_adam(b->critic, b->grad_critic, b->m_critic, b->v_critic, 2 * Pc, b->adam_steps, hp->lr_critic,
-                     hp->beta1, hp->beta2, hp->eps, 0, 0, 0.f, (unsigned int*)(b->adam_steps + 1), cv, st, amp_c,
-                     hp->amp_growth, hp->amp_backoff, hp->amp_interval);
+  SPK_TRY(launch_adam(b->critic, b->grad_critic, b->m_critic, b->v_critic, 2 * Pc, b->adam_steps, hp->lr_critic,
+                      hp->beta1, hp->beta2, hp->eps, 0, 0, 0.f, (unsigned int*)(b->adam_steps + 1), cv, st, amp_c,
+                      hp->amp_growth, hp->amp_backoff, hp->amp_interval, amp_c ? nullptr : polyak));
+  return (polyak && amp_c) ? launch_polyak(polyak->t, b->critic, 2 * Pc, polyak->tau, polyak->views, st) : SPIKERL_OK;
 }
 
 static int actor_optimise(const spikerl_td3_bufs* b, spikerl_comm* comm, const spikerl_td3_cfg* hp,
-                          const ActorDims& ad, size_t Pa, const Bf16Views* av, float* amp_a, cudaStream_t st) {
-  if (comm && b->fused_actor)
-    return fused_adam_launch(b->fused_actor, b->m_actor, b->v_actor, b->adam_steps + 2, hp->lr_actor, hp->beta1,
-                             hp->beta2, hp->eps, ad.off[SPIKERL_ACTOR_SIGMA], ad.off[SPIKERL_ACTOR_W1],
-                             ad.sigma_floor, (unsigned int*)(b->adam_steps + 3), av, st);
+                          const ActorDims& ad, size_t Pa, const Bf16Views* av, float* amp_a, cudaStream_t st,
+                          const PolyakFuse* polyak = nullptr) {
+  if (comm && b->fused_actor) {
+    SPK_TRY(fused_adam_launch(b->fused_actor, b->m_actor, b->v_actor, b->adam_steps + 2, hp->lr_actor, hp->beta1,
+                              hp->beta2, hp->eps, ad.off[SPIKERL_ACTOR_SIGMA], ad.off[SPIKERL_ACTOR_W1],
+                              ad.sigma_floor, (unsigned int*)(b->adam_steps + 3), av, st));
+    return polyak ? launch_polyak(polyak->t, b->actor, Pa, polyak->tau, polyak->views, st) : SPIKERL_OK;
+  }
   if (amp_a) SPK_TRY(launch_amp_check(b->grad_actor, Pa, amp_a, st));
-  return launch_adam(b->actor, b->grad_actor, b->m_actor, b->v_actor, Pa, b->adam_steps + 2, hp->lr_actor, hp->beta1,
-                     hp->beta2, hp->eps, ad.off[SPIKERL_ACTOR_SIGMA], ad.off[SPIKERL_ACTOR_W1], ad.sigma_floor,
-                     (unsigned int*)(b->adam_steps + 3), av, st, amp_a, hp->amp_growth, hp->amp_backoff,
-                     hp->amp_interval);
+  SPK_TRY(launch_adam(b->actor, b->grad_actor, b->m_actor, b->v_actor, Pa, b->adam_steps + 2, hp->lr_actor, hp->beta1,
+                      hp->beta2, hp->eps, ad.off[SPIKERL_ACTOR_SIGMA], ad.off[SPIKERL_ACTOR_W1], ad.sigma_floor,
+                      (unsigned int*)(b->adam_steps + 3), av, st, amp_a, hp->amp_growth, hp->amp_backoff,
+                      hp->amp_interval, amp_a ? nullptr : polyak));
+  return (polyak && amp_a) ? launch_polyak(polyak->t, b->actor, Pa, polyak->tau, polyak->views, st) : SPIKERL_OK;
 }
 
 __global__ void neg_mean_kernel(int B, const float* __restrict__ q, float* __restrict__ out) {
@@ -637,9 +647,10 @@ int spikerl_critic_fwd_bwd(const spikerl_critic_cfg* cfg, int batch, const float
     return SPIKERL_E_ARG;
   }
   SPK_TRY(critic_supported(c, false));
-  return critic_fwd_bwd(c, batch, params2, (const __nv_bfloat16*)params2_bf16, obs, obs_dim, act, act_dim, target_y,
-                        q, target_y ? loss : nullptr, grad_params2, grad_act, act_grad_scale, 2, workspace,
-                        (cudaStream_t)stream);
+  const TdY ty{target_y, nullptr, nullptr, nullptr, 0.f, batch, nullptr};
+  return critic_fwd_bwd(c, batch, params2, (const __nv_bfloat16*)params2_bf16, obs, obs_dim, act, act_dim,
+                        target_y ? &ty : nullptr, q, target_y ? loss : nullptr, grad_params2, grad_act, act_grad_scale,
+                        2, workspace, (cudaStream_t)stream);
 }
 
 int spikerl_adam(float* params, const float* grads, float* m, float* v, size_t n, long long* step_counter,
@@ -715,9 +726,9 @@ int spikerl_td3_update(const spikerl_actor_cfg* acfg, const spikerl_critic_cfg* 
 
   AuxPool* aux = nullptr;
   SPK_TRY(aux_pool(&aux));
-  cudaStream_t sA = aux->side[0], sB = aux->side[1], sC = aux->side[2];
+  cudaStream_t sA = aux->side[0], sB = aux->side[1];
   static const bool serial = [] { const char* e = getenv("SPIKERL_TD3_SERIAL"); return e && e[0] == '1'; }();
-  if (serial) sA = sB = sC = st;   // A/B switch: the same work on one stream
+  if (serial) sA = sB = st;   // A/B switch: the same work on one stream
   const bool actor_step = (step % hp->policy_delay == 0);
   void* cws_t = ws + W.critic_ws_t;
 
@@ -730,14 +741,15 @@ int spikerl_td3_update(const spikerl_actor_cfg* acfg, const spikerl_critic_cfg* 
     SPK_TRY(launch_replay_gather(B, ad.S, ad.A, b->rs, b->ra, b->rr, b->rs2, b->rd, b->replay_size, seed, rank,
                                  b->rng_counter, gs, st));
   }
-  // branch A: target path. 1. a~ = clip(pi'(s') + clip(eps), -1, 1); 2. y = r + gamma (1 - d) min(Q1', Q2')(s', a~)
+  // branch A: target path. 1. a~ = clip(pi'(s') + clip(eps), -1, 1) (smoothing in the target actor's decoder
+  // launch); 2. Q1', Q2'(s', a~) (y = r + gamma (1 - d) min(Q1', Q2') is formed where the loss reads it)
   SPK_TRY(stream_after(sA, st, aux->ev[0]));
-  SPK_TRY(actor_forward_impl(ad, B, b->actor_t, atbf, s2, a2, aws + actor_ws_layout(ad, B).tape, sA));
-  SPK_TRY(launch_target_action(B, ad.A, a2, noise, hp->policy_noise, hp->noise_clip, seed, rank, b->rng_counter,
-                               ctr_snap, at, sA));
+  {
+    const TargetSmooth ts{noise, hp->policy_noise, hp->noise_clip, seed, rank, b->rng_counter, ctr_snap, at, 1};
+    SPK_TRY(actor_forward_impl(ad, B, b->actor_t, atbf, s2, a2, aws + actor_ws_layout(ad, B).tape, sA, &ts));
+  }
   SPK_TRY(critic_fwd_bwd(cd, B, b->critic_t, ctbf, s2, ad.S, at, ad.A, nullptr, qt, nullptr, nullptr, nullptr, 0.f,
                          2, cws_t, sA));
-  SPK_TRY(launch_td_target(B, r, dn, qt, hp->gamma, y, sA));
   SPK_CHECK_CUDA(cudaEventRecord(aux->ev[1], sA));
   // branch B (actor steps): the policy's own forward pi(s) depends only on s and the actor
   if (actor_step) {
@@ -745,22 +757,21 @@ int spikerl_td3_update(const spikerl_actor_cfg* acfg, const spikerl_critic_cfg* 
     SPK_TRY(actor_forward_impl(ad, B, b->actor, abf, s, api, tape, sB));
     SPK_CHECK_CUDA(cudaEventRecord(aux->ev[3], sB));
   }
-  // 3. critic forward Q(s, a) overlaps branch A; the loss waits for y; grads, allreduce, Adam
+  // 3. critic forward Q(s, a) overlaps branch A; the loss waits for Q'; grads, allreduce, Adam
   // (the bf16 working copies are kept current by the optimiser kernels themselves: Bf16Views)
   const Bf16Views cv = critic_bf16_views(cd, ad.bf16 ? (__nv_bfloat16*)b->critic_bf16 : nullptr);
   const Bf16Views ctv = critic_bf16_views(cd, ad.bf16 ? (__nv_bfloat16*)b->critic_t_bf16 : nullptr);
   const Bf16Views av = actor_bf16_views(ad, ad.bf16 ? (__nv_bfloat16*)b->actor_bf16 : nullptr);
   const Bf16Views atv = actor_bf16_views(ad, ad.bf16 ? (__nv_bfloat16*)b->actor_t_bf16 : nullptr);
   float* const amp_c = b->amp, * const amp_a = b->amp ? b->amp + 4 : nullptr;   // loss scaling (or none)
-  SPK_TRY(critic_fwd_bwd(cd, B, b->critic, cbf, s, ad.S, a, ad.A, y, q, losses, b->grad_critic, nullptr, 0.f, 2,
+  const TdY tdy{nullptr, r, dn, qt, hp->gamma, B, y};   // y = r + gamma (1 - d) min Q' formed inside the loss
+  SPK_TRY(critic_fwd_bwd(cd, B, b->critic, cbf, s, ad.S, a, ad.A, &tdy, q, losses, b->grad_critic, nullptr, 0.f, 2,
                          cws, st, aux->ev[1], amp_c));
-  SPK_TRY(critic_optimise(b, comm, hp, Pc, &cv, amp_c, st));
+  // actor steps: the critic targets' soft update rides on the critic's Adam launch
+  const PolyakFuse cpol{b->critic_t, hp->tau, &ctv};
+  SPK_TRY(critic_optimise(b, comm, hp, Pc, &cv, amp_c, st, actor_step ? &cpol : nullptr));
   // 4. delayed actor update + targets
   if (actor_step) {
-    // branch C: the critic targets only need the updated critic
-    SPK_TRY(stream_after(sC, st, aux->ev[4]));
-    SPK_TRY(launch_polyak(b->critic_t, b->critic, 2 * Pc, hp->tau, &ctv, sC));
-    SPK_CHECK_CUDA(cudaEventRecord(aux->ev[5], sC));
     SPK_CHECK_CUDA(cudaStreamWaitEvent(st, aux->ev[3], 0));   // pi(s) from branch B
     // actor loss -mean Q1(s, pi(s)): formed by the mma critic's data-backward launch itself
     const bool mma = critic_mma_ok(cd);
@@ -772,9 +783,8 @@ int spikerl_td3_update(const spikerl_actor_cfg* acfg, const spikerl_critic_cfg* 
     }
     SPK_TRY(actor_backward_impl(ad, B, b->actor, abf, s, tape, ga, b->grad_actor, 0, aws, st,
                                 b->fused_actor ? nullptr : comm));
-    SPK_TRY(actor_optimise(b, comm, hp, ad, Pa, &av, amp_a, st));
-    SPK_TRY(launch_polyak(b->actor_t, b->actor, Pa, hp->tau, &atv, st));
-    SPK_CHECK_CUDA(cudaStreamWaitEvent(st, aux->ev[5], 0));   // join branch C
+    const PolyakFuse apol{b->actor_t, hp->tau, &atv};
+    SPK_TRY(actor_optimise(b, comm, hp, ad, Pa, &av, amp_a, st, &apol));
   }
   return SPIKERL_OK;
 }
@@ -853,7 +863,7 @@ int spikerl_td3_update_pair(const spikerl_actor_cfg* acfg, const spikerl_critic_
   const __nv_bfloat16* ctbf = (const __nv_bfloat16*)b->critic_t_bf16;
   AuxPool* aux = nullptr;
   SPK_TRY(aux_pool(&aux));
-  cudaStream_t sA[2] = {aux->side[0], aux->side[7]}, sB = aux->side[1], sC = aux->side[2];
+  cudaStream_t sA[2] = {aux->side[0], aux->side[7]}, sB = aux->side[1];
   cudaEvent_t evA[2] = {aux->ev[1], aux->ev[7]};
   // sample both minibatches in one launch (update k + 1 draws with the counter value update k
   // advances to)
@@ -871,12 +881,11 @@ int spikerl_td3_update_pair(const spikerl_actor_cfg* acfg, const spikerl_critic_
   for (int i = 0; i < 2; ++i) {
     const Slot& x = sl[i];
     SPK_TRY(stream_after(sA[i], st, aux->ev[i == 0 ? 0 : 6]));
-    SPK_TRY(actor_forward_impl(ad, B, b->actor_t, atbf, x.s2, x.a2, x.aws + actor_ws_layout(ad, B).tape, sA[i]));
-    SPK_TRY(launch_target_action(B, ad.A, x.a2, noise ? noise + (size_t)i * B * ad.A : nullptr, hp->policy_noise,
-                                 hp->noise_clip, seed, rank, b->rng_counter, x.snap, x.at, sA[i], i == 1 ? 1 : 0));
+    const TargetSmooth ts{noise ? noise + (size_t)i * B * ad.A : nullptr, hp->policy_noise, hp->noise_clip, seed,
+                          rank, b->rng_counter, x.snap, x.at, i == 1 ? 1 : 0};
+    SPK_TRY(actor_forward_impl(ad, B, b->actor_t, atbf, x.s2, x.a2, x.aws + actor_ws_layout(ad, B).tape, sA[i], &ts));
     SPK_TRY(critic_fwd_bwd(cd, B, b->critic_t, ctbf, x.s2, ad.S, x.at, ad.A, nullptr, x.qt, nullptr, nullptr, nullptr,
                            0.f, 2, x.cws_t, sA[i]));
-    SPK_TRY(launch_td_target(B, x.r, x.dn, x.qt, hp->gamma, x.y, sA[i]));
     SPK_CHECK_CUDA(cudaEventRecord(evA[i], sA[i]));
   }
   // branch B: pi(s) of update k + 1 (the actor is unchanged by update k)
@@ -889,17 +898,16 @@ int spikerl_td3_update_pair(const spikerl_actor_cfg* acfg, const spikerl_critic_
   const Bf16Views atv = actor_bf16_views(ad, ad.bf16 ? (__nv_bfloat16*)b->actor_t_bf16 : nullptr);
   float* const amp_c = b->amp, * const amp_a = b->amp ? b->amp + 4 : nullptr;   // loss scaling (or none)
   // the two critic updates, in order
+  const PolyakFuse cpol{b->critic_t, hp->tau, &ctv};
   for (int i = 0; i < 2; ++i) {
     const Slot& x = sl[i];
-    SPK_TRY(critic_fwd_bwd(cd, B, b->critic, cbf, x.s, ad.S, x.a, ad.A, x.y, x.q, losses, b->grad_critic, nullptr,
+    const TdY tdy{nullptr, x.r, x.dn, x.qt, hp->gamma, B, x.y};
+    SPK_TRY(critic_fwd_bwd(cd, B, b->critic, cbf, x.s, ad.S, x.a, ad.A, &tdy, x.q, losses, b->grad_critic, nullptr,
                            0.f, 2, x.cws, st, evA[i], amp_c));
-    SPK_TRY(critic_optimise(b, comm, hp, Pc, &cv, amp_c, st));
+    SPK_TRY(critic_optimise(b, comm, hp, Pc, &cv, amp_c, st, i == 1 ? &cpol : nullptr));
   }
   // delayed actor update + targets (update k + 1), exactly as spikerl_td3_update's actor step
   const Slot& x = sl[1];
-  SPK_TRY(stream_after(sC, st, aux->ev[4]));
-  SPK_TRY(launch_polyak(b->critic_t, b->critic, 2 * Pc, hp->tau, &ctv, sC));
-  SPK_CHECK_CUDA(cudaEventRecord(aux->ev[5], sC));
   SPK_CHECK_CUDA(cudaStreamWaitEvent(st, aux->ev[3], 0));
   const bool mma = critic_mma_ok(cd);
   SPK_TRY(critic_fwd_bwd(cd, B, b->critic, cbf, x.s, ad.S, x.api, ad.A, nullptr, x.q, mma ? losses + 1 : nullptr,
@@ -910,9 +918,8 @@ int spikerl_td3_update_pair(const spikerl_actor_cfg* acfg, const spikerl_critic_
   }
   SPK_TRY(actor_backward_impl(ad, B, b->actor, abf, x.s, x.tape, x.ga, b->grad_actor, 0, x.aws, st,
                               b->fused_actor ? nullptr : comm));
-  SPK_TRY(actor_optimise(b, comm, hp, ad, Pa, &av, amp_a, st));
-  SPK_TRY(launch_polyak(b->actor_t, b->actor, Pa, hp->tau, &atv, st));
-  SPK_CHECK_CUDA(cudaStreamWaitEvent(st, aux->ev[5], 0));
+  const PolyakFuse apol{b->actor_t, hp->tau, &atv};
+  SPK_TRY(actor_optimise(b, comm, hp, ad, Pa, &av, amp_a, st, &apol));
   return SPIKERL_OK;
 }
 
