@@ -7,12 +7,12 @@
 //   ENC  dL/dA = (sum_t G_1) W_1            -> dmu, dsigma partial sums over the tile's rows
 //                                                          DESIGN.md R6 (straight-through encoder)
 //   DW   dW_l = sum_{t,b} G_l^T o_{l-1}     -> deterministic split-K fp32 partials
-// One persistent, warp-specialised kernel (1 CTA/SM, 448 threads):
+// One persistent, warp-specialised kernel (1 CTA/SM, 448 threads; 512 for the long-K pair forward):
 //   warp 0      TMA producer (A tiles; B tiles when they are bf16 tensors)
 //   warp 1      TMEM allocator + single-thread tcgen05.mma issuer (M=128, N<=256, K=16 steps)
-//   warps 2-5   spike-bit expanders: u32 spike words -> bf16 {0,1} tiles in the 128B-swizzled
-//               UMMA layout (K-major for FWD, MN-major for DW)
-//   warps 6-13  epilogue, 2 groups x 4 warps: tcgen05.ld (32x32b) of the TMEM accumulator, one
+//   warps 2-5   spike-bit expanders (2-7 for the long-K pair forward): u32 spike words -> bf16 {0,1} tiles
+//               in the 128B-swizzled UMMA layout (K-major for FWD, MN-major for DW)
+//   next 8      epilogue, 2 groups x 4 warps: tcgen05.ld (32x32b) of the TMEM accumulator, one
 //               thread per neuron, each group owning half of the tile's columns (4 groups of 4
 //               warps measured no faster: the FWD / DX epilogues are bound by their instruction
 //               count, not by latency hiding)
@@ -42,13 +42,20 @@ enum Mode { FWD = 0, DX = 1, ENC = 2, DW = 3, FWDO = 4, WG = 5, CF1 = 6, CF2 = 7
 __host__ __device__ constexpr bool is_fwd(int m) { return m == FWD || m == FWDO; }
 __host__ __device__ constexpr bool is_crit(int m) { return m == CF1 || m == CF2 || m == CB1; }
 
+constexpr int NUM_EPI_WARPS = 8, NUM_EPI_GROUPS = NUM_EPI_WARPS / 4;
+constexpr int EXP_WARP0 = 2;
 constexpr int BM = 128, BK = 64, STAGES = 4;
+// Spike-expander warps per CTA: 4 (at most one warp per ring stage), or 6 in the X6 instantiation of
+// the pair forward (6-stage ring), launched for long K loops: ablation r02 (SPIKERL_TC_DBG) put its
+// expanders alone at ~80 % of FWD L1's time; A/B with 6: FWD L1 (59 k-blocks per unit) -3.4 %, while
+// FWD L2 (16 k-blocks) ran 2.8 % slower. The epilogue warps follow them; DX / ENC / WG / critic modes
+// leave the expander warps idle.
+__host__ __device__ constexpr int exp_warps(bool x6) { return x6 ? 6 : 4; }
+__host__ __device__ constexpr int epi_warp0(bool x6) { return EXP_WARP0 + exp_warps(x6); }
+__host__ __device__ constexpr int n_threads(bool x6) { return (epi_warp0(x6) + NUM_EPI_WARPS) * 32; }
 constexpr int A_STAGE = BM * BK * 2;             // 16 KB
 constexpr int B_STAGE = 256 * BK * 2;            // 32 KB
 constexpr int STAGE_BYTES = A_STAGE + B_STAGE;   // 48 KB
-constexpr int NUM_EXP_WARPS = 4, NUM_EPI_WARPS = 8, NUM_EPI_GROUPS = NUM_EPI_WARPS / 4;
-constexpr int EXP_WARP0 = 2, EPI_WARP0 = 2 + NUM_EXP_WARPS;
-constexpr int NUM_THREADS = (EPI_WARP0 + NUM_EPI_WARPS) * 32;  // 448
 // batch rows of a (t, b) tile per epilogue group (FWD / DX): a quarter of the tile, at least 4 (one
 // quad of the neuron-major planes); groups past BT / epi_hb(BT) idle
 __host__ __device__ constexpr int epi_hb(int bt) { return bt / NUM_EPI_GROUPS > 4 ? bt / NUM_EPI_GROUPS : 4; }
@@ -344,8 +351,8 @@ __device__ __forceinline__ Tile decode(const Params& p, int u, int rank, int CG)
 // RHO: the reset-gate-gradient variant (R11, rho = 1): FWD / FWDO write the fp32 membrane
 // planes, DX reads the previous layer's; a separate instantiation, so the default path carries no
 // extra registers for it
-template <int MODE, int BT, int CG, bool F16 = false, bool RHO = false>
-__global__ void __launch_bounds__(NUM_THREADS, 1)
+template <int MODE, int BT, int CG, bool F16 = false, bool RHO = false, bool X6 = false>
+__global__ void __launch_bounds__(n_threads(X6), 1)
     tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
               const __grid_constant__ CUtensorMap tmC, const Params p) {
   // A CTA of a pair holds at most 128 B rows (its half of the MMA's N), so its stages are 32 KB
@@ -369,6 +376,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
   constexpr bool A_MN = !is_fwd(MODE) && MODE != WG;
   constexpr bool B_MN = (MODE == DW);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  constexpr int EPI_WARP0 = epi_warp0(X6);
   const int rank = CG == 2 ? (int)cluster_ctarank() : 0;
   const int cid = blockIdx.x / CG, ncl = gridDim.x / CG;   // pair (or CTA) index and count
   if (threadIdx.x == 0) trace_stamp(p, 0);
@@ -497,7 +505,10 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     // store -> fence -> arrive chain paced DW/FWD L1 at ~1600 clk per k-block, with the MMAs
     // disabled). The spike words of the warp's next k-block are loaded one iteration ahead into
     // the other half of a statically indexed double buffer.
-    if (B_EXPAND) {
+    // at most one expander warp per ring stage: a warp waits on its stage's empty barrier by phase
+    // parity, so two warps must never own items of the same stage at once
+    constexpr int NEXP = exp_warps(X6) < NST ? exp_warps(X6) : NST;
+    if (B_EXPAND && warp - EXP_WARP0 < NEXP) {
       const int ew = warp - EXP_WARP0;
       uint32_t it = 0;   // ring iterations of all units so far (every warp counts all of them)
       for (int u = cid; u < p.n_units; u += ncl) {
@@ -549,14 +560,14 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
             }
           };
           // this warp's k-blocks of the unit: local index j = ew, ew + 4, ... (global it + j)
-          const int j0 = (int)((ew - it % NUM_EXP_WARPS + NUM_EXP_WARPS) % NUM_EXP_WARPS);
+          const int j0 = (int)((ew - it % NEXP + NEXP) % NEXP);
           if (j0 < nkb) ld(q[0], t.kb0 + j0);
-          for (int j = j0; j < nkb; j += 2 * NUM_EXP_WARPS) {
-            if (j + NUM_EXP_WARPS < nkb) ld(q[1], t.kb0 + j + NUM_EXP_WARPS);
+          for (int j = j0; j < nkb; j += 2 * NEXP) {
+            if (j + NEXP < nkb) ld(q[1], t.kb0 + j + NEXP);
             body(q[0], it + j);
-            if (j + NUM_EXP_WARPS >= nkb) break;
-            if (j + 2 * NUM_EXP_WARPS < nkb) ld(q[0], t.kb0 + j + 2 * NUM_EXP_WARPS);
-            body(q[1], it + j + NUM_EXP_WARPS);
+            if (j + NEXP >= nkb) break;
+            if (j + 2 * NEXP < nkb) ld(q[0], t.kb0 + j + 2 * NEXP);
+            body(q[1], it + j + NEXP);
           }
         } else {
           // MN-major: K row r = one (t,b) row; every CTA expands 256 columns = 8 words = 4 atoms of
@@ -613,14 +624,14 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
               else mbar_arrive(&full[stage]);
             }
           };
-          const int j0 = (int)((ew - it % NUM_EXP_WARPS + NUM_EXP_WARPS) % NUM_EXP_WARPS);
+          const int j0 = (int)((ew - it % NEXP + NEXP) % NEXP);
           if (j0 < nkb) ld(q[0], t.kb0 + j0);
-          for (int j = j0; j < nkb; j += 2 * NUM_EXP_WARPS) {
-            if (j + NUM_EXP_WARPS < nkb) ld(q[1], t.kb0 + j + NUM_EXP_WARPS);
+          for (int j = j0; j < nkb; j += 2 * NEXP) {
+            if (j + NEXP < nkb) ld(q[1], t.kb0 + j + NEXP);
             body(q[0], it + j);
-            if (j + NUM_EXP_WARPS >= nkb) break;
-            if (j + 2 * NUM_EXP_WARPS < nkb) ld(q[0], t.kb0 + j + 2 * NUM_EXP_WARPS);
-            body(q[1], it + j + NUM_EXP_WARPS);
+            if (j + NEXP >= nkb) break;
+            if (j + 2 * NEXP < nkb) ld(q[0], t.kb0 + j + 2 * NEXP);
+            body(q[1], it + j + NEXP);
           }
         }
         it += nkb;
@@ -1113,7 +1124,7 @@ static int pair_slots() {
       cudaGetLastError();
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(num_sms() / 2 * 2, 1, 1);
-    cfg.blockDim = dim3(NUM_THREADS, 1, 1);
+    cfg.blockDim = dim3(n_threads(false), 1, 1);
     cfg.dynamicSmemBytes = SMEM_BYTES;
     cudaLaunchAttribute at[1];
     at[0].id = cudaLaunchAttributeClusterDimension;
@@ -1142,16 +1153,16 @@ static bool pairs_enabled() {
   return v == 1;
 }
 
-template <int MODE, int BT, int CG, bool F16, bool RHO = false>
+template <int MODE, int BT, int CG, bool F16, bool RHO = false, bool X6 = false>
 static int launch_cg(const CUtensorMap& ma, const CUtensorMap& mb, const CUtensorMap& mc, const Params& p, cudaStream_t st) {
-  SPK_SMEM_ATTR((tc_kernel<MODE, BT, CG, F16, RHO>), SMEM_BYTES);
+  SPK_SMEM_ATTR((tc_kernel<MODE, BT, CG, F16, RHO, X6>), SMEM_BYTES);
   if (CG == 1) {
     const int ncta = num_sms();
     const int grid = p.n_units < ncta ? (int)p.n_units : ncta;
-    pdl((tc_kernel<MODE, BT, CG, F16, RHO>), grid, NUM_THREADS, SMEM_BYTES, st)(ma, mb, mc, p);
+    pdl((tc_kernel<MODE, BT, CG, F16, RHO, X6>), grid, n_threads(X6), SMEM_BYTES, st)(ma, mb, mc, p);
   } else {
     cudaLaunchConfig_t cfg = {};
-    cfg.blockDim = dim3(NUM_THREADS, 1, 1);
+    cfg.blockDim = dim3(n_threads(X6), 1, 1);
     cfg.dynamicSmemBytes = SMEM_BYTES;
     cfg.stream = st;
     cudaLaunchAttribute at[2];
@@ -1168,7 +1179,7 @@ static int launch_cg(const CUtensorMap& ma, const CUtensorMap& mb, const CUtenso
     const int slots = pair_slots();
     const long long grid = p.n_units < slots ? p.n_units : slots;
     cfg.gridDim = dim3((unsigned)(grid * CG), 1, 1);
-    cudaError_t e = cudaLaunchKernelEx(&cfg, tc_kernel<MODE, BT, CG, F16, RHO>, ma, mb, mc, p);
+    cudaError_t e = cudaLaunchKernelEx(&cfg, tc_kernel<MODE, BT, CG, F16, RHO, X6>, ma, mb, mc, p);
     if (e != cudaSuccess) { set_error("cudaLaunchKernelEx (pair): %s", cudaGetErrorString(e)); return SPIKERL_E_CUDA; }
   }
   SPK_LAUNCHED();
@@ -1199,6 +1210,8 @@ static int launch(const CUtensorMap& ma, const CUtensorMap& mb, const CUtensorMa
     }
     if (p.f16)
       return p.cg == 2 ? launch_cg<MODE, BT, 2, true>(ma, mb, mc, p, st) : launch_cg<MODE, BT, 1, true>(ma, mb, mc, p, st);
+    if constexpr (is_fwd(MODE))   // long K loops: 6 expander warps (see exp_warps)
+      if (p.cg == 2 && p.k_blocks >= 32) return launch_cg<MODE, BT, 2, false, false, true>(ma, mb, mc, p, st);
     return p.cg == 2 ? launch_cg<MODE, BT, 2, false>(ma, mb, mc, p, st) : launch_cg<MODE, BT, 1, false>(ma, mb, mc, p, st);
   } else {
     if (MODE != WG && p.f16)
