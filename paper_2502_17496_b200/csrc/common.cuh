@@ -86,6 +86,15 @@ __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;"
 __device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
 bool pdl_enabled();
 void note_launch_error(cudaError_t e);
+// Scheduling priority of the launches enqueued by this host thread (cudaLaunchAttributePriority;
+// 0 = the device default, the lowest; negative = higher). Set by LaunchPriority scopes around the
+// critical branches of the TD3 update DAG.
+int& launch_priority();
+struct LaunchPriority {
+  int old;
+  explicit LaunchPriority(int p) : old(launch_priority()) { launch_priority() = p; }
+  ~LaunchPriority() { launch_priority() = old; }
+};
 
 template <typename... KArgs>
 struct PdlLaunch {
@@ -100,11 +109,16 @@ struct PdlLaunch {
     cfg.blockDim = b;
     cfg.dynamicSmemBytes = smem;
     cfg.stream = st;
-    cudaLaunchAttribute at[1];
+    cudaLaunchAttribute at[2];
     at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
     at[0].val.programmaticStreamSerializationAllowed = pdl_enabled() ? 1 : 0;
     cfg.attrs = at;
     cfg.numAttrs = 1;
+    if (const int pr = launch_priority()) {
+      at[1].id = cudaLaunchAttributePriority;
+      at[1].val.priority = pr;
+      cfg.numAttrs = 2;
+    }
     const cudaError_t e = cudaLaunchKernelEx(&cfg, k, static_cast<KArgs>(args)...);
     if (e != cudaSuccess) note_launch_error(e);
   }

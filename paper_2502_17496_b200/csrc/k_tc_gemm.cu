@@ -1165,7 +1165,7 @@ static int launch_cg(const CUtensorMap& ma, const CUtensorMap& mb, const CUtenso
     cfg.blockDim = dim3(n_threads(X6), 1, 1);
     cfg.dynamicSmemBytes = SMEM_BYTES;
     cfg.stream = st;
-    cudaLaunchAttribute at[2];
+    cudaLaunchAttribute at[3];
     at[0].id = cudaLaunchAttributeClusterDimension;
     at[0].val.clusterDim.x = CG;
     at[0].val.clusterDim.y = 1;
@@ -1174,6 +1174,11 @@ static int launch_cg(const CUtensorMap& ma, const CUtensorMap& mb, const CUtenso
     at[1].val.programmaticStreamSerializationAllowed = pdl_enabled() ? 1 : 0;
     cfg.attrs = at;
     cfg.numAttrs = 2;
+    if (const int pr = launch_priority()) {
+      at[2].id = cudaLaunchAttributePriority;
+      at[2].val.priority = pr;
+      cfg.numAttrs = 3;
+    }
     // A persistent grid larger than the number of co-resident pairs would run a second wave of
     // whole pairs; size it to what the GPCs can actually hold (not simply 148 / 2).
     const int slots = pair_slots();

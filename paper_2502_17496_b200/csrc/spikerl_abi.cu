@@ -32,6 +32,11 @@ cudaError_t take_launch_error() {
   g_launch_err = cudaSuccess;
   return e;
 }
+int& launch_priority() {
+  thread_local int p = 0;
+  return p;
+}
+
 bool pdl_enabled() {
   static const bool on = [] { const char* e = getenv("SPIKERL_PDL"); return !(e && e[0] == '0'); }();
   return on;
@@ -669,6 +674,18 @@ int spikerl_polyak(float* target, const float* source, size_t n, float tau, spik
   return launch_polyak(target, source, n, tau, nullptr, (cudaStream_t)stream);
 }
 
+// raised launch priority of a TD3 update's critical chain (see spikerl_td3_update_pair)
+static int td3_priority(int batch) {
+  static const int prio_env = [] { const char* e = getenv("SPIKERL_TD3_PRIO"); return e ? atoi(e) : -1; }();
+  if (prio_env >= 0) return -prio_env;
+  int lo = 0, hi = 0;
+  if (cudaDeviceGetStreamPriorityRange(&lo, &hi) != cudaSuccess) {
+    cudaGetLastError();
+    return 0;
+  }
+  return batch < 1024 ? hi : 0;
+}
+
 int spikerl_td3_update(const spikerl_actor_cfg* acfg, const spikerl_critic_cfg* ccfg, const spikerl_td3_cfg* hp,
                        const spikerl_td3_bufs* b, long long step, unsigned long long seed, const long long* indices,
                        const float* noise, spikerl_comm* comm, float* losses, void* workspace,
@@ -706,6 +723,7 @@ int spikerl_td3_update(const spikerl_actor_cfg* acfg, const spikerl_critic_cfg* 
     set_error("replay holds %lld < batch %d transitions", b->replay_size, B);
     return SPIKERL_E_NOTREADY;
   }
+  LaunchPriority lp_hi(td3_priority(B));   // critical chain raised, branch B at the default
   cudaStream_t st = (cudaStream_t)stream;
   const Td3Ws W = td3_ws_layout(ad, cd, B);
   char* ws = (char*)workspace;
@@ -754,6 +772,7 @@ int spikerl_td3_update(const spikerl_actor_cfg* acfg, const spikerl_critic_cfg* 
   // branch B (actor steps): the policy's own forward pi(s) depends only on s and the actor
   if (actor_step) {
     SPK_TRY(stream_after(sB, st, aux->ev[2]));
+    LaunchPriority lp(0);
     SPK_TRY(actor_forward_impl(ad, B, b->actor, abf, s, api, tape, sB));
     SPK_CHECK_CUDA(cudaEventRecord(aux->ev[3], sB));
   }
@@ -837,6 +856,12 @@ int spikerl_td3_update_pair(const spikerl_actor_cfg* acfg, const spikerl_critic_
     set_error("replay holds %lld < batch %d transitions", b->replay_size, B);
     return SPIKERL_E_NOTREADY;
   }
+  // scheduling (latency regime, B < 1024): update k's target path and the critic / actor chain at a
+  // raised launch priority, the branches needed later (A1, B) at the default, so their CTAs fill in
+  // instead of competing. A/B r02: configs[1] -1 %, configs[2] -2.2 %, but configs[3] B = 4096 +3.5 %
+  // (there the late branches are long enough to become critical), hence the batch bound.
+  // SPIKERL_TD3_PRIO=<n>: priority -n at any batch (0: off).
+  LaunchPriority lp_hi(td3_priority(hp->batch));
   cudaStream_t st = (cudaStream_t)stream;
   const Td3Ws W = td3_ws_layout(ad, cd, B);
   struct Slot {
@@ -880,6 +905,7 @@ int spikerl_td3_update_pair(const spikerl_actor_cfg* acfg, const spikerl_critic_
   // target paths of both updates, concurrently (branches A0, A1); only the second advances the counter
   for (int i = 0; i < 2; ++i) {
     const Slot& x = sl[i];
+    LaunchPriority lp(i == 1 ? 0 : launch_priority());   // A1 (needed one critic update later): default
     SPK_TRY(stream_after(sA[i], st, aux->ev[i == 0 ? 0 : 6]));
     const TargetSmooth ts{noise ? noise + (size_t)i * B * ad.A : nullptr, hp->policy_noise, hp->noise_clip, seed,
                           rank, b->rng_counter, x.snap, x.at, i == 1 ? 1 : 0};
@@ -890,7 +916,10 @@ int spikerl_td3_update_pair(const spikerl_actor_cfg* acfg, const spikerl_critic_
   }
   // branch B: pi(s) of update k + 1 (the actor is unchanged by update k)
   SPK_TRY(stream_after(sB, st, aux->ev[2]));
-  SPK_TRY(actor_forward_impl(ad, B, b->actor, abf, sl[1].s, sl[1].api, sl[1].tape, sB));
+  {
+    LaunchPriority lp(0);
+    SPK_TRY(actor_forward_impl(ad, B, b->actor, abf, sl[1].s, sl[1].api, sl[1].tape, sB));
+  }
   SPK_CHECK_CUDA(cudaEventRecord(aux->ev[3], sB));
   const Bf16Views cv = critic_bf16_views(cd, ad.bf16 ? (__nv_bfloat16*)b->critic_bf16 : nullptr);
   const Bf16Views ctv = critic_bf16_views(cd, ad.bf16 ? (__nv_bfloat16*)b->critic_t_bf16 : nullptr);
