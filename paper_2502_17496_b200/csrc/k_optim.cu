@@ -18,7 +18,7 @@ static int ew_grid(size_t n, int per_thread) {
 // Streaming kernels (Adam, Polyak): exactly one wave of resident blocks, never more. A grid of
 // 8 blocks per SM with 3 resident ran 2.67 waves (ncu r01: Adam at configs[4] size 66% of the
 // copy peak, the partial last wave and the ramp of each wave exposed).
-template <typename K>
+template <int KEY, typename K>   // KEY: one occupancy cache per kernel (instantiations share K's type)
 static int stream_grid(K kernel, size_t n, int per_thread) {
   static int cache[32] = {};   // per device
   int& per_sm = cache[cur_device()];
@@ -100,6 +100,9 @@ Bf16Views actor_bf16_views(const ActorDims& d, __nv_bfloat16* out) {
 // ------------------------------------------------------------------ Adam
 // t = *counter + 1 is read by every block; the last block to finish (atomic ticket) stores it
 // back, so the call is graph-replayable with an on-device step count.
+// POL: the fused Polyak soft update of a target (PolyakFuse) — its own instantiation, so the plain
+// Adam keeps its register budget (92 vs 80 registers: one resident block per SM fewer)
+template <bool POL>
 __global__ void __launch_bounds__(256) adam_kernel(float* __restrict__ p, const float* __restrict__ g,
                                                    float* __restrict__ m, float* __restrict__ v,
                                                    size_t n, long long* counter, float lr, float b1,
@@ -146,7 +149,7 @@ __global__ void __launch_bounds__(256) adam_kernel(float* __restrict__ p, const 
         gg[u] = reinterpret_cast<const float4*>(g)[i];
         mm[u] = reinterpret_cast<float4*>(m)[i];
         vv[u] = reinterpret_cast<float4*>(v)[i];
-        if (tp) tt[u] = reinterpret_cast<float4*>(tp)[i];
+        if constexpr (POL) tt[u] = reinterpret_cast<float4*>(tp)[i];
       }
     }
 #pragma unroll
@@ -161,7 +164,7 @@ __global__ void __launch_bounds__(256) adam_kernel(float* __restrict__ p, const 
         const size_t e = 4 * i + j;
         if (e >= clo && e < chi) pa[j] = fmaxf(pa[j], cmin);
         store_views(views, e, pa[j]);
-        if (tp) {
+        if constexpr (POL) {
           float* ta = &tt[u].x;
           ta[j] = __fadd_rn(__fmul_rn(tau, pa[j]), __fmul_rn(omt, ta[j]));
           store_views(tviews, e, ta[j]);
@@ -170,7 +173,7 @@ __global__ void __launch_bounds__(256) adam_kernel(float* __restrict__ p, const 
       reinterpret_cast<float4*>(p)[i] = pp[u];
       reinterpret_cast<float4*>(m)[i] = mm[u];
       reinterpret_cast<float4*>(v)[i] = vv[u];
-      if (tp) reinterpret_cast<float4*>(tp)[i] = tt[u];
+      if constexpr (POL) reinterpret_cast<float4*>(tp)[i] = tt[u];
     }
   }
   for (size_t e = 4 * n4 + blockIdx.x * (size_t)blockDim.x + threadIdx.x; e < n && !skip; e += stride) {
@@ -180,7 +183,7 @@ __global__ void __launch_bounds__(256) adam_kernel(float* __restrict__ p, const 
     if (e >= clo && e < chi) pp = fmaxf(pp, cmin);
     p[e] = pp; m[e] = mm; v[e] = vv;
     store_views(views, e, pp);
-    if (tp) {
+    if constexpr (POL) {
       const float x = __fadd_rn(__fmul_rn(tau, pp), __fmul_rn(omt, tp[e]));
       tp[e] = x;
       store_views(tviews, e, x);
@@ -238,11 +241,15 @@ int launch_adam(float* p, const float* g, float* m, float* v, size_t n, long lon
     set_error("adam: buffers must be 16-byte aligned");
     return SPIKERL_E_ARG;
   }
-  pdl(adam_kernel, stream_grid(adam_kernel, n, 8), 256, 0, st)(p, g, m, v, n, counter, lr, b1, b2, eps, clo, chi,
-                                             cmin, ticket, views ? *views : none, amp, amp_growth, amp_backoff,
-                                             amp_interval, log((double)b1), log((double)b2),
-                                             polyak ? polyak->t : nullptr, polyak ? polyak->tau : 0.f,
-                                             (polyak && polyak->views) ? *polyak->views : none);
+  if (polyak)
+    pdl(adam_kernel<true>, stream_grid<1>(adam_kernel<true>, n, 8), 256, 0, st)(
+        p, g, m, v, n, counter, lr, b1, b2, eps, clo, chi, cmin, ticket, views ? *views : none, amp, amp_growth,
+        amp_backoff, amp_interval, log((double)b1), log((double)b2), polyak->t, polyak->tau,
+        polyak->views ? *polyak->views : none);
+  else
+    pdl(adam_kernel<false>, stream_grid<0>(adam_kernel<false>, n, 8), 256, 0, st)(
+        p, g, m, v, n, counter, lr, b1, b2, eps, clo, chi, cmin, ticket, views ? *views : none, amp, amp_growth,
+        amp_backoff, amp_interval, log((double)b1), log((double)b2), nullptr, 0.f, none);
   SPK_LAUNCHED();
   return SPIKERL_OK;
 }
@@ -288,7 +295,7 @@ __global__ void __launch_bounds__(256, 4) polyak_kernel(float* __restrict__ t, c
 int launch_polyak(float* t, const float* s, size_t n, float tau, const Bf16Views* views, cudaStream_t st) {
   const Bf16Views none{};
   ProfScope ps_("polyak", PB_HBM, 0.0, 12.0 * n, st);
-  pdl(polyak_kernel, stream_grid(polyak_kernel, n, 8), 256, 0, st)(t, s, n, tau, views ? *views : none);
+  pdl(polyak_kernel, stream_grid<2>(polyak_kernel, n, 8), 256, 0, st)(t, s, n, tau, views ? *views : none);
   SPK_LAUNCHED();
   return SPIKERL_OK;
 }
