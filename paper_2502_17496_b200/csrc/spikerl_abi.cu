@@ -889,6 +889,8 @@ int spikerl_td3_update_pair(const spikerl_actor_cfg* acfg, const spikerl_critic_
   AuxPool* aux = nullptr;
   SPK_TRY(aux_pool(&aux));
   cudaStream_t sA[2] = {aux->side[0], aux->side[7]}, sB = aux->side[1];
+  static const bool serial = [] { const char* e = getenv("SPIKERL_TD3_SERIAL"); return e && e[0] == '1'; }();
+  if (serial) sA[0] = sA[1] = sB = st;   // A/B switch: the same work on one stream
   cudaEvent_t evA[2] = {aux->ev[1], aux->ev[7]};
   // sample both minibatches in one launch (update k + 1 draws with the counter value update k
   // advances to)
