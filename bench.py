@@ -592,18 +592,22 @@ def e2e_td3(args, rank, world, td3_dev, shape, B, pair=False):
     f32 = dict(dtype=torch.float32, device="cuda")
     nb = 2 if pair else 1
     # device staging = a replay of nb B rows whose five arrays are views of ONE buffer, so a pinned
-    # host buffer with the same layout arrives in a single H2D copy
-    dev = torch.empty(nb * B * per, **f32)
+    # host buffer with the same layout arrives in a single H2D copy. pair: two such slots (rows
+    # [0, 2B) and [2B, 4B) of the staging replay, array by array), so the copy of the next pair's
+    # minibatches overlaps the current pair's updates
+    nslot = 2 if pair else 1
+    dev = torch.empty(nslot * nb * B * per, **f32)
 
-    def views(buf):
-        n, o, out = nb * B, 0, []
+    def views(buf, n=None):
+        n = nb * B if n is None else n
+        o, out = 0, []
         for w in (S, A, 1, S, 1):
             v = buf[o:o + n * w]
             out.append(v.view(n, w) if w > 1 else v)
             o += n * w
         return pk.ReplayShard(*out)
 
-    rs = views(dev)
+    rs = views(dev, nslot * nb * B)
     if pair:   # pinned host buffers, one per pair of pool minibatches, in the staging layout
         packed = []
         for g_i in range(nbuf // 2):
@@ -620,6 +624,7 @@ def e2e_td3(args, rank, world, td3_dev, shape, B, pair=False):
         t_dst.copy_(t_src)
     td3.refresh()
     idx = torch.arange(nb * B, dtype=torch.int64, device="cuda").view(nb, B)
+    idx_slot = [idx + sl * nb * B for sl in range(nslot)]
     loss_host = torch.empty(2, dtype=torch.float32).pin_memory()
 
     def h2d(h, j):
@@ -627,31 +632,44 @@ def e2e_td3(args, rank, world, td3_dev, shape, B, pair=False):
             dst[j * B:(j + 1) * B].copy_(src, non_blocking=True)          # one cudaMemcpyAsync H2D each
 
     if pair:
+        hv = [views(packed[g_i]) for g_i in range(len(packed))]
+
+        def h2d_slot(g_i, sl):   # pair g_i's two minibatches into staging slot sl: one H2D per array
+            dv = [rs.s, rs.a, rs.r, rs.s2, rs.d]
+            for src, dst in zip((hv[g_i].s, hv[g_i].a, hv[g_i].r, hv[g_i].s2, hv[g_i].d), dv):
+                dst[sl * nb * B:(sl + 1) * nb * B].copy_(src, non_blocking=True)
+
         graphs = []
-        cs = torch.cuda.Stream()
+        cs, cp = torch.cuda.Stream(), torch.cuda.Stream()
         cs.wait_stream(torch.cuda.current_stream())
         with torch.cuda.stream(cs):
-            for g_i in range(nbuf // 2):
+            for g_i in range(len(packed)):   # an even count: graph g_i reads slot g_i % 2
                 g = torch.cuda.CUDAGraph()
                 with torch.cuda.graph(g, stream=cs):
-                    dev.copy_(packed[g_i], non_blocking=True)      # both minibatches: one H2D copy
-                    td3.update_pair(1, indices=idx)
+                    cp.wait_stream(cs)
+                    with torch.cuda.stream(cp):   # the next pair's minibatches, during this pair's updates
+                        h2d_slot((g_i + 1) % len(packed), (g_i + 1) % 2)
+                    td3.update_pair(1, indices=idx_slot[g_i % 2])
+                    cs.wait_stream(cp)
                     loss_host.copy_(td3.losses, non_blocking=True)
                 graphs.append(g)
         torch.cuda.current_stream().wait_stream(cs)
+        h2d_slot(0, 0)                       # the first pair's data (every later copy is inside a step)
         torch.cuda.synchronize()
 
         def step(k):
             graphs[k % len(graphs)].replay()
 
-        for k in range(max(1, args.warmup // 2)):
+        nw = -(-max(1, args.warmup // 2) // len(graphs)) * len(graphs)   # whole cycles: graph 0 next
+        for k in range(nw):
             step(k)
         npair = max(1, args.steps // 2)
         total_ms = time_steps(step, npair, None, world)
         torch.cuda.synchronize()
         n_upd = 2 * npair
-        path = ("graph of [one H2D copy of two packed pinned host minibatches -> spikerl_td3_update_pair -> D2H "
-                "of the losses] per two updates (TD3.update_pair through the C ABI)")
+        path = ("graphs of [H2D copies of the next two pinned host minibatches on a copy stream || "
+                "spikerl_td3_update_pair on the current ones -> D2H of the losses] per two updates "
+                "(TD3.update_pair through the C ABI; double-buffered staging)")
     else:
         def step(k):
             h2d(host[k % nbuf], 0)
@@ -692,9 +710,12 @@ def run_actor(args, rank, world, workload):
     obs = torch.clamp(torch.randn(B, shape.obs_dim, device="cuda", generator=g), -5, 5)
     ga = torch.randn(B, shape.act_dim, device="cuda", generator=g)
 
+    def step_on(o, g):
+        actor.forward(o)
+        actor.backward(o, g, comm=comm)   # with comm: bucketed gradient mean overlapping the BPTT
+
     def step(k=0):
-        actor.forward(obs)
-        actor.backward(obs, ga, comm=comm)   # with comm: bucketed gradient mean overlapping the BPTT
+        step_on(obs, ga)
 
     lib = pk.lib()
     step()                          # first launches (module loading, tensor maps) outside the profile
@@ -768,7 +789,7 @@ def run_actor(args, rank, world, workload):
     if overlap:
         out["comm_overlap"] = overlap
     if not args.no_e2e:
-        out["e2e"] = e2e_actor(args, world, actor, step, obs, ga, gsum, shape)
+        out["e2e"] = e2e_actor(args, world, actor, step_on, obs, ga, gsum, shape)
     return out
 
 
@@ -786,34 +807,58 @@ def comm_overlap(tl):
     return out
 
 
-def e2e_actor(args, world, actor, step, obs, ga, gsum, shape):
+def e2e_actor(args, world, actor, step_on, obs, ga, gsum, shape):
     """End to end through the public API: every step copies its observations and upstream action
     gradients from pinned host memory and reads the parameter gradients back into pinned host
-    memory; one captured graph of [H2D, H2D -> forward -> backward (-> allreduce) -> D2H]."""
+    memory. Graphs (two, alternating device input buffers) of [H2D of the NEXT step's inputs on a
+    copy stream || forward -> backward (-> allreduce) on this step's -> D2H of the gradients]: the
+    input copies overlap the previous step's compute (every step's copy is inside the timed region
+    except the first, made before it)."""
     import torch
     host_obs = obs.cpu().pin_memory()
     host_ga = ga.cpu().pin_memory()
     grads_host = torch.empty(actor.n_params, dtype=torch.float32).pin_memory()
+    ins = [(obs, ga), (obs.clone(), ga.clone())]
 
-    def e2e_step(k=0):
-        obs.copy_(host_obs, non_blocking=True)
-        ga.copy_(host_ga, non_blocking=True)
-        step(k)
-        grads_host.copy_(actor.grads, non_blocking=True)
+    def h2d(i):
+        ins[i][0].copy_(host_obs, non_blocking=True)
+        ins[i][1].copy_(host_ga, non_blocking=True)
+
     if args.eager:
-        run = e2e_step
+        def run(k):
+            h2d(0)
+            step_on(*ins[0])
+            grads_host.copy_(actor.grads, non_blocking=True)
     else:
-        g = _capture(e2e_step)
-        run = lambda k: g.replay()
-    n = max(3, args.steps // 2)
-    for k in range(max(1, args.warmup // 2)):
+        graphs = []
+        cs, cp = torch.cuda.Stream(), torch.cuda.Stream()
+        cs.wait_stream(torch.cuda.current_stream())
+        with torch.cuda.stream(cs):
+            for i in range(2):
+                g = torch.cuda.CUDAGraph()
+                with torch.cuda.graph(g, stream=cs):
+                    cp.wait_stream(cs)
+                    with torch.cuda.stream(cp):
+                        h2d(1 - i)
+                    step_on(*ins[i])
+                    cs.wait_stream(cp)
+                    grads_host.copy_(actor.grads, non_blocking=True)
+                graphs.append(g)
+        torch.cuda.current_stream().wait_stream(cs)
+        h2d(0)
+        torch.cuda.synchronize()
+        run = lambda k: graphs[k % 2].replay()
+    n = max(4, args.steps // 2)
+    n += n % 2
+    for k in range(2 * max(1, args.warmup // 4)):
         run(k)
     total = time_steps(run, n, None, world)
     B = obs.shape[0]
     return {"value": round(n * gsum / (total / 1e3), 2), "unit": "samples/s",
             "h2d_bytes_per_step": B * (shape.obs_dim + shape.act_dim) * 4, "d2h_bytes_per_step": actor.n_params * 4,
-            "path": ("graph" if not args.eager else "eager") + " of [H2D obs + upstream grads from pinned host -> "
-                    "spikerl_actor_forward -> spikerl_actor_backward (-> allreduce) -> D2H of the gradients]"}
+            "path": ("graphs" if not args.eager else "eager") + " of [H2D of the next step's obs + upstream grads from "
+                    "pinned host on a copy stream || spikerl_actor_forward -> spikerl_actor_backward (-> allreduce) "
+                    "on this step's -> D2H of the gradients] (double-buffered inputs)"}
 
 
 def hbm_kernels(actor, summ, reps=20):
