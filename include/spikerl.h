@@ -141,6 +141,10 @@ size_t spikerl_critic_bf16_bytes(const spikerl_critic_cfg* cfg); /* twin pair: [
 /* Device buffers the caller allocates for one forward(+backward) at `batch`. */
 size_t spikerl_actor_tape_bytes(const spikerl_actor_cfg* cfg, int batch);
 size_t spikerl_actor_workspace_bytes(const spikerl_actor_cfg* cfg, int batch);
+/* Byte offset inside the actor workspace of the tape an inference-only forward (tape == NULL) writes:
+ * its spike / window planes, counts and actions (not the stimulation plane A, which such a forward
+ * does not compute; layout as spikerl_actor_tape_layout). For tests and diagnostics. */
+size_t spikerl_actor_workspace_tape_offset(const spikerl_actor_cfg* cfg, int batch);
 size_t spikerl_critic_workspace_bytes(const spikerl_critic_cfg* cfg, int batch);
 size_t spikerl_td3_workspace_bytes(const spikerl_actor_cfg* acfg, const spikerl_critic_cfg* ccfg,
                                    int batch);
@@ -189,7 +193,9 @@ int spikerl_critic_refresh_bf16(const spikerl_critic_cfg* cfg, int n_critics, co
 /* Actor forward: obs [B][S] fp32 -> actions [B][A] fp32 (tanh, bound 1).
  * params: flat fp32 (layout above); params_bf16: working copy (required iff precision=BF16).
  * tape: host descriptor whose .dev/.bytes the caller set (NULL = inference only: the spike
- * planes go to `workspace`). workspace: spikerl_actor_workspace_bytes(cfg, batch). */
+ * planes go to `workspace`, the encoder's stimulation plane A is not formed and the exact A is
+ * computed only where a spike is possible; spikes and actions are bitwise those of a recording
+ * forward). workspace: spikerl_actor_workspace_bytes(cfg, batch). */
 int spikerl_actor_forward(const spikerl_actor_cfg* cfg, int batch, const float* params,
                           const void* params_bf16, const float* obs, float* actions,
                           spikerl_tape* tape, void* workspace, spikerl_stream_t stream);

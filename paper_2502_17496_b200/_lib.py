@@ -159,6 +159,7 @@ _SIGS = {
     "spikerl_critic_bf16_bytes": (SZ, [C.POINTER(CriticCfg)]),
     "spikerl_actor_tape_bytes": (SZ, [C.POINTER(ActorCfg), I]),
     "spikerl_actor_workspace_bytes": (SZ, [C.POINTER(ActorCfg), I]),
+    "spikerl_actor_workspace_tape_offset": (SZ, [C.POINTER(ActorCfg), I]),
     "spikerl_critic_workspace_bytes": (SZ, [C.POINTER(CriticCfg), I]),
     "spikerl_td3_workspace_bytes": (SZ, [C.POINTER(ActorCfg), C.POINTER(CriticCfg), I]),
     "spikerl_td3_pair_workspace_bytes": (SZ, [C.POINTER(ActorCfg), C.POINTER(CriticCfg), I]),

@@ -180,6 +180,12 @@ class SpikingActor:
     def tape_view(self):
         return tape_view(self.cfg, self.batch, self.tape_buf, 0)
 
+    def inference_tape_view(self):
+        """The tape an inference-only forward (forward(obs, record=False)) left in the workspace (its
+        stimulation plane A is not written)."""
+        off = lib().spikerl_actor_workspace_tape_offset(C.byref(self.cfg), self.batch)
+        return tape_view(self.cfg, self.batch, self.ws, off)
+
     def spikes(self):
         """Host copies of the spike / mask planes as uint8 [T][B][N_l]."""
         return tape_spikes(self.cfg, self.tape_view())

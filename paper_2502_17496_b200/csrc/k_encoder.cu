@@ -30,8 +30,11 @@ constexpr int kEncWarps = kEncThreads / 32;
 
 // dynamic shared memory for R rows and T steps: bit words [T][R][8] + per-warp queues of R*32
 // (entry = row << 5 | lane as u16, and the element's A)
-inline size_t enc_smem_bytes(int R, int T) {
-  return (size_t)T * R * kEncWarps * 4 + (size_t)kEncWarps * R * 32 * (4 + 2);
+// SPK (spikes only): queue entries are the fp64 s - mu (8 B) and the u16 entry; plus per-warp fp64
+// den / 1/den of its 32 neurons
+inline size_t enc_smem_bytes(int R, int T, bool spk = false) {
+  return (size_t)T * R * kEncWarps * 4 + (size_t)kEncWarps * R * 32 * ((spk ? 8 : 4) + 2) +
+         (spk ? (size_t)kEncWarps * 32 * 16 : 0);
 }
 }  // namespace
 
@@ -72,21 +75,31 @@ __device__ __forceinline__ double exp_neg(double z, const ExpCoefs& k) {
 
 // TT > 0: T == TT at compile time (unrolled accumulate-and-fire); TT == 0: runtime T. RR rows per
 // tile (compile time: the tile index math is shifts).
-template <int TT, int RR>
+// SPK (spikes only; forward passes without a backward, e.g. TD3's target actor): A is not stored, so
+// only the elements that can fire need their exact A. An fp32 screen z32 = (s - mu)^2 / (2 sigma^2)
+// against zskip (host-derived, conservative: z32 > zskip implies A < thr for the fp64 A, whatever the
+// fp32 rounding) drops the rest (~90 % with the paper's receptive fields); the survivors are queued
+// per warp with their fp64 s - mu and get the same fp64 A and fire loop as the full kernel, one per
+// lane, so the spikes are bitwise those of the full kernel (tested).
+template <int TT, int RR, bool SPK = false>
 __global__ void __launch_bounds__(kEncThreads) enc_fwd_kernel(int B, int S, int E, int K0, int W0, int T,
                                                               float thr, const float* __restrict__ obs,
                                                               const float* __restrict__ mu,
                                                               const float* __restrict__ sigma,
                                                               float* __restrict__ A_out,
-                                                              uint32_t* __restrict__ bits0) {
+                                                              uint32_t* __restrict__ bits0, float zskip) {
   extern __shared__ __align__(16) unsigned char esm[];
   const int Tn = TT > 0 ? TT : T;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int nw = Tn * RR * kEncWarps;                                              // words of a tile
   uint32_t* w_sh = reinterpret_cast<uint32_t*>(esm);                               // [T][RR][8]
-  float* qA = reinterpret_cast<float*>(w_sh + nw) + warp * RR * 32;                // per-warp queue
-  uint16_t* qe = reinterpret_cast<uint16_t*>(reinterpret_cast<float*>(w_sh + nw) + kEncWarps * RR * 32) +
+  constexpr int QB = SPK ? 8 : 4;                                                  // queue value bytes
+  float* qA = reinterpret_cast<float*>(w_sh + nw) + warp * RR * 32;                // per-warp queue (full)
+  double* qd = reinterpret_cast<double*>(w_sh + nw) + warp * RR * 32;              // per-warp queue (SPK)
+  uint16_t* qe = reinterpret_cast<uint16_t*>(reinterpret_cast<unsigned char*>(w_sh + nw) + kEncWarps * RR * 32 * QB) +
                  warp * RR * 32;
+  double* nk_sh = reinterpret_cast<double*>(reinterpret_cast<unsigned char*>(w_sh + nw) +
+                                            kEncWarps * RR * 32 * (QB + 2)) + warp * 64;   // SPK: den, inv of 32 lanes
   const uint32_t lt = (1u << lane) - 1u;
   const int k = blockIdx.y * kEncThreads + tid;
   const bool kv = k < K0;
@@ -102,6 +115,12 @@ __global__ void __launch_bounds__(kEncThreads) enc_fwd_kernel(int B, int S, int 
   const double inv = __ddiv_rn(1.0, den);
   ExpCoefs kx;
   kx.load();
+  const float m32 = kv ? __ldg(mu + k) : 0.0f, inv32 = (float)inv;
+  if constexpr (SPK) {
+    nk_sh[lane] = den;
+    nk_sh[32 + lane] = inv;
+    __syncwarp();
+  }
   // the observation values of a tile are requested one tile ahead (ncu r02: loaded at the tile
   // start, their latency was the kernel's top stall); rows past B read row B - 1 and are not stored
   const float* op = obs + i;
@@ -118,9 +137,47 @@ __global__ void __launch_bounds__(kEncThreads) enc_fwd_kernel(int B, int S, int 
     // neurons / rows compute on clamped inputs and only their stores are predicated off (no
     // divergent branch around the fp64 chain).
     int cnt = 0;
+    if constexpr (SPK) {
+      // fp32 screen; survivors queued with their fp64 s - mu
+#pragma unroll
+      for (int r = 0; r < RR; ++r) {
+        const float d32 = __fsub_rn(sv[r], m32);
+        const bool need = kv && b0 + r < B && !(__fmul_rn(__fmul_rn(d32, d32), inv32) > zskip);
+        const uint32_t bal = __ballot_sync(0xffffffffu, need);
+        if (need) {
+          const int j = cnt + __popc(bal & lt);
+          qd[j] = __dsub_rn((double)sv[r], m);
+          qe[j] = (uint16_t)((r << 5) | lane);
+        }
+        cnt += __popc(bal);
+      }
+      __syncwarp();
+      // the exact A of each survivor (its own neuron's constants) and, where A >= thr, the fire loop
+      for (int j = lane; j < cnt; j += 32) {
+        const int e = qe[j];
+        const double dd = qd[j], dn = nk_sh[e & 31], iv = nk_sh[32 + (e & 31)];
+        const double q = __dmul_rn(dd, dd);
+        const double q0 = __dmul_rn(q, iv);
+        const double rr = __fma_rn(-q0, dn, q);
+        const float A = (float)exp_neg(__fma_rn(rr, iv, q0), kx);
+        if (A >= thr) {
+          const uint32_t bit = 1u << (e & 31);
+          uint32_t* wp = w_sh + (e >> 5) * kEncWarps + warp;
+          float acc = 0.0f;
+#pragma unroll
+          for (int st = 0; st < (TT > 0 ? TT : Tn); ++st) {
+            acc = __fadd_rn(acc, A);
+            if (acc >= 1.0f) {
+              acc = __fsub_rn(acc, 1.0f);
+              atomicOr(wp + st * RR * kEncWarps, bit);
+            }
+          }
+        }
+      }
+    }
     float* ap = A_out + (size_t)b0 * K0 + k;
 #pragma unroll
-    for (int r = 0; r < RR; ++r, ap += K0) {
+    for (int r = 0; r < RR && !SPK; ++r, ap += K0) {
       const bool live = kv && b0 + r < B;
       const double dd = __dsub_rn((double)sv[r], m);
       const double q = __dmul_rn(dd, dd);
@@ -145,7 +202,7 @@ __global__ void __launch_bounds__(kEncThreads) enc_fwd_kernel(int B, int S, int 
     // per lane, each spike OR-ed into its (t, row) word of the warp (shared atomics). ncu r02: a
     // branch-free variant that assembled whole words per lane from T-bit trains was 45 % slower
     // (dependent shared loads)
-    for (int j = lane; j < cnt; j += 32) {
+    for (int j = lane; j < cnt && !SPK; j += 32) {
       const float A = qA[j];
       const int e = qe[j];
       const uint32_t bit = 1u << (e & 31);
@@ -179,15 +236,15 @@ __global__ void __launch_bounds__(kEncThreads) enc_fwd_kernel(int B, int S, int 
   }
 }
 
-template <int TT, int RR>
-static int enc_launch(cudaStream_t st, const ActorDims& d, int B, float thr, const float* obs, const float* mu,
-                      const float* sigma, float* A, uint32_t* bits0) {
-  const size_t smem = enc_smem_bytes(RR, d.T);
+template <int TT, int RR, bool SPK>
+static int enc_launch(cudaStream_t st, const ActorDims& d, int B, float thr, float zskip, const float* obs,
+                      const float* mu, const float* sigma, float* A, uint32_t* bits0) {
+  const size_t smem = enc_smem_bytes(RR, d.T, SPK);
   if (smem > 160 * 1024) { set_error("encoder: T = %d too long for the shared tile", d.T); return SPIKERL_E_UNSUPPORTED; }
-  SPK_SMEM_ATTR((enc_fwd_kernel<TT, RR>), 160 * 1024);   // an upper bound; each launch asks for its own size
+  SPK_SMEM_ATTR((enc_fwd_kernel<TT, RR, SPK>), 160 * 1024);   // an upper bound; each launch asks for its own size
   // one wave of resident blocks (a second partial wave of row-walking blocks would double the time)
   int per_sm = 0;
-  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, enc_fwd_kernel<TT, RR>, kEncThreads, smem) !=
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, enc_fwd_kernel<TT, RR, SPK>, kEncThreads, smem) !=
           cudaSuccess || per_sm < 1) {
     cudaGetLastError();
     per_sm = 1;
@@ -196,27 +253,41 @@ static int enc_launch(cudaStream_t st, const ActorDims& d, int B, float thr, con
   int bx = num_sms() * per_sm / ky;
   if (bx > cdiv(B, RR)) bx = cdiv(B, RR);
   if (bx < 1) bx = 1;
-  pdl((enc_fwd_kernel<TT, RR>), dim3((unsigned)bx, (unsigned)ky), kEncThreads, smem, st)(
-      B, d.S, d.E, d.K0, d.Wd[0], d.T, thr, obs, mu, sigma, A, bits0);
+  pdl((enc_fwd_kernel<TT, RR, SPK>), dim3((unsigned)bx, (unsigned)ky), kEncThreads, smem, st)(
+      B, d.S, d.E, d.K0, d.Wd[0], d.T, thr, obs, mu, sigma, A, bits0, zskip);
   return SPIKERL_OK;
 }
 
+// A == NULL: spikes only (no stimulation plane; see enc_fwd_kernel's SPK)
 int launch_enc_fwd(const ActorDims& d, int B, const float* obs, const float* mu, const float* sigma,
                    float* A, uint32_t* bits0, cudaStream_t st) {
-  ProfScope ps_("enc_fwd", PB_HBM, 0.0, 4.0 * B * (d.S + d.K0 + (double)d.T * d.Wd[0]), st);
+  ProfScope ps_(A ? "enc_fwd" : "enc_fwd_spikes", PB_HBM, 0.0,
+                4.0 * B * (d.S + (A ? d.K0 : 0) + (double)d.T * d.Wd[0]), st);
   // no-fire bound (see the file header), rounded down to fp32
   const double thr64 = 1.0 / ((double)d.T * (1.0 + (double)d.T * 0x1p-22));
   float thr = (float)thr64;
   if ((double)thr > thr64) thr = nextafterf(thr, 0.0f);
+  // spikes-only screen: z32 > zskip implies A < thr. A = RN32(exp64(-z64)) < thr once the exact z
+  // exceeds -ln(thr) + 2^-23; z32 (three fp32 roundings of (s - mu)^2 / (2 sigma^2)) is within
+  // 6 * 2^-24 relative of the exact z; both margins are taken ~10x wide, and zskip rounded up
+  const double zs64 = (-log((double)thr) + 1e-6) * (1.0 + 1e-6);
+  float zskip = (float)zs64;
+  if ((double)zskip < zs64) zskip = nextafterf(zskip, INFINITY);
   // 8 rows per tile for the compiled T (a T = 32 tile is ~20 KB: eight resident blocks); 2 rows
   // for any other T (up to 255: 16 KB of words)
   switch (d.T) {
-#define SPK_ENC_T(n) \
-  case n: SPK_TRY((enc_launch<n, 8>(st, d, B, thr, obs, mu, sigma, A, bits0))); break;
+#define SPK_ENC_T(n)                                                                                    \
+  case n:                                                                                               \
+    if (A) SPK_TRY((enc_launch<n, 8, false>(st, d, B, thr, zskip, obs, mu, sigma, A, bits0)));          \
+    else SPK_TRY((enc_launch<n, 8, true>(st, d, B, thr, zskip, obs, mu, sigma, A, bits0)));             \
+    break;
     SPK_ENC_T(1) SPK_ENC_T(2) SPK_ENC_T(3) SPK_ENC_T(4) SPK_ENC_T(5) SPK_ENC_T(8) SPK_ENC_T(10) SPK_ENC_T(16)
     SPK_ENC_T(32)
 #undef SPK_ENC_T
-    default: SPK_TRY((enc_launch<0, 2>(st, d, B, thr, obs, mu, sigma, A, bits0))); break;
+    default:
+      if (A) SPK_TRY((enc_launch<0, 2, false>(st, d, B, thr, zskip, obs, mu, sigma, A, bits0)));
+      else SPK_TRY((enc_launch<0, 2, true>(st, d, B, thr, zskip, obs, mu, sigma, A, bits0)));
+      break;
   }
   SPK_LAUNCHED();
   return SPIKERL_OK;

@@ -225,11 +225,15 @@ static ActorWs actor_ws_layout(const ActorDims& d, int B) {
   return w;
 }
 
+// spikes_only: a forward no backward will read (inference, TD3's target actor): the encoder skips the
+// stimulation plane A and computes the exact A only where a spike is possible (enc_fwd_kernel SPK);
+// spike planes, counts and actions are bitwise those of the recording forward (tested)
 static int actor_forward_impl(const ActorDims& d, int B, const float* params,
                               const __nv_bfloat16* pb16, const float* obs, float* actions,
-                              char* tape, cudaStream_t st, const TargetSmooth* smooth = nullptr) {
+                              char* tape, cudaStream_t st, const TargetSmooth* smooth = nullptr,
+                              bool spikes_only = false) {
   const TapeLayout L = tape_layout(d, B);
-  float* A = (float*)(tape + L.A);
+  float* A = spikes_only ? nullptr : (float*)(tape + L.A);
   uint32_t* bits[4];
   uint32_t* mask[4];
   for (int l = 0; l < 4; ++l) { bits[l] = (uint32_t*)(tape + L.bits[l]); mask[l] = (uint32_t*)(tape + L.mask[l]); }
@@ -507,6 +511,12 @@ size_t spikerl_actor_workspace_bytes(const spikerl_actor_cfg* cfg, int batch) {
   return actor_ws_layout(d, batch).total;
 }
 
+size_t spikerl_actor_workspace_tape_offset(const spikerl_actor_cfg* cfg, int batch) {
+  ActorDims d;
+  if (actor_dims(cfg, &d) != SPIKERL_OK || batch < 1) return 0;
+  return actor_ws_layout(d, batch).tape;
+}
+
 size_t spikerl_critic_workspace_bytes(const spikerl_critic_cfg* cfg, int batch) {
   CriticDims d;
   if (critic_dims(cfg, &d) != SPIKERL_OK || batch < 1) return 0;
@@ -583,7 +593,7 @@ int spikerl_actor_forward(const spikerl_actor_cfg* cfg, int batch, const float* 
     tp = (char*)workspace + actor_ws_layout(d, batch).tape;
   }
   SPK_TRY(actor_forward_impl(d, batch, params, (const __nv_bfloat16*)params_bf16, obs, actions, tp,
-                             (cudaStream_t)stream));
+                             (cudaStream_t)stream, nullptr, tape == nullptr));
   if (tape) {
     tape->magic = kTapeMagic;
     tape->cfg_hash = actor_cfg_hash(cfg);
@@ -764,7 +774,7 @@ int spikerl_td3_update(const spikerl_actor_cfg* acfg, const spikerl_critic_cfg* 
   SPK_TRY(stream_after(sA, st, aux->ev[0]));
   {
     const TargetSmooth ts{noise, hp->policy_noise, hp->noise_clip, seed, rank, b->rng_counter, ctr_snap, at, 1};
-    SPK_TRY(actor_forward_impl(ad, B, b->actor_t, atbf, s2, a2, aws + actor_ws_layout(ad, B).tape, sA, &ts));
+    SPK_TRY(actor_forward_impl(ad, B, b->actor_t, atbf, s2, a2, aws + actor_ws_layout(ad, B).tape, sA, &ts, true));
   }
   SPK_TRY(critic_fwd_bwd(cd, B, b->critic_t, ctbf, s2, ad.S, at, ad.A, nullptr, qt, nullptr, nullptr, nullptr, 0.f,
                          2, cws_t, sA));
@@ -911,7 +921,7 @@ int spikerl_td3_update_pair(const spikerl_actor_cfg* acfg, const spikerl_critic_
     SPK_TRY(stream_after(sA[i], st, aux->ev[i == 0 ? 0 : 6]));
     const TargetSmooth ts{noise ? noise + (size_t)i * B * ad.A : nullptr, hp->policy_noise, hp->noise_clip, seed,
                           rank, b->rng_counter, x.snap, x.at, i == 1 ? 1 : 0};
-    SPK_TRY(actor_forward_impl(ad, B, b->actor_t, atbf, x.s2, x.a2, x.aws + actor_ws_layout(ad, B).tape, sA[i], &ts));
+    SPK_TRY(actor_forward_impl(ad, B, b->actor_t, atbf, x.s2, x.a2, x.aws + actor_ws_layout(ad, B).tape, sA[i], &ts, true));
     SPK_TRY(critic_fwd_bwd(cd, B, b->critic_t, ctbf, x.s2, ad.S, x.at, ad.A, nullptr, x.qt, nullptr, nullptr, nullptr,
                            0.f, 2, x.cws_t, sA[i]));
     SPK_CHECK_CUDA(cudaEventRecord(evA[i], sA[i]));

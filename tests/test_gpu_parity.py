@@ -66,6 +66,54 @@ def test_encoder_quotient_stress():
     assert check_encoder(gpu, shape, p, s) == 0
 
 
+@pytest.mark.parametrize("case", ["cfg1", "cfg3L", "cfg4_512", "cfg0", "T7", "T33", "stress"])
+def test_inference_forward_spikes_only(case):
+    """The inference-only forward (tape == NULL; TD3's target actor) skips the stimulation plane and
+    forms the exact A only where the fp32 screen z32 <= zskip says a spike is possible
+    (enc_fwd_kernel SPK): its spike / window planes, counts and actions equal the recording
+    forward's bit for bit, and its encoder spikes the oracle's — also over the wide sigma / mu
+    spread of the quotient stress case, where the screen's margins are tightest."""
+    import torch
+    import paper_2502_17496_b200 as pk
+    from tests._parity import check_encoder
+    engine = "auto"
+    if case == "stress":
+        shape = sg.ActorShape(3, 2, pop_enc=64, pop_dec=4, n1=32, n2=32, T=16, precision="bf16")
+        rng = np.random.default_rng(12)
+        p = sg.actor_params(shape, rng)
+        p["sigma"] = np.exp(rng.uniform(np.log(1e-3), np.log(30.0), p["sigma"].shape)).astype(np.float32)
+        p["mu"] = rng.normal(0, 3, p["mu"].shape).astype(np.float32)
+        B = 2048
+        s = rng.normal(0, 3, (B, 3)).astype(np.float32)
+        engine = "simt"
+    else:
+        name, B = {"cfg1": ("cfg1", None), "cfg3L": ("cfg3L", 4096), "cfg4_512": ("cfg4", 512), "cfg0": ("cfg0", None),
+                   "T7": ("cfg2", 96), "T33": ("cfg2", 45)}[case]
+        shape, _, B0 = sg.preset(name)
+        B = B or B0
+        if case == "T7":
+            shape, engine = sg.with_(shape, T=7), "simt"
+        if case == "T33":
+            shape, engine = sg.with_(shape, T=33), "simt"
+        p, s, _ = _inputs(shape, B, seed=21)
+    actor = pk.SpikingActor(pk.actor_cfg_from(shape, engine=engine), B)
+    actor.load(p)
+    obs = torch.from_numpy(np.ascontiguousarray(s)).cuda()
+    a_rec = actor.forward(obs).clone()
+    sp_rec = actor.spikes()
+    cnt_rec = actor.tape_view()["counts"].clone()
+    a_inf = actor.forward(obs, record=False).clone()
+    tv = actor.inference_tape_view()
+    sp_inf = pk.tape_spikes(actor.cfg, tv)
+    torch.cuda.synchronize()
+    assert torch.equal(a_rec, a_inf)
+    assert torch.equal(cnt_rec, tv["counts"])
+    for k in sp_rec:
+        assert np.array_equal(sp_rec[k], sp_inf[k]), k
+    gpu = dict(sp=sp_inf, A=None)
+    assert check_encoder(gpu, shape, p, s, a_stored=False) == 0
+
+
 @pytest.mark.parametrize("T", [7, 32, 33, 70])
 def test_encoder_timesteps(T):
     """Unrolled (T in the compiled set) and runtime-T (chunks of 32 steps) encoder variants."""

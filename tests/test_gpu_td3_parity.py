@@ -137,7 +137,8 @@ def run_td3_teacher_forced(preset, prec, B=None, nsteps=2, seed=7):
         # ---- target path (a2): pi'(s') teacher forced on the GPU's target tape
         at_pre = _actor(pk, td3, pre["actor_t"])
         st["target"] = check_actor(_gpu_actor_view(pk, td3, ws["tape_target"], ws["a2"]), shape,
-                                   {kk: v.astype(np.float32) for kk, v in at_pre.items()}, batch["s2"], None)
+                                   {kk: v.astype(np.float32) for kk, v in at_pre.items()}, batch["s2"], None,
+                                   a_stored=False)   # the target forward is spikes-only
         a2 = _f64(ws["a2"])
         at_ref = np.clip(a2 + np.clip(eps.astype(np.float64), -hp.noise_clip, hp.noise_clip), -1.0, 1.0)
         at = _f64(ws["at"])
