@@ -438,6 +438,41 @@ def test_critic_tcgen05_small_and_ragged_subprocess():
     assert r.returncode == 0 and "tc critic ok" in r.stdout, r.stdout[-2000:] + r.stderr[-2000:]
 
 
+@pytest.mark.parametrize("name,B", [("cfg1", 256), ("cfg3L", 4096)])
+def test_td3_schedule_independent_subprocess(name, B):
+    """The TD3 update-pair DAG's scheduling switches change streams, priorities and launch edges only:
+    four update pairs (captured graphs) end in bitwise identical actor / critic / target parameters and
+    Adam moments under the default schedule, SPIKERL_TD3_SERIAL=1 (one stream), SPIKERL_TD3_PRIO=0 / 5
+    (no / raised launch priority) and SPIKERL_PDL=0 (no programmatic dependent launch)."""
+    import os, subprocess, sys
+    code = (
+        "import hashlib, numpy as np, torch\n"
+        "import synthgen as sg, paper_2502_17496_b200 as pk\n"
+        f"shape, _, _ = sg.preset({name!r}); B = {B}\n"
+        "S, A = shape.obs_dim, shape.act_dim\n"
+        "rng = np.random.default_rng(3)\n"
+        "cs = sg.CriticShape(S + A, precision='bf16')\n"
+        "td3 = pk.TD3(pk.actor_cfg_from(shape), pk.critic_cfg(S + A), pk.td3_cfg(B), pk.replay_fill(4 * B, S, A, seed=4), seed=6)\n"
+        "td3.load(sg.actor_params(shape, rng), sg.critic_params(cs, rng), sg.critic_params(cs, rng))\n"
+        "td3.update_pair(1)\n"
+        "td3.capture_pair()\n"
+        "for _ in range(4): td3.replay_pair()\n"
+        "torch.cuda.synchronize()\n"
+        "h = hashlib.sha256()\n"
+        "for t in (td3.actor, td3.actor_t, td3.critic, td3.critic_t, td3.m_actor, td3.v_actor, td3.m_critic, td3.v_critic):\n"
+        "    h.update(t.cpu().numpy().tobytes())\n"
+        "print('digest', h.hexdigest())\n")
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    digests = {}
+    for label, extra in (("default", {}), ("serial", {"SPIKERL_TD3_SERIAL": "1"}), ("prio0", {"SPIKERL_TD3_PRIO": "0"}),
+                         ("prio5", {"SPIKERL_TD3_PRIO": "5"}), ("nopdl", {"SPIKERL_PDL": "0"})):
+        r = subprocess.run([sys.executable, "-c", code], cwd=root, capture_output=True, text=True, timeout=600,
+                           env=dict(os.environ, PYTHONPATH=root, **extra))
+        assert r.returncode == 0, (label, r.stdout[-1500:] + r.stderr[-1500:])
+        digests[label] = [l for l in r.stdout.splitlines() if l.startswith("digest")][-1]
+    assert len(set(digests.values())) == 1, digests
+
+
 @pytest.mark.parametrize("obs,act", [(17, 6), (111, 8)])
 def test_td3_bf16_copies_track_masters(obs, act):
     """Adam / Polyak write the bf16 working copies in place (Bf16Views): after several updates they
