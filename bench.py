@@ -562,6 +562,9 @@ def run_td3(args, rank, world, workload):
         d = [e for e in summ if e["name"] == dom][0]
         live = (d["launches"], d["total_ms"])
     out["roofline"] = dominant_kernel(summ, peaks(), live, total_ms)
+    iso = isolated_actor_kernel(td3, B, out["roofline"])
+    if iso:
+        out["roofline"]["isolated"] = iso
     if not pair or watched_graph is None:
         out["roofline"]["timing"] = "eager profiling pass (events around every launch); diagnostic run"
     else:
@@ -572,6 +575,45 @@ def run_td3(args, rank, world, workload):
                                      "interval includes sharing the GPU with the kernels overlapping it")
     out["kernel_breakdown"] = _breakdown(summ)
     return out
+
+
+def isolated_actor_kernel(td3, B, roof):
+    """Context for a dominant actor kernel of a TD3 DAG, whose live interval includes sharing the GPU
+    with the concurrent branches: the same kernel's mean duration when nothing else runs (an actor of
+    the same shape and parameters, eager forward + backward on one stream, events around every
+    launch, after one warm-up pass)."""
+    import torch
+    import paper_2502_17496_b200 as pk
+    from paper_2502_17496_b200 import _lib
+    name = roof.get("kernel", "")
+    if not (name.startswith("lif_") or name.startswith("enc_")) or roof.get("bound") != "tensor":
+        return None
+    actor = pk.SpikingActor(td3.acfg, B)
+    actor.params.copy_(td3.actor)
+    actor.refresh()
+    g = torch.Generator(device="cuda").manual_seed(1)
+    obs = torch.clamp(torch.randn(B, td3.acfg.obs_dim, device="cuda", generator=g), -5, 5)
+    ga = torch.randn(B, td3.acfg.act_dim, device="cuda", generator=g)
+
+    def fb():
+        for _ in range(3):
+            actor.forward(obs)
+            actor.backward(obs, ga)
+    fb()
+    torch.cuda.synchronize()
+    _lib.prof_enable(True)
+    fb()
+    torch.cuda.synchronize()
+    summ = _lib.prof_summary()
+    _lib.prof_enable(False)
+    e = [x for x in summ if x["name"] == name]
+    if not e:
+        return None
+    avg_s = e[0]["total_ms"] / e[0]["launches"] / 1e3
+    ach = roof["work_per_launch"] / avg_s / 1e12
+    return {"avg_launch_us": round(avg_s * 1e6, 3), "achieved": round(ach, 3), "frac": round(ach / roof["peak"], 5),
+            "how": "the same kernel alone: an actor of this shape and these parameters, eager forward + backward on "
+                   "one stream, CUDA events around each launch (context; the live figure above is the DAG's)"}
 
 
 def e2e_td3(args, rank, world, td3_dev, shape, B, pair=False):
