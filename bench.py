@@ -944,6 +944,38 @@ def hbm_kernels(actor, summ, reps=20):
         res[name] = {"achieved": round(gbs, 1), "unit": "GB/s", "peak": pk_peaks["hbm_gbs"],
                      "frac": round(gbs / pk_peaks["hbm_gbs"], 4), "bytes_per_launch": bpp * n,
                      "us_per_launch": round(us, 2), "params": n}
+    # the standalone forward-scan ablation (SURVEY D-2) at the configs[4] hidden-layer size: reads the
+    # fp32 currents [T][B][N] the fused FWD epilogue never writes, writes the spike / window planes
+    T, B, N = actor.cfg.T, actor.batch, actor.cfg.hidden2
+    W = (N + 31) // 32
+    cur = torch.randn(T * B * N, **f32) * 0.5
+    planes = torch.zeros(2, T * B * W, dtype=torch.int32, device="cuda")
+    stream = torch.cuda.current_stream().cuda_stream
+
+    def scan():
+        rc = pk.lib().spikerl_lif_scan_forward(cur.data_ptr(), T, B, N, actor.cfg.d_c, actor.cfg.d_v, actor.cfg.v_th,
+                                               actor.cfg.surr_window, planes[0].data_ptr(), planes[1].data_ptr(),
+                                               stream)
+        assert rc == 0, rc
+    scan()
+    tot = 0.0
+    for _ in range(reps // 4):
+        l2_flush(flush)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        scan()
+        e1.record()
+        torch.cuda.synchronize()
+        tot += e0.elapsed_time(e1)
+    us = tot / (reps // 4) * 1e3
+    nbytes = float(T) * B * (4 * N + 8 * W)
+    gbs = nbytes / (us / 1e6) / 1e9
+    res["lif_scan_ablation"] = {"achieved": round(gbs, 1), "unit": "GB/s", "peak": pk_peaks["hbm_gbs"],
+                                "frac": round(gbs / pk_peaks["hbm_gbs"], 4), "bytes_per_launch": nbytes,
+                                "us_per_launch": round(us, 2), "shape": [T, B, N],
+                                "what": "standalone forward LIF scan over fp32 currents (the ablation of the "
+                                        "fused FWD epilogue, which never writes them)"}
+    del cur, planes
     return res
 
 

@@ -249,6 +249,14 @@ int spikerl_adam(float* params, const float* grads, float* m, float* v, size_t n
 int spikerl_polyak(float* target, const float* source, size_t n, float tau,
                    spikerl_stream_t stream);
 
+/* Standalone forward LIF scan over precomputed input currents (north_star LIF equations;
+ * SPEC.md:141-149; R7): an ablation / diagnostic kernel showing what the
+ * fused FWD epilogue saves — the product path never materialises the currents. I [T][B][N] fp32
+ * (device); bits / mask [T][B][ceil(N/32)] u32 (device, caller-owned): spike o_t and window
+ * h_t = [|v_t - V_th| < window] planes, bit n % 32 of word n / 32. Errors: E_ARG on null / empty. */
+int spikerl_lif_scan_forward(const float* I, int T, int B, int N, float d_c, float d_v, float v_th,
+                             float window, uint32_t* bits, uint32_t* mask, spikerl_stream_t stream);
+
 /* ------------------------------------------------------------------------------------------
  * TD3 update (one step k). All buffers caller-owned.
  * ---------------------------------------------------------------------------------------- */

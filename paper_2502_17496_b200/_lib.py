@@ -174,6 +174,7 @@ _SIGS = {
     "spikerl_critic_fwd_bwd": (I, [C.POINTER(CriticCfg), I, P, P, P, I, P, I, P, P, P, P, P, F, P, P]),
     "spikerl_adam": (I, [P, P, P, P, SZ, P, F, F, F, F, SZ, SZ, F, P]),
     "spikerl_polyak": (I, [P, P, SZ, F, P]),
+    "spikerl_lif_scan_forward": (I, [P, I, I, I, F, F, F, F, P, P, P]),
     "spikerl_td3_update": (I, [C.POINTER(ActorCfg), C.POINTER(CriticCfg), C.POINTER(TD3Cfg),
                                C.POINTER(TD3Bufs), LL, ULL, P, P, P, P, P, P]),
     "spikerl_td3_update_pair": (I, [C.POINTER(ActorCfg), C.POINTER(CriticCfg), C.POINTER(TD3Cfg),

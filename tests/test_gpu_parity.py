@@ -114,6 +114,40 @@ def test_inference_forward_spikes_only(case):
     assert check_encoder(gpu, shape, p, s, a_stored=False) == 0
 
 
+@pytest.mark.parametrize("T,B,N", [(5, 37, 45), (16, 64, 256), (7, 3, 33), (33, 5, 70)])
+def test_lif_scan_ablation(T, B, N):
+    """The standalone forward-scan ablation kernel (spikerl_lif_scan_forward) against
+    the oracle's LIF layer (north_star equations), teacher forced on the kernel's own
+    reset decisions: a spike or window bit may differ only within 1e-5 of V_th or of a window edge
+    (the kernel scans the fp32-rounded currents, the oracle the fp64 ones)."""
+    import torch
+    import paper_2502_17496_b200 as pk
+    shape = sg.preset("cfg1")[0]
+    rng = np.random.default_rng(T * 1000 + N)
+    K = 40
+    o_in = (rng.random((T, B, K)) < 0.3).astype(np.uint8)
+    Wt = rng.normal(0, 0.6, (N, K))
+    _, _, I = oracle.lif_layer_forward(o_in, Wt, shape.d_c, shape.d_v, shape.v_th)
+    W = (N + 31) // 32
+    Id = torch.from_numpy(I.astype(np.float32)).cuda().contiguous()
+    bits = torch.zeros(T, B, W, dtype=torch.int32, device="cuda")
+    mask = torch.zeros(T, B, W, dtype=torch.int32, device="cuda")
+    lib = pk.lib()
+    rc = lib.spikerl_lif_scan_forward(Id.data_ptr(), T, B, N, shape.d_c, shape.d_v, shape.v_th, shape.surr_window,
+                                      bits.data_ptr(), mask.data_ptr(), torch.cuda.current_stream().cuda_stream)
+    assert rc == 0, rc
+    torch.cuda.synchronize()
+    O = pk.unpack_bits(bits, N)
+    H = pk.unpack_bits(mask, N)
+    V, O_ref, _ = oracle.lif_layer_forward(o_in, Wt, shape.d_c, shape.d_v, shape.v_th, forced_o=O)
+    near = np.abs(V - shape.v_th) < 1e-5
+    assert not np.any((O.astype(bool) != O_ref.astype(bool)) & ~near)
+    h_ref = np.abs(V - shape.v_th) < shape.surr_window
+    near_h = np.minimum(np.abs(V - (shape.v_th - shape.surr_window)), np.abs(V - (shape.v_th + shape.surr_window))) < 1e-5
+    assert not np.any((H.astype(bool) != h_ref) & ~near_h)
+    assert O.any() and (~O.astype(bool)).any()
+
+
 @pytest.mark.parametrize("T", [7, 32, 33, 70])
 def test_encoder_timesteps(T):
     """Unrolled (T in the compiled set) and runtime-T (chunks of 32 steps) encoder variants."""
