@@ -298,7 +298,7 @@ __device__ __forceinline__ void tma3(const CUtensorMap* m, void* dst, uint64_t* 
 }
 }  // namespace osc
 
-template <typename GTy, int TT>
+template <typename GTy, int TT, bool RHO = false>   // RHO: rho = 1 (v3 read), its own instantiation
 __global__ void __launch_bounds__(256, 4) dec_bwd_outscan_tma_kernel(
     const __grid_constant__ CUtensorMap map_o, const __grid_constant__ CUtensorMap map_h, int B, int T, int A,
     int D, int N3, int W3, int NO, int R, int planeS, float dcc, float dvc, float zh,
@@ -411,13 +411,14 @@ __global__ void __launch_bounds__(256, 4) dec_bwd_outscan_tma_kernel(
       for (int t = T - 1; t >= 0; --t) {
         const uint32_t o8 = (so[t * tstr] >> sh) & 0xFFu, h8 = (sm[t * tstr] >> sh) & 0xFFu;
         float G[8], vv[8];
-        if (v3) {   // rho = 1: v_t of the 8 neurons (same element offsets as G3)
+        if constexpr (RHO) {   // rho = 1: v_t of the 8 neurons (same element offsets as G3)
           const float4 a = reinterpret_cast<const float4*>(v3 + go)[0], c = reinterpret_cast<const float4*>(v3 + go)[1];
           vv[0] = a.x; vv[1] = a.y; vv[2] = a.z; vv[3] = a.w; vv[4] = c.x; vv[5] = c.y; vv[6] = c.z; vv[7] = c.w;
         }
 #pragma unroll
         for (int i = 0; i < 8; ++i) {
-          const float gi = v3 ? __fmaf_rn(-__fmul_rn(zdv, vv[i]), dvn[i], g[i]) : g[i];
+          float gi = g[i];
+          if constexpr (RHO) gi = __fmaf_rn(-__fmul_rn(zdv, vv[i]), dvn[i], g[i]);
           const float hg = ((h8 >> i) & 1u) ? gi : 0.0f;
           const float dvt = ((o8 >> i) & 1u) ? hg : __fmaf_rn(dvc, dvn[i], hg);
           const float dct = __fmaf_rn(dcc, dcn[i], dvt);
@@ -483,6 +484,10 @@ int launch_dec_bwd_outscan(const ActorDims& d, int B, const float* grad_a, const
       SPK_LAUNCHED();
       return SPIKERL_OK;
     };
+    if (v3) {   // rho = 1 (bf16 / fp32 operands; fp16 is rejected at configuration)
+      if (d.bf16) return launch(dec_bwd_outscan_tma_kernel<__nv_bfloat16, 0, true>, (__nv_bfloat16*)G3);
+      return launch(dec_bwd_outscan_tma_kernel<float, 0, true>, (float*)G3);
+    }
     if (d.f16) {
       if (d.T == 16) return launch(dec_bwd_outscan_tma_kernel<__half, 16>, (__half*)G3);
       if (d.T == 5) return launch(dec_bwd_outscan_tma_kernel<__half, 5>, (__half*)G3);
