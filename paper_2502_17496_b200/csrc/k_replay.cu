@@ -23,14 +23,19 @@ __global__ void replay_gather_kernel(int B, int S, int A, const float* __restric
   pdl_wait();
   pdl_trigger();
   const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
-  if (blockIdx.x == 0 && threadIdx.x < gs.n && gs.snap[threadIdx.x])
-    *gs.snap[threadIdx.x] = *counter + threadIdx.x;
+  if (blockIdx.x == 0 && threadIdx.x < gs.n) {
+    unsigned long long* const sn = threadIdx.x ? gs.snap[1] : gs.snap[0];
+    if (sn) *sn = *counter + threadIdx.x;
+  }
   if (warp >= gs.n * B) return;
   const int slot = warp / B, row = warp - slot * B;
+  // slot pointers by selection (a runtime-indexed kernel-parameter array goes through local memory)
+  const bool s1 = slot != 0;
+  const long long* const idx = s1 ? gs.idx[1] : gs.idx[0];
   long long i = 0;
   if (lane == 0) {
-    if (gs.idx[slot]) {
-      i = gs.idx[slot][row];
+    if (idx) {
+      i = idx[row];
     } else {
       const unsigned long long ctr = *counter + slot;
       const uint4 x = Philox::gen(make_uint4((uint32_t)row, P_INDEX, (uint32_t)ctr, (uint32_t)(ctr >> 32)),
@@ -40,15 +45,34 @@ __global__ void replay_gather_kernel(int B, int S, int A, const float* __restric
     }
   }
   i = __shfl_sync(0xffffffffu, i, 0);
-  float* const s = gs.s[slot]; float* const s2 = gs.s2[slot]; float* const a = gs.a[slot];
-  for (int c = lane; c < S; c += 32) {
-    s[(size_t)row * S + c] = rs[(size_t)i * S + c];
-    s2[(size_t)row * S + c] = rs2[(size_t)i * S + c];
+  float* const s = s1 ? gs.s[1] : gs.s[0];
+  float* const s2 = s1 ? gs.s2[1] : gs.s2[0];
+  float* const a = s1 ? gs.a[1] : gs.a[0];
+  const float* const src_s = rs + (size_t)i * S;
+  const float* const src_s2 = rs2 + (size_t)i * S;
+  float* const dst_s = s + (size_t)row * S;
+  float* const dst_s2 = s2 + (size_t)row * S;
+  // 16-byte copies when the rows are 16-byte aligned (S % 4 == 0 and aligned bases: configs[3]'s 376)
+  if (((S & 3) | (((uintptr_t)rs | (uintptr_t)rs2 | (uintptr_t)s | (uintptr_t)s2) & 15)) == 0) {
+    const float4* ps = reinterpret_cast<const float4*>(src_s);
+    const float4* ps2 = reinterpret_cast<const float4*>(src_s2);
+    float4* qs = reinterpret_cast<float4*>(dst_s);
+    float4* qs2 = reinterpret_cast<float4*>(dst_s2);
+    for (int c = lane; c < (S >> 2); c += 32) {
+      const float4 x = __ldg(ps + c), y = __ldg(ps2 + c);
+      qs[c] = x;
+      qs2[c] = y;
+    }
+  } else {
+    for (int c = lane; c < S; c += 32) {
+      dst_s[c] = src_s[c];
+      dst_s2[c] = src_s2[c];
+    }
   }
   for (int c = lane; c < A; c += 32) a[(size_t)row * A + c] = ra[(size_t)i * A + c];
   if (lane == 0) {
-    gs.r[slot][row] = rr[i];
-    gs.d[slot][row] = rd[i];
+    (s1 ? gs.r[1] : gs.r[0])[row] = rr[i];
+    (s1 ? gs.d[1] : gs.d[0])[row] = rd[i];
   }
 }
 

@@ -710,7 +710,7 @@ __global__ void __launch_bounds__(n_threads(X6), 1)
 #pragma unroll
           for (int qi = 0; qi < NQ; ++qi) { qo[qi] = 0ull; qh[qi] = 0ull; }
           // TMEM loads of CH timesteps are issued together and waited once
-          constexpr int CH = HB >= 16 ? 2 : (HB >= 8 ? 4 : 8);
+          constexpr int CH = HB >= 16 ? 1 : (HB >= 8 ? 4 : 8);
           for (int t0 = 0; t0 < p.T; t0 += CH) {
             uint32_t rr[CH][HB];
 #pragma unroll
