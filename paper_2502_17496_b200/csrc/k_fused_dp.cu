@@ -71,6 +71,7 @@ __global__ void __launch_bounds__(256) fused_allreduce_adam_kernel(
     gq[q] = q < W ? (const float*)ncclGetLsaPointer(gwin, 0, q) : nullptr;
     pq[q] = q < W ? (float*)ncclGetLsaPointer(pwin, 0, q) : nullptr;
   }
+  float* const pmine = (float*)ncclGetLsaPointer(pwin, 0, r);   // (pq[r] with a runtime r would live in local memory)
   const size_t per = (n + W - 1) / W, lo = (size_t)r * per, hi = lo + per < n ? lo + per : n;
   const size_t stride = (size_t)gridDim.x * blockDim.x;
   // 2. this rank's shard: mean over ranks, Adam, the new value to every rank
@@ -86,7 +87,7 @@ __global__ void __launch_bounds__(256) fused_allreduce_adam_kernel(
     }
     const float g = __fdiv_rn(s, (float)W);
     float mm = m[e], vv = v[e];
-    float pp = adam_elem(pq[r][e], g, mm, vv, b1, omb1, b2, omb2, bc2_sqrt, eps, step_size);
+    float pp = adam_elem(pmine[e], g, mm, vv, b1, omb1, b2, omb2, bc2_sqrt, eps, step_size);
     if (e >= clo && e < chi) pp = fmaxf(pp, cmin);
     m[e] = mm;
     v[e] = vv;
@@ -101,7 +102,7 @@ __global__ void __launch_bounds__(256) fused_allreduce_adam_kernel(
   // 3. every shard is everywhere; the 16-bit working copies of every parameter, the step count
   bar.sync(ncclCoopCta(), cuda::memory_order_acq_rel);
   if (views.kind != 0)
-    for (size_t e = blockIdx.x * (size_t)blockDim.x + threadIdx.x; e < n; e += stride) store_views(views, e, pq[r][e]);
+    for (size_t e = blockIdx.x * (size_t)blockDim.x + threadIdx.x; e < n; e += stride) store_views(views, e, pmine[e]);
   __syncthreads();
   if (threadIdx.x == 0) {
     __threadfence();
