@@ -918,3 +918,37 @@ def test_td3_fp16_actor_with_loss_scaling():
         assert torch.equal(a, b)
     with pytest.raises(pk.SpikeRLError):
         pk.SpikingActor(pk.actor_cfg_from(shape, engine="simt"), 8)
+
+
+# ------------------------------------------------------------------------------ bench contract
+@pytest.mark.parametrize("args", [["--workload", "cfg1", "--steps", "4", "--warmup", "3"],
+                                  ["--workload", "cfg0", "--steps", "4", "--warmup", "3"],
+                                  ["--impl", "reference", "--workload", "cfg1", "--steps", "1", "--warmup", "1"]])
+def test_bench_contract(args):
+    """bench.py prints one JSON line with the contract's keys (short runs; the driver's full runs use
+    the same code): value / metric / unit / timing keys, clocks, the launch count, e2e with the copied
+    bytes, the live roofline with its peak and traffic, the oracle baseline; the reference arm its own
+    line with impl = reference."""
+    import json, os, subprocess, sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    r = subprocess.run([sys.executable, "bench.py", *args, "--no-cpu-baseline"] if "--impl" not in args else
+                       [sys.executable, "bench.py", *args], cwd=root, capture_output=True, text=True, timeout=900)
+    assert r.returncode == 0, r.stderr[-2000:]
+    d = json.loads(r.stdout.strip().splitlines()[-1])
+    for k in ("metric", "value", "unit", "n_gpus", "steps", "warmup", "ms_per_step", "higher_is_better", "scaling",
+              "vs_baseline", "dtype", "data", "config", "e2e"):
+        assert k in d, k
+    assert d["value"] > 0 and d["ms_per_step"] > 0 and d["n_gpus"] == 1
+    assert d["e2e"]["value"] > 0 and "unit" in d["e2e"]
+    if "--impl" in args:
+        assert d["impl"] == "reference" and d["cpu_baseline"]["kind"] == "oracle"
+        assert d["e2e"]["h2d_bytes_per_step"] == 0
+        return
+    assert d["config"]["workload"].startswith(args[1])
+    assert d["gpu_launches"] > 0
+    assert d["e2e"]["h2d_bytes_per_step"] > 0 and d["e2e"]["d2h_bytes_per_step"] > 0
+    assert set(d["clocks"]) >= {"sm_mhz", "sm_max_mhz", "reasons"}
+    roof = d["roofline"]
+    for k in ("bound", "achieved", "peak", "unit", "frac", "traffic", "timing"):
+        assert k in roof, k
+    assert 0 < roof["frac"] <= 1.5 and roof["peak"] > 0
