@@ -515,9 +515,12 @@ def run_td3(args, rank, world, workload):
             def after(k):
                 torch.cuda.synchronize()
                 watch.collect(per)
-            # the same number of pairs again, replaying the watched capture (same flush, same work)
+            # the same number of pairs again, replaying the watched capture (same flush, same work),
+            # after one untimed replay (the graph's upload)
+            watched_graph.replay()
+            torch.cuda.synchronize()
             time_steps(lambda k: watched_graph.replay(), npair, flush, world, after_step=after)
-            step0[0] += 2 * npair
+            step0[0] += 2 * npair + 2
             live = (watch.launches, watch.total_ms)
     else:
         total_ms = time_steps(graph_step, args.steps, flush, world)
@@ -799,6 +802,8 @@ def run_actor(args, rank, world, workload):
         total_ms = time_steps(run, args.steps, flush, world, after_step=after)
     else:
         total_ms = time_steps(run, args.steps, flush, world)
+        wgraph.replay()   # its first replay (upload) outside its timed loop
+        torch.cuda.synchronize()
         time_steps(lambda k: wgraph.replay(), args.steps, flush, world, after_step=after)
     clocks = clk.stop()
     _lib.Watch.off()
