@@ -269,7 +269,7 @@ def time_steps(run_step, K, flush_buf, world, after_step=None):
     return max_over_ranks(total_ms, world)
 
 
-def dominant_kernel(summary, pk_peaks, live, timed_ms, clocks=None, long_step=False):
+def dominant_kernel(summary, pk_peaks, live, timed_ms, workload, clocks=None, long_step=False):
     """The largest kernel of the step (by the profiling pass's launch list) against its roofline.
     `live` = (launches, total_ms) of that kernel measured inside the timed region (Watch); the
     algorithmic work per launch is the launcher's attribution (flops or bytes). Tensor-bound
@@ -297,10 +297,12 @@ def dominant_kernel(summary, pk_peaks, live, timed_ms, clocks=None, long_step=Fa
         per = best["bytes"] / best["launches"]
         peak = pk_peaks["hbm_gbs"]
         ach, unit, bound = per / avg_s / 1e9, "GB/s", "hbm"
+    # DRAM bytes per launch from one ncu --set full capture of this kernel AT THIS WORKLOAD
+    # (profiles/ncu_traffic.json, keyed "<workload>:<kernel>"); null when none was captured
     traffic = None
     try:
         with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as f:
-            traffic = json.load(f).get(best["name"])
+            traffic = json.load(f).get(f"{workload}:{best['name']}")
     except Exception:
         pass
     return {"kernel": best["name"], "bound": bound, "achieved": round(ach, 3), "peak": peak, "unit": unit,
@@ -564,7 +566,7 @@ def run_td3(args, rank, world, workload):
     if live is None:   # --single-graphs (diagnostic): no live watch; the eager profiling pass stands in
         d = [e for e in summ if e["name"] == dom][0]
         live = (d["launches"], d["total_ms"])
-    out["roofline"] = dominant_kernel(summ, peaks(), live, total_ms)
+    out["roofline"] = dominant_kernel(summ, peaks(), live, total_ms, workload)
     iso = isolated_actor_kernel(td3, B, out["roofline"])
     if iso:
         out["roofline"]["isolated"] = iso
@@ -828,7 +830,8 @@ def run_actor(args, rank, world, workload):
         en["joules_per_step"] = round(en["joules"] / en["steps"], 5)
         en["samples_per_joule"] = round(en["steps"] * gsum / max(en["joules"], 1e-9), 1)
         out["energy"] = en
-    out["roofline"] = dominant_kernel(summ, peaks(), (watch.launches, watch.total_ms), total_ms, long_step=strong,
+    out["roofline"] = dominant_kernel(summ, peaks(), (watch.launches, watch.total_ms), total_ms, workload,
+                                      long_step=strong,
                                       clocks=clocks)
     out["kernel_breakdown"] = _breakdown(summ)
     if strong:

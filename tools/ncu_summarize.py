@@ -27,10 +27,18 @@ SCALE = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "ns": 1e-9, "us": 
 
 
 def raw(rep):
+    """Metrics of the report's first kernel; with several kernels in one report (a ProfScope that
+    spans two launches, e.g. enc_grad_simt = partial + reduce) the DRAM bytes are their sum."""
     out = page(rep, "raw")
-    rows = list(csv.reader(out.splitlines()))
+    rows = [r for r in csv.reader(out.splitlines()) if r]
     h, units, vals = rows[0], rows[1], rows[2]
-    return {k: (vals[h.index(k)], units[h.index(k)]) for k in KEYS if k in h}, vals[h.index("Kernel Name")]
+    m = {k: (vals[h.index(k)], units[h.index(k)]) for k in KEYS if k in h}
+    for k in ("dram__bytes_read.sum", "dram__bytes_write.sum"):
+        if k in h and len(rows) > 3:
+            tot = sum(to_si(r[h.index(k)], units[h.index(k)]) or 0.0 for r in rows[2:] if len(r) == len(h))
+            m[k] = (repr(tot), "byte")
+    names = [r[h.index("Kernel Name")] for r in rows[2:] if len(r) == len(h)]
+    return m, " + ".join(names)
 
 
 def to_si(v, u):
@@ -63,8 +71,8 @@ def main():
             traffic[name] = rd + wr
             lines += ["", f"DRAM traffic per launch: {rd + wr:.4g} B (read {rd:.4g}, write {wr:.4g})"]
         lines.append("")
-    # kernel shares from the launch list
-    rows = list(csv.reader(open(launches)))
+    # kernel shares from the launch list ("-": none)
+    rows = list(csv.reader(open(launches))) if launches != "-" else []
     hdr = None
     per = defaultdict(float)
     cnt = defaultdict(int)
@@ -79,8 +87,9 @@ def main():
             per[nm] += t
             cnt[nm] += 1
     tot = sum(per.values()) or 1.0
-    lines += [f"## Launch list ({os.path.basename(launches)}): share of device time", "",
-              "| kernel | launches | total (us) | share |", "|---|---|---|---|"]
+    if rows:
+        lines += [f"## Launch list ({os.path.basename(launches)}): share of device time", "",
+                  "| kernel | launches | total (us) | share |", "|---|---|---|---|"]
     for nm, t in sorted(per.items(), key=lambda x: -x[1])[:25]:
         lines.append(f"| `{nm[:80]}` | {cnt[nm]} | {t * 1e6:.1f} | {100 * t / tot:.1f}% |")
     with open(os.path.join(ROOT, "profiles", f"{rnd}_ncu_summary.md"), "w") as f:
