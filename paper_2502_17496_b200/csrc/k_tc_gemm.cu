@@ -1153,6 +1153,17 @@ static bool pairs_enabled() {
   return v == 1;
 }
 
+// A/B diagnostics: SPIKERL_TC_CG_LEGACY=<bits> restores the earlier pairing rule per mode (pairs
+// whenever the tile count allows): 2 DW, 4 ENC
+static int cg_legacy() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("SPIKERL_TC_CG_LEGACY");
+    v = e ? atoi(e) : 0;
+  }
+  return v;
+}
+
 template <int MODE, int BT, int CG, bool F16, bool RHO = false, bool X6 = false>
 static int launch_cg(const CUtensorMap& ma, const CUtensorMap& mb, const CUtensorMap& mc, const Params& p, cudaStream_t st) {
   SPK_SMEM_ATTR((tc_kernel<MODE, BT, CG, F16, RHO, X6>), SMEM_BYTES);
@@ -1281,6 +1292,9 @@ int launch_lif_fwd_tc(const ActorDims& d, int l, int B, const uint32_t* bits_in,
   const int mt = d.P[l] / BM;
   p.Bt = choose_bt(d.T, B, mt, FWD_MAX_BT);
   p.BN = d.T * p.Bt;
+  // (single CTAs below K = 1024 were ~1 us faster per launch alone at configs[1], but slower inside
+  // the TD3 update DAG, where three forward passes share the GPU: configs[2] 120.0 -> 128.8 us per
+  // update, A/B r02; kept paired)
   p.cg = (pairs_enabled() && mt % 2 == 0) ? 2 : 1;
   p.m_tiles = mt / p.cg;
   p.n_tiles = (B + p.Bt - 1) / p.Bt;
@@ -1347,7 +1361,13 @@ int launch_lif_dx_tc(const ActorDims& d, int l, int B, const void* Gl, const __n
   return launch_bt<DX>(p.Bt, ma, mb, p, st, &mc);
 }
 
-static int enc_cg(const ActorDims& d) { return (pairs_enabled() && (d.P[0] / BM) % 2 == 0) ? 2 : 1; }
+// CTA pairs for ENC only with a long contraction (K = n_1 >= 512): with n_1 = 256 the unit's four
+// k-blocks are short against its epilogue and single CTAs were faster at every batch measured
+// (configs[1..3]: 19.1 -> 16.6, 26.8 -> 21.3, 20.7 -> 17.9 us; B = 4096 59.2 -> 53.9 us), while at
+// configs[4] (n_1 = 1024) the two are within 2 %
+static int enc_cg(const ActorDims& d) {
+  return (pairs_enabled() && (d.P[0] / BM) % 2 == 0 && (d.P[1] / BK >= 8 || (cg_legacy() & 4))) ? 2 : 1;
+}
 
 // batch columns per ENC unit: 256 when that still gives every SM (pair) a unit; smaller batches
 // use narrower units (>= 16) so the per-unit epilogue loop over the batch stays short (cfg1:
@@ -1397,33 +1417,47 @@ int launch_enc_grad_tc(const ActorDims& d, int B, const void* Gsum, const __nv_b
   return launch_enc_grad_reduce(d, NUM_EPI_GROUPS * p.n_tiles, partial, dmu, dsigma, accumulate, st);
 }
 
-// split-K plan for dW_l: pick the split count s minimising a simple cost model in units of one
-// k-block of MMAs: waves(s) x (k-blocks per unit + dump) + the fixed-order reduction of the s
-// partial tiles spread over the GPU. A unit's epilogue (dumping a 256 x 512 fp32 partial tile) costs
-// about 8 k-blocks and is not overlapped for pair units (single TMEM buffer). (The previous
-// wave-efficiency-only rule chose 320 one-k-block units for dW3 at configs[3] B = 4096: 278 us.)
-static int dw_cg(const ActorDims& d, int l) { return (pairs_enabled() && (d.P[l] / BM) % 2 == 0) ? 2 : 1; }
+// split-K plan for dW_l: pick the CTA grouping cg and split count s minimising a simple cost model
+// in units of one single-CTA k-block (a 128 x 256 x 64 MMA step per SM): waves x (k-blocks per unit
+// x kKb(cg) + dump(cg)) + the fixed-order reduction of the partial tiles spread over the GPU. A pair
+// unit covers a 256 x 512 tile: its k-block does twice a single CTA's MMA work per SM for ~1.28x the
+// time (configs[4]: DW L1 4.40 ms paired vs 6.88 ms single), and its epilogue dumps twice the
+// fp32 partial columns per CTA (~10 k-blocks, not overlapped: single TMEM buffer) against ~5 for a
+// single CTA's 128 x 256 tile. Pairs win when the contraction is long (configs[4]); with few
+// k-blocks the dumps dominate and single CTAs win (configs[1] DW L2 28.4 -> 19.8 us, configs[2] DW L1
+// 38.1 -> 27.0 us, configs[3] B = 4096 DW L3 41.6 -> 26.4 us). (The wave-efficiency-only rule of r01
+// chose 320 one-k-block units for dW3 at configs[3] B = 4096: 278 us.)
+struct DwPlan { int cg, splits, kps; };
+
+static DwPlan dw_plan(const ActorDims& d, int l, int B) {
+  const int k_blocks = cdiv((long long)d.T * B, BK);
+  DwPlan best_p{1, 1, k_blocks};
+  double best = 1e300;
+  for (int cg = 1; cg <= 2; ++cg) {
+    if (cg == 2 && !(pairs_enabled() && (d.P[l] / BM) % 2 == 0)) continue;
+    // single CTAs only for short contractions (T B < 8192): at configs[3] B = 4096 the model's
+    // single-CTA DW L2 / L3 were faster alone but 1.5 us per update slower inside the TD3 DAG (A/B r02)
+    if (cg == 1 && (k_blocks >= 128 || (cg_legacy() & 2)) && pairs_enabled() && (d.P[l] / BM) % 2 == 0) continue;
+    const int m_tiles = d.P[l] / BM / cg, n_tiles = cdiv(d.P[l - 1], dw_unit_cols(cg));
+    const long long mn = (long long)m_tiles * n_tiles;
+    const int slots = cg == 2 ? pair_slots() : num_sms();   // concurrent units (CTA pairs when cg = 2)
+    const double kKb = cg == 2 ? 1.28 : 1.0, kDump = cg == 2 ? 10.0 : 5.0;
+    const int s_max = k_blocks < 8 * slots ? k_blocks : 8 * slots;
+    for (int s = 1; s <= s_max; ++s) {
+      const int per = cdiv(k_blocks, s), ss = cdiv(k_blocks, per);
+      if (ss != s) continue;   // the same partition as a smaller s
+      const long long units = mn * ss;
+      const double cost = (double)cdiv(units, slots) * (per * kKb + kDump) + (double)units * kDump / slots;
+      if (cost < best - 1e-9) { best = cost; best_p = DwPlan{cg, ss, per}; }
+    }
+  }
+  return best_p;
+}
 
 void tc_dw_plan(const ActorDims& d, int l, int B, int* splits, int* kps) {
-  const int cg = dw_cg(d, l);
-  const int m_tiles = d.P[l] / BM / cg, n_tiles = cdiv(d.P[l - 1], dw_unit_cols(cg));
-  const int k_blocks = cdiv((long long)d.T * B, BK);
-  const long long mn = (long long)m_tiles * n_tiles;
-  const int slots = cg == 2 ? pair_slots() : num_sms();   // concurrent units (CTA pairs when cg = 2)
-  constexpr double kDump = 8.0;
-  int best_s = 1;
-  double best = 1e300;
-  const int s_max = k_blocks < 8 * slots ? k_blocks : 8 * slots;
-  for (int s = 1; s <= s_max; ++s) {
-    const int per = cdiv(k_blocks, s), ss = cdiv(k_blocks, per);
-    if (ss != s) continue;   // the same partition as a smaller s
-    const long long units = mn * ss;
-    const double cost = (double)cdiv(units, slots) * (per + kDump) + (double)units * kDump / slots;
-    if (cost < best - 1e-9) { best = cost; best_s = s; }
-  }
-  const int per = cdiv(k_blocks, best_s);
-  *kps = per;
-  *splits = cdiv(k_blocks, per);
+  const DwPlan pl = dw_plan(d, l, B);
+  *kps = pl.kps;
+  *splits = pl.splits;
 }
 
 size_t tc_dw_partial_bytes(const ActorDims& d, int B, int l) {
@@ -1440,13 +1474,13 @@ int launch_lif_dw_tc(const ActorDims& d, int l, int B, const void* Gl, const uin
   p.f16 = d.f16; p.one2 = d.f16 ? 0x3C003C00u : 0x3F803F80u;
   p.T = d.T; p.B = B; p.BN = DW_BN;
   p.R = d.T * B;
-  p.cg = dw_cg(d, l);
+  const DwPlan pl = dw_plan(d, l, B);
+  p.cg = pl.cg;
   p.m_tiles = d.P[l] / BM / p.cg;
   p.n_tiles = cdiv(d.P[l - 1], dw_unit_cols(p.cg));
   p.k_blocks = cdiv(p.R, BK);
-  int splits, kps;
-  tc_dw_plan(d, l, B, &splits, &kps);
-  p.kps = kps;
+  const int splits = pl.splits;
+  p.kps = pl.kps;
   p.n_units = p.m_tiles * p.n_tiles * splits;
   p.bits_dw = bits_prev; p.w_dw = d.Wd[l - 1];
   p.dw_part = part; p.ldp = d.P[l - 1]; p.split_stride = (long long)d.P[l] * d.P[l - 1];
