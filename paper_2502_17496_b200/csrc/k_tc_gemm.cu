@@ -94,7 +94,7 @@ struct Params {
   // ENC
   const float* A; const float* obs; const float* mu; const float* sigma; float* partial; int K0, S, E;
   // DW
-  const uint32_t* bits_dw; int w_dw; float* dw_part; long long split_stride; int ldp; int R;
+  const uint32_t* bits_dw; int w_dw; float* dw_part; long long split_stride; int ldp; int R; int ldr;
   // WG jobs (critic weight gradients): A / B row bases in the stacked operand maps, partial offset
   // (elements, within one split), row stride and valid columns of the output tile
   int wg_njobs; int wg_arow[8], wg_brow[8], wg_ld[8], wg_ncol[8]; long long wg_off[8];
@@ -1004,10 +1004,15 @@ __global__ void __launch_bounds__(n_threads(X6), 1)
           }
         }
       } else {  // DW: group g writes columns [GC g, GC g + GC) of the unit (GC = 64, or 128 for DW2)
+        // The partial tile is stored column-major (part[split][col][row], rows = this layer's
+        // neurons contiguous, stride ldr), so one store instruction of the warp (32 consecutive
+        // neurons of one column) is one full 128-byte line; the row-major float4 stores it replaces
+        // touched 32 lines per instruction and paced the epilogue (~5 us per unit at configs[1]).
+        // dw_reduce_kernel transposes back to the master layout.
         constexpr int GC = (DW2 ? 2 * DW_BN : DW_BN) / NUM_EPI_GROUPS;
         const int c0 = g * GC;
         const int col0 = t.n * dw_unit_cols(CG) + c0;
-        float* dst = p.dw_part + (size_t)t.split * p.split_stride + (size_t)row * p.ldp + col0;
+        float* dst = p.dw_part + (size_t)t.split * p.split_stride + (size_t)col0 * p.ldr + row;
         for (int j1 = 0; j1 < GC; j1 += 32) {   // 4 loads in flight per wait
           if (col0 + j1 < p.ldp) {               // ldp is a multiple of 128
             uint32_t rr[4][8];
@@ -1015,12 +1020,9 @@ __global__ void __launch_bounds__(n_threads(X6), 1)
             for (int ci = 0; ci < 4; ++ci) tmem_ld8(taddr + c0 + j1 + 8 * ci, rr[ci]);
             tmem_ld_wait();
 #pragma unroll
-            for (int ci = 0; ci < 4; ++ci) {
-              const uint32_t (&r)[8] = rr[ci];
-              float4* d4 = reinterpret_cast<float4*>(dst + j1 + 8 * ci);
-              d4[0] = make_float4(__uint_as_float(r[0]), __uint_as_float(r[1]), __uint_as_float(r[2]), __uint_as_float(r[3]));
-              d4[1] = make_float4(__uint_as_float(r[4]), __uint_as_float(r[5]), __uint_as_float(r[6]), __uint_as_float(r[7]));
-            }
+            for (int ci = 0; ci < 4; ++ci)
+#pragma unroll
+              for (int e = 0; e < 8; ++e) dst[(size_t)(j1 + 8 * ci + e) * p.ldr] = __uint_as_float(rr[ci][e]);
           }
         }
       }
@@ -1046,18 +1048,41 @@ __global__ void __launch_bounds__(n_threads(X6), 1)
   }
 }
 
-// dW[n][k] (master layout) = sum over splits (fixed order) of the partial tiles
-__global__ void dw_reduce_kernel(const float* __restrict__ part, int splits, long long split_stride, int ldp,
-                                 int N, int K, float* __restrict__ dW, int accum) {
+// dW[n][k] (master layout) = sum over splits (fixed order) of the column-major partial tiles
+// part[split][k][n] (row stride ldr): one element per thread, 32 x 32 tiles through shared memory,
+// so both the partial reads (along n) and the dW writes (along k) are coalesced; the split loop
+// issues 8 loads before their (in-order) adds. Block (32, 32).
+__global__ void __launch_bounds__(1024) dw_reduce_kernel(const float* __restrict__ part, int splits,
+                                                         long long split_stride, int ldr, int N, int K,
+                                                         float* __restrict__ dW, int accum) {
+  __shared__ float tile[32][33];
   pdl_wait();
   pdl_trigger();
-  const long long total = (long long)N * K;
-  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < total; i += (long long)gridDim.x * blockDim.x) {
-    const int n = (int)(i / K), k = (int)(i % K);
-    const float* src = part + (size_t)n * ldp + k;
-    float s = 0.f;
-    for (int sp = 0; sp < splits; ++sp) s = __fadd_rn(s, src[(size_t)sp * split_stride]);
-    dW[i] = accum ? __fadd_rn(dW[i], s) : s;
+  const int tx = threadIdx.x, ty = threadIdx.y;
+  const int k0 = blockIdx.x * 32, n0 = blockIdx.y * 32;
+  {
+    const int k = k0 + ty, n = n0 + tx;
+    if (k < K && n < N) {
+      const float* src = part + (size_t)k * ldr + n;
+      float s = 0.f;
+      int sp = 0;
+      for (; sp + 8 <= splits; sp += 8) {
+        float v[8];
+#pragma unroll
+        for (int j = 0; j < 8; ++j) v[j] = src[(size_t)(sp + j) * split_stride];
+#pragma unroll
+        for (int j = 0; j < 8; ++j) s = __fadd_rn(s, v[j]);
+      }
+      for (; sp < splits; ++sp) s = __fadd_rn(s, src[(size_t)sp * split_stride]);
+      tile[ty][tx] = s;
+    }
+  }
+  __syncthreads();
+  const int n = n0 + ty, k = k0 + tx;
+  if (k < K && n < N) {
+    const float s = tile[tx][ty];
+    float* o = dW + (size_t)n * K + k;
+    *o = accum ? __fadd_rn(*o, s) : s;
   }
 }
 
@@ -1468,8 +1493,6 @@ size_t tc_dw_partial_bytes(const ActorDims& d, int B, int l) {
 
 int launch_lif_dw_tc(const ActorDims& d, int l, int B, const void* Gl, const uint32_t* bits_prev, float* dW,
                      float* part, int accumulate, cudaStream_t st) {
-  ProfScope ps_(l == 1 ? "lif_dw_tc_L1" : (l == 2 ? "lif_dw_tc_L2" : "lif_dw_tc_L3"), PB_TENSOR,
-                2.0 * d.T * B * (double)d.N[l] * d.N[l - 1], 0.0, st);
   Params p{};
   p.f16 = d.f16; p.one2 = d.f16 ? 0x3C003C00u : 0x3F803F80u;
   p.T = d.T; p.B = B; p.BN = DW_BN;
@@ -1483,7 +1506,7 @@ int launch_lif_dw_tc(const ActorDims& d, int l, int B, const void* Gl, const uin
   p.kps = pl.kps;
   p.n_units = p.m_tiles * p.n_tiles * splits;
   p.bits_dw = bits_prev; p.w_dw = d.Wd[l - 1];
-  p.dw_part = part; p.ldp = d.P[l - 1]; p.split_stride = (long long)d.P[l] * d.P[l - 1];
+  p.dw_part = part; p.ldp = d.P[l - 1]; p.ldr = d.P[l]; p.split_stride = (long long)d.P[l] * d.P[l - 1];
   CUtensorMap ma, mb;
   {  // A = G_l viewed [T*B][P_l]: M = P_l contiguous (MN-major), K = rows (ends at N_3 for G_3, as above)
     const uint64_t dims[2] = {(uint64_t)(l == 3 ? d.N[3] : d.P[l]), (uint64_t)p.R};
@@ -1492,10 +1515,16 @@ int launch_lif_dw_tc(const ActorDims& d, int l, int B, const void* Gl, const uin
     SPK_TRY(make_map(&ma, Gl, 2, dims, strides, box, CU_TENSOR_MAP_SWIZZLE_128B, d.f16));
   }
   mb = ma;
-  SPK_TRY(launch_bt<DW>(8, ma, mb, p, st));
-  const long long total = (long long)d.N[l] * d.N[l - 1];
-  const int grid = (int)((total + 255) / 256 < 148 * 8 ? (total + 255) / 256 : 148 * 8);
-  pdl(dw_reduce_kernel, grid, 256, 0, st)(part, splits, p.split_stride, p.ldp, d.N[l], d.N[l - 1], dW, accumulate);
+  {
+    ProfScope ps_(l == 1 ? "lif_dw_tc_L1" : (l == 2 ? "lif_dw_tc_L2" : "lif_dw_tc_L3"), PB_TENSOR,
+                  2.0 * d.T * B * (double)d.N[l] * d.N[l - 1], 0.0, st);
+    SPK_TRY(launch_bt<DW>(8, ma, mb, p, st));
+  }
+  // the split-K reduction: reads every partial once, writes (accumulate: reads too) dW
+  ProfScope pr_(l == 1 ? "dw_reduce_L1" : (l == 2 ? "dw_reduce_L2" : "dw_reduce_L3"), PB_HBM, 0.0,
+                4.0 * (double)d.N[l] * d.N[l - 1] * (splits + (accumulate ? 2 : 1)), st);
+  pdl(dw_reduce_kernel, dim3(cdiv(d.N[l - 1], 32), cdiv(d.N[l], 32)), dim3(32, 32), 0, st)(
+      part, splits, p.split_stride, p.ldr, d.N[l], d.N[l - 1], dW, accumulate);
   SPK_LAUNCHED();
   return SPIKERL_OK;
 }
