@@ -597,6 +597,46 @@ __global__ void critic_wgrad_reduce_kernel(int splits, int in, int inq, long lon
   }
 }
 
+// The same sum over the column-major partials of the tcgen05 weight-gradient launch
+// (launch_critic_wgrad_tc: part[(s 2 + z) msz + c 256 + r], dW1's columns after dW2's 256): 32 x 32
+// tiles through shared memory so the partial reads (along r) and the master-layout writes (along c)
+// are both coalesced; one element per thread, 8 loads in flight, splits added in order.
+// grid (cdiv(256 + in, 32), 256 / 32, 2), block (32, 32).
+__global__ void __launch_bounds__(1024) critic_wgrad_reduce_cm_kernel(int splits, int in, long long msz, long long P,
+                                                                      long long oW1, long long oW2,
+                                                                      const float* __restrict__ wpart,
+                                                                      float* __restrict__ grad2) {
+  __shared__ float tile[32][33];
+  pdl_wait();
+  pdl_trigger();
+  const int tx = threadIdx.x, ty = threadIdx.y, z = blockIdx.z;
+  const int c0 = blockIdx.x * 32, r0 = blockIdx.y * 32;
+  const bool w2 = c0 < HW;               // 256 is a multiple of 32: a tile is all dW2 or all dW1
+  const int cb = w2 ? c0 : c0 - HW;      // first column within its matrix
+  const int ncol = w2 ? HW : in;
+  {
+    const int c = cb + ty, r = r0 + tx;
+    if (c < ncol) {
+      const float* src = wpart + (size_t)z * msz + (w2 ? 0 : (size_t)HW * HW) + (size_t)c * HW + r;
+      const size_t sst = 2 * (size_t)msz;
+      float sum = 0.f;
+      int s = 0;
+      for (; s + 8 <= splits; s += 8) {
+        float v[8];
+#pragma unroll
+        for (int j = 0; j < 8; ++j) v[j] = src[(size_t)(s + j) * sst];
+#pragma unroll
+        for (int j = 0; j < 8; ++j) sum = __fadd_rn(sum, v[j]);
+      }
+      for (; s < splits; ++s) sum = __fadd_rn(sum, src[(size_t)s * sst]);
+      tile[ty][tx] = sum;
+    }
+  }
+  __syncthreads();
+  const int r = r0 + ty, c = cb + tx;
+  if (c < ncol) grad2[z * P + (w2 ? oW2 : oW1) + (size_t)r * ncol + c] = tile[tx][ty];
+}
+
 // db1 = rowsum dZ1T, db2 = rowsum dZ2T, dW3 = dQ^T H2, db3 = sum dQ. Small batches: one warp per
 // output (blockIdx.x * 8 + warp); large batches (B > 1024): one block per output, each thread a
 // strided subset of the rows with four partial sums, then a fixed tree (ncu r02: the warp-per-output
@@ -1061,8 +1101,9 @@ static int critic_tc_fwd_bwd(const CriticDims& c, int B, const float* params2, c
       const long long msz = (long long)HW * HW + (long long)HW * L.inq;
       SPK_TRY(launch_critic_wgrad_tc(Bp, L.inq, round_up(L.inq, 64), w.dZ2T, w.XT, w.wpart, msz, st));
       const int splits = tc_wgrad_splits(Bp, L.inq);
-      pdl(critic_wgrad_reduce_kernel, 148 * 4, 256, 0, st)(splits, c.in, L.inq, L.P, (long long)c.off[SPIKERL_CRITIC_W1],
-                                                         (long long)c.off[SPIKERL_CRITIC_W2], w.wpart, grad2);
+      pdl(critic_wgrad_reduce_cm_kernel, dim3(cdiv(HW + c.in, 32), HW / 32, 2), dim3(32, 32), 0, st)(
+          splits, c.in, msz, L.P, (long long)c.off[SPIKERL_CRITIC_W1], (long long)c.off[SPIKERL_CRITIC_W2], w.wpart,
+          grad2);
       SPK_LAUNCHED();
     }
     SPK_TRY(stream_after(st, sb, aux->ev[17]));
@@ -1140,8 +1181,9 @@ int critic_mma_fwd_bwd(const CriticDims& c, int B, const float* params2, const _
         const long long msz = (long long)HW * HW + (long long)HW * L.inq;
         SPK_TRY(launch_critic_wgrad_tc(Bp, L.inq, round_up(L.inq, 64), w.dZ2T, w.XT, w.wpart, msz, st));
         const int splits = tc_wgrad_splits(Bp, L.inq);
-        pdl(critic_wgrad_reduce_kernel, 148 * 4, 256, 0, st)(splits, c.in, L.inq, L.P, (long long)c.off[SPIKERL_CRITIC_W1],
-                                                           (long long)c.off[SPIKERL_CRITIC_W2], w.wpart, grad2);
+        pdl(critic_wgrad_reduce_cm_kernel, dim3(cdiv(HW + c.in, 32), HW / 32, 2), dim3(32, 32), 0, st)(
+            splits, c.in, msz, L.P, (long long)c.off[SPIKERL_CRITIC_W1], (long long)c.off[SPIKERL_CRITIC_W2], w.wpart,
+            grad2);
         SPK_LAUNCHED();
       } else {
         // K split in multiples of 16 batch rows (Bp is a multiple of RB = 16)

@@ -982,12 +982,14 @@ __global__ void __launch_bounds__(n_threads(X6), 1)
           epi_bar_sync();
         }
       } else if constexpr (MODE == WG) {
-        // dump the fp32 tile of this (job, split): row = output row within the job's 256, group g
-        // covers columns [128 g, 128 g + 128); columns past the job's width are not stored
+        // dump the fp32 tile of this (job, split) column-major (row stride wg_ld = 256: one warp
+        // store = 32 consecutive rows of one column = one 128-byte line, as the DW dump): row =
+        // output row within the job's 256, group g covers columns [128 g, 128 g + 128); columns past
+        // the job's width are not stored
         constexpr int GC = DW_BN / NUM_EPI_GROUPS;
         const int c0 = g * GC, ld = p.wg_ld[t.n], nc = p.wg_ncol[t.n];
-        float* dst = p.dw_part + (size_t)t.split * p.split_stride + p.wg_off[t.n] +
-                     (size_t)(rank * BM + 32 * q + lane) * ld + c0;
+        float* dst = p.dw_part + (size_t)t.split * p.split_stride + p.wg_off[t.n] + (size_t)c0 * ld +
+                     (rank * BM + 32 * q + lane);
         for (int j1 = 0; j1 < GC; j1 += 32) {
           if (c0 + j1 < nc) {   // nc is a multiple of 32
             uint32_t rr[4][8];
@@ -995,12 +997,9 @@ __global__ void __launch_bounds__(n_threads(X6), 1)
             for (int ci = 0; ci < 4; ++ci) tmem_ld8(taddr + c0 + j1 + 8 * ci, rr[ci]);
             tmem_ld_wait();
 #pragma unroll
-            for (int ci = 0; ci < 4; ++ci) {
-              const uint32_t (&r)[8] = rr[ci];
-              float4* d4 = reinterpret_cast<float4*>(dst + j1 + 8 * ci);
-              d4[0] = make_float4(__uint_as_float(r[0]), __uint_as_float(r[1]), __uint_as_float(r[2]), __uint_as_float(r[3]));
-              d4[1] = make_float4(__uint_as_float(r[4]), __uint_as_float(r[5]), __uint_as_float(r[6]), __uint_as_float(r[7]));
-            }
+            for (int ci = 0; ci < 4; ++ci)
+#pragma unroll
+              for (int e = 0; e < 8; ++e) dst[(size_t)(j1 + 8 * ci + e) * ld] = __uint_as_float(rr[ci][e]);
           }
         }
       } else {  // DW: group g writes columns [GC g, GC g + GC) of the unit (GC = 64, or 128 for DW2)
@@ -1533,7 +1532,8 @@ int launch_lif_dw_tc(const ActorDims& d, int l, int B, const void* Gl, const uin
 // Operands (mma critic workspace): A = [dZ2T z0 | dZ2T z1 | dZ1T z0 | dZ1T z1] rows of Bp bf16 (one
 // stacked 2-D map), B = [XT (xtr rows) | H1T z0 | H1T z1]. Jobs: per critic z, dW2 (A rows z 256,
 // B = H1T z) and dW1 in 256-column tiles (A rows 512 + z 256, B = XT rows n 256). Output: fp32
-// partials in the layout critic_wgrad_reduce_kernel adds up: part[(s 2 + z) msz + ...].
+// partials, column-major (row stride 256), in the layout critic_wgrad_reduce_cm_kernel adds up:
+// part[(s 2 + z) msz + c 256 + r] (dW2), part[(s 2 + z) msz + 256^2 + c 256 + r] (dW1).
 int tc_wgrad_splits(int Bp, int inq) {
   const int jobs = 2 * (1 + cdiv(inq, 256));
   const int kblocks = cdiv(Bp, BK);
@@ -1561,9 +1561,9 @@ int launch_critic_wgrad_tc(int Bp, int inq, int xtr, const __nv_bfloat16* dZT, c
     p.wg_arow[nj] = z * HWc; p.wg_brow[nj] = xtr + z * HWc; p.wg_ld[nj] = HWc; p.wg_ncol[nj] = HWc;
     p.wg_off[nj] = (long long)z * msz; ++nj;
     for (int n = 0; n * 256 < inq; ++n) {
-      p.wg_arow[nj] = 2 * HWc + z * HWc; p.wg_brow[nj] = n * 256; p.wg_ld[nj] = inq;
+      p.wg_arow[nj] = 2 * HWc + z * HWc; p.wg_brow[nj] = n * 256; p.wg_ld[nj] = HWc;
       p.wg_ncol[nj] = inq - n * 256 < 256 ? inq - n * 256 : 256;
-      p.wg_off[nj] = (long long)z * msz + (long long)HWc * HWc + n * 256; ++nj;
+      p.wg_off[nj] = (long long)z * msz + (long long)HWc * HWc + (long long)n * 256 * HWc; ++nj;
     }
   }
   if (nj > 8) { set_error("critic wgrad tc: input width too large"); return SPIKERL_E_UNSUPPORTED; }
