@@ -109,7 +109,8 @@ struct Params {
   int dbg;     // diagnostics only (SPIKERL_TC_DBG, wrong results): 1 = expanders skip their smem
                // stores, 2 = epilogue skips its work, 4 = MMA issuer skips the MMAs, 8 = DW
                // expanders skip their global loads, 16 = TMA producer skips its loads (and the
-               // expect_tx, so the stage completes on the expanders' arrivals alone)
+               // expect_tx, so the stage completes on the expanders' arrivals alone); 32 (results
+               // unchanged, A/B) = no weight loads before the PDL wait
 };
 
 // Phase timeline of one launch (SPIKERL_TC_TRACE=<n>: the n-th tc launch of the process), read by
@@ -401,7 +402,74 @@ __global__ void __launch_bounds__(n_threads(X6), 1)
   if (CG == 2) cluster_sync_all();   // the peer's barriers exist before any remote arrive
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
-  // the prologue above overlaps the previous kernel (PDL); global memory only after this point
+  // TMA loads of one ring stage. what & 1: the stage's expect_tx and its weight operand (A = W for
+  // the actor modes, B = the critic's weights for the critic modes); what & 2: the other operand
+  const uint32_t bytes_b = (MODE == DX) ? 128u * p.T * p.Bt / CG
+                           : ((MODE == ENC || MODE == WG || is_crit(MODE)) ? 128u * p.BN / CG : 0u);
+  auto load_stage = [&](const Tile& t, int kb, int stage, int what) {
+    uint8_t* sA = smem + stage * SB_;
+    uint8_t* sB = sA + A_STAGE;
+    uint64_t* bar = &full[stage];
+    if (CG == 1) {
+      // critic modes: unit column t.n = critic z * (256 / BN) + hidden block; A's K rows of
+      // critic z start at z * cr_aoff (H1T / dZ2T stack both critics)
+      const int cz = is_crit(MODE) ? t.n / (256 / p.BN) : 0, ch = is_crit(MODE) ? t.n % (256 / p.BN) : 0;
+      const int ka = kb * BK + (is_crit(MODE) ? cz * p.cr_aoff : 0);
+      auto ld_a = [&]() {
+        if (!A_MN) {
+          tma_2d(&tmA, sA, bar, kb * BK, t.m * BM);
+        } else {
+          tma_2d(&tmA, sA, bar, t.m * BM, ka);
+          tma_2d(&tmA, sA + 8192, bar, t.m * BM + 64, ka);
+        }
+      };
+      auto ld_b = [&]() {
+        if (is_crit(MODE)) tma_2d(cz == 0 ? &tmB : &tmC, sB, bar, kb * BK, ch * p.BN);
+        if (MODE == DX) tma_3d(&tmB, sB, bar, kb * BK, t.n * p.Bt, 0);
+        if (MODE == ENC) tma_2d(&tmB, sB, bar, kb * BK, t.n * p.BN);
+      };
+      if (what & 1) {
+        mbar_expect_tx(bar, (uint32_t)A_STAGE + bytes_b);
+        if (is_crit(MODE)) ld_b(); else ld_a();
+      }
+      if (what & 2) {
+        if (is_crit(MODE)) ld_a(); else ld_b();
+      }
+    } else if (MODE == WG) {
+      if (rank == 0) mbar_expect_tx(bar, 2u * ((uint32_t)A_STAGE + bytes_b));
+      tma_2d_cg2(&tmA, sA, bar, kb * BK, p.wg_arow[t.n] + rank * BM);
+      tma_2d_cg2(&tmB, sB, bar, kb * BK, p.wg_brow[t.n] + rank * (p.BN / 2));
+    } else {
+      if (what & 1) {
+        if (rank == 0) mbar_expect_tx(bar, 2u * ((uint32_t)A_STAGE + bytes_b));
+        if (!A_MN) {
+          tma_2d_cg2(&tmA, sA, bar, kb * BK, t.m * BM);
+        } else {
+          tma_2d_cg2(&tmA, sA, bar, t.m * BM, kb * BK);
+          tma_2d_cg2(&tmA, sA + 8192, bar, t.m * BM + 64, kb * BK);
+        }
+      }
+      if (what & 2) {
+        if (MODE == DX) tma_3d_cg2(&tmB, sB, bar, kb * BK, t.n * p.Bt, rank * (p.T / 2));
+        if (MODE == ENC) tma_2d_cg2(&tmB, sB, bar, kb * BK, t.n * p.BN + rank * (p.BN / 2));
+      }
+    }
+  };
+  // The weight operand of the first ring pass is requested BEFORE the PDL wait, so its latency
+  // overlaps the previous kernel's tail: the weights are never written by the kernel this one
+  // follows in the library's sequences (an actor tcgen05 launch follows the encoder or another
+  // forward / backward kernel, a critic one the Xᵀ / dZ2 kernels or another critic mode; only the
+  // optimiser and the parameter refresh write weights, and none of them directly precedes a
+  // tcgen05 launch). Everything the previous kernel produces is read after the wait.
+  constexpr bool PRE_W = is_fwd(MODE) || MODE == DX || MODE == ENC || is_crit(MODE);
+  int npre = 0;
+  if (PRE_W && warp == 0 && lane == 0 && !(p.dbg & 16) && !(p.dbg & 32) && cid < p.n_units) {
+    const Tile t = decode<MODE>(p, cid, rank, CG);
+    npre = t.kb1 - t.kb0 < NST ? t.kb1 - t.kb0 : NST;
+    for (int j2 = 0; j2 < npre; ++j2) load_stage(t, t.kb0 + j2, j2, 1);   // ring stages start empty
+  }
+  // the prologue above overlaps the previous kernel (PDL); everything else it may have written only
+  // after this point
   pdl_wait();
   pdl_trigger();
   if (threadIdx.x == 0) trace_stamp(p, 1);
@@ -410,48 +478,21 @@ __global__ void __launch_bounds__(n_threads(X6), 1)
     // ===================== TMA producer (both CTAs load their own halves) =====================
     if (lane == 0) {
       uint32_t it = 0;
-      const uint32_t bytes_b = (MODE == DX) ? 128u * p.T * p.Bt / CG
-                               : ((MODE == ENC || MODE == WG || is_crit(MODE)) ? 128u * p.BN / CG : 0u);
       for (int u = cid; u < p.n_units; u += ncl) {
         const Tile t = decode<MODE>(p, u, rank, CG);
         for (int kb = t.kb0; kb < t.kb1; ++kb, ++it) {
           const int stage = it % NST;
+          if ((int)it < npre) {   // weights already requested: the other operand only
+            load_stage(t, kb, stage, 2);
+            continue;
+          }
           const uint32_t ph = (it / NST) & 1;
           mbar_wait(&empty[stage], ph ^ 1);
-          uint8_t* sA = smem + stage * SB_;
-          uint8_t* sB = sA + A_STAGE;
           if (p.dbg & 16) {
             if (CG == 1 || rank == 0) mbar_arrive(&full[stage]);
-          } else if (CG == 1) {
-            mbar_expect_tx(&full[stage], (uint32_t)A_STAGE + bytes_b);
-            // critic modes: unit column t.n = critic z * (256 / BN) + hidden block; A's K rows of
-            // critic z start at z * cr_aoff (H1T / dZ2T stack both critics)
-            const int cz = is_crit(MODE) ? t.n / (256 / p.BN) : 0, ch = is_crit(MODE) ? t.n % (256 / p.BN) : 0;
-            const int ka = kb * BK + (is_crit(MODE) ? cz * p.cr_aoff : 0);
-            if (!A_MN) {
-              tma_2d(&tmA, sA, &full[stage], kb * BK, t.m * BM);
-            } else {
-              tma_2d(&tmA, sA, &full[stage], t.m * BM, ka);
-              tma_2d(&tmA, sA + 8192, &full[stage], t.m * BM + 64, ka);
-            }
-            if (is_crit(MODE)) tma_2d(cz == 0 ? &tmB : &tmC, sB, &full[stage], kb * BK, ch * p.BN);
-            if (MODE == DX) tma_3d(&tmB, sB, &full[stage], kb * BK, t.n * p.Bt, 0);
-            if (MODE == ENC) tma_2d(&tmB, sB, &full[stage], kb * BK, t.n * p.BN);
-            if (it == 0) trace_stamp(p, 2);
-          } else if (MODE == WG) {
-            if (rank == 0) mbar_expect_tx(&full[stage], 2u * ((uint32_t)A_STAGE + bytes_b));
-            tma_2d_cg2(&tmA, sA, &full[stage], kb * BK, p.wg_arow[t.n] + rank * BM);
-            tma_2d_cg2(&tmB, sB, &full[stage], kb * BK, p.wg_brow[t.n] + rank * (p.BN / 2));
           } else {
-            if (rank == 0) mbar_expect_tx(&full[stage], 2u * ((uint32_t)A_STAGE + bytes_b));
-            if (!A_MN) {
-              tma_2d_cg2(&tmA, sA, &full[stage], kb * BK, t.m * BM);
-            } else {
-              tma_2d_cg2(&tmA, sA, &full[stage], t.m * BM, kb * BK);
-              tma_2d_cg2(&tmA, sA + 8192, &full[stage], t.m * BM + 64, kb * BK);
-            }
-            if (MODE == DX) tma_3d_cg2(&tmB, sB, &full[stage], kb * BK, t.n * p.Bt, rank * (p.T / 2));
-            if (MODE == ENC) tma_2d_cg2(&tmB, sB, &full[stage], kb * BK, t.n * p.BN + rank * (p.BN / 2));
+            load_stage(t, kb, stage, 3);
+            if (CG == 1 && it == 0) trace_stamp(p, 2);
           }
         }
       }
@@ -717,6 +758,7 @@ __global__ void __launch_bounds__(n_threads(X6), 1)
             for (int ci = 0; ci < CH; ++ci)
               if (t0 + ci < p.T) tmem_ldn<HB>(taddr + (t0 + ci) * BT + jb, rr[ci]);
             tmem_ld_wait();
+            if (t0 == 0 && titer == 0 && warp == EPI_WARP0 && lane == 0) trace_stamp(p, 10);
 #pragma unroll
             for (int ci = 0; ci < CH; ++ci) {
               const int tt = t0 + ci;
@@ -766,6 +808,7 @@ __global__ void __launch_bounds__(n_threads(X6), 1)
               }
             }
           }
+          if (titer == 0 && warp == EPI_WARP0 && lane == 0) trace_stamp(p, 11);
           if constexpr (OUT) {
             if (row < p.n3) {
 #pragma unroll

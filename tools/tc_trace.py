@@ -2,7 +2,8 @@
 actor forward+backward at the given config, re-run in a fresh process with SPIKERL_TC_TRACE=n and
 print the %globaltimer stamps of CTA 0 relative to its entry (ns):
   1 setup done  2 first TMA issued  3 first full stage  4 first accumulator committed
-  6 epilogue got accumulator  7 epilogue done (unit 0)  8 teardown start  9 TMEM freed"""
+  6 epilogue got accumulator  7 epilogue done (unit 0)  8 teardown start  9 TMEM freed
+  10 FWD epilogue: first TMEM load back  11 FWD epilogue: scan done"""
 import os, sys, subprocess, json, ctypes as C
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 
