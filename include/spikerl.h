@@ -138,6 +138,13 @@ size_t spikerl_critic_param_count(const spikerl_critic_cfg* cfg);
 /* bf16 working copies (opaque, zero-padded tensor-core layout); produced by *_refresh_bf16. */
 size_t spikerl_actor_bf16_bytes(const spikerl_actor_cfg* cfg);
 size_t spikerl_critic_bf16_bytes(const spikerl_critic_cfg* cfg); /* twin pair: [2][P] + W1^T, W2^T each */
+/* Element offsets of the tensor-core critic's bf16 twin buffer (bf16, hidden 256-256, in_dim <= 512):
+ * out[0] first per-critic block (after the [2][P] plain copy), out[1] block stride, then within a
+ * block out[2] W1p [H1][inp] (rows zero padded to inp = out[6]), out[3] W1T [inq][H1], out[4] W2T
+ * [H1][H2], out[5] W2 [H2][H1], out[6] inp, out[7] inq. TD3 updates keep the whole buffer current
+ * except the transposed blocks nothing reads: the targets' W1T / W2T, and the online critics' W1T
+ * rows outside the action columns [S, S+A) (spikerl_td3_update). E_UNSUPPORTED for other critics. */
+int spikerl_critic_bf16_layout(const spikerl_critic_cfg* cfg, long long* out8);
 /* Device buffers the caller allocates for one forward(+backward) at `batch`. */
 size_t spikerl_actor_tape_bytes(const spikerl_actor_cfg* cfg, int batch);
 size_t spikerl_actor_workspace_bytes(const spikerl_actor_cfg* cfg, int batch);

@@ -157,6 +157,7 @@ _SIGS = {
     "spikerl_critic_param_count": (SZ, [C.POINTER(CriticCfg)]),
     "spikerl_actor_bf16_bytes": (SZ, [C.POINTER(ActorCfg)]),
     "spikerl_critic_bf16_bytes": (SZ, [C.POINTER(CriticCfg)]),
+    "spikerl_critic_bf16_layout": (C.c_int, [C.POINTER(CriticCfg), C.POINTER(C.c_longlong)]),
     "spikerl_actor_tape_bytes": (SZ, [C.POINTER(ActorCfg), I]),
     "spikerl_actor_workspace_bytes": (SZ, [C.POINTER(ActorCfg), I]),
     "spikerl_actor_workspace_tape_offset": (SZ, [C.POINTER(ActorCfg), I]),

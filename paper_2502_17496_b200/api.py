@@ -428,6 +428,27 @@ class TD3:
         check(lb.spikerl_critic_refresh_bf16(C.byref(self.ccfg), 2, _p(self.critic_t), _p(self.critic_t_bf16), s),
               "r")
 
+    def bf16_maintained(self, target: bool) -> torch.Tensor:
+        """Bool mask over the critic twin bf16 buffer (as int16 elements) of what the updates keep current:
+        everything but the transposed blocks nothing reads (spikerl_critic_bf16_layout)."""
+        n = self.critic_bf16.numel() // 2
+        mask = torch.ones(n, dtype=torch.bool, device=self.critic_bf16.device)
+        o = (C.c_longlong * 8)()
+        if lib().spikerl_critic_bf16_layout(C.byref(self.ccfg), o) != 0:
+            return mask
+        base, tb, _, w1t, w2t, _, _, inq = list(o)
+        H = 256
+        S, A = self.acfg.obs_dim, self.acfg.act_dim
+        for z in range(2):
+            blk = base + z * tb
+            rows = mask[blk + w1t: blk + w1t + inq * H].view(inq, H)
+            rows[:] = False
+            if not target:
+                rows[S:S + A] = True
+                continue
+            mask[blk + w2t: blk + w2t + H * H] = False
+        return mask
+
     def update(self, step: int, indices: torch.Tensor | None = None, noise: torch.Tensor | None = None):
         check(lib().spikerl_td3_update(C.byref(self.acfg), C.byref(self.ccfg), C.byref(self.hp), C.byref(self._bufs),
                                        step, self.seed, _p(indices), _p(noise),

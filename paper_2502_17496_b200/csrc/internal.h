@@ -129,6 +129,10 @@ struct Bf16Views {
   FastDiv colsd[3];
   long long P, tb, oW1, oW2, W1p, W1T, W2T, W2c;   // critic (per-critic block after the [2][P] copy)
   int in, H1, H2, inp;
+  // critic: the transposed blocks kept current — W1T rows [w1t_lo, w1t_hi) (dQ1/da reads only the
+  // action rows [S, S+A)), W2T when w2t (the data backward's operand; forward-only copies such as the
+  // TD3 targets need neither)
+  int w1t_lo, w1t_hi, w2t;
   FastDiv Pd, ind, H1d;
 };
 Bf16Views actor_bf16_views(const ActorDims& d, __nv_bfloat16* out);
@@ -175,13 +179,13 @@ __device__ __forceinline__ void store_views(const Bf16Views& v, size_t e, float 
   if (r >= 0 && r < (long long)v.H1 * v.in) {          // W1[j][i] -> W1p[j][i], W1T[i][j]
     const uint32_t j = fdiv((uint32_t)r, v.ind), i = (uint32_t)r - j * (uint32_t)v.in;
     blk[v.W1p + (long long)j * v.inp + i] = h;
-    blk[v.W1T + (long long)i * v.H1 + j] = h;
+    if ((int)i >= v.w1t_lo && (int)i < v.w1t_hi) blk[v.W1T + (long long)i * v.H1 + j] = h;
     return;
   }
   r = l - v.oW2;
   if (r >= 0 && r < (long long)v.H2 * v.H1) {          // W2[j2][j1] -> W2T[j1][j2], W2c[j2][j1]
     const uint32_t j2 = fdiv((uint32_t)r, v.H1d), j1 = (uint32_t)r - j2 * (uint32_t)v.H1;
-    blk[v.W2T + (long long)j1 * v.H2 + j2] = h;
+    if (v.w2t) blk[v.W2T + (long long)j1 * v.H2 + j2] = h;
     blk[v.W2c + r] = h;
   }
 }
@@ -235,11 +239,33 @@ size_t critic_ws_bytes(const CriticDims& c, int B);
 size_t critic_bf16_elems(const CriticDims& c);   // twin pair incl. the mma path's padded/transposed copies
 int launch_critic_refresh(const CriticDims& c, const float* params2, __nv_bfloat16* out, cudaStream_t st);
 bool critic_mma_ok(const CriticDims& c);
+void critic_bf16_layout(const CriticDims& c, long long* out8);   // spikerl_critic_bf16_layout
 size_t critic_mma_ws_bytes(const CriticDims& c, int B);
 int critic_mma_fwd_bwd(const CriticDims& c, int B, const float* params2, const __nv_bfloat16* pb, const float* obs,
                        int S, const float* act, int A, const TdY* y, float* q, float* loss, float* grad2,
                        float* grad_act, float act_scale, int nz, void* ws, cudaStream_t st,
                        cudaEvent_t wait_before_loss = nullptr, const float* dq_scale = nullptr);
+// Fused small-batch critic launches (bf16 tensor-core critic, B <= 512; SPIKERL_CRITIC_FUSED=0 turns
+// them off): the whole critic update of a TD3 step (forward, loss, data backward, weight / bias
+// gradients, Adam (+ the targets' Polyak step when polyak != NULL) and the bf16 views) as one launch
+// with grid barriers, and the actor objective's critic pass (forward of critic 0, dQ1/da, -mean Q) as
+// one launch. Bitwise the results of the separate launches. steps: the critic's {t, ticket} slots of
+// spikerl_td3_bufs.adam_steps (the grid barrier uses the high word of steps[1]); ticket (actor pass):
+// a zero-at-rest counter word.
+bool critic_fused_ok(const CriticDims& c, int B);
+// the critic's Adam (+ the targets' Polyak) with coalesced stores of the transposed bf16 copy; bitwise
+// launch_adam's result (no loss scaling)
+bool critic_adam_ok(const CriticDims& c, const Bf16Views* views, const PolyakFuse* polyak);
+int launch_critic_adam(const CriticDims& c, float* params2, const float* grad2, float* m, float* v, long long* steps,
+                       float lr, float b1, float b2, float eps, const Bf16Views* views, const PolyakFuse* polyak,
+                       cudaStream_t st);
+int critic_update_fused(const CriticDims& c, int B, float* params2, const __nv_bfloat16* pb, const float* obs, int S,
+                        const float* act, int A, const TdY& y, float* q, float* loss, float* grad2, void* ws,
+                        float* m, float* v, long long* steps, float lr, float b1, float b2, float eps,
+                        const Bf16Views* views, const PolyakFuse* polyak, cudaStream_t st);
+int critic_actor_fused(const CriticDims& c, int B, const float* params2, const __nv_bfloat16* pb, const float* obs,
+                       int S, const float* act, int A, float* q, float* loss, float* grad_act, float act_scale,
+                       void* ws, unsigned int* ticket, cudaStream_t st);
 // y: the TD target (critic update) or NULL (forward / actor objective). wait_before_loss (optional):
 // the stream waits on this event after the forward and before the loss (the target critics' Q' are
 // produced concurrently on another stream).

@@ -12,7 +12,7 @@
 //   dQ1/da      A = dz1 [16][H1] (smem)      B = W1T [in_p+32][H1]
 //   dW2         A = dZ2T [H2][Bp]            B = H1T [H1][Bp]
 //   dW1         A = dZ1T [H1][Bp]            B = XT  [in_q][Bp]
-#include "internal.h"
+#include "adam_body.cuh"
 
 namespace spk {
 
@@ -107,6 +107,7 @@ __device__ __forceinline__ void stage_wait(uint64_t* bar) {
       : "memory");
 }
 constexpr size_t kW2Smem = (size_t)HW * (HW + SPAD) * 2;   // staged W2 / W2T (135 KB)
+constexpr size_t kFusedSmem = kW2Smem + (size_t)RB * (512 + SPAD) * 2;   // + the X tile of the fused kernels
 
 // bf16 twin buffer: [2][P] (fp32 layout; P may be odd), then (from element blk_base(P), a multiple
 // of 8 so every row is 16-byte aligned for bulk copies) one block per critic holding every operand
@@ -339,7 +340,7 @@ __global__ void __launch_bounds__(256) critic_fwd_mma_kernel(
 }
 
 // phase timeline of CTA (0, 0) of the last data-backward launch (diagnostics; spikerl_debug_critic_trace)
-__device__ unsigned long long g_ctrace[8];
+__device__ unsigned long long g_ctrace[16];
 __device__ __forceinline__ void cstamp(int i) {
   if (blockIdx.x == 0 && blockIdx.y == 0 && threadIdx.x == 0) {
     unsigned long long t;
@@ -964,6 +965,612 @@ __global__ void __launch_bounds__(256) critic_gact_kernel(int B, int Bp, int S, 
   }
 }
 
+// ------------------------------------------------------------------ fused small-batch critic update
+// The latency regime (configs[1..2], configs[3] B = 100): the critic update of a TD3 step as ONE
+// launch instead of forward, data backward, weight / bias gradients and Adam (four dependent launches
+// of ~5 us each at B = 256, mostly ramp and operand latency). Three phases separated by grid-wide
+// barriers (every CTA resident: grid <= SMs, one CTA per SM by its shared memory):
+//   F  one 16-row tile of one critic per CTA: forward (W2 staged once), Q, dQ = 2 (Q - y) / B and the
+//      loss partial, dZ2, dH1 = dZ2 W2 read from the SAME staged W2 through ldmatrix.trans (no second
+//      135 KB staging of W2^T), dZ1; the ReLU masks stay in registers (no Z1 / Z2 planes); the
+//      transposed bf16 operands of the weight gradients go to the workspace;
+//   W  the weight-gradient tiles and the bias / w3 gradients of both critics, the loss scalar;
+//   A  Adam over both critics (+ the targets' Polyak step on actor updates), the bf16 views.
+// Every value is formed by the same operations in the same order as the four-launch path (the same
+// MMA k order, the same reductions, adam_body), so the result is bitwise that path's (tested).
+struct CritFusedArgs {
+  int B, Bp, S, A, inp, inq, in, nb;          // nb = Bp / RB row tiles per critic
+  const float* obs;
+  const float* act;
+  const __nv_bfloat16* pb;                    // bf16 twin buffer (mma layout)
+  long long P, tb, W1p, W2c, W1T, oW3, oB1, oB2, oB3, oW1, oW2;
+  float* params;                              // [2][P] fp32 masters (read: biases; written: Adam)
+  TdY y;
+  float act_scale;
+  float *q, *loss, *grad2, *dq, *part;
+  __nv_bfloat16 *XT, *H1T, *H2T, *dZ2T, *dZ1T;
+  float* grad_act;
+  // Adam
+  float *m, *v;
+  long long* counter;
+  unsigned int *ticket, *gbar;
+  float lr, b1, b2, eps;
+  double lnb1, lnb2;
+  float* tp;
+  float tau;
+  int dbg;   // SPIKERL_CRITIC_FUSED_DBG ablation bits (wrong results by design): 1 no bf16 views in
+             // Adam, 2 no Adam, 4 no bias tasks, 8 no weight-gradient tasks
+};
+
+// grid-wide barrier over a counter that is 0 at rest (the last CTA of the launch zeroes it); a
+// grid that could not be co-resident traps after ~2 s instead of hanging the device
+__device__ __forceinline__ void grid_barrier(unsigned int* ctr, unsigned int G, unsigned int& target) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    target += G;
+    __threadfence();
+    atomicAdd(ctr, 1u);
+    const long long t0 = clock64();
+    unsigned int v;
+    while (true) {
+      asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(ctr) : "memory");
+      if ((int)(v - target) >= 0) break;
+      if (clock64() - t0 > (1LL << 32)) __trap();
+    }
+  }
+  __syncthreads();
+}
+
+// acc[nt] += A[16 x K] * B with B stored [K][N] row-major in shared memory (n contiguous, row stride
+// ldb elements, column offset applied by the caller): the B fragments come from ldmatrix.trans, so
+// the values and the k order of every MMA are those of warp_mma_ss over the transposed matrix.
+template <int NT>
+__device__ __forceinline__ void warp_mma_ss_t(float (&acc)[NT][4], const __nv_bfloat16* A, int lda,
+                                              const __nv_bfloat16* Bkn, int ldb, int K) {
+  static_assert(NT % 2 == 0, "two n-tiles per ldmatrix.x4");
+  const int lane = threadIdx.x & 31, g = lane >> 2, t = lane & 3;
+  const __nv_bfloat16* a0 = A + g * lda + 2 * t;
+  const __nv_bfloat16* a1 = A + (g + 8) * lda + 2 * t;
+  // matrix j = lane / 8: k rows (j & 1) * 8 .. + 7 of n-tile (j >> 1)
+  const uint32_t bb = smem_addr(Bkn + ((lane & 7) + ((lane >> 3) & 1) * 8) * ldb + ((lane >> 4) * 8));
+#pragma unroll 4
+  for (int k0 = 0; k0 < K; k0 += 16) {
+    const uint32_t a[4] = {ld32(a0 + k0), ld32(a1 + k0), ld32(a0 + k0 + 8), ld32(a1 + k0 + 8)};
+#pragma unroll
+    for (int nt = 0; nt < NT; nt += 2) {
+      uint32_t r0, r1, r2, r3;
+      asm volatile("ldmatrix.sync.aligned.m8n8.x4.trans.shared.b16 {%0,%1,%2,%3}, [%4];"
+                   : "=r"(r0), "=r"(r1), "=r"(r2), "=r"(r3)
+                   : "r"(bb + (uint32_t)((k0 * ldb + nt * 8) * 2)));
+      mma16816(acc[nt], a, r0, r1);
+      mma16816(acc[nt + 1], a, r2, r3);
+    }
+  }
+}
+
+// 16-byte asynchronous global -> shared copies (LDGSTS: no register staging, any shared destination,
+// so padded rows need no per-row bulk copy; 256 per-row bulk copies issued at a launch's start stalled
+// the issuing threads for ~2 us, trace r02)
+__device__ __forceinline__ void cp16(void* sdst, const void* gsrc) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_addr(sdst)), "l"(gsrc) : "memory");
+}
+__device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void cp_wait_all() { asm volatile("cp.async.wait_group 0;" ::: "memory"); }
+// rows x (cols bf16, a multiple of 8) from global (row stride gld elements) into shared memory (row
+// stride sld elements), every thread of the CTA issuing its share
+__device__ __forceinline__ void cp_rows(__nv_bfloat16* sdst, int sld, const __nv_bfloat16* gsrc, long long gld, int rows,
+                                        int cols) {
+  const int cpr = cols >> 3;   // 16-byte chunks per row
+  for (int c = threadIdx.x; c < rows * cpr; c += blockDim.x) {
+    const int r = c / cpr, k = c - r * cpr;
+    cp16(sdst + (size_t)r * sld + 8 * k, gsrc + (size_t)r * gld + 8 * k);
+  }
+}
+
+// One output row's batch sum from a shared-memory row (bf16 values x[b], b < B), in exactly the order
+// of critic_bias_grads_kernel's warp-per-output form (lane-strided, four partial sums, xor tree);
+// dqs != NULL: the terms are dq[b] x[b] (dW3); x == NULL: the terms are dq[b] (db3).
+__device__ __forceinline__ float warp_row_sum(const __nv_bfloat16* x, const float* dqs, int B) {
+  const int lane = threadIdx.x & 31;
+  auto term = [&](int b) -> float {
+    if (!x) return dqs[b];
+    const float v = __bfloat162float(x[b]);
+    return dqs ? __fmul_rn(dqs[b], v) : v;
+  };
+  float s4[4] = {0.f, 0.f, 0.f, 0.f};
+  int b = lane;
+  for (; b + 3 * 32 < B; b += 4 * 32) {
+#pragma unroll
+    for (int k = 0; k < 4; ++k) s4[k] = __fadd_rn(s4[k], term(b + k * 32));
+  }
+  for (int k = 0; b < B; b += 32, ++k) s4[k & 3] = __fadd_rn(s4[k & 3], term(b));
+  float s = __fadd_rn(__fadd_rn(s4[0], s4[1]), __fadd_rn(s4[2], s4[3]));
+  for (int off = 16; off > 0; off >>= 1) s = __fadd_rn(s, __shfl_xor_sync(0xffffffffu, s, off));
+  return s;
+}
+
+// Phase W of the fused critic update, one task = one CTA: both operands of a 64 x 64 weight-gradient
+// tile staged whole in shared memory (cp.async, one round trip), the tile's MMAs (8 warps x 16 x 32,
+// K = Bp in the k order of critic_wgrad_mma_kernel), and the bias sums whose rows the tile holds:
+//   kind 0  dW2 tile (rows j2 of dZ2T, cols j1 of H1T); column block 0 also db2 of its rows;
+//   kind 1  dW1 tile (rows j of dZ1T, cols i of X^T); column block 0 also db1;
+//   kind 2  dW3 of 64 units (rows of H2T, times dQ); unit block 0 also db3.
+__device__ __forceinline__ int wtask_count(int in) { return 2 * 16 + 2 * 4 * ((in + 63) / 64) + 2 * 4; }
+__device__ __forceinline__ void crit_wtask(const CritFusedArgs& a, int task, __nv_bfloat16* sm) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, g = lane >> 2, t = lane & 3;
+  const int Bp = a.Bp, B = a.B, ld = Bp + SPAD;
+  const int nc1 = (a.in + 63) / 64;
+  int kind, z, rb, cb;
+  if (task < 32) { kind = 0; z = task / 16; rb = (task % 16) / 4; cb = task % 4; }
+  else if ((task -= 32) < 8 * nc1) { kind = 1; z = task / (4 * nc1); rb = (task % (4 * nc1)) / nc1; cb = task % nc1; }
+  else { task -= 8 * nc1; kind = 2; z = task / 4; rb = task % 4; cb = 0; }
+  const int m0 = rb * 64, n0 = cb * 64;
+  __nv_bfloat16* As = sm;
+  __nv_bfloat16* Bs = sm + (size_t)64 * ld;
+  float* dqs = reinterpret_cast<float*>(sm + (size_t)128 * ld);   // [B] (kind 2)
+  const __nv_bfloat16* Ag = (kind == 0 ? a.dZ2T : kind == 1 ? a.dZ1T : a.H2T) + ((size_t)z * HW + m0) * Bp;
+  cp_rows(As, ld, Ag, Bp, 64, Bp);
+  if (kind == 0) cp_rows(Bs, ld, a.H1T + ((size_t)z * HW + n0) * Bp, Bp, 64, Bp);
+  if (kind == 1) cp_rows(Bs, ld, a.XT + (size_t)n0 * Bp, Bp, 64, Bp);
+  cp_commit();
+  if (kind == 2)
+    for (int b = threadIdx.x; b < B; b += blockDim.x) dqs[b] = a.dq[(size_t)z * B + b];
+  cp_wait_all();
+  __syncthreads();
+  float* gz = a.grad2 + z * a.P;
+  if (kind < 2) {
+    const int ncols = kind == 0 ? HW : a.in;
+    const int wm = (warp & 3) * 16, wn = (warp >> 2) * 32;
+    float acc[4][4] = {};
+    warp_mma_ss<4>(acc, As + (size_t)wm * ld, ld, Bs + (size_t)wn * ld, ld, Bp);
+    float* out = gz + (kind == 0 ? a.oW2 : a.oW1);
+#pragma unroll
+    for (int nt = 0; nt < 4; ++nt)
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        const int r = m0 + wm + g + (e >> 1) * 8, col = n0 + wn + nt * 8 + 2 * t + (e & 1);
+        if (col < ncols) out[(size_t)r * ncols + col] = acc[nt][e];
+      }
+    if (cb == 0) {
+      for (int rr = warp; rr < 64; rr += 8) {
+        const float s = warp_row_sum(As + (size_t)rr * ld, nullptr, B);
+        if (lane == 0) gz[(kind == 0 ? a.oB2 : a.oB1) + m0 + rr] = s;
+      }
+    }
+  } else {
+    for (int rr = warp; rr < 64; rr += 8) {
+      const float s = warp_row_sum(As + (size_t)rr * ld, dqs, B);
+      if (lane == 0) gz[a.oW3 + m0 + rr] = s;
+    }
+    if (rb == 0 && warp == 0) {
+      const float s = warp_row_sum(nullptr, dqs, B);
+      if (lane == 0) gz[a.oB3] = s;
+    }
+  }
+  __syncthreads();   // the shared operands are reused by the CTA's next task
+}
+
+// Phase F for one 16-row tile (rows r0.., critic z). MODE 0: critic update (dQ from the TD target,
+// transposed operands, h2 and dQ stored for phase W); MODE 1: the actor objective on critic 0 (dQ =
+// act_scale, the loss partial sums Q, dQ1/da of the tile's rows).
+template <int MODE>
+__device__ __forceinline__ void crit_tile(const CritFusedArgs& a, int z, int tile, __nv_bfloat16* w2s, uint64_t* wbar,
+                                          __nv_bfloat16* xs, __nv_bfloat16* h1s, __nv_bfloat16* d2s,
+                                          __nv_bfloat16* d1s, float (*red)[RB], float* qs, float* dqs) {
+  const int tid = threadIdx.x, warp = tid >> 5;
+  const int lane = tid & 31, g = lane >> 2, t = lane & 3;
+  const int B = a.B, r0 = tile * RB;
+  const int in = a.S + a.A, ldx = a.inp + SPAD, ldh = HW + SPAD;
+  const long long P = a.P;
+  // W2 into shared memory (cp.async, non-blocking) while the X tile and layer 1 run
+  cp_rows(w2s, HW + SPAD, a.pb + blk_base(P) + z * a.tb + a.W2c, HW, HW, HW);
+  cp_commit();
+  {
+    float xv[2][16];
+#pragma unroll
+    for (int rr = 0; rr < 2; ++rr) {
+      const int b = r0 + warp + 8 * rr;
+#pragma unroll
+      for (int cc = 0; cc < 16; ++cc) {
+        const int i = lane + 32 * cc;
+        float v = 0.f;
+        if (b < B && i < in) v = i < a.S ? a.obs[(size_t)b * a.S + i] : a.act[(size_t)b * a.A + (i - a.S)];
+        xv[rr][cc] = v;
+      }
+    }
+#pragma unroll
+    for (int rr = 0; rr < 2; ++rr)
+#pragma unroll
+      for (int cc = 0; cc < 16; ++cc) {
+        const int i = lane + 32 * cc;
+        if (i < a.inp) xs[(warp + 8 * rr) * ldx + i] = __float2bfloat16_rn(xv[rr][cc]);
+      }
+  }
+  __syncthreads();
+  if (MODE == 0) cstamp(8);
+  if (MODE == 0 && z == 0) {
+    for (int idx = tid; idx < RB * a.inq; idx += 256) {
+      const int i = idx / RB, r = idx - i * RB;
+      a.XT[(size_t)i * a.Bp + r0 + r] = i < a.inp ? xs[r * ldx + i] : __float2bfloat16_rn(0.f);
+    }
+  }
+  const int n0 = warp * NTW * 8;
+  uint32_t m1 = 0u, m2 = 0u;   // ReLU masks of the warp's fragments (bit nt * 4 + e), rows < B only
+  {
+    const __nv_bfloat16* W1p = a.pb + blk_base(P) + z * a.tb + a.W1p;
+    const float* b1 = a.params + z * P + a.oB1;
+    float acc[NTW][4] = {};
+    float bias[NTW][2];
+#pragma unroll
+    for (int nt = 0; nt < NTW; ++nt) { bias[nt][0] = b1[n0 + nt * 8 + 2 * t]; bias[nt][1] = b1[n0 + nt * 8 + 2 * t + 1]; }
+    warp_mma<NTW>(acc, xs, ldx, W1p + (size_t)n0 * a.inp, a.inp, a.inp);
+#pragma unroll
+    for (int nt = 0; nt < NTW; ++nt)
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        const int r = g + (e >> 1) * 8, col = n0 + nt * 8 + 2 * t + (e & 1), b = r0 + r;
+        const float zz = __fadd_rn(acc[nt][e], bias[nt][e & 1]);
+        h1s[r * ldh + col] = b < B ? __float2bfloat16_rn(fmaxf(zz, 0.f)) : __float2bfloat16_rn(0.f);
+        if (b < B && zz > 0.f) m1 |= 1u << (nt * 4 + e);
+      }
+  }
+  __syncthreads();
+  if (MODE == 0) cstamp(9);
+  if (MODE == 0) {
+    for (int idx = tid; idx < RB * HW; idx += 256) {
+      const int col = idx / RB, r = idx - col * RB;
+      a.H1T[((size_t)z * HW + col) * a.Bp + r0 + r] = h1s[r * ldh + col];
+    }
+  }
+  float w3v[NTW][2];
+  {
+    const float* b2 = a.params + z * P + a.oB2;
+    const __nv_bfloat16* W3 = a.pb + z * P + a.oW3;
+    float acc[NTW][4] = {};
+    float bias[NTW][2];
+#pragma unroll
+    for (int nt = 0; nt < NTW; ++nt)
+#pragma unroll
+      for (int u = 0; u < 2; ++u) {
+        bias[nt][u] = b2[n0 + nt * 8 + 2 * t + u];
+        w3v[nt][u] = __bfloat162float(W3[n0 + nt * 8 + 2 * t + u]);
+      }
+    cp_wait_all();
+    __syncthreads();
+    if (MODE == 0) cstamp(10);
+    warp_mma_ss<NTW>(acc, h1s, ldh, w2s + (size_t)n0 * ldh, ldh, HW);
+    float qp[2] = {0.f, 0.f};
+#pragma unroll
+    for (int nt = 0; nt < NTW; ++nt)
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        const int r = g + (e >> 1) * 8, col = n0 + nt * 8 + 2 * t + (e & 1), b = r0 + r;
+        const float zz = __fadd_rn(acc[nt][e], bias[nt][e & 1]);
+        const float h = bf16_round(fmaxf(zz, 0.f));
+        qp[e >> 1] = __fmaf_rn(h, w3v[nt][e & 1], qp[e >> 1]);
+        if (MODE == 0) d2s[r * ldh + col] = __float2bfloat16_rn(h);   // h2 (bf16-exact), staged for H2T
+        if (b < B && zz > 0.f) m2 |= 1u << (nt * 4 + e);
+      }
+#pragma unroll
+    for (int hh = 0; hh < 2; ++hh) {
+      float s = qp[hh];
+      s = __fadd_rn(s, __shfl_xor_sync(0xffffffffu, s, 1));
+      s = __fadd_rn(s, __shfl_xor_sync(0xffffffffu, s, 2));
+      if (t == 0) red[warp][g + hh * 8] = s;
+    }
+  }
+  __syncthreads();
+  if (MODE == 0) {   // h2^T for dW3 (rows past B are never read)
+    for (int idx = tid; idx < RB * HW; idx += 256) {
+      const int col = idx / RB, r = idx - col * RB;
+      a.H2T[((size_t)z * HW + col) * a.Bp + r0 + r] = d2s[r * ldh + col];
+    }
+  }
+  if (tid < RB) {
+    float s = red[0][tid];
+    for (int w = 1; w < NWARP; ++w) s = __fadd_rn(s, red[w][tid]);
+    const float qv = __fadd_rn(s, a.params[z * P + a.oB3]);
+    qs[tid] = qv;
+    if (r0 + tid < B) a.q[(size_t)z * B + r0 + tid] = qv;
+  }
+  __syncthreads();
+  if (MODE == 0) cstamp(11);
+  if (warp == 0) {   // dQ and the loss partial, as critic_bwd_data_mma_kernel forms them
+    float d = 0.f, c = 0.f;
+    const int b = r0 + lane;
+    if (lane < RB && b < B) {
+      const float qv = qs[lane];
+      if (MODE == 0) {
+        const float e = __fsub_rn(qv, a.y.get(b, z));
+        d = __fdiv_rn(__fmul_rn(2.0f, e), (float)B);
+        c = __fmul_rn(e, e);
+      } else {
+        d = a.act_scale;
+        c = qv;
+      }
+      a.dq[(size_t)z * B + b] = d;
+    }
+    if (lane < RB) dqs[lane] = d;
+    float cs[RB];
+#pragma unroll
+    for (int r = 0; r < RB; ++r) cs[r] = __shfl_sync(0xffffffffu, c, r);
+    if (lane == 0) {
+      float sum = 0.f;
+#pragma unroll
+      for (int r = 0; r < RB; ++r) sum = __fadd_rn(sum, cs[r]);
+      a.part[z * a.nb + tile] = sum;
+    }
+  }
+  __syncthreads();
+  if (MODE == 0) cstamp(12);
+#pragma unroll
+  for (int nt = 0; nt < NTW; ++nt)
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      const int r = g + (e >> 1) * 8, col = n0 + nt * 8 + 2 * t + (e & 1);
+      d2s[r * ldh + col] = __float2bfloat16_rn((m2 >> (nt * 4 + e)) & 1u ? __fmul_rn(dqs[r], w3v[nt][e & 1]) : 0.f);
+    }
+  __syncthreads();
+  if (MODE == 0) {
+    for (int idx = tid; idx < RB * HW; idx += 256) {
+      const int j = idx / RB, r = idx - j * RB;
+      a.dZ2T[((size_t)z * HW + j) * a.Bp + r0 + r] = d2s[r * ldh + j];
+    }
+  }
+  {
+    float acc[NTW][4] = {};
+    warp_mma_ss_t<NTW>(acc, d2s, ldh, w2s + n0, ldh, HW);
+#pragma unroll
+    for (int nt = 0; nt < NTW; ++nt)
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        const int r = g + (e >> 1) * 8, col = n0 + nt * 8 + 2 * t + (e & 1);
+        d1s[r * ldh + col] = __float2bfloat16_rn((m1 >> (nt * 4 + e)) & 1u ? acc[nt][e] : 0.f);
+      }
+  }
+  __syncthreads();
+  if (MODE == 0) cstamp(13);
+  if (MODE == 0) {
+    for (int idx = tid; idx < RB * HW; idx += 256) {
+      const int j = idx / RB, r = idx - j * RB;
+      a.dZ1T[((size_t)z * HW + j) * a.Bp + r0 + r] = d1s[r * ldh + j];
+    }
+    return;
+  }
+  // MODE 1: columns [S, S+A) of dZ1 W1 (the tail of critic_bwd_data_mma_kernel)
+  {
+    __shared__ float gpart[NWARP][RB][32];
+    const __nv_bfloat16* W1T = a.pb + blk_base(P) + a.W1T;
+    const int c0 = a.S & ~7;
+    for (int cb = c0; cb < a.S + a.A; cb += 32) {
+      float acc[4][4] = {};
+      const int kw = warp * (HW / NWARP);
+      warp_mma<4, 2>(acc, d1s + kw, ldh, W1T + (size_t)cb * HW + kw, HW, HW / NWARP);
+#pragma unroll
+      for (int nt = 0; nt < 4; ++nt)
+#pragma unroll
+        for (int e = 0; e < 4; ++e) gpart[warp][g + (e >> 1) * 8][nt * 8 + 2 * t + (e & 1)] = acc[nt][e];
+      __syncthreads();
+      for (int idx = tid; idx < RB * 32; idx += 256) {
+        const int r = idx >> 5, cl = idx & 31, col = cb + cl, b = r0 + r;
+        float sum = 0.f;
+#pragma unroll
+        for (int w = 0; w < NWARP; ++w) sum = __fadd_rn(sum, gpart[w][r][cl]);
+        if (b < B && col >= a.S && col < a.S + a.A) a.grad_act[(size_t)b * a.A + (col - a.S)] = sum;
+      }
+      __syncthreads();
+    }
+  }
+}
+
+// Phase A of the fused critic update: Adam over both critics (adam_elem, the arithmetic of
+// adam_kernel) with the layout-aware bf16 stores. W2 goes in 32 x 32 tiles: the master / moment
+// accesses and the row-major bf16 copies are coalesced along j1, and the transposed copy W2T (the
+// data backward's operand) leaves through a shared-memory transpose as 64-byte row segments instead
+// of one scattered 2-byte store per element (ncu/trace r02: the scattered view stores were 60 % of
+// the Adam phase). Everything else (W1, biases, w3, b3) is a flat loop through store_views. The last
+// CTA stores the step count and zeroes the ticket and the grid-barrier counter.
+template <bool POL>
+__device__ __forceinline__ void critic_adam_phase(const CritFusedArgs& a, const Bf16Views& views, const Bf16Views& tviews,
+                                                  unsigned int cta, unsigned int G) {
+  __shared__ float s_coef[2];
+  __shared__ long long s_t;
+  __shared__ unsigned short tile[32][34];
+  if (threadIdx.x == 0) {
+    const long long tt = *(volatile long long*)a.counter + 1;
+    s_t = tt;
+    adam_coefs(a.lr, a.lnb1, a.lnb2, tt, &s_coef[0], &s_coef[1]);
+  }
+  __syncthreads();
+  const float step_size = s_coef[0], bc2_sqrt = s_coef[1];
+  const float b1 = a.b1, b2 = a.b2, omb1 = 1.0f - b1, omb2 = 1.0f - b2, eps = a.eps;
+  const float tau = a.tau, omt = 1.0f - tau;
+  const long long P = a.P, nW2 = (long long)HW * HW, nrest = P - nW2;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const bool tiled = views.kind == 2 && (!POL || tviews.kind == 2);
+  const int ntile = tiled ? 2 * (HW / 32) * (HW / 32) : 0;
+  const long long nflat = tiled ? 2 * nrest : 2 * P;
+  const int nft = (int)((nflat + 1023) / 1024);
+  for (int task = (int)cta; task < ntile + nft; task += (int)G) {
+    if (task < ntile) {
+      const int z = task / 64, tr = (task % 64) / 8, tc = task % 8;
+      const int j1 = tc * 32 + lane;
+      float pp[4], gg[4], mm[4], vv[4], tt[4];
+      long long e[4];
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        const int j2 = tr * 32 + warp * 4 + k;
+        e[k] = z * P + a.oW2 + (long long)j2 * HW + j1;
+        pp[k] = a.params[e[k]]; gg[k] = a.grad2[e[k]]; mm[k] = a.m[e[k]]; vv[k] = a.v[e[k]];
+        if constexpr (POL) tt[k] = a.tp[e[k]];
+      }
+      __nv_bfloat16* blk = views.out + blk_base(P) + z * views.tb;
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        const int j2 = tr * 32 + warp * 4 + k;
+        pp[k] = adam_elem(pp[k], gg[k], mm[k], vv[k], b1, omb1, b2, omb2, bc2_sqrt, eps, step_size);
+        a.params[e[k]] = pp[k]; a.m[e[k]] = mm[k]; a.v[e[k]] = vv[k];
+        const unsigned short h = op16_bits(pp[k], false);
+        reinterpret_cast<unsigned short*>(views.out)[e[k]] = h;
+        reinterpret_cast<unsigned short*>(blk)[views.W2c + (long long)j2 * HW + j1] = h;
+        tile[warp * 4 + k][lane] = h;
+        if constexpr (POL) {
+          const float x = __fadd_rn(__fmul_rn(tau, pp[k]), __fmul_rn(omt, tt[k]));
+          a.tp[e[k]] = x;
+          const unsigned short ht = op16_bits(x, false);
+          reinterpret_cast<unsigned short*>(tviews.out)[e[k]] = ht;
+          __nv_bfloat16* tblk = tviews.out + blk_base(P) + z * tviews.tb;
+          reinterpret_cast<unsigned short*>(tblk)[tviews.W2c + (long long)j2 * HW + j1] = ht;
+          if (tviews.w2t) reinterpret_cast<unsigned short*>(tblk)[tviews.W2T + (long long)j1 * HW + j2] = ht;
+        }
+      }
+      if (views.w2t) {
+        __syncthreads();
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {   // W2T[j1][j2]: row j1 = tc 32 + warp 4 + k, the 32 j2 of the tile along the lanes
+          const int j1r = warp * 4 + k;
+          reinterpret_cast<unsigned short*>(blk)[views.W2T + (long long)(tc * 32 + j1r) * HW + tr * 32 + lane] =
+              tile[lane][j1r];
+        }
+        __syncthreads();
+      }
+    } else {
+      const long long f0 = (long long)(task - ntile) * 1024 + threadIdx.x;
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        const long long f = f0 + 256 * k;
+        if (f >= nflat) break;
+        long long ee;
+        if (tiled) {
+          const int z = f >= nrest ? 1 : 0;
+          const long long l = f - z * nrest;
+          ee = z * P + (l < a.oW2 ? l : l + nW2);
+        } else {
+          ee = f;
+        }
+        float mv = a.m[ee], vv = a.v[ee];
+        const float pn = adam_elem(a.params[ee], a.grad2[ee], mv, vv, b1, omb1, b2, omb2, bc2_sqrt, eps, step_size);
+        a.params[ee] = pn; a.m[ee] = mv; a.v[ee] = vv;
+        store_views(views, (size_t)ee, pn);
+        if constexpr (POL) {
+          const float x = __fadd_rn(__fmul_rn(tau, pn), __fmul_rn(omt, a.tp[ee]));
+          a.tp[ee] = x;
+          store_views(tviews, (size_t)ee, x);
+        }
+      }
+    }
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    const unsigned int done = atomicAdd(a.ticket, 1u);
+    if (done == G - 1) {
+      *a.counter = s_t;
+      *a.ticket = 0u;
+      *a.gbar = 0u;
+      __threadfence();
+    }
+  }
+}
+
+// The critic's Adam (+ Polyak) as a launch of its own (the separate-launch path): the tiled,
+// layout-aware element loop of the fused update (coalesced W2T stores), same arithmetic as adam_kernel.
+template <bool POL>
+__global__ void __launch_bounds__(256) critic_adam_kernel(const __grid_constant__ CritFusedArgs a,
+                                                          const __grid_constant__ Bf16Views views,
+                                                          const __grid_constant__ Bf16Views tviews) {
+  pdl_wait();
+  pdl_trigger();
+  critic_adam_phase<POL>(a, views, tviews, blockIdx.x, gridDim.x);
+}
+
+template <bool POL>
+__global__ void __launch_bounds__(256, 1) critic_update_fused_kernel(const __grid_constant__ CritFusedArgs a,
+                                                                      const __grid_constant__ Bf16Views views,
+                                                                      const __grid_constant__ Bf16Views tviews) {
+  extern __shared__ __align__(128) uint8_t dsm[];
+  __nv_bfloat16* const w2s = (__nv_bfloat16*)dsm;
+  __nv_bfloat16* const xs = (__nv_bfloat16*)(dsm + kW2Smem);   // [RB][512 + SPAD]
+  __shared__ __align__(8) uint64_t wbar;
+  __shared__ __align__(16) __nv_bfloat16 h1s[RB * (HW + SPAD)];
+  __shared__ __align__(16) __nv_bfloat16 d2s[RB * (HW + SPAD)];
+  __shared__ __align__(16) __nv_bfloat16 d1s[RB * (HW + SPAD)];
+  __shared__ float red[NWARP][RB];
+  __shared__ float qs[RB], dqs[RB];
+  const unsigned int G = gridDim.x, cta = blockIdx.x;
+  if (threadIdx.x == 0) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_addr(&wbar)) : "memory");
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  cstamp(0);
+  pdl_wait();   // no early trigger: a dependent launched before this grid is resident could take its SMs
+  cstamp(1);
+  unsigned int target = 0;
+  // ---- F
+  if ((int)cta < 2 * a.nb)
+    crit_tile<0>(a, (int)cta / a.nb, (int)cta % a.nb, w2s, &wbar, xs, h1s, d2s, d1s, red, qs, dqs);
+  cstamp(2);
+  grid_barrier(a.gbar, G, target);
+  cstamp(3);
+  // ---- W: weight-gradient tiles with their bias sums (crit_wtask), then the loss
+  {
+    const int nt = wtask_count(a.in);
+    for (int task = (int)cta; task < nt; task += (int)G)
+      if (!(a.dbg & 8)) crit_wtask(a, task, w2s);
+    if (cta == G - 1 && a.loss) final_loss(a.part, a.nb, 2, 0, a.B, a.loss);
+  }
+  cstamp(4);
+  grid_barrier(a.gbar, G, target);
+  cstamp(5);
+  pdl_trigger();   // every CTA of this grid is resident by now
+  // ---- A: Adam over both critics (+ Polyak of the targets), the bf16 views; the last CTA stores the
+  // step count and zeroes the barrier counter
+  if (a.dbg & 2) {
+    if (cta == 0 && threadIdx.x == 0) *a.gbar = 0u;
+  } else if (a.dbg & 1) {
+    const Bf16Views none{};
+    adam_body<POL>(a.params, a.grad2, a.m, a.v, 2 * (size_t)a.P, a.counter, a.lr, a.b1, a.b2, a.eps, 0, 0, 0.f,
+                   a.ticket, none, nullptr, 2.f, 0.5f, 2000, a.lnb1, a.lnb2, a.tp, a.tau, none, cta, G, a.gbar);
+  } else {
+    critic_adam_phase<POL>(a, views, tviews, cta, G);
+  }
+  cstamp(6);
+}
+
+// The actor objective's critic pass of a TD3 actor step as one launch (forward of critic 0 at
+// (s, pi(s)), dQ = act_scale, data backward, dQ1/da, the actor loss -mean Q by the last CTA).
+__global__ void __launch_bounds__(256, 1) critic_actor_fused_kernel(const __grid_constant__ CritFusedArgs a) {
+  extern __shared__ __align__(128) uint8_t dsm[];
+  __nv_bfloat16* const w2s = (__nv_bfloat16*)dsm;
+  __nv_bfloat16* const xs = (__nv_bfloat16*)(dsm + kW2Smem);   // [RB][512 + SPAD]
+  __shared__ __align__(8) uint64_t wbar;
+  __shared__ __align__(16) __nv_bfloat16 h1s[RB * (HW + SPAD)];
+  __shared__ __align__(16) __nv_bfloat16 d2s[RB * (HW + SPAD)];
+  __shared__ __align__(16) __nv_bfloat16 d1s[RB * (HW + SPAD)];
+  __shared__ float red[NWARP][RB];
+  __shared__ float qs[RB], dqs[RB];
+  __shared__ bool last;
+  if (threadIdx.x == 0) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_addr(&wbar)) : "memory");
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  pdl_wait();
+  pdl_trigger();
+  crit_tile<1>(a, 0, blockIdx.x, w2s, &wbar, xs, h1s, d2s, d1s, red, qs, dqs);
+  if (threadIdx.x == 0) {
+    __threadfence();
+    last = atomicAdd(a.ticket, 1u) == gridDim.x - 1;
+  }
+  __syncthreads();
+  if (last) {
+    __threadfence();
+    if (a.loss) final_loss(a.part, a.nb, 1, 1, a.B, a.loss);
+    if (threadIdx.x == 0) *a.ticket = 0u;
+  }
+}
+
 }  // namespace
 
 bool critic_mma_ok(const CriticDims& c) { return c.bf16 && c.H1 == HW && c.H2 == HW && c.in <= 512; }
@@ -980,6 +1587,11 @@ size_t critic_mma_ws_bytes(const CriticDims& c, int B) {
   return total;
 }
 
+void critic_bf16_layout(const CriticDims& c, long long* o) {
+  const MmaLayout L = mma_layout(c);
+  o[0] = blk_base(L.P); o[1] = L.tb; o[2] = L.W1p; o[3] = L.W1T; o[4] = L.W2T; o[5] = L.W2c; o[6] = L.inp; o[7] = L.inq;
+}
+
 Bf16Views critic_bf16_views(const CriticDims& c, __nv_bfloat16* out) {
   Bf16Views v{};
   if (!out || !c.bf16) return v;
@@ -994,6 +1606,7 @@ Bf16Views critic_bf16_views(const CriticDims& c, __nv_bfloat16* out) {
   v.oW2 = (long long)c.off[SPIKERL_CRITIC_W2];
   v.W1p = L.W1p; v.W1T = L.W1T; v.W2T = L.W2T; v.W2c = L.W2c;
   v.in = c.in; v.H1 = c.H1; v.H2 = c.H2; v.inp = L.inp;
+  v.w1t_lo = 0; v.w1t_hi = c.in; v.w2t = 1;   // everything (callers narrow it: TD3's targets, action rows)
   v.Pd = make_fastdiv((uint32_t)v.P); v.ind = make_fastdiv((uint32_t)c.in); v.H1d = make_fastdiv((uint32_t)c.H1);
   return v;
 }
@@ -1205,9 +1818,122 @@ int critic_mma_fwd_bwd(const CriticDims& c, int B, const float* params2, const _
   return SPIKERL_OK;
 }
 
+
+// ------------------------------------------------------------------ fused small-batch launches
+// SPIKERL_CRITIC_FUSED: 1 = every eligible batch (B <= 512), 0 = never; default from B = 384 (r02 A/B,
+// one box: configs[2] B = 512 116.6 -> 110.5 us per update; configs[1] B = 256 84.5 -> 86.9 and configs[3]
+// B = 100 114.2 -> 135.3 slower: there the separate forward overlaps the target path and the phases'
+// dependent round trips outweigh the launches saved)
+bool critic_fused_ok(const CriticDims& c, int B) {
+  static const int env = [] { const char* e = getenv("SPIKERL_CRITIC_FUSED"); return e ? atoi(e) : -1; }();
+  if (env == 0 || (env < 0 && B < 384)) return false;
+  return critic_mma_ok(c) && !critic_tc_ok(c, B) && wgrad_splits(B) == 0 && 2 * (round_up(B, RB) / RB) <= num_sms();
+}
+
+static CritFusedArgs fused_args(const CriticDims& c, int B, float* params2, const __nv_bfloat16* pb, const float* obs,
+                                int S, const float* act, int A, void* ws) {
+  const MmaLayout L = mma_layout(c);
+  const MmaWs w = mma_carve(c, B, ws, nullptr);
+  CritFusedArgs a{};
+  a.B = B; a.Bp = round_up(B, RB); a.S = S; a.A = A; a.inp = L.inp; a.inq = L.inq; a.in = c.in; a.nb = a.Bp / RB;
+  a.obs = obs; a.act = act; a.pb = pb;
+  a.P = L.P; a.tb = L.tb; a.W1p = L.W1p; a.W2c = L.W2c; a.W1T = L.W1T;
+  a.oW3 = (long long)c.off[SPIKERL_CRITIC_W3]; a.oB1 = (long long)c.off[SPIKERL_CRITIC_B1];
+  a.oB2 = (long long)c.off[SPIKERL_CRITIC_B2]; a.oB3 = (long long)c.off[SPIKERL_CRITIC_B3];
+  a.oW1 = (long long)c.off[SPIKERL_CRITIC_W1]; a.oW2 = (long long)c.off[SPIKERL_CRITIC_W2];
+  a.params = params2;
+  a.dq = w.dq; a.part = w.part; a.H2T = w.H2T;
+  a.XT = w.XT; a.H1T = w.H1T; a.dZ2T = w.dZ2T; a.dZ1T = w.dZ1T;
+  return a;
+}
+
+// grid of the fused update: every row tile of both critics, and one CTA per SM for the weight-gradient
+// and Adam phases (64 CTAs: configs[1] 102 vs 86 us per update, r02) (SPIKERL_CRITIC_FUSED_G overrides; always <= the SM count: the grid barriers need
+// the whole grid resident)
+static int fused_grid(int tiles) {
+  static const int env = [] { const char* e = getenv("SPIKERL_CRITIC_FUSED_G"); return e ? atoi(e) : 148; }();
+  int g = tiles > env ? tiles : env;
+  return g < num_sms() ? g : num_sms();
+}
+
+int critic_update_fused(const CriticDims& c, int B, float* params2, const __nv_bfloat16* pb, const float* obs, int S,
+                        const float* act, int A, const TdY& y, float* q, float* loss, float* grad2, void* ws,
+                        float* m, float* v, long long* steps, float lr, float b1, float b2, float eps,
+                        const Bf16Views* views, const PolyakFuse* polyak, cudaStream_t st) {
+  if (!critic_fused_ok(c, B)) { set_error("critic_update_fused: unsupported shape"); return SPIKERL_E_UNSUPPORTED; }
+  if (((uintptr_t)params2 | (uintptr_t)grad2 | (uintptr_t)m | (uintptr_t)v | (uintptr_t)(polyak ? polyak->t : nullptr)) & 15) {
+    set_error("critic_update_fused: buffers must be 16-byte aligned");
+    return SPIKERL_E_ARG;
+  }
+  CritFusedArgs a = fused_args(c, B, params2, pb, obs, S, act, A, ws);
+  a.y = y; a.q = q; a.loss = loss; a.grad2 = grad2;
+  a.m = m; a.v = v; a.counter = steps;
+  a.ticket = (unsigned int*)(steps + 1);           // Adam's ticket (low word of steps[1])
+  a.gbar = (unsigned int*)(steps + 1) + 1;         // the grid barrier (high word; 0 at rest)
+  a.lr = lr; a.b1 = b1; a.b2 = b2; a.eps = eps; a.lnb1 = log((double)b1); a.lnb2 = log((double)b2);
+  a.tp = polyak ? polyak->t : nullptr; a.tau = polyak ? polyak->tau : 0.f;
+  static const int dbg = [] { const char* e = getenv("SPIKERL_CRITIC_FUSED_DBG"); return e ? atoi(e) : 0; }();
+  a.dbg = dbg;
+  const Bf16Views none{};
+  const int G = fused_grid(2 * a.nb);
+  const double fl = 2.0 * B * 2 * ((double)c.in * HW + (double)HW * HW + HW) * 3.0;
+  ProfScope ps_(polyak ? "critic_update_fused_polyak" : "critic_update_fused", PB_TENSOR, fl, 0.0, st);
+  if (polyak) {
+    SPK_SMEM_ATTR(critic_update_fused_kernel<true>, kFusedSmem);
+    pdl(critic_update_fused_kernel<true>, G, 256, kFusedSmem, st)(a, views ? *views : none,
+                                                               polyak->views ? *polyak->views : none);
+  } else {
+    SPK_SMEM_ATTR(critic_update_fused_kernel<false>, kFusedSmem);
+    pdl(critic_update_fused_kernel<false>, G, 256, kFusedSmem, st)(a, views ? *views : none, none);
+  }
+  SPK_LAUNCHED();
+  return SPIKERL_OK;
+}
+
+bool critic_adam_ok(const CriticDims& c, const Bf16Views* views, const PolyakFuse* polyak) {
+  return critic_mma_ok(c) && views && views->kind == 2 && (!polyak || (polyak->views && polyak->views->kind == 2));
+}
+
+int launch_critic_adam(const CriticDims& c, float* params2, const float* grad2, float* m, float* v, long long* steps,
+                       float lr, float b1, float b2, float eps, const Bf16Views* views, const PolyakFuse* polyak,
+                       cudaStream_t st) {
+  if (!critic_adam_ok(c, views, polyak)) { set_error("critic adam: needs the tensor-core critic's bf16 views"); return SPIKERL_E_ARG; }
+  const MmaLayout L = mma_layout(c);
+  CritFusedArgs a{};
+  a.P = L.P; a.oW2 = (long long)c.off[SPIKERL_CRITIC_W2];
+  a.params = params2; a.grad2 = const_cast<float*>(grad2); a.m = m; a.v = v; a.counter = steps;
+  a.ticket = (unsigned int*)(steps + 1); a.gbar = (unsigned int*)(steps + 1) + 1;
+  a.lr = lr; a.b1 = b1; a.b2 = b2; a.eps = eps; a.lnb1 = log((double)b1); a.lnb2 = log((double)b2);
+  a.tp = polyak ? polyak->t : nullptr; a.tau = polyak ? polyak->tau : 0.f;
+  const long long nrest = L.P - (long long)HW * HW;
+  const int tasks = 2 * (HW / 32) * (HW / 32) + (int)((2 * nrest + 1023) / 1024);
+  const int G = tasks < 2 * num_sms() ? tasks : 2 * num_sms();
+  const Bf16Views none{};
+  ProfScope ps_(polyak ? "adam_polyak" : "adam", PB_HBM, 0.0, (polyak ? 40.0 : 28.0) * 2 * L.P, st);
+  if (polyak)
+    pdl(critic_adam_kernel<true>, G, 256, 0, st)(a, *views, *polyak->views);
+  else
+    pdl(critic_adam_kernel<false>, G, 256, 0, st)(a, *views, none);
+  SPK_LAUNCHED();
+  return SPIKERL_OK;
+}
+
+int critic_actor_fused(const CriticDims& c, int B, const float* params2, const __nv_bfloat16* pb, const float* obs,
+                       int S, const float* act, int A, float* q, float* loss, float* grad_act, float act_scale,
+                       void* ws, unsigned int* ticket, cudaStream_t st) {
+  if (!critic_fused_ok(c, B)) { set_error("critic_actor_fused: unsupported shape"); return SPIKERL_E_UNSUPPORTED; }
+  CritFusedArgs a = fused_args(c, B, const_cast<float*>(params2), pb, obs, S, act, A, ws);
+  a.q = q; a.loss = loss; a.grad_act = grad_act; a.act_scale = act_scale; a.ticket = ticket;
+  ProfScope ps_("critic_actor_fused", PB_TENSOR, 2.0 * B * ((double)c.in * HW + 2.0 * HW * HW + HW), 0.0, st);
+  SPK_SMEM_ATTR(critic_actor_fused_kernel, kFusedSmem);
+  pdl(critic_actor_fused_kernel, a.nb, 256, kFusedSmem, st)(a);
+  SPK_LAUNCHED();
+  return SPIKERL_OK;
+}
+
 }  // namespace spk
 
 extern "C" int spikerl_debug_critic_trace(unsigned long long* host8) {
-  if (cudaMemcpyFromSymbol(host8, spk::g_ctrace, sizeof(unsigned long long) * 8) != cudaSuccess) return 5;
+  if (cudaMemcpyFromSymbol(host8, spk::g_ctrace, sizeof(unsigned long long) * 16) != cudaSuccess) return 5;
   return 0;
 }

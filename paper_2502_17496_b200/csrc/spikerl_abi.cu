@@ -397,8 +397,27 @@ static Td3Ws td3_ws_layout(const ActorDims& ad, const CriticDims& cd, int B) {
 // polyak (actor steps): the target soft update t <- tau p + (1 - tau) t of that network, fused into its
 // Adam launch (one launch less at the end of the update's critical path); with the fused allreduce
 // + Adam kernel or loss scaling it stays a launch of its own right after, same arithmetic.
-static int critic_optimise(const spikerl_td3_bufs* b, spikerl_comm* comm, const spikerl_td3_cfg* hp, size_t Pc,
-                           const Bf16Views* cv, float* amp_c, cudaStream_t st, const PolyakFuse* polyak = nullptr) {
+// bf16 views of a TD3 critic: the online twins keep W1T only for the action rows [S, S+A) (dQ1/da), the
+// targets (forward only) neither W1T nor W2T
+static Bf16Views td3_critic_views(const CriticDims& cd, const ActorDims& ad, void* buf, bool target) {
+  Bf16Views v = critic_bf16_views(cd, ad.bf16 ? (__nv_bfloat16*)buf : nullptr);
+  if (v.kind == 2) {
+    v.w1t_lo = target ? 0 : ad.S;
+    v.w1t_hi = target ? 0 : ad.S + ad.A;
+    v.w2t = target ? 0 : 1;
+  }
+  return v;
+}
+
+// the whole critic update as one launch (k_critic_mma.cu critic_update_fused): bf16 small-batch critic,
+// one GPU (no gradient allreduce between the gradients and Adam), no loss scaling
+static bool critic_update_fusable(const CriticDims& cd, int B, const spikerl_td3_bufs* b, spikerl_comm* comm) {
+  return !comm && !b->amp && critic_fused_ok(cd, B);
+}
+
+static int critic_optimise(const spikerl_td3_bufs* b, spikerl_comm* comm, const spikerl_td3_cfg* hp, const CriticDims& cd,
+                           size_t Pc, const Bf16Views* cv, float* amp_c, cudaStream_t st,
+                           const PolyakFuse* polyak = nullptr) {
   if (comm && b->fused_critic) {
     SPK_TRY(fused_adam_launch(b->fused_critic, b->m_critic, b->v_critic, b->adam_steps, hp->lr_critic, hp->beta1,
                               hp->beta2, hp->eps, 0, 0, 0.f, (unsigned int*)(b->adam_steps + 1), cv, st));
@@ -406,6 +425,12 @@ static int critic_optimise(const spikerl_td3_bufs* b, spikerl_comm* comm, const 
   }
   SPK_TRY(spikerl_allreduce_grads(comm, b->grad_critic, 2 * Pc, st));
   if (amp_c) SPK_TRY(launch_amp_check(b->grad_critic, 2 * Pc, amp_c, st));
+  // the tensor-core critic: the layout-aware Adam (coalesced W2T stores); SPIKERL_CRITIC_ADAM_TILED=0: the
+  // flat adam_kernel (same result)
+  static const bool tiled = [] { const char* e = getenv("SPIKERL_CRITIC_ADAM_TILED"); return !(e && e[0] == '0'); }();
+  if (tiled && !amp_c && critic_adam_ok(cd, cv, polyak))
+    return launch_critic_adam(cd, b->critic, b->grad_critic, b->m_critic, b->v_critic, b->adam_steps, hp->lr_critic,
+                              hp->beta1, hp->beta2, hp->eps, cv, polyak, st);
   SPK_TRY(launch_adam(b->critic, b->grad_critic, b->m_critic, b->v_critic, 2 * Pc, b->adam_steps, hp->lr_critic,
                       hp->beta1, hp->beta2, hp->eps, 0, 0, 0.f, (unsigned int*)(b->adam_steps + 1), cv, st, amp_c,
                       hp->amp_growth, hp->amp_backoff, hp->amp_interval, amp_c ? nullptr : polyak));
@@ -495,6 +520,15 @@ size_t spikerl_actor_bf16_bytes(const spikerl_actor_cfg* cfg) {
 size_t spikerl_critic_bf16_bytes(const spikerl_critic_cfg* cfg) {
   CriticDims d;
   return critic_dims(cfg, &d) == SPIKERL_OK ? align_up(critic_bf16_elems(d) * 2, 16) : 0;
+}
+
+int spikerl_critic_bf16_layout(const spikerl_critic_cfg* cfg, long long* out8) {
+  CriticDims d;
+  SPK_TRY(critic_dims(cfg, &d));
+  if (!out8) { set_error("spikerl_critic_bf16_layout: null output"); return SPIKERL_E_ARG; }
+  if (!critic_mma_ok(d)) { set_error("spikerl_critic_bf16_layout: not the tensor-core critic"); return SPIKERL_E_UNSUPPORTED; }
+  critic_bf16_layout(d, out8);
+  return SPIKERL_OK;
 }
 
 size_t spikerl_actor_tape_bytes(const spikerl_actor_cfg* cfg, int batch) {
@@ -788,24 +822,35 @@ int spikerl_td3_update(const spikerl_actor_cfg* acfg, const spikerl_critic_cfg* 
   }
   // 3. critic forward Q(s, a) overlaps branch A; the loss waits for Q'; grads, allreduce, Adam
   // (the bf16 working copies are kept current by the optimiser kernels themselves: Bf16Views)
-  const Bf16Views cv = critic_bf16_views(cd, ad.bf16 ? (__nv_bfloat16*)b->critic_bf16 : nullptr);
-  const Bf16Views ctv = critic_bf16_views(cd, ad.bf16 ? (__nv_bfloat16*)b->critic_t_bf16 : nullptr);
+  const Bf16Views cv = td3_critic_views(cd, ad, b->critic_bf16, false);
+  const Bf16Views ctv = td3_critic_views(cd, ad, b->critic_t_bf16, true);
   const Bf16Views av = actor_bf16_views(ad, ad.bf16 ? (__nv_bfloat16*)b->actor_bf16 : nullptr);
   const Bf16Views atv = actor_bf16_views(ad, ad.bf16 ? (__nv_bfloat16*)b->actor_t_bf16 : nullptr);
   float* const amp_c = b->amp, * const amp_a = b->amp ? b->amp + 4 : nullptr;   // loss scaling (or none)
   const TdY tdy{nullptr, r, dn, qt, hp->gamma, B, y};   // y = r + gamma (1 - d) min Q' formed inside the loss
-  SPK_TRY(critic_fwd_bwd(cd, B, b->critic, cbf, s, ad.S, a, ad.A, &tdy, q, losses, b->grad_critic, nullptr, 0.f, 2,
-                         cws, st, aux->ev[1], amp_c));
   // actor steps: the critic targets' soft update rides on the critic's Adam launch
   const PolyakFuse cpol{b->critic_t, hp->tau, &ctv};
-  SPK_TRY(critic_optimise(b, comm, hp, Pc, &cv, amp_c, st, actor_step ? &cpol : nullptr));
+  if (critic_update_fusable(cd, B, b, comm)) {
+    SPK_CHECK_CUDA(cudaStreamWaitEvent(st, aux->ev[1], 0));   // Q' from branch A
+    SPK_TRY(critic_update_fused(cd, B, b->critic, cbf, s, ad.S, a, ad.A, tdy, q, losses, b->grad_critic, cws,
+                                b->m_critic, b->v_critic, b->adam_steps, hp->lr_critic, hp->beta1, hp->beta2, hp->eps,
+                                &cv, actor_step ? &cpol : nullptr, st));
+  } else {
+    SPK_TRY(critic_fwd_bwd(cd, B, b->critic, cbf, s, ad.S, a, ad.A, &tdy, q, losses, b->grad_critic, nullptr, 0.f, 2,
+                           cws, st, aux->ev[1], amp_c));
+    SPK_TRY(critic_optimise(b, comm, hp, cd, Pc, &cv, amp_c, st, actor_step ? &cpol : nullptr));
+  }
   // 4. delayed actor update + targets
   if (actor_step) {
     SPK_CHECK_CUDA(cudaStreamWaitEvent(st, aux->ev[3], 0));   // pi(s) from branch B
     // actor loss -mean Q1(s, pi(s)): formed by the mma critic's data-backward launch itself
     const bool mma = critic_mma_ok(cd);
-    SPK_TRY(critic_fwd_bwd(cd, B, b->critic, cbf, s, ad.S, api, ad.A, nullptr, q, mma ? losses + 1 : nullptr, nullptr,
-                           ga, -1.0f / (float)B, 1, cws, st, nullptr, amp_a));
+    if (!amp_a && critic_fused_ok(cd, B))
+      SPK_TRY(critic_actor_fused(cd, B, b->critic, cbf, s, ad.S, api, ad.A, q, losses + 1, ga, -1.0f / (float)B, cws,
+                                 (unsigned int*)(b->adam_steps + 3) + 1, st));
+    else
+      SPK_TRY(critic_fwd_bwd(cd, B, b->critic, cbf, s, ad.S, api, ad.A, nullptr, q, mma ? losses + 1 : nullptr, nullptr,
+                             ga, -1.0f / (float)B, 1, cws, st, nullptr, amp_a));
     if (!mma) {
       pdl(neg_mean_kernel, 1, 256, 0, st)(B, q, losses + 1);
       SPK_LAUNCHED();
@@ -933,26 +978,38 @@ int spikerl_td3_update_pair(const spikerl_actor_cfg* acfg, const spikerl_critic_
     SPK_TRY(actor_forward_impl(ad, B, b->actor, abf, sl[1].s, sl[1].api, sl[1].tape, sB));
   }
   SPK_CHECK_CUDA(cudaEventRecord(aux->ev[3], sB));
-  const Bf16Views cv = critic_bf16_views(cd, ad.bf16 ? (__nv_bfloat16*)b->critic_bf16 : nullptr);
-  const Bf16Views ctv = critic_bf16_views(cd, ad.bf16 ? (__nv_bfloat16*)b->critic_t_bf16 : nullptr);
+  const Bf16Views cv = td3_critic_views(cd, ad, b->critic_bf16, false);
+  const Bf16Views ctv = td3_critic_views(cd, ad, b->critic_t_bf16, true);
   const Bf16Views av = actor_bf16_views(ad, ad.bf16 ? (__nv_bfloat16*)b->actor_bf16 : nullptr);
   const Bf16Views atv = actor_bf16_views(ad, ad.bf16 ? (__nv_bfloat16*)b->actor_t_bf16 : nullptr);
   float* const amp_c = b->amp, * const amp_a = b->amp ? b->amp + 4 : nullptr;   // loss scaling (or none)
   // the two critic updates, in order
   const PolyakFuse cpol{b->critic_t, hp->tau, &ctv};
+  const bool fuse_c = critic_update_fusable(cd, B, b, comm);
   for (int i = 0; i < 2; ++i) {
     const Slot& x = sl[i];
     const TdY tdy{nullptr, x.r, x.dn, x.qt, hp->gamma, B, x.y};
+    if (fuse_c) {
+      SPK_CHECK_CUDA(cudaStreamWaitEvent(st, evA[i], 0));
+      SPK_TRY(critic_update_fused(cd, B, b->critic, cbf, x.s, ad.S, x.a, ad.A, tdy, x.q, losses, b->grad_critic, x.cws,
+                                  b->m_critic, b->v_critic, b->adam_steps, hp->lr_critic, hp->beta1, hp->beta2,
+                                  hp->eps, &cv, i == 1 ? &cpol : nullptr, st));
+      continue;
+    }
     SPK_TRY(critic_fwd_bwd(cd, B, b->critic, cbf, x.s, ad.S, x.a, ad.A, &tdy, x.q, losses, b->grad_critic, nullptr,
                            0.f, 2, x.cws, st, evA[i], amp_c));
-    SPK_TRY(critic_optimise(b, comm, hp, Pc, &cv, amp_c, st, i == 1 ? &cpol : nullptr));
+    SPK_TRY(critic_optimise(b, comm, hp, cd, Pc, &cv, amp_c, st, i == 1 ? &cpol : nullptr));
   }
   // delayed actor update + targets (update k + 1), exactly as spikerl_td3_update's actor step
   const Slot& x = sl[1];
   SPK_CHECK_CUDA(cudaStreamWaitEvent(st, aux->ev[3], 0));
   const bool mma = critic_mma_ok(cd);
-  SPK_TRY(critic_fwd_bwd(cd, B, b->critic, cbf, x.s, ad.S, x.api, ad.A, nullptr, x.q, mma ? losses + 1 : nullptr,
-                         nullptr, x.ga, -1.0f / (float)B, 1, x.cws, st, nullptr, amp_a));
+  if (!amp_a && critic_fused_ok(cd, B))
+    SPK_TRY(critic_actor_fused(cd, B, b->critic, cbf, x.s, ad.S, x.api, ad.A, x.q, losses + 1, x.ga, -1.0f / (float)B,
+                               x.cws, (unsigned int*)(b->adam_steps + 3) + 1, st));
+  else
+    SPK_TRY(critic_fwd_bwd(cd, B, b->critic, cbf, x.s, ad.S, x.api, ad.A, nullptr, x.q, mma ? losses + 1 : nullptr,
+                           nullptr, x.ga, -1.0f / (float)B, 1, x.cws, st, nullptr, amp_a));
   if (!mma) {
     pdl(neg_mean_kernel, 1, 256, 0, st)(B, x.q, losses + 1);
     SPK_LAUNCHED();

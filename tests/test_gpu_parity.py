@@ -507,6 +507,49 @@ def test_td3_schedule_independent_subprocess(name, B):
     assert len(set(digests.values())) == 1, digests
 
 
+@pytest.mark.parametrize("name,B", [("cfg1", 256), ("cfg1", 200), ("cfg2", 512), ("cfg3s", 100), ("cfg3s", 37)])
+def test_td3_fused_critic_matches_separate_launches_subprocess(name, B):
+    """The fused small-batch critic launches (the whole critic update, forward to Adam + Polyak, with
+    grid barriers; the actor objective's critic pass) are bitwise the separate launches
+    (SPIKERL_CRITIC_FUSED=0), and the layout-aware critic Adam is bitwise the flat adam_kernel
+    (SPIKERL_CRITIC_ADAM_TILED=0): two single updates, then three captured update pairs end in identical
+    parameters, targets, Adam moments and step counts, losses and dQ1/da, at several grid sizes."""
+    import os, subprocess, sys
+    code = (
+        "import hashlib, numpy as np, torch\n"
+        "import synthgen as sg, paper_2502_17496_b200 as pk\n"
+        f"shape, _, _ = sg.preset({name!r}); B = {B}\n"
+        "S, A = shape.obs_dim, shape.act_dim\n"
+        "rng = np.random.default_rng(5)\n"
+        "cs = sg.CriticShape(S + A, precision='bf16')\n"
+        "td3 = pk.TD3(pk.actor_cfg_from(shape), pk.critic_cfg(S + A), pk.td3_cfg(B), pk.replay_fill(4 * B, S, A, seed=4), seed=7)\n"
+        "td3.load(sg.actor_params(shape, rng), sg.critic_params(cs, rng), sg.critic_params(cs, rng))\n"
+        "h = hashlib.sha256()\n"
+        "for k in (1, 2):\n"
+        "    td3.update(k)\n"
+        "    torch.cuda.synchronize()\n"
+        "    h.update(td3.losses.cpu().numpy().tobytes())\n"
+        "td3.update_pair(3)\n"
+        "td3.capture_pair()\n"
+        "for _ in range(3): td3.replay_pair()\n"
+        "torch.cuda.synchronize()\n"
+        "for t in (td3.actor, td3.actor_t, td3.critic, td3.critic_t, td3.m_actor, td3.v_actor, td3.m_critic,\n"
+        "          td3.v_critic, td3.adam_steps, td3.losses, td3.critic_bf16, td3.critic_t_bf16):\n"
+        "    h.update(t.cpu().numpy().tobytes())\n"
+        "print('digest', h.hexdigest())\n")
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    digests = {}
+    for label, extra in (("fused", {"SPIKERL_CRITIC_FUSED": "1"}), ("separate", {"SPIKERL_CRITIC_FUSED": "0"}),
+                         ("separate_flat_adam", {"SPIKERL_CRITIC_FUSED": "0", "SPIKERL_CRITIC_ADAM_TILED": "0"}),
+                         ("fused_g148", {"SPIKERL_CRITIC_FUSED": "1", "SPIKERL_CRITIC_FUSED_G": "148"}),
+                         ("fused_gmin", {"SPIKERL_CRITIC_FUSED": "1", "SPIKERL_CRITIC_FUSED_G": "1"})):
+        r = subprocess.run([sys.executable, "-c", code], cwd=root, capture_output=True, text=True, timeout=600,
+                           env=dict(os.environ, PYTHONPATH=root, **extra))
+        assert r.returncode == 0, (label, r.stdout[-1500:] + r.stderr[-1500:])
+        digests[label] = [l for l in r.stdout.splitlines() if l.startswith("digest")][-1]
+    assert len(set(digests.values())) == 1, digests
+
+
 @pytest.mark.parametrize("obs,act", [(17, 6), (111, 8)])
 def test_td3_bf16_copies_track_masters(obs, act):
     """Adam / Polyak write the bf16 working copies in place (Bf16Views): after several updates they
@@ -525,9 +568,15 @@ def test_td3_bf16_copies_track_masters(obs, act):
     kept = [t.clone() for t in (td3.actor_bf16, td3.actor_t_bf16, td3.critic_bf16, td3.critic_t_bf16)]
     td3.refresh()
     torch.cuda.synchronize()
-    for name, a, b in zip(("actor", "actor_t", "critic", "critic_t"), kept,
-                          (td3.actor_bf16, td3.actor_t_bf16, td3.critic_bf16, td3.critic_t_bf16)):
+    for name, a, b in zip(("actor", "actor_t"), kept[:2], (td3.actor_bf16, td3.actor_t_bf16)):
         assert torch.equal(a, b), name
+    # critics: every element the updates maintain (all but the transposed blocks nothing reads:
+    # the targets' W1T / W2T, the online W1T rows outside the action columns)
+    for name, a, b, tgt in (("critic", kept[2], td3.critic_bf16, False), ("critic_t", kept[3], td3.critic_t_bf16, True)):
+        m = td3.bf16_maintained(tgt)
+        a16, b16 = a.view(torch.int16)[:m.numel()], b.view(torch.int16)[:m.numel()]
+        assert torch.equal(a16[m], b16[m]), name
+        assert int((~m).sum()) < m.numel() // 2, name
 
 
 def test_td3_graph_replay_matches_eager():

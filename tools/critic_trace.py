@@ -15,7 +15,7 @@ td3.load(sg.actor_params(shape, rng), sg.critic_params(cs, rng), sg.critic_param
 for k in range(1, 9):   # ends with an actor step: the last launch forms dQ1/da
     td3.update(k)
 torch.cuda.synchronize()
-buf = (C.c_ulonglong * 8)()
+buf = (C.c_ulonglong * 16)()
 _lib.lib().spikerl_debug_critic_trace(buf)
 v = list(buf)
 names = ["entry", "after_pdl", "d2s_ticket", "dZ2T", "l2_mma", "dZ1T", "grad_act"]
