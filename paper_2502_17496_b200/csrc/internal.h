@@ -253,6 +253,7 @@ int critic_mma_fwd_bwd(const CriticDims& c, int B, const float* params2, const _
 // spikerl_td3_bufs.adam_steps (the grid barrier uses the high word of steps[1]); ticket (actor pass):
 // a zero-at-rest counter word.
 bool critic_fused_ok(const CriticDims& c, int B);
+bool critic_act_fused_ok(const CriticDims& c, int B);
 // the critic's Adam (+ the targets' Polyak) with coalesced stores of the transposed bf16 copy; bitwise
 // launch_adam's result (no loss scaling)
 bool critic_adam_ok(const CriticDims& c, const Bf16Views* views, const PolyakFuse* polyak);

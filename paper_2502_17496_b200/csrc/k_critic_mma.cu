@@ -1918,10 +1918,16 @@ int launch_critic_adam(const CriticDims& c, float* params2, const float* grad2, 
   return SPIKERL_OK;
 }
 
+// the actor objective's critic pass as one launch: SPIKERL_CRITIC_ACT_FUSED=0 turns it off
+bool critic_act_fused_ok(const CriticDims& c, int B) {
+  static const int env = [] { const char* e = getenv("SPIKERL_CRITIC_ACT_FUSED"); return e ? atoi(e) : 1; }();
+  return env != 0 && critic_mma_ok(c) && !critic_tc_ok(c, B) && wgrad_splits(B) == 0;
+}
+
 int critic_actor_fused(const CriticDims& c, int B, const float* params2, const __nv_bfloat16* pb, const float* obs,
                        int S, const float* act, int A, float* q, float* loss, float* grad_act, float act_scale,
                        void* ws, unsigned int* ticket, cudaStream_t st) {
-  if (!critic_fused_ok(c, B)) { set_error("critic_actor_fused: unsupported shape"); return SPIKERL_E_UNSUPPORTED; }
+  if (!critic_act_fused_ok(c, B)) { set_error("critic_actor_fused: unsupported shape"); return SPIKERL_E_UNSUPPORTED; }
   CritFusedArgs a = fused_args(c, B, const_cast<float*>(params2), pb, obs, S, act, A, ws);
   a.q = q; a.loss = loss; a.grad_act = grad_act; a.act_scale = act_scale; a.ticket = ticket;
   ProfScope ps_("critic_actor_fused", PB_TENSOR, 2.0 * B * ((double)c.in * HW + 2.0 * HW * HW + HW), 0.0, st);

@@ -845,7 +845,7 @@ int spikerl_td3_update(const spikerl_actor_cfg* acfg, const spikerl_critic_cfg* 
     SPK_CHECK_CUDA(cudaStreamWaitEvent(st, aux->ev[3], 0));   // pi(s) from branch B
     // actor loss -mean Q1(s, pi(s)): formed by the mma critic's data-backward launch itself
     const bool mma = critic_mma_ok(cd);
-    if (!amp_a && critic_fused_ok(cd, B))
+    if (!amp_a && critic_act_fused_ok(cd, B))
       SPK_TRY(critic_actor_fused(cd, B, b->critic, cbf, s, ad.S, api, ad.A, q, losses + 1, ga, -1.0f / (float)B, cws,
                                  (unsigned int*)(b->adam_steps + 3) + 1, st));
     else
@@ -1004,7 +1004,7 @@ int spikerl_td3_update_pair(const spikerl_actor_cfg* acfg, const spikerl_critic_
   const Slot& x = sl[1];
   SPK_CHECK_CUDA(cudaStreamWaitEvent(st, aux->ev[3], 0));
   const bool mma = critic_mma_ok(cd);
-  if (!amp_a && critic_fused_ok(cd, B))
+  if (!amp_a && critic_act_fused_ok(cd, B))
     SPK_TRY(critic_actor_fused(cd, B, b->critic, cbf, x.s, ad.S, x.api, ad.A, x.q, losses + 1, x.ga, -1.0f / (float)B,
                                x.cws, (unsigned int*)(b->adam_steps + 3) + 1, st));
   else
