@@ -509,19 +509,17 @@ __global__ void __launch_bounds__(256) critic_bwd_data_mma_kernel(
 // ------------------------------------------------------------------ weight gradients
 // blockIdx.z = critic; blockIdx.y < HW/16: dW2 row tile; else dW1 row tile. Each CTA: 16 rows x
 // 256 columns (4 warps x 64), K = Bp batch rows. Writes the fp32 master layout.
-__global__ void __launch_bounds__(256) critic_wgrad_mma_kernel(
-    int Bp, int in, int inq, long long P, long long oW1, long long oW2, const __nv_bfloat16* __restrict__ XT,
-    const __nv_bfloat16* __restrict__ H1T, const __nv_bfloat16* __restrict__ dZ2T,
+__device__ __forceinline__ void critic_wgrad_mma_body(
+    int bx, int by, int z, int Bp, int in, int inq, long long P, long long oW1, long long oW2,
+    const __nv_bfloat16* __restrict__ XT, const __nv_bfloat16* __restrict__ H1T, const __nv_bfloat16* __restrict__ dZ2T,
     const __nv_bfloat16* __restrict__ dZ1T, float* __restrict__ grad2) {
-  pdl_wait();
-  pdl_trigger();
-  const int z = blockIdx.z, tid = threadIdx.x, warp = tid >> 5;
+  const int tid = threadIdx.x, warp = tid >> 5;
   const int lane = tid & 31, g = lane >> 2, t = lane & 3;
   const int ntile = HW / RB;
-  const bool w2 = blockIdx.y < ntile;
-  const int m0 = (w2 ? blockIdx.y : blockIdx.y - ntile) * RB;
+  const bool w2 = by < ntile;
+  const int m0 = (w2 ? by : by - ntile) * RB;
   const int ncols = w2 ? HW : in;
-  const int n0 = blockIdx.x * 256 + warp * NTW * 8;
+  const int n0 = bx * 256 + warp * NTW * 8;
   if (n0 >= ncols) return;
   const __nv_bfloat16* Am = (w2 ? dZ2T : dZ1T) + ((size_t)z * HW + m0) * Bp;
   const __nv_bfloat16* Bm = w2 ? H1T + (size_t)z * HW * Bp : XT;
@@ -738,6 +736,46 @@ __global__ void __launch_bounds__(256) critic_bias_grads_kernel(int B, int Bp, l
     else if (o < 2 * HW) base[oB2 + (o - HW)] = s;
     else if (o < 3 * HW) base[oW3 + (o - 2 * HW)] = s;
     else base[oB3] = s;
+  }
+}
+
+// Small batches (B <= 512): the weight gradients (critic_wgrad_mma_body, grid rows [0, 2 HW / 16)) and
+// the bias / w3 gradients (critic_bias_grads_kernel's warp-per-output form, 8 outputs per CTA, the
+// grid rows after them) as ONE launch: no side-stream fork / join in front of the critic's Adam (a
+// joined branch is a full graph edge, so the Adam launch could not start early; same per-output
+// arithmetic, bitwise the two-launch result).
+__global__ void __launch_bounds__(256) critic_wgrad_mma_kernel(
+    int Bp, int in, int inq, long long P, long long oW1, long long oW2, const __nv_bfloat16* __restrict__ XT,
+    const __nv_bfloat16* __restrict__ H1T, const __nv_bfloat16* __restrict__ dZ2T,
+    const __nv_bfloat16* __restrict__ dZ1T, float* __restrict__ grad2, int B, long long oB1, long long oB2,
+    long long oW3, long long oB3, const float* __restrict__ dq, const float* __restrict__ Hh2) {
+  pdl_wait();
+  pdl_trigger();
+  const int ntile = HW / RB;
+  if ((int)blockIdx.y < 2 * ntile) {
+    critic_wgrad_mma_body(blockIdx.x, blockIdx.y, blockIdx.z, Bp, in, inq, P, oW1, oW2, XT, H1T, dZ2T, dZ1T, grad2);
+    return;
+  }
+  const int z = blockIdx.z;
+  const int bt = (blockIdx.y - 2 * ntile) * gridDim.x + blockIdx.x;   // bias CTA index
+  const int o = bt * 8 + (threadIdx.x >> 5), lane = threadIdx.x & 31;
+  const int nout = 3 * HW + 1;
+  if (o >= nout) return;
+  float s4[4] = {0.f, 0.f, 0.f, 0.f};
+  int b = lane;
+  for (; b + 3 * 32 < B; b += 4 * 32) {
+#pragma unroll
+    for (int k = 0; k < 4; ++k) s4[k] = __fadd_rn(s4[k], bias_row_term(o, z, b + k * 32, Bp, B, dZ1T, dZ2T, dq, Hh2, nullptr));
+  }
+  for (int k = 0; b < B; b += 32, ++k) s4[k & 3] = __fadd_rn(s4[k & 3], bias_row_term(o, z, b, Bp, B, dZ1T, dZ2T, dq, Hh2, nullptr));
+  float sum = __fadd_rn(__fadd_rn(s4[0], s4[1]), __fadd_rn(s4[2], s4[3]));
+  for (int off = 16; off > 0; off >>= 1) sum = __fadd_rn(sum, __shfl_xor_sync(0xffffffffu, sum, off));
+  if (lane == 0) {
+    float* base = grad2 + z * P;
+    if (o < HW) base[oB1 + o] = sum;
+    else if (o < 2 * HW) base[oB2 + (o - HW)] = sum;
+    else if (o < 3 * HW) base[oW3 + (o - 2 * HW)] = sum;
+    else base[oB3] = sum;
   }
 }
 
@@ -1769,7 +1807,24 @@ int critic_mma_fwd_bwd(const CriticDims& c, int B, const float* params2, const _
         oW3, L.W1T, L.W2T, w.Z1, w.Z2, w.dZ2T, w.dZ1T, grad_act, want_params ? 1 : 0, dq_scale);
     SPK_LAUNCHED();
   }
-  if (want_params) {
+  // merged weight + bias gradient launch: SPIKERL_CRITIC_WG_MERGE=0/1 never / always; default for inputs
+  // wider than 256 (A/B r02, one box: configs[3] B = 100 118.0 -> 112.2 us per update; configs[1] (in 23)
+  // 81.9 -> 83.7, where the side-stream bias kernel overlapping the weight-gradient launch is faster)
+  static const int merge_env = [] { const char* e = getenv("SPIKERL_CRITIC_WG_MERGE"); return e ? atoi(e) : -1; }();
+  const bool merge = merge_env < 0 ? L.inq > HW : merge_env != 0;
+  if (want_params && wgrad_splits(B) == 0 && merge) {
+    // small batches: weight and bias / w3 gradients as one launch (critic_wgrad_mma_kernel)
+    ProfScope ps_("critic_wgrad_mma", PB_TENSOR, 2.0 * B * nz * ((double)HW * HW + (double)HW * c.in), 0.0, st);
+    const int nwx = cdiv(L.inq > HW ? L.inq : HW, 256);
+    const int nby = cdiv(cdiv(3 * HW + 1, 8), nwx);
+    dim3 grid(nwx, 2 * (HW / RB) + nby, nz);
+    pdl(critic_wgrad_mma_kernel, grid, 256, 0, st)(Bp, c.in, L.inq, L.P, (long long)c.off[SPIKERL_CRITIC_W1],
+                                                  (long long)c.off[SPIKERL_CRITIC_W2], w.XT, w.H1T, w.dZ2T, w.dZ1T,
+                                                  grad2, B, (long long)c.off[SPIKERL_CRITIC_B1],
+                                                  (long long)c.off[SPIKERL_CRITIC_B2], oW3,
+                                                  (long long)c.off[SPIKERL_CRITIC_B3], w.dq, w.Hh2);
+    SPK_LAUNCHED();
+  } else if (want_params) {
     // the bias / w3 gradients run next to the weight-gradient GEMM
     AuxPool* aux = nullptr;
     SPK_TRY(aux_pool(&aux));
@@ -1782,13 +1837,7 @@ int critic_mma_fwd_bwd(const CriticDims& c, int B, const float* params2, const _
     {
       ProfScope ps_("critic_wgrad_mma", PB_TENSOR, 2.0 * B * nz * ((double)HW * HW + (double)HW * c.in), 0.0, st);
       const int ws = wgrad_splits(B);
-      if (ws == 0) {
-        dim3 grid(cdiv(L.inq > HW ? L.inq : HW, 256), 2 * (HW / RB), nz);
-        pdl(critic_wgrad_mma_kernel, grid, 256, 0, st)(Bp, c.in, L.inq, L.P, (long long)c.off[SPIKERL_CRITIC_W1],
-                                                      (long long)c.off[SPIKERL_CRITIC_W2], w.XT, w.H1T, w.dZ2T, w.dZ1T,
-                                                      grad2);
-        SPK_LAUNCHED();
-      } else if (tc_wgrad_ok(c, w, Bp)) {
+      if (tc_wgrad_ok(c, w, Bp)) {
         // tcgen05: both weight gradients of both critics as one split-K launch of K-major operand
         // tiles (the mma.sync split kernel below took 104 us at configs[3] B = 4096)
         const long long msz = (long long)HW * HW + (long long)HW * L.inq;
@@ -1797,6 +1846,12 @@ int critic_mma_fwd_bwd(const CriticDims& c, int B, const float* params2, const _
         pdl(critic_wgrad_reduce_cm_kernel, dim3(cdiv(HW + c.in, 32), HW / 32, 2), dim3(32, 32), 0, st)(
             splits, c.in, msz, L.P, (long long)c.off[SPIKERL_CRITIC_W1], (long long)c.off[SPIKERL_CRITIC_W2], w.wpart,
             grad2);
+        SPK_LAUNCHED();
+      } else if (ws == 0) {   // SPIKERL_CRITIC_WG_MERGE=0: the weight gradients alone (bias CTAs none)
+        dim3 grid(cdiv(L.inq > HW ? L.inq : HW, 256), 2 * (HW / RB), nz);
+        pdl(critic_wgrad_mma_kernel, grid, 256, 0, st)(Bp, c.in, L.inq, L.P, (long long)c.off[SPIKERL_CRITIC_W1],
+                                                      (long long)c.off[SPIKERL_CRITIC_W2], w.XT, w.H1T, w.dZ2T, w.dZ1T,
+                                                      grad2, B, 0, 0, 0, 0, w.dq, w.Hh2);
         SPK_LAUNCHED();
       } else {
         // K split in multiples of 16 batch rows (Bp is a multiple of RB = 16)

@@ -542,6 +542,8 @@ def test_td3_fused_critic_matches_separate_launches_subprocess(name, B):
     for label, extra in (("fused", {"SPIKERL_CRITIC_FUSED": "1"}), ("separate", {"SPIKERL_CRITIC_FUSED": "0"}),
                          ("separate_flat_adam", {"SPIKERL_CRITIC_FUSED": "0", "SPIKERL_CRITIC_ADAM_TILED": "0",
                                                  "SPIKERL_CRITIC_ACT_FUSED": "0"}),
+                         ("separate_merged_wg", {"SPIKERL_CRITIC_FUSED": "0", "SPIKERL_CRITIC_WG_MERGE": "1"}),
+                         ("separate_split_wg", {"SPIKERL_CRITIC_FUSED": "0", "SPIKERL_CRITIC_WG_MERGE": "0"}),
                          ("fused_g148", {"SPIKERL_CRITIC_FUSED": "1", "SPIKERL_CRITIC_FUSED_G": "148"}),
                          ("fused_gmin", {"SPIKERL_CRITIC_FUSED": "1", "SPIKERL_CRITIC_FUSED_G": "1"})):
         r = subprocess.run([sys.executable, "-c", code], cwd=root, capture_output=True, text=True, timeout=600,
