@@ -169,3 +169,21 @@ def test_workspace_sizes_host_only(L):
     # the TD3 workspace holds the actor workspace, a tape and two critic workspaces (online + target)
     assert w > a2 + lib.spikerl_actor_tape_bytes(C.byref(c), 256) + 2 * lib.spikerl_critic_workspace_bytes(C.byref(cc), 256) - 1
     assert lib.spikerl_actor_workspace_bytes(C.byref(c), 0) == 0
+
+
+@pytest.mark.parametrize("in_dim", [23, 119, 393, 512])
+def test_critic_bf16_layout(L, in_dim):
+    """spikerl_critic_bf16_layout (host only): the per-critic blocks W1p | W1T | W2T | W2 tile the bf16
+    buffer spikerl_critic_bf16_bytes sizes, after the [2][P] plain copy; other critics are refused."""
+    from paper_2502_17496_b200 import critic_cfg, critic_offsets
+    c = critic_cfg(in_dim)
+    o = (C.c_longlong * 8)()
+    assert L.lib().spikerl_critic_bf16_layout(C.byref(c), o) == 0
+    base, tb, w1p, w1t, w2t, w2, inp, inq = list(o)
+    P = critic_offsets(c)[-1]
+    H = 256
+    assert base >= 2 * P and base % 8 == 0 and inp % 16 == 0 and inp >= in_dim and inq >= inp
+    assert (w1p, w1t, w2t, w2) == (0, H * inp, H * inp + inq * H, H * inp + inq * H + H * H)
+    assert tb == w2 + H * H
+    assert L.lib().spikerl_critic_bf16_bytes(C.byref(c)) >= 2 * (base + 2 * tb)
+    assert L.lib().spikerl_critic_bf16_layout(C.byref(critic_cfg(in_dim, precision="fp32")), o) != 0
