@@ -235,6 +235,21 @@ struct TdY {
     return v;
   }
 };
+// The target actor's decoder and TD3 target-policy smoothing formed inside the target critics' forward
+// launch (the action columns of its input tile), one launch less on the target path: per (row, action)
+// dec_fwd_kernel's arithmetic, then smooth_action; the z = 0 CTAs store a' (act_out, act_tape) and a~
+// (ts.at) as the decoder launch would, and advance the counter when ts.advance.
+struct CriticDecode {
+  const uint8_t* counts;   // [B][A D] output-layer spike counts (NULL: no decoding)
+  const float* Wd;
+  const float* bd;
+  int D, T;
+  float* act_out;
+  float* act_tape;
+  TargetSmooth ts;
+};
+constexpr int kDecMaxD = 16;
+bool critic_decode_ok(const CriticDims& c, int B, int A, int D);   // small-batch tensor-core critic, A <= 32, D <= 16
 size_t critic_ws_bytes(const CriticDims& c, int B);
 size_t critic_bf16_elems(const CriticDims& c);   // twin pair incl. the mma path's padded/transposed copies
 int launch_critic_refresh(const CriticDims& c, const float* params2, __nv_bfloat16* out, cudaStream_t st);
@@ -244,7 +259,8 @@ size_t critic_mma_ws_bytes(const CriticDims& c, int B);
 int critic_mma_fwd_bwd(const CriticDims& c, int B, const float* params2, const __nv_bfloat16* pb, const float* obs,
                        int S, const float* act, int A, const TdY* y, float* q, float* loss, float* grad2,
                        float* grad_act, float act_scale, int nz, void* ws, cudaStream_t st,
-                       cudaEvent_t wait_before_loss = nullptr, const float* dq_scale = nullptr);
+                       cudaEvent_t wait_before_loss = nullptr, const float* dq_scale = nullptr,
+                       const CriticDecode* dec = nullptr);
 // Fused small-batch critic launches (bf16 tensor-core critic, B <= 512; SPIKERL_CRITIC_FUSED=0 turns
 // them off): the whole critic update of a TD3 step (forward, loss, data backward, weight / bias
 // gradients, Adam (+ the targets' Polyak step when polyak != NULL) and the bf16 views) as one launch
@@ -274,7 +290,8 @@ int critic_fwd_bwd(const CriticDims& c, int B, const float* params2, const __nv_
                    const float* obs, int S, const float* act, int A, const TdY* y, float* q,
                    float* loss, float* grad2, float* grad_act, float act_scale, int n_critics,
                    void* ws, cudaStream_t st, cudaEvent_t wait_before_loss = nullptr,
-                   const float* dq_scale = nullptr);   // dq_scale: device loss scale applied to dQ
+                   const float* dq_scale = nullptr,   // dq_scale: device loss scale applied to dQ
+                   const CriticDecode* dec = nullptr);   // forward only: actions decoded in the launch
 
 // ---- replay / TD3 glue (k_replay.cu)
 // minibatch destinations of one gather launch (1 slot, or the 2 updates of a pair); idx[slot] = NULL:

@@ -99,9 +99,22 @@ __global__ void dec_fwd_kernel(int B, int A, int D, int T, const uint8_t* __rest
   const int N3 = A * D;
   const float invT = 1.0f / (float)T;
   float pre = 0.f;
-  for (int e = 0; e < D; ++e) {
-    const float fr = (float)counts[(size_t)b * N3 + j * D + e] / (float)T;
-    pre = __fadd_rn(pre, __fmul_rn(Wd[j * D + e], fr));
+  if (D <= kDecMaxD) {   // every count and weight requested before the (ordered) sum: one round trip
+    uint32_t cv[kDecMaxD];
+    float wv[kDecMaxD];
+#pragma unroll
+    for (int e = 0; e < kDecMaxD; ++e) {
+      cv[e] = e < D ? counts[(size_t)b * N3 + j * D + e] : 0u;
+      wv[e] = e < D ? Wd[j * D + e] : 0.f;
+    }
+#pragma unroll
+    for (int e = 0; e < kDecMaxD; ++e)
+      if (e < D) pre = __fadd_rn(pre, __fmul_rn(wv[e], (float)cv[e] / (float)T));
+  } else {
+    for (int e = 0; e < D; ++e) {
+      const float fr = (float)counts[(size_t)b * N3 + j * D + e] / (float)T;
+      pre = __fadd_rn(pre, __fmul_rn(Wd[j * D + e], fr));
+    }
   }
   (void)invT;
   pre = __fadd_rn(pre, bd[j]);

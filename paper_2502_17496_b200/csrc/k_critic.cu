@@ -293,10 +293,11 @@ size_t critic_ws_bytes(const CriticDims& c, int B) {
 int critic_fwd_bwd(const CriticDims& c, int B, const float* params2, const __nv_bfloat16* pb16,
                    const float* obs, int S, const float* act, int A, const TdY* y, float* q,
                    float* loss, float* grad2, float* grad_act, float act_scale, int nz, void* ws,
-                   cudaStream_t st, cudaEvent_t wait_before_loss, const float* dq_scale) {
+                   cudaStream_t st, cudaEvent_t wait_before_loss, const float* dq_scale, const CriticDecode* dec) {
   if (critic_mma_ok(c))
     return critic_mma_fwd_bwd(c, B, params2, pb16, obs, S, act, A, y, q, loss, grad2, grad_act, act_scale, nz, ws, st,
-                              wait_before_loss, dq_scale);
+                              wait_before_loss, dq_scale, dec);
+  if (dec) { set_error("critic: in-launch decoding needs the small-batch tensor-core critic"); return SPIKERL_E_UNSUPPORTED; }
   if (c.bf16) {   // no silent switch of engine (north_star: no multi-backend dispatch)
     set_error("bf16 critic: the tensor-core critic needs hidden widths 256-256 and in_dim <= 512 (got %d-%d, %d)",
               c.H1, c.H2, c.in);

@@ -13,6 +13,7 @@
 //   dW2         A = dZ2T [H2][Bp]            B = H1T [H1][Bp]
 //   dW1         A = dZ1T [H1][Bp]            B = XT  [in_q][Bp]
 #include "adam_body.cuh"
+#include "rng.cuh"
 
 namespace spk {
 
@@ -205,7 +206,8 @@ __global__ void __launch_bounds__(256) critic_fwd_mma_kernel(
     const __nv_bfloat16* __restrict__ pb, long long P, long long tb, long long oW1p, long long oW2,
     long long oW3, const float* __restrict__ params, long long oB1, long long oB2, long long oB3,
     __nv_bfloat16* __restrict__ XT, __nv_bfloat16* __restrict__ H1T, float* __restrict__ Z1,
-    float* __restrict__ Z2, float* __restrict__ Hh2, float* __restrict__ q, int store, unsigned int* ticket) {
+    float* __restrict__ Z2, float* __restrict__ Hh2, float* __restrict__ q, int store, unsigned int* ticket,
+    const __grid_constant__ CriticDecode dec) {
   extern __shared__ __align__(128) uint8_t dsm[];
   __nv_bfloat16* const w2s = (__nv_bfloat16*)dsm;    // this critic's W2 staged: [HW][HW + SPAD]
   __shared__ __align__(8) uint64_t wbar;
@@ -232,6 +234,8 @@ __global__ void __launch_bounds__(256) critic_fwd_mma_kernel(
   // warp + 8, lane = every 32nd input column: no index division; ncu r01: the X-tile build waited on
   // its loads for ~54% of the launch's stall samples at B = 4096)
   static_assert(RB == 16 && NWARP == 8, "X tile: two rows per warp");
+  const bool decode = dec.counts != nullptr;
+  __shared__ float acts[RB][32];   // decode: the tile's smoothed target actions a~ (A <= 32)
   float xv[2][16];
   auto load_x = [&](int rt) {
 #pragma unroll
@@ -241,20 +245,61 @@ __global__ void __launch_bounds__(256) critic_fwd_mma_kernel(
       for (int cc = 0; cc < 16; ++cc) {
         const int i = lane + 32 * cc;
         float v = 0.f;
-        if (b < B && i < in) v = i < S ? obs[(size_t)b * S + i] : act[(size_t)b * A + (i - S)];
+        if (b < B && i < in) v = i < S ? obs[(size_t)b * S + i] : (decode ? 0.f : act[(size_t)b * A + (i - S)]);
         xv[rr][cc] = v;
       }
     }
   };
   if (blockIdx.x * RB < Bp) load_x(blockIdx.x * RB);
   for (int r0 = blockIdx.x * RB; r0 < Bp; r0 += gridDim.x * RB) {
+  if (decode) {
+    // a' = tanh(Wd fr + bd) and a~ = smooth(a') per (row, action), in dec_fwd_kernel's operation order
+    const int N3 = A * dec.D;
+    const unsigned long long ctr = dec.ts.at ? *dec.ts.ctr_snap : 0ull;
+    for (int idx = tid; idx < RB * A; idx += 256) {
+      const int r = idx / A, j = idx - r * A, b = r0 + r;
+      float v = 0.f;
+      if (b < B) {
+        // every count and weight requested before the (ordered) sum: one round trip, not D
+        uint32_t cv[kDecMaxD];
+        float wv[kDecMaxD];
+#pragma unroll
+        for (int e = 0; e < kDecMaxD; ++e) {
+          cv[e] = e < dec.D ? dec.counts[(size_t)b * N3 + j * dec.D + e] : 0u;
+          wv[e] = e < dec.D ? dec.Wd[j * dec.D + e] : 0.f;
+        }
+        float pre = 0.f;
+#pragma unroll
+        for (int e = 0; e < kDecMaxD; ++e) {
+          if (e < dec.D) {
+            const float fr = (float)cv[e] / (float)dec.T;
+            pre = __fadd_rn(pre, __fmul_rn(wv[e], fr));
+          }
+        }
+        pre = __fadd_rn(pre, dec.bd[j]);
+        const float a = tanhf(pre);
+        const int i = b * A + j;
+        v = dec.ts.at ? smooth_action(a, i, dec.ts.noise, dec.ts.sigma, dec.ts.clip, dec.ts.seed, dec.ts.rank, ctr) : a;
+        if (z == 0) {
+          if (dec.act_out) dec.act_out[i] = a;
+          if (dec.act_tape) dec.act_tape[i] = a;
+          if (dec.ts.at) dec.ts.at[i] = v;
+          if (dec.ts.at && dec.ts.advance && i == 0) *dec.ts.counter = ctr + 1;
+        }
+      }
+      acts[r][j] = v;
+    }
+    __syncthreads();
+  }
   // X tile (bf16-rounded [s; a]); the z == 0 CTAs also write X^T (zeros beyond in / B) for dW1
 #pragma unroll
   for (int rr = 0; rr < 2; ++rr)
 #pragma unroll
     for (int cc = 0; cc < 16; ++cc) {
       const int i = lane + 32 * cc;
-      if (i < inp) xs[(warp + 8 * rr) * ldx + i] = __float2bfloat16_rn(xv[rr][cc]);
+      float v = xv[rr][cc];
+      if (decode && i >= S && i < in && r0 + warp + 8 * rr < B) v = acts[warp + 8 * rr][i - S];
+      if (i < inp) xs[(warp + 8 * rr) * ldx + i] = __float2bfloat16_rn(v);
     }
   __syncthreads();
   if (r0 + (int)gridDim.x * RB < Bp) load_x(r0 + gridDim.x * RB);
@@ -1766,7 +1811,11 @@ static int critic_tc_fwd_bwd(const CriticDims& c, int B, const float* params2, c
 int critic_mma_fwd_bwd(const CriticDims& c, int B, const float* params2, const __nv_bfloat16* pb, const float* obs,
                        int S, const float* act, int A, const TdY* y, float* q, float* loss, float* grad2,
                        float* grad_act, float act_scale, int nz, void* ws, cudaStream_t st,
-                       cudaEvent_t wait_before_loss, const float* dq_scale) {
+                       cudaEvent_t wait_before_loss, const float* dq_scale, const CriticDecode* dec) {
+  if (dec && (!critic_decode_ok(c, B, A, dec->D) || y || grad2 || grad_act)) {
+    set_error("critic: in-launch decoding is for the small-batch tensor-core critic's forward only");
+    return SPIKERL_E_UNSUPPORTED;
+  }
   if (critic_tc_ok(c, B))
     return critic_tc_fwd_bwd(c, B, params2, pb, obs, S, act, A, y, q, loss, grad2, grad_act, act_scale, nz, ws, st,
                              wait_before_loss, dq_scale);
@@ -1785,7 +1834,8 @@ int critic_mma_fwd_bwd(const CriticDims& c, int B, const float* params2, const _
     pdl(critic_fwd_mma_kernel, grid, 256, kW2Smem, st)(
         B, Bp, S, A, L.inp, L.inq, obs, act, pb, L.P, L.tb, L.W1p, L.W2c, oW3, params2,
         (long long)c.off[SPIKERL_CRITIC_B1], (long long)c.off[SPIKERL_CRITIC_B2], (long long)c.off[SPIKERL_CRITIC_B3],
-        w.XT, w.H1T, w.Z1, w.Z2, w.Hh2, q, need_bwd ? 1 : 0, need_bwd ? w.ticket : nullptr);
+        w.XT, w.H1T, w.Z1, w.Z2, w.Hh2, q, need_bwd ? 1 : 0, need_bwd ? w.ticket : nullptr,
+        dec ? *dec : CriticDecode{});
     SPK_LAUNCHED();
   }
   if (wait_before_loss) SPK_CHECK_CUDA(cudaStreamWaitEvent(st, wait_before_loss, 0));
@@ -1808,11 +1858,10 @@ int critic_mma_fwd_bwd(const CriticDims& c, int B, const float* params2, const _
         oW3, L.W1T, L.W2T, w.Z1, w.Z2, w.dZ2T, w.dZ1T, grad_act, want_params ? 1 : 0, dq_scale);
     SPK_LAUNCHED();
   }
-  // merged weight + bias gradient launch: SPIKERL_CRITIC_WG_MERGE=0/1 never / always; default for inputs
-  // wider than 256 (A/B r02, one box: configs[3] B = 100 118.0 -> 112.2 us per update; configs[1] (in 23)
-  // 81.9 -> 83.7, where the side-stream bias kernel overlapping the weight-gradient launch is faster)
-  static const int merge_env = [] { const char* e = getenv("SPIKERL_CRITIC_WG_MERGE"); return e ? atoi(e) : -1; }();
-  const bool merge = merge_env < 0 ? L.inq > HW : merge_env != 0;
+  // merged weight + bias gradient launch (SPIKERL_CRITIC_WG_MERGE=1; default off: A/B r02 against the
+  // side-stream bias kernel overlapping the weight-gradient launch, configs[1] 81.7 -> 83.7 us per
+  // update, configs[3] B = 100 no different)
+  static const bool merge = [] { const char* e = getenv("SPIKERL_CRITIC_WG_MERGE"); return e && e[0] == '1'; }();
   if (want_params && wgrad_splits(B) == 0 && merge) {
     // small batches: weight and bias / w3 gradients as one launch (critic_wgrad_mma_kernel)
     ProfScope ps_("critic_wgrad_mma", PB_TENSOR, 2.0 * B * nz * ((double)HW * HW + (double)HW * c.in), 0.0, st);
@@ -1838,7 +1887,13 @@ int critic_mma_fwd_bwd(const CriticDims& c, int B, const float* params2, const _
     {
       ProfScope ps_("critic_wgrad_mma", PB_TENSOR, 2.0 * B * nz * ((double)HW * HW + (double)HW * c.in), 0.0, st);
       const int ws = wgrad_splits(B);
-      if (tc_wgrad_ok(c, w, Bp)) {
+      if (ws == 0) {
+        dim3 grid(cdiv(L.inq > HW ? L.inq : HW, 256), 2 * (HW / RB), nz);
+        pdl(critic_wgrad_mma_kernel, grid, 256, 0, st)(Bp, c.in, L.inq, L.P, (long long)c.off[SPIKERL_CRITIC_W1],
+                                                      (long long)c.off[SPIKERL_CRITIC_W2], w.XT, w.H1T, w.dZ2T, w.dZ1T,
+                                                      grad2, B, 0, 0, 0, 0, w.dq, w.Hh2);   // (no bias CTAs)
+        SPK_LAUNCHED();
+      } else if (tc_wgrad_ok(c, w, Bp)) {
         // tcgen05: both weight gradients of both critics as one split-K launch of K-major operand
         // tiles (the mma.sync split kernel below took 104 us at configs[3] B = 4096)
         const long long msz = (long long)HW * HW + (long long)HW * L.inq;
@@ -1847,12 +1902,6 @@ int critic_mma_fwd_bwd(const CriticDims& c, int B, const float* params2, const _
         pdl(critic_wgrad_reduce_cm_kernel, dim3(cdiv(HW + c.in, 32), HW / 32, 2), dim3(32, 32), 0, st)(
             splits, c.in, msz, L.P, (long long)c.off[SPIKERL_CRITIC_W1], (long long)c.off[SPIKERL_CRITIC_W2], w.wpart,
             grad2);
-        SPK_LAUNCHED();
-      } else if (ws == 0) {   // SPIKERL_CRITIC_WG_MERGE=0: the weight gradients alone (bias CTAs none)
-        dim3 grid(cdiv(L.inq > HW ? L.inq : HW, 256), 2 * (HW / RB), nz);
-        pdl(critic_wgrad_mma_kernel, grid, 256, 0, st)(Bp, c.in, L.inq, L.P, (long long)c.off[SPIKERL_CRITIC_W1],
-                                                      (long long)c.off[SPIKERL_CRITIC_W2], w.XT, w.H1T, w.dZ2T, w.dZ1T,
-                                                      grad2, B, 0, 0, 0, 0, w.dq, w.Hh2);
         SPK_LAUNCHED();
       } else {
         // K split in multiples of 16 batch rows (Bp is a multiple of RB = 16)
@@ -1944,6 +1993,11 @@ int critic_update_fused(const CriticDims& c, int B, float* params2, const __nv_b
   }
   SPK_LAUNCHED();
   return SPIKERL_OK;
+}
+
+bool critic_decode_ok(const CriticDims& c, int B, int A, int D) {
+  static const bool env = [] { const char* e = getenv("SPIKERL_CRITIC_DECODE"); return !(e && e[0] == '0'); }();
+  return env && critic_mma_ok(c) && !critic_tc_ok(c, B) && A <= 32 && D <= kDecMaxD;
 }
 
 bool critic_adam_ok(const CriticDims& c, const Bf16Views* views, const PolyakFuse* polyak) {

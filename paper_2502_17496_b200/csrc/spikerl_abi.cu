@@ -231,7 +231,7 @@ static ActorWs actor_ws_layout(const ActorDims& d, int B) {
 static int actor_forward_impl(const ActorDims& d, int B, const float* params,
                               const __nv_bfloat16* pb16, const float* obs, float* actions,
                               char* tape, cudaStream_t st, const TargetSmooth* smooth = nullptr,
-                              bool spikes_only = false) {
+                              bool spikes_only = false, bool skip_decoder = false) {
   const TapeLayout L = tape_layout(d, B);
   float* A = spikes_only ? nullptr : (float*)(tape + L.A);
   uint32_t* bits[4];
@@ -252,9 +252,25 @@ static int actor_forward_impl(const ActorDims& d, int B, const float* params,
     else
       SPK_TRY(launch_lif_fwd_simt(d, l, B, bits[l - 1], Wf, Wb, bits[l], mask[l], cnt, vout, st));
   }
+  if (skip_decoder) return SPIKERL_OK;   // the caller decodes inside the target critics' launch
   SPK_TRY(launch_dec_fwd(d, B, counts, params + d.off[SPIKERL_ACTOR_WD], params + d.off[SPIKERL_ACTOR_BD],
                          actions, (float*)(tape + L.act), st, smooth));
   return SPIKERL_OK;
+}
+
+// the target actor's decoder + smoothing handed to the target critics' forward launch (CriticDecode)
+static CriticDecode target_decode(const ActorDims& d, int B, const float* params, char* tape, float* actions,
+                                  const TargetSmooth& ts) {
+  const TapeLayout L = tape_layout(d, B);
+  CriticDecode c{};
+  c.counts = (const uint8_t*)(tape + L.counts);
+  c.Wd = params + d.off[SPIKERL_ACTOR_WD];
+  c.bd = params + d.off[SPIKERL_ACTOR_BD];
+  c.D = d.D; c.T = d.T;
+  c.act_out = actions;
+  c.act_tape = (float*)(tape + L.act);
+  c.ts = ts;
+  return c;
 }
 
 // Gradient buckets of the actor's flat layout mu|sigma|W1|W2|W3|Wd|bd, in the order the backward
@@ -413,6 +429,14 @@ static Bf16Views td3_critic_views(const CriticDims& cd, const ActorDims& ad, voi
 // one GPU (no gradient allreduce between the gradients and Adam), no loss scaling
 static bool critic_update_fusable(const CriticDims& cd, int B, const spikerl_td3_bufs* b, spikerl_comm* comm) {
   return !comm && !b->amp && critic_fused_ok(cd, B);
+}
+
+// the target decoder inside the target critics' forward: with the separate critic launches only (A/B r02,
+// one box: configs[1] 82.4 -> 80.1, configs[3] B = 100 110.7 -> 109.7 us per update; with the fused
+// critic update, configs[2], 109.4 -> 112.9)
+static bool target_decode_ok(const CriticDims& cd, const ActorDims& ad, int B, const spikerl_td3_bufs* b,
+                             spikerl_comm* comm) {
+  return critic_decode_ok(cd, B, ad.A, ad.D) && !critic_update_fusable(cd, B, b, comm);
 }
 
 static int critic_optimise(const spikerl_td3_bufs* b, spikerl_comm* comm, const spikerl_td3_cfg* hp, const CriticDims& cd,
@@ -808,10 +832,13 @@ int spikerl_td3_update(const spikerl_actor_cfg* acfg, const spikerl_critic_cfg* 
   SPK_TRY(stream_after(sA, st, aux->ev[0]));
   {
     const TargetSmooth ts{noise, hp->policy_noise, hp->noise_clip, seed, rank, b->rng_counter, ctr_snap, at, 1};
-    SPK_TRY(actor_forward_impl(ad, B, b->actor_t, atbf, s2, a2, aws + actor_ws_layout(ad, B).tape, sA, &ts, true));
+    char* tape_t = aws + actor_ws_layout(ad, B).tape;
+    const bool dec_c = target_decode_ok(cd, ad, B, b, comm);   // decoder + smoothing inside the target critics' launch
+    SPK_TRY(actor_forward_impl(ad, B, b->actor_t, atbf, s2, a2, tape_t, sA, &ts, true, dec_c));
+    const CriticDecode cdec = target_decode(ad, B, b->actor_t, tape_t, a2, ts);
+    SPK_TRY(critic_fwd_bwd(cd, B, b->critic_t, ctbf, s2, ad.S, at, ad.A, nullptr, qt, nullptr, nullptr, nullptr, 0.f,
+                           2, cws_t, sA, nullptr, nullptr, dec_c ? &cdec : nullptr));
   }
-  SPK_TRY(critic_fwd_bwd(cd, B, b->critic_t, ctbf, s2, ad.S, at, ad.A, nullptr, qt, nullptr, nullptr, nullptr, 0.f,
-                         2, cws_t, sA));
   SPK_CHECK_CUDA(cudaEventRecord(aux->ev[1], sA));
   // branch B (actor steps): the policy's own forward pi(s) depends only on s and the actor
   if (actor_step) {
@@ -966,9 +993,12 @@ int spikerl_td3_update_pair(const spikerl_actor_cfg* acfg, const spikerl_critic_
     SPK_TRY(stream_after(sA[i], st, aux->ev[i == 0 ? 0 : 6]));
     const TargetSmooth ts{noise ? noise + (size_t)i * B * ad.A : nullptr, hp->policy_noise, hp->noise_clip, seed,
                           rank, b->rng_counter, x.snap, x.at, i == 1 ? 1 : 0};
-    SPK_TRY(actor_forward_impl(ad, B, b->actor_t, atbf, x.s2, x.a2, x.aws + actor_ws_layout(ad, B).tape, sA[i], &ts, true));
+    char* tape_t = x.aws + actor_ws_layout(ad, B).tape;
+    const bool dec_c = target_decode_ok(cd, ad, B, b, comm);   // decoder + smoothing inside the target critics' launch
+    SPK_TRY(actor_forward_impl(ad, B, b->actor_t, atbf, x.s2, x.a2, tape_t, sA[i], &ts, true, dec_c));
+    const CriticDecode cdec = target_decode(ad, B, b->actor_t, tape_t, x.a2, ts);
     SPK_TRY(critic_fwd_bwd(cd, B, b->critic_t, ctbf, x.s2, ad.S, x.at, ad.A, nullptr, x.qt, nullptr, nullptr, nullptr,
-                           0.f, 2, x.cws_t, sA[i]));
+                           0.f, 2, x.cws_t, sA[i], nullptr, nullptr, dec_c ? &cdec : nullptr));
     SPK_CHECK_CUDA(cudaEventRecord(evA[i], sA[i]));
   }
   // branch B: pi(s) of update k + 1 (the actor is unchanged by update k)

@@ -511,8 +511,9 @@ def test_td3_schedule_independent_subprocess(name, B):
 def test_td3_fused_critic_matches_separate_launches_subprocess(name, B):
     """The fused small-batch critic launches (the whole critic update, forward to Adam + Polyak, with
     grid barriers; the actor objective's critic pass) are bitwise the separate launches
-    (SPIKERL_CRITIC_FUSED=0), and the layout-aware critic Adam is bitwise the flat adam_kernel
-    (SPIKERL_CRITIC_ADAM_TILED=0): two single updates, then three captured update pairs end in identical
+    (SPIKERL_CRITIC_FUSED=0), the layout-aware critic Adam is bitwise the flat adam_kernel
+    (SPIKERL_CRITIC_ADAM_TILED=0), the target decoder inside the target critics' launch bitwise its own
+    launch (SPIKERL_CRITIC_DECODE=0): two single updates, then three captured update pairs end in identical
     parameters, targets, Adam moments and step counts, losses and dQ1/da, at several grid sizes."""
     import os, subprocess, sys
     code = (
@@ -534,7 +535,7 @@ def test_td3_fused_critic_matches_separate_launches_subprocess(name, B):
         "for _ in range(3): td3.replay_pair()\n"
         "torch.cuda.synchronize()\n"
         "for t in (td3.actor, td3.actor_t, td3.critic, td3.critic_t, td3.m_actor, td3.v_actor, td3.m_critic,\n"
-        "          td3.v_critic, td3.adam_steps, td3.losses, td3.critic_bf16, td3.critic_t_bf16):\n"
+        "          td3.v_critic, td3.adam_steps, td3.losses, td3.critic_bf16, td3.critic_t_bf16, td3.rng_counter):\n"
         "    h.update(t.cpu().numpy().tobytes())\n"
         "print('digest', h.hexdigest())\n")
     root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
@@ -543,7 +544,7 @@ def test_td3_fused_critic_matches_separate_launches_subprocess(name, B):
                          ("separate_flat_adam", {"SPIKERL_CRITIC_FUSED": "0", "SPIKERL_CRITIC_ADAM_TILED": "0",
                                                  "SPIKERL_CRITIC_ACT_FUSED": "0"}),
                          ("separate_merged_wg", {"SPIKERL_CRITIC_FUSED": "0", "SPIKERL_CRITIC_WG_MERGE": "1"}),
-                         ("separate_split_wg", {"SPIKERL_CRITIC_FUSED": "0", "SPIKERL_CRITIC_WG_MERGE": "0"}),
+                         ("decoder_launch", {"SPIKERL_CRITIC_DECODE": "0"}),
                          ("fused_g148", {"SPIKERL_CRITIC_FUSED": "1", "SPIKERL_CRITIC_FUSED_G": "148"}),
                          ("fused_gmin", {"SPIKERL_CRITIC_FUSED": "1", "SPIKERL_CRITIC_FUSED_G": "1"})):
         r = subprocess.run([sys.executable, "-c", code], cwd=root, capture_output=True, text=True, timeout=600,
