@@ -16,7 +16,7 @@ td3 = pk.TD3(pk.actor_cfg_from(shape), pk.critic_cfg(cs.in_dim), pk.td3_cfg(B), 
 td3.load(sg.actor_params(shape, rng), sg.critic_params(cs, rng), sg.critic_params(cs, rng))
 td3.update_pair(1)
 td3.capture_pair()
-names = ["entry", "after_pdl", "F", "bar1", "W", "bar2", "adam", "-", "x_tile", "l1", "w2_staged", "q", "dq", "dH1"]
+names = ["entry", "after_pdl", "F", "bar1", "W", "bar2", "adam", "w_staged", "x_tile", "l1", "w2_staged", "q", "dq", "dH1", "w_mma", "w_bias"]
 rows = []
 for _ in range(reps):
     for _ in range(50):   # back to back: clocks under load, as in the bench loop
@@ -25,7 +25,7 @@ for _ in range(reps):
     buf = (C.c_ulonglong * 16)()
     _lib.lib().spikerl_debug_critic_trace(buf)
     v = list(buf)
-    rows.append([(x - v[0]) for x in v[:14]])
-med = [sorted(r[i] for r in rows)[len(rows) // 2] for i in range(14)]
+    rows.append([(x - v[0]) for x in v[:16]])
+med = [sorted(r[i] for r in rows)[len(rows) // 2] for i in range(16)]
 print(json.dumps({"workload": name, "G": os.environ.get("SPIKERL_CRITIC_FUSED_G", "default"),
                   "ns_since_entry": dict(zip(names, med))}))
