@@ -1143,11 +1143,15 @@ __device__ __forceinline__ void cp_wait_all() { asm volatile("cp.async.wait_grou
 // stride sld elements), every thread of the CTA issuing its share
 __device__ __forceinline__ void cp_rows(__nv_bfloat16* sdst, int sld, const __nv_bfloat16* gsrc, long long gld, int rows,
                                         int cols) {
-  const int cpr = cols >> 3;   // 16-byte chunks per row
-  for (int c = threadIdx.x; c < rows * cpr; c += blockDim.x) {
-    const int r = c / cpr, k = c - r * cpr;
-    cp16(sdst + (size_t)r * sld + 8 * k, gsrc + (size_t)r * gld + 8 * k);
-  }
+  // thread = (row offset, chunk): one division per call, not one per chunk (the per-chunk division made
+  // issuing a 128 KB stage ~700 instructions per thread, trace r02)
+  const int cpr = cols >> 3;   // 16-byte chunks per row (<= blockDim.x)
+  const int rpp = (int)blockDim.x / cpr, tr = (int)threadIdx.x / cpr, tk = (int)threadIdx.x - tr * cpr;
+  if (tr >= rpp) return;
+  const __nv_bfloat16* g = gsrc + (size_t)tr * gld + 8 * tk;
+  __nv_bfloat16* d = sdst + (size_t)tr * sld + 8 * tk;
+#pragma unroll 4
+  for (int r = tr; r < rows; r += rpp, g += (size_t)rpp * gld, d += (size_t)rpp * sld) cp16(d, g);
 }
 
 // One output row's batch sum from a shared-memory row (bf16 values x[b], b < B), in exactly the order
