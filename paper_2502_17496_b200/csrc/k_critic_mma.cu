@@ -318,7 +318,9 @@ __global__ void __launch_bounds__(256) critic_fwd_mma_kernel(
     float bias[NTW][2];   // requested before the MMAs (latency hidden behind them)
 #pragma unroll
     for (int nt = 0; nt < NTW; ++nt) { bias[nt][0] = b1[n0 + nt * 8 + 2 * t]; bias[nt][1] = b1[n0 + nt * 8 + 2 * t + 1]; }
-    warp_mma<NTW>(acc, xs, ldx, W1p + (size_t)n0 * inp, inp, inp);
+    // wide inputs (configs[3]: K = 400): eight k-steps of weight fragments in flight, not four
+    if (inp > 128) warp_mma<NTW, 8>(acc, xs, ldx, W1p + (size_t)n0 * inp, inp, inp);
+    else warp_mma<NTW>(acc, xs, ldx, W1p + (size_t)n0 * inp, inp, inp);
 #pragma unroll
     for (int nt = 0; nt < NTW; ++nt) {
 #pragma unroll
@@ -1336,7 +1338,8 @@ __device__ __forceinline__ void crit_tile(const CritFusedArgs& a, int z, int til
     float bias[NTW][2];
 #pragma unroll
     for (int nt = 0; nt < NTW; ++nt) { bias[nt][0] = b1[n0 + nt * 8 + 2 * t]; bias[nt][1] = b1[n0 + nt * 8 + 2 * t + 1]; }
-    warp_mma<NTW>(acc, xs, ldx, W1p + (size_t)n0 * a.inp, a.inp, a.inp);
+    if (a.inp > 128) warp_mma<NTW, 8>(acc, xs, ldx, W1p + (size_t)n0 * a.inp, a.inp, a.inp);
+    else warp_mma<NTW>(acc, xs, ldx, W1p + (size_t)n0 * a.inp, a.inp, a.inp);
 #pragma unroll
     for (int nt = 0; nt < NTW; ++nt)
 #pragma unroll
