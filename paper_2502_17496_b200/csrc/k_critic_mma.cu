@@ -1309,10 +1309,9 @@ __device__ __forceinline__ void crit_tile(const CritFusedArgs& a, int z, int til
         xv[rr][cc] = v;
       }
     }
-    // W2 into shared memory (cp.async, non-blocking) behind the X-tile loads, while layer 1 runs
-    // (issued first, its 128 KB queued ahead of the X loads: the X tile took 3.2 us, trace r02)
-    cp_rows(w2s, HW + SPAD, a.pb + blk_base(P) + z * a.tb + a.W2c, HW, HW, HW);
-    cp_commit();
+    // W2 into shared memory (per-row bulk copies on the TMA engine, completing on an mbarrier) behind
+    // the X-tile loads, while layer 1 runs
+    stage_rows(w2s, a.pb + blk_base(P) + z * a.tb + a.W2c, HW, HW, wbar);
 #pragma unroll
     for (int rr = 0; rr < 2; ++rr)
 #pragma unroll
@@ -1371,8 +1370,7 @@ __device__ __forceinline__ void crit_tile(const CritFusedArgs& a, int z, int til
         bias[nt][u] = b2[n0 + nt * 8 + 2 * t + u];
         w3v[nt][u] = __bfloat162float(W3[n0 + nt * 8 + 2 * t + u]);
       }
-    cp_wait_all();
-    __syncthreads();
+    stage_wait(wbar);
     if (MODE == 0) cstamp(10);
     warp_mma_ss<NTW>(acc, h1s, ldh, w2s + (size_t)n0 * ldh, ldh, HW);
     float qp[2] = {0.f, 0.f};
