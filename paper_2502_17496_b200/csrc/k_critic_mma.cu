@@ -1296,6 +1296,13 @@ __device__ __forceinline__ void crit_tile(const CritFusedArgs& a, int z, int til
   const int B = a.B, r0 = tile * RB;
   const int in = a.S + a.A, ldx = a.inp + SPAD, ldh = HW + SPAD;
   const long long P = a.P;
+  // the loss inputs of the tile's rows (TD target or its parts) and b3, requested now: they were on
+  // the dQ / Q critical path as two late round trips (trace r02)
+  float yv = 0.f, b3v = 0.f;
+  if (tid < RB) {
+    b3v = a.params[z * P + a.oB3];
+    if (MODE == 0 && r0 + tid < B) yv = a.y.at(r0 + tid);
+  }
   {
     float xv[2][16];
 #pragma unroll
@@ -1403,7 +1410,7 @@ __device__ __forceinline__ void crit_tile(const CritFusedArgs& a, int z, int til
   if (tid < RB) {
     float s = red[0][tid];
     for (int w = 1; w < NWARP; ++w) s = __fadd_rn(s, red[w][tid]);
-    const float qv = __fadd_rn(s, a.params[z * P + a.oB3]);
+    const float qv = __fadd_rn(s, b3v);
     qs[tid] = qv;
     if (r0 + tid < B) a.q[(size_t)z * B + r0 + tid] = qv;
   }
@@ -1415,7 +1422,8 @@ __device__ __forceinline__ void crit_tile(const CritFusedArgs& a, int z, int til
     if (lane < RB && b < B) {
       const float qv = qs[lane];
       if (MODE == 0) {
-        const float e = __fsub_rn(qv, a.y.get(b, z));
+        if (a.y.out && z == 0) a.y.out[b] = yv;   // TdY::get's store, with the value read up front
+        const float e = __fsub_rn(qv, yv);
         d = __fdiv_rn(__fmul_rn(2.0f, e), (float)B);
         c = __fmul_rn(e, e);
       } else {
