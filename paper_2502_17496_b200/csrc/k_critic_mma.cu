@@ -1287,10 +1287,30 @@ __device__ __forceinline__ void crit_wtask(const CritFusedArgs& a, int task, __n
 // Phase F for one 16-row tile (rows r0.., critic z). MODE 0: critic update (dQ from the TD target,
 // transposed operands, h2 and dQ stored for phase W); MODE 1: the actor objective on critic 0 (dQ =
 // act_scale, the loss partial sums Q, dQ1/da of the tile's rows).
+// the [s; a] values of a tile's rows (warp = rows warp and warp + 8, lane = every 32nd column)
+__device__ __forceinline__ void load_xtile(const CritFusedArgs& a, int tile, float (&xv)[2][16]) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, in = a.S + a.A;
+#pragma unroll
+  for (int rr = 0; rr < 2; ++rr) {
+    const int b = tile * RB + warp + 8 * rr;
+#pragma unroll
+    for (int cc = 0; cc < 16; ++cc) {
+      const int i = lane + 32 * cc;
+      float v = 0.f;
+      if (b < a.B && i < in) v = i < a.S ? a.obs[(size_t)b * a.S + i] : a.act[(size_t)b * a.A + (i - a.S)];
+      xv[rr][cc] = v;
+    }
+  }
+}
+
+// xv: the tile's [s; a] (load_xtile), requested by the caller BEFORE its PDL wait — the TD3 callers'
+// inputs were written by kernels that completed before this launch's predecessor (the gather, the
+// target path / pi(s) branches behind full graph edges), so their round trip overlaps the wait
 template <int MODE>
 __device__ __forceinline__ void crit_tile(const CritFusedArgs& a, int z, int tile, __nv_bfloat16* w2s, uint64_t* wbar,
                                           __nv_bfloat16* xs, __nv_bfloat16* h1s, __nv_bfloat16* d2s,
-                                          __nv_bfloat16* d1s, float (*red)[RB], float* qs, float* dqs) {
+                                          __nv_bfloat16* d1s, float (*red)[RB], float* qs, float* dqs,
+                                          const float (&xv)[2][16]) {
   const int tid = threadIdx.x, warp = tid >> 5;
   const int lane = tid & 31, g = lane >> 2, t = lane & 3;
   const int B = a.B, r0 = tile * RB;
@@ -1304,18 +1324,6 @@ __device__ __forceinline__ void crit_tile(const CritFusedArgs& a, int z, int til
     if (MODE == 0 && r0 + tid < B) yv = a.y.at(r0 + tid);
   }
   {
-    float xv[2][16];
-#pragma unroll
-    for (int rr = 0; rr < 2; ++rr) {
-      const int b = r0 + warp + 8 * rr;
-#pragma unroll
-      for (int cc = 0; cc < 16; ++cc) {
-        const int i = lane + 32 * cc;
-        float v = 0.f;
-        if (b < B && i < in) v = i < a.S ? a.obs[(size_t)b * a.S + i] : a.act[(size_t)b * a.A + (i - a.S)];
-        xv[rr][cc] = v;
-      }
-    }
     // W2 into shared memory (per-row bulk copies on the TMA engine, completing on an mbarrier) behind
     // the X-tile loads, while layer 1 runs
     stage_rows(w2s, a.pb + blk_base(P) + z * a.tb + a.W2c, HW, HW, wbar);
@@ -1646,12 +1654,14 @@ __global__ void __launch_bounds__(256, 1) critic_update_fused_kernel(const __gri
   }
   __syncthreads();
   cstamp(0);
+  float xv[2][16];
+  if ((int)cta < 2 * a.nb) load_xtile(a, (int)cta % a.nb, xv);   // before the wait (see crit_tile)
   pdl_wait();   // no early trigger: a dependent launched before this grid is resident could take its SMs
   cstamp(1);
   unsigned int target = 0;
   // ---- F
   if ((int)cta < 2 * a.nb)
-    crit_tile<0>(a, (int)cta / a.nb, (int)cta % a.nb, w2s, &wbar, xs, h1s, d2s, d1s, red, qs, dqs);
+    crit_tile<0>(a, (int)cta / a.nb, (int)cta % a.nb, w2s, &wbar, xs, h1s, d2s, d1s, red, qs, dqs, xv);
   cstamp(2);
   grid_barrier(a.gbar, G, target);
   cstamp(3);
@@ -1698,9 +1708,11 @@ __global__ void __launch_bounds__(256, 1) critic_actor_fused_kernel(const __grid
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   __syncthreads();
+  float xv[2][16];
+  load_xtile(a, blockIdx.x, xv);   // before the wait (see crit_tile)
   pdl_wait();
   pdl_trigger();
-  crit_tile<1>(a, 0, blockIdx.x, w2s, &wbar, xs, h1s, d2s, d1s, red, qs, dqs);
+  crit_tile<1>(a, 0, blockIdx.x, w2s, &wbar, xs, h1s, d2s, d1s, red, qs, dqs, xv);
   if (threadIdx.x == 0) {
     __threadfence();
     last = atomicAdd(a.ticket, 1u) == gridDim.x - 1;
