@@ -2022,11 +2022,12 @@ static CritFusedArgs fused_args(const CriticDims& c, int B, float* params2, cons
   return a;
 }
 
-// grid of the fused update: every row tile of both critics, and one CTA per SM for the weight-gradient
-// and Adam phases (64 CTAs: configs[1] 102 vs 86 us per update, r02) (SPIKERL_CRITIC_FUSED_G overrides; always <= the SM count: the grid barriers need
+// grid of the fused update: every row tile of both critics, and 96 CTAs (at least) for the weight-gradient
+// and Adam phases (configs[2] per update, late r02, three alternating rounds: 64 CTAs 101.9, 96 100.5,
+// 128 102.5, 148 101.7 us) (SPIKERL_CRITIC_FUSED_G overrides; always <= the SM count: the grid barriers need
 // the whole grid resident)
 static int fused_grid(int tiles) {
-  static const int env = [] { const char* e = getenv("SPIKERL_CRITIC_FUSED_G"); return e ? atoi(e) : 148; }();
+  static const int env = [] { const char* e = getenv("SPIKERL_CRITIC_FUSED_G"); return e ? atoi(e) : 96; }();
   int g = tiles > env ? tiles : env;
   return g < num_sms() ? g : num_sms();
 }
